@@ -1,0 +1,27 @@
+# Build the B200-native library (sm_100a) in-tree.
+NVCC ?= nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O3
+SRC := paper_2309_03523_b200/csrc
+OUT := paper_2309_03523_b200/lib
+CU := common spmm stale exchange dense rnn gemm_tc
+OBJS := $(addprefix build/,$(addsuffix .o,$(CU))) build/layout.o
+
+all: $(OUT)/libdgc_b200.so
+
+build/%.o: $(SRC)/%.cu $(SRC)/common.cuh include/dgc_b200.h
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+build/layout.o: $(SRC)/layout.cpp include/dgc_b200.h
+	@mkdir -p build
+	g++ -O3 -std=c++17 -fPIC -c $< -o $@
+
+$(OUT)/libdgc_b200.so: $(OBJS)
+	@mkdir -p $(OUT)
+	$(NVCC) $(ARCH) -shared --cudart static -o $@ $(OBJS)
+
+clean:
+	rm -rf build $(OUT)/libdgc_b200.so
+
+.PHONY: all clean

@@ -1,0 +1,188 @@
+/*
+ * dgc_b200.h -- C ABI of the B200-native DGC chunk-partitioned DGNN step.
+ *
+ * Plain pointers and sizes only: device pointers are CUDA global-memory
+ * addresses, `stream` is a cudaStream_t passed as void*. Every entry point
+ * returns 0 on success and a negative code on failure; dgc_last_error()
+ * returns the message (thread-local). Nothing here allocates or frees caller
+ * memory except the opaque layout handle.
+ *
+ * The reference (`dynpart`, pure Python) has no FFI; each entry
+ * point below names the reference function whose semantics it implements on
+ * the GPU (file:line relative to the reference's pkg/src/dynpart/). The
+ * ctypes binding a maintainer adds to the reference is in INTEGRATION.md.
+ */
+#ifndef DGC_B200_H
+#define DGC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DGC_OK 0
+#define DGC_ERR_ARG -1
+#define DGC_ERR_CUDA -2
+#define DGC_ERR_PLAN -3 /* plan/graph mismatch, cf. sim.py:108 PlanGraphMismatch */
+
+int dgc_version(void);
+const char* dgc_last_error(void);
+
+/* ------------------------------------------------------------------ */
+/* Host: plan -> per-device layout.                  */
+/* Consumes the reference plan unchanged: Plan.structure_device        */
+/* (sim.py:120), chunk membership (partition.py:49-56), FusionPlan      */
+/* groups (fusion.py:78-105), DynamicGraph index views                 */
+/* (graphstore.py:209-221).                                           */
+/* ------------------------------------------------------------------ */
+typedef struct dgc_plan_view {
+  int64_t n_instances;
+  const int32_t* inst_entity;     /* [n_instances] global (snapshot-major) order */
+  const int32_t* inst_t;          /* [n_instances] 1-based timestep */
+  int64_t n_spatial_edges;
+  const int32_t* spatial_edges;   /* [E,2] spatial_edge_index() order */
+  int64_t n_temporal_links;
+  const int32_t* temporal_links;  /* [L,2] temporal_link_index() order */
+  const int32_t* structure_device;/* [n_instances] Plan.structure_device */
+  const int32_t* chunk_of;        /* [n_instances] chunk id */
+  int32_t n_devices;
+  int64_t n_groups;               /* 0 = no fusion plan (build_plan(fuse=False)) */
+  const int32_t* group_device;    /* [n_groups] in FusionPlan order */
+  const int64_t* group_ptr;       /* [n_groups+1] */
+  const int32_t* group_chunks;    /* chunk ids per group */
+} dgc_plan_view;
+
+typedef struct dgc_layout dgc_layout;
+
+/* Field ids of dgc_layout_field(); all fields are int64 arrays. */
+enum dgc_layout_field_id {
+  DGC_F_OWN_GID = 0, DGC_F_HALO_GID, DGC_F_GROUP_PTR, DGC_F_ROW_PTR, DGC_F_COL,
+  DGC_F_DEG, DGC_F_T_ROW_PTR, DGC_F_T_COL, DGC_F_KEY_ROWS, DGC_F_SEND_PTR,
+  DGC_F_SEND_POS, DGC_F_RECV_PTR, DGC_F_RECV_SLOT, DGC_F_RUN_PTR, DGC_F_RUN_ROWS,
+  DGC_F_RUN_PRED_GID, DGC_F_RUN_CARRY, DGC_F_SLOT_ROW, DGC_F_SLOT_MASK,
+  DGC_F_SLOT_CARRY, DGC_F_TKEY_ROWS, DGC_F_TSEND_PTR, DGC_F_TSEND_POS,
+  DGC_F_TRECV_PTR, DGC_F_TRECV_CARRY, DGC_F_SCALARS, DGC_F_KEY_NCUT, DGC_F_COUNT
+};
+/* DGC_F_SCALARS = [n_own, n_halo, n_rows, row_len, padding, naive_padding,
+ *                  n_carry, loaded_rows] (loaded_rows: sim.py:339-360)
+ * DGC_F_KEY_NCUT = cut spatial messages sourced by each boundary key
+ * (MessageSet rows with src = key, costmodel.py:121-123) for the billing. */
+
+int dgc_layout_build(const dgc_plan_view* plan, int32_t device, dgc_layout** out);
+int64_t dgc_layout_field(const dgc_layout* lay, int32_t field, const int64_t** data);
+void dgc_layout_free(dgc_layout* lay);
+
+/* fusion.py:278-313 pack_sequences keyed by sequence index (FFD,
+ * fusion.py:249-275). Outputs are [capacity_rows*row_len]; row_len must be
+ * max(lengths). slot_seq/slot_pos = -1 on padding. */
+int dgc_pack_sequences(const int32_t* lengths, int64_t n, int32_t row_len,
+                       int64_t capacity_rows, int32_t* slot_seq, int32_t* slot_pos,
+                       uint8_t* mask, int64_t* n_rows, int64_t* padding);
+
+/* ------------------------------------------------------------------ */
+/* Device index arrays are int32 (per-device nnz < 2^31).              */
+/* ------------------------------------------------------------------ */
+
+/* K1: structure encoder aggregation (GCNConv normalisation), fp32.
+ * Replaces the analytic structure cost true_cost('structure')
+ * (costmodel.py:259-263, billed per fusion group sim.py:339-360,485-486).
+ *   out[i] = act( dinv[i] * sum_{c in row i} dinv[c] * Y[c] + bias )
+ * act: 0 none, 1 relu. Rows in fusion-group order; ONE launch covers all
+ * fusion groups of the device. bias may be NULL. The backward uses the same
+ * kernel on the transposed CSR (t_row_ptr, t_col). */
+int dgc_spmm_csr(const int32_t* row_ptr, const int32_t* col, const float* dinv,
+                 const float* Y, const float* bias, float* out,
+                 int64_t n_rows, int32_t width, int32_t act, void* stream);
+
+/* K2: tcgen05 TF32 GEMM (TMA -> SMEM -> TMEM), fp32 storage, fp32 accumulate.
+ *   C[M,N] = (accumulate ? C : 0) + op(A) op(B)  (+ bias[N]) (* (relu_src > 0))
+ *   a_mn = 0: A is [M,K] (row stride lda); a_mn = 1: A stored as [K,M] (A^T)
+ *   b_mn = 1: B is [K,N] (row stride ldb); b_mn = 0: B stored as [N,K] (B^T)
+ * precision: 1 = TF32, 3 = 3xTF32 (fp32-accurate; the parity mode).
+ * k_splits > 1 splits K over CTAs, writes partials to `partial`
+ * [splits, M, N] and reduces them in fixed order (deterministic). With
+ * precision 3 the library raises splits so that no TMEM accumulation chain
+ * exceeds 16 k-blocks (512 K): the tensor-core fp32 accumulator truncates,
+ * which biases long chains. dgc_gemm_splits() returns the split count a call
+ * will use, to size `partial` (splits * M * N floats).
+ * Replaces the x@W / h@U products of GruCell.step (fusion.py:410-412). */
+int dgc_gemm_splits(int64_t K, int32_t precision, int32_t k_splits);
+int dgc_gemm_tf32(const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
+                  int64_t ldc, int64_t M, int64_t N, int64_t K, int32_t a_mn, int32_t b_mn,
+                  int32_t precision, const float* bias, const float* relu_src,
+                  int32_t accumulate, int32_t k_splits, float* partial, void* stream);
+
+/* K3/K4: masked recurrent time encoder over FFD-packed runs.
+ * cell: 0 = GRU in the reference form of GruCell.step (fusion.py:409-413),
+ *       1 = LSTM (same conventions). Gate order GRU (r,z,c), LSTM (i,f,g,o).
+ * gx [n_inst, G*H] = x Wx + b (precomputed by K2), U [H, G*H].
+ * slot_row/slot_carry [R*L] int32 (-1 = none), slot_mask [R*L] uint8: the
+ * carry mask of gru_forward_masked (fusion.py:457-462). A run start with a
+ * remote predecessor loads carry[slot_carry] (h | c for LSTM) instead of 0.
+ * h_out/c_out rows have stride ld_out (LSTM: one [n_inst, 2H] h|c buffer).
+ * save [n_inst, dgc_rnn_save_floats] per-instance activations (instance order:
+ * GRU [h_in, r*h_in, r, z, c], LSTM [h_in, c_in, i, f, g, o, tanh(c)]).
+ * The first H columns of save are the operand of dU = save[:, :H]^T dgx. */
+int dgc_rnn_save_floats(int32_t cell, int32_t H);
+int dgc_rnn_fwd(int32_t cell, const float* gx, const float* U, const int32_t* slot_row,
+                const uint8_t* slot_mask, const int32_t* slot_carry, const float* carry,
+                int64_t n_rows, int32_t row_len, int32_t H, int64_t ld_out, float* h_out,
+                float* c_out, float* save, void* stream);
+/* BPTT over the same packing (Ut = U^T, [G*H, H], see dgc_transpose): dh_out [n_inst,H] -> dgx [n_inst,G*H]
+ * (d pre-activations; dWx = x^T dgx, db = colsum(dgx), dx = dgx Wx^T,
+ * dU = save-operand^T dgx by K2). Carries from other devices are constants. */
+int dgc_rnn_bwd(int32_t cell, const float* Ut, const int32_t* slot_row, const uint8_t* slot_mask,
+                int64_t n_rows, int32_t row_len, int32_t H, const float* save,
+                const float* dh_out, float* dgx, void* stream);
+
+/* K5: stale filter. dgc_stale_distance = the distance half of
+ * filter_transmissions / max_cache_gap (stale.py:140-151,205-212):
+ * dist[k] = ||Y[key_rows[k]] - cache[k]||_2 in fp32, fixed sequential order;
+ * dmax[0] = max over keys with cached[k] (0 if none), via a fixed-order tree. */
+int dgc_stale_distance(const float* Y, const int32_t* key_rows, const float* cache,
+                       const uint8_t* cached, int64_t n_keys, int32_t width, float* dist,
+                       float* dmax, void* stream);
+/* dgc_stale_select = the decision half (stale.py:166-176): send[k] =
+ * !cached[k] || dist[k] > theta (strict); sent keys refresh the cache with a
+ * copy of the current row and become cached. theta < 0 sends everything. */
+int dgc_stale_select(const float* Y, const int32_t* key_rows, const float* dist, float theta,
+                     float* cache, uint8_t* cached, uint8_t* send, int64_t n_keys,
+                     int32_t width, void* stream);
+
+/* K6: exchange pack/unpack (boundary rows; bytes billed as sim.py:514-543).
+ * dgc_compact_sent: out_pos = [i for i in 0..n) if send[pos[i]]] in order,
+ * *count (device int32) = its length. */
+int dgc_compact_sent(const int32_t* pos, int64_t n, const uint8_t* send, int32_t* out_idx,
+                     int32_t* count, void* stream);
+/* out[i,:] = Y[rows[idx[i]],:]  (rows/idx may be NULL = identity) */
+int dgc_gather_rows(const float* Y, const int32_t* rows, const int32_t* idx, int64_t n,
+                    int32_t width, float* out, void* stream);
+/* dst[rows[idx[i]],:] (+)= src[i,:]  (add != 0 accumulates; indices distinct) */
+int dgc_scatter_rows(const float* src, const int32_t* rows, const int32_t* idx, int64_t n,
+                     int32_t width, float* dst, int32_t add, void* stream);
+
+/* K8: softmax cross-entropy readout. dlogits = (softmax - onehot) * scale;
+ * loss_partial[ceil(n/256)] = per-block fp64 sums of -log p[label]. */
+int dgc_softmax_xent(const float* logits, const int32_t* labels, int64_t n, int32_t C,
+                     float scale, float* dlogits, double* loss_partial, void* stream);
+/* Deterministic column sums out[j] (+)= sum_i X[i, j] (bias gradients);
+ * scratch >= ceil(n/1024)*width floats. */
+int dgc_colsum(const float* X, int64_t n, int32_t width, int64_t ld, float* out,
+               int32_t accumulate, float* scratch, void* stream);
+/* dZ = dH * (H > 0) elementwise */
+int dgc_relu_bwd(const float* dH, const float* H, float* dZ, int64_t n, void* stream);
+
+/* out[c, r] = in[r, c] (fp32, tiled through shared memory) */
+int dgc_transpose(const float* in, int64_t rows, int64_t cols, float* out, void* stream);
+
+/* Optimizers over the flat parameter buffer (after the K7 all-reduce). */
+int dgc_sgd(float* p, const float* g, float* mom, int64_t n, float lr, float momentum,
+            void* stream);
+int dgc_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, float beta1,
+             float beta2, float eps, int32_t step, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -90,10 +90,17 @@ class OracleDGNN:
         self.mom = {k: np.zeros_like(v) for k, v in self.p.items()}
         self.vel = {k: np.zeros_like(v) for k, v in self.p.items()}
         self.step_count = 0
+        self.tie_log: list[dict] = []
 
     # -- staleness (stale.py) ------------------------------------------------
-    def _decide(self, r, values, cache, cached):
-        """One global decision per cache: D_r = max over devices (sim.py:455-459)."""
+    def _decide(self, r, values, cache, cached, forced=None, tag=""):
+        """One global decision per cache: D_r = max over devices (sim.py:455-459).
+
+        ``forced`` (per-device bool arrays) replays another implementation's
+        decisions; the oracle's own decision is still computed and every key
+        where they differ is recorded in self.tie_log with its distance and
+        theta, so tests can assert the disagreement lies in the fp32 tie band
+        (SURVEY.md §7 (ii))."""
         if self.D == 1:
             return [np.zeros(0, bool) for _ in values], 0.0, 0.0
         mode = self.cfg.stale_mode
@@ -109,15 +116,25 @@ class OracleDGNN:
             d_r = max([float(dd[cc].max()) for dd, cc in zip(dists, cached) if cc.any()] or [0.0])
             theta = threshold(self.losses, r, d_r, mode, self.cfg.static_fraction)
         sends = []
-        for v, c, cc, dd in zip(values, cache, cached, dists):
+        for d, (v, c, cc, dd) in enumerate(zip(values, cache, cached, dists)):
             s = (~cc) | (dd > theta)
+            if forced is not None:
+                f = np.asarray(forced[d], bool)
+                for k in np.flatnonzero(f != s):
+                    self.tie_log.append(dict(epoch=r, cache=tag, device=d, key=int(k),
+                                             dist=float(dd[k]), theta=float(theta),
+                                             scale=float(np.abs(v[k]).max())))
+                s = f
             c[s] = v[s]
             cc |= s
             sends.append(s)
         return sends, theta, d_r
 
     # -- forward/backward of one epoch ---------------------------------------
-    def epoch(self, r):
+    def epoch(self, r, forced=None):
+        """One epoch; ``forced`` = {cache tag: per-device send masks} replays
+        externally made stale decisions (see _decide)."""
+        forced = forced or {}
         cfg, D, G, H = self.cfg, self.D, self.G, self.cfg.H
         out = {"send": {}, "theta": {}, "d_r": {}}
         hin = self.X
@@ -126,7 +143,8 @@ class OracleDGNN:
         for l, (W, b) in enumerate([("W1", "b1"), ("W2", "b2")]):
             Y = [h @ self.p[W] for h in hin]
             vals = [Y[d][self.L[d].key_rows] for d in range(D)]
-            sends, theta, d_r = self._decide(r, vals, self.scache[l], self.scached[l])
+            sends, theta, d_r = self._decide(r, vals, self.scache[l], self.scached[l],
+                                             forced.get(f"s{l}"), f"s{l}")
             fresh = [np.zeros(self.L[d].n_halo, bool) for d in range(D)]
             for d in range(D):
                 lay = self.L[d]
@@ -168,7 +186,8 @@ class OracleDGNN:
                 if cfg.rnn == "lstm":
                     v = np.concatenate([v, c_out[lay.tkey_rows]], axis=1)
                 tvals.append(v)
-            tsends, ttheta, td_r = self._decide(r, tvals, self.tcache[k], self.tcached[k])
+            tsends, ttheta, td_r = self._decide(r, tvals, self.tcache[k], self.tcached[k],
+                                                forced.get(f"t{k}"), f"t{k}")
             for d in range(D):
                 lay = self.L[d]
                 for p in range(D):

@@ -1,0 +1,150 @@
+// Readout loss (K8), deterministic reductions and optimizers.
+//
+// The reference loss trace is synthetic (sim.py:323-324); the B200 trainer
+// feeds the real mean cross-entropy into EpochLossTrace.append (stale.py:80),
+// which drives threshold() unchanged. Every reduction has a fixed order.
+#include "common.cuh"
+
+namespace {
+
+__global__ void __launch_bounds__(256) softmax_xent_kernel(const float* __restrict__ logits,
+                                                          const int32_t* __restrict__ labels,
+                                                          int64_t n, int C, float scale,
+                                                          float* __restrict__ dlogits,
+                                                          double* __restrict__ loss_partial) {
+  __shared__ double red[256];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double l = 0.0;
+  if (i < n) {
+    const float* x = logits + i * C;
+    float m = -INFINITY;
+    for (int c = 0; c < C; ++c) m = fmaxf(m, x[c]);
+    float s = 0.f;
+    for (int c = 0; c < C; ++c) s += __expf(x[c] - m);
+    const float ls = logf(s);
+    const int y = labels[i];
+    l = -(double)(x[y] - m - ls);
+    const float inv = 1.f / s;
+    for (int c = 0; c < C; ++c) {
+      float p = __expf(x[c] - m) * inv;
+      if (c == y) p -= 1.f;
+      dlogits[i * C + c] = p * scale;
+    }
+  }
+  red[threadIdx.x] = l;
+  __syncthreads();
+  for (int off = 128; off > 0; off >>= 1) {
+    if ((int)threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) loss_partial[blockIdx.x] = red[0];
+}
+
+// stage 1: block b sums rows [b*1024, (b+1)*1024) of every column
+__global__ void colsum_stage1(const float* __restrict__ X, int64_t n, int width, int64_t ld,
+                              float* __restrict__ scratch) {
+  const int64_t r0 = (int64_t)blockIdx.x * 1024;
+  const int64_t r1 = min(r0 + 1024, n);
+  for (int j = threadIdx.x; j < width; j += blockDim.x) {
+    float acc = 0.f;
+    for (int64_t r = r0; r < r1; ++r) acc += X[r * ld + j];
+    scratch[(int64_t)blockIdx.x * width + j] = acc;
+  }
+}
+
+__global__ void colsum_stage2(const float* __restrict__ scratch, int nblk, int width,
+                              float* __restrict__ out, int accumulate) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= width) return;
+  float acc = 0.f;
+  for (int b = 0; b < nblk; ++b) acc += scratch[(int64_t)b * width + j];
+  out[j] = accumulate ? out[j] + acc : acc;
+}
+
+__global__ void relu_bwd_kernel(const float4* __restrict__ dH, const float4* __restrict__ H,
+                                float4* __restrict__ dZ, int64_t n4) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 g = dH[i], h = H[i];
+    dZ[i] = make_float4(h.x > 0.f ? g.x : 0.f, h.y > 0.f ? g.y : 0.f, h.z > 0.f ? g.z : 0.f,
+                        h.w > 0.f ? g.w : 0.f);
+  }
+}
+
+__global__ void sgd_kernel(float* __restrict__ p, const float* __restrict__ g,
+                           float* __restrict__ mom, int64_t n, float lr, float mu) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = fmaf(mu, mom[i], g[i]);
+    mom[i] = v;
+    p[i] = fmaf(-lr, v, p[i]);
+  }
+}
+
+__global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g,
+                            float* __restrict__ m, float* __restrict__ v, int64_t n, float lr,
+                            float b1, float b2, float eps, float c1, float c2) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    const float mi = b1 * m[i] + (1.f - b1) * gi;
+    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    p[i] -= lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+  }
+}
+
+}  // namespace
+
+extern "C" int dgc_softmax_xent(const float* logits, const int32_t* labels, int64_t n, int32_t C,
+                                float scale, float* dlogits, double* loss_partial, void* stream) {
+  DGC_REQUIRE(C >= 1, "softmax_xent: C must be >= 1");
+  if (n == 0) return DGC_OK;
+  const int blocks = (int)((n + 255) / 256);
+  softmax_xent_kernel<<<blocks, 256, 0, dgc::as_stream(stream)>>>(logits, labels, n, C, scale,
+                                                                 dlogits, loss_partial);
+  DGC_CHECK_LAUNCH("softmax_xent_kernel");
+  return DGC_OK;
+}
+
+extern "C" int dgc_colsum(const float* X, int64_t n, int32_t width, int64_t ld, float* out,
+                          int32_t accumulate, float* scratch, void* stream) {
+  cudaStream_t s = dgc::as_stream(stream);
+  const int nblk = (int)((n + 1023) / 1024);
+  if (nblk > 0) {
+    colsum_stage1<<<nblk, 256, 0, s>>>(X, n, width, ld, scratch);
+    DGC_CHECK_LAUNCH("colsum_stage1");
+  }
+  colsum_stage2<<<(width + 255) / 256, 256, 0, s>>>(scratch, nblk, width, out, accumulate);
+  DGC_CHECK_LAUNCH("colsum_stage2");
+  return DGC_OK;
+}
+
+extern "C" int dgc_relu_bwd(const float* dH, const float* H, float* dZ, int64_t n, void* stream) {
+  DGC_REQUIRE(n % 4 == 0, "relu_bwd: n must be a multiple of 4");
+  if (n == 0) return DGC_OK;
+  relu_bwd_kernel<<<dgc::grid_for(n / 4, 256), 256, 0, dgc::as_stream(stream)>>>(
+      reinterpret_cast<const float4*>(dH), reinterpret_cast<const float4*>(H),
+      reinterpret_cast<float4*>(dZ), n / 4);
+  DGC_CHECK_LAUNCH("relu_bwd_kernel");
+  return DGC_OK;
+}
+
+extern "C" int dgc_sgd(float* p, const float* g, float* mom, int64_t n, float lr, float momentum,
+                       void* stream) {
+  if (n == 0) return DGC_OK;
+  sgd_kernel<<<dgc::grid_for(n, 256), 256, 0, dgc::as_stream(stream)>>>(p, g, mom, n, lr, momentum);
+  DGC_CHECK_LAUNCH("sgd_kernel");
+  return DGC_OK;
+}
+
+extern "C" int dgc_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr,
+                        float beta1, float beta2, float eps, int32_t step, void* stream) {
+  if (n == 0) return DGC_OK;
+  const float c1 = 1.f - powf(beta1, (float)step), c2 = 1.f - powf(beta2, (float)step);
+  adam_kernel<<<dgc::grid_for(n, 256), 256, 0, dgc::as_stream(stream)>>>(p, g, m, v, n, lr, beta1,
+                                                                       beta2, eps, c1, c2);
+  DGC_CHECK_LAUNCH("adam_kernel");
+  return DGC_OK;
+}

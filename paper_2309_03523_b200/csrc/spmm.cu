@@ -1,0 +1,122 @@
+// K1: batched gather-SpMM of the GCN structure encoder (fp32).
+//
+// One launch covers every fusion group of a device: rows are laid out in
+// fusion-group order, so a fused group is a contiguous row
+// segment and the whole device is one batched CSR. Each row is handled by a
+// sub-warp of LPR lanes; every lane owns NV float4 columns, so one neighbour
+// row is fetched as LPR*NV coalesced 16-byte loads (a 512-byte row at W=128
+// is one fully coalesced warp transaction). Neighbour indices are broadcast
+// within the sub-warp and unrolled four deep to keep enough loads in flight
+// for the degree-skewed hub rows; the reduction order is the CSR order, so
+// the result is bitwise deterministic (no atomics).
+//
+// Semantics replace the analytic structure-encoder cost of the reference
+// (costmodel.py:259-263 via sim.py:339-360,485-486) with real arithmetic:
+//   out[i] = act( dinv[i] * sum_{c in row i} dinv[c] * Y[c] + bias ).
+#include "common.cuh"
+
+namespace {
+
+template <int LPR, int NV>
+__global__ void __launch_bounds__(256) spmm_csr_kernel(
+    const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+    const float* __restrict__ dinv, const float4* __restrict__ Y,
+    const float* __restrict__ bias, float4* __restrict__ out, int64_t n_rows, int act) {
+  constexpr int W4 = LPR * NV;  // float4 per row
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = (int)(tid % LPR);
+  const int64_t stride = ((int64_t)gridDim.x * blockDim.x) / LPR;
+  for (int64_t row = tid / LPR; row < n_rows; row += stride) {
+    const int beg = __ldg(row_ptr + row), end = __ldg(row_ptr + row + 1);
+    float4 acc[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    int e = beg;
+    for (; e + 4 <= end; e += 4) {
+      int c[4];
+      float w[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) c[u] = __ldg(col + e + u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) w[u] = __ldg(dinv + c[u]);
+      float4 y[4][NV];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) y[u][v] = __ldg(Y + (int64_t)c[u] * W4 + lane + v * LPR);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          acc[v].x = fmaf(w[u], y[u][v].x, acc[v].x);
+          acc[v].y = fmaf(w[u], y[u][v].y, acc[v].y);
+          acc[v].z = fmaf(w[u], y[u][v].z, acc[v].z);
+          acc[v].w = fmaf(w[u], y[u][v].w, acc[v].w);
+        }
+    }
+    for (; e < end; ++e) {
+      const int c = __ldg(col + e);
+      const float w = __ldg(dinv + c);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const float4 y = __ldg(Y + (int64_t)c * W4 + lane + v * LPR);
+        acc[v].x = fmaf(w, y.x, acc[v].x);
+        acc[v].y = fmaf(w, y.y, acc[v].y);
+        acc[v].z = fmaf(w, y.z, acc[v].z);
+        acc[v].w = fmaf(w, y.w, acc[v].w);
+      }
+    }
+    const float di = __ldg(dinv + row);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int j4 = lane + v * LPR;
+      float4 b = bias ? __ldg(reinterpret_cast<const float4*>(bias) + j4)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 o;
+      o.x = fmaf(di, acc[v].x, b.x);
+      o.y = fmaf(di, acc[v].y, b.y);
+      o.z = fmaf(di, acc[v].z, b.z);
+      o.w = fmaf(di, acc[v].w, b.w);
+      if (act == 1) {
+        o.x = fmaxf(o.x, 0.f);
+        o.y = fmaxf(o.y, 0.f);
+        o.z = fmaxf(o.z, 0.f);
+        o.w = fmaxf(o.w, 0.f);
+      }
+      out[row * W4 + j4] = o;
+    }
+  }
+}
+
+template <int LPR, int NV>
+int launch(const int32_t* rp, const int32_t* col, const float* dinv, const float* Y,
+           const float* bias, float* out, int64_t n, int act, cudaStream_t s) {
+  const int block = 256;
+  const int grid = dgc::grid_for(n * LPR, block, 8);
+  spmm_csr_kernel<LPR, NV><<<grid, block, 0, s>>>(rp, col, dinv,
+                                                  reinterpret_cast<const float4*>(Y), bias,
+                                                  reinterpret_cast<float4*>(out), n, act);
+  DGC_CHECK_LAUNCH("spmm_csr_kernel");
+  return DGC_OK;
+}
+
+}  // namespace
+
+extern "C" int dgc_spmm_csr(const int32_t* row_ptr, const int32_t* col, const float* dinv,
+                            const float* Y, const float* bias, float* out, int64_t n_rows,
+                            int32_t width, int32_t act, void* stream) {
+  DGC_REQUIRE(width > 0 && width % 4 == 0, "spmm: width must be a positive multiple of 4");
+  if (n_rows == 0) return DGC_OK;
+  cudaStream_t s = dgc::as_stream(stream);
+  switch (width) {
+    case 4: return launch<1, 1>(row_ptr, col, dinv, Y, bias, out, n_rows, act, s);
+    case 8: return launch<2, 1>(row_ptr, col, dinv, Y, bias, out, n_rows, act, s);
+    case 16: return launch<4, 1>(row_ptr, col, dinv, Y, bias, out, n_rows, act, s);
+    case 32: return launch<8, 1>(row_ptr, col, dinv, Y, bias, out, n_rows, act, s);
+    case 64: return launch<16, 1>(row_ptr, col, dinv, Y, bias, out, n_rows, act, s);
+    case 128: return launch<32, 1>(row_ptr, col, dinv, Y, bias, out, n_rows, act, s);
+    case 256: return launch<32, 2>(row_ptr, col, dinv, Y, bias, out, n_rows, act, s);
+    case 512: return launch<32, 4>(row_ptr, col, dinv, Y, bias, out, n_rows, act, s);
+    default: return dgc::fail(DGC_ERR_ARG, "spmm: unsupported width (use 4..512, power of two)");
+  }
+}

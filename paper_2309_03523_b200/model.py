@@ -1,0 +1,92 @@
+"""DGNN model definitions for the chunk-partitioned step.
+
+The reference has no DGNN arithmetic beyond the GRU forward;
+the models follow the paper's evaluation set restated with
+the reference's conventions:
+  * T-GCN style  = ModelProfile.recurrent(): 2 GCN layers + 1 GRU layer
+    (reference GruCell form, fusion.py:341-413);
+  * MPNN-LSTM    = ModelProfile(1,2,2,...): 2 GCN layers + 2 LSTM layers.
+Parameters are initialised like GruCell.random (fusion.py:392-407): uniform
++-1/sqrt(fan_in), numpy default_rng(seed), in parameter order.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+GATES = {"gru": 3, "lstm": 4}
+
+
+@dataclass
+class DGNNConfig:
+    F: int = 16
+    H: int = 16
+    C: int = 16
+    rnn: str = "gru"
+    n_rnn: int = 1
+    precision: str = "fp32"     # "fp32": 3xTF32 GEMMs (parity); "tf32": 1-pass TF32 (perf)
+    optimizer: str = "adam"
+    lr: float = 0.01
+    momentum: float = 0.9
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+
+    @property
+    def G(self) -> int:
+        return GATES[self.rnn]
+
+    @property
+    def carry_width(self) -> int:
+        return self.H * (2 if self.rnn == "lstm" else 1)
+
+    @classmethod
+    def for_profile(cls, profile: dict, F: int, H: int | None = None, C: int = 16, **kw):
+        """Model of a reference ModelProfile (costmodel.py:50-92)."""
+        if profile.get("spatial_msgs_per_block", 2) != 2 or profile.get("blocks", 1) != 1:
+            raise ValueError("only the 1-block, 2-GCN-layer profiles of C1/C2 are modelled")
+        n_rnn = int(profile.get("temporal_msgs_per_block", 1))
+        if n_rnn < 1:
+            raise ValueError("temporal_msgs_per_block = 0 (EvolveGCN) is not modelled yet")
+        H = H if H is not None else int(profile.get("embedding_dim", 16))
+        rnn = "gru" if n_rnn == 1 else "lstm"
+        return cls(F=F, H=H, C=C, rnn=rnn, n_rnn=n_rnn, **kw)
+
+
+def param_shapes(cfg: DGNNConfig):
+    H, G = cfg.H, cfg.G
+    shapes = [("W1", (cfg.F, H), cfg.F), ("b1", (H,), H), ("W2", (H, H), H), ("b2", (H,), H)]
+    for k in range(cfg.n_rnn):
+        shapes += [(f"Wx{k}", (H, G * H), H), (f"U{k}", (H, G * H), H), (f"br{k}", (G * H,), H)]
+    shapes += [("Wo", (H, cfg.C), H), ("bo", (cfg.C,), H)]
+    return shapes
+
+
+def init_params(cfg: DGNNConfig, seed: int = 0) -> dict:
+    rng = np.random.default_rng(seed)
+    out = {}
+    for name, shape, fan in param_shapes(cfg):
+        s = 1.0 / np.sqrt(fan)
+        out[name] = rng.uniform(-s, s, size=shape).astype(np.float32)
+    return out
+
+
+def flat_offsets(cfg: DGNNConfig):
+    """Offsets of each parameter in the flat buffer (128-byte aligned so every
+    view is a valid TMA base address)."""
+    offs, o = {}, 0
+    for name, shape, _ in param_shapes(cfg):
+        n = int(np.prod(shape))
+        offs[name] = (o, shape)
+        o += (n + 31) // 32 * 32
+    return offs, o
+
+
+def synthetic_inputs(n_instances: int, F: int, C: int, seed: int = 0):
+    """Seeded N(0,1) fp32 features and uniform labels per instance in the
+    reference's global order."""
+    rng = np.random.default_rng(seed + 1)
+    X = rng.standard_normal((n_instances, F), dtype=np.float32)
+    y = np.random.default_rng(seed + 2).integers(0, C, size=n_instances).astype(np.int32)
+    return X, y

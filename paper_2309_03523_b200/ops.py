@@ -1,0 +1,225 @@
+"""Thin torch-tensor wrappers over the C ABI (include/dgc_b200.h).
+
+PyTorch is plumbing here: device memory, the current stream and NCCL. Every
+function validates dtype/device/contiguity and launches exactly the native
+kernel named in its docstring on the current CUDA stream; there is no
+fallback path.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _native
+
+_NULL = None
+
+# Optional per-launch profiler (bench.py): records CUDA events around every
+# native call on the current stream with its algorithmic bytes / flops.
+_prof = None
+
+
+class profile:
+    """Context manager collecting (name, start, end, bytes, flops, kernels)."""
+
+    def __init__(self):
+        self.records = []
+
+    def __enter__(self):
+        global _prof
+        _prof = self.records
+        return self
+
+    def __exit__(self, *exc):
+        global _prof
+        _prof = None
+
+    def summary(self):
+        torch.cuda.synchronize()
+        out = {}
+        for name, s, e, nbytes, flops, nk in self.records:
+            d = out.setdefault(name, dict(ms=0.0, launches=0, kernels=0, bytes=0.0, flops=0.0))
+            d["ms"] += s.elapsed_time(e)
+            d["launches"] += 1
+            d["kernels"] += nk
+            d["bytes"] += nbytes
+            d["flops"] += flops
+        return out
+
+
+def _run(name, fn, nbytes=0.0, flops=0.0, kernels=1):
+    if _prof is None:
+        return fn()
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    s.record()
+    rc = fn()
+    e.record()
+    _prof.append((name, s, e, float(nbytes), float(flops), kernels))
+    return rc
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _req(t, dtype, name):
+    if t is None:
+        return
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+
+
+def spmm_csr(row_ptr, col, dinv, Y, bias, out, act: int, nnz=0, n_cols=0):
+    """K1 dgc_spmm_csr: out = act(dinv_i * sum_c dinv_c Y_c + bias).
+    Algorithmic bytes: 4W(n_cols + n_rows) + 4(n_rows+1)
+    + 4 nnz (+ 4 n_cols for dinv)."""
+    _req(row_ptr, torch.int32, "row_ptr"); _req(col, torch.int32, "col")
+    _req(Y, torch.float32, "Y"); _req(out, torch.float32, "out")
+    n = row_ptr.numel() - 1
+    W = out.shape[-1] if out.dim() > 1 else 1
+    nb = 4 * W * (n_cols + n) + 4 * (n + 1) + 4 * nnz + 4 * n_cols
+    _run("spmm_csr", lambda: _native.check(_native.lib().dgc_spmm_csr(
+        _p(row_ptr), _p(col), _p(dinv), _p(Y), _p(bias), _p(out), n, W, act, _stream()),
+        "dgc_spmm_csr"), nb, 2 * nnz * W)
+    return out
+
+
+def gemm(A, B, C, M, N, K, *, a_mn=False, b_mn=True, lda=None, ldb=None, ldc=None,
+         precision=3, bias=None, relu_src=None, accumulate=False, k_splits=1, partial=None):
+    """K2 dgc_gemm_tf32 (tcgen05). Defaults: A [M,K] row-major, B [K,N] row-major."""
+    for t, nm in ((A, "A"), (B, "B"), (C, "C")):
+        _req(t, torch.float32, nm)
+    if partial is None and gemm_splits(K, precision, k_splits) > 1:
+        raise ValueError(f"gemm: K={K} needs a split-K partial buffer "
+                         f"({gemm_splits(K, precision, k_splits)} splits)")
+    lda = lda if lda is not None else (M if a_mn else K)
+    ldb = ldb if ldb is not None else (N if b_mn else K)
+    ldc = ldc if ldc is not None else N
+    splits = gemm_splits(K, precision, k_splits)
+    nb = 4 * (M * K + K * N + M * N * (1 + int(accumulate) + int(relu_src is not None)))
+    _run("gemm_tf32" if precision == 1 else "gemm_3xtf32", lambda: _native.check(
+        _native.lib().dgc_gemm_tf32(
+            _p(A), lda, _p(B), ldb, _p(C), ldc, M, N, K, int(a_mn), int(b_mn), precision,
+            _p(bias), _p(relu_src), int(accumulate), k_splits, _p(partial), _stream()),
+        "dgc_gemm_tf32"), nb, 2.0 * M * N * K, 1 + int(splits > 1))
+    return C
+
+
+def gemm_splits(K, precision, k_splits):
+    """Split count dgc_gemm_tf32 will use for a K-long contraction."""
+    return _native.lib().dgc_gemm_splits(K, precision, k_splits)
+
+
+def rnn_save_floats(cell: int, H: int) -> int:
+    return _native.lib().dgc_rnn_save_floats(cell, H)
+
+
+def rnn_fwd(cell, gx, U, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, H, ld_out,
+            h_out, c_out, save):
+    """K3/K4 dgc_rnn_fwd (masked GRU/LSTM over packed runs)."""
+    _req(gx, torch.float32, "gx"); _req(slot_row, torch.int32, "slot_row")
+    _req(slot_mask, torch.uint8, "slot_mask"); _req(slot_carry, torch.int32, "slot_carry")
+    n_inst, G = gx.shape[0], (3 if cell == 0 else 4)
+    sf = rnn_save_floats(cell, H)
+    nb = 4 * n_inst * (G * H + sf + H * (1 + cell)) + 9 * n_rows * row_len + 4 * G * H * H
+    _run("gru_fwd" if cell == 0 else "lstm_fwd", lambda: _native.check(
+        _native.lib().dgc_rnn_fwd(cell, _p(gx), _p(U), _p(slot_row), _p(slot_mask),
+                                  _p(slot_carry), _p(carry), n_rows, row_len, H, ld_out,
+                                  _p(h_out), _p(c_out), _p(save), _stream()), "dgc_rnn_fwd"),
+        nb, 2.0 * n_rows * row_len * H * G * H)
+
+
+def rnn_bwd(cell, Ut, slot_row, slot_mask, n_rows, row_len, H, save, dh_out, dgx):
+    """K3/K4 dgc_rnn_bwd (BPTT over packed runs)."""
+    _req(dh_out, torch.float32, "dh_out"); _req(dgx, torch.float32, "dgx")
+    n_inst, G = dgx.shape[0], (3 if cell == 0 else 4)
+    sf = rnn_save_floats(cell, H)
+    nb = 4 * n_inst * (G * H + sf + H) + 5 * n_rows * row_len + 4 * G * H * H
+    _run("gru_bwd" if cell == 0 else "lstm_bwd", lambda: _native.check(
+        _native.lib().dgc_rnn_bwd(cell, _p(Ut), _p(slot_row), _p(slot_mask), n_rows, row_len, H,
+                                  _p(save), _p(dh_out), _p(dgx), _stream()), "dgc_rnn_bwd"),
+        nb, 2.0 * n_rows * row_len * H * G * H)
+
+
+def transpose(x, out):
+    _run("transpose", lambda: _native.check(_native.lib().dgc_transpose(
+        _p(x), x.shape[0], x.shape[1], _p(out), _stream()), "dgc_transpose"), 8 * x.numel())
+    return out
+
+
+def stale_distance(Y, key_rows, cache, cached, width, dist, dmax):
+    """K5 dgc_stale_distance."""
+    k = key_rows.numel()
+    _run("stale_distance", lambda: _native.check(_native.lib().dgc_stale_distance(
+        _p(Y), _p(key_rows), _p(cache), _p(cached), k, width, _p(dist), _p(dmax), _stream()),
+        "dgc_stale_distance"), k * (8 * width + 9), 3 * k * width, 2)
+
+
+def stale_select(Y, key_rows, dist, theta, cache, cached, send, width):
+    """K5 dgc_stale_select (strict > theta; theta < 0 sends all)."""
+    k = key_rows.numel()
+    _run("stale_select", lambda: _native.check(_native.lib().dgc_stale_select(
+        _p(Y), _p(key_rows), _p(dist), float(theta), _p(cache), _p(cached), _p(send), k, width,
+        _stream()), "dgc_stale_select"), k * 10)
+
+
+def compact_sent(pos, send, out_idx, count):
+    """K6 dgc_compact_sent."""
+    _run("compact_sent", lambda: _native.check(_native.lib().dgc_compact_sent(
+        _p(pos), pos.numel(), _p(send), _p(out_idx), _p(count), _stream()), "dgc_compact_sent"),
+        9 * pos.numel())
+
+
+def gather_rows(Y, rows, idx, n, width, out):
+    """K6 dgc_gather_rows: out[i] = Y[rows[idx[i]]]."""
+    _run("gather_rows", lambda: _native.check(_native.lib().dgc_gather_rows(
+        _p(Y), _p(rows), _p(idx), n, width, _p(out), _stream()), "dgc_gather_rows"),
+        n * (8 * width + 8))
+    return out
+
+
+def scatter_rows(src, rows, idx, n, width, dst, add=False):
+    """K6 dgc_scatter_rows: dst[rows[idx[i]]] (+)= src[i]."""
+    _run("scatter_rows", lambda: _native.check(_native.lib().dgc_scatter_rows(
+        _p(src), _p(rows), _p(idx), n, width, _p(dst), int(add), _stream()), "dgc_scatter_rows"),
+        n * (4 * width * (2 + int(add)) + 8))
+    return dst
+
+
+def softmax_xent(logits, labels, C, scale, dlogits, loss_partial):
+    """K8 dgc_softmax_xent."""
+    n = labels.numel()
+    _run("softmax_xent", lambda: _native.check(_native.lib().dgc_softmax_xent(
+        _p(logits), _p(labels), n, C, float(scale), _p(dlogits), _p(loss_partial), _stream()),
+        "dgc_softmax_xent"), n * (8 * C + 4))
+
+
+def colsum(X, n, width, ld, out, scratch, accumulate=False):
+    _run("colsum", lambda: _native.check(_native.lib().dgc_colsum(
+        _p(X), n, width, ld, _p(out), int(accumulate), _p(scratch), _stream()), "dgc_colsum"),
+        4 * n * width, n * width, 2)
+    return out
+
+
+def relu_bwd(dH, H, dZ):
+    _run("relu_bwd", lambda: _native.check(_native.lib().dgc_relu_bwd(
+        _p(dH), _p(H), _p(dZ), dH.numel(), _stream()), "dgc_relu_bwd"), 12 * dH.numel())
+    return dZ
+
+
+def sgd(p, g, mom, lr, momentum):
+    _run("sgd", lambda: _native.check(_native.lib().dgc_sgd(
+        _p(p), _p(g), _p(mom), p.numel(), float(lr), float(momentum), _stream()), "dgc_sgd"),
+        20 * p.numel())
+
+
+def adam(p, g, m, v, lr, b1, b2, eps, step):
+    _run("adam", lambda: _native.check(_native.lib().dgc_adam(
+        _p(p), _p(g), _p(m), _p(v), p.numel(), float(lr), float(b1), float(b2), float(eps),
+        int(step), _stream()), "dgc_adam"), 28 * p.numel())

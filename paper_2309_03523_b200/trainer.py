@@ -1,0 +1,568 @@
+"""The B200 chunk-partitioned DGNN training step behind the reference's
+trainer API (simulate_epoch / run_epochs, sim.py:423-599).
+
+One ``Shard`` = one device's share of the reference plan (its fusion groups,
+SURVEY.md §8(b)). ``Shard.step`` is a generator that yields at every
+collective; a ``Runner`` services the yields either with torch.distributed
+NCCL (one process per GPU, the production path) or by direct device copies
+among all shards of one process (``LocalRunner``: D virtual devices on one
+GPU, used for parity tests and single-GPU runs of multi-device plans). The
+arithmetic is identical in both.
+
+Per epoch and shard:
+  GCN layer l: Y = H_{l-1} W_l (K2) -> [K5 stale filter, MAX all-reduce of D_r,
+    K6 pack, all-to-allv, unpack into halo rows] -> H_l = relu(A_hat Y + b) (K1)
+  RNN layer k: gx = x Wx + b (K2) -> masked GRU/LSTM over packed runs (K3/K4)
+    -> carry exchange for the next epoch (K5/K6)
+  readout + CE (K2, K8) -> backward (K2/K3/K4/K1 transposed, reverse all-to-allv
+  of fresh halo gradients) -> SUM all-reduce of the flat gradient (K7) ->
+  Adam/SGD.
+"""
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import ops
+from .layout import DeviceLayout, build_layout
+from .model import DGNNConfig, flat_offsets, init_params, synthetic_inputs
+from .plan import PlanArrays
+from .stale import (EmbeddingCacheGPU, EpochLossTrace, StaleConfig, StaleMode, cache_gap_gpu,
+                    filter_transmissions_gpu, threshold)
+
+
+@dataclass
+class EpochReport:
+    """Fields of the reference EpochReport (sim.py:259-303), filled with
+    measured times and the reference-billed bytes of the actual send masks;
+    the extra fields are additive."""
+    method: str
+    epoch: int
+    per_device_compute_ms: list
+    per_device_wall_ms: list
+    spatial_traffic_bytes: int
+    temporal_traffic_bytes: int
+    shuffle_bytes: int
+    loading_bytes: int
+    padding_slots: int
+    naive_padding_slots: int
+    load_divergence: float
+    wall_ms: float
+    stale_theta: float = 0.0
+    stale_d: float = 0.0
+    stale_sent_bytes: int = 0
+    stale_avoided_bytes: int = 0
+    stale_reduction_pct: float = 0.0
+    loss: float = 0.0
+    exchanged_rows: int = 0
+    exchanged_bytes: int = 0
+    stale_detail: dict = field(default_factory=dict)
+
+    @property
+    def traffic_bytes(self) -> int:
+        return self.spatial_traffic_bytes + self.temporal_traffic_bytes + self.shuffle_bytes
+
+    def to_dict(self) -> dict:
+        d = dict(self.__dict__)
+        d["traffic_bytes"] = self.traffic_bytes
+        return d
+
+
+def _dev_i32(a, device):
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32), device=device)
+
+
+class Shard:
+    """One device's state: layout tensors, activations, caches, parameters."""
+
+    def __init__(self, pa: PlanArrays, lay: DeviceLayout, cfg: DGNNConfig, params: dict,
+                 X: np.ndarray, y: np.ndarray, stale: StaleConfig, n_total: int, device):
+        self.pa, self.lay, self.cfg, self.stale = pa, lay, cfg, stale
+        self.d, self.D = lay.device, lay.n_devices
+        self.device = device
+        self.n_total = n_total
+        dev = device
+        n, nh, H, F = lay.n_own, lay.n_halo, cfg.H, cfg.F
+        self.n, self.nh, self.nloc = n, nh, n + nh
+        self.prec = 3 if cfg.precision == "fp32" else 1
+        # layout on device
+        self.row_ptr = _dev_i32(lay.row_ptr, dev)
+        self.col = _dev_i32(lay.col, dev)
+        self.t_row_ptr = _dev_i32(lay.t_row_ptr, dev)
+        self.t_col = _dev_i32(lay.t_col, dev)
+        self.dinv = torch.as_tensor(lay.dinv.astype(np.float32), device=dev)
+        self.slot_row = _dev_i32(lay.slot_row, dev)
+        self.slot_mask = torch.as_tensor(lay.slot_mask.astype(np.uint8), device=dev)
+        self.slot_carry = _dev_i32(lay.slot_carry, dev)
+        self.R, self.L = lay.n_rows, lay.row_len
+        self.nnz = lay.nnz
+        self.key_rows = _dev_i32(lay.key_rows, dev)
+        self.key_ncut = torch.as_tensor(lay.key_ncut.astype(np.int64), device=dev)
+        self.tkey_rows = _dev_i32(lay.tkey_rows, dev)
+        peers = [p for p in range(self.D) if p != self.d]
+        self.peers = peers
+        sp, rp = lay.send_ptr, lay.recv_ptr
+        tsp, trp = lay.tsend_ptr, lay.trecv_ptr
+        self.send_pos = {p: _dev_i32(lay.send_pos[sp[p]:sp[p + 1]], dev) for p in peers}
+        self.send_rows = {p: _dev_i32(lay.key_rows[lay.send_pos[sp[p]:sp[p + 1]]], dev) for p in peers}
+        self.recv_slot = {p: _dev_i32(lay.recv_slot[rp[p]:rp[p + 1]], dev) for p in peers}
+        self.tsend_pos = {p: _dev_i32(lay.tsend_pos[tsp[p]:tsp[p + 1]], dev) for p in peers}
+        self.tsend_rows = {p: _dev_i32(lay.tkey_rows[lay.tsend_pos[tsp[p]:tsp[p + 1]]], dev) for p in peers}
+        self.trecv_carry = {p: _dev_i32(lay.trecv_carry[trp[p]:trp[p + 1]], dev) for p in peers}
+        # data
+        self.X = torch.as_tensor(X[lay.own_gid], device=dev).contiguous()
+        self.y = torch.as_tensor(y[lay.own_gid].astype(np.int32), device=dev)
+        # parameters (flat) and optimizer state
+        self.offs, P = flat_offsets(cfg)
+        self.params = torch.zeros(P, dtype=torch.float32, device=dev)
+        self.grads = torch.zeros(P, dtype=torch.float32, device=dev)
+        self.m = torch.zeros(P, dtype=torch.float32, device=dev)
+        self.v = torch.zeros(P, dtype=torch.float32, device=dev)
+        for k, arr in params.items():
+            self.p(k).copy_(torch.as_tensor(np.asarray(arr, np.float32)))
+        # activations
+        G, GH = cfg.G, cfg.G * H
+        f32 = dict(dtype=torch.float32, device=dev)
+        self.Yext = [torch.zeros((self.nloc, H), **f32) for _ in range(2)]
+        self.Hl = [torch.zeros((n, H), **f32) for _ in range(2)]
+        self.hw = cfg.carry_width
+        self.gx = torch.zeros((n, GH), **f32)
+        self.hbuf = [torch.zeros((n, self.hw), **f32) for _ in range(cfg.n_rnn)]
+        self.sf = ops.rnn_save_floats(0 if cfg.rnn == "gru" else 1, H)
+        self.save = [torch.zeros((n, self.sf), **f32) for _ in range(cfg.n_rnn)]
+        self.carry = [torch.zeros((max(lay.n_carry, 1), self.hw), **f32) for _ in range(cfg.n_rnn)]
+        self.logits = torch.zeros((n, cfg.C), **f32)
+        self.dlogits = torch.zeros((n, cfg.C), **f32)
+        self.loss_partial = torch.zeros(max(1, (n + 255) // 256), dtype=torch.float64, device=dev)
+        self.dh = torch.zeros((n, H), **f32)
+        self.dh2 = torch.zeros((n, H), **f32)
+        self.dgx = torch.zeros((n, GH), **f32)
+        self.Ut = torch.zeros((GH, H), **f32)
+        self.dYext = torch.zeros((self.nloc, H), **f32)
+        self.colsum_scratch = torch.zeros(max(1, (n + 1023) // 1024) * max(GH, cfg.C, H), **f32)
+        # split-K for weight gradients: ~one wave of 148 SMs
+        kb = max(1, (n + 31) // 32)
+        self.ksplit = max(1, min(148, kb // 4))
+        n_split = ops.gemm_splits(max(n, 1), self.prec, self.ksplit)
+        self.partial = torch.zeros(n_split * max(F, H) * max(GH, H, cfg.C), **f32)
+        # stale caches (spatial per GCN layer, temporal per RNN layer)
+        stale_on = stale.mode is not StaleMode.OFF and self.D > 1
+        self.stale_on = stale_on
+        self.scache = [EmbeddingCacheGPU(len(lay.key_rows), H, dev) for _ in range(2)] if stale_on else None
+        self.tcache = [EmbeddingCacheGPU(len(lay.tkey_rows), self.hw, dev) for _ in range(cfg.n_rnn)] if stale_on else None
+        self.compact_idx = torch.zeros(max(1, len(lay.key_rows), len(lay.tkey_rows)), dtype=torch.int32, device=dev)
+        self.fresh = [{} for _ in range(2)]  # layer -> {peer: (recv idx tensor)}
+        self.sent = [{} for _ in range(2)]   # layer -> {peer: (send idx tensor or None, count)}
+        self.step_count = 0
+        self.events = None
+
+    def p(self, name):
+        o, shape = self.offs[name]
+        n = int(np.prod(shape))
+        return self.params[o:o + n].view(*shape)
+
+    def g(self, name):
+        o, shape = self.offs[name]
+        n = int(np.prod(shape))
+        return self.grads[o:o + n].view(*shape)
+
+    def gp(self, name):
+        """data pointer offset helper for column slices"""
+        return self.offs[name][0]
+
+    # -- exchanges ------------------------------------------------------------
+    def _decide(self, r, trace, Y, keys, cache, key):
+        """Stale decision of one cache: returns (theta, d_r) and leaves the send
+        mask in cache.send. Yields one MAX all-reduce for the global D_r."""
+        d_r = 0.0
+        theta = 0.0
+        if r >= 2:
+            cache_gap_gpu(Y, keys, cache)
+            dmax = yield ("max", cache.dmax)
+            d_r = float(dmax.item())
+            theta = threshold(trace, r, d_r, self.stale)
+        filter_transmissions_gpu(Y, keys, cache, theta)
+        return theta, d_r
+
+    def _exchange_rows(self, Y, width, send_pos, send_rows, dst, recv_rows, cache):
+        """Pack the (stale-filtered) rows per peer, all-to-allv, unpack.
+        Returns {peer: received idx tensor} and {peer: (sent idx, count)}."""
+        sends, idxs, sent = [], [], {}
+        for p in self.peers:
+            if cache is not None:
+                cnt = torch.zeros(1, dtype=torch.int32, device=self.device)
+                ops.compact_sent(send_pos[p], cache.send, self.compact_idx, cnt)
+                c = int(cnt.item())
+                idx = self.compact_idx[:c].clone()
+            else:
+                c = send_pos[p].numel()
+                idx = torch.arange(c, dtype=torch.int32, device=self.device)
+            buf = torch.empty((c, width), dtype=torch.float32, device=self.device)
+            ops.gather_rows(Y, send_rows[p], idx, c, width, buf)
+            sends.append(buf)
+            idxs.append(idx)
+            sent[p] = (idx, c)
+        recv = yield ("a2av", sends, idxs)
+        fresh = {}
+        for p, (buf, idx) in zip(self.peers, zip(*recv)):
+            ops.scatter_rows(buf, recv_rows[p], idx, idx.numel(), width, dst)
+            fresh[p] = idx
+        return fresh, sent
+
+    def _exchange_back(self, l, dYext, H):
+        """Reverse all-to-allv of the gradients of fresh halo rows
+        (Appendix B.4: reused rows return nothing)."""
+        sends, idxs = [], []
+        for p in self.peers:
+            idx = self.fresh[l][p]
+            buf = torch.empty((idx.numel(), H), dtype=torch.float32, device=self.device)
+            ops.gather_rows(dYext, self.recv_slot[p], idx, idx.numel(), H, buf)
+            sends.append(buf)
+            idxs.append(idx)
+        recv = yield ("a2av", sends, idxs)
+        for p, (buf, _) in zip(self.peers, zip(*recv)):
+            idx, c = self.sent[l][p]
+            ops.scatter_rows(buf, self.send_rows[p], idx, c, H, dYext, add=True)
+
+    # -- one training step ----------------------------------------------------
+    def step(self, r: int, trace: EpochLossTrace):
+        cfg, H, n, prec = self.cfg, self.cfg.H, self.n, self.prec
+        G, GH = cfg.G, cfg.G * cfg.H
+        cell = 0 if cfg.rnn == "gru" else 1
+        info = {"theta": {}, "d_r": {}, "billed_sp": 0, "billed_tm": 0, "rows": 0}
+        D = self.D
+        # ---------------- forward: structure encoder ----------------
+        hin, ldin, kin = self.X, cfg.F, cfg.F
+        for l, (W, b) in enumerate((("W1", "b1"), ("W2", "b2"))):
+            Y = self.Yext[l]
+            ops.gemm(hin, self.p(W), Y, n, H, kin, lda=ldin, precision=prec)
+            if D > 1:
+                cache = self.scache[l] if self.stale_on else None
+                if cache is not None:
+                    th, dr = yield from self._decide(r, trace, Y, self.key_rows, cache, f"s{l}")
+                    info["theta"][f"s{l}"], info["d_r"][f"s{l}"] = th, dr
+                    billed = int((cache.send.to(torch.int64) * self.key_ncut).sum().item())
+                else:
+                    billed = int(self.key_ncut.sum().item()) if self.key_ncut.numel() else 0
+                info["billed_sp"] += billed
+                fresh, sent = yield from self._exchange_rows(
+                    Y, H, self.send_pos, self.send_rows, Y, self.recv_slot, cache)
+                self.fresh[l], self.sent[l] = fresh, sent
+                info["rows"] += sum(c for _, c in sent.values())
+            ops.spmm_csr(self.row_ptr, self.col, self.dinv, Y, self.p(b), self.Hl[l], act=1,
+                         nnz=self.nnz, n_cols=self.nloc)
+            hin, ldin, kin = self.Hl[l], H, H
+        # ---------------- forward: time encoder ----------------
+        xr, ldx = self.Hl[1], H
+        for k in range(cfg.n_rnn):
+            ops.gemm(xr, self.p(f"Wx{k}"), self.gx, n, GH, H, lda=ldx, precision=prec,
+                     bias=self.p(f"br{k}"))
+            hb = self.hbuf[k]
+            c_out = hb[:, H:] if cell == 1 else None
+            ops.rnn_fwd(cell, self.gx, self.p(f"U{k}"), self.slot_row, self.slot_mask,
+                        self.slot_carry, self.carry[k], self.R, self.L, H, self.hw, hb, c_out,
+                        self.save[k])
+            if D > 1:
+                cache = self.tcache[k] if self.stale_on else None
+                if cache is not None:
+                    th, dr = yield from self._decide(r, trace, hb, self.tkey_rows, cache, f"t{k}")
+                    info["theta"][f"t{k}"], info["d_r"][f"t{k}"] = th, dr
+                    info["billed_tm"] += int(cache.send.to(torch.int64).sum().item())
+                else:
+                    info["billed_tm"] += int(self.tkey_rows.numel())
+                _, tsent = yield from self._exchange_rows(
+                    hb, self.hw, self.tsend_pos, self.tsend_rows, self.carry[k], self.trecv_carry,
+                    cache)
+                info["rows"] += sum(c for _, c in tsent.values())
+            xr, ldx = hb, self.hw
+        # ---------------- readout + loss ----------------
+        ops.gemm(xr, self.p("Wo"), self.logits, n, cfg.C, H, lda=ldx, precision=prec,
+                 bias=self.p("bo"))
+        ops.softmax_xent(self.logits, self.y, cfg.C, 1.0 / self.n_total, self.dlogits,
+                         self.loss_partial)
+        loss_local = self.loss_partial.sum().reshape(1)
+        loss = yield ("sum", loss_local)
+        info["loss"] = float(loss.item()) / self.n_total
+        # ---------------- backward ----------------
+        self.grads.zero_()
+        ks, part = self.ksplit, self.partial
+        ops.gemm(xr, self.dlogits, self.g("Wo"), H, cfg.C, n, a_mn=True, lda=ldx, precision=prec,
+                 k_splits=ks, partial=part)
+        ops.colsum(self.dlogits, n, cfg.C, cfg.C, self.g("bo"), self.colsum_scratch)
+        ops.gemm(self.dlogits, self.p("Wo"), self.dh, n, H, cfg.C, b_mn=False, ldb=cfg.C,
+                 precision=prec)
+        for k in reversed(range(cfg.n_rnn)):
+            ops.transpose(self.p(f"U{k}"), self.Ut)
+            ops.rnn_bwd(cell, self.Ut, self.slot_row, self.slot_mask, self.R, self.L, H,
+                        self.save[k], self.dh, self.dgx)
+            xin, ldxin = (self.Hl[1], H) if k == 0 else (self.hbuf[k - 1], self.hw)
+            ops.gemm(xin, self.dgx, self.g(f"Wx{k}"), H, GH, n, a_mn=True, lda=ldxin,
+                     precision=prec, k_splits=ks, partial=part)
+            ops.colsum(self.dgx, n, GH, GH, self.g(f"br{k}"), self.colsum_scratch)
+            gU = self.g(f"U{k}")
+            if cell == 0:
+                ops.gemm(self.save[k], self.dgx, gU, H, 2 * H, n, a_mn=True, lda=self.sf,
+                         ldb=GH, ldc=GH, precision=prec, k_splits=ks, partial=part)
+                ops.gemm(self.save[k][:, H:], self.dgx[:, 2 * H:], gU[:, 2 * H:], H, H, n,
+                         a_mn=True, lda=self.sf, ldb=GH, ldc=GH, precision=prec, k_splits=ks,
+                         partial=part)
+            else:
+                ops.gemm(self.save[k], self.dgx, gU, H, GH, n, a_mn=True, lda=self.sf, ldb=GH,
+                         ldc=GH, precision=prec, k_splits=ks, partial=part)
+            relu_src = self.Hl[1] if k == 0 else None
+            ops.gemm(self.dgx, self.p(f"Wx{k}"), self.dh2, n, H, GH, b_mn=False, ldb=GH,
+                     precision=prec, relu_src=relu_src)
+            self.dh, self.dh2 = self.dh2, self.dh
+        dZ = self.dh  # = dH2 * (H2 > 0), fused into the last GEMM epilogue
+        for l in (1, 0):
+            W, b = ("W1", "b1") if l == 0 else ("W2", "b2")
+            ops.colsum(dZ, n, H, H, self.g(b), self.colsum_scratch)
+            ops.spmm_csr(self.t_row_ptr, self.t_col, self.dinv, dZ, None, self.dYext, act=0,
+                         nnz=self.nnz, n_cols=n)
+            if D > 1:
+                yield from self._exchange_back(l, self.dYext, H)
+            hin_l, ldin_l, kin_l = (self.X, cfg.F, cfg.F) if l == 0 else (self.Hl[0], H, H)
+            ops.gemm(hin_l, self.dYext, self.g(W), kin_l, H, n, a_mn=True, lda=ldin_l, ldb=H,
+                     precision=prec, k_splits=ks, partial=part)
+            if l == 1:
+                ops.gemm(self.dYext, self.p("W2"), self.dh2, n, H, H, b_mn=False, ldb=H,
+                         precision=prec, relu_src=self.Hl[0])
+                dZ = self.dh2
+        # ---------------- gradient all-reduce + update ----------------
+        if D > 1:
+            yield ("sum", self.grads)
+        self.step_count += 1
+        if cfg.optimizer == "adam":
+            ops.adam(self.params, self.grads, self.m, self.v, cfg.lr, cfg.beta1, cfg.beta2,
+                     cfg.eps, self.step_count)
+        else:
+            ops.sgd(self.params, self.grads, self.m, cfg.lr, cfg.momentum)
+        return info
+
+
+# -- runners ------------------------------------------------------------------
+
+class LocalRunner:
+    """Services the collectives of all shards of one process by direct copies
+    (virtual devices on one GPU)."""
+
+    def run(self, gens):
+        results = [None] * len(gens)
+        reqs = []
+        for g in gens:
+            reqs.append(next(g))
+        live = [True] * len(gens)
+        while any(live):
+            kind = next(r for r, a in zip(reqs, live) if a)[0]
+            outs = self._service(kind, [r for r in reqs])
+            for i, g in enumerate(gens):
+                if not live[i]:
+                    continue
+                try:
+                    reqs[i] = g.send(outs[i])
+                except StopIteration as stop:
+                    results[i] = stop.value
+                    live[i] = False
+        return results
+
+    def _service(self, kind, reqs):
+        D = len(reqs)
+        if kind == "max":
+            m = torch.stack([r[1].reshape(-1)[0] for r in reqs]).max().reshape(1)
+            return [m.clone() for _ in reqs]
+        if kind == "sum":
+            acc = reqs[0][1].clone()
+            for r in reqs[1:]:
+                acc += r[1]
+            for r in reqs:
+                r[1].copy_(acc)
+            return [r[1] for r in reqs]
+        if kind == "a2av":
+            outs = []
+            for d in range(D):
+                bufs, idxs = [], []
+                for p in range(D):
+                    if p == d:
+                        continue
+                    j = d if d < p else d - 1  # position of d among p's peers
+                    bufs.append(reqs[p][1][j])
+                    idxs.append(reqs[p][2][j])
+                outs.append((bufs, idxs))
+            return outs
+        raise ValueError(kind)
+
+
+class NcclRunner:
+    """One shard per process; collectives through torch.distributed (NCCL)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+
+    def run(self, gens):
+        (g,) = gens
+        dist = self.dist
+        try:
+            req = next(g)
+            while True:
+                kind = req[0]
+                if kind == "max":
+                    t = req[1].clone()
+                    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+                    out = t
+                elif kind == "sum":
+                    dist.all_reduce(req[1], op=dist.ReduceOp.SUM, group=self.group)
+                    out = req[1]
+                else:
+                    out = self._a2av(req[1], req[2])
+                req = g.send(out)
+        except StopIteration as stop:
+            return [stop.value]
+
+    def _a2av(self, bufs, idxs):
+        dist = self.dist
+        D = dist.get_world_size(self.group)
+        me = dist.get_rank(self.group)
+        dev = bufs[0].device if bufs else idxs[0].device
+        width = bufs[0].shape[1] if bufs else 1
+        send_counts = [0] * D
+        peers = [p for p in range(D) if p != me]
+        for p, b in zip(peers, bufs):
+            send_counts[p] = b.shape[0]
+        sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
+        rc = torch.empty_like(sc)
+        dist.all_to_all_single(rc, sc, group=self.group)
+        recv_counts = rc.tolist()
+        send_f = torch.cat([b.reshape(-1) for b in bufs]) if bufs else torch.empty(0, device=dev)
+        send_i = torch.cat(idxs) if idxs else torch.empty(0, dtype=torch.int32, device=dev)
+        recv_f = torch.empty(sum(recv_counts) * width, dtype=torch.float32, device=dev)
+        recv_i = torch.empty(sum(recv_counts), dtype=torch.int32, device=dev)
+        dist.all_to_all_single(recv_f, send_f, [c * width for c in recv_counts],
+                               [c * width for c in send_counts], group=self.group)
+        dist.all_to_all_single(recv_i, send_i, recv_counts, send_counts, group=self.group)
+        out_b, out_i, off = [], [], 0
+        for p in peers:
+            c = recv_counts[p]
+            out_b.append(recv_f[off * width:(off + c) * width].view(c, width))
+            out_i.append(recv_i[off:off + c])
+            off += c
+        return out_b, out_i
+
+
+# -- the trainer ----------------------------------------------------------------
+
+class DGNNTrainer:
+    """Chunk-partitioned DGNN training on B200 driven by the reference plan.
+
+    ``distributed=True``: this process owns the shard of rank
+    torch.distributed.get_rank() (one GPU per rank, NCCL). Otherwise all D
+    shards of the plan live on ``device`` and exchange locally."""
+
+    def __init__(self, pa: PlanArrays, cfg: DGNNConfig, stale_config=None, seed: int = 0,
+                 device=None, distributed: bool = False, features=None, labels=None,
+                 params=None):
+        self.pa, self.cfg = pa, cfg
+        self.stale = StaleConfig.coerce(stale_config)
+        self.device = torch.device(device or "cuda")
+        self.trace = EpochLossTrace()
+        X, y = (features, labels) if features is not None else synthetic_inputs(
+            pa.n_instances, cfg.F, cfg.C, seed)
+        self.params0 = params if params is not None else init_params(cfg, seed)
+        if distributed:
+            import torch.distributed as dist
+            ranks = [dist.get_rank()]
+            if dist.get_world_size() != pa.n_devices:
+                raise ValueError("world size must equal the plan's n_devices")
+            self.runner = NcclRunner()
+        else:
+            ranks = list(range(pa.n_devices))
+            self.runner = LocalRunner()
+        self.layouts = [build_layout(pa, d) for d in ranks]
+        self.shards = [Shard(pa, lay, cfg, self.params0, X, y, self.stale, pa.n_instances,
+                             self.device) for lay in self.layouts]
+        prof = pa.profile or {}
+        self.s_bytes = int(prof.get("bytes_per_scalar", 4))
+        self.blocks = int(prof.get("blocks", 1))
+        self.method = "pgc"
+        self.epoch_no = 0
+
+    def run_epoch(self):
+        r = self.epoch_no + 1
+        torch.cuda.synchronize(self.device)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        infos = self.runner.run([s.step(r, self.trace) for s in self.shards])
+        t1.record()
+        torch.cuda.synchronize(self.device)
+        ms = t0.elapsed_time(t1)
+        self.epoch_no = r
+        loss = infos[0]["loss"]
+        self.trace.append(loss)
+        return self._report(r, ms, infos, loss)
+
+    def _report(self, r, ms, infos, loss):
+        cfg = self.cfg
+        H, s = cfg.H, self.s_bytes
+        per_msg = self.blocks * H * s  # one layer's share of a reference message
+        billed_sp = sum(i["billed_sp"] for i in infos) * per_msg
+        billed_tm = sum(i["billed_tm"] for i in infos) * per_msg
+        full_sp = 2 * sum(int(l.key_ncut.sum()) for l in self.layouts) * per_msg
+        full_tm = cfg.n_rnn * sum(len(l.tkey_rows) for l in self.layouts) * per_msg
+        if len(self.shards) == 1 and self.pa.n_devices > 1:
+            import torch.distributed as dist
+            t = torch.tensor([billed_sp, billed_tm, full_sp, full_tm], dtype=torch.float64,
+                             device=self.device)
+            dist.all_reduce(t)
+            billed_sp, billed_tm, full_sp, full_tm = (int(x) for x in t.tolist())
+        sent = billed_sp + billed_tm
+        full = full_sp + full_tm
+        avoided = full - sent
+        theta = infos[0]["theta"].get("s0", 0.0)
+        d_r = infos[0]["d_r"].get("s0", 0.0)
+        loading = sum(l.loaded_rows for l in self.layouts) * self.pa.feature_dim * s
+        walls = [ms] * len(self.shards)
+        return EpochReport(
+            method=self.method, epoch=r, per_device_compute_ms=walls, per_device_wall_ms=walls,
+            spatial_traffic_bytes=billed_sp, temporal_traffic_bytes=billed_tm, shuffle_bytes=0,
+            loading_bytes=loading if r == 1 else 0,
+            padding_slots=sum(l.padding for l in self.layouts),
+            naive_padding_slots=sum(l.naive_padding for l in self.layouts),
+            load_divergence=1.0, wall_ms=ms, stale_theta=theta, stale_d=d_r,
+            stale_sent_bytes=sent if self.stale.mode is not StaleMode.OFF else 0,
+            stale_avoided_bytes=avoided if self.stale.mode is not StaleMode.OFF else 0,
+            stale_reduction_pct=(100.0 * avoided / full if full and self.stale.mode is not StaleMode.OFF else 0.0),
+            loss=loss, exchanged_rows=sum(i["rows"] for i in infos),
+            exchanged_bytes=sum(i["rows"] for i in infos) * H * 4,
+            stale_detail={"theta": infos[0]["theta"], "d_r": infos[0]["d_r"]})
+
+    def params(self, shard: int = 0) -> dict:
+        sh = self.shards[shard]
+        return {k: sh.p(k).detach().cpu().numpy().copy() for k in sh.offs}
+
+    def grads(self, shard: int = 0) -> dict:
+        sh = self.shards[shard]
+        return {k: sh.g(k).detach().cpu().numpy().copy() for k in sh.offs}
+
+
+def run_epochs(g, plan=None, profile=None, cluster=None, epochs: int = 1, stale_config=None,
+               drift_spec=None, seed: int = 0, coeffs=None, initial_loss=None, loss_decay=None,
+               *, cfg: DGNNConfig | None = None, F: int | None = None, H: int | None = None,
+               distributed: bool = False, device=None):
+    """Drop-in for dynpart.sim.run_epochs (sim.py:569-599): same positional
+    signature, real training. ``g``/``plan`` may be a dynpart DynamicGraph +
+    Plan (converted unchanged) or a PlanArrays (plan=None). drift_spec,
+    coeffs, initial_loss and loss_decay drive the reference's simulated
+    embeddings/loss and are ignored: the embeddings and the loss trace are real."""
+    from .plan import from_dynpart
+    pa = g if isinstance(g, PlanArrays) else from_dynpart(g, plan)
+    prof = profile.to_dict() if hasattr(profile, "to_dict") else (profile or pa.profile)
+    if cfg is None:
+        cfg = DGNNConfig.for_profile(prof, F=F or pa.feature_dim, H=H)
+    trainer = DGNNTrainer(pa, cfg, stale_config, seed=seed, device=device, distributed=distributed)
+    return [trainer.run_epoch() for _ in range(epochs)]

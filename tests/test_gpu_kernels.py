@@ -1,0 +1,226 @@
+"""GPU parity of the individual kernels, called through the C ABI.
+Float kernels are checked against a plain fp64 reference; the GRU and the
+stale filter against the golden vectors the unmodified reference produced."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+dev = "cuda"
+
+
+def t(a, dtype=torch.float32):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype, device=dev)
+
+
+def close(got, ref, rtol, what=""):
+    got, ref = np.asarray(got, np.float64), np.asarray(ref, np.float64)
+    scale = max(1e-30, float(np.abs(ref).max()))
+    err = float(np.abs(got - ref).max()) / scale
+    assert err <= rtol, f"{what}: max |err|/max|ref| = {err:.3e} > {rtol}"
+
+
+@pytest.mark.parametrize("a_mn", [False, True])
+@pytest.mark.parametrize("b_mn", [False, True])
+@pytest.mark.parametrize("prec,tol", [(3, 2e-6), (1, 2e-3)])
+@pytest.mark.parametrize("M,N,K", [(1000, 16, 16), (777, 48, 16), (640, 128, 128),
+                                   (300, 384, 128), (129, 64, 40), (5000, 512, 128)])
+def test_gemm_tf32(a_mn, b_mn, prec, tol, M, N, K):
+    from paper_2309_03523_b200 import ops
+    rng = np.random.default_rng(M + N + K)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((K, N)).astype(np.float32)
+    ref = A.astype(np.float64) @ B.astype(np.float64)
+    # TMA needs 16-byte row strides: pad the leading dimension of transposed copies
+    def padded(x):
+        ld = (x.shape[1] + 3) // 4 * 4
+        out = np.zeros((x.shape[0], ld), np.float32)
+        out[:, :x.shape[1]] = x
+        return t(out), ld
+    Ad, lda = padded(A.T) if a_mn else padded(A)
+    Bd, ldb = padded(B) if b_mn else padded(B.T)
+    C = torch.full((M, N), 7.0, device=dev)
+    ops.gemm(Ad, Bd, C, M, N, K, a_mn=a_mn, b_mn=b_mn, lda=lda, ldb=ldb, precision=prec)
+    close(C.cpu().numpy(), ref, tol, f"gemm a_mn={a_mn} b_mn={b_mn} p={prec}")
+
+
+@pytest.mark.parametrize("splits", [1, 7, 64])
+def test_gemm_split_k_weight_gradient(splits):
+    from paper_2309_03523_b200 import ops
+    rng = np.random.default_rng(5)
+    n, F, H = 20000, 128, 96
+    X = rng.standard_normal((n, F)).astype(np.float32)
+    dY = rng.standard_normal((n, H)).astype(np.float32)
+    ref = X.astype(np.float64).T @ dY.astype(np.float64)
+    C = torch.zeros((F, H), device=dev)
+    part = torch.zeros(ops.gemm_splits(n, 3, splits) * F * H, device=dev)
+    ops.gemm(t(X), t(dY), C, F, H, n, a_mn=True, precision=3, k_splits=splits, partial=part)
+    close(C.cpu().numpy(), ref, 5e-6, "split-K")
+    # determinism: bitwise identical on rerun
+    C2 = torch.zeros_like(C)
+    ops.gemm(t(X), t(dY), C2, F, H, n, a_mn=True, precision=3, k_splits=splits, partial=part)
+    assert torch.equal(C, C2)
+
+
+def test_gemm_epilogues_and_strides():
+    from paper_2309_03523_b200 import ops
+    rng = np.random.default_rng(6)
+    M, N, K, ld = 700, 64, 32, 80
+    A = rng.standard_normal((M, ld)).astype(np.float32)
+    B = rng.standard_normal((K, N)).astype(np.float32)
+    bias = rng.standard_normal(N).astype(np.float32)
+    relu = rng.standard_normal((M, N)).astype(np.float32)
+    C0 = rng.standard_normal((M, N)).astype(np.float32)
+    ref = (C0 + A[:, :K].astype(np.float64) @ B + bias) * (relu > 0)
+    C = t(C0)
+    ops.gemm(t(A), t(B), C, M, N, K, lda=ld, precision=3, bias=t(bias), relu_src=t(relu),
+             accumulate=True)
+    close(C.cpu().numpy(), ref, 2e-6, "epilogue")
+
+
+def _csr(n_rows, n_cols, rng, max_deg=40):
+    deg = rng.integers(0, max_deg, size=n_rows)
+    deg[rng.random(n_rows) < 0.2] = 0
+    rp = np.concatenate([[0], np.cumsum(deg + 1)]).astype(np.int32)
+    col = []
+    for i, d in enumerate(deg):
+        c = np.sort(np.concatenate([[i], rng.choice(n_cols, size=d)]))
+        col.append(c)
+    return rp, np.concatenate(col).astype(np.int32)
+
+
+@pytest.mark.parametrize("W", [16, 128, 512])
+def test_spmm_csr(W):
+    from paper_2309_03523_b200 import ops
+    rng = np.random.default_rng(W)
+    n_rows, n_cols = 3000, 3500
+    rp, col = _csr(n_rows, n_cols, rng)
+    dinv = rng.random(n_cols).astype(np.float32) + 0.1
+    Y = rng.standard_normal((n_cols, W)).astype(np.float32)
+    b = rng.standard_normal(W).astype(np.float32)
+    ref = np.zeros((n_rows, W))
+    for i in range(n_rows):
+        cs = col[rp[i]:rp[i + 1]]
+        ref[i] = dinv[i] * (dinv[cs, None].astype(np.float64) * Y[cs]).sum(0) + b
+    out = torch.zeros((n_rows, W), device=dev)
+    ops.spmm_csr(t(rp, torch.int32), t(col, torch.int32), t(dinv), t(Y), t(b), out, act=1)
+    close(out.cpu().numpy(), np.maximum(ref, 0), 1e-6, "spmm relu")
+    ops.spmm_csr(t(rp, torch.int32), t(col, torch.int32), t(dinv), t(Y), None, out, act=0)
+    close(out.cpu().numpy(), ref - b, 1e-6, "spmm")
+
+
+def test_gru_forward_masked_matches_reference_golden(golden_dir):
+    """Golden vectors of the reference gru_forward_masked (fusion.py:428-469),
+    fp32 GPU vs fp64 reference within allclose(rtol=1e-4, atol=1e-6*max|ref|)
+    (SURVEY.md §8(c) parity metric)."""
+    from paper_2309_03523_b200.fusion import GruCell, gru_forward_masked, pack_sequences
+    z = np.load(golden_dir / "gru.npz")
+    for ci in range(4):
+        p = f"c{ci}_"
+        cell = GruCell(*(z[p + k] for k in GruCell.__dataclass_fields__))
+        lengths = z[p + "lengths"].tolist()
+        xs = z[p + "x"]
+        offs = np.concatenate([[0], np.cumsum(lengths)])
+        seqs = [(e, l) for e, l in enumerate(lengths)]
+        inputs = {e: xs[offs[e]:offs[e + 1]] for e, _ in seqs}
+        out = gru_forward_masked(cell, pack_sequences(seqs), inputs)
+        got = np.concatenate([out[e] for e, _ in seqs])
+        ref = z[p + "h"]
+        np.testing.assert_allclose(got, ref, rtol=1e-4, atol=1e-6 * np.abs(ref).max())
+
+
+def test_stale_filter_matches_reference_golden(golden_dir):
+    """K5 against filter_transmissions/threshold on the reference DriftStream:
+    identical send sets except keys inside the fp32-vs-fp64 tie band."""
+    from paper_2309_03523_b200 import stale as st
+    z = np.load(golden_dir / "stale.npz")
+    modes = {"static3": st.StaleConfig.static(0.3), "tighten": st.StaleConfig.adaptive(True),
+             "relax": st.StaleConfig.adaptive(), "off": st.StaleConfig.off()}
+    for name, cfg in modes.items():
+        emb, send, theta_ref = z[name + "_emb"], z[name + "_send"], z[name + "_theta"]
+        n, dim = emb.shape[1:]
+        cache = st.EmbeddingCacheGPU(n, dim, dev)
+        trace = st.EpochLossTrace()
+        for r in range(1, emb.shape[0] + 1):
+            keys = np.arange(n)[(np.arange(n) + r) % 4 != 0]
+            Y = t(emb[r - 1])
+            # the reference cache is keyed by instance: emulate with all n keys
+            # but only the boundary subset participates this epoch
+            sub = st.EmbeddingCacheGPU(len(keys), dim, dev)
+            sub.values.copy_(cache.values[t(keys, torch.long)])
+            sub.cached.copy_(cache.cached[t(keys, torch.long)])
+            kr = t(keys, torch.int32)
+            theta = 0.0
+            if r >= 2:
+                dmax = st.cache_gap_gpu(Y, kr, sub)
+                d_r = float(dmax.item())
+                theta = st.threshold(trace, r, d_r, cfg)
+                assert theta == pytest.approx(theta_ref[r - 1], rel=1e-6)
+            s = st.filter_transmissions_gpu(Y, kr, sub, theta).cpu().numpy().astype(bool)
+            got = np.zeros(n, np.uint8)
+            got[keys[s]] = 1
+            mism = np.flatnonzero(got != send[r - 1])
+            if len(mism):
+                dist = sub.dist.cpu().numpy()
+                pos = np.searchsorted(keys, mism)
+                assert np.all(np.abs(dist[pos] - theta) <= 1e-5 * max(theta, 1e-30)), name
+            cache.values[t(keys, torch.long)] = sub.values
+            cache.cached[t(keys, torch.long)] = sub.cached
+            trace.append(2.0 * 0.9 ** (r - 1))
+
+
+def test_exchange_pack_unpack():
+    from paper_2309_03523_b200 import ops
+    rng = np.random.default_rng(9)
+    n_keys, W = 5000, 16
+    pos = np.sort(rng.choice(n_keys, 3000, replace=False)).astype(np.int32)
+    send = (rng.random(n_keys) < 0.3).astype(np.uint8)
+    out = torch.zeros(3000, dtype=torch.int32, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+    ops.compact_sent(t(pos, torch.int32), t(send, torch.uint8), out, cnt)
+    ref = np.flatnonzero(send[pos])
+    c = int(cnt.item())
+    assert c == len(ref)
+    np.testing.assert_array_equal(out[:c].cpu().numpy(), ref)
+    Y = rng.standard_normal((n_keys, W)).astype(np.float32)
+    rows = rng.permutation(n_keys)[:3000].astype(np.int32)
+    buf = torch.zeros((c, W), device=dev)
+    ops.gather_rows(t(Y), t(rows, torch.int32), out[:c], c, W, buf)
+    np.testing.assert_array_equal(buf.cpu().numpy(), Y[rows[ref]])
+    dst = torch.zeros((n_keys, W), device=dev)
+    ops.scatter_rows(buf, t(rows, torch.int32), out[:c], c, W, dst, add=True)
+    ops.scatter_rows(buf, t(rows, torch.int32), out[:c], c, W, dst, add=True)
+    exp = np.zeros((n_keys, W), np.float32)
+    exp[rows[ref]] = 2 * Y[rows[ref]]
+    np.testing.assert_array_equal(dst.cpu().numpy(), exp)
+
+
+def test_softmax_xent_colsum_optimizers():
+    from paper_2309_03523_b200 import ops
+    rng = np.random.default_rng(10)
+    n, C = 3001, 16
+    logits = rng.standard_normal((n, C)).astype(np.float32) * 3
+    y = rng.integers(0, C, n).astype(np.int32)
+    dl = torch.zeros((n, C), device=dev)
+    lp = torch.zeros((n + 255) // 256, dtype=torch.float64, device=dev)
+    ops.softmax_xent(t(logits), t(y, torch.int32), C, 0.5, dl, lp)
+    x = logits.astype(np.float64)
+    m = x.max(1, keepdims=True)
+    logp = x - m - np.log(np.exp(x - m).sum(1, keepdims=True))
+    assert float(lp.sum()) == pytest.approx(-logp[np.arange(n), y].sum(), rel=1e-5)
+    g = np.exp(logp)
+    g[np.arange(n), y] -= 1
+    close(dl.cpu().numpy(), 0.5 * g, 1e-5, "dlogits")
+    out = torch.zeros(C, device=dev)
+    scratch = torch.zeros(((n + 1023) // 1024) * C, device=dev)
+    ops.colsum(t(logits), n, C, C, out, scratch)
+    close(out.cpu().numpy(), x.sum(0), 1e-5, "colsum")
+    p = rng.standard_normal(1000).astype(np.float32)
+    gr = rng.standard_normal(1000).astype(np.float32)
+    pd, md, vd = t(p), torch.zeros(1000, device=dev), torch.zeros(1000, device=dev)
+    ops.adam(pd, t(gr), md, vd, 0.01, 0.9, 0.999, 1e-8, 1)
+    mm = 0.1 * gr
+    vv = 0.001 * gr * gr
+    ref = p - 0.01 * (mm / 0.1) / (np.sqrt(vv / 0.001) + 1e-8)
+    close(pd.cpu().numpy(), ref, 1e-6, "adam")

@@ -31,6 +31,15 @@ CONFIGS = {
                profile=ModelProfile(1, 2, 1, "previous-only", 16, 4), fuse=True),
     "c2": dict(N=200_000, T=32, sigma_mult=1.0, D=1, F=16,
                profile=ModelProfile(1, 2, 2, "previous-only", 16, 4), fuse=True),
+    # the C2 graph re-planned for 2/4/8 devices (strong-scaling runs); fusion
+    # off: numerics are fusion-invariant and the Python
+    # fusion planner does not finish at this size in useful time
+    "c2d2": dict(N=200_000, T=32, sigma_mult=1.0, D=2, F=16,
+                 profile=ModelProfile(1, 2, 2, "previous-only", 16, 4), fuse=False),
+    "c2d4": dict(N=200_000, T=32, sigma_mult=1.0, D=4, F=16,
+                 profile=ModelProfile(1, 2, 2, "previous-only", 16, 4), fuse=False),
+    "c2d8": dict(N=200_000, T=32, sigma_mult=1.0, D=8, F=16,
+                 profile=ModelProfile(1, 2, 2, "previous-only", 16, 4), fuse=False),
     # small multi-device variants used by the parity tests (fast to plan)
     "t2": dict(N=3_000, T=8, sigma_mult=1.0, D=2, F=16,
                profile=ModelProfile(1, 2, 1, "previous-only", 16, 4), fuse=True),
