@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--C", type=int, default=16)
     ap.add_argument("--config", default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--detail", action="store_true", help="per-shape kernel table on stderr")
     ap.add_argument("--cpu-sample-s", type=float, default=25.0)
     return ap.parse_args()
 
@@ -216,6 +217,7 @@ def run_ours(args):
         tr.run_epoch()
     # ---- device-timed region (inputs resident in HBM) ----
     times = []
+    ops._prof_detail = args.detail
     prof = ops.profile()
     with ClockSampler(local) as clocks, prof:
         for _ in range(args.steps):
@@ -260,7 +262,7 @@ def run_ours(args):
             dist.destroy_process_group()
         return
     hbm, tflops, src = peaks()
-    top = max(kern.items(), key=lambda kv: kv[1]["ms"])
+    top = max(((k.split("[")[0], v) for k, v in kern.items()), key=lambda kv: kv[1]["ms"])
     name, d = top
     avg_ms = d["ms"] / d["launches"]
     achieved = (d["bytes"] / d["launches"]) / (avg_ms / 1e3) / 1e9
@@ -269,6 +271,10 @@ def run_ours(args):
                       "TFLOPs": (v["flops"] / v["launches"]) / (v["ms"] / v["launches"] / 1e3) / 1e12}
                   for k, v in sorted(kern.items(), key=lambda kv: -kv[1]["ms"])}
     gpu_launches = int(sum(v["kernels"] for v in kern.values()) / args.steps)
+    if args.detail:
+        for k, v in per_kernel.items():
+            print(f"{k:48s} {v['ms_per_step']*1e3:9.1f} us/step  x{v['launches_per_step']:.0f}  "
+                  f"{v['GBps']:8.1f} GB/s {v['TFLOPs']:7.2f} TF/s", file=sys.stderr)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         t_cpu, n_ep = cpu_epoch_time(pa, cfg, args.cpu_sample_s)

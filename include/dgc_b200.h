@@ -167,7 +167,7 @@ int dgc_scatter_rows(const float* src, const int32_t* rows, const int32_t* idx, 
 int dgc_softmax_xent(const float* logits, const int32_t* labels, int64_t n, int32_t C,
                      float scale, float* dlogits, double* loss_partial, void* stream);
 /* Deterministic column sums out[j] (+)= sum_i X[i, j] (bias gradients);
- * scratch >= ceil(n/1024)*width floats. */
+ * scratch >= 296*width floats (<= 2 row blocks per SM). */
 int dgc_colsum(const float* X, int64_t n, int32_t width, int64_t ld, float* out,
                int32_t accumulate, float* scratch, void* stream);
 /* dZ = dH * (H > 0) elementwise */

@@ -40,15 +40,44 @@ __global__ void __launch_bounds__(256) softmax_xent_kernel(const float* __restri
   if (threadIdx.x == 0) loss_partial[blockIdx.x] = red[0];
 }
 
-// stage 1: block b sums rows [b*1024, (b+1)*1024) of every column
-__global__ void colsum_stage1(const float* __restrict__ X, int64_t n, int width, int64_t ld,
-                              float* __restrict__ scratch) {
-  const int64_t r0 = (int64_t)blockIdx.x * 1024;
-  const int64_t r1 = min(r0 + 1024, n);
-  for (int j = threadIdx.x; j < width; j += blockDim.x) {
-    float acc = 0.f;
-    for (int64_t r = r0; r < r1; ++r) acc += X[r * ld + j];
-    scratch[(int64_t)blockIdx.x * width + j] = acc;
+// stage 1: block b sums rows [b*rows_per, (b+1)*rows_per) of every column.
+// Threads tile (row group, float4 column); partials are combined across row
+// groups in fixed order through shared memory (deterministic).
+__global__ void __launch_bounds__(256) colsum_stage1(const float* __restrict__ X, int64_t n,
+                                                     int width, int64_t ld, int64_t rows_per,
+                                                     float* __restrict__ scratch) {
+  extern __shared__ float4 red4[];
+  const int w4 = width / 4;
+  const int cols = w4 < 256 ? w4 : 256;
+  const int groups = 256 / cols;
+  const int tc = threadIdx.x % cols, tg = threadIdx.x / cols;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per;
+  const int64_t r1 = min(r0 + rows_per, n);
+  for (int c = tc; c < w4; c += cols) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (tg < groups) {
+      for (int64_t r = r0 + tg; r < r1; r += groups) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(X + r * ld) + c);
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+      }
+    }
+    __syncthreads();
+    red4[threadIdx.x] = acc;
+    __syncthreads();
+    if (tg == 0) {
+      float4 s = red4[tc];
+      for (int g = 1; g < groups; ++g) {
+        const float4 v = red4[g * cols + tc];
+        s.x += v.x;
+        s.y += v.y;
+        s.z += v.z;
+        s.w += v.w;
+      }
+      reinterpret_cast<float4*>(scratch + (int64_t)blockIdx.x * width)[c] = s;
+    }
   }
 }
 
@@ -110,10 +139,14 @@ extern "C" int dgc_softmax_xent(const float* logits, const int32_t* labels, int6
 
 extern "C" int dgc_colsum(const float* X, int64_t n, int32_t width, int64_t ld, float* out,
                           int32_t accumulate, float* scratch, void* stream) {
+  DGC_REQUIRE(width % 4 == 0 && ld % 4 == 0, "colsum: width and ld must be multiples of 4");
   cudaStream_t s = dgc::as_stream(stream);
-  const int nblk = (int)((n + 1023) / 1024);
+  // ~2 blocks per SM, at least 64 rows each; scratch holds nblk*width floats
+  int64_t rows_per = (n + 2 * dgc::kNumSMs - 1) / (2 * dgc::kNumSMs);
+  if (rows_per < 64) rows_per = 64;
+  const int nblk = (int)((n + rows_per - 1) / rows_per);
   if (nblk > 0) {
-    colsum_stage1<<<nblk, 256, 0, s>>>(X, n, width, ld, scratch);
+    colsum_stage1<<<nblk, 256, 256 * sizeof(float4), s>>>(X, n, width, ld, rows_per, scratch);
     DGC_CHECK_LAUNCH("colsum_stage1");
   }
   colsum_stage2<<<(width + 255) / 256, 256, 0, s>>>(scratch, nblk, width, out, accumulate);

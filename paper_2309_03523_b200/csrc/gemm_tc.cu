@@ -259,34 +259,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_wait(tmem_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // TMEM -> registers (thread = row) -> padded smem transpose -> coalesced
+    // 128-byte row stores (lane = column), epilogue applied in the store pass.
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
-    const int64_t row = m0 + q * 32 + lane;
+    float* stg = reinterpret_cast<float*>(tmem_slot + 4) + (warp - 2) * 32 * 33;
     for (int c = 0; c < bn; c += 32) {
       float v[32];
       tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
-      if (row < M) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) stg[lane * 33 + i] = v[i];
+      __syncwarp();
+      const int64_t n = n0 + c + lane;
+      const bool col_ok = (c + lane < bn) && (n < N);
+      for (int r = 0; r < 32; ++r) {
+        const int64_t row = m0 + q * 32 + r;
+        if (row >= M || !col_ok) continue;
+        float x = stg[r * 33 + lane];
         if (partial) {
-          float* dst = partial + ((int64_t)z * M + row) * N;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int64_t n = n0 + c + i;
-            if (c + i < bn && n < N) dst[n] = v[i];
-          }
+          partial[((int64_t)z * M + row) * N + n] = x;
         } else {
-          float* dst = C + row * ldc;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int64_t n = n0 + c + i;
-            if (c + i < bn && n < N) {
-              float x = v[i];
-              if (accumulate) x += dst[n];
-              if (bias) x += __ldg(bias + n);
-              if (relu_src && !(relu_src[row * ldc + n] > 0.f)) x = 0.f;
-              dst[n] = x;
-            }
-          }
+          float* dst = C + row * ldc + n;
+          if (accumulate) x += *dst;
+          if (bias) x += __ldg(bias + n);
+          if (relu_src && !(relu_src[row * ldc + n] > 0.f)) x = 0.f;
+          *dst = x;
         }
       }
+      __syncwarp();
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -359,7 +358,7 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, float* C, int64_t 
                 cudaStream_t s) {
   const int ab = kABytes + bn * BK * 4;
   const int stage_bytes = ab * (SPLIT3 ? 2 : 1);
-  const int budget = 220 * 1024;
+  const int budget = 200 * 1024;
   int stages = (budget - 2048) / stage_bytes;
   stages = stages > 4 ? 4 : stages;
   if (const char* env = getenv("DGC_GEMM_MAX_STAGES")) {
@@ -367,7 +366,7 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, float* C, int64_t 
     if (cap >= 1 && cap < stages) stages = cap;
   }
   if (stages < 1) return dgc::fail(DGC_ERR_ARG, "gemm: tile does not fit shared memory");
-  const size_t smem = (size_t)stages * stage_bytes + 1024 + 256;
+  const size_t smem = (size_t)stages * stage_bytes + 1024 + 256 + 4 * 32 * 33 * 4;
   auto kern = gemm_tf32_kernel<A_MN, B_MN, SPLIT3>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return dgc::cuda_fail(e, "gemm: set smem");

@@ -16,6 +16,7 @@ _NULL = None
 # Optional per-launch profiler (bench.py): records CUDA events around every
 # native call on the current stream with its algorithmic bytes / flops.
 _prof = None
+_prof_detail = False
 
 
 class profile:
@@ -103,7 +104,10 @@ def gemm(A, B, C, M, N, K, *, a_mn=False, b_mn=True, lda=None, ldb=None, ldc=Non
     ldc = ldc if ldc is not None else N
     splits = gemm_splits(K, precision, k_splits)
     nb = 4 * (M * K + K * N + M * N * (1 + int(accumulate) + int(relu_src is not None)))
-    _run("gemm_tf32" if precision == 1 else "gemm_3xtf32", lambda: _native.check(
+    gname = "gemm_tf32" if precision == 1 else "gemm_3xtf32"
+    if _prof_detail:
+        gname += f"[{M}x{N}x{K} a{int(a_mn)}b{int(b_mn)} s{splits}]"
+    _run(gname, lambda: _native.check(
         _native.lib().dgc_gemm_tf32(
             _p(A), lda, _p(B), ldb, _p(C), ldc, M, N, K, int(a_mn), int(b_mn), precision,
             _p(bias), _p(relu_src), int(accumulate), k_splits, _p(partial), _stream()),

@@ -143,7 +143,7 @@ class Shard:
         self.dgx = torch.zeros((n, GH), **f32)
         self.Ut = torch.zeros((GH, H), **f32)
         self.dYext = torch.zeros((self.nloc, H), **f32)
-        self.colsum_scratch = torch.zeros(max(1, (n + 1023) // 1024) * max(GH, cfg.C, H), **f32)
+        self.colsum_scratch = torch.zeros(2 * 148 * max(GH, cfg.C, H), **f32)
         # split-K for weight gradients: ~one wave of 148 SMs
         kb = max(1, (n + 31) // 32)
         self.ksplit = max(1, min(148, kb // 4))
