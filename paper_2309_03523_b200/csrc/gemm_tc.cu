@@ -129,9 +129,12 @@ template <bool A_MN, bool B_MN, bool SPLIT3>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, int bn, int stages,
-                     int kb_total, int kb_per_split, const float* __restrict__ bias,
-                     const float* __restrict__ relu_src, int accumulate,
-                     float* __restrict__ partial) {
+                     int kb_total, int kb_per_split, int m_tiles, int n_tiles, int splits,
+                     const float* __restrict__ bias, const float* __restrict__ relu_src,
+                     int accumulate, float* __restrict__ partial) {
+  // Persistent: CTA c owns tiles c, c+G, ... of the (split, n-tile, m-tile)
+  // space (m fastest, so a CTA's consecutive tiles share the B panel). Two TMEM
+  // accumulators let the epilogue drain tile i while the MMA runs tile i+1.
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~(uintptr_t)1023);
@@ -141,16 +144,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * stage_bytes);
   uint64_t* empty = full + stages;
   uint64_t* conv = empty + stages;
-  uint64_t* tmem_full = conv + stages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tfull = conv + stages;   // [2]
+  uint64_t* tempty = tfull + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* stg_base = reinterpret_cast<float*>(tmem_slot + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t m0 = (int64_t)blockIdx.x * BM;
-  const int64_t n0 = (int64_t)blockIdx.y * bn;
-  const int z = blockIdx.z;
-  const int kb0 = z * kb_per_split;
-  const int nkb = min(kb_total, kb0 + kb_per_split) - kb0;
-  const uint32_t tmem_cols = bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256;
+  const int n_tiles_total = m_tiles * n_tiles * splits;
+  const uint32_t acc_cols = bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256;
+  const uint32_t tmem_cols = 2 * acc_cols;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -158,7 +160,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&empty[s], 1);
       mbar_init(&conv[s], 128);
     }
-    mbar_init(tmem_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
@@ -174,118 +179,168 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
 
+  auto tile_coords = [&](int t, int64_t& m0, int64_t& n0, int& z, int& kb0, int& nkb) {
+    const int mt = t % m_tiles;
+    const int rest = t / m_tiles;
+    const int nt = rest % n_tiles;
+    z = rest / n_tiles;
+    m0 = (int64_t)mt * BM;
+    n0 = (int64_t)nt * bn;
+    kb0 = z * kb_per_split;
+    nkb = min(kb_total, kb0 + kb_per_split) - kb0;
+  };
+
   if (warp == 0) {
     if (lane == 0) {
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % stages;
-        const uint32_t ph = (kb / stages) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* sa = smem + (size_t)s * stage_bytes;
-        uint8_t* sb = sa + kABytes;
-        mbar_expect_tx(&full[s], (uint32_t)ab_bytes);
-        const int k0 = (kb0 + kb) * BK;
-        if (!A_MN) {
-          tma_load_2d(sa, &tmA, k0, (int)m0, &full[s]);
-        } else {
+      int g = 0;
+      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+        int64_t m0, n0;
+        int z, kb0, nkb;
+        tile_coords(t, m0, n0, z, kb0, nkb);
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const int s = g % stages;
+          const uint32_t ph = (g / stages) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* sa = smem + (size_t)s * stage_bytes;
+          uint8_t* sb = sa + kABytes;
+          mbar_expect_tx(&full[s], (uint32_t)ab_bytes);
+          const int k0 = (kb0 + kb) * BK;
+          if (!A_MN) {
+            tma_load_2d(sa, &tmA, k0, (int)m0, &full[s]);
+          } else {
 #pragma unroll
-          for (int i = 0; i < BM / 32; ++i) tma_load_2d(sa + i * 4096, &tmA, (int)m0 + 32 * i, k0, &full[s]);
-        }
-        if (!B_MN) {
-          tma_load_2d(sb, &tmB, k0, (int)n0, &full[s]);
-        } else {
-          for (int i = 0; i < bn / 32; ++i) tma_load_2d(sb + i * 4096, &tmB, (int)n0 + 32 * i, k0, &full[s]);
+            for (int i = 0; i < BM / 32; ++i)
+              tma_load_2d(sa + i * 4096, &tmA, (int)m0 + 32 * i, k0, &full[s]);
+          }
+          if (!B_MN) {
+            tma_load_2d(sb, &tmB, k0, (int)n0, &full[s]);
+          } else {
+            for (int i = 0; i < bn / 32; ++i)
+              tma_load_2d(sb + i * 4096, &tmB, (int)n0 + 32 * i, k0, &full[s]);
+          }
         }
       }
     }
   } else if (warp == 1) {
     const uint32_t idesc = idesc_tf32(bn, A_MN, B_MN);
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % stages;
-      const uint32_t ph = (kb / stages) & 1;
-      mbar_wait(SPLIT3 ? &conv[s] : &full[s], ph);
+    int g = 0, i = 0;
+    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++i) {
+      int64_t m0, n0;
+      int z, kb0, nkb;
+      tile_coords(t, m0, n0, z, kb0, nkb);
+      const int a = i & 1;
+      const uint32_t aph = (i >> 1) & 1;
+      mbar_wait(&tempty[a], aph ^ 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (lane == 0) {
-        const uint32_t sa = smem_u32(smem + (size_t)s * stage_bytes);
-        const uint32_t sb = sa + kABytes;
+      const uint32_t tacc = tmem_base + (uint32_t)a * acc_cols;
+      for (int kb = 0; kb < nkb; ++kb, ++g) {
+        const int s = g % stages;
+        const uint32_t ph = (g / stages) & 1;
+        mbar_wait(SPLIT3 ? &conv[s] : &full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (lane == 0) {
+          const uint32_t sa = smem_u32(smem + (size_t)s * stage_bytes);
+          const uint32_t sb = sa + kABytes;
 #pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {
-          // K-major: advance 32 B inside the 128-B swizzle row; MN-major: eight
-          // k-rows (two 512-B atoms, 1024 B) per MMA, MN chunks 4096 B apart.
-          const uint32_t ao = A_MN ? kk * 1024 : kk * 32;
-          const uint32_t bo = B_MN ? kk * 1024 : kk * 32;
-          const uint64_t ad = A_MN ? mndesc(sa + ao) : kdesc(sa + ao);
-          const uint64_t bd = B_MN ? mndesc(sb + bo) : kdesc(sb + bo);
-          const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
-          mma_tf32(tmem_base, ad, bd, idesc, acc);
-          if (SPLIT3) {
-            const uint64_t adl = A_MN ? mndesc(sa + ab_bytes + ao) : kdesc(sa + ab_bytes + ao);
-            const uint64_t bdl = B_MN ? mndesc(sb + ab_bytes + bo) : kdesc(sb + ab_bytes + bo);
-            mma_tf32(tmem_base, ad, bdl, idesc, 1u);
-            mma_tf32(tmem_base, adl, bd, idesc, 1u);
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            // K-major: advance 32 B inside the 128-B swizzle row; MN-major: eight
+            // k-rows (two 512-B atoms, 1024 B) per MMA, MN chunks 4096 B apart.
+            const uint32_t ao = A_MN ? kk * 1024 : kk * 32;
+            const uint32_t bo = B_MN ? kk * 1024 : kk * 32;
+            const uint64_t ad = A_MN ? mndesc(sa + ao) : kdesc(sa + ao);
+            const uint64_t bd = B_MN ? mndesc(sb + bo) : kdesc(sb + bo);
+            mma_tf32(tacc, ad, bd, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+            if (SPLIT3) {
+              const uint64_t adl = A_MN ? mndesc(sa + ab_bytes + ao) : kdesc(sa + ab_bytes + ao);
+              const uint64_t bdl = B_MN ? mndesc(sb + ab_bytes + bo) : kdesc(sb + ab_bytes + bo);
+              mma_tf32(tacc, ad, bdl, idesc, 1u);
+              mma_tf32(tacc, adl, bd, idesc, 1u);
+            }
+          }
+          mma_commit(&empty[s]);
+          if (kb == nkb - 1) mma_commit(&tfull[a]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    const int tq = threadIdx.x - 64;  // 0..127
+    const int q = warp & 3;           // TMEM lane quadrant this warp may access
+    float* stg = stg_base + (warp - 2) * 32 * 33;
+    int g = 0, i = 0;
+    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++i) {
+      int64_t m0, n0;
+      int z, kb0, nkb;
+      tile_coords(t, m0, n0, z, kb0, nkb);
+      if (SPLIT3) {
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const int s = g % stages;
+          const uint32_t ph = (g / stages) & 1;
+          mbar_wait(&full[s], ph);
+          float4* hi = reinterpret_cast<float4*>(smem + (size_t)s * stage_bytes);
+          float4* lo = reinterpret_cast<float4*>(smem + (size_t)s * stage_bytes + ab_bytes);
+          for (int e = tq; e < ab_bytes / 16; e += 128) {
+            const float4 x = hi[e];
+            float4 h, l;
+            h.x = __uint_as_float(to_tf32(x.x));
+            h.y = __uint_as_float(to_tf32(x.y));
+            h.z = __uint_as_float(to_tf32(x.z));
+            h.w = __uint_as_float(to_tf32(x.w));
+            l.x = x.x - h.x;
+            l.y = x.y - h.y;
+            l.z = x.z - h.z;
+            l.w = x.w - h.w;
+            hi[e] = h;
+            lo[e] = l;
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive(&conv[s]);
+        }
+      }
+      const int a = i & 1;
+      const uint32_t aph = (i >> 1) & 1;
+      mbar_wait(&tfull[a], aph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      // TMEM -> registers (thread = row) -> padded smem transpose -> coalesced
+      // 128-byte row stores (lane = column), epilogue fused into the store pass.
+      for (int c = 0; c < bn; c += 32) {
+        float v[32];
+        tmem_ld32(tmem_base + (uint32_t)a * acc_cols + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
+#pragma unroll
+        for (int u = 0; u < 32; ++u) stg[lane * 33 + u] = v[u];
+        __syncwarp();
+        const int64_t n = n0 + c + lane;
+        const bool col_ok = (c + lane < bn) && (n < N);
+        const float bn_v = (bias && col_ok) ? __ldg(bias + n) : 0.f;
+#pragma unroll
+        for (int r0 = 0; r0 < 32; r0 += 8) {
+          float x[8], aux[8], acc_in[8];
+          bool ok[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int64_t row = m0 + q * 32 + r0 + u;
+            ok[u] = col_ok && row < M;
+            x[u] = stg[(r0 + u) * 33 + lane];
+            aux[u] = (ok[u] && relu_src) ? relu_src[row * ldc + n] : 1.f;
+            acc_in[u] = (ok[u] && accumulate && !partial) ? C[row * ldc + n] : 0.f;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (!ok[u]) continue;
+            const int64_t row = m0 + q * 32 + r0 + u;
+            if (partial) {
+              partial[((int64_t)z * M + row) * N + n] = x[u];
+            } else {
+              float y = x[u] + acc_in[u] + bn_v;
+              if (relu_src && !(aux[u] > 0.f)) y = 0.f;
+              C[row * ldc + n] = y;
+            }
           }
         }
-        mma_commit(&empty[s]);
+        __syncwarp();
       }
-      __syncwarp();
-    }
-    if (lane == 0) mma_commit(tmem_full);
-    __syncwarp();
-  } else {
-    const int t = threadIdx.x - 64;  // 0..127
-    if (SPLIT3) {
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % stages;
-        const uint32_t ph = (kb / stages) & 1;
-        mbar_wait(&full[s], ph);
-        float4* hi = reinterpret_cast<float4*>(smem + (size_t)s * stage_bytes);
-        float4* lo = reinterpret_cast<float4*>(smem + (size_t)s * stage_bytes + ab_bytes);
-        for (int i = t; i < ab_bytes / 16; i += 128) {
-          const float4 x = hi[i];
-          float4 h, l;
-          h.x = __uint_as_float(to_tf32(x.x));
-          h.y = __uint_as_float(to_tf32(x.y));
-          h.z = __uint_as_float(to_tf32(x.z));
-          h.w = __uint_as_float(to_tf32(x.w));
-          l.x = x.x - h.x;
-          l.y = x.y - h.y;
-          l.z = x.z - h.z;
-          l.w = x.w - h.w;
-          hi[i] = h;
-          lo[i] = l;
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&conv[s]);
-      }
-    }
-    mbar_wait(tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    // TMEM -> registers (thread = row) -> padded smem transpose -> coalesced
-    // 128-byte row stores (lane = column), epilogue applied in the store pass.
-    const int q = warp & 3;  // TMEM lane quadrant this warp may access
-    float* stg = reinterpret_cast<float*>(tmem_slot + 4) + (warp - 2) * 32 * 33;
-    for (int c = 0; c < bn; c += 32) {
-      float v[32];
-      tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) stg[lane * 33 + i] = v[i];
-      __syncwarp();
-      const int64_t n = n0 + c + lane;
-      const bool col_ok = (c + lane < bn) && (n < N);
-      for (int r = 0; r < 32; ++r) {
-        const int64_t row = m0 + q * 32 + r;
-        if (row >= M || !col_ok) continue;
-        float x = stg[r * 33 + lane];
-        if (partial) {
-          partial[((int64_t)z * M + row) * N + n] = x;
-        } else {
-          float* dst = C + row * ldc + n;
-          if (accumulate) x += *dst;
-          if (bias) x += __ldg(bias + n);
-          if (relu_src && !(relu_src[row * ldc + n] > 0.f)) x = 0.f;
-          *dst = x;
-        }
-      }
-      __syncwarp();
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&tempty[a]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -358,8 +413,8 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, float* C, int64_t 
                 cudaStream_t s) {
   const int ab = kABytes + bn * BK * 4;
   const int stage_bytes = ab * (SPLIT3 ? 2 : 1);
-  const int budget = 200 * 1024;
-  int stages = (budget - 2048) / stage_bytes;
+  const int budget = 190 * 1024;
+  int stages = budget / stage_bytes;
   stages = stages > 4 ? 4 : stages;
   if (const char* env = getenv("DGC_GEMM_MAX_STAGES")) {
     const int cap = atoi(env);
@@ -370,9 +425,11 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, float* C, int64_t 
   auto kern = gemm_tf32_kernel<A_MN, B_MN, SPLIT3>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return dgc::cuda_fail(e, "gemm: set smem");
-  dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)ntiles, (unsigned)splits);
-  kern<<<grid, kThreads, smem, s>>>(ma, mb, C, ldc, M, N, bn, stages, kb_total, kb_per, bias,
-                                    relu_src, accumulate, partial);
+  const int m_tiles = (int)((M + BM - 1) / BM);
+  const int total = m_tiles * ntiles * splits;
+  const int grid = total < dgc::kNumSMs ? total : dgc::kNumSMs;
+  kern<<<grid, kThreads, smem, s>>>(ma, mb, C, ldc, M, N, bn, stages, kb_total, kb_per, m_tiles,
+                                    ntiles, splits, bias, relu_src, accumulate, partial);
   DGC_CHECK_LAUNCH("gemm_tf32_kernel");
   return DGC_OK;
 }
