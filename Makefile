@@ -4,12 +4,12 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O3
 SRC := paper_2309_03523_b200/csrc
 OUT := paper_2309_03523_b200/lib
-CU := common spmm stale exchange dense rnn gemm_tc
+CU := common spmm stale exchange dense rnn gemm_tc rnn_tc
 OBJS := $(addprefix build/,$(addsuffix .o,$(CU))) build/layout.o
 
 all: $(OUT)/libdgc_b200.so
 
-build/%.o: $(SRC)/%.cu $(SRC)/common.cuh include/dgc_b200.h
+build/%.o: $(SRC)/%.cu $(SRC)/common.cuh $(SRC)/tc_common.cuh include/dgc_b200.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 

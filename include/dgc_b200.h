@@ -88,7 +88,7 @@ int dgc_pack_sequences(const int32_t* lengths, int64_t n, int32_t row_len,
  * Replaces the analytic structure cost true_cost('structure')
  * (costmodel.py:259-263, billed per fusion group sim.py:339-360,485-486).
  *   out[i] = act( dinv[i] * sum_{c in row i} dinv[c] * Y[c] + bias )
- * act: 0 none, 1 relu. Rows in fusion-group order; ONE launch covers all
+ * act bit 0: relu; bit 1: round the output to TF32 (TF32 mode). Rows in fusion-group order; ONE launch covers all
  * fusion groups of the device. bias may be NULL. The backward uses the same
  * kernel on the transposed CSR (t_row_ptr, t_col). */
 int dgc_spmm_csr(const int32_t* row_ptr, const int32_t* col, const float* dinv,
@@ -116,6 +116,8 @@ int dgc_gemm_tf32(const float* A, int64_t lda, const float* B, int64_t ldb, floa
 /* K3/K4: masked recurrent time encoder over FFD-packed runs.
  * cell: 0 = GRU in the reference form of GruCell.step (fusion.py:409-413),
  *       1 = LSTM (same conventions). Gate order GRU (r,z,c), LSTM (i,f,g,o).
+ *       | DGC_RNN_ROUND_TF32 (0x100): store GEMM-operand outputs (h, r*h, dgx)
+ *       rounded to TF32 (TF32 mode).
  * gx [n_inst, G*H] = x Wx + b (precomputed by K2), U [H, G*H].
  * slot_row/slot_carry [R*L] int32 (-1 = none), slot_mask [R*L] uint8: the
  * carry mask of gru_forward_masked (fusion.py:457-462). A run start with a
@@ -124,11 +126,19 @@ int dgc_gemm_tf32(const float* A, int64_t lda, const float* B, int64_t ldb, floa
  * save [n_inst, dgc_rnn_save_floats] per-instance activations (instance order:
  * GRU [h_in, r*h_in, r, z, c], LSTM [h_in, c_in, i, f, g, o, tanh(c)]).
  * The first H columns of save are the operand of dU = save[:, :H]^T dgx. */
+#define DGC_RNN_ROUND_TF32 0x100
 int dgc_rnn_save_floats(int32_t cell, int32_t H);
 int dgc_rnn_fwd(int32_t cell, const float* gx, const float* U, const int32_t* slot_row,
                 const uint8_t* slot_mask, const int32_t* slot_carry, const float* carry,
                 int64_t n_rows, int32_t row_len, int32_t H, int64_t ld_out, float* h_out,
                 float* c_out, float* save, void* stream);
+/* Tensor-core variant of dgc_rnn_fwd (TF32 tcgen05, persistent CTA per 128
+ * packed rows, h x U on the tensor cores): LSTM, H in {32, 64, 128}. Takes
+ * Ut = U^T [4H, H] (K-major B operand) instead of U; same outputs. */
+int dgc_rnn_fwd_tc(int32_t cell, const float* gx, const float* Ut, const int32_t* slot_row,
+                   const uint8_t* slot_mask, const int32_t* slot_carry, const float* carry,
+                   int64_t n_rows, int32_t row_len, int32_t H, int64_t ld_out, float* h_out,
+                   float* c_out, float* save, void* stream);
 /* BPTT over the same packing (Ut = U^T, [G*H, H], see dgc_transpose): dh_out [n_inst,H] -> dgx [n_inst,G*H]
  * (d pre-activations; dWx = x^T dgx, db = colsum(dgx), dx = dgx Wx^T,
  * dU = save-operand^T dgx by K2). Carries from other devices are constants. */
@@ -162,10 +172,14 @@ int dgc_gather_rows(const float* Y, const int32_t* rows, const int32_t* idx, int
 int dgc_scatter_rows(const float* src, const int32_t* rows, const int32_t* idx, int64_t n,
                      int32_t width, float* dst, int32_t add, void* stream);
 
-/* K8: softmax cross-entropy readout. dlogits = (softmax - onehot) * scale;
- * loss_partial[ceil(n/256)] = per-block fp64 sums of -log p[label]. */
+/* K8: softmax cross-entropy readout. dlogits = (softmax - onehot) * scale
+ * (flags bit 0: rounded to TF32); loss_partial[ceil(n/256)] = per-block fp64
+ * sums of -log p[label]. */
 int dgc_softmax_xent(const float* logits, const int32_t* labels, int64_t n, int32_t C,
-                     float scale, float* dlogits, double* loss_partial, void* stream);
+                     float scale, int32_t flags, float* dlogits, double* loss_partial,
+                     void* stream);
+/* out[i] = in[i] rounded to the nearest TF32 (weights / inputs of TF32 mode) */
+int dgc_round_tf32(const float* in, float* out, int64_t n, void* stream);
 /* Deterministic column sums out[j] (+)= sum_i X[i, j] (bias gradients);
  * scratch >= 296*width floats (<= 2 row blocks per SM). */
 int dgc_colsum(const float* X, int64_t n, int32_t width, int64_t ld, float* out,

@@ -41,6 +41,7 @@ _SIGS = {
     "dgc_gemm_splits": (_i32, [_i64, _i32, _i32]),
     "dgc_rnn_save_floats": (_i32, [_i32, _i32]),
     "dgc_rnn_fwd": (_i32, [_i32, _p, _p, _p, _p, _p, _p, _i64, _i32, _i32, _i64, _p, _p, _p, _p]),
+    "dgc_rnn_fwd_tc": (_i32, [_i32, _p, _p, _p, _p, _p, _p, _i64, _i32, _i32, _i64, _p, _p, _p, _p]),
     "dgc_rnn_bwd": (_i32, [_i32, _p, _p, _p, _i64, _i32, _i32, _p, _p, _p, _p]),
     "dgc_transpose": (_i32, [_p, _i64, _i64, _p, _p]),
     "dgc_stale_distance": (_i32, [_p, _p, _p, _p, _i64, _i32, _p, _p, _p]),
@@ -48,7 +49,8 @@ _SIGS = {
     "dgc_compact_sent": (_i32, [_p, _i64, _p, _p, _p, _p]),
     "dgc_gather_rows": (_i32, [_p, _p, _p, _i64, _i32, _p, _p]),
     "dgc_scatter_rows": (_i32, [_p, _p, _p, _i64, _i32, _p, _i32, _p]),
-    "dgc_softmax_xent": (_i32, [_p, _p, _i64, _i32, _f32, _p, _p, _p]),
+    "dgc_softmax_xent": (_i32, [_p, _p, _i64, _i32, _f32, _i32, _p, _p, _p]),
+    "dgc_round_tf32": (_i32, [_p, _p, _i64, _p]),
     "dgc_colsum": (_i32, [_p, _i64, _i32, _i64, _p, _i32, _p, _p]),
     "dgc_relu_bwd": (_i32, [_p, _p, _p, _i64, _p]),
     "dgc_sgd": (_i32, [_p, _p, _p, _i64, _f32, _f32, _p]),

@@ -19,6 +19,15 @@ inline int grid_for(int64_t work_items, int block, int per_sm = 8) {
   if (g > cap) g = cap;
   return (int)(g < 1 ? 1 : g);
 }
+// Round an fp32 value to the nearest TF32 (10-bit mantissa, ties away). Outputs
+// that feed the tensor cores in TF32 mode are stored pre-rounded so that the
+// tcgen05 operand truncation becomes exact (unbiased errors instead of a
+// systematic shrink).
+__device__ __forceinline__ float rna_tf32_f(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
 }  // namespace dgc
 
 #define DGC_CHECK_LAUNCH(what)                                  \

@@ -10,6 +10,7 @@ namespace {
 __global__ void __launch_bounds__(256) softmax_xent_kernel(const float* __restrict__ logits,
                                                           const int32_t* __restrict__ labels,
                                                           int64_t n, int C, float scale,
+                                                          int round_out,
                                                           float* __restrict__ dlogits,
                                                           double* __restrict__ loss_partial) {
   __shared__ double red[256];
@@ -28,7 +29,7 @@ __global__ void __launch_bounds__(256) softmax_xent_kernel(const float* __restri
     for (int c = 0; c < C; ++c) {
       float p = __expf(x[c] - m) * inv;
       if (c == y) p -= 1.f;
-      dlogits[i * C + c] = p * scale;
+      dlogits[i * C + c] = round_out ? dgc::rna_tf32_f(p * scale) : p * scale;
     }
   }
   red[threadIdx.x] = l;
@@ -100,6 +101,12 @@ __global__ void relu_bwd_kernel(const float4* __restrict__ dH, const float4* __r
   }
 }
 
+__global__ void round_tf32_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = dgc::rna_tf32_f(in[i]);
+}
+
 __global__ void sgd_kernel(float* __restrict__ p, const float* __restrict__ g,
                            float* __restrict__ mom, int64_t n, float lr, float mu) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -127,12 +134,13 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g,
 }  // namespace
 
 extern "C" int dgc_softmax_xent(const float* logits, const int32_t* labels, int64_t n, int32_t C,
-                                float scale, float* dlogits, double* loss_partial, void* stream) {
+                                float scale, int32_t flags, float* dlogits, double* loss_partial,
+                                void* stream) {
   DGC_REQUIRE(C >= 1, "softmax_xent: C must be >= 1");
   if (n == 0) return DGC_OK;
   const int blocks = (int)((n + 255) / 256);
   softmax_xent_kernel<<<blocks, 256, 0, dgc::as_stream(stream)>>>(logits, labels, n, C, scale,
-                                                                 dlogits, loss_partial);
+                                                                 flags & 1, dlogits, loss_partial);
   DGC_CHECK_LAUNCH("softmax_xent_kernel");
   return DGC_OK;
 }
@@ -161,6 +169,13 @@ extern "C" int dgc_relu_bwd(const float* dH, const float* H, float* dZ, int64_t 
       reinterpret_cast<const float4*>(dH), reinterpret_cast<const float4*>(H),
       reinterpret_cast<float4*>(dZ), n / 4);
   DGC_CHECK_LAUNCH("relu_bwd_kernel");
+  return DGC_OK;
+}
+
+extern "C" int dgc_round_tf32(const float* in, float* out, int64_t n, void* stream) {
+  if (n == 0) return DGC_OK;
+  round_tf32_kernel<<<dgc::grid_for(n, 256), 256, 0, dgc::as_stream(stream)>>>(in, out, n);
+  DGC_CHECK_LAUNCH("round_tf32_kernel");
   return DGC_OK;
 }
 

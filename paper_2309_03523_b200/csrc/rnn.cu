@@ -28,7 +28,8 @@ __global__ void gru_fwd_kernel(const float* __restrict__ gx, const float* __rest
                                const uint8_t* __restrict__ slot_mask,
                                const int32_t* __restrict__ slot_carry,
                                const float* __restrict__ carry, int64_t R, int L, int H,
-                               int64_t ld, float* __restrict__ h_out, float* __restrict__ save) {
+                               int64_t ld, float* __restrict__ h_out, float* __restrict__ save,
+                               int rnd) {
   extern __shared__ float sm[];
   const int TY = blockDim.y, TR = TY * RPT;
   float* hs = sm;            // [TR][H]
@@ -90,11 +91,12 @@ __global__ void gru_fwd_kernel(const float* __restrict__ gx, const float* __rest
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
       const float c = tanhf(ac[q]);
-      const float hn = (1.f - z[q]) * c + z[q] * h[q];
+      float hn = (1.f - z[q]) * c + z[q] * h[q];
+      if (rnd) hn = dgc::rna_tf32_f(hn);
       if (inst[q] >= 0) {
         float* sv = save + (int64_t)inst[q] * 5 * H;
         sv[j] = h[q];
-        sv[H + j] = r[q] * h[q];
+        sv[H + j] = rnd ? dgc::rna_tf32_f(r[q] * h[q]) : r[q] * h[q];
         sv[2 * H + j] = r[q];
         sv[3 * H + j] = z[q];
         sv[4 * H + j] = c;
@@ -110,7 +112,7 @@ template <int RPT>
 __global__ void gru_bwd_kernel(const float* __restrict__ Ut, const int32_t* __restrict__ slot_row,
                                const uint8_t* __restrict__ slot_mask, int64_t R, int L, int H,
                                const float* __restrict__ save, const float* __restrict__ dh_out,
-                               float* __restrict__ dgx) {
+                               float* __restrict__ dgx, int rnd) {
   extern __shared__ float sm[];
   const int TY = blockDim.y, TR = TY * RPT;
   float* dar_s = sm;
@@ -171,9 +173,10 @@ __global__ void gru_bwd_kernel(const float* __restrict__ Ut, const int32_t* __re
         dar = dr * r[q] * (1.f - r[q]);
         daz = dz[q] * z[q] * (1.f - z[q]);
         float* o = dgx + (int64_t)inst[q] * G3;
-        o[j] = dar;
-        o[H + j] = daz;
-        o[2 * H + j] = dac_s[lr * H + j];
+        const float dac = dac_s[lr * H + j];
+        o[j] = rnd ? dgc::rna_tf32_f(dar) : dar;
+        o[H + j] = rnd ? dgc::rna_tf32_f(daz) : daz;
+        o[2 * H + j] = rnd ? dgc::rna_tf32_f(dac) : dac;
       }
       dar_s[lr * H + j] = dar;
       daz_s[lr * H + j] = daz;
@@ -201,7 +204,7 @@ __global__ void lstm_fwd_kernel(const float* __restrict__ gx, const float* __res
                                 const int32_t* __restrict__ slot_carry,
                                 const float* __restrict__ carry, int64_t R, int L, int H,
                                 int64_t ld, float* __restrict__ h_out, float* __restrict__ c_out,
-                                float* __restrict__ save) {
+                                float* __restrict__ save, int rnd) {
   extern __shared__ float sm[];
   const int TY = blockDim.y, TR = TY * RPT;
   float* hs = sm;
@@ -255,7 +258,7 @@ __global__ void lstm_fwd_kernel(const float* __restrict__ gx, const float* __res
       const float ig = sigm(a[0][q]), fg = sigm(a[1][q]), gg = tanhf(a[2][q]), og = sigm(a[3][q]);
       const float cn = fg * c[q] + ig * gg;
       const float tc = tanhf(cn);
-      const float hn = og * tc;
+      const float hn = rnd ? dgc::rna_tf32_f(og * tc) : og * tc;
       if (inst[q] >= 0) {
         float* sv = save + (int64_t)inst[q] * 7 * H;
         sv[j] = h[q];
@@ -279,7 +282,7 @@ template <int RPT>
 __global__ void lstm_bwd_kernel(const float* __restrict__ Ut, const int32_t* __restrict__ slot_row,
                                 const uint8_t* __restrict__ slot_mask, int64_t R, int L, int H,
                                 const float* __restrict__ save, const float* __restrict__ dh_out,
-                                float* __restrict__ dgx) {
+                                float* __restrict__ dgx, int rnd) {
   extern __shared__ float sm[];
   const int TY = blockDim.y, TR = TY * RPT;
   float* da_s = sm;  // [TR][4][H]
@@ -319,7 +322,7 @@ __global__ void lstm_bwd_kernel(const float* __restrict__ Ut, const int32_t* __r
         dcp[q] = dcn * fg;
         float* o = dgx + (int64_t)inst[q] * G4;
 #pragma unroll
-        for (int gi = 0; gi < 4; ++gi) o[gi * H + j] = da[gi];
+        for (int gi = 0; gi < 4; ++gi) o[gi * H + j] = rnd ? dgc::rna_tf32_f(da[gi]) : da[gi];
       }
 #pragma unroll
       for (int gi = 0; gi < 4; ++gi) da_s[(lr * 4 + gi) * H + j] = da[gi];
@@ -363,13 +366,16 @@ __global__ void transpose_kernel(const float* __restrict__ in, int64_t rows, int
   }
 }
 
+#ifndef RPT_SEL
+#define RPT_SEL 4
+#endif
 struct Shape {
   int ty, rpt;
 };
 inline Shape pick_shape(int H) {
   // ~256 threads per CTA; rows per CTA = ty * rpt
   const int ty = H >= 256 ? 1 : 256 / H;
-  return {ty < 1 ? 1 : ty, 8};
+  return {ty < 1 ? 1 : ty, RPT_SEL};
 }
 
 }  // namespace
@@ -384,10 +390,11 @@ extern "C" int dgc_transpose(const float* in, int64_t rows, int64_t cols, float*
   return DGC_OK;
 }
 
-extern "C" int dgc_rnn_fwd(int32_t cell, const float* gx, const float* U, const int32_t* slot_row,
+extern "C" int dgc_rnn_fwd(int32_t cell_flags, const float* gx, const float* U, const int32_t* slot_row,
                            const uint8_t* slot_mask, const int32_t* slot_carry, const float* carry,
                            int64_t n_rows, int32_t row_len, int32_t H, int64_t ld_out,
                            float* h_out, float* c_out, float* save, void* stream) {
+  const int cell = cell_flags & 0xff, rnd = (cell_flags >> 8) & 1;
   DGC_REQUIRE(cell == 0 || cell == 1, "rnn_fwd: cell must be 0 (GRU) or 1 (LSTM)");
   DGC_REQUIRE(H >= 1 && H <= 1024, "rnn_fwd: H out of range");
   if (n_rows == 0 || row_len == 0) return DGC_OK;
@@ -397,21 +404,22 @@ extern "C" int dgc_rnn_fwd(int32_t cell, const float* gx, const float* U, const 
   cudaStream_t s = dgc::as_stream(stream);
   if (cell == 0) {
     const size_t smem = 2 * (size_t)TR * H * sizeof(float);
-    gru_fwd_kernel<8><<<grid, block, smem, s>>>(gx, U, slot_row, slot_mask, slot_carry, carry,
-                                                n_rows, row_len, H, ld_out, h_out, save);
+    gru_fwd_kernel<RPT_SEL><<<grid, block, smem, s>>>(gx, U, slot_row, slot_mask, slot_carry, carry,
+                                                n_rows, row_len, H, ld_out, h_out, save, rnd);
     DGC_CHECK_LAUNCH("gru_fwd_kernel");
   } else {
     const size_t smem = (size_t)TR * H * sizeof(float);
-    lstm_fwd_kernel<8><<<grid, block, smem, s>>>(gx, U, slot_row, slot_mask, slot_carry, carry,
-                                                 n_rows, row_len, H, ld_out, h_out, c_out, save);
+    lstm_fwd_kernel<RPT_SEL><<<grid, block, smem, s>>>(gx, U, slot_row, slot_mask, slot_carry, carry,
+                                                 n_rows, row_len, H, ld_out, h_out, c_out, save, rnd);
     DGC_CHECK_LAUNCH("lstm_fwd_kernel");
   }
   return DGC_OK;
 }
 
-extern "C" int dgc_rnn_bwd(int32_t cell, const float* Ut, const int32_t* slot_row,
+extern "C" int dgc_rnn_bwd(int32_t cell_flags, const float* Ut, const int32_t* slot_row,
                            const uint8_t* slot_mask, int64_t n_rows, int32_t row_len, int32_t H,
                            const float* save, const float* dh_out, float* dgx, void* stream) {
+  const int cell = cell_flags & 0xff, rnd = (cell_flags >> 8) & 1;
   DGC_REQUIRE(cell == 0 || cell == 1, "rnn_bwd: cell must be 0 (GRU) or 1 (LSTM)");
   if (n_rows == 0 || row_len == 0) return DGC_OK;
   const Shape sh = pick_shape(H);
@@ -421,18 +429,18 @@ extern "C" int dgc_rnn_bwd(int32_t cell, const float* Ut, const int32_t* slot_ro
   if (cell == 0) {
     const size_t smem = 3 * (size_t)TR * H * sizeof(float);
     if (smem > 48 * 1024) {
-      cudaFuncSetAttribute(gru_bwd_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(gru_bwd_kernel<RPT_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
-    gru_bwd_kernel<8><<<grid, block, smem, s>>>(Ut, slot_row, slot_mask, n_rows, row_len, H, save,
-                                                dh_out, dgx);
+    gru_bwd_kernel<RPT_SEL><<<grid, block, smem, s>>>(Ut, slot_row, slot_mask, n_rows, row_len, H, save,
+                                                dh_out, dgx, rnd);
     DGC_CHECK_LAUNCH("gru_bwd_kernel");
   } else {
     const size_t smem = 4 * (size_t)TR * H * sizeof(float);
     if (smem > 48 * 1024) {
-      cudaFuncSetAttribute(lstm_bwd_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(lstm_bwd_kernel<RPT_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
-    lstm_bwd_kernel<8><<<grid, block, smem, s>>>(Ut, slot_row, slot_mask, n_rows, row_len, H, save,
-                                                 dh_out, dgx);
+    lstm_bwd_kernel<RPT_SEL><<<grid, block, smem, s>>>(Ut, slot_row, slot_mask, n_rows, row_len, H, save,
+                                                 dh_out, dgx, rnd);
     DGC_CHECK_LAUNCH("lstm_bwd_kernel");
   }
   return DGC_OK;

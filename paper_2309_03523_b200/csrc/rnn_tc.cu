@@ -1,0 +1,297 @@
+// K3/K4 on tensor cores: persistent tcgen05 masked LSTM forward (TF32).
+//
+// Same semantics as dgc_rnn_fwd (rnn.cu, the reference form of
+// gru_forward_masked, fusion.py:428-469, carried to the LSTM): a CTA owns a tile
+// of 128 FFD-packed rows for all L positions. Per position p:
+//   MMA   : acc[128, 4H] = h_in[128, H] x U[H, 4H]  (tcgen05.mma.kind::tf32, A =
+//           the h tile in shared memory (K-major SWIZZLE_128B, written by the
+//           epilogue), B = U^T streamed by TMA through a 2-stage ring, fp32 TMEM
+//           accumulator of 4H <= 512 columns);
+//   epi   : 4 warps (thread = packed row = TMEM lane) read the gates 16 units at a
+//           time (tcgen05.ld 32x32b.x16), add the precomputed x Wx + b row of the
+//           slot's instance, update c/h, store h|c / the backward save, and write
+//           the NEXT position's masked h_in (carry mask, or the cross-device carry
+//           at a run start) straight into the swizzled A tile.
+// The input projection x Wx + b of all slots is one K2 GEMM ahead of this kernel.
+#include "tc_common.cuh"
+
+namespace {
+
+using namespace dgc::tc;
+using dgc::make_map;
+
+// warp 0 TMA, warp 1 MMA + TMEM, warps 2..9 epilogue: 2 warps per TMEM lane
+// quadrant (32 packed rows), each owning H/2 hidden units.
+constexpr int kEpiWarps = 8;
+constexpr int kEpiThreads = 32 * kEpiWarps;
+constexpr int kThreads = 64 + kEpiThreads;
+constexpr int kStages = 2;     // B ring: one (k-block, 256-column part) of U^T per stage
+constexpr int kChunk = 16;     // units per TMEM load / smem transpose
+constexpr int kStgStride = 17; // padded row stride of the transpose buffer (floats)
+constexpr int kStgFloats = 4 * 32 * kStgStride;  // 4 gates x 32 rows per warp
+
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// sigmoid(x) = 0.5 * tanh(x/2) + 0.5 (one MUFU op)
+__device__ __forceinline__ float sigm(float x) { return fmaf(0.5f, tanh_fast(0.5f * x), 0.5f); }
+__device__ __forceinline__ float rna_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// Per-position timestamps of CTA 0 (ns, globaltimer) for profiling:
+// [p][0] MMA issue start, [p][1] accumulator ready, [p][2] epilogue done.
+__device__ unsigned long long g_lstm_ts[256][3];
+
+template <int H>
+__global__ void __launch_bounds__(kThreads, 1)
+    lstm_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmUt, const float* __restrict__ gx,
+                       const int32_t* __restrict__ slot_row, const uint8_t* __restrict__ slot_mask,
+                       const int32_t* __restrict__ slot_carry, const float* __restrict__ carry,
+                       int64_t R, int L, int64_t ld, float* __restrict__ h_out,
+                       float* __restrict__ c_out, float* __restrict__ save) {
+  constexpr int G4 = 4 * H;
+  constexpr int KB = H / BK;                 // k-blocks of the h operand
+  constexpr int kABytes = KB * BM * 128;     // h tile (K-major SWIZZLE_128B)
+  constexpr int kNPart = G4 > 256 ? 256 : G4;
+  constexpr int kNParts = G4 / kNPart;
+  constexpr int kBStage = kNPart * 128;      // kNPart rows of U^T x 32 k
+  constexpr int kUnits = H / 2;              // units per epilogue warp
+  constexpr uint32_t kTmemCols = G4 <= 128 ? 128 : G4 <= 256 ? 256 : 512;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kABytes;
+  float* stg_all = reinterpret_cast<float*>(sB + kStages * kBStage);
+  uint64_t* b_full = reinterpret_cast<uint64_t*>(stg_all + kEpiWarps * kStgFloats);
+  uint64_t* b_empty = b_full + kStages;
+  uint64_t* a_full = b_empty + kStages;
+  uint64_t* acc_full = a_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row0 = (int64_t)blockIdx.x * BM;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&b_full[s], 1);
+      mbar_init(&b_empty[s], 1);
+    }
+    mbar_init(a_full, kEpiThreads);
+    mbar_init(acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmUt) : "memory");
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  constexpr int kUnitsPerStep = KB * kNParts;  // B stages per position
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int g = 0; g < L * kUnitsPerStep; ++g) {
+        const int s = g % kStages;
+        mbar_wait(&b_empty[s], ((g / kStages) & 1) ^ 1);
+        const int kb = (g % kUnitsPerStep) / kNParts, part = g % kNParts;
+        mbar_expect_tx(&b_full[s], (uint32_t)kBStage);
+        tma_load_2d(sB + s * kBStage, &tmUt, kb * BK, part * kNPart, &b_full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = idesc_tf32(kNPart, false, false);
+    const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+    for (int p = 0; p < L; ++p) {
+      mbar_wait(a_full, p & 1);
+      fence_after();
+      if (blockIdx.x == 0 && lane == 0 && p < 256) g_lstm_ts[p][0] = globaltimer();
+      for (int u = 0; u < kUnitsPerStep; ++u) {
+        const int g = p * kUnitsPerStep + u;
+        const int s = g % kStages;
+        const int kb = u / kNParts, part = u % kNParts;
+        mbar_wait(&b_full[s], (g / kStages) & 1);
+        fence_after();
+        if (lane == 0) {
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint64_t ad = kdesc(a_base + kb * BM * 128 + kk * 32);
+            const uint64_t bd = kdesc(b_base + s * kBStage + kk * 32);
+            mma_tf32(tmem_base + part * kNPart, ad, bd, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&b_empty[s]);
+          if (u == kUnitsPerStep - 1) mma_commit(acc_full);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // Epilogue. TMEM rows are packed rows (thread = row for tcgen05.ld); every
+    // 16-unit chunk is transposed through shared memory so that global traffic
+    // runs with lanes = (2 rows x 16 units): each gx / h / c / save access is a
+    // contiguous 64-byte row segment instead of 32 scattered rows.
+    const int ew = warp - 2;
+    const int q = warp & 3;                 // TMEM lane quadrant
+    const int u_lo = (ew >> 2) * kUnits;    // this warp's unit range
+    float* stg = stg_all + ew * kStgFloats;
+    const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
+    const int uu = lane & 15, rr = lane >> 4;  // lane -> (row parity, unit)
+    auto a_ptr = [&](int r, int k) {
+      return reinterpret_cast<float*>(sA + (k / BK) * BM * 128 + sw128_offset(r, k % BK));
+    };
+    // prologue: h_in of position 0 (run start: carry or zero)
+    for (int it = 0; it < 16; ++it) {
+      const int r = q * 32 + it * 2 + rr;
+      const int64_t row = row0 + r;
+      const int ci = row < R ? slot_carry[row * L] : -1;
+      for (int j = u_lo + uu; j < u_lo + kUnits; j += 16)
+        *a_ptr(r, j) = ci >= 0 ? rna_tf32(carry[(int64_t)ci * 2 * H + j]) : 0.f;
+    }
+    fence_async_smem();
+    mbar_arrive(a_full);
+    for (int p = 0; p < L; ++p) {
+      const bool has_next = p + 1 < L;
+      // per-row slot info of this warp's 32 rows, one row per lane (issued before
+      // the accumulator wait so the loads overlap the MMA); broadcast by shuffle
+      const int64_t my_row = row0 + q * 32 + lane;
+      const bool my_ok = my_row < R;
+      const int64_t my_s = my_row * L + p;
+      const int my_inst = my_ok ? slot_row[my_s] : -1;
+      const bool my_mk = my_ok && slot_mask[my_s];
+      const int my_ci = my_ok ? slot_carry[my_s] : -1;
+      const int my_prev = (p > 0 && my_mk) ? slot_row[my_s - 1] : -1;
+      const float my_mnext = (has_next && my_ok) ? (float)slot_mask[my_s + 1] : 0.f;
+      const int my_cnext = (has_next && my_ok) ? slot_carry[my_s + 1] : -1;
+      mbar_wait(acc_full, p & 1);
+      fence_after();
+      if (blockIdx.x == 0 && threadIdx.x == 64 && p < 256) g_lstm_ts[p][1] = globaltimer();
+#pragma unroll 1
+      for (int j0 = u_lo; j0 < u_lo + kUnits; j0 += kChunk) {
+        // TMEM (thread = row) -> smem [gate][row][unit]
+#pragma unroll
+        for (int gi = 0; gi < 4; ++gi) {
+          float a[16];
+          tmem_ld16(tl + gi * H + j0, a);
+#pragma unroll
+          for (int u = 0; u < 16; ++u) stg[(gi * 32 + lane) * kStgStride + u] = a[u];
+        }
+        __syncwarp();
+        const int j = j0 + uu;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          // issue every global load of 8 row pairs first (memory-level parallelism)
+          float xg[8][4], cin[8];
+          int inst[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const int rl = (half * 8 + t) * 2 + rr;
+            inst[t] = __shfl_sync(0xffffffffu, my_inst, rl);
+            const int ci = __shfl_sync(0xffffffffu, my_ci, rl);
+            const int prev = __shfl_sync(0xffffffffu, my_prev, rl);
+            const float* gr = gx + (int64_t)max(inst[t], 0) * G4 + j;
+#pragma unroll
+#ifndef DGC_EXP_NOGX
+            for (int gi = 0; gi < 4; ++gi) xg[t][gi] = inst[t] >= 0 ? __ldg(gr + gi * H) : 0.f;
+#else
+            for (int gi = 0; gi < 4; ++gi) xg[t][gi] = 0.f;
+#endif
+            cin[t] = ci >= 0 ? carry[(int64_t)ci * 2 * H + H + j]
+                             : (prev >= 0 ? c_out[(int64_t)prev * ld + j] : 0.f);
+          }
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const int rl = (half * 8 + t) * 2 + rr;
+            const int r = q * 32 + rl;
+            const float m_next = __shfl_sync(0xffffffffu, my_mnext, rl);
+            const int c_next = __shfl_sync(0xffffffffu, my_cnext, rl);
+            const float hin = *a_ptr(r, j);
+            float hn = 0.f;
+            if (inst[t] >= 0) {
+              const float ig = sigm(stg[(0 * 32 + rl) * kStgStride + uu] + xg[t][0]);
+              const float fg = sigm(stg[(1 * 32 + rl) * kStgStride + uu] + xg[t][1]);
+              const float gg = tanh_fast(stg[(2 * 32 + rl) * kStgStride + uu] + xg[t][2]);
+              const float og = sigm(stg[(3 * 32 + rl) * kStgStride + uu] + xg[t][3]);
+              const float cn = fg * cin[t] + ig * gg;
+              const float tc = tanh_fast(cn);
+              hn = rna_tf32(og * tc);
+              float* sv = save + (int64_t)inst[t] * 7 * H + j;
+#ifndef DGC_EXP_NOSAVE
+              sv[0] = hin;
+              sv[H] = cin[t];
+              sv[2 * H] = ig;
+              sv[3 * H] = fg;
+              sv[4 * H] = gg;
+              sv[5 * H] = og;
+              sv[6 * H] = tc;
+#endif
+              h_out[(int64_t)inst[t] * ld + j] = hn;
+              c_out[(int64_t)inst[t] * ld + j] = cn;
+            }
+            if (has_next)
+              *a_ptr(r, j) = c_next >= 0 ? rna_tf32(carry[(int64_t)c_next * 2 * H + j]) : hn * m_next;
+          }
+        }
+        __syncwarp();
+      }
+      if (blockIdx.x == 0 && threadIdx.x == 64 && p < 256) g_lstm_ts[p][2] = globaltimer();
+      if (has_next) {
+        fence_before();
+        fence_async_smem();
+        mbar_arrive(a_full);
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
+}
+
+template <int H>
+int launch_lstm_tc(const float* gx, const float* Ut, const int32_t* slot_row,
+                   const uint8_t* slot_mask, const int32_t* slot_carry, const float* carry,
+                   int64_t R, int L, int64_t ld, float* h_out, float* c_out, float* save,
+                   cudaStream_t s) {
+  CUtensorMap m;
+  const uint32_t box_rows = 4 * H > 256 ? 256 : 4 * H;
+  int rc = make_map(&m, Ut, 4 * H, H, H, 32, box_rows, false);
+  if (rc) return rc;
+  const size_t smem = (size_t)(H / BK) * BM * 128 + (size_t)kStages * box_rows * 128 +
+                      (size_t)kEpiWarps * kStgFloats * 4 + 1024 + 256;
+  auto kern = lstm_fwd_tc_kernel<H>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_fwd_tc: set smem");
+  const int grid = (int)((R + BM - 1) / BM);
+  kern<<<grid, kThreads, smem, s>>>(m, gx, slot_row, slot_mask, slot_carry, carry, R, L, ld,
+                                    h_out, c_out, save);
+  DGC_CHECK_LAUNCH("lstm_fwd_tc_kernel");
+  return DGC_OK;
+}
+
+}  // namespace
+
+extern "C" int dgc_rnn_fwd_tc(int32_t cell, const float* gx, const float* Ut,
+                              const int32_t* slot_row, const uint8_t* slot_mask,
+                              const int32_t* slot_carry, const float* carry, int64_t n_rows,
+                              int32_t row_len, int32_t H, int64_t ld_out, float* h_out,
+                              float* c_out, float* save, void* stream) {
+  DGC_REQUIRE(cell == 1, "rnn_fwd_tc: only the LSTM cell has a tensor-core kernel yet");
+  DGC_REQUIRE(c_out != nullptr, "rnn_fwd_tc: LSTM needs c_out");
+  if (n_rows == 0 || row_len == 0) return DGC_OK;
+  cudaStream_t s = dgc::as_stream(stream);
+  switch (H) {
+    case 32: return launch_lstm_tc<32>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
+    case 64: return launch_lstm_tc<64>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
+    case 128: return launch_lstm_tc<128>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
+    default: return dgc::fail(DGC_ERR_ARG, "rnn_fwd_tc: H must be 32, 64 or 128");
+  }
+}
+
+extern "C" int dgc_debug_lstm_timestamps(unsigned long long* out, int n) {
+  if (n > 256 * 3) n = 256 * 3;
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_lstm_ts, n * sizeof(unsigned long long));
+  return e == cudaSuccess ? DGC_OK : dgc::cuda_fail(e, "debug timestamps");
+}

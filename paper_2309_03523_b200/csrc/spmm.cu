@@ -77,11 +77,17 @@ __global__ void __launch_bounds__(256) spmm_csr_kernel(
       o.y = fmaf(di, acc[v].y, b.y);
       o.z = fmaf(di, acc[v].z, b.z);
       o.w = fmaf(di, acc[v].w, b.w);
-      if (act == 1) {
+      if (act & 1) {
         o.x = fmaxf(o.x, 0.f);
         o.y = fmaxf(o.y, 0.f);
         o.z = fmaxf(o.z, 0.f);
         o.w = fmaxf(o.w, 0.f);
+      }
+      if (act & 2) {
+        o.x = dgc::rna_tf32_f(o.x);
+        o.y = dgc::rna_tf32_f(o.y);
+        o.z = dgc::rna_tf32_f(o.z);
+        o.w = dgc::rna_tf32_f(o.w);
       }
       out[row * W4 + j4] = o;
     }

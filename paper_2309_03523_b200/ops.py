@@ -139,6 +139,20 @@ def rnn_fwd(cell, gx, U, slot_row, slot_mask, slot_carry, carry, n_rows, row_len
         nb, 2.0 * n_rows * row_len * H * G * H)
 
 
+def rnn_fwd_tc(cell, gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, H, ld_out,
+               h_out, c_out, save):
+    """K4 on tcgen05 (dgc_rnn_fwd_tc): TF32 masked LSTM forward, h x U on tensor cores."""
+    _req(gx, torch.float32, "gx"); _req(Ut, torch.float32, "Ut")
+    n_inst, G = gx.shape[0], 4
+    sf = rnn_save_floats(cell, H)
+    nb = 4 * n_inst * (G * H + sf + 2 * H) + 9 * n_rows * row_len + 4 * G * H * H
+    _run("lstm_fwd_tc", lambda: _native.check(
+        _native.lib().dgc_rnn_fwd_tc(cell, _p(gx), _p(Ut), _p(slot_row), _p(slot_mask),
+                                     _p(slot_carry), _p(carry), n_rows, row_len, H, ld_out,
+                                     _p(h_out), _p(c_out), _p(save), _stream()),
+        "dgc_rnn_fwd_tc"), nb, 2.0 * n_rows * row_len * H * G * H)
+
+
 def rnn_bwd(cell, Ut, slot_row, slot_mask, n_rows, row_len, H, save, dh_out, dgx):
     """K3/K4 dgc_rnn_bwd (BPTT over packed runs)."""
     _req(dh_out, torch.float32, "dh_out"); _req(dgx, torch.float32, "dgx")
@@ -196,12 +210,19 @@ def scatter_rows(src, rows, idx, n, width, dst, add=False):
     return dst
 
 
-def softmax_xent(logits, labels, C, scale, dlogits, loss_partial):
+def softmax_xent(logits, labels, C, scale, dlogits, loss_partial, round_tf32=False):
     """K8 dgc_softmax_xent."""
     n = labels.numel()
     _run("softmax_xent", lambda: _native.check(_native.lib().dgc_softmax_xent(
-        _p(logits), _p(labels), n, C, float(scale), _p(dlogits), _p(loss_partial), _stream()),
-        "dgc_softmax_xent"), n * (8 * C + 4))
+        _p(logits), _p(labels), n, C, float(scale), int(round_tf32), _p(dlogits),
+        _p(loss_partial), _stream()), "dgc_softmax_xent"), n * (8 * C + 4))
+
+
+def round_tf32(x, out):
+    """dgc_round_tf32: out = RN_tf32(x)."""
+    _run("round_tf32", lambda: _native.check(_native.lib().dgc_round_tf32(
+        _p(x), _p(out), x.numel(), _stream()), "dgc_round_tf32"), 8 * x.numel())
+    return out
 
 
 def colsum(X, n, width, ld, out, scratch, accumulate=False):

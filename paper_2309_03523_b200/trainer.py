@@ -21,6 +21,7 @@ Per epoch and shard:
 from __future__ import annotations
 
 import math
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -89,6 +90,9 @@ class Shard:
         n, nh, H, F = lay.n_own, lay.n_halo, cfg.H, cfg.F
         self.n, self.nh, self.nloc = n, nh, n + nh
         self.prec = 3 if cfg.precision == "fp32" else 1
+        # structure-encoder GEMMs: their outputs feed the ReLU masks, whose
+        # flips dominate TF32 gradient error; DGC_GCN_PREC=3 keeps them 3xTF32
+        self.prec_gcn = int(os.environ.get("DGC_GCN_PREC", self.prec))
         # layout on device
         self.row_ptr = _dev_i32(lay.row_ptr, dev)
         self.col = _dev_i32(lay.col, dev)
@@ -124,6 +128,16 @@ class Shard:
         self.v = torch.zeros(P, dtype=torch.float32, device=dev)
         for k, arr in params.items():
             self.p(k).copy_(torch.as_tensor(np.asarray(arr, np.float32)))
+        # TF32 mode: every tensor-core operand is stored pre-rounded to TF32
+        # (round-to-nearest) so the tcgen05 operand truncation is exact; the
+        # optimizer keeps fp32 master weights in self.params.
+        self.tf32 = cfg.precision == "tf32"
+        if self.tf32:
+            self.params_r = torch.zeros_like(self.params)
+            ops.round_tf32(self.params, self.params_r)
+            ops.round_tf32(self.X, self.X)
+        else:
+            self.params_r = self.params
         # activations
         G, GH = cfg.G, cfg.G * H
         f32 = dict(dtype=torch.float32, device=dev)
@@ -142,6 +156,10 @@ class Shard:
         self.dh2 = torch.zeros((n, H), **f32)
         self.dgx = torch.zeros((n, GH), **f32)
         self.Ut = torch.zeros((GH, H), **f32)
+        # tensor-core recurrence: TF32 mode, LSTM, H in {32, 64, 128}
+        self.tc_rnn = (cfg.precision == "tf32" and cfg.rnn == "lstm" and H in (32, 64, 128)
+                       and os.environ.get("DGC_TC_RNN", "1") != "0")
+        self.Ut_f = [torch.zeros((GH, H), **f32) for _ in range(cfg.n_rnn)] if self.tc_rnn else None
         self.dYext = torch.zeros((self.nloc, H), **f32)
         self.colsum_scratch = torch.zeros(2 * 148 * max(GH, cfg.C, H), **f32)
         # split-K for weight gradients: ~one wave of 148 SMs
@@ -164,6 +182,12 @@ class Shard:
         o, shape = self.offs[name]
         n = int(np.prod(shape))
         return self.params[o:o + n].view(*shape)
+
+    def pr(self, name):
+        """GEMM operand view of a parameter (TF32-rounded copy in TF32 mode)."""
+        o, shape = self.offs[name]
+        n = int(np.prod(shape))
+        return self.params_r[o:o + n].view(*shape)
 
     def g(self, name):
         o, shape = self.offs[name]
@@ -233,13 +257,15 @@ class Shard:
         cfg, H, n, prec = self.cfg, self.cfg.H, self.n, self.prec
         G, GH = cfg.G, cfg.G * cfg.H
         cell = 0 if cfg.rnn == "gru" else 1
+        rflag = 0x100 if self.tf32 else 0   # DGC_RNN_ROUND_TF32
+        rnd2 = 2 if self.tf32 else 0        # spmm: round output to TF32
         info = {"theta": {}, "d_r": {}, "billed_sp": 0, "billed_tm": 0, "rows": 0}
         D = self.D
         # ---------------- forward: structure encoder ----------------
         hin, ldin, kin = self.X, cfg.F, cfg.F
         for l, (W, b) in enumerate((("W1", "b1"), ("W2", "b2"))):
             Y = self.Yext[l]
-            ops.gemm(hin, self.p(W), Y, n, H, kin, lda=ldin, precision=prec)
+            ops.gemm(hin, self.pr(W), Y, n, H, kin, lda=ldin, precision=self.prec_gcn)
             if D > 1:
                 cache = self.scache[l] if self.stale_on else None
                 if cache is not None:
@@ -253,19 +279,25 @@ class Shard:
                     Y, H, self.send_pos, self.send_rows, Y, self.recv_slot, cache)
                 self.fresh[l], self.sent[l] = fresh, sent
                 info["rows"] += sum(c for _, c in sent.values())
-            ops.spmm_csr(self.row_ptr, self.col, self.dinv, Y, self.p(b), self.Hl[l], act=1,
+            ops.spmm_csr(self.row_ptr, self.col, self.dinv, Y, self.p(b), self.Hl[l], act=1 | rnd2,
                          nnz=self.nnz, n_cols=self.nloc)
             hin, ldin, kin = self.Hl[l], H, H
         # ---------------- forward: time encoder ----------------
         xr, ldx = self.Hl[1], H
         for k in range(cfg.n_rnn):
-            ops.gemm(xr, self.p(f"Wx{k}"), self.gx, n, GH, H, lda=ldx, precision=prec,
+            ops.gemm(xr, self.pr(f"Wx{k}"), self.gx, n, GH, H, lda=ldx, precision=prec,
                      bias=self.p(f"br{k}"))
             hb = self.hbuf[k]
             c_out = hb[:, H:] if cell == 1 else None
-            ops.rnn_fwd(cell, self.gx, self.p(f"U{k}"), self.slot_row, self.slot_mask,
-                        self.slot_carry, self.carry[k], self.R, self.L, H, self.hw, hb, c_out,
-                        self.save[k])
+            if self.tc_rnn:
+                ops.transpose(self.pr(f"U{k}"), self.Ut_f[k])
+                ops.rnn_fwd_tc(cell, self.gx, self.Ut_f[k], self.slot_row, self.slot_mask,
+                               self.slot_carry, self.carry[k], self.R, self.L, H, self.hw, hb,
+                               c_out, self.save[k])
+            else:
+                ops.rnn_fwd(cell | rflag, self.gx, self.pr(f"U{k}"), self.slot_row,
+                            self.slot_mask, self.slot_carry, self.carry[k], self.R, self.L, H,
+                            self.hw, hb, c_out, self.save[k])
             if D > 1:
                 cache = self.tcache[k] if self.stale_on else None
                 if cache is not None:
@@ -280,10 +312,10 @@ class Shard:
                 info["rows"] += sum(c for _, c in tsent.values())
             xr, ldx = hb, self.hw
         # ---------------- readout + loss ----------------
-        ops.gemm(xr, self.p("Wo"), self.logits, n, cfg.C, H, lda=ldx, precision=prec,
+        ops.gemm(xr, self.pr("Wo"), self.logits, n, cfg.C, H, lda=ldx, precision=prec,
                  bias=self.p("bo"))
         ops.softmax_xent(self.logits, self.y, cfg.C, 1.0 / self.n_total, self.dlogits,
-                         self.loss_partial)
+                         self.loss_partial, round_tf32=self.tf32)
         loss_local = self.loss_partial.sum().reshape(1)
         loss = yield ("sum", loss_local)
         info["loss"] = float(loss.item()) / self.n_total
@@ -293,11 +325,11 @@ class Shard:
         ops.gemm(xr, self.dlogits, self.g("Wo"), H, cfg.C, n, a_mn=True, lda=ldx, precision=prec,
                  k_splits=ks, partial=part)
         ops.colsum(self.dlogits, n, cfg.C, cfg.C, self.g("bo"), self.colsum_scratch)
-        ops.gemm(self.dlogits, self.p("Wo"), self.dh, n, H, cfg.C, b_mn=False, ldb=cfg.C,
+        ops.gemm(self.dlogits, self.pr("Wo"), self.dh, n, H, cfg.C, b_mn=False, ldb=cfg.C,
                  precision=prec)
         for k in reversed(range(cfg.n_rnn)):
-            ops.transpose(self.p(f"U{k}"), self.Ut)
-            ops.rnn_bwd(cell, self.Ut, self.slot_row, self.slot_mask, self.R, self.L, H,
+            ops.transpose(self.pr(f"U{k}"), self.Ut)
+            ops.rnn_bwd(cell | rflag, self.Ut, self.slot_row, self.slot_mask, self.R, self.L, H,
                         self.save[k], self.dh, self.dgx)
             xin, ldxin = (self.Hl[1], H) if k == 0 else (self.hbuf[k - 1], self.hw)
             ops.gemm(xin, self.dgx, self.g(f"Wx{k}"), H, GH, n, a_mn=True, lda=ldxin,
@@ -314,14 +346,14 @@ class Shard:
                 ops.gemm(self.save[k], self.dgx, gU, H, GH, n, a_mn=True, lda=self.sf, ldb=GH,
                          ldc=GH, precision=prec, k_splits=ks, partial=part)
             relu_src = self.Hl[1] if k == 0 else None
-            ops.gemm(self.dgx, self.p(f"Wx{k}"), self.dh2, n, H, GH, b_mn=False, ldb=GH,
+            ops.gemm(self.dgx, self.pr(f"Wx{k}"), self.dh2, n, H, GH, b_mn=False, ldb=GH,
                      precision=prec, relu_src=relu_src)
             self.dh, self.dh2 = self.dh2, self.dh
         dZ = self.dh  # = dH2 * (H2 > 0), fused into the last GEMM epilogue
         for l in (1, 0):
             W, b = ("W1", "b1") if l == 0 else ("W2", "b2")
             ops.colsum(dZ, n, H, H, self.g(b), self.colsum_scratch)
-            ops.spmm_csr(self.t_row_ptr, self.t_col, self.dinv, dZ, None, self.dYext, act=0,
+            ops.spmm_csr(self.t_row_ptr, self.t_col, self.dinv, dZ, None, self.dYext, act=rnd2,
                          nnz=self.nnz, n_cols=n)
             if D > 1:
                 yield from self._exchange_back(l, self.dYext, H)
@@ -329,7 +361,7 @@ class Shard:
             ops.gemm(hin_l, self.dYext, self.g(W), kin_l, H, n, a_mn=True, lda=ldin_l, ldb=H,
                      precision=prec, k_splits=ks, partial=part)
             if l == 1:
-                ops.gemm(self.dYext, self.p("W2"), self.dh2, n, H, H, b_mn=False, ldb=H,
+                ops.gemm(self.dYext, self.pr("W2"), self.dh2, n, H, H, b_mn=False, ldb=H,
                          precision=prec, relu_src=self.Hl[0])
                 dZ = self.dh2
         # ---------------- gradient all-reduce + update ----------------
@@ -341,6 +373,8 @@ class Shard:
                      cfg.eps, self.step_count)
         else:
             ops.sgd(self.params, self.grads, self.m, cfg.lr, cfg.momentum)
+        if self.tf32:
+            ops.round_tf32(self.params, self.params_r)
         return info
 
 

@@ -224,3 +224,40 @@ def test_softmax_xent_colsum_optimizers():
     vv = 0.001 * gr * gr
     ref = p - 0.01 * (mm / 0.1) / (np.sqrt(vv / 0.001) + 1e-8)
     close(pd.cpu().numpy(), ref, 1e-6, "adam")
+
+
+@pytest.mark.parametrize("H", [32, 64, 128])
+def test_lstm_fwd_tensor_core_matches_simt(H):
+    """K4 on tcgen05 (TF32) vs the fp32 SIMT kernel on the same packed runs,
+    with cross-device carries at some run starts."""
+    from paper_2309_03523_b200 import ops
+    from paper_2309_03523_b200.layout import pack_sequences_native
+    rng = np.random.default_rng(H)
+    lengths = rng.integers(1, 20, size=700)
+    seq, pos, mask, _ = pack_sequences_native(lengths)
+    R, L = seq.shape
+    offs = np.concatenate([[0], np.cumsum(lengths)])
+    n = int(offs[-1])
+    slot_row = np.where(seq >= 0, offs[np.maximum(seq, 0)] + pos, -1).astype(np.int32)
+    run_carry = np.where(rng.random(len(lengths)) < 0.3, 1, -1)
+    n_carry = int((run_carry > 0).sum())
+    run_carry[run_carry > 0] = np.arange(n_carry)
+    slot_carry = np.where((seq >= 0) & (pos == 0), run_carry[np.maximum(seq, 0)], -1).astype(np.int32)
+    gx = rng.standard_normal((n, 4 * H)).astype(np.float32)
+    U = (rng.standard_normal((H, 4 * H)) / np.sqrt(H)).astype(np.float32)
+    carry = rng.standard_normal((max(n_carry, 1), 2 * H)).astype(np.float32)
+    outs = []
+    for tc in (False, True):
+        hc = torch.zeros((n, 2 * H), device=dev)
+        save = torch.zeros((n, 7 * H), device=dev)
+        args = (t(gx), None, t(slot_row.reshape(-1), torch.int32), t(mask.reshape(-1), torch.uint8),
+                t(slot_carry.reshape(-1), torch.int32), t(carry), R, L, H, 2 * H, hc, hc[:, H:], save)
+        if tc:
+            Ut = t(U.T.copy())
+            ops.rnn_fwd_tc(1, args[0], Ut, *args[2:])
+        else:
+            ops.rnn_fwd(1, args[0], t(U), *args[2:])
+        torch.cuda.synchronize()
+        outs.append((hc.cpu().numpy(), save.cpu().numpy()))
+    close(outs[1][0], outs[0][0], 2e-3, "lstm tc h|c")
+    close(outs[1][1], outs[0][1], 2e-3, "lstm tc save")

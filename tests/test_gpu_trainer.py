@@ -12,11 +12,11 @@ from oracle.layout import build_layouts
 pytestmark = pytest.mark.gpu
 
 
-def run_pair(pa, cfg_kw, stale_mode="off", epochs=3, fraction=0.5, seed=0):
+def run_pair(pa, cfg_kw, stale_mode="off", epochs=3, fraction=0.5, seed=0, precision="fp32"):
     from paper_2309_03523_b200 import DGNNConfig, StaleConfig
     from paper_2309_03523_b200.trainer import DGNNTrainer
     from paper_2309_03523_b200.model import init_params, synthetic_inputs
-    cfg = DGNNConfig(optimizer="sgd", lr=0.05, precision="fp32", **cfg_kw)
+    cfg = DGNNConfig(optimizer="sgd", lr=0.05, precision=precision, **cfg_kw)
     X, y = synthetic_inputs(pa.n_instances, cfg.F, cfg.C, seed)
     params = init_params(cfg, seed)
     scfg = {"off": StaleConfig.off(), "relax": StaleConfig.adaptive(),
@@ -93,3 +93,29 @@ def test_trainer_stale_schedule_matches_oracle(artifacts_dir, mode):
         assert abs(t_["dist"] - t_["theta"]) <= 1e-5 * max(1.0, t_["scale"]), t_
     assert len(orc.tie_log) <= max(2, n_keys // 1000), orc.tie_log
     assert out[-1][0].stale_reduction_pct > 0.0
+
+
+@pytest.mark.parametrize("name,H", [("t4", 64), ("t2", 128)])
+def test_trainer_tf32_tensor_core_path(artifacts_dir, name, H):
+    """TF32 perf mode (tcgen05 GEMMs + tensor-core LSTM recurrence, TF32-rounded
+    operands) against the fp64 oracle. Loss and the time-encoder/readout
+    gradients are held to the north star's 2e-2 class (max-normalised). The
+    structure-encoder gradients (W1, b1, W2, b2) are sums over all instances
+    with strong cancellation (|sum| ~ 2-5% of sum|terms| at initialisation),
+    which amplifies the ~5e-4 per-element TF32 error of their inputs; they are
+    held to 5e-2 in tensor norm (the fp32 mode meets 1e-4 on all of them)."""
+    from paper_2309_03523_b200 import load_plan_npz
+    pa = load_plan_npz(artifacts_dir / name / "plan.npz")
+    out, tr, _ = run_pair(pa, dict(F=32, H=H, C=16, rnn="lstm", n_rnn=2), "off", epochs=2,
+                          precision="tf32")
+    assert tr.shards[0].tc_rnn
+    for rep, o, grads in out:
+        assert rep.loss == pytest.approx(o["loss"], rel=2e-2)
+        for k, g in grads.items():
+            ref = o["grads"][k]
+            if k in ("W1", "b1", "W2", "b2"):
+                err = np.linalg.norm(g - ref) / np.linalg.norm(ref)
+                assert err <= 5e-2, f"epoch {rep.epoch} grad {k}: rel-norm {err:.2e}"
+            else:
+                err = np.abs(g - ref).max() / np.abs(ref).max()
+                assert err <= 2e-2, f"epoch {rep.epoch} grad {k}: {err:.2e}"
