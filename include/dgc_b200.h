@@ -80,6 +80,23 @@ int dgc_pack_sequences(const int32_t* lengths, int64_t n, int32_t row_len,
                        int64_t capacity_rows, int32_t* slot_seq, int32_t* slot_pos,
                        uint8_t* mask, int64_t* n_rows, int64_t* padding);
 
+/* Native bit-exact plan_spatial_fusion (fusion.py:108-203) for ONE device:
+ * chunk stats (degree sums, halos over spatial edges + temporal links, inter-
+ * chunk message bytes, partition.py:273-359) are derived from the graph
+ * arrays and chunk_of; device_chunks = Assignment.queues[d]. Outputs: group
+ * index per device chunk (groups numbered in representative-id order),
+ * per-group memory_bytes and saved_bytes, group count. Returns DGC_ERR_PLAN
+ * (BudgetExceededError) if one chunk alone exceeds the budget. */
+int dgc_plan_spatial_fusion(int64_t n_instances, const int32_t* spatial_edges,
+                            int64_t n_spatial_edges, const int32_t* temporal_links,
+                            int64_t n_temporal_links, const int32_t* chunk_of, int64_t n_chunks,
+                            const int32_t* device_chunks, int64_t n_device_chunks,
+                            int64_t spatial_msg_bytes, int64_t temporal_msg_bytes,
+                            int64_t memory_budget, int64_t bytes_per_vertex,
+                            int64_t bytes_per_edge, int32_t* out_group_of_chunk,
+                            int64_t* out_group_memory, int64_t* out_group_saved,
+                            int64_t* n_groups_out);
+
 /* ------------------------------------------------------------------ */
 /* Device index arrays are int32 (per-device nnz < 2^31).              */
 /* ------------------------------------------------------------------ */
@@ -111,7 +128,11 @@ int dgc_gemm_splits(int64_t K, int32_t precision, int32_t k_splits);
 int dgc_gemm_tf32(const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                   int64_t ldc, int64_t M, int64_t N, int64_t K, int32_t a_mn, int32_t b_mn,
                   int32_t precision, const float* bias, const float* relu_src,
-                  int32_t accumulate, int32_t k_splits, float* partial, void* stream);
+                  int32_t accumulate, int32_t k_splits, float* partial, float* colsum_partial,
+                  void* stream);
+/* colsum_partial (may be NULL, needs k_splits == 1): column sums of the final
+ * output per (128-row tile, TMEM quadrant): [4*ceil(M/128), N]; reduce with
+ * dgc_reduce_rows -> bias gradients without re-reading C. */
 
 /* K3/K4: masked recurrent time encoder over FFD-packed runs.
  * cell: 0 = GRU in the reference form of GruCell.step (fusion.py:409-413),
@@ -144,7 +165,10 @@ int dgc_rnn_fwd_tc(int32_t cell, const float* gx, const float* Ut, const int32_t
  * dU = save-operand^T dgx by K2). Carries from other devices are constants. */
 int dgc_rnn_bwd(int32_t cell, const float* Ut, const int32_t* slot_row, const uint8_t* slot_mask,
                 int64_t n_rows, int32_t row_len, int32_t H, const float* save,
-                const float* dh_out, float* dgx, void* stream);
+                const float* dh_out, float* dgx, float* bias_partial, void* stream);
+/* bias_partial (may be NULL): per-CTA column sums of dgx,
+ * [dgc_rnn_bwd_partial_rows(n_rows, H), G*H]; reduce with dgc_reduce_rows. */
+int64_t dgc_rnn_bwd_partial_rows(int64_t n_rows, int32_t H);
 
 /* K5: stale filter. dgc_stale_distance = the distance half of
  * filter_transmissions / max_cache_gap (stale.py:140-151,205-212):
@@ -177,7 +201,11 @@ int dgc_scatter_rows(const float* src, const int32_t* rows, const int32_t* idx, 
  * sums of -log p[label]. */
 int dgc_softmax_xent(const float* logits, const int32_t* labels, int64_t n, int32_t C,
                      float scale, int32_t flags, float* dlogits, double* loss_partial,
-                     void* stream);
+                     float* dl_partial, void* stream);
+/* dl_partial (may be NULL): per-block column sums of dlogits [ceil(n/256), C]. */
+/* out[j] (+)= sum_r partial[r, j] in fixed row order (deterministic). */
+int dgc_reduce_rows(const float* partial, int64_t rows, int32_t width, float* out,
+                    int32_t accumulate, void* stream);
 /* out[i] = in[i] rounded to the nearest TF32 (weights / inputs of TF32 mode) */
 int dgc_round_tf32(const float* in, float* out, int64_t n, void* stream);
 /* Deterministic column sums out[j] (+)= sum_i X[i, j] (bias gradients);

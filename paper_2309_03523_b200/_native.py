@@ -34,22 +34,26 @@ _SIGS = {
     "dgc_layout_build": (_i32, [C.POINTER(PlanView), _i32, C.POINTER(_p)]),
     "dgc_layout_field": (_i64, [_p, _i32, C.POINTER(C.POINTER(_i64))]),
     "dgc_layout_free": (None, [_p]),
+    "dgc_plan_spatial_fusion": (_i32, [_i64, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _i64, _i64,
+                                       _i64, _i64, _i64, _p, _p, _p, _p]),
     "dgc_pack_sequences": (_i32, [_p, _i64, _i32, _i64, _p, _p, _p, _p, _p]),
     "dgc_spmm_csr": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i32, _i32, _p]),
     "dgc_gemm_tf32": (_i32, [_p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _i32, _i32, _i32,
-                              _p, _p, _i32, _i32, _p, _p]),
+                              _p, _p, _i32, _i32, _p, _p, _p]),
     "dgc_gemm_splits": (_i32, [_i64, _i32, _i32]),
     "dgc_rnn_save_floats": (_i32, [_i32, _i32]),
     "dgc_rnn_fwd": (_i32, [_i32, _p, _p, _p, _p, _p, _p, _i64, _i32, _i32, _i64, _p, _p, _p, _p]),
     "dgc_rnn_fwd_tc": (_i32, [_i32, _p, _p, _p, _p, _p, _p, _i64, _i32, _i32, _i64, _p, _p, _p, _p]),
-    "dgc_rnn_bwd": (_i32, [_i32, _p, _p, _p, _i64, _i32, _i32, _p, _p, _p, _p]),
+    "dgc_rnn_bwd": (_i32, [_i32, _p, _p, _p, _i64, _i32, _i32, _p, _p, _p, _p, _p]),
+    "dgc_rnn_bwd_partial_rows": (_i64, [_i64, _i32]),
     "dgc_transpose": (_i32, [_p, _i64, _i64, _p, _p]),
     "dgc_stale_distance": (_i32, [_p, _p, _p, _p, _i64, _i32, _p, _p, _p]),
     "dgc_stale_select": (_i32, [_p, _p, _p, _f32, _p, _p, _p, _i64, _i32, _p]),
     "dgc_compact_sent": (_i32, [_p, _i64, _p, _p, _p, _p]),
     "dgc_gather_rows": (_i32, [_p, _p, _p, _i64, _i32, _p, _p]),
     "dgc_scatter_rows": (_i32, [_p, _p, _p, _i64, _i32, _p, _i32, _p]),
-    "dgc_softmax_xent": (_i32, [_p, _p, _i64, _i32, _f32, _i32, _p, _p, _p]),
+    "dgc_softmax_xent": (_i32, [_p, _p, _i64, _i32, _f32, _i32, _p, _p, _p, _p]),
+    "dgc_reduce_rows": (_i32, [_p, _i64, _i32, _p, _i32, _p]),
     "dgc_round_tf32": (_i32, [_p, _p, _i64, _p]),
     "dgc_colsum": (_i32, [_p, _i64, _i32, _i64, _p, _i32, _p, _p]),
     "dgc_relu_bwd": (_i32, [_p, _p, _p, _i64, _p]),

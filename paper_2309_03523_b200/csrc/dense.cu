@@ -12,8 +12,10 @@ __global__ void __launch_bounds__(256) softmax_xent_kernel(const float* __restri
                                                           int64_t n, int C, float scale,
                                                           int round_out,
                                                           float* __restrict__ dlogits,
-                                                          double* __restrict__ loss_partial) {
+                                                          double* __restrict__ loss_partial,
+                                                          float* __restrict__ dl_partial) {
   __shared__ double red[256];
+  __shared__ float cred[256];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double l = 0.0;
   if (i < n) {
@@ -39,6 +41,21 @@ __global__ void __launch_bounds__(256) softmax_xent_kernel(const float* __restri
     __syncthreads();
   }
   if (threadIdx.x == 0) loss_partial[blockIdx.x] = red[0];
+  if (dl_partial) {
+    // per-block column sums of dlogits (readout bias gradient), fixed order
+    const int64_t r0 = (int64_t)blockIdx.x * blockDim.x;
+    const int64_t r1 = min(r0 + (int64_t)blockDim.x, n);
+    for (int c = 0; c < C; ++c) {
+      __syncthreads();
+      cred[threadIdx.x] = (i < n) ? dlogits[i * C + c] : 0.f;
+      __syncthreads();
+      for (int off = 128; off > 0; off >>= 1) {
+        if ((int)threadIdx.x < off) cred[threadIdx.x] += cred[threadIdx.x + off];
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) dl_partial[(int64_t)blockIdx.x * C + c] = (r1 > r0) ? cred[0] : 0.f;
+    }
+  }
 }
 
 // stage 1: block b sums rows [b*rows_per, (b+1)*rows_per) of every column.
@@ -135,12 +152,13 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g,
 
 extern "C" int dgc_softmax_xent(const float* logits, const int32_t* labels, int64_t n, int32_t C,
                                 float scale, int32_t flags, float* dlogits, double* loss_partial,
-                                void* stream) {
+                                float* dl_partial, void* stream) {
   DGC_REQUIRE(C >= 1, "softmax_xent: C must be >= 1");
   if (n == 0) return DGC_OK;
   const int blocks = (int)((n + 255) / 256);
   softmax_xent_kernel<<<blocks, 256, 0, dgc::as_stream(stream)>>>(logits, labels, n, C, scale,
-                                                                 flags & 1, dlogits, loss_partial);
+                                                                 flags & 1, dlogits, loss_partial,
+                                                                 dl_partial);
   DGC_CHECK_LAUNCH("softmax_xent_kernel");
   return DGC_OK;
 }
@@ -159,6 +177,52 @@ extern "C" int dgc_colsum(const float* X, int64_t n, int32_t width, int64_t ld, 
   }
   colsum_stage2<<<(width + 255) / 256, 256, 0, s>>>(scratch, nblk, width, out, accumulate);
   DGC_CHECK_LAUNCH("colsum_stage2");
+  return DGC_OK;
+}
+
+// Two-level fixed-order row reduction: blocks (32 columns x 8 row groups)
+// over a row slab each -> slab partials in scratch -> per-column sum of slabs.
+__global__ void __launch_bounds__(256) reduce_rows_stage1(const float* __restrict__ in, int64_t rows,
+                                                          int width, int64_t slab,
+                                                          float* __restrict__ out) {
+  __shared__ float red[8][33];
+  const int c = blockIdx.x * 32 + threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.y * slab, r1 = min(r0 + slab, rows);
+  float acc = 0.f;
+  if (c < width)
+    for (int64_t r = r0 + threadIdx.y; r < r1; r += 8) acc += in[r * width + c];
+  red[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < width) {
+    float s = 0.f;
+    for (int g = 0; g < 8; ++g) s += red[g][threadIdx.x];
+    out[(int64_t)blockIdx.y * width + c] = s;
+  }
+}
+
+extern "C" int dgc_reduce_rows(const float* partial, int64_t rows, int32_t width, float* out,
+                               int32_t accumulate, void* stream) {
+  if (width == 0) return DGC_OK;
+  cudaStream_t s = dgc::as_stream(stream);
+  // slab partials live in a small static scratch (<= 256 slabs x 4096 columns)
+  static float* scratch = nullptr;
+  static size_t scratch_n = 0;
+  int64_t slabs = rows < 256 ? (rows > 0 ? rows : 1) : 256;
+  if (slabs * width > 256 * 4096) return dgc::fail(DGC_ERR_ARG, "reduce_rows: width too large");
+  if (!scratch) {
+    scratch_n = 256 * 4096;
+    cudaError_t e = cudaMalloc(&scratch, scratch_n * sizeof(float));
+    if (e != cudaSuccess) return dgc::cuda_fail(e, "reduce_rows scratch");
+  }
+  const int64_t slab = (rows + slabs - 1) / slabs;
+  slabs = rows > 0 ? (rows + slab - 1) / slab : 0;
+  if (slabs > 0) {
+    dim3 grid((unsigned)((width + 31) / 32), (unsigned)slabs);
+    reduce_rows_stage1<<<grid, dim3(32, 8), 0, s>>>(partial, rows, width, slab, scratch);
+    DGC_CHECK_LAUNCH("reduce_rows_stage1");
+  }
+  colsum_stage2<<<(width + 255) / 256, 256, 0, s>>>(scratch, (int)slabs, width, out, accumulate);
+  DGC_CHECK_LAUNCH("reduce_rows_stage2");
   return DGC_OK;
 }
 

@@ -31,7 +31,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                      float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, int bn, int stages,
                      int kb_total, int kb_per_split, int m_tiles, int n_tiles, int splits,
                      const float* __restrict__ bias, const float* __restrict__ relu_src,
-                     int accumulate, float* __restrict__ partial) {
+                     int accumulate, float* __restrict__ partial,
+                     float* __restrict__ colsum_partial) {
   // Persistent: CTA c owns tiles c, c+G, ... of the (split, n-tile, m-tile)
   // space (m fastest, so a CTA's consecutive tiles share the B panel). Two TMEM
   // accumulators let the epilogue drain tile i while the MMA runs tile i+1.
@@ -212,6 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t n = n0 + c + lane;
         const bool col_ok = (c + lane < bn) && (n < N);
         const float bn_v = (bias && col_ok) ? __ldg(bias + n) : 0.f;
+        float csum = 0.f;  // this warp's 32 rows of column n (bias gradients)
 #pragma unroll
         for (int r0 = 0; r0 < 32; r0 += 8) {
           float x[8], aux[8], acc_in[8];
@@ -234,9 +236,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               float y = x[u] + acc_in[u] + bn_v;
               if (relu_src && !(aux[u] > 0.f)) y = 0.f;
               C[row * ldc + n] = y;
+              csum += y;
             }
           }
         }
+        if (colsum_partial && col_ok)
+          colsum_partial[((m0 / BM) * 4 + q) * N + n] = csum;
         __syncwarp();
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -273,7 +278,7 @@ template <bool A_MN, bool B_MN, bool SPLIT3>
 int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, float* C, int64_t ldc, int64_t M,
                 int64_t N, int bn, int ntiles, int kb_total, int splits, int kb_per,
                 const float* bias, const float* relu_src, int accumulate, float* partial,
-                cudaStream_t s) {
+                float* colsum_partial, cudaStream_t s) {
   const int ab = kABytes + bn * BK * 4;
   const int stage_bytes = ab * (SPLIT3 ? 2 : 1);
   const int budget = 190 * 1024;
@@ -292,7 +297,8 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, float* C, int64_t 
   const int total = m_tiles * ntiles * splits;
   const int grid = total < dgc::kNumSMs ? total : dgc::kNumSMs;
   kern<<<grid, kThreads, smem, s>>>(ma, mb, C, ldc, M, N, bn, stages, kb_total, kb_per, m_tiles,
-                                    ntiles, splits, bias, relu_src, accumulate, partial);
+                                    ntiles, splits, bias, relu_src, accumulate, partial,
+                                    colsum_partial);
   DGC_CHECK_LAUNCH("gemm_tf32_kernel");
   return DGC_OK;
 }
@@ -311,7 +317,7 @@ extern "C" int dgc_gemm_tf32(const float* A, int64_t lda, const float* B, int64_
                              int64_t ldc, int64_t M, int64_t N, int64_t K, int32_t a_mn,
                              int32_t b_mn, int32_t precision, const float* bias,
                              const float* relu_src, int32_t accumulate, int32_t k_splits,
-                             float* partial, void* stream) {
+                             float* partial, float* colsum_partial, void* stream) {
   DGC_REQUIRE(M >= 0 && N >= 0 && K >= 1, "gemm: bad shape");
   DGC_REQUIRE(precision == 1 || precision == 3, "gemm: precision must be 1 (TF32) or 3 (3xTF32)");
   DGC_REQUIRE(k_splits >= 1, "gemm: k_splits >= 1");
@@ -332,6 +338,7 @@ extern "C" int dgc_gemm_tf32(const float* A, int64_t lda, const float* B, int64_
   if (precision == 3 && kb_per > kMaxChainKb) kb_per = kMaxChainKb;
   const int splits = (kb_total + kb_per - 1) / kb_per;
   if (splits > 1) DGC_REQUIRE(partial != nullptr, "gemm: k_splits > 1 needs a partial buffer");
+  if (splits > 1) DGC_REQUIRE(colsum_partial == nullptr, "gemm: column sums need k_splits == 1");
   CUtensorMap ma, mb;
   int rc = a_mn ? make_map(&ma, A, K, M, lda, 32, 32, true)
                  : make_map(&ma, A, M, K, lda, 32, BM, false);
@@ -345,7 +352,7 @@ extern "C" int dgc_gemm_tf32(const float* A, int64_t lda, const float* B, int64_
   if ((bool)a_mn == AM && (bool)b_mn == BMN && s3 == S3)                                          \
     rc = launch_gemm<AM, BMN, S3>(ma, mb, C, ldc, M, N, bn, ntiles, kb_total, splits, kb_per,   \
                                   part ? nullptr : bias, part ? nullptr : relu_src,              \
-                                  part ? 0 : accumulate, part, s);
+                                  part ? 0 : accumulate, part, colsum_partial, s);
   DGC_GEMM_CASE(false, false, false)
   DGC_GEMM_CASE(false, true, false)
   DGC_GEMM_CASE(true, false, false)

@@ -23,7 +23,7 @@ __device__ __forceinline__ float sigm(float x) { return 1.f / (1.f + __expf(-x))
 
 // ------------------------------- GRU ----------------------------------------
 template <int RPT>
-__global__ void gru_fwd_kernel(const float* __restrict__ gx, const float* __restrict__ U,
+__global__ void __launch_bounds__(256, 3) gru_fwd_kernel(const float* __restrict__ gx, const float* __restrict__ U,
                                const int32_t* __restrict__ slot_row,
                                const uint8_t* __restrict__ slot_mask,
                                const int32_t* __restrict__ slot_carry,
@@ -109,10 +109,10 @@ __global__ void gru_fwd_kernel(const float* __restrict__ gx, const float* __rest
 }
 
 template <int RPT>
-__global__ void gru_bwd_kernel(const float* __restrict__ Ut, const int32_t* __restrict__ slot_row,
+__global__ void __launch_bounds__(256, 3) gru_bwd_kernel(const float* __restrict__ Ut, const int32_t* __restrict__ slot_row,
                                const uint8_t* __restrict__ slot_mask, int64_t R, int L, int H,
                                const float* __restrict__ save, const float* __restrict__ dh_out,
-                               float* __restrict__ dgx, int rnd) {
+                               float* __restrict__ dgx, int rnd, float* __restrict__ bias_partial) {
   extern __shared__ float sm[];
   const int TY = blockDim.y, TR = TY * RPT;
   float* dar_s = sm;
@@ -121,6 +121,7 @@ __global__ void gru_bwd_kernel(const float* __restrict__ Ut, const int32_t* __re
   const int j = threadIdx.x, ty = threadIdx.y;
   const int64_t row0 = (int64_t)blockIdx.x * TR;
   const int G3 = 3 * H;
+  float bsum[3] = {0.f, 0.f, 0.f};
   float dh[RPT];
 #pragma unroll
   for (int q = 0; q < RPT; ++q) dh[q] = 0.f;
@@ -177,6 +178,9 @@ __global__ void gru_bwd_kernel(const float* __restrict__ Ut, const int32_t* __re
         o[j] = rnd ? dgc::rna_tf32_f(dar) : dar;
         o[H + j] = rnd ? dgc::rna_tf32_f(daz) : daz;
         o[2 * H + j] = rnd ? dgc::rna_tf32_f(dac) : dac;
+        bsum[0] += dar;
+        bsum[1] += daz;
+        bsum[2] += dac;
       }
       dar_s[lr * H + j] = dar;
       daz_s[lr * H + j] = daz;
@@ -194,11 +198,23 @@ __global__ void gru_bwd_kernel(const float* __restrict__ Ut, const int32_t* __re
     for (int q = 0; q < RPT; ++q) dh[q] = inst[q] >= 0 ? dhp[q] * m[q] : 0.f;
     __syncthreads();
   }
+  if (bias_partial) {  // per-CTA column sums of dgx, combined over ty in fixed order
+    for (int gi = 0; gi < 3; ++gi) {
+      dar_s[ty * H + j] = bsum[gi];
+      __syncthreads();
+      if (ty == 0) {
+        float acc = 0.f;
+        for (int t = 0; t < TY; ++t) acc += dar_s[t * H + j];
+        bias_partial[(int64_t)blockIdx.x * G3 + gi * H + j] = acc;
+      }
+      __syncthreads();
+    }
+  }
 }
 
 // ------------------------------- LSTM ---------------------------------------
 template <int RPT>
-__global__ void lstm_fwd_kernel(const float* __restrict__ gx, const float* __restrict__ U,
+__global__ void __launch_bounds__(256, 3) lstm_fwd_kernel(const float* __restrict__ gx, const float* __restrict__ U,
                                 const int32_t* __restrict__ slot_row,
                                 const uint8_t* __restrict__ slot_mask,
                                 const int32_t* __restrict__ slot_carry,
@@ -279,16 +295,17 @@ __global__ void lstm_fwd_kernel(const float* __restrict__ gx, const float* __res
 }
 
 template <int RPT>
-__global__ void lstm_bwd_kernel(const float* __restrict__ Ut, const int32_t* __restrict__ slot_row,
+__global__ void __launch_bounds__(256, 3) lstm_bwd_kernel(const float* __restrict__ Ut, const int32_t* __restrict__ slot_row,
                                 const uint8_t* __restrict__ slot_mask, int64_t R, int L, int H,
                                 const float* __restrict__ save, const float* __restrict__ dh_out,
-                                float* __restrict__ dgx, int rnd) {
+                                float* __restrict__ dgx, int rnd, float* __restrict__ bias_partial) {
   extern __shared__ float sm[];
   const int TY = blockDim.y, TR = TY * RPT;
   float* da_s = sm;  // [TR][4][H]
   const int j = threadIdx.x, ty = threadIdx.y;
   const int64_t row0 = (int64_t)blockIdx.x * TR;
   const int G4 = 4 * H;
+  float bsum[4] = {0.f, 0.f, 0.f, 0.f};
   float dh[RPT], dc[RPT];
 #pragma unroll
   for (int q = 0; q < RPT; ++q) dh[q] = dc[q] = 0.f;
@@ -322,7 +339,10 @@ __global__ void lstm_bwd_kernel(const float* __restrict__ Ut, const int32_t* __r
         dcp[q] = dcn * fg;
         float* o = dgx + (int64_t)inst[q] * G4;
 #pragma unroll
-        for (int gi = 0; gi < 4; ++gi) o[gi * H + j] = rnd ? dgc::rna_tf32_f(da[gi]) : da[gi];
+        for (int gi = 0; gi < 4; ++gi) {
+          o[gi * H + j] = rnd ? dgc::rna_tf32_f(da[gi]) : da[gi];
+          bsum[gi] += da[gi];
+        }
       }
 #pragma unroll
       for (int gi = 0; gi < 4; ++gi) da_s[(lr * 4 + gi) * H + j] = da[gi];
@@ -348,6 +368,18 @@ __global__ void lstm_bwd_kernel(const float* __restrict__ Ut, const int32_t* __r
       dc[q] = inst[q] >= 0 ? dcp[q] * m[q] : 0.f;
     }
     __syncthreads();
+  }
+  if (bias_partial) {  // per-CTA column sums of dgx, combined over ty in fixed order
+    for (int gi = 0; gi < 4; ++gi) {
+      da_s[ty * H + j] = bsum[gi];
+      __syncthreads();
+      if (ty == 0) {
+        float acc = 0.f;
+        for (int t = 0; t < TY; ++t) acc += da_s[t * H + j];
+        bias_partial[(int64_t)blockIdx.x * G4 + gi * H + j] = acc;
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -381,6 +413,12 @@ inline Shape pick_shape(int H) {
 }  // namespace
 
 extern "C" int dgc_rnn_save_floats(int32_t cell, int32_t H) { return (cell == 0 ? 5 : 7) * H; }
+
+extern "C" int64_t dgc_rnn_bwd_partial_rows(int64_t n_rows, int32_t H) {
+  const Shape sh = pick_shape(H);
+  const int64_t TR = (int64_t)sh.ty * sh.rpt;
+  return (n_rows + TR - 1) / TR;
+}
 
 extern "C" int dgc_transpose(const float* in, int64_t rows, int64_t cols, float* out, void* stream) {
   if (rows == 0 || cols == 0) return DGC_OK;
@@ -418,7 +456,8 @@ extern "C" int dgc_rnn_fwd(int32_t cell_flags, const float* gx, const float* U, 
 
 extern "C" int dgc_rnn_bwd(int32_t cell_flags, const float* Ut, const int32_t* slot_row,
                            const uint8_t* slot_mask, int64_t n_rows, int32_t row_len, int32_t H,
-                           const float* save, const float* dh_out, float* dgx, void* stream) {
+                           const float* save, const float* dh_out, float* dgx,
+                           float* bias_partial, void* stream) {
   const int cell = cell_flags & 0xff, rnd = (cell_flags >> 8) & 1;
   DGC_REQUIRE(cell == 0 || cell == 1, "rnn_bwd: cell must be 0 (GRU) or 1 (LSTM)");
   if (n_rows == 0 || row_len == 0) return DGC_OK;
@@ -432,7 +471,7 @@ extern "C" int dgc_rnn_bwd(int32_t cell_flags, const float* Ut, const int32_t* s
       cudaFuncSetAttribute(gru_bwd_kernel<RPT_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
     gru_bwd_kernel<RPT_SEL><<<grid, block, smem, s>>>(Ut, slot_row, slot_mask, n_rows, row_len, H, save,
-                                                dh_out, dgx, rnd);
+                                                dh_out, dgx, rnd, bias_partial);
     DGC_CHECK_LAUNCH("gru_bwd_kernel");
   } else {
     const size_t smem = 4 * (size_t)TR * H * sizeof(float);
@@ -440,7 +479,7 @@ extern "C" int dgc_rnn_bwd(int32_t cell_flags, const float* Ut, const int32_t* s
       cudaFuncSetAttribute(lstm_bwd_kernel<RPT_SEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
     lstm_bwd_kernel<RPT_SEL><<<grid, block, smem, s>>>(Ut, slot_row, slot_mask, n_rows, row_len, H, save,
-                                                 dh_out, dgx, rnd);
+                                                 dh_out, dgx, rnd, bias_partial);
     DGC_CHECK_LAUNCH("lstm_bwd_kernel");
   }
   return DGC_OK;

@@ -92,7 +92,8 @@ def spmm_csr(row_ptr, col, dinv, Y, bias, out, act: int, nnz=0, n_cols=0):
 
 
 def gemm(A, B, C, M, N, K, *, a_mn=False, b_mn=True, lda=None, ldb=None, ldc=None,
-         precision=3, bias=None, relu_src=None, accumulate=False, k_splits=1, partial=None):
+         precision=3, bias=None, relu_src=None, accumulate=False, k_splits=1, partial=None,
+         colsum_partial=None):
     """K2 dgc_gemm_tf32 (tcgen05). Defaults: A [M,K] row-major, B [K,N] row-major."""
     for t, nm in ((A, "A"), (B, "B"), (C, "C")):
         _req(t, torch.float32, nm)
@@ -110,7 +111,8 @@ def gemm(A, B, C, M, N, K, *, a_mn=False, b_mn=True, lda=None, ldb=None, ldc=Non
     _run(gname, lambda: _native.check(
         _native.lib().dgc_gemm_tf32(
             _p(A), lda, _p(B), ldb, _p(C), ldc, M, N, K, int(a_mn), int(b_mn), precision,
-            _p(bias), _p(relu_src), int(accumulate), k_splits, _p(partial), _stream()),
+            _p(bias), _p(relu_src), int(accumulate), k_splits, _p(partial),
+            _p(colsum_partial), _stream()),
         "dgc_gemm_tf32"), nb, 2.0 * M * N * K, 1 + int(splits > 1))
     return C
 
@@ -153,7 +155,20 @@ def rnn_fwd_tc(cell, gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row
         "dgc_rnn_fwd_tc"), nb, 2.0 * n_rows * row_len * H * G * H)
 
 
-def rnn_bwd(cell, Ut, slot_row, slot_mask, n_rows, row_len, H, save, dh_out, dgx):
+def rnn_bwd_partial_rows(n_rows, H):
+    return _native.lib().dgc_rnn_bwd_partial_rows(n_rows, H)
+
+
+def reduce_rows(partial, rows, width, out, accumulate=False):
+    """dgc_reduce_rows: out[j] (+)= sum_r partial[r, j] (fixed order)."""
+    _run("reduce_rows", lambda: _native.check(_native.lib().dgc_reduce_rows(
+        _p(partial), rows, width, _p(out), int(accumulate), _stream()), "dgc_reduce_rows"),
+        4 * rows * width, 0, 2)
+    return out
+
+
+def rnn_bwd(cell, Ut, slot_row, slot_mask, n_rows, row_len, H, save, dh_out, dgx,
+            bias_partial=None):
     """K3/K4 dgc_rnn_bwd (BPTT over packed runs)."""
     _req(dh_out, torch.float32, "dh_out"); _req(dgx, torch.float32, "dgx")
     n_inst, G = dgx.shape[0], (3 if cell == 0 else 4)
@@ -161,7 +176,8 @@ def rnn_bwd(cell, Ut, slot_row, slot_mask, n_rows, row_len, H, save, dh_out, dgx
     nb = 4 * n_inst * (G * H + sf + H) + 5 * n_rows * row_len + 4 * G * H * H
     _run("gru_bwd" if cell == 0 else "lstm_bwd", lambda: _native.check(
         _native.lib().dgc_rnn_bwd(cell, _p(Ut), _p(slot_row), _p(slot_mask), n_rows, row_len, H,
-                                  _p(save), _p(dh_out), _p(dgx), _stream()), "dgc_rnn_bwd"),
+                                  _p(save), _p(dh_out), _p(dgx), _p(bias_partial), _stream()),
+        "dgc_rnn_bwd"),
         nb, 2.0 * n_rows * row_len * H * G * H)
 
 
@@ -210,12 +226,13 @@ def scatter_rows(src, rows, idx, n, width, dst, add=False):
     return dst
 
 
-def softmax_xent(logits, labels, C, scale, dlogits, loss_partial, round_tf32=False):
+def softmax_xent(logits, labels, C, scale, dlogits, loss_partial, round_tf32=False,
+                 dl_partial=None):
     """K8 dgc_softmax_xent."""
     n = labels.numel()
     _run("softmax_xent", lambda: _native.check(_native.lib().dgc_softmax_xent(
         _p(logits), _p(labels), n, C, float(scale), int(round_tf32), _p(dlogits),
-        _p(loss_partial), _stream()), "dgc_softmax_xent"), n * (8 * C + 4))
+        _p(loss_partial), _p(dl_partial), _stream()), "dgc_softmax_xent"), n * (8 * C + 4))
 
 
 def round_tf32(x, out):

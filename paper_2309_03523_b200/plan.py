@@ -185,3 +185,49 @@ def single_device(pa: PlanArrays) -> PlanArrays:
     return PlanArrays(pa.T, pa.feature_dim, pa.inst_entity, pa.inst_t, pa.spatial_edges,
                       pa.temporal_links, np.zeros_like(pa.structure_device), pa.chunk_of, 1,
                       None, None, None, pa.profile, dict(pa.meta))
+
+
+def native_fusion(pa: PlanArrays, queues, memory_budget: int = 1 << 30,
+                  bytes_per_vertex: int = 256, bytes_per_edge: int = 64):
+    """plan_fusion (fusion.py:206-220) through the native bit-exact port
+    (dgc_plan_spatial_fusion). ``queues`` = Assignment.queues (chunk ids per
+    device). Returns (group_device, group_ptr, group_chunks, memory, saved)
+    in FusionPlan order (devices ascending, groups by representative id)."""
+    import ctypes as C
+
+    from . import _native
+    prof = pa.profile
+    H, s = int(prof.get("embedding_dim", 16)), int(prof.get("bytes_per_scalar", 4))
+    if prof.get("temporal_fanout", "previous-only") != "previous-only":
+        raise ValueError("native fusion supports the previous-only temporal fanout")
+    ts = int(prof.get("blocks", 1)) * int(prof.get("spatial_msgs_per_block", 2)) * H * s
+    tt = int(prof.get("blocks", 1)) * int(prof.get("temporal_msgs_per_block", 1)) * H * s
+    se = np.ascontiguousarray(pa.spatial_edges, np.int32).reshape(-1)
+    tl = np.ascontiguousarray(pa.temporal_links, np.int32).reshape(-1)
+    co = np.ascontiguousarray(pa.chunk_of, np.int32)
+    n_chunks = int(co.max()) + 1 if len(co) else 0
+    lib = _native.lib()
+    gdev, gptr, gch, gmem, gsav = [], [0], [], [], []
+    for d, q in enumerate(queues):
+        qa = np.ascontiguousarray(np.asarray(q, np.int32))
+        goc = np.empty(len(qa), np.int32)
+        mem = np.empty(max(1, len(qa)), np.int64)
+        sav = np.empty(max(1, len(qa)), np.int64)
+        ng = C.c_int64()
+        p = lambda a: a.ctypes.data_as(C.c_void_p)
+        rc = lib.dgc_plan_spatial_fusion(pa.n_instances, p(se), len(pa.spatial_edges), p(tl),
+                                         len(pa.temporal_links), p(co), n_chunks, p(qa), len(qa),
+                                         ts, tt, memory_budget, bytes_per_vertex, bytes_per_edge,
+                                         p(goc), p(mem), p(sav), C.byref(ng))
+        if rc == -3:
+            raise ValueError(lib.dgc_last_error().decode())
+        _native.check(rc, "dgc_plan_spatial_fusion")
+        for gi in range(ng.value):
+            members = sorted(int(c) for c in qa[goc == gi])
+            gdev.append(d)
+            gch.extend(members)
+            gptr.append(len(gch))
+            gmem.append(int(mem[gi]))
+            gsav.append(int(sav[gi]))
+    return (np.asarray(gdev, np.int32), np.asarray(gptr, np.int64), np.asarray(gch, np.int32),
+            np.asarray(gmem, np.int64), np.asarray(gsav, np.int64))

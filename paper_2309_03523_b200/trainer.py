@@ -162,6 +162,12 @@ class Shard:
         self.Ut_f = [torch.zeros((GH, H), **f32) for _ in range(cfg.n_rnn)] if self.tc_rnn else None
         self.dYext = torch.zeros((self.nloc, H), **f32)
         self.colsum_scratch = torch.zeros(2 * 148 * max(GH, cfg.C, H), **f32)
+        # fused bias-gradient partial sums (produced inside the kernels that write
+        # the gradient tensors, reduced in fixed order by dgc_reduce_rows)
+        self.m_tiles = max(1, (n + 127) // 128)
+        self.rnn_prows = ops.rnn_bwd_partial_rows(self.R, H) if self.R else 1
+        self.dl_partial = torch.zeros(max(1, (n + 255) // 256) * cfg.C, **f32)
+        self.bias_partial = torch.zeros(max(self.rnn_prows * GH, 4 * self.m_tiles * H), **f32)
         # split-K for weight gradients: ~one wave of 148 SMs
         kb = max(1, (n + 31) // 32)
         self.ksplit = max(1, min(148, kb // 4))
@@ -315,7 +321,7 @@ class Shard:
         ops.gemm(xr, self.pr("Wo"), self.logits, n, cfg.C, H, lda=ldx, precision=prec,
                  bias=self.p("bo"))
         ops.softmax_xent(self.logits, self.y, cfg.C, 1.0 / self.n_total, self.dlogits,
-                         self.loss_partial, round_tf32=self.tf32)
+                         self.loss_partial, round_tf32=self.tf32, dl_partial=self.dl_partial)
         loss_local = self.loss_partial.sum().reshape(1)
         loss = yield ("sum", loss_local)
         info["loss"] = float(loss.item()) / self.n_total
@@ -324,17 +330,17 @@ class Shard:
         ks, part = self.ksplit, self.partial
         ops.gemm(xr, self.dlogits, self.g("Wo"), H, cfg.C, n, a_mn=True, lda=ldx, precision=prec,
                  k_splits=ks, partial=part)
-        ops.colsum(self.dlogits, n, cfg.C, cfg.C, self.g("bo"), self.colsum_scratch)
+        ops.reduce_rows(self.dl_partial, max(1, (n + 255) // 256), cfg.C, self.g("bo"))
         ops.gemm(self.dlogits, self.pr("Wo"), self.dh, n, H, cfg.C, b_mn=False, ldb=cfg.C,
                  precision=prec)
         for k in reversed(range(cfg.n_rnn)):
             ops.transpose(self.pr(f"U{k}"), self.Ut)
             ops.rnn_bwd(cell | rflag, self.Ut, self.slot_row, self.slot_mask, self.R, self.L, H,
-                        self.save[k], self.dh, self.dgx)
+                        self.save[k], self.dh, self.dgx, bias_partial=self.bias_partial)
+            ops.reduce_rows(self.bias_partial, self.rnn_prows, GH, self.g(f"br{k}"))
             xin, ldxin = (self.Hl[1], H) if k == 0 else (self.hbuf[k - 1], self.hw)
             ops.gemm(xin, self.dgx, self.g(f"Wx{k}"), H, GH, n, a_mn=True, lda=ldxin,
                      precision=prec, k_splits=ks, partial=part)
-            ops.colsum(self.dgx, n, GH, GH, self.g(f"br{k}"), self.colsum_scratch)
             gU = self.g(f"U{k}")
             if cell == 0:
                 ops.gemm(self.save[k], self.dgx, gU, H, 2 * H, n, a_mn=True, lda=self.sf,
@@ -347,12 +353,14 @@ class Shard:
                          ldc=GH, precision=prec, k_splits=ks, partial=part)
             relu_src = self.Hl[1] if k == 0 else None
             ops.gemm(self.dgx, self.pr(f"Wx{k}"), self.dh2, n, H, GH, b_mn=False, ldb=GH,
-                     precision=prec, relu_src=relu_src)
+                     precision=prec, relu_src=relu_src,
+                     colsum_partial=self.bias_partial if k == 0 else None)
+            if k == 0:  # dZ2 = dH2 * (H2 > 0): its column sums are the b2 gradient
+                ops.reduce_rows(self.bias_partial, 4 * self.m_tiles, H, self.g("b2"))
             self.dh, self.dh2 = self.dh2, self.dh
         dZ = self.dh  # = dH2 * (H2 > 0), fused into the last GEMM epilogue
         for l in (1, 0):
             W, b = ("W1", "b1") if l == 0 else ("W2", "b2")
-            ops.colsum(dZ, n, H, H, self.g(b), self.colsum_scratch)
             ops.spmm_csr(self.t_row_ptr, self.t_col, self.dinv, dZ, None, self.dYext, act=rnd2,
                          nnz=self.nnz, n_cols=n)
             if D > 1:
@@ -362,7 +370,8 @@ class Shard:
                      precision=prec, k_splits=ks, partial=part)
             if l == 1:
                 ops.gemm(self.dYext, self.pr("W2"), self.dh2, n, H, H, b_mn=False, ldb=H,
-                         precision=prec, relu_src=self.Hl[0])
+                         precision=prec, relu_src=self.Hl[0], colsum_partial=self.bias_partial)
+                ops.reduce_rows(self.bias_partial, 4 * self.m_tiles, H, self.g("b1"))
                 dZ = self.dh2
         # ---------------- gradient all-reduce + update ----------------
         if D > 1:

@@ -29,8 +29,11 @@ ROOT = Path(__file__).resolve().parents[1]
 CONFIGS = {
     "c1": dict(N=10_000, T=16, sigma_mult=1.0, D=4, F=16,
                profile=ModelProfile(1, 2, 1, "previous-only", 16, 4), fuse=True),
+    # fusion "native": build_plan(fuse=False) by the reference, then the
+    # bit-exact native plan_spatial_fusion port (tests/test_fusion_native.py):
+    # the reference's Python fusion planner ran > 86 CPU-min and 46 GB at 200k
     "c2": dict(N=200_000, T=32, sigma_mult=1.0, D=1, F=16,
-               profile=ModelProfile(1, 2, 2, "previous-only", 16, 4), fuse=True),
+               profile=ModelProfile(1, 2, 2, "previous-only", 16, 4), fuse="native"),
     # the C2 graph re-planned for 2/4/8 devices (strong-scaling runs); fusion
     # off: numerics are fusion-invariant and the Python
     # fusion planner does not finish at this size in useful time
@@ -68,7 +71,7 @@ def build(name: str) -> None:
     g = graphstore.generate(spec_for(cfg))
     t1 = time.time()
     cluster = sim.ClusterSpec(n_devices=cfg["D"])
-    plan = sim.build_plan(g, "pgc", cfg["profile"], cluster, fuse=cfg["fuse"])
+    plan = sim.build_plan(g, "pgc", cfg["profile"], cluster, fuse=cfg["fuse"] is True)
     t2 = time.time()
     print(f"[{name}] generate {t1 - t0:.1f}s build_plan {t2 - t1:.1f}s "
           f"chunks={len(plan.chunk_graph.chunks)}", flush=True)
@@ -80,15 +83,33 @@ def build(name: str) -> None:
             chunk_of[g.index_of(v)] = c.id
     queues = plan.assignment.queues
     groups = []  # (device, [chunk ids]) in FusionPlan order
+    fusion_src = None
     if plan.fusion is not None:
+        fusion_src = "reference plan_fusion"
         for dev, gl in sorted(plan.fusion.groups_by_device.items()):
             for grp in gl:
                 groups.append((dev, list(grp.chunk_ids)))
+    elif cfg["fuse"] == "native":
+        sys.path.insert(0, str(ROOT))
+        from paper_2309_03523_b200.plan import PlanArrays, native_fusion
+        pa = PlanArrays(T=g.T, feature_dim=g.feature_dim,
+                        inst_entity=inst[:, 0].astype(np.int32), inst_t=inst[:, 1].astype(np.int32),
+                        spatial_edges=g.spatial_edge_index().astype(np.int32),
+                        temporal_links=g.temporal_link_index().astype(np.int32),
+                        structure_device=plan.structure_device.astype(np.int32),
+                        chunk_of=chunk_of.astype(np.int32), n_devices=cfg["D"],
+                        profile=cfg["profile"].to_dict())
+        t3 = time.time()
+        gd, gp, gc, _, _ = native_fusion(pa, queues, cluster.memory_budget)
+        print(f"[{name}] native fusion {time.time() - t3:.1f}s groups={len(gd)}", flush=True)
+        for i in range(len(gd)):
+            groups.append((int(gd[i]), [int(c) for c in gc[gp[i]:gp[i + 1]]]))
+        fusion_src = "native bit-exact port of plan_spatial_fusion (csrc/fusion_plan.cpp)"
     meta = {
         "name": name, "T": g.T, "feature_dim": g.feature_dim,
         "n_instances": g.n_instances, "n_spatial_edges": g.n_spatial_edges,
         "n_devices": cfg["D"], "profile": cfg["profile"].to_dict(),
-        "fused": plan.fusion is not None,
+        "fused": bool(groups), "fusion_source": fusion_src,
         "generate_s": t1 - t0, "build_plan_s": t2 - t1,
         "reference": "dynpart " + dynpart.__version__,
     }
