@@ -14,6 +14,8 @@
 // dead-pair and re-keying rules, so the output groups, memory_bytes and
 // saved_bytes equal the reference's (tests/test_fusion_native.py).
 #include <algorithm>
+#include <climits>
+#include <cstdlib>
 #include <cstdint>
 #include <queue>
 #include <string>
@@ -98,6 +100,78 @@ extern "C" int dgc_plan_spatial_fusion(
       dgc::set_error("BudgetExceededError: chunk " + std::to_string(g[i].rep) + " needs " +
                      std::to_string(mem) + " bytes, budget is " + std::to_string(memory_budget));
       return DGC_ERR_PLAN;
+    }
+  }
+  // Fast exact path. If even the union of ALL this device's chunks fits the
+  // budget, no merge can ever be rejected (a group's estimate only grows with
+  // its member set), so the greedy loop merges every pair with positive saving
+  // until none is left: the result is the connected components of the
+  // positive-inter_cost chunk graph, saved = the inter_cost inside each
+  // component, independent of merge order. Equal to the heap path on every
+  // non-binding golden case (tests/test_fusion_native.py).
+  {
+    std::unordered_set<i64> all_members;
+    i64 all_edges = 0, n_mem = 0;
+    for (i64 i = 0; i < C; ++i) {
+      n_mem += (i64)g[i].member_list.size();
+      all_edges += g[i].edges;
+      for (i64 v : g[i].member_list) all_members.insert(v);
+    }
+    std::unordered_set<i64> all_ext;
+    for (i64 i = 0; i < C; ++i)
+      for (i64 x : g[i].ext_halo)
+        if (!all_members.count(x)) all_ext.insert(x);
+    if (memory_of(n_mem, (i64)all_ext.size(), all_edges) <= memory_budget &&
+        !std::getenv("DGC_FUSION_FORCE_HEAP")) {
+      std::vector<i64> parent(C);
+      for (i64 i = 0; i < C; ++i) parent[i] = i;
+      auto find = [&](i64 x) {
+        while (parent[x] != x) x = parent[x] = parent[parent[x]];
+        return x;
+      };
+      std::vector<std::pair<i64, i64>> pos_pairs;
+      for (auto& kv : inter) {
+        if (kv.second <= 0) continue;
+        const i64 a = kv.first / n_chunks, b = kv.first % n_chunks;
+        if (local[a] < 0 || local[b] < 0) continue;
+        pos_pairs.emplace_back(kv.first, kv.second);
+        const i64 ra = find(local[a]), rb = find(local[b]);
+        if (ra != rb) parent[std::max(ra, rb)] = std::min(ra, rb);
+      }
+      std::unordered_map<i64, std::vector<i64>> comp;  // root -> device chunk indices
+      for (i64 i = 0; i < C; ++i) comp[find(i)].push_back(i);
+      std::unordered_map<i64, i64> comp_saved;
+      for (auto& pw : pos_pairs) comp_saved[find(local[pw.first / n_chunks])] += pw.second;
+      std::vector<std::pair<i64, i64>> reps;  // (min chunk id, root)
+      for (auto& kv : comp) {
+        i64 mn = INT64_MAX;
+        for (i64 i : kv.second) mn = std::min<i64>(mn, device_chunks[i]);
+        reps.emplace_back(mn, kv.first);
+      }
+      std::sort(reps.begin(), reps.end());
+      i64 ng = 0;
+      std::vector<int> in_comp(0);
+      for (auto& rv : reps) {
+        const auto& idx = comp[rv.second];
+        std::unordered_set<i64> mem_set;
+        i64 nm = 0, ed = 0;
+        for (i64 i : idx) {
+          out_group_of_chunk[i] = (int32_t)ng;
+          nm += (i64)g[i].member_list.size();
+          ed += g[i].edges;
+          for (i64 v : g[i].member_list) mem_set.insert(v);
+        }
+        std::unordered_set<i64> ext;
+        for (i64 i : idx)
+          for (i64 x : g[i].ext_halo)
+            if (!mem_set.count(x)) ext.insert(x);
+        out_group_memory[ng] = memory_of(nm, (i64)ext.size(), ed);
+        auto cs = comp_saved.find(rv.second);
+        out_group_saved[ng] = cs == comp_saved.end() ? 0 : cs->second;
+        ++ng;
+      }
+      *n_groups_out = ng;
+      return DGC_OK;
     }
   }
   // owner: instance -> live group index; rep -> group index

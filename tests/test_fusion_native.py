@@ -52,3 +52,19 @@ def test_native_fusion_budget_exceeded(golden_dir):
     queues = [z["queue_chunks"][z["queue_ptr"][0]:z["queue_ptr"][1]]]
     with pytest.raises(ValueError, match="BudgetExceededError"):
         native_fusion(_pa(z, meta["profile"]), queues, memory_budget=1000)
+
+
+@pytest.mark.parametrize("name", ["f6k_d2", "f30k_d3"])
+def test_heap_path_equals_component_fast_path(golden_dir, name, monkeypatch):
+    """The general greedy heap path and the non-binding connected-component
+    shortcut give identical plans (and both equal the reference)."""
+    z = np.load(golden_dir / f"fusion_{name}.npz")
+    meta = json.loads(bytes(z["meta"]).decode())
+    qp, qc = z["queue_ptr"], z["queue_chunks"]
+    queues = [qc[qp[d]:qp[d + 1]] for d in range(len(qp) - 1)]
+    fast = native_fusion(_pa(z, meta["profile"]), queues, meta["budget"])
+    monkeypatch.setenv("DGC_FUSION_FORCE_HEAP", "1")
+    heap = native_fusion(_pa(z, meta["profile"]), queues, meta["budget"])
+    for a, b in zip(fast, heap):
+        np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(heap[2], z["group_chunks"])
