@@ -22,7 +22,8 @@ namespace {
 
 using namespace dgc::tc;
 using dgc::make_map;
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;  // 2 per TMEM lane quadrant, round-robin 32-column chunks
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kABytes = BM * BK * 4;  // 16 KiB
 
 template <bool A_MN, bool B_MN, bool SPLIT3>
@@ -32,22 +33,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                      int kb_total, int kb_per_split, int m_tiles, int n_tiles, int splits,
                      const float* __restrict__ bias, const float* __restrict__ relu_src,
                      int accumulate, float* __restrict__ partial,
-                     float* __restrict__ colsum_partial) {
-  // Persistent: CTA c owns tiles c, c+G, ... of the (split, n-tile, m-tile)
-  // space (m fastest, so a CTA's consecutive tiles share the B panel). Two TMEM
-  // accumulators let the epilogue drain tile i while the MMA runs tile i+1.
+                     float* __restrict__ colsum_partial, int b_res) {
+  // Persistent: CTA c owns tiles c, c+G, ... of the (split, m-tile, n-tile)
+  // space, n fastest. With G a multiple of n_tiles every CTA keeps ONE n-tile,
+  // so (b_res) its whole B panel is loaded into shared memory once and only A
+  // streams; the n_tiles CTAs sharing an A tile run together (L2 dedups A).
+  // Two TMEM accumulators let the epilogue drain tile i while the MMA runs i+1.
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~(uintptr_t)1023);
   const int b_bytes = bn * BK * 4;
   const int ab_bytes = kABytes + b_bytes;
+  const int ld_bytes = b_res ? kABytes : ab_bytes;  // bytes TMA-loaded per stage
   const int stage_bytes = ab_bytes * (SPLIT3 ? 2 : 1);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * stage_bytes);
+  uint8_t* bres = smem + (size_t)stages * (b_res ? kABytes : stage_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(bres + (b_res ? (size_t)kb_total * b_bytes : 0));
   uint64_t* empty = full + stages;
   uint64_t* conv = empty + stages;
   uint64_t* tfull = conv + stages;   // [2]
   uint64_t* tempty = tfull + 2;      // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bres_full = tempty + 2;  // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_full + 1);
   float* stg_base = reinterpret_cast<float*>(tmem_slot + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -59,12 +65,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
-      mbar_init(&conv[s], 128);
+      mbar_init(&conv[s], 32 * kEpiWarps);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], 32 * kEpiWarps);
     }
+    mbar_init(bres_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
@@ -81,10 +88,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   auto tile_coords = [&](int t, int64_t& m0, int64_t& n0, int& z, int& kb0, int& nkb) {
-    const int mt = t % m_tiles;
-    const int rest = t / m_tiles;
-    const int nt = rest % n_tiles;
-    z = rest / n_tiles;
+    const int nt = t % n_tiles;
+    const int rest = t / n_tiles;
+    const int mt = rest % m_tiles;
+    z = rest / m_tiles;
     m0 = (int64_t)mt * BM;
     n0 = (int64_t)nt * bn;
     kb0 = z * kb_per_split;
@@ -93,6 +100,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
+      if (b_res && (int)blockIdx.x < n_tiles_total) {
+        // the CTA's fixed n-tile: its whole B panel once
+        const int64_t n0 = (int64_t)(blockIdx.x % n_tiles) * bn;
+        mbar_expect_tx(bres_full, (uint32_t)(kb_total * b_bytes));
+        for (int kb = 0; kb < kb_total; ++kb) {
+          uint8_t* sb = bres + (size_t)kb * b_bytes;
+          if (!B_MN) {
+            tma_load_2d(sb, &tmB, kb * BK, (int)n0, bres_full);
+          } else {
+            for (int i = 0; i < bn / 32; ++i)
+              tma_load_2d(sb + i * 4096, &tmB, (int)n0 + 32 * i, kb * BK, bres_full);
+          }
+        }
+      }
       int g = 0;
       for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
         int64_t m0, n0;
@@ -102,9 +123,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = g % stages;
           const uint32_t ph = (g / stages) & 1;
           mbar_wait(&empty[s], ph ^ 1);
-          uint8_t* sa = smem + (size_t)s * stage_bytes;
+          uint8_t* sa = smem + (size_t)s * (b_res ? kABytes : stage_bytes);
           uint8_t* sb = sa + kABytes;
-          mbar_expect_tx(&full[s], (uint32_t)ab_bytes);
+          mbar_expect_tx(&full[s], (uint32_t)ld_bytes);
           const int k0 = (kb0 + kb) * BK;
           if (!A_MN) {
             tma_load_2d(sa, &tmA, k0, (int)m0, &full[s]);
@@ -113,17 +134,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < BM / 32; ++i)
               tma_load_2d(sa + i * 4096, &tmA, (int)m0 + 32 * i, k0, &full[s]);
           }
-          if (!B_MN) {
-            tma_load_2d(sb, &tmB, k0, (int)n0, &full[s]);
-          } else {
-            for (int i = 0; i < bn / 32; ++i)
-              tma_load_2d(sb + i * 4096, &tmB, (int)n0 + 32 * i, k0, &full[s]);
+          if (!b_res) {
+            if (!B_MN) {
+              tma_load_2d(sb, &tmB, k0, (int)n0, &full[s]);
+            } else {
+              for (int i = 0; i < bn / 32; ++i)
+                tma_load_2d(sb + i * 4096, &tmB, (int)n0 + 32 * i, k0, &full[s]);
+            }
           }
         }
       }
     }
   } else if (warp == 1) {
     const uint32_t idesc = idesc_tf32(bn, A_MN, B_MN);
+    if (b_res) {
+      mbar_wait(bres_full, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
     int g = 0, i = 0;
     for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++i) {
       int64_t m0, n0;
@@ -140,8 +167,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(SPLIT3 ? &conv[s] : &full[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (lane == 0) {
-          const uint32_t sa = smem_u32(smem + (size_t)s * stage_bytes);
-          const uint32_t sb = sa + kABytes;
+          const uint32_t sa = smem_u32(smem + (size_t)s * (b_res ? kABytes : stage_bytes));
+          const uint32_t sb = b_res ? smem_u32(bres + (size_t)(kb0 + kb) * b_bytes) : sa + kABytes;
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
             // K-major: advance 32 B inside the 128-B swizzle row; MN-major: eight
@@ -165,7 +192,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    const int tq = threadIdx.x - 64;  // 0..127
+    const int tq = threadIdx.x - 64;  // 0..32*kEpiWarps-1
+    const int chalf = (warp - 2) >> 2;  // first 32-column chunk of this warp
     const int q = warp & 3;           // TMEM lane quadrant this warp may access
     float* stg = stg_base + (warp - 2) * 32 * 33;
     int g = 0, i = 0;
@@ -180,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&full[s], ph);
           float4* hi = reinterpret_cast<float4*>(smem + (size_t)s * stage_bytes);
           float4* lo = reinterpret_cast<float4*>(smem + (size_t)s * stage_bytes + ab_bytes);
-          for (int e = tq; e < ab_bytes / 16; e += 128) {
+          for (int e = tq; e < ab_bytes / 16; e += 32 * kEpiWarps) {
             const float4 x = hi[e];
             float4 h, l;
             h.x = __uint_as_float(to_tf32(x.x));
@@ -204,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       // TMEM -> registers (thread = row) -> padded smem transpose -> coalesced
       // 128-byte row stores (lane = column), epilogue fused into the store pass.
-      for (int c = 0; c < bn; c += 32) {
+      for (int c = 32 * chalf; c < bn; c += 32 * (kEpiWarps / 4)) {
         float v[32];
         tmem_ld32(tmem_base + (uint32_t)a * acc_cols + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
 #pragma unroll
@@ -214,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool col_ok = (c + lane < bn) && (n < N);
         const float bn_v = (bias && col_ok) ? __ldg(bias + n) : 0.f;
         float csum = 0.f;  // this warp's 32 rows of column n (bias gradients)
-#pragma unroll
+#pragma unroll 1
         for (int r0 = 0; r0 < 32; r0 += 8) {
           float x[8], aux[8], acc_in[8];
           bool ok[8];
@@ -281,24 +309,30 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, float* C, int64_t 
                 float* colsum_partial, cudaStream_t s) {
   const int ab = kABytes + bn * BK * 4;
   const int stage_bytes = ab * (SPLIT3 ? 2 : 1);
-  const int budget = 190 * 1024;
-  int stages = budget / stage_bytes;
+  const int budget = 155 * 1024;  // + ~68 KB epilogue staging + barriers <= 227 KB
+  // B panel resident in shared memory when one CTA keeps one n-tile and it fits
+  const int bres_bytes = kb_total * bn * BK * 4;
+  const int b_res = (!SPLIT3 && splits == 1 && bres_bytes <= 96 * 1024 &&
+                     !getenv("DGC_GEMM_NO_BRES")) ? 1 : 0;
+  int stages = b_res ? (budget - bres_bytes) / kABytes : budget / stage_bytes;
   stages = stages > 4 ? 4 : stages;
   if (const char* env = getenv("DGC_GEMM_MAX_STAGES")) {
     const int cap = atoi(env);
     if (cap >= 1 && cap < stages) stages = cap;
   }
   if (stages < 1) return dgc::fail(DGC_ERR_ARG, "gemm: tile does not fit shared memory");
-  const size_t smem = (size_t)stages * stage_bytes + 1024 + 256 + 4 * 32 * 33 * 4;
+  const size_t smem = (size_t)stages * (b_res ? kABytes : stage_bytes) +
+                      (b_res ? (size_t)bres_bytes : 0) + 1024 + 256 + kEpiWarps * 32 * 33 * 4;
   auto kern = gemm_tf32_kernel<A_MN, B_MN, SPLIT3>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return dgc::cuda_fail(e, "gemm: set smem");
   const int m_tiles = (int)((M + BM - 1) / BM);
   const int total = m_tiles * ntiles * splits;
-  const int grid = total < dgc::kNumSMs ? total : dgc::kNumSMs;
+  int grid = (dgc::kNumSMs / ntiles) * ntiles;  // multiple of n_tiles: fixed n per CTA
+  if (grid > total) grid = total;
   kern<<<grid, kThreads, smem, s>>>(ma, mb, C, ldc, M, N, bn, stages, kb_total, kb_per, m_tiles,
                                     ntiles, splits, bias, relu_src, accumulate, partial,
-                                    colsum_partial);
+                                    colsum_partial, b_res);
   DGC_CHECK_LAUNCH("gemm_tf32_kernel");
   return DGC_OK;
 }
