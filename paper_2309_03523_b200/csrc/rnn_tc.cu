@@ -250,6 +250,262 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
 }
 
+// ---------------------------------------------------------------------------
+// Backward (BPTT) on tensor cores. Per position p, from the last to the first:
+//   epi : dh = m(p+1) * acc[(p+1)%2] + dh_out[inst], dc = dc carried (global
+//         scratch, per tile row x unit); saved gates -> da (4 gates) -> dgx,
+//         bias partial sums, carried dc = dcn * f * m(p); da is written straight
+//         into a ring of K-major SWIZZLE_128B A k-blocks (32 gate columns each);
+//   MMA : acc[p%2] = da[128, 4H] x U^T  (B = U itself, [H, 4H] K-major, TMA ring)
+//         = the gradient w.r.t. h_in(p), consumed by the epilogue of p-1.
+// Two TMEM accumulators + an acc_empty barrier let the MMA of p-1 start on the
+// first da k-blocks while the epilogue of p is still reading acc[(p+1)%2].
+constexpr int kBwdEpiWarps = 8;
+constexpr int kBwdEpiThreads = 32 * kBwdEpiWarps;
+constexpr int kBwdThreads = 64 + kBwdEpiThreads;
+constexpr int kBwdAStages = 8;
+constexpr int kBwdBStages = 4;
+
+template <int H>
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    lstm_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmU, const int32_t* __restrict__ slot_row,
+                       const uint8_t* __restrict__ slot_mask, int64_t R, int L,
+                       const float* __restrict__ save, const float* __restrict__ dh_out,
+                       float* __restrict__ dgx, float* __restrict__ dc_scr, int rnd,
+                       float* __restrict__ bias_partial) {
+  constexpr int G4 = 4 * H;
+  constexpr int NC = H / 32;                 // 32-unit chunks
+  constexpr int KB = G4 / BK;                // k-blocks of da per position (= 4*NC)
+  constexpr int kAStage = BM * 128;          // 16 KB
+  constexpr int kBStage = H * 128;           // H rows of U x 32 k
+  constexpr uint32_t kTmemCols = 2 * H <= 32 ? 32 : 2 * H <= 64 ? 64 : 2 * H <= 128 ? 128 : 256;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + kBwdAStages * kAStage;
+  float* stg_all = reinterpret_cast<float*>(sB + kBwdBStages * kBStage);
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(stg_all + kBwdEpiWarps * 32 * 33);
+  uint64_t* a_empty = a_full + kBwdAStages;
+  uint64_t* b_full = a_empty + kBwdAStages;
+  uint64_t* b_empty = b_full + kBwdBStages;
+  uint64_t* acc_full = b_empty + kBwdBStages;   // [2]
+  uint64_t* acc_empty = acc_full + 2;           // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row0 = (int64_t)blockIdx.x * BM;
+  if (warp == 0 && lane == 0) {
+    // a k-block (gate, chunk) is written by the 4 quadrant warps of one half
+    for (int s = 0; s < kBwdAStages; ++s) {
+      mbar_init(&a_full[s], 128);
+      mbar_init(&a_empty[s], 1);
+    }
+    for (int s = 0; s < kBwdBStages; ++s) {
+      mbar_init(&b_full[s], 1);
+      mbar_init(&b_empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], kBwdEpiThreads);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmU) : "memory");
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  // k-block sequence per position: i = c*4 + g  (chunk c, gate g), K offset g*H + 32c
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int seq = 0; seq < L * KB; ++seq) {
+        const int s = seq % kBwdBStages;
+        mbar_wait(&b_empty[s], ((seq / kBwdBStages) & 1) ^ 1);
+        const int i = seq % KB, c = i >> 2, g = i & 3;
+        mbar_expect_tx(&b_full[s], (uint32_t)kBStage);
+        tma_load_2d(sB + s * kBStage, &tmU, g * H + 32 * c, 0, &b_full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = idesc_tf32(H, false, false);
+    const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+    for (int t = 0; t < L; ++t) {  // t = L-1-p
+      const int p = L - 1 - t;
+      const int a = p & 1;
+      mbar_wait(&acc_empty[a], ((t >> 1) & 1) ^ 1);
+      fence_after();
+      for (int i = 0; i < KB; ++i) {
+        const int seq = t * KB + i;
+        const int sa = seq % kBwdAStages, sb = seq % kBwdBStages;
+        mbar_wait(&a_full[sa], (seq / kBwdAStages) & 1);
+        mbar_wait(&b_full[sb], (seq / kBwdBStages) & 1);
+        fence_after();
+        if (lane == 0) {
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk)
+            mma_tf32(tmem_base + a * H, kdesc(a_base + sa * kAStage + kk * 32),
+                     kdesc(b_base + sb * kBStage + kk * 32), idesc, (i > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&a_empty[sa]);
+          mma_commit(&b_empty[sb]);
+          if (i == KB - 1) mma_commit(&acc_full[a]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    const int ew = warp - 2;
+    const int q = warp & 3;            // TMEM lane quadrant = rows q*32..q*32+31
+    const int half = ew >> 2;          // chunks c with c % 2 == half
+    float* stg = stg_all + ew * 32 * 33;
+    const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
+    const int64_t my_row = row0 + q * 32 + lane;
+    const bool my_ok = my_row < R;
+    float bsum[(NC + 1) / 2][4];
+#pragma unroll
+    for (int cc = 0; cc < (NC + 1) / 2; ++cc)
+#pragma unroll
+      for (int g = 0; g < 4; ++g) bsum[cc][g] = 0.f;
+    for (int t = 0; t < L; ++t) {
+      const int p = L - 1 - t;
+      const bool has_next = p + 1 < L;
+      const int64_t my_s = my_row * L + p;
+      const int my_inst = my_ok ? slot_row[my_s] : -1;
+      const float my_m = my_ok ? (float)slot_mask[my_s] : 0.f;
+      const float my_mnext = (has_next && my_ok) ? (float)slot_mask[my_s + 1] : 0.f;
+      if (has_next) {
+        mbar_wait(&acc_full[(p + 1) & 1], ((t - 1) >> 1) & 1);
+        fence_after();
+      }
+#pragma unroll 1
+      for (int c = half, cc = 0; c < NC; c += 2, ++cc) {
+        const int j = 32 * c + lane;  // this lane's hidden unit
+        if (has_next) {
+          float v[32];
+          tmem_ld32(tl + ((p + 1) & 1) * H + 32 * c, v);
+#pragma unroll
+          for (int u = 0; u < 32; ++u) stg[lane * 33 + u] = v[u];
+        }
+        __syncwarp();
+        // acquire the 4 A k-blocks (c, g) of this position
+        const int seq0 = t * KB + c * 4;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int seq = seq0 + g;
+          mbar_wait(&a_empty[seq % kBwdAStages], ((seq / kBwdAStages) & 1) ^ 1);
+        }
+#pragma unroll 1
+        for (int r0 = 0; r0 < 32; r0 += 8) {
+          float ld[8][6], dhv[8], dcv[8];
+          int inst[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int rl = r0 + u;
+            inst[u] = __shfl_sync(0xffffffffu, my_inst, rl);
+            const float mn = __shfl_sync(0xffffffffu, my_mnext, rl);
+            const int64_t trow = (int64_t)blockIdx.x * BM + q * 32 + rl;
+            dhv[u] = has_next ? mn * stg[rl * 33 + lane] : 0.f;
+            dcv[u] = has_next ? dc_scr[trow * H + j] : 0.f;
+            if (inst[u] >= 0) {
+              dhv[u] += dh_out[(int64_t)inst[u] * H + j];
+              const float* sv = save + (int64_t)inst[u] * 7 * H + j;
+#pragma unroll
+              for (int k = 0; k < 6; ++k) ld[u][k] = sv[(k + 1) * H];  // c_in,i,f,g,o,tc
+            } else {
+#pragma unroll
+              for (int k = 0; k < 6; ++k) ld[u][k] = 0.f;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int rl = r0 + u;
+            const int r = q * 32 + rl;
+            const float mp = __shfl_sync(0xffffffffu, my_m, rl);
+            const int64_t trow = (int64_t)blockIdx.x * BM + r;
+            float da[4] = {0.f, 0.f, 0.f, 0.f};
+            float dcp = 0.f;
+            if (inst[u] >= 0) {
+              const float c_in = ld[u][0], ig = ld[u][1], fg = ld[u][2], gg = ld[u][3],
+                          og = ld[u][4], tc = ld[u][5];
+              const float g_ = dhv[u];
+              const float d_o = g_ * tc;
+              const float dcn = dcv[u] + g_ * og * (1.f - tc * tc);
+              da[0] = dcn * gg * ig * (1.f - ig);
+              da[1] = dcn * c_in * fg * (1.f - fg);
+              da[2] = dcn * ig * (1.f - gg * gg);
+              da[3] = d_o * og * (1.f - og);
+              dcp = dcn * fg * mp;
+              float* o = dgx + (int64_t)inst[u] * G4 + j;
+#pragma unroll
+              for (int g = 0; g < 4; ++g) {
+                if (rnd) da[g] = rna_tf32(da[g]);
+                o[g * H] = da[g];
+                bsum[cc][g] += da[g];
+              }
+            }
+            if (row0 + r < R) dc_scr[trow * H + j] = dcp;
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              const int seq = seq0 + g;
+              *reinterpret_cast<float*>(sA + (seq % kBwdAStages) * kAStage + sw128_offset(r, lane)) = da[g];
+            }
+          }
+        }
+        fence_async_smem();
+#pragma unroll
+        for (int g = 0; g < 4; ++g) mbar_arrive(&a_full[(seq0 + g) % kBwdAStages]);
+        __syncwarp();
+      }
+      if (has_next) {  // release the accumulator this position read
+        fence_before();
+        mbar_arrive(&acc_empty[(p + 1) & 1]);
+      }
+    }
+    // bias partials: combine the 4 quadrant warps of each half in fixed order
+    if (bias_partial) {
+      __syncwarp();
+      for (int cc = 0; cc < (NC + 1) / 2; ++cc) {  // uniform trip count for bar.sync
+        const int c = half + 2 * cc;
+        for (int g = 0; g < 4; ++g) {
+          stg[lane] = bsum[cc][g];
+          asm volatile("bar.sync 1, %0;" ::"r"(kBwdEpiThreads));
+          if (q == 0 && c < NC) {
+            float acc = 0.f;
+            for (int qq = 0; qq < 4; ++qq)
+              acc += stg_all[((qq + 4 * half) - 0) * 32 * 33 + lane];
+            bias_partial[(int64_t)blockIdx.x * G4 + g * H + 32 * c + lane] = acc;
+          }
+          asm volatile("bar.sync 1, %0;" ::"r"(kBwdEpiThreads));
+        }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
+}
+
+template <int H>
+int launch_lstm_bwd_tc(const float* U, const int32_t* slot_row, const uint8_t* slot_mask,
+                       int64_t R, int L, const float* save, const float* dh_out, float* dgx,
+                       float* dc_scr, int rnd, float* bias_partial, cudaStream_t s) {
+  CUtensorMap m;
+  int rc = make_map(&m, U, H, 4 * H, 4 * H, 32, H, false);
+  if (rc) return rc;
+  const size_t smem = (size_t)kBwdAStages * BM * 128 + (size_t)kBwdBStages * H * 128 +
+                      (size_t)kBwdEpiWarps * 32 * 33 * 4 + 1024 + 512;
+  auto kern = lstm_bwd_tc_kernel<H>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_bwd_tc: set smem");
+  const int grid = (int)((R + BM - 1) / BM);
+  kern<<<grid, kBwdThreads, smem, s>>>(m, slot_row, slot_mask, R, L, save, dh_out, dgx, dc_scr,
+                                       rnd, bias_partial);
+  DGC_CHECK_LAUNCH("lstm_bwd_tc_kernel");
+  return DGC_OK;
+}
+
 template <int H>
 int launch_lstm_tc(const float* gx, const float* Ut, const int32_t* slot_row,
                    const uint8_t* slot_mask, const int32_t* slot_carry, const float* carry,
@@ -295,3 +551,21 @@ extern "C" int dgc_debug_lstm_timestamps(unsigned long long* out, int n) {
   cudaError_t e = cudaMemcpyFromSymbol(out, g_lstm_ts, n * sizeof(unsigned long long));
   return e == cudaSuccess ? DGC_OK : dgc::cuda_fail(e, "debug timestamps");
 }
+
+extern "C" int dgc_rnn_bwd_tc(int32_t cell_flags, const float* U, const int32_t* slot_row,
+                              const uint8_t* slot_mask, int64_t n_rows, int32_t row_len, int32_t H,
+                              const float* save, const float* dh_out, float* dgx, float* dc_scratch,
+                              float* bias_partial, void* stream) {
+  const int cell = cell_flags & 0xff, rnd = (cell_flags >> 8) & 1;
+  DGC_REQUIRE(cell == 1, "rnn_bwd_tc: only the LSTM cell has a tensor-core kernel yet");
+  if (n_rows == 0 || row_len == 0) return DGC_OK;
+  cudaStream_t s = dgc::as_stream(stream);
+  switch (H) {
+    case 32: return launch_lstm_bwd_tc<32>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
+    case 64: return launch_lstm_bwd_tc<64>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
+    case 128: return launch_lstm_bwd_tc<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
+    default: return dgc::fail(DGC_ERR_ARG, "rnn_bwd_tc: H must be 32, 64 or 128");
+  }
+}
+
+extern "C" int64_t dgc_rnn_tc_tiles(int64_t n_rows) { return (n_rows + 127) / 128; }

@@ -155,6 +155,24 @@ def rnn_fwd_tc(cell, gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row
         "dgc_rnn_fwd_tc"), nb, 2.0 * n_rows * row_len * H * G * H)
 
 
+def rnn_bwd_tc(cell, U, slot_row, slot_mask, n_rows, row_len, H, save, dh_out, dgx, dc_scratch,
+               bias_partial=None):
+    """K4 BPTT on tcgen05 (dgc_rnn_bwd_tc): dh = da U^T on tensor cores."""
+    _req(dh_out, torch.float32, "dh_out"); _req(dgx, torch.float32, "dgx")
+    n_inst, G = dgx.shape[0], 4
+    sf = rnn_save_floats(1, H)
+    nb = 4 * n_inst * (G * H + 6 * H + H) + 5 * n_rows * row_len + 4 * G * H * H
+    _run("lstm_bwd_tc", lambda: _native.check(
+        _native.lib().dgc_rnn_bwd_tc(cell, _p(U), _p(slot_row), _p(slot_mask), n_rows, row_len, H,
+                                     _p(save), _p(dh_out), _p(dgx), _p(dc_scratch),
+                                     _p(bias_partial), _stream()), "dgc_rnn_bwd_tc"),
+        nb, 2.0 * n_rows * row_len * H * G * H)
+
+
+def rnn_tc_tiles(n_rows):
+    return _native.lib().dgc_rnn_tc_tiles(n_rows)
+
+
 def rnn_bwd_partial_rows(n_rows, H):
     return _native.lib().dgc_rnn_bwd_partial_rows(n_rows, H)
 

@@ -160,6 +160,10 @@ class Shard:
         self.tc_rnn = (cfg.precision == "tf32" and cfg.rnn == "lstm" and H in (32, 64, 128)
                        and os.environ.get("DGC_TC_RNN", "1") != "0")
         self.Ut_f = [torch.zeros((GH, H), **f32) for _ in range(cfg.n_rnn)] if self.tc_rnn else None
+        if self.tc_rnn:
+            tiles = ops.rnn_tc_tiles(max(self.R, 1))
+            self.rnn_dc_scratch = torch.zeros((tiles * 128, H), **f32)
+            self.rnn_tc_prows = tiles
         self.dYext = torch.zeros((self.nloc, H), **f32)
         self.colsum_scratch = torch.zeros(2 * 148 * max(GH, cfg.C, H), **f32)
         # fused bias-gradient partial sums (produced inside the kernels that write
@@ -167,7 +171,8 @@ class Shard:
         self.m_tiles = max(1, (n + 127) // 128)
         self.rnn_prows = ops.rnn_bwd_partial_rows(self.R, H) if self.R else 1
         self.dl_partial = torch.zeros(max(1, (n + 255) // 256) * cfg.C, **f32)
-        self.bias_partial = torch.zeros(max(self.rnn_prows * GH, 4 * self.m_tiles * H), **f32)
+        prows = max(self.rnn_prows, ops.rnn_tc_tiles(max(self.R, 1)))
+        self.bias_partial = torch.zeros(max(prows * GH, 4 * self.m_tiles * H), **f32)
         # split-K for weight gradients: ~one wave of 148 SMs
         kb = max(1, (n + 31) // 32)
         self.ksplit = max(1, min(148, kb // 4))
@@ -334,10 +339,16 @@ class Shard:
         ops.gemm(self.dlogits, self.pr("Wo"), self.dh, n, H, cfg.C, b_mn=False, ldb=cfg.C,
                  precision=prec)
         for k in reversed(range(cfg.n_rnn)):
-            ops.transpose(self.pr(f"U{k}"), self.Ut)
-            ops.rnn_bwd(cell | rflag, self.Ut, self.slot_row, self.slot_mask, self.R, self.L, H,
-                        self.save[k], self.dh, self.dgx, bias_partial=self.bias_partial)
-            ops.reduce_rows(self.bias_partial, self.rnn_prows, GH, self.g(f"br{k}"))
+            if self.tc_rnn:
+                ops.rnn_bwd_tc(cell | rflag, self.pr(f"U{k}"), self.slot_row, self.slot_mask,
+                               self.R, self.L, H, self.save[k], self.dh, self.dgx,
+                               self.rnn_dc_scratch, bias_partial=self.bias_partial)
+                ops.reduce_rows(self.bias_partial, self.rnn_tc_prows, GH, self.g(f"br{k}"))
+            else:
+                ops.transpose(self.pr(f"U{k}"), self.Ut)
+                ops.rnn_bwd(cell | rflag, self.Ut, self.slot_row, self.slot_mask, self.R, self.L,
+                            H, self.save[k], self.dh, self.dgx, bias_partial=self.bias_partial)
+                ops.reduce_rows(self.bias_partial, self.rnn_prows, GH, self.g(f"br{k}"))
             xin, ldxin = (self.Hl[1], H) if k == 0 else (self.hbuf[k - 1], self.hw)
             ops.gemm(xin, self.dgx, self.g(f"Wx{k}"), H, GH, n, a_mn=True, lda=ldxin,
                      precision=prec, k_splits=ks, partial=part)

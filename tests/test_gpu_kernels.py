@@ -261,3 +261,42 @@ def test_lstm_fwd_tensor_core_matches_simt(H):
         outs.append((hc.cpu().numpy(), save.cpu().numpy()))
     close(outs[1][0], outs[0][0], 2e-3, "lstm tc h|c")
     close(outs[1][1], outs[0][1], 2e-3, "lstm tc save")
+
+
+@pytest.mark.parametrize("H", [32, 64, 128])
+def test_lstm_bwd_tensor_core_matches_simt(H):
+    """K4 BPTT on tcgen05 (TF32) vs the fp32 SIMT BPTT on the same packed runs:
+    dgx and the fused bias partial sums."""
+    from paper_2309_03523_b200 import ops
+    from paper_2309_03523_b200.layout import pack_sequences_native
+    rng = np.random.default_rng(H + 1)
+    lengths = rng.integers(1, 20, size=700)
+    seq, pos, mask, _ = pack_sequences_native(lengths)
+    R, L = seq.shape
+    offs = np.concatenate([[0], np.cumsum(lengths)])
+    n = int(offs[-1])
+    slot_row = np.where(seq >= 0, offs[np.maximum(seq, 0)] + pos, -1).astype(np.int32).reshape(-1)
+    U = (rng.standard_normal((H, 4 * H)) / np.sqrt(H)).astype(np.float32)
+    save = np.concatenate([rng.standard_normal((n, 2 * H)),            # h_in, c_in
+                           rng.random((n, 4 * H)),                      # i, f, g, o
+                           np.tanh(rng.standard_normal((n, H)))], 1).astype(np.float32)
+    dh = rng.standard_normal((n, H)).astype(np.float32)
+    outs = []
+    for tc in (False, True):
+        dgx = torch.zeros((n, 4 * H), device=dev)
+        sr, sm = t(slot_row, torch.int32), t(mask.reshape(-1), torch.uint8)
+        if tc:
+            tiles = ops.rnn_tc_tiles(R)
+            bp = torch.zeros((tiles, 4 * H), device=dev)
+            scr = torch.zeros((tiles * 128, H), device=dev)
+            ops.rnn_bwd_tc(1, t(U), sr, sm, R, L, H, t(save), t(dh), dgx, scr, bias_partial=bp)
+            bias = bp.sum(0)
+        else:
+            rows = ops.rnn_bwd_partial_rows(R, H)
+            bp = torch.zeros((rows, 4 * H), device=dev)
+            ops.rnn_bwd(1, t(U.T.copy()), sr, sm, R, L, H, t(save), t(dh), dgx, bias_partial=bp)
+            bias = bp.sum(0)
+        torch.cuda.synchronize()
+        outs.append((dgx.cpu().numpy(), bias.cpu().numpy()))
+    close(outs[1][0], outs[0][0], 3e-3, "lstm bwd tc dgx")
+    close(outs[1][1], outs[0][1], 3e-3, "lstm bwd tc bias")

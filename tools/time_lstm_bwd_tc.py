@@ -1,0 +1,26 @@
+import sys
+sys.path.insert(0, ".")
+import numpy as np, torch
+from paper_2309_03523_b200 import ops
+from paper_2309_03523_b200.layout import pack_sequences_native
+H = int(sys.argv[1]) if len(sys.argv) > 1 else 128
+lengths = np.full(6250, 32)
+seq, pos, mask, _ = pack_sequences_native(lengths)
+R, L = seq.shape
+offs = np.concatenate([[0], np.cumsum(lengths)])
+n = int(offs[-1])
+slot_row = np.where(seq >= 0, offs[np.maximum(seq, 0)] + pos, -1).astype(np.int32).reshape(-1)
+dev = "cuda"
+U = torch.randn((H, 4 * H), device=dev) / H ** 0.5
+sr = torch.tensor(slot_row, device=dev); sm = torch.tensor(mask.reshape(-1), device=dev)
+save = torch.rand((n, 7 * H), device=dev); dh = torch.randn((n, H), device=dev)
+dgx = torch.zeros((n, 4 * H), device=dev)
+tiles = ops.rnn_tc_tiles(R)
+bp = torch.zeros((tiles, 4 * H), device=dev); scr = torch.zeros((tiles * 128, H), device=dev)
+fn = lambda: ops.rnn_bwd_tc(1, U, sr, sm, R, L, H, save, dh, dgx, scr, bias_partial=bp)
+fn(); torch.cuda.synchronize()
+s = torch.cuda.Event(enable_timing=True); e = torch.cuda.Event(enable_timing=True)
+s.record()
+for _ in range(3): fn()
+e.record(); torch.cuda.synchronize()
+print("lstm bwd tc H", H, f"{s.elapsed_time(e)/3:.3f} ms")
