@@ -4,7 +4,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O3
 SRC := paper_2309_03523_b200/csrc
 OUT := paper_2309_03523_b200/lib
-CU := common spmm stale exchange dense rnn gemm_tc rnn_tc
+CU := common spmm stale exchange dense rnn gemm_tc rnn_tc evolve
 OBJS := $(addprefix build/,$(addsuffix .o,$(CU))) build/layout.o build/fusion_plan.o
 
 all: $(OUT)/libdgc_b200.so

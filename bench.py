@@ -144,9 +144,10 @@ def cpu_epoch_time(pa, cfg, budget_s):
     from paper_2309_03523_b200.model import init_params, synthetic_inputs
     X, y = synthetic_inputs(pa.n_instances, cfg.F, cfg.C, 0)
     lays = [build_layout(pa, d) for d in range(pa.n_devices)]
+    T = int(pa.inst_t.max())
     ocfg = od.OracleConfig(F=cfg.F, H=cfg.H, C=cfg.C, rnn=cfg.rnn, n_rnn=cfg.n_rnn,
-                           optimizer="adam", lr=1e-3)
-    orc = od.OracleDGNN(lays, X, y, init_params(cfg, 0), ocfg)
+                           model=cfg.model, T=T, optimizer="adam", lr=1e-3)
+    orc = od.OracleDGNN(lays, X, y, init_params(cfg, 0), ocfg, inst_t=pa.inst_t)
     times = []
     t_start = time.perf_counter()
     r = 0
@@ -297,7 +298,10 @@ def run_ours(args):
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {pa.n_instances} instances x {pa.T} snapshots, "
                                f"{pa.n_spatial_edges} edges (power-law, sigma=mu), "
-                               f"{cfg.n_rnn}-layer {cfg.rnn.upper()} + 2 GCN, F={cfg.F} H={cfg.H} "
+                               + (f"EvolveGCN-O (2 GCN, per-snapshot weights), F={cfg.F} H={cfg.H} "
+                                  if cfg.model == "evolve" else
+                                  f"{cfg.n_rnn}-layer {cfg.rnn.upper()} + 2 GCN, F={cfg.F} H={cfg.H} ")
+                               + 
                                f"C={cfg.C}, chunk plan of the reference planner "
                                f"({'fused' if pa.fused else 'unfused'}, D={pa.n_devices})",
                    "epoch_ms": step_ms, "l2": "flushed (320 MB write) before every timed step",

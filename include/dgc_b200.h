@@ -51,6 +51,9 @@ typedef struct dgc_plan_view {
   const int32_t* group_device;    /* [n_groups] in FusionPlan order */
   const int64_t* group_ptr;       /* [n_groups+1] */
   const int32_t* group_chunks;    /* chunk ids per group */
+  int32_t segment_rows;           /* 0, or: group rows by snapshot, each snapshot block
+                                     padded (own_gid -1) to a multiple of segment_rows
+                                     (per-snapshot weights, EvolveGCN) */
 } dgc_plan_view;
 
 typedef struct dgc_layout dgc_layout;
@@ -62,10 +65,12 @@ enum dgc_layout_field_id {
   DGC_F_SEND_POS, DGC_F_RECV_PTR, DGC_F_RECV_SLOT, DGC_F_RUN_PTR, DGC_F_RUN_ROWS,
   DGC_F_RUN_PRED_GID, DGC_F_RUN_CARRY, DGC_F_SLOT_ROW, DGC_F_SLOT_MASK,
   DGC_F_SLOT_CARRY, DGC_F_TKEY_ROWS, DGC_F_TSEND_PTR, DGC_F_TSEND_POS,
-  DGC_F_TRECV_PTR, DGC_F_TRECV_CARRY, DGC_F_SCALARS, DGC_F_KEY_NCUT, DGC_F_COUNT
+  DGC_F_TRECV_PTR, DGC_F_TRECV_CARRY, DGC_F_SCALARS, DGC_F_KEY_NCUT, DGC_F_SEG_PTR,
+  DGC_F_COUNT
 };
 /* DGC_F_SCALARS = [n_own, n_halo, n_rows, row_len, padding, naive_padding,
  *                  n_carry, loaded_rows] (loaded_rows: sim.py:339-360)
+ * DGC_F_SEG_PTR = row start of each snapshot block (segment_rows > 0 only)
  * DGC_F_KEY_NCUT = cut spatial messages sourced by each boundary key
  * (MessageSet rows with src = key, costmodel.py:121-123) for the billing. */
 
@@ -133,6 +138,41 @@ int dgc_gemm_tf32(const float* A, int64_t lda, const float* B, int64_t ldb, floa
 /* colsum_partial (may be NULL, needs k_splits == 1): column sums of the final
  * output per (128-row tile, TMEM quadrant): [4*ceil(M/128), N]; reduce with
  * dgc_reduce_rows -> bias gradients without re-reading C. */
+
+/* Segmented K2 for per-snapshot weights (EvolveGCN). Exactly one of:
+ *  row-segmented: seg_of_mtile [ceil(M/128)] = snapshot of each 128-row tile
+ *    (rows grouped by snapshot and 128-aligned, dgc_plan_view.segment_rows);
+ *    B holds b_nseg stacked matrices ([b_nseg*K, N] if b_mn else [b_nseg*N, K]);
+ *  K-segmented: kitems [n_kitems, 2] = (first k-block, k-block count >= 1) work
+ *    items, item_ptr [n_seg+1] = items of each segment; every item writes
+ *    partial[item] [M, N]; C [n_seg*M, N] (row stride ldc) = per-segment sums
+ *    in fixed order (segments without items -> 0): per-snapshot dW = X_t^T dY_t. */
+int dgc_gemm_tf32_segmented(const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
+                            int64_t ldc, int64_t M, int64_t N, int64_t K, int32_t a_mn,
+                            int32_t b_mn, int32_t precision, const float* bias,
+                            const float* relu_src, const int32_t* seg_of_mtile, int32_t b_nseg,
+                            const int32_t* kitems, int32_t n_kitems, const int32_t* item_ptr,
+                            int32_t n_seg, float* partial, float* colsum_partial, void* stream);
+
+/* EvolveGCN-O weight evolution (matrix GRU in the reference gate form of
+ * GruCell.step, fusion.py:409-413, input = hidden = W_{t-1}):
+ *   R = s(S_r W + B_r), Z = s(S_z W + B_z), C = tanh(P_c W + Q_c (R*W) + B_c),
+ *   W_t = (1-Z)*C + Z*W_{t-1}.  W, B_* [Fl, Hl]; S_r, S_z, P_c, Q_c [Fl, Fl].
+ * fwd takes the TRANSPOSED gate matrices; writes Wstack [T+1, Fl, Hl]
+ * (Wstack[0] = W0) and saves r, z, c, w_prev, r*w_prev laid out [Fl, T, Hl].
+ * bwd takes the gate matrices as is and dW_direct [T, Fl, Hl] (d loss / d W_t
+ * from the snapshot-t GCN rows); writes dW0 [Fl, Hl], pre-activation grads
+ * da_r, da_z, da_c [Fl, T, Hl] (then dS_r = da_r w^T etc. are K2 GEMMs with
+ * K = T*Hl) and the bias grads dB_* [Fl, Hl]. flags bit 0: TF32-round saves. */
+int dgc_evolve_fwd(int32_t Fl, int32_t Hl, int32_t T, const float* W0, const float* SrT,
+                   const float* SzT, const float* PcT, const float* QcT, const float* Br,
+                   const float* Bz, const float* Bc, float* Wstack, float* sv_r, float* sv_z,
+                   float* sv_c, float* sv_w, float* sv_rw, int32_t flags, void* stream);
+int dgc_evolve_bwd(int32_t Fl, int32_t Hl, int32_t T, const float* Sr, const float* Sz,
+                   const float* Pc, const float* Qc, const float* sv_r, const float* sv_z,
+                   const float* sv_c, const float* sv_w, const float* dW_direct, float* dW0,
+                   float* da_r, float* da_z, float* da_c, float* dBr, float* dBz, float* dBc,
+                   int32_t flags, void* stream);
 
 /* K3/K4: masked recurrent time encoder over FFD-packed runs.
  * cell: 0 = GRU in the reference form of GruCell.step (fusion.py:409-413),
@@ -206,7 +246,7 @@ int dgc_scatter_rows(const float* src, const int32_t* rows, const int32_t* idx, 
 
 /* K8: softmax cross-entropy readout. dlogits = (softmax - onehot) * scale
  * (flags bit 0: rounded to TF32); loss_partial[ceil(n/256)] = per-block fp64
- * sums of -log p[label]. */
+ * sums of -log p[label]. labels < 0 mark padding rows (no loss, zero grad). */
 int dgc_softmax_xent(const float* logits, const int32_t* labels, int64_t n, int32_t C,
                      float scale, int32_t flags, float* dlogits, double* loss_partial,
                      float* dl_partial, void* stream);

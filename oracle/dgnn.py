@@ -47,6 +47,8 @@ class OracleConfig:
     stale_mode: str = "off"
     static_fraction: float = 0.5
     optimizer: str = "sgd"
+    model: str = "rnn"        # "rnn" (GCN + GRU/LSTM) or "evolve" (EvolveGCN-O)
+    T: int = 0                # snapshots (evolve)
     lr: float = 0.05
     momentum: float = 0.9
     beta1: float = 0.9
@@ -54,7 +56,59 @@ class OracleConfig:
     eps: float = 1e-8
 
 
+def evolve_forward(W0, Sr, Sz, Pc, Qc, Br, Bz, Bc, T):
+    """EvolveGCN-O with the reference GRU form (fusion.py:409-413), input =
+    hidden = W_{t-1}: returns [W_0..W_T] and the per-step saves."""
+    Ws, saves = [W0], []
+    w = W0
+    for _ in range(T):
+        r = sig(Sr @ w + Br)
+        z = sig(Sz @ w + Bz)
+        c = np.tanh(Pc @ w + Qc @ (r * w) + Bc)
+        saves.append((w, r, z, c))
+        w = (1.0 - z) * c + z * w
+        Ws.append(w)
+    return Ws, saves
+
+
+def evolve_backward(Sr, Sz, Pc, Qc, saves, dW_direct):
+    """BPTT of evolve_forward; dW_direct[t-1] = d loss / d W_t (t = 1..T)."""
+    g_Sr, g_Sz, g_Pc, g_Qc = (np.zeros_like(Sr) for _ in range(4))
+    g_Br = np.zeros_like(saves[0][0]) if saves else 0.0
+    g_Bz, g_Bc = np.zeros_like(g_Br), np.zeros_like(g_Br)
+    carry = np.zeros_like(g_Br)
+    for t in reversed(range(len(saves))):
+        w, r, z, c = saves[t]
+        g = carry + dW_direct[t]
+        dz = g * (w - c)
+        dc = g * (1.0 - z)
+        dw = g * z
+        dac = dc * (1.0 - c * c)
+        g_Pc += dac @ w.T
+        g_Qc += dac @ (r * w).T
+        g_Bc += dac
+        drw = Qc.T @ dac
+        dw += drw * r + Pc.T @ dac
+        dar = drw * w * r * (1.0 - r)
+        daz = dz * z * (1.0 - z)
+        g_Sr += dar @ w.T
+        g_Sz += daz @ w.T
+        g_Br += dar
+        g_Bz += daz
+        dw += Sr.T @ dar + Sz.T @ daz
+        carry = dw
+    return carry, g_Sr, g_Sz, g_Pc, g_Qc, g_Br, g_Bz, g_Bc
+
+
+EVOLVE_KEYS = ("Sr", "Sz", "Pc", "Qc", "Br", "Bz", "Bc")
+
+
 def param_names(cfg: OracleConfig):
+    if cfg.model == "evolve":
+        names = []
+        for l in (1, 2):
+            names += [f"W{l}_0"] + [f"{k}{l}" for k in EVOLVE_KEYS] + [f"b{l}"]
+        return names + ["Wo", "bo"]
     names = ["W1", "b1", "W2", "b2"]
     for k in range(cfg.n_rnn):
         names += [f"Wx{k}", f"U{k}", f"br{k}"]
@@ -62,14 +116,22 @@ def param_names(cfg: OracleConfig):
 
 
 class OracleDGNN:
-    def __init__(self, layouts, X, y, params: dict, cfg: OracleConfig):
+    def __init__(self, layouts, X, y, params: dict, cfg: OracleConfig, inst_t=None):
         self.L = layouts
+        self.t_own = None
+        if cfg.model == "evolve":
+            # snapshot (0-based) of every own row; -1 on padding rows
+            self.t_own = [np.where(lay.own_gid >= 0, np.asarray(inst_t)[np.maximum(lay.own_gid, 0)] - 1, -1)
+                          for lay in layouts]
         self.D = len(layouts)
         self.cfg = cfg
         self.G = GATES[cfg.rnn]
-        self.X = [np.asarray(X, np.float64)[lay.own_gid] for lay in layouts]
-        self.y = [np.asarray(y)[lay.own_gid] for lay in layouts]
-        self.n_total = sum(lay.n_own for lay in layouts)
+        self.X = [np.where((lay.own_gid >= 0)[:, None],
+                           np.asarray(X, np.float64)[np.maximum(lay.own_gid, 0)], 0.0)
+                  for lay in layouts]
+        self.y = [np.where(lay.own_gid >= 0, np.asarray(y)[np.maximum(lay.own_gid, 0)], -1)
+                  for lay in layouts]
+        self.n_total = sum(int((lay.own_gid >= 0).sum()) for lay in layouts)
         self.p = {k: np.array(v, dtype=np.float64) for k, v in params.items()}
         self.A = []
         for lay in layouts:
@@ -140,8 +202,25 @@ class OracleDGNN:
         hin = self.X
         acts = []
         fresh_all = []
+        evo = []
+        if cfg.model == "evolve":
+            for l in (1, 2):
+                Ws, sv = evolve_forward(self.p[f"W{l}_0"], *[self.p[f"{k}{l}"] for k in EVOLVE_KEYS],
+                                        cfg.T)
+                evo.append((Ws, sv))
         for l, (W, b) in enumerate([("W1", "b1"), ("W2", "b2")]):
-            Y = [h @ self.p[W] for h in hin]
+            if cfg.model == "evolve":
+                Ws = evo[l][0]
+                Y = []
+                for d in range(D):
+                    yd = np.zeros((len(hin[d]), H))
+                    for t in range(cfg.T):
+                        rows = self.t_own[d] == t
+                        if rows.any():
+                            yd[rows] = hin[d][rows] @ Ws[t + 1]
+                    Y.append(yd)
+            else:
+                Y = [h @ self.p[W] for h in hin]
             vals = [Y[d][self.L[d].key_rows] for d in range(D)]
             sends, theta, d_r = self._decide(r, vals, self.scache[l], self.scached[l],
                                              forced.get(f"s{l}"), f"s{l}")
@@ -170,7 +249,7 @@ class OracleDGNN:
         # time encoder
         rnn_saves = []
         xr = hin
-        for k in range(cfg.n_rnn):
+        for k in range(cfg.n_rnn if cfg.model == "rnn" else 0):
             outs, saves = [], []
             for d in range(D):
                 o, s = self._rnn_fwd(d, k, xr[d])
@@ -212,9 +291,11 @@ class OracleDGNN:
             s = e.sum(axis=1, keepdims=True)
             logp = logits - m - np.log(s)
             yi = self.y[d]
-            loss_sum += -logp[np.arange(len(yi)), yi].sum()
+            real = yi >= 0
+            loss_sum += -logp[np.arange(len(yi))[real], yi[real]].sum()
             g = e / s
-            g[np.arange(len(yi)), yi] -= 1.0
+            g[np.arange(len(yi))[real], yi[real]] -= 1.0
+            g[~real] = 0.0
             dlogits.append(g / self.n_total)
         loss = loss_sum / self.n_total
         out["loss"] = loss
@@ -227,7 +308,7 @@ class OracleDGNN:
             grads["Wo"] += hr[d].T @ dlogits[d]
             grads["bo"] += dlogits[d].sum(axis=0)
             dh.append(dlogits[d] @ self.p["Wo"].T)
-        for k in reversed(range(cfg.n_rnn)):
+        for k in reversed(range(cfg.n_rnn if cfg.model == "rnn" else 0)):
             xr_k, saves = rnn_saves[k]
             dx = []
             for d in range(D):
@@ -260,6 +341,24 @@ class OracleDGNN:
                     rows = lay.key_rows[pos[m]]
                     np.add.at(dY_own[d], rows, dY_halo[p][slots[m]])
             dh = []
+            if cfg.model == "evolve":
+                Ws, sv = evo[l]
+                dW_direct = [np.zeros_like(Ws[0]) for _ in range(cfg.T)]
+                for d in range(D):
+                    dhd = np.zeros_like(hin_l[d])
+                    for t in range(cfg.T):
+                        rows = self.t_own[d] == t
+                        if rows.any():
+                            dW_direct[t] += hin_l[d][rows].T @ dY_own[d][rows]
+                            dhd[rows] = dY_own[d][rows] @ Ws[t + 1].T
+                    dh.append(dhd)
+                ln = l + 1
+                out_g = evolve_backward(*[self.p[f"{k}{ln}"] for k in ("Sr", "Sz", "Pc", "Qc")],
+                                        sv, dW_direct)
+                grads[f"W{ln}_0"] += out_g[0]
+                for k, gk in zip(EVOLVE_KEYS, out_g[1:]):
+                    grads[f"{k}{ln}"] += gk
+                continue
             for d in range(D):
                 grads[W] += hin_l[d].T @ dY_own[d]
                 dh.append(dY_own[d] @ self.p[W].T)

@@ -25,6 +25,7 @@ class PlanView(C.Structure):
         ("n_temporal_links", _i64), ("temporal_links", _p),
         ("structure_device", _p), ("chunk_of", _p), ("n_devices", _i32),
         ("n_groups", _i64), ("group_device", _p), ("group_ptr", _p), ("group_chunks", _p),
+        ("segment_rows", _i32),
     ]
 
 
@@ -41,6 +42,10 @@ _SIGS = {
     "dgc_gemm_tf32": (_i32, [_p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _i32, _i32, _i32,
                               _p, _p, _i32, _i32, _p, _p, _p]),
     "dgc_gemm_splits": (_i32, [_i64, _i32, _i32]),
+    "dgc_gemm_tf32_segmented": (_i32, [_p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _i32, _i32,
+                                        _i32, _p, _p, _p, _i32, _p, _i32, _p, _i32, _p, _p, _p]),
+    "dgc_evolve_fwd": (_i32, [_i32, _i32, _i32] + [_p] * 14 + [_i32, _p]),
+    "dgc_evolve_bwd": (_i32, [_i32, _i32, _i32] + [_p] * 16 + [_i32, _p]),
     "dgc_rnn_save_floats": (_i32, [_i32, _i32]),
     "dgc_rnn_fwd": (_i32, [_i32, _p, _p, _p, _p, _p, _p, _i64, _i32, _i32, _i64, _p, _p, _p, _p]),
     "dgc_rnn_fwd_tc": (_i32, [_i32, _p, _p, _p, _p, _p, _p, _i64, _i32, _i32, _i64, _p, _p, _p, _p]),

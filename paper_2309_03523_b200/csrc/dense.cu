@@ -25,12 +25,13 @@ __global__ void __launch_bounds__(256) softmax_xent_kernel(const float* __restri
     float s = 0.f;
     for (int c = 0; c < C; ++c) s += __expf(x[c] - m);
     const float ls = logf(s);
-    const int y = labels[i];
-    l = -(double)(x[y] - m - ls);
+    const int y = labels[i];  // y < 0: padding row (no loss, no gradient)
+    l = y >= 0 ? -(double)(x[y] - m - ls) : 0.0;
     const float inv = 1.f / s;
     for (int c = 0; c < C; ++c) {
       float p = __expf(x[c] - m) * inv;
       if (c == y) p -= 1.f;
+      if (y < 0) p = 0.f;
       dlogits[i * C + c] = round_out ? dgc::rna_tf32_f(p * scale) : p * scale;
     }
   }

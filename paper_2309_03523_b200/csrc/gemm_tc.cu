@@ -33,7 +33,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                      int kb_total, int kb_per_split, int m_tiles, int n_tiles, int splits,
                      const float* __restrict__ bias, const float* __restrict__ relu_src,
                      int accumulate, float* __restrict__ partial,
-                     float* __restrict__ colsum_partial, int b_res) {
+                     float* __restrict__ colsum_partial, int b_res,
+                     const int32_t* __restrict__ seg_of_mtile, int b_seg_rows,
+                     const int32_t* __restrict__ kitems) {
   // Persistent: CTA c owns tiles c, c+G, ... of the (split, m-tile, n-tile)
   // space, n fastest. With G a multiple of n_tiles every CTA keeps ONE n-tile,
   // so (b_res) its whole B panel is loaded into shared memory once and only A
@@ -94,8 +96,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     z = rest / m_tiles;
     m0 = (int64_t)mt * BM;
     n0 = (int64_t)nt * bn;
-    kb0 = z * kb_per_split;
-    nkb = min(kb_total, kb0 + kb_per_split) - kb0;
+    if (kitems) {  // K-segmented work items (per-snapshot weight gradients)
+      kb0 = kitems[2 * z];
+      nkb = kitems[2 * z + 1];
+    } else {
+      kb0 = z * kb_per_split;
+      nkb = min(kb_total, kb0 + kb_per_split) - kb0;
+    }
   };
 
   if (warp == 0) {
@@ -127,6 +134,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* sb = sa + kABytes;
           mbar_expect_tx(&full[s], (uint32_t)ld_bytes);
           const int k0 = (kb0 + kb) * BK;
+          // row-segmented B (one weight matrix per snapshot block of 128-row tiles)
+          const int boff = seg_of_mtile ? seg_of_mtile[m0 / BM] * b_seg_rows : 0;
           if (!A_MN) {
             tma_load_2d(sa, &tmA, k0, (int)m0, &full[s]);
           } else {
@@ -136,10 +145,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (!b_res) {
             if (!B_MN) {
-              tma_load_2d(sb, &tmB, k0, (int)n0, &full[s]);
+              tma_load_2d(sb, &tmB, k0, (int)n0 + boff, &full[s]);
             } else {
               for (int i = 0; i < bn / 32; ++i)
-                tma_load_2d(sb + i * 4096, &tmB, (int)n0 + 32 * i, k0, &full[s]);
+                tma_load_2d(sb + i * 4096, &tmB, (int)n0 + 32 * i, k0 + boff, &full[s]);
             }
           }
         }
@@ -302,18 +311,43 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ partial, int spli
   }
 }
 
+// out[s] = sum of the partials of segment s's work items, fixed order.
+__global__ void seg_reduce_kernel(const float* __restrict__ partial, const int32_t* __restrict__ item_ptr,
+                                  int n_seg, int64_t M, int64_t N, float* __restrict__ C,
+                                  int64_t ldc) {
+  const int64_t per = M * N;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < per * n_seg;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int sg = (int)(i / per);
+    const int64_t e = i % per, r = e / N, n = e % N;
+    float acc = 0.f;
+    for (int z = item_ptr[sg]; z < item_ptr[sg + 1]; ++z) acc += partial[(int64_t)z * per + e];
+    C[((int64_t)sg * M + r) * ldc + n] = acc;
+  }
+}
+
+struct SegOpts {
+  const int32_t* seg_of_mtile = nullptr;  // row-segmented B
+  int b_seg_rows = 0;
+  int b_nseg = 1;
+  const int32_t* kitems = nullptr;        // K-segmented items (kb0, nkb)
+  int n_kitems = 0;
+  const int32_t* item_ptr = nullptr;      // items of each segment
+  int n_seg = 0;
+};
+
 template <bool A_MN, bool B_MN, bool SPLIT3>
 int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, float* C, int64_t ldc, int64_t M,
                 int64_t N, int bn, int ntiles, int kb_total, int splits, int kb_per,
                 const float* bias, const float* relu_src, int accumulate, float* partial,
-                float* colsum_partial, cudaStream_t s) {
+                float* colsum_partial, const SegOpts& so, cudaStream_t s) {
   const int ab = kABytes + bn * BK * 4;
   const int stage_bytes = ab * (SPLIT3 ? 2 : 1);
   const int budget = 155 * 1024;  // + ~68 KB epilogue staging + barriers <= 227 KB
   // B panel resident in shared memory when one CTA keeps one n-tile and it fits
   const int bres_bytes = kb_total * bn * BK * 4;
-  const int b_res = (!SPLIT3 && splits == 1 && bres_bytes <= 96 * 1024 &&
-                     !getenv("DGC_GEMM_NO_BRES")) ? 1 : 0;
+  const int b_res = (!SPLIT3 && splits == 1 && bres_bytes <= 96 * 1024 && !so.seg_of_mtile &&
+                     !so.kitems && !getenv("DGC_GEMM_NO_BRES")) ? 1 : 0;
   int stages = b_res ? (budget - bres_bytes) / kABytes : budget / stage_bytes;
   stages = stages > 4 ? 4 : stages;
   if (const char* env = getenv("DGC_GEMM_MAX_STAGES")) {
@@ -332,7 +366,8 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, float* C, int64_t 
   if (grid > total) grid = total;
   kern<<<grid, kThreads, smem, s>>>(ma, mb, C, ldc, M, N, bn, stages, kb_total, kb_per, m_tiles,
                                     ntiles, splits, bias, relu_src, accumulate, partial,
-                                    colsum_partial, b_res);
+                                    colsum_partial, b_res, so.seg_of_mtile, so.b_seg_rows,
+                                    so.kitems);
   DGC_CHECK_LAUNCH("gemm_tf32_kernel");
   return DGC_OK;
 }
@@ -347,11 +382,11 @@ extern "C" int dgc_gemm_splits(int64_t K, int32_t precision, int32_t k_splits) {
   return kb_per > 0 ? (kb_total + kb_per - 1) / kb_per : 1;
 }
 
-extern "C" int dgc_gemm_tf32(const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
-                             int64_t ldc, int64_t M, int64_t N, int64_t K, int32_t a_mn,
-                             int32_t b_mn, int32_t precision, const float* bias,
-                             const float* relu_src, int32_t accumulate, int32_t k_splits,
-                             float* partial, float* colsum_partial, void* stream) {
+static int gemm_impl(const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
+                     int64_t ldc, int64_t M, int64_t N, int64_t K, int32_t a_mn, int32_t b_mn,
+                     int32_t precision, const float* bias, const float* relu_src,
+                     int32_t accumulate, int32_t k_splits, float* partial, float* colsum_partial,
+                     const SegOpts& so, void* stream) {
   DGC_REQUIRE(M >= 0 && N >= 0 && K >= 1, "gemm: bad shape");
   DGC_REQUIRE(precision == 1 || precision == 3, "gemm: precision must be 1 (TF32) or 3 (3xTF32)");
   DGC_REQUIRE(k_splits >= 1, "gemm: k_splits >= 1");
@@ -370,37 +405,80 @@ extern "C" int dgc_gemm_tf32(const float* A, int64_t lda, const float* B, int64_
   // and finishes the sum in the round-to-nearest split-K reduction.
   constexpr int kMaxChainKb = 16;
   if (precision == 3 && kb_per > kMaxChainKb) kb_per = kMaxChainKb;
-  const int splits = (kb_total + kb_per - 1) / kb_per;
-  if (splits > 1) DGC_REQUIRE(partial != nullptr, "gemm: k_splits > 1 needs a partial buffer");
+  const int splits = so.kitems ? so.n_kitems : (kb_total + kb_per - 1) / kb_per;
+  if (splits > 1 || so.kitems)
+    DGC_REQUIRE(partial != nullptr, "gemm: split-K / K-segmented items need a partial buffer");
   if (splits > 1) DGC_REQUIRE(colsum_partial == nullptr, "gemm: column sums need k_splits == 1");
   CUtensorMap ma, mb;
   int rc = a_mn ? make_map(&ma, A, K, M, lda, 32, 32, true)
                  : make_map(&ma, A, M, K, lda, 32, BM, false);
   if (rc) return rc;
-  rc = b_mn ? make_map(&mb, B, K, N, ldb, 32, 32, true)
-            : make_map(&mb, B, N, K, ldb, 32, (uint32_t)bn, false);
+  const int64_t nseg = so.b_nseg > 0 ? so.b_nseg : 1;
+  rc = b_mn ? make_map(&mb, B, K * nseg, N, ldb, 32, 32, true)
+            : make_map(&mb, B, N * nseg, K, ldb, 32, (uint32_t)bn, false);
   if (rc) return rc;
-  float* part = splits > 1 ? partial : nullptr;
+  float* part = (splits > 1 || so.kitems) ? partial : nullptr;
   const bool s3 = precision == 3;
+  if (so.kitems && splits == 0) {
+    rc = DGC_OK;
+  } else {
 #define DGC_GEMM_CASE(AM, BMN, S3)                                                               \
   if ((bool)a_mn == AM && (bool)b_mn == BMN && s3 == S3)                                          \
     rc = launch_gemm<AM, BMN, S3>(ma, mb, C, ldc, M, N, bn, ntiles, kb_total, splits, kb_per,   \
                                   part ? nullptr : bias, part ? nullptr : relu_src,              \
-                                  part ? 0 : accumulate, part, colsum_partial, s);
-  DGC_GEMM_CASE(false, false, false)
-  DGC_GEMM_CASE(false, true, false)
-  DGC_GEMM_CASE(true, false, false)
-  DGC_GEMM_CASE(true, true, false)
-  DGC_GEMM_CASE(false, false, true)
-  DGC_GEMM_CASE(false, true, true)
-  DGC_GEMM_CASE(true, false, true)
-  DGC_GEMM_CASE(true, true, true)
+                                  part ? 0 : accumulate, part, colsum_partial, so, s);
+    DGC_GEMM_CASE(false, false, false)
+    DGC_GEMM_CASE(false, true, false)
+    DGC_GEMM_CASE(true, false, false)
+    DGC_GEMM_CASE(true, true, false)
+    DGC_GEMM_CASE(false, false, true)
+    DGC_GEMM_CASE(false, true, true)
+    DGC_GEMM_CASE(true, false, true)
+    DGC_GEMM_CASE(true, true, true)
 #undef DGC_GEMM_CASE
+  }
   if (rc) return rc;
-  if (part) {
+  if (so.kitems) {
+    seg_reduce_kernel<<<dgc::grid_for(M * N * so.n_seg, 256), 256, 0, s>>>(
+        part, so.item_ptr, so.n_seg, M, N, C, ldc);
+    DGC_CHECK_LAUNCH("seg_reduce_kernel");
+  } else if (part) {
     splitk_reduce_kernel<<<dgc::grid_for(M * N, 256), 256, 0, s>>>(part, splits, M, N, C, ldc,
                                                                    bias, relu_src, accumulate);
     DGC_CHECK_LAUNCH("splitk_reduce_kernel");
   }
   return DGC_OK;
+}
+
+extern "C" int dgc_gemm_tf32(const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
+                             int64_t ldc, int64_t M, int64_t N, int64_t K, int32_t a_mn,
+                             int32_t b_mn, int32_t precision, const float* bias,
+                             const float* relu_src, int32_t accumulate, int32_t k_splits,
+                             float* partial, float* colsum_partial, void* stream) {
+  return gemm_impl(A, lda, B, ldb, C, ldc, M, N, K, a_mn, b_mn, precision, bias, relu_src,
+                   accumulate, k_splits, partial, colsum_partial, SegOpts{}, stream);
+}
+
+extern "C" int dgc_gemm_tf32_segmented(const float* A, int64_t lda, const float* B, int64_t ldb,
+                                       float* C, int64_t ldc, int64_t M, int64_t N, int64_t K,
+                                       int32_t a_mn, int32_t b_mn, int32_t precision,
+                                       const float* bias, const float* relu_src,
+                                       const int32_t* seg_of_mtile, int32_t b_nseg,
+                                       const int32_t* kitems, int32_t n_kitems,
+                                       const int32_t* item_ptr, int32_t n_seg, float* partial,
+                                       float* colsum_partial, void* stream) {
+  DGC_REQUIRE(!(seg_of_mtile && kitems), "gemm_segmented: row- and K-segmentation are exclusive");
+  // stacked per-segment B: a 32-row TMA box must not run into the next matrix
+  DGC_REQUIRE(!seg_of_mtile || (b_mn ? K % 32 == 0 : N % 16 == 0),
+              "gemm_segmented: row-segmented B needs K % 32 == 0 (MN-major) / N % 16 == 0");
+  SegOpts so;
+  so.seg_of_mtile = seg_of_mtile;
+  so.b_nseg = b_nseg > 0 ? b_nseg : 1;
+  so.b_seg_rows = seg_of_mtile ? (int)(b_mn ? K : N) : 0;
+  so.kitems = kitems;
+  so.n_kitems = n_kitems;
+  so.item_ptr = item_ptr;
+  so.n_seg = n_seg;
+  return gemm_impl(A, lda, B, ldb, C, ldc, M, N, K, a_mn, b_mn, precision, bias, relu_src, 0, 1,
+                   partial, colsum_partial, so, stream);
 }

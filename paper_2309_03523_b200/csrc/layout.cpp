@@ -132,15 +132,43 @@ void build(const dgc_plan_view& pv, int d, dgc_layout& out) {
     own_key.emplace_back(seg, i);
   }
   std::sort(own_key.begin(), own_key.end());
-  const i64 n_own = (i64)own_key.size();
   auto& own = F[DGC_F_OWN_GID];
   auto& gptr = F[DGC_F_GROUP_PTR];
-  own.resize(n_own);
+  auto& segp = F[DGC_F_SEG_PTR];
   gptr.clear();
-  for (i64 k = 0; k < n_own; ++k) {
-    own[k] = own_key[k].second;
-    if (k == 0 || own_key[k].first != own_key[k - 1].first) gptr.push_back(k);
+  segp.clear();
+  own.clear();
+  if (pv.segment_rows > 0) {
+    // EvolveGCN (per-snapshot weights): rows grouped by snapshot, each snapshot
+    // block padded with -1 rows to a multiple of segment_rows so every GEMM
+    // M-tile lies in one snapshot. Fusion groups of such plans are
+    // snapshot-local, so a group stays one contiguous segment.
+    i64 T = 0;
+    for (i64 i = 0; i < N; ++i) T = std::max<i64>(T, pv.inst_t[i]);
+    std::stable_sort(own_key.begin(), own_key.end(), [&](const std::pair<i64, i64>& a,
+                                                         const std::pair<i64, i64>& b) {
+      return pv.inst_t[a.second] < pv.inst_t[b.second];
+    });
+    size_t k = 0;
+    for (i64 t = 1; t <= T; ++t) {
+      segp.push_back((i64)own.size());
+      i64 prev_seg = -1;
+      while (k < own_key.size() && pv.inst_t[own_key[k].second] == t) {
+        if (own_key[k].first != prev_seg) gptr.push_back((i64)own.size());
+        prev_seg = own_key[k].first;
+        own.push_back(own_key[k].second);
+        ++k;
+      }
+      while (own.size() % (size_t)pv.segment_rows) own.push_back(-1);
+    }
+    segp.push_back((i64)own.size());
+  } else {
+    for (size_t k = 0; k < own_key.size(); ++k) {
+      own.push_back(own_key[k].second);
+      if (k == 0 || own_key[k].first != own_key[k - 1].first) gptr.push_back((i64)k);
+    }
   }
+  const i64 n_own = (i64)own.size();
   gptr.push_back(n_own);
   // global adjacency (neighbours sorted by gid) and degrees
   const i64 E = pv.n_spatial_edges;
@@ -162,12 +190,15 @@ void build(const dgc_plan_view& pv, int d, dgc_layout& out) {
   }
   // local ids: own then halo (ascending gid)
   std::vector<i64> local(N, -1);
-  for (i64 k = 0; k < n_own; ++k) local[own[k]] = k;
+  for (i64 k = 0; k < n_own; ++k)
+    if (own[k] >= 0) local[own[k]] = k;
   auto& halo = F[DGC_F_HALO_GID];
   halo.clear();
-  for (i64 k = 0; k < n_own; ++k)
+  for (i64 k = 0; k < n_own; ++k) {
+    if (own[k] < 0) continue;
     for (i64 e = adj_ptr[own[k]]; e < adj_ptr[own[k] + 1]; ++e)
       if (sdev[adj[e]] != d) halo.push_back(adj[e]);
+  }
   std::sort(halo.begin(), halo.end());
   halo.erase(std::unique(halo.begin(), halo.end()), halo.end());
   const i64 n_halo = (i64)halo.size();
@@ -178,7 +209,7 @@ void build(const dgc_plan_view& pv, int d, dgc_layout& out) {
   deg.resize(n_loc);
   for (i64 c = 0; c < n_loc; ++c) {
     const i64 g = c < n_own ? own[c] : halo[c - n_own];
-    deg[c] = adj_ptr[g + 1] - adj_ptr[g];
+    deg[c] = g >= 0 ? adj_ptr[g + 1] - adj_ptr[g] : 0;  // padding rows: no entries
   }
   // forward CSR with self loop, columns by neighbour gid
   auto& rp = F[DGC_F_ROW_PTR];
@@ -187,6 +218,10 @@ void build(const dgc_plan_view& pv, int d, dgc_layout& out) {
   col.clear();
   for (i64 k = 0; k < n_own; ++k) {
     const i64 u = own[k];
+    if (u < 0) {  // padding row: empty
+      rp.push_back((i64)col.size());
+      continue;
+    }
     bool self_done = false;
     for (i64 e = adj_ptr[u]; e < adj_ptr[u + 1]; ++e) {
       if (!self_done && adj[e] > u) {
@@ -214,7 +249,9 @@ void build(const dgc_plan_view& pv, int d, dgc_layout& out) {
       for (i64 e = rp[k]; e < rp[k + 1]; ++e) tcol[fill[col[e]]++] = k;
   }
   // boundary keys (ascending gid) and per-peer lists
-  std::vector<i64> own_sorted(own.begin(), own.end());
+  std::vector<i64> own_sorted;
+  for (i64 g : own)
+    if (g >= 0) own_sorted.push_back(g);
   std::sort(own_sorted.begin(), own_sorted.end());
   auto& keys = F[DGC_F_KEY_ROWS];
   keys.clear();
@@ -353,6 +390,7 @@ void build(const dgc_plan_view& pv, int d, dgc_layout& out) {
       };
       for (i64 k = gptr[gi]; k < gptr[gi + 1]; ++k) {
         const i64 g = own[k];
+        if (g < 0) continue;
         mark(g);
         for (i64 e = adj_ptr[g]; e < adj_ptr[g + 1]; ++e) mark(adj[e]);
         if (pred[g] >= 0) mark(pred[g]);

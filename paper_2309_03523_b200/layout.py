@@ -13,7 +13,7 @@ from .plan import PlanArrays, PlanGraphMismatch
 FIELDS = ["own_gid", "halo_gid", "group_ptr", "row_ptr", "col", "deg", "t_row_ptr", "t_col",
           "key_rows", "send_ptr", "send_pos", "recv_ptr", "recv_slot", "run_ptr", "run_rows",
           "run_pred_gid", "run_carry", "slot_row", "slot_mask", "slot_carry", "tkey_rows",
-          "tsend_ptr", "tsend_pos", "trecv_ptr", "trecv_carry", "scalars", "key_ncut"]
+          "tsend_ptr", "tsend_pos", "trecv_ptr", "trecv_carry", "scalars", "key_ncut", "seg_ptr"]
 
 
 @dataclass
@@ -68,12 +68,17 @@ class DeviceLayout:
     def dinv(self):
         return (1.0 / np.sqrt(self.arrays["deg"].astype(np.float64) + 1.0))
 
+    @property
+    def real_rows(self):
+        """mask of own rows that are instances (False on snapshot padding rows)"""
+        return self.arrays["own_gid"] >= 0
+
 
 def _ptr(a):
     return a.ctypes.data_as(C.c_void_p) if a is not None else None
 
 
-def build_layout(pa: PlanArrays, device: int) -> DeviceLayout:
+def build_layout(pa: PlanArrays, device: int, segment_rows: int = 0) -> DeviceLayout:
     pa.validate()
     lib = _native.lib()
     keep = dict(e=np.ascontiguousarray(pa.inst_entity, np.int32),
@@ -97,6 +102,7 @@ def build_layout(pa: PlanArrays, device: int) -> DeviceLayout:
         pv.group_device, pv.group_ptr, pv.group_chunks = _ptr(keep["gd"]), _ptr(keep["gp"]), _ptr(keep["gc"])
     else:
         pv.n_groups = 0
+    pv.segment_rows = int(segment_rows)
     handle = C.c_void_p()
     rc = lib.dgc_layout_build(C.byref(pv), device, C.byref(handle))
     if rc == -3:

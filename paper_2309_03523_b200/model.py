@@ -26,6 +26,8 @@ class DGNNConfig:
     rnn: str = "gru"
     n_rnn: int = 1
     precision: str = "fp32"     # "fp32": 3xTF32 GEMMs (parity); "tf32": 1-pass TF32 (perf)
+    model: str = "rnn"          # "rnn": GCN + GRU/LSTM; "evolve": EvolveGCN-O (C3)
+    T: int = 0                  # snapshots (EvolveGCN weight evolution length)
     optimizer: str = "adam"
     lr: float = 0.01
     momentum: float = 0.9
@@ -47,15 +49,28 @@ class DGNNConfig:
         if profile.get("spatial_msgs_per_block", 2) != 2 or profile.get("blocks", 1) != 1:
             raise ValueError("only the 1-block, 2-GCN-layer profiles of C1/C2 are modelled")
         n_rnn = int(profile.get("temporal_msgs_per_block", 1))
-        if n_rnn < 1:
-            raise ValueError("temporal_msgs_per_block = 0 (EvolveGCN) is not modelled yet")
         H = H if H is not None else int(profile.get("embedding_dim", 16))
+        if n_rnn == 0:
+            # EvolveGCN-style (ModelProfile(1,2,0)): per-snapshot GCN weights from a
+            # weight GRU, no vertex-level temporal messages
+            return cls(F=F, H=H, C=C, rnn="gru", n_rnn=0, model="evolve", **kw)
         rnn = "gru" if n_rnn == 1 else "lstm"
         return cls(F=F, H=H, C=C, rnn=rnn, n_rnn=n_rnn, **kw)
 
 
+EVOLVE_KEYS = ("Sr", "Sz", "Pc", "Qc", "Br", "Bz", "Bc")
+
+
 def param_shapes(cfg: DGNNConfig):
     H, G = cfg.H, cfg.G
+    if cfg.model == "evolve":
+        shapes = []
+        for l, Fl in ((1, cfg.F), (2, H)):
+            shapes.append((f"W{l}_0", (Fl, H), Fl))
+            for k in EVOLVE_KEYS:
+                shapes.append((f"{k}{l}", (Fl, Fl) if k[0] in "SPQ" else (Fl, H), Fl))
+            shapes.append((f"b{l}", (H,), H))
+        return shapes + [("Wo", (H, cfg.C), H), ("bo", (cfg.C,), H)]
     shapes = [("W1", (cfg.F, H), cfg.F), ("b1", (H,), H), ("W2", (H, H), H), ("b2", (H,), H)]
     for k in range(cfg.n_rnn):
         shapes += [(f"Wx{k}", (H, G * H), H), (f"U{k}", (H, G * H), H), (f"br{k}", (G * H,), H)]

@@ -117,6 +117,42 @@ def gemm(A, B, C, M, N, K, *, a_mn=False, b_mn=True, lda=None, ldb=None, ldc=Non
     return C
 
 
+def gemm_segmented(A, B, C, M, N, K, *, a_mn=False, b_mn=True, lda=None, ldb=None, ldc=None,
+                   precision=3, bias=None, relu_src=None, seg_of_mtile=None, b_nseg=1,
+                   kitems=None, n_kitems=0, item_ptr=None, n_seg=0, partial=None,
+                   colsum_partial=None):
+    """K2 for per-snapshot weights (dgc_gemm_tf32_segmented)."""
+    lda = lda if lda is not None else (M if a_mn else K)
+    ldb = ldb if ldb is not None else (N if b_mn else K)
+    ldc = ldc if ldc is not None else N
+    nb = 4 * (M * K + K * N * max(b_nseg, 1) + M * N * max(1, n_seg))
+    gname = "gemm_seg_tf32" if precision == 1 else "gemm_seg_3xtf32"
+    if _prof_detail:
+        gname += f"[{M}x{N}x{K} a{int(a_mn)}b{int(b_mn)} {'K' if kitems is not None else 'M'}]"
+    _run(gname, lambda: _native.check(_native.lib().dgc_gemm_tf32_segmented(
+        _p(A), lda, _p(B), ldb, _p(C), ldc, M, N, K, int(a_mn), int(b_mn), precision, _p(bias),
+        _p(relu_src), _p(seg_of_mtile), int(b_nseg), _p(kitems), int(n_kitems), _p(item_ptr),
+        int(n_seg), _p(partial), _p(colsum_partial), _stream()), "dgc_gemm_tf32_segmented"),
+        nb, 2.0 * M * N * K, 1 + int(kitems is not None))
+    return C
+
+
+def evolve_fwd(Fl, Hl, T, W0, SrT, SzT, PcT, QcT, Br, Bz, Bc, Wstack, sv, rnd=False):
+    """EvolveGCN-O weight evolution forward (dgc_evolve_fwd); sv = (r, z, c, w, rw)."""
+    _run("evolve_fwd", lambda: _native.check(_native.lib().dgc_evolve_fwd(
+        Fl, Hl, T, _p(W0), _p(SrT), _p(SzT), _p(PcT), _p(QcT), _p(Br), _p(Bz), _p(Bc),
+        _p(Wstack), *[_p(x) for x in sv], int(rnd), _stream()), "dgc_evolve_fwd"),
+        4 * T * Fl * Hl * 6 + 16 * T * Fl * Fl, 8.0 * T * Fl * Fl * Hl)
+
+
+def evolve_bwd(Fl, Hl, T, Sr, Sz, Pc, Qc, sv, dW_direct, dW0, da, dB, rnd=False):
+    """EvolveGCN-O weight evolution BPTT (dgc_evolve_bwd); da/dB = (r, z, c) triples."""
+    _run("evolve_bwd", lambda: _native.check(_native.lib().dgc_evolve_bwd(
+        Fl, Hl, T, _p(Sr), _p(Sz), _p(Pc), _p(Qc), *[_p(x) for x in sv[:4]], _p(dW_direct),
+        _p(dW0), *[_p(x) for x in da], *[_p(x) for x in dB], int(rnd), _stream()),
+        "dgc_evolve_bwd"), 4 * T * Fl * Hl * 8 + 16 * T * Fl * Fl, 8.0 * T * Fl * Fl * Hl)
+
+
 def gemm_splits(K, precision, k_splits):
     """Split count dgc_gemm_tf32 will use for a K-long contraction."""
     return _native.lib().dgc_gemm_splits(K, precision, k_splits)

@@ -71,8 +71,12 @@ def _i32(x):
 
 
 def load_plan_npz(path) -> PlanArrays:
-    z = np.load(path)
+    z = dict(np.load(path))
     meta = json.loads(bytes(z["meta"]).decode())
+    if "graph_npz" in meta:  # plans of one graph share a graph file (artifacts/<g>_graph.npz)
+        g = np.load(Path(path).parent.parent / meta["graph_npz"])
+        for k in ("inst_entity", "inst_t", "spatial_edges", "temporal_links"):
+            z[k] = g[k]
     fused = bool(meta.get("fused")) and len(z["group_device"]) > 0
     pa = PlanArrays(
         T=int(meta["T"]), feature_dim=int(meta["feature_dim"]),

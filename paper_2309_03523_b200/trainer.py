@@ -117,9 +117,13 @@ class Shard:
         self.tsend_pos = {p: _dev_i32(lay.tsend_pos[tsp[p]:tsp[p + 1]], dev) for p in peers}
         self.tsend_rows = {p: _dev_i32(lay.tkey_rows[lay.tsend_pos[tsp[p]:tsp[p + 1]]], dev) for p in peers}
         self.trecv_carry = {p: _dev_i32(lay.trecv_carry[trp[p]:trp[p + 1]], dev) for p in peers}
-        # data
-        self.X = torch.as_tensor(X[lay.own_gid], device=dev).contiguous()
-        self.y = torch.as_tensor(y[lay.own_gid].astype(np.int32), device=dev)
+        # data (snapshot padding rows of EvolveGCN layouts: zero features, label -1)
+        real = lay.own_gid >= 0
+        gid = np.maximum(lay.own_gid, 0)
+        self.X = torch.as_tensor(np.where(real[:, None], X[gid], 0).astype(np.float32),
+                                 device=dev).contiguous()
+        self.y = torch.as_tensor(np.where(real, y[gid], -1).astype(np.int32), device=dev)
+        self.n_real = int(real.sum())
         # parameters (flat) and optimizer state
         self.offs, P = flat_offsets(cfg)
         self.params = torch.zeros(P, dtype=torch.float32, device=dev)
@@ -183,11 +187,51 @@ class Shard:
         self.stale_on = stale_on
         self.scache = [EmbeddingCacheGPU(len(lay.key_rows), H, dev) for _ in range(2)] if stale_on else None
         self.tcache = [EmbeddingCacheGPU(len(lay.tkey_rows), self.hw, dev) for _ in range(cfg.n_rnn)] if stale_on else None
+        self.evolve = cfg.model == "evolve"
+        if self.evolve:
+            self._init_evolve(lay, cfg, dev)
         self.compact_idx = torch.zeros(max(1, len(lay.key_rows), len(lay.tkey_rows)), dtype=torch.int32, device=dev)
         self.fresh = [{} for _ in range(2)]  # layer -> {peer: (recv idx tensor)}
         self.sent = [{} for _ in range(2)]   # layer -> {peer: (send idx tensor or None, count)}
         self.step_count = 0
         self.events = None
+
+    def _init_evolve(self, lay, cfg, dev):
+        """Per-snapshot weight machinery of EvolveGCN-O (C3)."""
+        H, T = cfg.H, cfg.T
+        f32 = dict(dtype=torch.float32, device=dev)
+        seg = lay.seg_ptr.astype(np.int64)
+        assert len(seg) == T + 1, (len(seg), T)
+        m_tiles = max(1, self.n // 128)
+        tile_seg = np.zeros(m_tiles, np.int32)
+        for t in range(T):
+            tile_seg[seg[t] // 128:seg[t + 1] // 128] = t
+        self.seg_of_mtile = torch.as_tensor(tile_seg, device=dev)
+        # K-segmented work items for dW_t = X_t^T dY_t (chain <= 16 k-blocks in fp32 mode)
+        cap = 16 if self.prec == 3 else 1 << 30
+        items, item_ptr = [], [0]
+        for t in range(T):
+            kb0, kb1 = seg[t] // 32, seg[t + 1] // 32
+            for a in range(kb0, kb1, cap):
+                items.append((a, min(cap, kb1 - a)))
+            item_ptr.append(len(items))
+        self.kitems = torch.as_tensor(np.asarray(items, np.int32).reshape(-1), device=dev)
+        self.n_kitems = len(items)
+        self.item_ptr = torch.as_tensor(np.asarray(item_ptr, np.int32), device=dev)
+        Fmax = max(cfg.F, H)
+        self.evo_partial = torch.zeros(max(1, self.n_kitems) * Fmax * H, **f32)
+        self.evo = []
+        for Fl in (cfg.F, H):
+            e = dict(Fl=Fl,
+                     Wstack=torch.zeros(((T + 1) * Fl, H), **f32),
+                     sv=[torch.zeros((Fl, T * H), **f32) for _ in range(5)],  # r z c w rw
+                     gT=[torch.zeros((Fl, Fl), **f32) for _ in range(4)],      # SrT SzT PcT QcT
+                     dW_direct=torch.zeros((T * Fl, H), **f32),
+                     da=[torch.zeros((Fl, T * H), **f32) for _ in range(3)])
+            self.evo.append(e)
+        self.evo_gsplit = max(1, min(64, (T * H) // 128))
+        self.evo_gpartial = torch.zeros(
+            ops.gemm_splits(T * H, self.prec, self.evo_gsplit) * Fmax * Fmax, **f32)
 
     def p(self, name):
         o, shape = self.offs[name]
@@ -273,10 +317,22 @@ class Shard:
         info = {"theta": {}, "d_r": {}, "billed_sp": 0, "billed_tm": 0, "rows": 0}
         D = self.D
         # ---------------- forward: structure encoder ----------------
+        if self.evolve:  # EvolveGCN-O: W_t for every snapshot, per layer
+            for l, e in enumerate(self.evo, start=1):
+                for gi, k in enumerate(("Sr", "Sz", "Pc", "Qc")):
+                    ops.transpose(self.p(f"{k}{l}"), e["gT"][gi])
+                ops.evolve_fwd(e["Fl"], H, cfg.T, self.p(f"W{l}_0"), *e["gT"], self.p(f"Br{l}"),
+                               self.p(f"Bz{l}"), self.p(f"Bc{l}"), e["Wstack"], e["sv"],
+                               rnd=self.tf32)
         hin, ldin, kin = self.X, cfg.F, cfg.F
         for l, (W, b) in enumerate((("W1", "b1"), ("W2", "b2"))):
             Y = self.Yext[l]
-            ops.gemm(hin, self.pr(W), Y, n, H, kin, lda=ldin, precision=self.prec_gcn)
+            if self.evolve:
+                e = self.evo[l]
+                ops.gemm_segmented(hin, e["Wstack"][kin:], Y, n, H, kin, lda=ldin, precision=prec,
+                                   seg_of_mtile=self.seg_of_mtile, b_nseg=cfg.T)
+            else:
+                ops.gemm(hin, self.pr(W), Y, n, H, kin, lda=ldin, precision=self.prec_gcn)
             if D > 1:
                 cache = self.scache[l] if self.stale_on else None
                 if cache is not None:
@@ -295,7 +351,7 @@ class Shard:
             hin, ldin, kin = self.Hl[l], H, H
         # ---------------- forward: time encoder ----------------
         xr, ldx = self.Hl[1], H
-        for k in range(cfg.n_rnn):
+        for k in range(cfg.n_rnn if not self.evolve else 0):
             ops.gemm(xr, self.pr(f"Wx{k}"), self.gx, n, GH, H, lda=ldx, precision=prec,
                      bias=self.p(f"br{k}"))
             hb = self.hbuf[k]
@@ -336,9 +392,14 @@ class Shard:
         ops.gemm(xr, self.dlogits, self.g("Wo"), H, cfg.C, n, a_mn=True, lda=ldx, precision=prec,
                  k_splits=ks, partial=part)
         ops.reduce_rows(self.dl_partial, max(1, (n + 255) // 256), cfg.C, self.g("bo"))
-        ops.gemm(self.dlogits, self.pr("Wo"), self.dh, n, H, cfg.C, b_mn=False, ldb=cfg.C,
-                 precision=prec)
-        for k in reversed(range(cfg.n_rnn)):
+        if self.evolve:  # no time encoder: dZ2 = (dlogits Wo^T) * (H2 > 0), b2 fused
+            ops.gemm(self.dlogits, self.pr("Wo"), self.dh, n, H, cfg.C, b_mn=False, ldb=cfg.C,
+                     precision=prec, relu_src=self.Hl[1], colsum_partial=self.bias_partial)
+            ops.reduce_rows(self.bias_partial, 4 * self.m_tiles, H, self.g("b2"))
+        else:
+            ops.gemm(self.dlogits, self.pr("Wo"), self.dh, n, H, cfg.C, b_mn=False, ldb=cfg.C,
+                     precision=prec)
+        for k in reversed(range(cfg.n_rnn if not self.evolve else 0)):
             if self.tc_rnn:
                 ops.rnn_bwd_tc(cell | rflag, self.pr(f"U{k}"), self.slot_row, self.slot_mask,
                                self.R, self.L, H, self.save[k], self.dh, self.dgx,
@@ -377,6 +438,20 @@ class Shard:
             if D > 1:
                 yield from self._exchange_back(l, self.dYext, H)
             hin_l, ldin_l, kin_l = (self.X, cfg.F, cfg.F) if l == 0 else (self.Hl[0], H, H)
+            if self.evolve:
+                e = self.evo[l]
+                ops.gemm_segmented(hin_l, self.dYext, e["dW_direct"], kin_l, H, n, a_mn=True,
+                                   lda=ldin_l, ldb=H, precision=prec, kitems=self.kitems,
+                                   n_kitems=self.n_kitems, item_ptr=self.item_ptr, n_seg=cfg.T,
+                                   partial=self.evo_partial)
+                if l == 1:
+                    ops.gemm_segmented(self.dYext, e["Wstack"][kin_l:], self.dh2, n, H, H,
+                                       b_mn=False, ldb=H, precision=prec, relu_src=self.Hl[0],
+                                       seg_of_mtile=self.seg_of_mtile, b_nseg=cfg.T,
+                                       colsum_partial=self.bias_partial)
+                    ops.reduce_rows(self.bias_partial, 4 * self.m_tiles, H, self.g("b1"))
+                    dZ = self.dh2
+                continue
             ops.gemm(hin_l, self.dYext, self.g(W), kin_l, H, n, a_mn=True, lda=ldin_l, ldb=H,
                      precision=prec, k_splits=ks, partial=part)
             if l == 1:
@@ -384,6 +459,18 @@ class Shard:
                          precision=prec, relu_src=self.Hl[0], colsum_partial=self.bias_partial)
                 ops.reduce_rows(self.bias_partial, 4 * self.m_tiles, H, self.g("b1"))
                 dZ = self.dh2
+        if self.evolve:  # BPTT through the weight evolution, gate-matrix grads by K2
+            for l, e in enumerate(self.evo, start=1):
+                Fl, TH = e["Fl"], cfg.T * H
+                ops.evolve_bwd(Fl, H, cfg.T, self.pr(f"Sr{l}"), self.pr(f"Sz{l}"),
+                               self.pr(f"Pc{l}"), self.pr(f"Qc{l}"), e["sv"], e["dW_direct"],
+                               self.g(f"W{l}_0"), e["da"],
+                               (self.g(f"Br{l}"), self.g(f"Bz{l}"), self.g(f"Bc{l}")),
+                               rnd=self.tf32)
+                for k, da, op in (("Sr", e["da"][0], e["sv"][3]), ("Sz", e["da"][1], e["sv"][3]),
+                                  ("Pc", e["da"][2], e["sv"][3]), ("Qc", e["da"][2], e["sv"][4])):
+                    ops.gemm(da, op, self.g(f"{k}{l}"), Fl, Fl, TH, b_mn=False, ldb=TH,
+                             precision=prec, k_splits=self.evo_gsplit, partial=self.evo_gpartial)
         # ---------------- gradient all-reduce + update ----------------
         if D > 1:
             yield ("sum", self.grads)
@@ -536,7 +623,10 @@ class DGNNTrainer:
         else:
             ranks = list(range(pa.n_devices))
             self.runner = LocalRunner()
-        self.layouts = [build_layout(pa, d) for d in ranks]
+        seg_rows = 128 if cfg.model == "evolve" else 0
+        if cfg.model == "evolve" and cfg.T == 0:
+            cfg.T = int(pa.inst_t.max())
+        self.layouts = [build_layout(pa, d, segment_rows=seg_rows) for d in ranks]
         self.shards = [Shard(pa, lay, cfg, self.params0, X, y, self.stale, pa.n_instances,
                              self.device) for lay in self.layouts]
         prof = pa.profile or {}

@@ -119,3 +119,32 @@ def test_trainer_tf32_tensor_core_path(artifacts_dir, name, H):
             else:
                 err = np.abs(g - ref).max() / np.abs(ref).max()
                 assert err <= 2e-2, f"epoch {rep.epoch} grad {k}: {err:.2e}"
+
+
+@pytest.mark.parametrize("precision,tol", [("fp32", 1e-4), ("tf32", 5e-2)])
+def test_trainer_evolvegcn_matches_oracle(artifacts_dir, precision, tol):
+    """C3 model (EvolveGCN-O weight evolution + per-snapshot GCN on snapshot-
+    segmented layouts) on the reference's 2-device EvolveGCN plan vs the oracle."""
+    from paper_2309_03523_b200 import DGNNConfig, load_plan_npz
+    from paper_2309_03523_b200.model import init_params, synthetic_inputs
+    from paper_2309_03523_b200.trainer import DGNNTrainer
+    pa = load_plan_npz(artifacts_dir / "e2" / "plan.npz")
+    T = int(pa.inst_t.max())
+    cfg = DGNNConfig(F=32, H=32, C=8, model="evolve", n_rnn=0, T=T, optimizer="sgd", lr=0.05,
+                     precision=precision)
+    X, y = synthetic_inputs(pa.n_instances, cfg.F, cfg.C, 0)
+    params = init_params(cfg, 0)
+    tr = DGNNTrainer(pa, cfg, None, features=X, labels=y, params=params)
+    lays = build_layouts(pa.n_instances, pa.inst_entity, pa.inst_t, pa.spatial_edges,
+                         pa.temporal_links, pa.structure_device, pa.chunk_of, pa.n_devices,
+                         pa.group_device, pa.group_ptr, pa.group_chunks)
+    ocfg = OracleConfig(F=32, H=32, C=8, model="evolve", T=T, n_rnn=0, optimizer="sgd", lr=0.05)
+    orc = OracleDGNN(lays, X, y, params, ocfg, inst_t=pa.inst_t)
+    for r in (1, 2, 3):
+        rep = tr.run_epoch()
+        o = orc.epoch(r)
+        assert rep.loss == pytest.approx(o["loss"], rel=tol)
+        for k, g in tr.grads(0).items():
+            ref = o["grads"][k]
+            err = np.linalg.norm(g - ref) / max(np.linalg.norm(ref), 1e-30)
+            assert err <= tol, f"epoch {r} grad {k}: {err:.2e}"

@@ -106,3 +106,28 @@ def test_stale_schedule_first_epoch_sends_all(t2):
     for e in (e2, e3):
         assert e["theta"]["s0"] <= e["d_r"]["s0"] + 1e-15
         assert e["d_r"]["s0"] > 0
+
+
+def test_oracle_evolvegcn_gradients_finite_difference(artifacts_dir):
+    """EvolveGCN-O oracle (C3 model): directional finite differences through the
+    weight evolution, the per-snapshot GCN and the partitioned exchange."""
+    from paper_2309_03523_b200.model import DGNNConfig, init_params as pinit
+    z, meta = load_plan(artifacts_dir / "e2" / "plan.npz")
+    lays = layouts_for(z, meta)
+    T = int(meta["T"])
+    cfg = OracleConfig(F=6, H=5, C=4, model="evolve", T=T, n_rnn=0, lr=0.0)
+    pc = DGNNConfig(F=6, H=5, C=4, model="evolve", n_rnn=0, T=T)
+    n = len(z["inst_entity"])
+    rng = np.random.default_rng(7)
+    X = rng.normal(size=(n, cfg.F))
+    y = rng.integers(0, cfg.C, size=n)
+    p0 = {k: v.astype(np.float64) for k, v in pinit(pc, 1).items()}
+    base = OracleDGNN(lays, X, y, p0, cfg, inst_t=z["inst_t"]).epoch(1)
+    for trial in range(3):
+        v = {k: rng.normal(size=np.shape(a)) for k, a in p0.items()}
+        eps = 1e-6
+        lp = OracleDGNN(lays, X, y, {k: p0[k] + eps * v[k] for k in p0}, cfg, inst_t=z["inst_t"]).epoch(1)["loss"]
+        lm = OracleDGNN(lays, X, y, {k: p0[k] - eps * v[k] for k in p0}, cfg, inst_t=z["inst_t"]).epoch(1)["loss"]
+        fd = (lp - lm) / (2 * eps)
+        an = sum(float((base["grads"][k] * v[k]).sum()) for k in p0)
+        assert fd == pytest.approx(an, rel=1e-6, abs=1e-10)

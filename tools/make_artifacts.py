@@ -43,6 +43,17 @@ CONFIGS = {
                  profile=ModelProfile(1, 2, 2, "previous-only", 16, 4), fuse=False),
     "c2d8": dict(N=200_000, T=32, sigma_mult=1.0, D=8, F=16,
                  profile=ModelProfile(1, 2, 2, "previous-only", 16, 4), fuse=False),
+    # C3: EvolveGCN-style profile ModelProfile(1,2,0): no vertex-level temporal
+    # messages, so chunks are snapshot-local
+    "c3d2": dict(N=1_000_000, T=64, sigma_mult=1.0, D=2, F=16,
+                 profile=ModelProfile(1, 2, 0, "previous-only", 16, 4), fuse="native"),
+    "c3d4": dict(N=1_000_000, T=64, sigma_mult=1.0, D=4, F=16,
+                 profile=ModelProfile(1, 2, 0, "previous-only", 16, 4), fuse="native"),
+    "c3d8": dict(N=1_000_000, T=64, sigma_mult=1.0, D=8, F=16,
+                 profile=ModelProfile(1, 2, 0, "previous-only", 16, 4), fuse="native"),
+    # small EvolveGCN plans for the parity tests
+    "e2": dict(N=3_000, T=8, sigma_mult=1.0, D=2, F=16,
+               profile=ModelProfile(1, 2, 0, "previous-only", 16, 4), fuse=True),
     # small multi-device variants used by the parity tests (fast to plan)
     "t2": dict(N=3_000, T=8, sigma_mult=1.0, D=2, F=16,
                profile=ModelProfile(1, 2, 1, "previous-only", 16, 4), fuse=True),
@@ -137,6 +148,34 @@ def build(name: str) -> None:
     print(f"[{name}] wrote {out}", flush=True)
 
 
+
+
+def share_graphs(groups=(("c2", ("c2", "c2d2", "c2d4", "c2d8")), ("c3", ("c3d2", "c3d4", "c3d8")))):
+    """Plans of one graph share artifacts/<g>_graph.npz (the graph arrays); each
+    plan.npz keeps only the plan arrays and names its graph file in meta."""
+    import hashlib
+    gkeys = ["inst_entity", "inst_t", "spatial_edges", "temporal_links"]
+    for gname, members in groups:
+        ref = None
+        for m in members:
+            p = ROOT / "artifacts" / m / "plan.npz"
+            if not p.exists():
+                continue
+            z = dict(np.load(p))
+            if "inst_entity" not in z:
+                continue  # already split
+            h = hashlib.sha1(b"".join(z[k].tobytes() for k in gkeys)).hexdigest()
+            if ref is None:
+                ref = h
+                np.savez_compressed(ROOT / "artifacts" / f"{gname}_graph.npz", **{k: z[k] for k in gkeys})
+            assert h == ref, (m, "graph differs")
+            meta = json.loads(bytes(z["meta"]).decode())
+            meta.update(graph_npz=f"{gname}_graph.npz", graph_sha1=h)
+            rest = {k: v for k, v in z.items() if k not in gkeys and k != "meta"}
+            np.savez_compressed(p, meta=np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8), **rest)
+
+
 if __name__ == "__main__":
     for n in sys.argv[1:]:
         build(n)
+    share_graphs()
