@@ -251,6 +251,229 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Forward, 2-CTA cluster variant: the two CTAs of a cluster share one 128-row
+// tile and each owns HALF of the hidden units (all four gates of them), so the
+// epilogue-bound recurrence runs on twice the SMs. Each CTA's MMA computes its
+// 2H gate columns from the FULL h tile; the epilogues write their h halves into
+// both CTAs' A tiles (DSMEM st.shared::cluster) and arrive on both CTAs'
+// a_full; MMA completion is multicast to both CTAs' acc_full, so neither
+// epilogue overwrites an h tile the partner's MMA is still reading.
+template <int H>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    lstm_fwd_tc2_kernel(const __grid_constant__ CUtensorMap tmUt, const float* __restrict__ gx,
+                        const int32_t* __restrict__ slot_row, const uint8_t* __restrict__ slot_mask,
+                        const int32_t* __restrict__ slot_carry, const float* __restrict__ carry,
+                        int64_t R, int L, int64_t ld, float* __restrict__ h_out,
+                        float* __restrict__ c_out, float* __restrict__ save) {
+  constexpr int G4 = 4 * H;
+  constexpr int HU = H / 2;                  // units owned by this CTA
+  constexpr int NP = 4 * HU;                 // MMA N: 4 gates x HU units (<= 256)
+  constexpr int KB = H / BK;
+  constexpr int kABytes = KB * BM * 128;
+  constexpr int kBStage = NP * 128;
+  constexpr int kUnits = HU / 2;             // units per epilogue warp (2 warps per quadrant)
+  constexpr uint32_t kTmemCols = NP <= 128 ? 128 : 256;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kABytes;
+  float* stg_all = reinterpret_cast<float*>(sB + kStages * kBStage);
+  uint64_t* b_full = reinterpret_cast<uint64_t*>(stg_all + kEpiWarps * kStgFloats);
+  uint64_t* b_empty = b_full + kStages;
+  uint64_t* a_full = b_empty + kStages;
+  uint64_t* acc_full = a_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_rank(), peer = crank ^ 1u;
+  const int64_t row0 = (int64_t)(blockIdx.x >> 1) * BM;
+  const int u0 = (int)crank * HU;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&b_full[s], 1);
+      mbar_init(&b_empty[s], 1);
+    }
+    mbar_init(a_full, 2 * kEpiThreads);  // local + partner epilogue threads
+    mbar_init(acc_full, 2);              // both CTAs' MMAs (multicast commit)
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmUt) : "memory");
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+  fence_before();
+  __syncthreads();
+  cluster_sync_all();  // barriers of both CTAs initialised before any remote access
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int g = 0; g < L * KB; ++g) {
+        const int s = g % kStages;
+        mbar_wait(&b_empty[s], ((g / kStages) & 1) ^ 1);
+        const int kb = g % KB;
+        mbar_expect_tx(&b_full[s], (uint32_t)kBStage);
+#pragma unroll
+        for (int gi = 0; gi < 4; ++gi)  // U^T rows of gate gi, this CTA's units
+          tma_load_2d(sB + s * kBStage + gi * HU * 128, &tmUt, kb * BK, gi * H + u0, &b_full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = idesc_tf32(NP, false, false);
+    const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+    for (int p = 0; p < L; ++p) {
+      mbar_wait_cluster(a_full, p & 1);
+      fence_after();
+      for (int kb = 0; kb < KB; ++kb) {
+        const int g = p * KB + kb;
+        const int s = g % kStages;
+        mbar_wait(&b_full[s], (g / kStages) & 1);
+        fence_after();
+        if (lane == 0) {
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk)
+            mma_tf32(tmem_base, kdesc(a_base + kb * BM * 128 + kk * 32),
+                     kdesc(b_base + s * kBStage + kk * 32), idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&b_empty[s]);
+          if (kb == KB - 1) mma_commit_mc(acc_full, (uint16_t)0x3);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    const int ew = warp - 2;
+    const int q = warp & 3;
+    const int ul0 = (ew >> 2) * kUnits;     // local unit range of this warp
+    float* stg = stg_all + ew * kStgFloats;
+    const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
+    const int uu = lane & 15, rr = lane >> 4;
+    const uint32_t sA_peer = map_peer(sA, peer);
+    auto a_off = [&](int r, int k) { return (uint32_t)((k / BK) * BM * 128) + sw128_offset(r, k % BK); };
+    auto put_h = [&](int r, int k, float v) {  // both CTAs' h tiles
+      const uint32_t off = a_off(r, k);
+      *reinterpret_cast<float*>(sA + off) = v;
+      st_cluster_f32(sA_peer + off, v);
+    };
+    for (int it = 0; it < 16; ++it) {
+      const int r = q * 32 + it * 2 + rr;
+      const int64_t row = row0 + r;
+      const int ci = row < R ? slot_carry[row * L] : -1;
+      for (int ul = ul0 + uu; ul < ul0 + kUnits; ul += 16) {
+        const int j = u0 + ul;
+        put_h(r, j, ci >= 0 ? rna_tf32(carry[(int64_t)ci * 2 * H + j]) : 0.f);
+      }
+    }
+    asm volatile("fence.proxy.async;" ::: "memory");
+    mbar_arrive(a_full);
+    mbar_arrive_cluster(map_peer(a_full, peer));
+    for (int p = 0; p < L; ++p) {
+      const bool has_next = p + 1 < L;
+      const int64_t my_row = row0 + q * 32 + lane;
+      const bool my_ok = my_row < R;
+      const int64_t my_s = my_row * L + p;
+      const int my_inst = my_ok ? slot_row[my_s] : -1;
+      const bool my_mk = my_ok && slot_mask[my_s];
+      const int my_ci = my_ok ? slot_carry[my_s] : -1;
+      const int my_prev = (p > 0 && my_mk) ? slot_row[my_s - 1] : -1;
+      const float my_mnext = (has_next && my_ok) ? (float)slot_mask[my_s + 1] : 0.f;
+      const int my_cnext = (has_next && my_ok) ? slot_carry[my_s + 1] : -1;
+      mbar_wait_cluster(acc_full, p & 1);
+      fence_after();
+#pragma unroll 1
+      for (int c0 = ul0; c0 < ul0 + kUnits; c0 += kChunk) {
+#pragma unroll
+        for (int gi = 0; gi < 4; ++gi) {
+          float a[16];
+          tmem_ld16(tl + gi * HU + c0, a);
+#pragma unroll
+          for (int u = 0; u < 16; ++u) stg[(gi * 32 + lane) * kStgStride + u] = a[u];
+        }
+        __syncwarp();
+        const int j = u0 + c0 + uu;  // global unit of this lane
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          float xg[8][4], cin[8];
+          int inst[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const int rl = (half * 8 + t) * 2 + rr;
+            inst[t] = __shfl_sync(0xffffffffu, my_inst, rl);
+            const int ci = __shfl_sync(0xffffffffu, my_ci, rl);
+            const int prev = __shfl_sync(0xffffffffu, my_prev, rl);
+            const float* gr = gx + (int64_t)max(inst[t], 0) * G4 + j;
+#pragma unroll
+            for (int gi = 0; gi < 4; ++gi) xg[t][gi] = inst[t] >= 0 ? __ldg(gr + gi * H) : 0.f;
+            cin[t] = ci >= 0 ? carry[(int64_t)ci * 2 * H + H + j]
+                             : (prev >= 0 ? c_out[(int64_t)prev * ld + j] : 0.f);
+          }
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const int rl = (half * 8 + t) * 2 + rr;
+            const int r = q * 32 + rl;
+            const float m_next = __shfl_sync(0xffffffffu, my_mnext, rl);
+            const int c_next = __shfl_sync(0xffffffffu, my_cnext, rl);
+            const float hin = *reinterpret_cast<const float*>(sA + a_off(r, j));
+            float hn = 0.f;
+            if (inst[t] >= 0) {
+              const float ig = sigm(stg[(0 * 32 + rl) * kStgStride + uu] + xg[t][0]);
+              const float fg = sigm(stg[(1 * 32 + rl) * kStgStride + uu] + xg[t][1]);
+              const float gg = tanh_fast(stg[(2 * 32 + rl) * kStgStride + uu] + xg[t][2]);
+              const float og = sigm(stg[(3 * 32 + rl) * kStgStride + uu] + xg[t][3]);
+              const float cn = fg * cin[t] + ig * gg;
+              const float tc = tanh_fast(cn);
+              hn = rna_tf32(og * tc);
+              float* sv = save + (int64_t)inst[t] * 7 * H + j;
+              sv[0] = hin;
+              sv[H] = cin[t];
+              sv[2 * H] = ig;
+              sv[3 * H] = fg;
+              sv[4 * H] = gg;
+              sv[5 * H] = og;
+              sv[6 * H] = tc;
+              h_out[(int64_t)inst[t] * ld + j] = hn;
+              c_out[(int64_t)inst[t] * ld + j] = cn;
+            }
+            if (has_next)
+              put_h(r, j, c_next >= 0 ? rna_tf32(carry[(int64_t)c_next * 2 * H + j]) : hn * m_next);
+          }
+        }
+        __syncwarp();
+      }
+      if (has_next) {
+        fence_before();
+        asm volatile("fence.proxy.async;" ::: "memory");
+        mbar_arrive(a_full);
+        mbar_arrive_cluster(map_peer(a_full, peer));
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the partner may still be writing into our shared memory
+  if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
+}
+
+template <int H>
+int launch_lstm_tc2(const float* gx, const float* Ut, const int32_t* slot_row,
+                    const uint8_t* slot_mask, const int32_t* slot_carry, const float* carry,
+                    int64_t R, int L, int64_t ld, float* h_out, float* c_out, float* save,
+                    cudaStream_t s) {
+  CUtensorMap m;
+  int rc = make_map(&m, Ut, 4 * H, H, H, 32, H / 2, false);
+  if (rc) return rc;
+  const size_t smem = (size_t)(H / BK) * BM * 128 + (size_t)kStages * 2 * H * 128 +
+                      (size_t)kEpiWarps * kStgFloats * 4 + 1024 + 256;
+  auto kern = lstm_fwd_tc2_kernel<H>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_fwd_tc2: set smem");
+  const int grid = 2 * (int)((R + BM - 1) / BM);
+  kern<<<grid, kThreads, smem, s>>>(m, gx, slot_row, slot_mask, slot_carry, carry, R, L, ld,
+                                    h_out, c_out, save);
+  DGC_CHECK_LAUNCH("lstm_fwd_tc2_kernel");
+  return DGC_OK;
+}
+
+// ---------------------------------------------------------------------------
 // Backward (BPTT) on tensor cores. Per position p, from the last to the first:
 //   epi : dh = m(p+1) * acc[(p+1)%2] + dh_out[inst], dc = dc carried (global
 //         scratch, per tile row x unit); saved gates -> da (4 gates) -> dgx,
@@ -487,6 +710,267 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
 }
 
+// Backward, 2-CTA cluster variant (H = 128): CTA c owns hidden units
+// [c*H/2, (c+1)*H/2). Its epilogue computes da for those units (8 of the 16
+// da k-blocks per position) and writes them into BOTH CTAs' A rings (DSMEM);
+// each CTA's MMA then forms dh_prev for its own units only (N = H/2) from all
+// 16 k-blocks. Ring slots are released by a multicast commit from both MMAs.
+// k-block sequence per position interleaves the owners: chunk order 0, 2, 1, 3.
+template <int H>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBwdThreads, 1)
+    lstm_bwd_tc2_kernel(const __grid_constant__ CUtensorMap tmU, const int32_t* __restrict__ slot_row,
+                        const uint8_t* __restrict__ slot_mask, int64_t R, int L,
+                        const float* __restrict__ save, const float* __restrict__ dh_out,
+                        float* __restrict__ dgx, float* __restrict__ dc_scr, int rnd,
+                        float* __restrict__ bias_partial) {
+  static_assert(H == 128, "cluster BPTT is specialised for H = 128");
+  constexpr int kRB = 8;                     // rows per load batch (memory-level parallelism)
+  constexpr int G4 = 4 * H;
+  constexpr int HU = H / 2;
+  constexpr int NC = H / 32;                 // 32-unit chunks (4)
+  constexpr int KB = G4 / BK;                // 16 da k-blocks per position
+  constexpr int kAStage = BM * 128;
+  constexpr int kBStage = HU * 128;          // HU rows of U x 32 k
+  constexpr uint32_t kTmemCols = 128;        // 2 x HU accumulators
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + kBwdAStages * kAStage;
+  float* stg_all = reinterpret_cast<float*>(sB + kBwdBStages * kBStage);
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(stg_all + kBwdEpiWarps * 32 * 33);
+  uint64_t* a_empty = a_full + kBwdAStages;
+  uint64_t* b_full = a_empty + kBwdAStages;
+  uint64_t* b_empty = b_full + kBwdBStages;
+  uint64_t* acc_full = b_empty + kBwdBStages;   // [2]
+  uint64_t* acc_empty = acc_full + 2;           // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_rank(), peer = crank ^ 1u;
+  const int64_t tile = blockIdx.x >> 1;
+  const int64_t row0 = tile * BM;
+  const int u0 = (int)crank * HU;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kBwdAStages; ++s) {
+      mbar_init(&a_full[s], kBwdEpiThreads);  // all 8 epilogue warps of the owner CTA
+      mbar_init(&a_empty[s], 2);    // both MMAs (multicast commit)
+    }
+    for (int s = 0; s < kBwdBStages; ++s) {
+      mbar_init(&b_full[s], 1);
+      mbar_init(&b_empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], kBwdEpiThreads);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmU) : "memory");
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+  fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  // sequence position m (0..NC-1) -> chunk (interleaved owners)
+  auto chunk_at = [](int m) { return (m & 1) * (NC / 2) + (m >> 1); };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int seq = 0; seq < L * KB; ++seq) {
+        const int s = seq % kBwdBStages;
+        mbar_wait(&b_empty[s], ((seq / kBwdBStages) & 1) ^ 1);
+        const int i = seq % KB, c = chunk_at(i >> 2), g = i & 3;
+        mbar_expect_tx(&b_full[s], (uint32_t)kBStage);
+        tma_load_2d(sB + s * kBStage, &tmU, g * H + 32 * c, u0, &b_full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = idesc_tf32(HU, false, false);
+    const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+    for (int t = 0; t < L; ++t) {
+      const int p = L - 1 - t;
+      const int a = p & 1;
+      mbar_wait(&acc_empty[a], ((t >> 1) & 1) ^ 1);
+      fence_after();
+      for (int i = 0; i < KB; ++i) {
+        const int seq = t * KB + i;
+        const int sa = seq % kBwdAStages, sb = seq % kBwdBStages;
+        mbar_wait_cluster(&a_full[sa], (seq / kBwdAStages) & 1);
+        mbar_wait(&b_full[sb], (seq / kBwdBStages) & 1);
+        fence_after();
+        if (lane == 0) {
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk)
+            mma_tf32(tmem_base + a * HU, kdesc(a_base + sa * kAStage + kk * 32),
+                     kdesc(b_base + sb * kBStage + kk * 32), idesc, (i > 0 || kk > 0) ? 1u : 0u);
+          mma_commit_mc(&a_empty[sa], (uint16_t)0x3);
+          mma_commit(&b_empty[sb]);
+          if (i == KB - 1) mma_commit(&acc_full[a]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // All 8 epilogue warps work on one 32-unit chunk at a time, in k-block
+    // sequence order (warp = quadrant q x row half h: 16 rows each), so a ring
+    // slot is never waited on by warps that could be working on another chunk.
+    const int ew = warp - 2;
+    const int q = warp & 3;
+    const int h = ew >> 2;                  // row half of the quadrant
+    float* stg = stg_all + ew * 32 * 33;
+    const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
+    const uint32_t sA_peer = map_peer(sA, peer);
+    const int64_t my_row = row0 + q * 32 + lane;
+    const bool my_ok = my_row < R;
+    float bsum[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    for (int t = 0; t < L; ++t) {
+      const int p = L - 1 - t;
+      const bool has_next = p + 1 < L;
+      const int64_t my_s = my_row * L + p;
+      const int my_inst = my_ok ? slot_row[my_s] : -1;
+      const float my_m = my_ok ? (float)slot_mask[my_s] : 0.f;
+      const float my_mnext = (has_next && my_ok) ? (float)slot_mask[my_s + 1] : 0.f;
+      if (blockIdx.x == 0 && threadIdx.x == 64 && t < 256) g_lstm_ts[t][0] = globaltimer();
+      if (has_next) {
+        mbar_wait(&acc_full[(p + 1) & 1], ((t - 1) >> 1) & 1);
+        fence_after();
+        if (blockIdx.x == 0 && threadIdx.x == 64 && t < 256) g_lstm_ts[t][1] = globaltimer();
+      }
+#pragma unroll 1
+      for (int lc = 0; lc < 2; ++lc) {
+        const int c = (int)crank * (NC / 2) + lc;  // global 32-unit chunk
+        const int m = 2 * lc + (int)crank;         // position in the k-block sequence
+        const int j = 32 * c + lane;
+        if (has_next) {
+          float v[32];
+          tmem_ld32(tl + ((p + 1) & 1) * HU + 32 * lc, v);
+#pragma unroll
+          for (int u = 0; u < 32; ++u) stg[lane * 33 + u] = v[u];
+        }
+        __syncwarp();
+        const int seq0 = t * KB + m * 4;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int seq = seq0 + g;
+          mbar_wait(&a_empty[seq % kBwdAStages], ((seq / kBwdAStages) & 1) ^ 1);
+        }
+#pragma unroll 1
+        for (int r0 = 16 * h; r0 < 16 * h + 16; r0 += kRB) {
+          float ld[kRB][6], dhv[kRB], dcv[kRB];
+          int inst[kRB];
+#pragma unroll
+          for (int u = 0; u < kRB; ++u) {
+            const int rl = r0 + u;
+            inst[u] = __shfl_sync(0xffffffffu, my_inst, rl);
+            const float mn = __shfl_sync(0xffffffffu, my_mnext, rl);
+            const int64_t trow = row0 + q * 32 + rl;
+            dhv[u] = has_next ? mn * stg[rl * 33 + lane] : 0.f;
+            dcv[u] = has_next ? dc_scr[trow * H + j] : 0.f;
+            if (inst[u] >= 0) {
+              dhv[u] += dh_out[(int64_t)inst[u] * H + j];
+              const float* sv = save + (int64_t)inst[u] * 7 * H + j;
+#pragma unroll
+              for (int k = 0; k < 6; ++k) ld[u][k] = sv[(k + 1) * H];
+            } else {
+#pragma unroll
+              for (int k = 0; k < 6; ++k) ld[u][k] = 0.f;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kRB; ++u) {
+            const int rl = r0 + u;
+            const int r = q * 32 + rl;
+            const float mp = __shfl_sync(0xffffffffu, my_m, rl);
+            const int64_t trow = row0 + r;
+            float da[4] = {0.f, 0.f, 0.f, 0.f};
+            float dcp = 0.f;
+            if (inst[u] >= 0) {
+              const float c_in = ld[u][0], ig = ld[u][1], fg = ld[u][2], gg = ld[u][3],
+                          og = ld[u][4], tc = ld[u][5];
+              const float g_ = dhv[u];
+              const float d_o = g_ * tc;
+              const float dcn = dcv[u] + g_ * og * (1.f - tc * tc);
+              da[0] = dcn * gg * ig * (1.f - ig);
+              da[1] = dcn * c_in * fg * (1.f - fg);
+              da[2] = dcn * ig * (1.f - gg * gg);
+              da[3] = d_o * og * (1.f - og);
+              dcp = dcn * fg * mp;
+              float* o = dgx + (int64_t)inst[u] * G4 + j;
+#pragma unroll
+              for (int g = 0; g < 4; ++g) {
+                if (rnd) da[g] = rna_tf32(da[g]);
+                o[g * H] = da[g];
+                bsum[lc][g] += da[g];
+              }
+            }
+            if (trow < R) dc_scr[trow * H + j] = dcp;
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              const uint32_t off =
+                  (uint32_t)(((seq0 + g) % kBwdAStages) * kAStage) + sw128_offset(r, lane);
+              *reinterpret_cast<float*>(sA + off) = da[g];
+              st_cluster_f32(sA_peer + off, da[g]);
+            }
+          }
+        }
+        asm volatile("fence.proxy.async;" ::: "memory");
+        if (lc == 1 && blockIdx.x == 0 && threadIdx.x == 64 && t < 256) g_lstm_ts[t][2] = globaltimer();
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int sl = (seq0 + g) % kBwdAStages;
+          mbar_arrive(&a_full[sl]);
+          mbar_arrive_cluster(map_peer(&a_full[sl], peer));
+        }
+        __syncwarp();
+      }
+      if (has_next) {
+        fence_before();
+        mbar_arrive(&acc_empty[(p + 1) & 1]);
+      }
+    }
+    if (bias_partial) {  // combine the 8 warps (4 quadrants x 2 halves) in fixed order
+      for (int lc = 0; lc < 2; ++lc) {
+        const int c = (int)crank * (NC / 2) + lc;
+        for (int g = 0; g < 4; ++g) {
+          stg[lane] = bsum[lc][g];
+          asm volatile("bar.sync 1, %0;" ::"r"(kBwdEpiThreads));
+          if (ew == 0) {
+            float acc = 0.f;
+            for (int w = 0; w < kBwdEpiWarps; ++w) acc += stg_all[w * 32 * 33 + lane];
+            bias_partial[tile * G4 + g * H + 32 * c + lane] = acc;
+          }
+          asm volatile("bar.sync 1, %0;" ::"r"(kBwdEpiThreads));
+        }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
+}
+
+template <int H>
+int launch_lstm_bwd_tc2(const float* U, const int32_t* slot_row, const uint8_t* slot_mask,
+                        int64_t R, int L, const float* save, const float* dh_out, float* dgx,
+                        float* dc_scr, int rnd, float* bias_partial, cudaStream_t s) {
+  CUtensorMap m;
+  int rc = make_map(&m, U, H, 4 * H, 4 * H, 32, H / 2, false);
+  if (rc) return rc;
+  const size_t smem = (size_t)kBwdAStages * BM * 128 + (size_t)kBwdBStages * (H / 2) * 128 +
+                      (size_t)kBwdEpiWarps * 32 * 33 * 4 + 1024 + 512;
+  auto kern = lstm_bwd_tc2_kernel<H>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_bwd_tc2: set smem");
+  const int grid = 2 * (int)((R + BM - 1) / BM);
+  kern<<<grid, kBwdThreads, smem, s>>>(m, slot_row, slot_mask, R, L, save, dh_out, dgx, dc_scr,
+                                       rnd, bias_partial);
+  DGC_CHECK_LAUNCH("lstm_bwd_tc2_kernel");
+  return DGC_OK;
+}
+
 template <int H>
 int launch_lstm_bwd_tc(const float* U, const int32_t* slot_row, const uint8_t* slot_mask,
                        int64_t R, int L, const float* save, const float* dh_out, float* dgx,
@@ -540,8 +1024,14 @@ extern "C" int dgc_rnn_fwd_tc(int32_t cell, const float* gx, const float* Ut,
   cudaStream_t s = dgc::as_stream(stream);
   switch (H) {
     case 32: return launch_lstm_tc<32>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
-    case 64: return launch_lstm_tc<64>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
-    case 128: return launch_lstm_tc<128>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
+    case 64:
+      if (!getenv("DGC_NO_CLUSTER_RNN"))
+        return launch_lstm_tc2<64>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
+      return launch_lstm_tc<64>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
+    case 128:
+      if (!getenv("DGC_NO_CLUSTER_RNN"))
+        return launch_lstm_tc2<128>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
+      return launch_lstm_tc<128>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
     default: return dgc::fail(DGC_ERR_ARG, "rnn_fwd_tc: H must be 32, 64 or 128");
   }
 }
@@ -563,7 +1053,10 @@ extern "C" int dgc_rnn_bwd_tc(int32_t cell_flags, const float* U, const int32_t*
   switch (H) {
     case 32: return launch_lstm_bwd_tc<32>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
     case 64: return launch_lstm_bwd_tc<64>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
-    case 128: return launch_lstm_bwd_tc<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
+    case 128:
+      if (!getenv("DGC_NO_CLUSTER_RNN"))
+        return launch_lstm_bwd_tc2<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
+      return launch_lstm_bwd_tc<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
     default: return dgc::fail(DGC_ERR_ARG, "rnn_bwd_tc: H must be 32, 64 or 128");
   }
 }

@@ -24,3 +24,14 @@ s.record()
 for _ in range(3): fn()
 e.record(); torch.cuda.synchronize()
 print("lstm bwd tc H", H, f"{s.elapsed_time(e)/3:.3f} ms")
+import ctypes
+from paper_2309_03523_b200 import _native
+lib = _native.lib()
+fn(); torch.cuda.synchronize()
+buf = (ctypes.c_ulonglong * (256 * 3))()
+lib.dgc_debug_lstm_timestamps(buf, 256 * 3)
+ts = np.array(buf[:L * 3], dtype=np.float64).reshape(L, 3)
+t0 = ts[0, 0]
+for t in range(1, 6):
+    print(f"t={t} start {(ts[t,0]-t0)/1e3:8.2f} acc_ready {(ts[t,1]-t0)/1e3:8.2f} epi_done {(ts[t,2]-t0)/1e3:8.2f} us")
+print("mean per-step: wait-acc", np.mean(ts[1:,1]-ts[1:,0])/1e3, "epi", np.mean(ts[1:,2]-ts[1:,1])/1e3, "step", np.mean(np.diff(ts[:,0]))/1e3)
