@@ -9,7 +9,8 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libdgc_b200.so"
+LIB_PATH = Path(os.environ.get("DGC_LIB_PATH") or
+                Path(__file__).resolve().parent / "lib" / "libdgc_b200.so")
 
 _i32, _i64, _f32, _p = C.c_int32, C.c_int64, C.c_float, C.c_void_p
 

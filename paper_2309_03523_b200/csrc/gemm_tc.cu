@@ -29,6 +29,7 @@ constexpr int kABytes = BM * BK * 4;  // 16 KiB
 template <bool A_MN, bool B_MN, bool SPLIT3>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmC, int tma_store,
                      float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, int bn, int stages,
                      int kb_total, int kb_per_split, int m_tiles, int n_tiles, int splits,
                      const float* __restrict__ bias, const float* __restrict__ relu_src,
@@ -56,7 +57,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;      // [2]
   uint64_t* bres_full = tempty + 2;  // [1]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_full + 1);
-  float* stg_base = reinterpret_cast<float*>(tmem_slot + 4);
+  // epilogue staging (transpose buffers, or 4 KB SWIZZLE_128B boxes), 1024-B aligned
+  float* stg_base = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(tmem_slot + 4) + 1023) & ~(uintptr_t)1023);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles_total = m_tiles * n_tiles * splits;
@@ -239,6 +242,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t aph = (i >> 1) & 1;
       mbar_wait(&tfull[a], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (tma_store) {
+        // TMEM -> registers (thread = row) [+ bias] -> this warp's SWIZZLE_128B
+        // staging box [32 rows x 32 cols] -> one TMA store per chunk (the copy
+        // engine writes the tile; the epilogue never issues global stores).
+        uint8_t* box = reinterpret_cast<uint8_t*>(stg_base + (warp - 2) * 1024);  // 4 KB, aligned
+        for (int c = 32 * chalf; c < bn; c += 32 * (kEpiWarps / 4)) {
+          float v[32];
+          tmem_ld32(tmem_base + (uint32_t)a * acc_cols + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
+          if (bias) {
+            const int64_t nb = n0 + c;
+#pragma unroll
+            for (int u = 0; u < 32; ++u) v[u] += (nb + u < N) ? __ldg(bias + nb + u) : 0.f;
+          }
+          if (lane == 0) bulk_wait_read<0>();  // previous chunk's store has left the box
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(box + sw128_offset(lane, 4 * j)) =
+                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmC, box, (int)(n0 + c), (int)(m0 + q * 32));
+            bulk_commit();
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        mbar_arrive(&tempty[a]);
+        continue;
+      }
       // TMEM -> registers (thread = row) -> padded smem transpose -> coalesced
       // 128-byte row stores (lane = column), epilogue fused into the store pass.
       for (int c = 32 * chalf; c < bn; c += 32 * (kEpiWarps / 4)) {
@@ -285,6 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&tempty[a]);
     }
   }
+  if (tma_store && warp >= 2 && lane == 0) bulk_wait<0>();  // stores complete before exit
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1) {
@@ -337,7 +371,8 @@ struct SegOpts {
 };
 
 template <bool A_MN, bool B_MN, bool SPLIT3>
-int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, float* C, int64_t ldc, int64_t M,
+int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, int tma_store,
+                float* C, int64_t ldc, int64_t M,
                 int64_t N, int bn, int ntiles, int kb_total, int splits, int kb_per,
                 const float* bias, const float* relu_src, int accumulate, float* partial,
                 float* colsum_partial, const SegOpts& so, cudaStream_t s) {
@@ -356,7 +391,7 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, float* C, int64_t 
   }
   if (stages < 1) return dgc::fail(DGC_ERR_ARG, "gemm: tile does not fit shared memory");
   const size_t smem = (size_t)stages * (b_res ? kABytes : stage_bytes) +
-                      (b_res ? (size_t)bres_bytes : 0) + 1024 + 256 + kEpiWarps * 32 * 33 * 4;
+                      (b_res ? (size_t)bres_bytes : 0) + 1024 + 256 + 1024 + kEpiWarps * 32 * 33 * 4;
   auto kern = gemm_tf32_kernel<A_MN, B_MN, SPLIT3>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return dgc::cuda_fail(e, "gemm: set smem");
@@ -364,7 +399,7 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, float* C, int64_t 
   const int total = m_tiles * ntiles * splits;
   int grid = (dgc::kNumSMs / ntiles) * ntiles;  // multiple of n_tiles: fixed n per CTA
   if (grid > total) grid = total;
-  kern<<<grid, kThreads, smem, s>>>(ma, mb, C, ldc, M, N, bn, stages, kb_total, kb_per, m_tiles,
+  kern<<<grid, kThreads, smem, s>>>(ma, mb, mc, tma_store, C, ldc, M, N, bn, stages, kb_total, kb_per, m_tiles,
                                     ntiles, splits, bias, relu_src, accumulate, partial,
                                     colsum_partial, b_res, so.seg_of_mtile, so.b_seg_rows,
                                     so.kitems);
@@ -419,12 +454,18 @@ static int gemm_impl(const float* A, int64_t lda, const float* B, int64_t ldb, f
   if (rc) return rc;
   float* part = (splits > 1 || so.kitems) ? partial : nullptr;
   const bool s3 = precision == 3;
+  // plain / bias-only outputs leave through TMA stores (box 32 cols x 32 rows)
+  CUtensorMap mc;
+  int tma_store = (!part && !relu_src && !accumulate && !colsum_partial &&
+                   !getenv("DGC_GEMM_NO_TMA_STORE")) ? 1 : 0;
+  if (tma_store && make_map(&mc, C, M, N, ldc, 32, 32, false) != DGC_OK) tma_store = 0;
   if (so.kitems && splits == 0) {
     rc = DGC_OK;
   } else {
 #define DGC_GEMM_CASE(AM, BMN, S3)                                                               \
   if ((bool)a_mn == AM && (bool)b_mn == BMN && s3 == S3)                                          \
-    rc = launch_gemm<AM, BMN, S3>(ma, mb, C, ldc, M, N, bn, ntiles, kb_total, splits, kb_per,   \
+    rc = launch_gemm<AM, BMN, S3>(ma, mb, mc, tma_store, C, ldc, M, N, bn, ntiles, kb_total,     \
+                                  splits, kb_per,                                                \
                                   part ? nullptr : bias, part ? nullptr : relu_src,              \
                                   part ? 0 : accumulate, part, colsum_partial, so, s);
     DGC_GEMM_CASE(false, false, false)

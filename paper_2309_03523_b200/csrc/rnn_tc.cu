@@ -29,6 +29,11 @@ constexpr int kStages = 2;     // B ring: one (k-block, 256-column part) of U^T 
 constexpr int kChunk = 16;     // units per TMEM load / smem transpose
 constexpr int kStgStride = 17; // padded row stride of the transpose buffer (floats)
 constexpr int kStgFloats = 4 * 32 * kStgStride;  // 4 gates x 32 rows per warp
+// L2 prefetch distance (positions) of the cluster kernels; < 0 disables
+int rnn_prefetch_distance() {
+  const char* e = getenv("DGC_RNN_PF");
+  return e ? atoi(e) : 1;
+}
 
 __device__ __forceinline__ float tanh_fast(float x) {
   float y;
@@ -264,7 +269,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         const int32_t* __restrict__ slot_row, const uint8_t* __restrict__ slot_mask,
                         const int32_t* __restrict__ slot_carry, const float* __restrict__ carry,
                         int64_t R, int L, int64_t ld, float* __restrict__ h_out,
-                        float* __restrict__ c_out, float* __restrict__ save) {
+                        float* __restrict__ c_out, float* __restrict__ save, int kPf) {
   constexpr int G4 = 4 * H;
   constexpr int HU = H / 2;                  // units owned by this CTA
   constexpr int NP = 4 * HU;                 // MMA N: 4 gates x HU units (<= 256)
@@ -366,8 +371,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     asm volatile("fence.proxy.async;" ::: "memory");
     mbar_arrive(a_full);
     mbar_arrive_cluster(map_peer(a_full, peer));
+    // L2 prefetch of the gx rows kPf positions ahead (each CTA of the pair pulls
+    // half of every row; the unit-half-0 warps issue it, one row per lane)
+    const int64_t pf_row = row0 + q * 32 + lane;
+    auto prefetch_pos = [&](int pp) {
+      if (kPf < 0 || ul0 != 0 || pp >= L || pf_row >= R) return;
+      const int inst = slot_row[pf_row * L + pp];
+      if (inst >= 0) prefetch_l2_bulk(gx + (int64_t)inst * G4 + crank * (G4 / 2), G4 * 2);
+    };
+    for (int pp = 0; pp <= kPf; ++pp) prefetch_pos(pp);
     for (int p = 0; p < L; ++p) {
       const bool has_next = p + 1 < L;
+      prefetch_pos(p + kPf + 1);
       const int64_t my_row = row0 + q * 32 + lane;
       const bool my_ok = my_row < R;
       const int64_t my_s = my_row * L + p;
@@ -453,6 +468,544 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
 }
 
+// Forward, 2-CTA cluster variant with EW epilogue warps: EW/4 warps per TMEM
+// lane quadrant, each owning 32/(EW/4) rows and all HU units of this CTA (16-unit
+// chunks, transposed through shared memory so lanes = (row parity, unit)). The
+// carried c of a cell stays in registers (a thread owns the same cells at every
+// position), so only run starts with a cross-device predecessor read memory.
+template <int H, int EW>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
+    lstm_fwd_tc2w_kernel(const __grid_constant__ CUtensorMap tmUt, const float* __restrict__ gx,
+                         const int32_t* __restrict__ slot_row, const uint8_t* __restrict__ slot_mask,
+                         const int32_t* __restrict__ slot_carry, const float* __restrict__ carry,
+                         int64_t R, int L, int64_t ld, float* __restrict__ h_out,
+                         float* __restrict__ c_out, float* __restrict__ save, int kPf) {
+  constexpr int kEpiT = 32 * EW;
+  constexpr int WPQ = EW / 4;
+  constexpr int RPW = 32 / WPQ;              // rows per warp (even)
+  constexpr int NT = RPW / 2;                // row pairs per chunk
+  constexpr int G4 = 4 * H;
+  constexpr int HU = H / 2;
+  constexpr int NCH = HU / kChunk;           // 16-unit chunks per CTA
+  constexpr int NP = 4 * HU;
+  constexpr int KB = H / BK;
+  constexpr int kABytes = KB * BM * 128;
+  constexpr int kBStage = NP * 128;
+  constexpr int kStgW = 4 * RPW * kStgStride;
+  constexpr uint32_t kTmemCols = NP <= 128 ? 128 : 256;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kABytes;
+  float* stg_all = reinterpret_cast<float*>(sB + kStages * kBStage);
+  float* c_all = stg_all + EW * kStgW;       // carried c: [EW][NCH][NT][32]
+  uint64_t* b_full = reinterpret_cast<uint64_t*>(c_all + EW * NCH * NT * 32);
+  uint64_t* b_empty = b_full + kStages;
+  uint64_t* a_full = b_empty + kStages;
+  uint64_t* acc_full = a_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_rank(), peer = crank ^ 1u;
+  const int64_t row0 = (int64_t)(blockIdx.x >> 1) * BM;
+  const int u0 = (int)crank * HU;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&b_full[s], 1);
+      mbar_init(&b_empty[s], 1);
+    }
+    mbar_init(a_full, 2 * kEpiT);
+    mbar_init(acc_full, 2);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmUt) : "memory");
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+  fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int g = 0; g < L * KB; ++g) {
+        const int s = g % kStages;
+        mbar_wait(&b_empty[s], ((g / kStages) & 1) ^ 1);
+        const int kb = g % KB;
+        mbar_expect_tx(&b_full[s], (uint32_t)kBStage);
+#pragma unroll
+        for (int gi = 0; gi < 4; ++gi)
+          tma_load_2d(sB + s * kBStage + gi * HU * 128, &tmUt, kb * BK, gi * H + u0, &b_full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = idesc_tf32(NP, false, false);
+    const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+    for (int p = 0; p < L; ++p) {
+      mbar_wait_cluster(a_full, p & 1);
+      fence_after();
+      if (blockIdx.x == 0 && lane == 0 && p < 256) g_lstm_ts[p][0] = globaltimer();
+      for (int kb = 0; kb < KB; ++kb) {
+        const int g = p * KB + kb;
+        const int s = g % kStages;
+        mbar_wait(&b_full[s], (g / kStages) & 1);
+        fence_after();
+        if (lane == 0) {
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk)
+            mma_tf32(tmem_base, kdesc(a_base + kb * BM * 128 + kk * 32),
+                     kdesc(b_base + s * kBStage + kk * 32), idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&b_empty[s]);
+          if (kb == KB - 1) mma_commit_mc(acc_full, (uint16_t)0x3);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    const int ew = warp - 2;
+    const int q = warp & 3;
+    const int rb = (ew >> 2) * RPW;          // first quadrant row of this warp
+    float* stg = stg_all + ew * kStgW;
+    const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
+    const int uu = lane & 15, rr = lane >> 4;
+    const uint32_t sA_peer = map_peer(sA, peer);
+    auto a_off = [&](int r, int k) { return (uint32_t)((k / BK) * BM * 128) + sw128_offset(r, k % BK); };
+    auto put_h = [&](int r, int k, float v) {
+      const uint32_t off = a_off(r, k);
+      *reinterpret_cast<float*>(sA + off) = v;
+#ifndef DGC_EXP_NODSMEM
+      st_cluster_f32(sA_peer + off, v);
+#endif
+    };
+    const int64_t my_row = row0 + q * 32 + lane;
+    const bool my_ok = my_row < R;
+    // prologue: h_in of position 0 for this warp's rows (run start: carry or zero)
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const int r = q * 32 + rb + 2 * t + rr;
+      const int64_t row = row0 + r;
+      const int ci = row < R ? slot_carry[row * L] : -1;
+      for (int ul = uu; ul < HU; ul += 16) {
+        const int j = u0 + ul;
+        put_h(r, j, ci >= 0 ? rna_tf32(carry[(int64_t)ci * 2 * H + j]) : 0.f);
+      }
+    }
+    asm volatile("fence.proxy.async;" ::: "memory");
+    mbar_arrive(a_full);
+    mbar_arrive_cluster(map_peer(a_full, peer));
+    auto prefetch_pos = [&](int pp) {
+      if (kPf < 0 || pp >= L || !my_ok || (ew >> 2) != 0) return;
+      const int inst = slot_row[my_row * L + pp];
+      if (inst >= 0) prefetch_l2_bulk(gx + (int64_t)inst * G4 + crank * (G4 / 2), G4 * 2);
+    };
+    for (int pp = 0; pp <= kPf; ++pp) prefetch_pos(pp);
+    float* creg = c_all + ew * NCH * NT * 32 + lane;  // [ch][t] at (ch * NT + t) * 32
+    // per-row slot info (lane = quadrant row), loaded one position ahead
+    int n_inst = my_ok ? slot_row[my_row * L] : -1;
+    int n_mk = 0;  // mask of position 0 is always 0
+    int n_ci = my_ok ? slot_carry[my_row * L] : -1;
+    for (int p = 0; p < L; ++p) {
+      const bool has_next = p + 1 < L;
+      prefetch_pos(p + kPf + 1);
+      const int my_inst = n_inst, my_mk = n_mk, my_ci = n_ci;
+      if (has_next && my_ok) {
+        const int64_t s1 = my_row * L + p + 1;
+        n_inst = slot_row[s1];
+        n_mk = slot_mask[s1];
+        n_ci = slot_carry[s1];
+      } else {
+        n_inst = -1; n_mk = 0; n_ci = -1;
+      }
+      const float my_mnext = (float)n_mk;
+      const int my_cnext = n_ci;
+      mbar_wait_cluster(acc_full, p & 1);
+      fence_after();
+      if (blockIdx.x == 0 && threadIdx.x == 64 && p < 256) g_lstm_ts[p][1] = globaltimer();
+#pragma unroll 1
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int c0 = ch * kChunk;
+#pragma unroll
+        for (int gi = 0; gi < 4; ++gi) {
+          float a[16];
+          tmem_ld16(tl + gi * HU + c0, a);
+          if (lane >= rb && lane < rb + RPW) {
+#pragma unroll
+            for (int u = 0; u < 16; ++u) stg[(gi * RPW + lane - rb) * kStgStride + u] = a[u];
+          }
+        }
+        __syncwarp();
+        const int j = u0 + c0 + uu;
+        float xg[NT][4], cin[NT];
+        int inst[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int rl = rb + 2 * t + rr;
+          inst[t] = __shfl_sync(0xffffffffu, my_inst, rl);
+          const int ci = __shfl_sync(0xffffffffu, my_ci, rl);
+          const int mk = __shfl_sync(0xffffffffu, my_mk, rl);
+          const float* gr = gx + (int64_t)max(inst[t], 0) * G4 + j;
+#pragma unroll
+#ifdef DGC_EXP_NOLOAD
+          for (int gi = 0; gi < 4; ++gi) xg[t][gi] = 0.01f * (float)((inst[t] + gi) & 7);
+#else
+          for (int gi = 0; gi < 4; ++gi) xg[t][gi] = inst[t] >= 0 ? __ldg(gr + gi * H) : 0.f;
+#endif
+          cin[t] = ci >= 0 ? carry[(int64_t)ci * 2 * H + H + j] : (mk ? creg[(ch * NT + t) * 32] : 0.f);
+        }
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int rl = rb + 2 * t + rr;
+          const int r = q * 32 + rl;
+          const int sl = 2 * t + rr;         // row within this warp's stg
+          const float m_next = __shfl_sync(0xffffffffu, my_mnext, rl);
+          const int c_next = __shfl_sync(0xffffffffu, my_cnext, rl);
+          const float hin = *reinterpret_cast<const float*>(sA + a_off(r, j));
+          float hn = 0.f, cn = 0.f;
+          if (inst[t] >= 0) {
+            const float ig = sigm(stg[(0 * RPW + sl) * kStgStride + uu] + xg[t][0]);
+            const float fg = sigm(stg[(1 * RPW + sl) * kStgStride + uu] + xg[t][1]);
+            const float gg = tanh_fast(stg[(2 * RPW + sl) * kStgStride + uu] + xg[t][2]);
+            const float og = sigm(stg[(3 * RPW + sl) * kStgStride + uu] + xg[t][3]);
+            cn = fg * cin[t] + ig * gg;
+            const float tc = tanh_fast(cn);
+            hn = rna_tf32(og * tc);
+#ifndef DGC_EXP_NOSTORE
+            float* sv = save + (int64_t)inst[t] * 7 * H + j;
+            sv[0] = hin;
+            sv[H] = cin[t];
+            sv[2 * H] = ig;
+            sv[3 * H] = fg;
+            sv[4 * H] = gg;
+            sv[5 * H] = og;
+            sv[6 * H] = tc;
+            h_out[(int64_t)inst[t] * ld + j] = hn;
+            c_out[(int64_t)inst[t] * ld + j] = cn;
+#else
+            if (hn + hin + tc == 1234.5f) save[0] = hn;
+#endif
+          }
+          creg[(ch * NT + t) * 32] = cn;
+          if (has_next)
+            put_h(r, j, c_next >= 0 ? rna_tf32(carry[(int64_t)c_next * 2 * H + j]) : hn * m_next);
+        }
+        __syncwarp();
+      }
+      if (blockIdx.x == 0 && threadIdx.x == 64 && p < 256) g_lstm_ts[p][2] = globaltimer();
+      if (has_next) {
+        fence_before();
+        asm volatile("fence.proxy.async;" ::: "memory");
+        mbar_arrive(a_full);
+        mbar_arrive_cluster(map_peer(a_full, peer));
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
+}
+
+template <int H, int EW>
+int launch_lstm_tc2w(const float* gx, const float* Ut, const int32_t* slot_row,
+                     const uint8_t* slot_mask, const int32_t* slot_carry, const float* carry,
+                     int64_t R, int L, int64_t ld, float* h_out, float* c_out, float* save,
+                     cudaStream_t s) {
+  CUtensorMap m;
+  int rc = make_map(&m, Ut, 4 * H, H, H, 32, H / 2, false);
+  if (rc) return rc;
+  constexpr int RPW = 32 / (EW / 4);
+  const size_t smem = (size_t)(H / BK) * BM * 128 + (size_t)kStages * 2 * H * 128 +
+                      (size_t)EW * 4 * RPW * kStgStride * 4 + (size_t)EW * (H / 32) * (RPW / 2) * 128 +
+                      1024 + 256;
+  auto kern = lstm_fwd_tc2w_kernel<H, EW>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_fwd_tc2w: set smem");
+  const int grid = 2 * (int)((R + BM - 1) / BM);
+  kern<<<grid, 64 + 32 * EW, smem, s>>>(m, gx, slot_row, slot_mask, slot_carry, carry, R, L, ld,
+                                        h_out, c_out, save, rnn_prefetch_distance());
+  DGC_CHECK_LAUNCH("lstm_fwd_tc2w_kernel");
+  return DGC_OK;
+}
+
+// Forward, 2-CTA cluster, vectorised epilogue (16 warps = 4 per TMEM lane
+// quadrant, 8 rows each). A lane owns one row and 4 consecutive units of a
+// 16-unit chunk (lane = 8 rows x 4 unit quads), so every global / shared / DSMEM
+// access is a 16-byte vector and the per-row slot info is loaded per lane (no
+// shuffles). The carried c stays in shared memory per lane (same cells at every
+// position); the next chunk's gx loads are issued before the current chunk's math.
+constexpr int kVEW = 16;
+__device__ __forceinline__ float4 f4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ float4 zero4() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+
+template <int H>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
+    lstm_fwd_tc2v_kernel(const __grid_constant__ CUtensorMap tmUt, const float* __restrict__ gx,
+                         const int32_t* __restrict__ slot_row, const uint8_t* __restrict__ slot_mask,
+                         const int32_t* __restrict__ slot_carry, const float* __restrict__ carry,
+                         int64_t R, int L, int64_t ld, float* __restrict__ h_out,
+                         float* __restrict__ c_out, float* __restrict__ save) {
+  constexpr int kEpiT = 32 * kVEW;
+  constexpr int G4 = 4 * H;
+  constexpr int HU = H / 2;
+  constexpr int NCH = HU / 16;               // 16-unit chunks per CTA
+  constexpr int NP = 4 * HU;
+  constexpr int KB = H / BK;
+  constexpr int kABytes = KB * BM * 128;
+  constexpr int kBStage = NP * 128;
+  constexpr int kStgW = 4 * 8 * 16;          // [gate][8 rows][16 units]
+  constexpr uint32_t kTmemCols = NP <= 128 ? 128 : 256;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kABytes;
+  float* stg_all = reinterpret_cast<float*>(sB + kStages * kBStage);
+  float* c_all = stg_all + kVEW * kStgW;     // carried c: [warp][chunk][lane] float4
+  uint64_t* b_full = reinterpret_cast<uint64_t*>(c_all + kVEW * NCH * 32 * 4);
+  uint64_t* b_empty = b_full + kStages;
+  uint64_t* a_full = b_empty + kStages;
+  uint64_t* acc_full = a_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_rank(), peer = crank ^ 1u;
+  const int64_t row0 = (int64_t)(blockIdx.x >> 1) * BM;
+  const int u0 = (int)crank * HU;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&b_full[s], 1);
+      mbar_init(&b_empty[s], 1);
+    }
+    mbar_init(a_full, 2 * kEpiT);
+    mbar_init(acc_full, 2);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmUt) : "memory");
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+  fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int g = 0; g < L * KB; ++g) {
+        const int s = g % kStages;
+        mbar_wait(&b_empty[s], ((g / kStages) & 1) ^ 1);
+        const int kb = g % KB;
+        mbar_expect_tx(&b_full[s], (uint32_t)kBStage);
+#pragma unroll
+        for (int gi = 0; gi < 4; ++gi)
+          tma_load_2d(sB + s * kBStage + gi * HU * 128, &tmUt, kb * BK, gi * H + u0, &b_full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = idesc_tf32(NP, false, false);
+    const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+    for (int p = 0; p < L; ++p) {
+      mbar_wait_cluster(a_full, p & 1);
+      fence_after();
+      if (blockIdx.x == 0 && lane == 0 && p < 256) g_lstm_ts[p][0] = globaltimer();
+      for (int kb = 0; kb < KB; ++kb) {
+        const int g = p * KB + kb;
+        const int s = g % kStages;
+        mbar_wait(&b_full[s], (g / kStages) & 1);
+        fence_after();
+        if (lane == 0) {
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk)
+            mma_tf32(tmem_base, kdesc(a_base + kb * BM * 128 + kk * 32),
+                     kdesc(b_base + s * kBStage + kk * 32), idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&b_empty[s]);
+          if (kb == KB - 1) mma_commit_mc(acc_full, (uint16_t)0x3);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    const int ew = warp - 2;
+    const int q = warp & 3;                  // TMEM lane quadrant (warp id % 4)
+    const int rb = (ew >> 2) * 8;            // first quadrant row of this warp
+    const int r8 = lane >> 2, uq = lane & 3;
+    const int r = q * 32 + rb + r8;          // tile row of this lane
+    const int64_t grow = row0 + r;
+    const bool ok = grow < R;
+    float* stg = stg_all + ew * kStgW;
+    float* creg = c_all + (ew * NCH * 32 + lane) * 4;  // + ch * 128
+    const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
+    const uint32_t sA_peer = map_peer(sA, peer);
+    auto a_off = [&](int k) { return (uint32_t)((k / BK) * BM * 128) + sw128_offset(r, k % BK); };
+    auto put_h = [&](int k, float4 v) {
+      const uint32_t off = a_off(k);
+      st4(reinterpret_cast<float*>(sA + off), v);
+#ifndef DGC_EXP_NODSMEM
+      st_cluster_v4(sA_peer + off, v);
+#endif
+    };
+    // prologue: h_in of position 0 (run start: carry or zero)
+    {
+      const int ci = ok ? slot_carry[grow * L] : -1;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int j = u0 + ch * 16 + uq * 4;
+        float4 v = zero4();
+        if (ci >= 0) {
+          v = f4(carry + (int64_t)ci * 2 * H + j);
+          v = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
+        }
+        put_h(j, v);
+        st4(creg + ch * 128, zero4());
+      }
+    }
+    asm volatile("fence.proxy.async;" ::: "memory");
+    mbar_arrive(a_full);
+    mbar_arrive_cluster(map_peer(a_full, peer));
+    int n_inst = ok ? slot_row[grow * L] : -1, n_mk = 0, n_ci = ok ? slot_carry[grow * L] : -1;
+    for (int p = 0; p < L; ++p) {
+      const bool has_next = p + 1 < L;
+      const int inst = n_inst, mk = n_mk, ci = n_ci;
+      if (has_next && ok) {
+        const int64_t s1 = grow * L + p + 1;
+        n_inst = slot_row[s1];
+        n_mk = slot_mask[s1];
+        n_ci = slot_carry[s1];
+      } else {
+        n_inst = -1; n_mk = 0; n_ci = -1;
+      }
+      const float m_next = (float)n_mk;
+      const float* gxr = gx + (int64_t)max(inst, 0) * G4 + u0 + uq * 4;
+      float4 xg[4];
+#pragma unroll
+      for (int gi = 0; gi < 4; ++gi) xg[gi] = inst >= 0 ? ldg4(gxr + gi * H) : zero4();
+#ifdef DGC_EXP_NOLOAD
+      for (int gi = 0; gi < 4; ++gi) xg[gi] = make_float4(0.01f * gi, 0.02f, 0.03f * (inst & 3), 0.f);
+#endif
+      mbar_wait_cluster(acc_full, p & 1);
+      fence_after();
+      if (blockIdx.x == 0 && threadIdx.x == 64 && p < 256) g_lstm_ts[p][1] = globaltimer();
+#pragma unroll 1
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int c0 = ch * 16;
+        const int j = u0 + c0 + uq * 4;
+        {
+          float a[64];
+#ifndef DGC_EXP_NOTMEM
+          tmem_ld16x4(tl + c0, tl + HU + c0, tl + 2 * HU + c0, tl + 3 * HU + c0, a);
+#else
+#pragma unroll
+          for (int u = 0; u < 64; ++u) a[u] = 0.01f * (float)((lane + u) & 7);
+#endif
+          if (lane >= rb && lane < rb + 8) {
+#pragma unroll
+            for (int gi = 0; gi < 4; ++gi) {
+              float* d = stg + (gi * 8 + lane - rb) * 16;
+#pragma unroll
+              for (int u = 0; u < 16; u += 4)
+                st4(d + u, make_float4(a[gi * 16 + u], a[gi * 16 + u + 1], a[gi * 16 + u + 2],
+                                       a[gi * 16 + u + 3]));
+            }
+          }
+        }
+        __syncwarp();
+        float4 pre[4];
+#pragma unroll
+        for (int gi = 0; gi < 4; ++gi) pre[gi] = f4(stg + (gi * 8 + r8) * 16 + uq * 4);
+        // next chunk's gx in flight while this chunk computes
+        float4 xn[4];
+#pragma unroll
+        for (int gi = 0; gi < 4; ++gi)
+#ifndef DGC_EXP_NOLOAD
+          xn[gi] = (inst >= 0 && ch + 1 < NCH) ? ldg4(gxr + gi * H + c0 + 16) : zero4();
+#else
+          xn[gi] = make_float4(0.01f * gi, 0.02f * ch, 0.03f * (inst & 3), 0.f);
+#endif
+        float4 cin = zero4();
+        if (ci >= 0) cin = f4(carry + (int64_t)ci * 2 * H + H + j);
+        else if (mk) cin = f4(creg + ch * 128);
+        const float4 hin = f4(reinterpret_cast<const float*>(sA + a_off(j)));
+        float4 hn = zero4(), cn = zero4();
+        if (inst >= 0) {
+          float4 ig, fg, gg, og, tc;
+#define DGC_LSTM_CELL(c)                                          \
+  ig.c = sigm(pre[0].c + xg[0].c);                                \
+  fg.c = sigm(pre[1].c + xg[1].c);                                \
+  gg.c = tanh_fast(pre[2].c + xg[2].c);                           \
+  og.c = sigm(pre[3].c + xg[3].c);                                \
+  cn.c = fg.c * cin.c + ig.c * gg.c;                              \
+  tc.c = tanh_fast(cn.c);                                         \
+  hn.c = rna_tf32(og.c * tc.c);
+          DGC_LSTM_CELL(x) DGC_LSTM_CELL(y) DGC_LSTM_CELL(z) DGC_LSTM_CELL(w)
+#undef DGC_LSTM_CELL
+#ifndef DGC_EXP_NOSTORE
+          float* sv = save + (int64_t)inst * 7 * H + j;
+          st4(sv, hin);
+          st4(sv + H, cin);
+          st4(sv + 2 * H, ig);
+          st4(sv + 3 * H, fg);
+          st4(sv + 4 * H, gg);
+          st4(sv + 5 * H, og);
+          st4(sv + 6 * H, tc);
+          st4(h_out + (int64_t)inst * ld + j, hn);
+          st4(c_out + (int64_t)inst * ld + j, cn);
+#else
+          if (hn.x + tc.y + hin.z + og.w + ig.x + fg.y + gg.z == 1234.5f) save[0] = 1.f;
+#endif
+        }
+        st4(creg + ch * 128, cn);
+        if (has_next) {
+          float4 v;
+          if (n_ci >= 0) {
+            v = f4(carry + (int64_t)n_ci * 2 * H + j);
+            v = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
+          } else {
+            v = make_float4(hn.x * m_next, hn.y * m_next, hn.z * m_next, hn.w * m_next);
+          }
+          put_h(j, v);
+        }
+#pragma unroll
+        for (int gi = 0; gi < 4; ++gi) xg[gi] = xn[gi];
+        __syncwarp();
+      }
+      if (blockIdx.x == 0 && threadIdx.x == 64 && p < 256) g_lstm_ts[p][2] = globaltimer();
+      if (has_next) {
+        fence_before();
+        asm volatile("fence.proxy.async;" ::: "memory");
+        mbar_arrive(a_full);
+        mbar_arrive_cluster(map_peer(a_full, peer));
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
+}
+
+template <int H>
+int launch_lstm_tc2v(const float* gx, const float* Ut, const int32_t* slot_row,
+                     const uint8_t* slot_mask, const int32_t* slot_carry, const float* carry,
+                     int64_t R, int L, int64_t ld, float* h_out, float* c_out, float* save,
+                     cudaStream_t s) {
+  CUtensorMap m;
+  int rc = make_map(&m, Ut, 4 * H, H, H, 32, H / 2, false);
+  if (rc) return rc;
+  const size_t smem = (size_t)(H / BK) * BM * 128 + (size_t)kStages * 2 * H * 128 +
+                      (size_t)kVEW * 4 * 8 * 16 * 4 + (size_t)kVEW * (H / 32) * 32 * 16 +
+                      1024 + 256;
+  auto kern = lstm_fwd_tc2v_kernel<H>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_fwd_tc2v: set smem");
+  const int grid = 2 * (int)((R + BM - 1) / BM);
+  kern<<<grid, 64 + 32 * kVEW, smem, s>>>(m, gx, slot_row, slot_mask, slot_carry, carry, R, L, ld,
+                                          h_out, c_out, save);
+  DGC_CHECK_LAUNCH("lstm_fwd_tc2v_kernel");
+  return DGC_OK;
+}
+
 template <int H>
 int launch_lstm_tc2(const float* gx, const float* Ut, const int32_t* slot_row,
                     const uint8_t* slot_mask, const int32_t* slot_carry, const float* carry,
@@ -468,7 +1021,7 @@ int launch_lstm_tc2(const float* gx, const float* Ut, const int32_t* slot_row,
   if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_fwd_tc2: set smem");
   const int grid = 2 * (int)((R + BM - 1) / BM);
   kern<<<grid, kThreads, smem, s>>>(m, gx, slot_row, slot_mask, slot_carry, carry, R, L, ld,
-                                    h_out, c_out, save);
+                                    h_out, c_out, save, rnn_prefetch_distance());
   DGC_CHECK_LAUNCH("lstm_fwd_tc2_kernel");
   return DGC_OK;
 }
@@ -722,7 +1275,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBwdThreads, 1)
                         const uint8_t* __restrict__ slot_mask, int64_t R, int L,
                         const float* __restrict__ save, const float* __restrict__ dh_out,
                         float* __restrict__ dgx, float* __restrict__ dc_scr, int rnd,
-                        float* __restrict__ bias_partial) {
+                        float* __restrict__ bias_partial, int kPf) {
   static_assert(H == 128, "cluster BPTT is specialised for H = 128");
   constexpr int kRB = 8;                     // rows per load batch (memory-level parallelism)
   constexpr int G4 = 4 * H;
@@ -825,9 +1378,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBwdThreads, 1)
     const int64_t my_row = row0 + q * 32 + lane;
     const bool my_ok = my_row < R;
     float bsum[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    // L2 prefetch kPf positions ahead (backwards): row-half-0 warps pull half of
+    // the saved-activation row, row-half-1 warps this CTA's half of dh_out
+    auto prefetch_pos = [&](int pp) {
+      if (kPf < 0 || pp < 0 || !my_ok) return;
+      const int inst = slot_row[my_row * L + pp];
+      if (inst < 0) return;
+      if (h == 0)
+        prefetch_l2_bulk(save + (int64_t)inst * 7 * H + crank * (7 * H / 2), 7 * H * 2);
+      else
+        prefetch_l2_bulk(dh_out + (int64_t)inst * H + u0, HU * 4);
+    };
+    for (int pp = L - 1; pp >= L - 1 - kPf; --pp) prefetch_pos(pp);
     for (int t = 0; t < L; ++t) {
       const int p = L - 1 - t;
       const bool has_next = p + 1 < L;
+      prefetch_pos(p - kPf - 1);
       const int64_t my_s = my_row * L + p;
       const int my_inst = my_ok ? slot_row[my_s] : -1;
       const float my_m = my_ok ? (float)slot_mask[my_s] : 0.f;
@@ -867,6 +1433,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBwdThreads, 1)
             const float mn = __shfl_sync(0xffffffffu, my_mnext, rl);
             const int64_t trow = row0 + q * 32 + rl;
             dhv[u] = has_next ? mn * stg[rl * 33 + lane] : 0.f;
+#ifdef DGC_EXP_NOLOAD
+            dcv[u] = has_next ? 0.5f : 0.f;
+            if (inst[u] >= 0) {
+              dhv[u] += 0.25f * (float)(inst[u] & 7);
+#pragma unroll
+              for (int k = 0; k < 6; ++k) ld[u][k] = 0.1f * k + 1e-3f * (float)(inst[u] & 15);
+            } else {
+#else
             dcv[u] = has_next ? dc_scr[trow * H + j] : 0.f;
             if (inst[u] >= 0) {
               dhv[u] += dh_out[(int64_t)inst[u] * H + j];
@@ -874,6 +1448,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
               for (int k = 0; k < 6; ++k) ld[u][k] = sv[(k + 1) * H];
             } else {
+#endif
 #pragma unroll
               for (int k = 0; k < 6; ++k) ld[u][k] = 0.f;
             }
@@ -901,17 +1476,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
               for (int g = 0; g < 4; ++g) {
                 if (rnd) da[g] = rna_tf32(da[g]);
+#ifndef DGC_EXP_NOSTORE
                 o[g * H] = da[g];
+#endif
                 bsum[lc][g] += da[g];
               }
             }
+#ifndef DGC_EXP_NOSTORE
             if (trow < R) dc_scr[trow * H + j] = dcp;
+#else
+            if (dcp == 1234.5f) dc_scr[0] = dcp;
+#endif
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
               const uint32_t off =
                   (uint32_t)(((seq0 + g) % kBwdAStages) * kAStage) + sw128_offset(r, lane);
               *reinterpret_cast<float*>(sA + off) = da[g];
+#ifndef DGC_EXP_NODSMEM
               st_cluster_f32(sA_peer + off, da[g]);
+#endif
             }
           }
         }
@@ -952,6 +1535,282 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBwdThreads, 1)
   if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
 }
 
+// Backward, 2-CTA cluster variant with EW epilogue warps (EW/4 per TMEM lane
+// quadrant, 32/(EW/4) rows each; more warps = more loads in flight for this
+// latency-bound epilogue). The carried dc of a (row, unit) cell stays in
+// registers: a thread owns the same cells at every position.
+template <int H, int EW>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
+    lstm_bwd_tc2w_kernel(const __grid_constant__ CUtensorMap tmU, const int32_t* __restrict__ slot_row,
+                         const uint8_t* __restrict__ slot_mask, int64_t R, int L,
+                         const float* __restrict__ save, const float* __restrict__ dh_out,
+                         float* __restrict__ dgx, int rnd, float* __restrict__ bias_partial,
+                         int kPf) {
+  static_assert(H == 128, "cluster BPTT is specialised for H = 128");
+  constexpr int kEpiT = 32 * EW;
+  constexpr int WPQ = EW / 4;                // warps per lane quadrant
+  constexpr int RPW = 32 / WPQ;              // rows per warp
+  constexpr int kRB = EW >= 16 ? 4 : 8;      // rows per load batch
+  constexpr int NB = RPW / kRB;              // batches per chunk
+  constexpr int G4 = 4 * H;
+  constexpr int HU = H / 2;
+  constexpr int NC = H / 32;
+  constexpr int KB = G4 / BK;
+  constexpr int kAStage = BM * 128;
+  constexpr int kBStage = HU * 128;
+  constexpr uint32_t kTmemCols = 128;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + kBwdAStages * kAStage;
+  float* stg_all = reinterpret_cast<float*>(sB + kBwdBStages * kBStage);
+  constexpr int kStg = (RPW > 1 ? RPW : 1) * 33;  // >= 32 floats (bias combine)
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(stg_all + EW * kStg);
+  uint64_t* a_empty = a_full + kBwdAStages;
+  uint64_t* b_full = a_empty + kBwdAStages;
+  uint64_t* b_empty = b_full + kBwdBStages;
+  uint64_t* acc_full = b_empty + kBwdBStages;   // [2]
+  uint64_t* acc_empty = acc_full + 2;           // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_rank(), peer = crank ^ 1u;
+  const int64_t tile = blockIdx.x >> 1;
+  const int64_t row0 = tile * BM;
+  const int u0 = (int)crank * HU;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kBwdAStages; ++s) {
+      mbar_init(&a_full[s], kEpiT);
+      mbar_init(&a_empty[s], 2);
+    }
+    for (int s = 0; s < kBwdBStages; ++s) {
+      mbar_init(&b_full[s], 1);
+      mbar_init(&b_empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], kEpiT);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmU) : "memory");
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+  fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  auto chunk_at = [](int m) { return (m & 1) * (NC / 2) + (m >> 1); };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int seq = 0; seq < L * KB; ++seq) {
+        const int s = seq % kBwdBStages;
+        mbar_wait(&b_empty[s], ((seq / kBwdBStages) & 1) ^ 1);
+        const int i = seq % KB, c = chunk_at(i >> 2), g = i & 3;
+        mbar_expect_tx(&b_full[s], (uint32_t)kBStage);
+        tma_load_2d(sB + s * kBStage, &tmU, g * H + 32 * c, u0, &b_full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = idesc_tf32(HU, false, false);
+    const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+    for (int t = 0; t < L; ++t) {
+      const int p = L - 1 - t;
+      const int a = p & 1;
+      mbar_wait(&acc_empty[a], ((t >> 1) & 1) ^ 1);
+      fence_after();
+      for (int i = 0; i < KB; ++i) {
+        const int seq = t * KB + i;
+        const int sa = seq % kBwdAStages, sb = seq % kBwdBStages;
+        mbar_wait_cluster(&a_full[sa], (seq / kBwdAStages) & 1);
+        mbar_wait(&b_full[sb], (seq / kBwdBStages) & 1);
+        fence_after();
+        if (lane == 0) {
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk)
+            mma_tf32(tmem_base + a * HU, kdesc(a_base + sa * kAStage + kk * 32),
+                     kdesc(b_base + sb * kBStage + kk * 32), idesc, (i > 0 || kk > 0) ? 1u : 0u);
+          mma_commit_mc(&a_empty[sa], (uint16_t)0x3);
+          mma_commit(&b_empty[sb]);
+          if (i == KB - 1) mma_commit(&acc_full[a]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    const int ew = warp - 2;
+    const int q = warp & 3;                 // TMEM lane quadrant (warp id % 4)
+    const int hq = ew >> 2;                 // row group within the quadrant
+    const int rb = hq * RPW;                // first quadrant row of this warp
+    float* stg = stg_all + ew * kStg;
+    const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
+    const uint32_t sA_peer = map_peer(sA, peer);
+    const int64_t my_row = row0 + q * 32 + lane;
+    const bool my_ok = my_row < R;
+    float bsum[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    float dcr[2][RPW];                      // carried dc of this thread's cells
+#pragma unroll
+    for (int lc = 0; lc < 2; ++lc)
+#pragma unroll
+      for (int u = 0; u < RPW; ++u) dcr[lc][u] = 0.f;
+    auto prefetch_pos = [&](int pp) {
+      if (kPf < 0 || pp < 0 || !my_ok || hq != 0) return;
+      const int inst = slot_row[my_row * L + pp];
+      if (inst < 0) return;
+      prefetch_l2_bulk(save + (int64_t)inst * 7 * H + crank * (7 * H / 2), 7 * H * 2);
+      prefetch_l2_bulk(dh_out + (int64_t)inst * H + u0, HU * 4);
+    };
+    for (int pp = L - 1; pp >= L - 1 - kPf; --pp) prefetch_pos(pp);
+    for (int t = 0; t < L; ++t) {
+      const int p = L - 1 - t;
+      const bool has_next = p + 1 < L;
+      prefetch_pos(p - kPf - 1);
+      const int64_t my_s = my_row * L + p;
+      const int my_inst = my_ok ? slot_row[my_s] : -1;
+      const float my_m = my_ok ? (float)slot_mask[my_s] : 0.f;
+      const float my_mnext = (has_next && my_ok) ? (float)slot_mask[my_s + 1] : 0.f;
+      if (blockIdx.x == 0 && threadIdx.x == 64 && t < 256) g_lstm_ts[t][0] = globaltimer();
+      if (has_next) {
+        mbar_wait(&acc_full[(p + 1) & 1], ((t - 1) >> 1) & 1);
+        fence_after();
+        if (blockIdx.x == 0 && threadIdx.x == 64 && t < 256) g_lstm_ts[t][1] = globaltimer();
+      }
+#pragma unroll
+      for (int lc = 0; lc < 2; ++lc) {
+        const int c = (int)crank * (NC / 2) + lc;
+        const int m = 2 * lc + (int)crank;
+        const int j = 32 * c + lane;
+        if (has_next) {
+          float v[32];
+          tmem_ld32(tl + ((p + 1) & 1) * HU + 32 * lc, v);
+          if (lane >= rb && lane < rb + RPW) {
+#pragma unroll
+            for (int u = 0; u < 32; ++u) stg[(lane - rb) * 33 + u] = v[u];
+          }
+        }
+        __syncwarp();
+        const int seq0 = t * KB + m * 4;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int seq = seq0 + g;
+          mbar_wait(&a_empty[seq % kBwdAStages], ((seq / kBwdAStages) & 1) ^ 1);
+        }
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          float ld[kRB][6], dhv[kRB];
+          int inst[kRB];
+#pragma unroll
+          for (int u = 0; u < kRB; ++u) {
+            const int rl = rb + b * kRB + u;
+            inst[u] = __shfl_sync(0xffffffffu, my_inst, rl);
+            const float mn = __shfl_sync(0xffffffffu, my_mnext, rl);
+            dhv[u] = has_next ? mn * stg[(b * kRB + u) * 33 + lane] : 0.f;
+            if (inst[u] >= 0) {
+              dhv[u] += dh_out[(int64_t)inst[u] * H + j];
+              const float* sv = save + (int64_t)inst[u] * 7 * H + j;
+#pragma unroll
+              for (int k = 0; k < 6; ++k) ld[u][k] = sv[(k + 1) * H];
+            } else {
+#pragma unroll
+              for (int k = 0; k < 6; ++k) ld[u][k] = 0.f;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kRB; ++u) {
+            const int rl = rb + b * kRB + u;
+            const int r = q * 32 + rl;
+            const float mp = __shfl_sync(0xffffffffu, my_m, rl);
+            float& dc = dcr[lc][b * kRB + u];
+            float da[4] = {0.f, 0.f, 0.f, 0.f};
+            float dcp = 0.f;
+            if (inst[u] >= 0) {
+              const float c_in = ld[u][0], ig = ld[u][1], fg = ld[u][2], gg = ld[u][3],
+                          og = ld[u][4], tc = ld[u][5];
+              const float g_ = dhv[u];
+              const float d_o = g_ * tc;
+              const float dcn = dc + g_ * og * (1.f - tc * tc);
+              da[0] = dcn * gg * ig * (1.f - ig);
+              da[1] = dcn * c_in * fg * (1.f - fg);
+              da[2] = dcn * ig * (1.f - gg * gg);
+              da[3] = d_o * og * (1.f - og);
+              dcp = dcn * fg * mp;
+              float* o = dgx + (int64_t)inst[u] * G4 + j;
+#pragma unroll
+              for (int g = 0; g < 4; ++g) {
+                if (rnd) da[g] = rna_tf32(da[g]);
+                o[g * H] = da[g];
+                bsum[lc][g] += da[g];
+              }
+            }
+            dc = dcp;
+            const uint32_t off0 = sw128_offset(r, lane);
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              const uint32_t off = (uint32_t)(((seq0 + g) % kBwdAStages) * kAStage) + off0;
+              *reinterpret_cast<float*>(sA + off) = da[g];
+              st_cluster_f32(sA_peer + off, da[g]);
+            }
+          }
+        }
+        asm volatile("fence.proxy.async;" ::: "memory");
+        if (lc == 1 && blockIdx.x == 0 && threadIdx.x == 64 && t < 256) g_lstm_ts[t][2] = globaltimer();
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int sl = (seq0 + g) % kBwdAStages;
+          mbar_arrive(&a_full[sl]);
+          mbar_arrive_cluster(map_peer(&a_full[sl], peer));
+        }
+        __syncwarp();
+      }
+      if (has_next) {
+        fence_before();
+        mbar_arrive(&acc_empty[(p + 1) & 1]);
+      }
+    }
+    if (bias_partial) {  // combine the EW warps in fixed order
+      for (int lc = 0; lc < 2; ++lc) {
+        const int c = (int)crank * (NC / 2) + lc;
+        for (int g = 0; g < 4; ++g) {
+          stg[lane] = bsum[lc][g];
+          asm volatile("bar.sync 1, %0;" ::"r"(kEpiT));
+          if (ew == 0) {
+            float acc = 0.f;
+            for (int w = 0; w < EW; ++w) acc += stg_all[w * kStg + lane];
+            bias_partial[tile * G4 + g * H + 32 * c + lane] = acc;
+          }
+          asm volatile("bar.sync 1, %0;" ::"r"(kEpiT));
+        }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
+}
+
+template <int H, int EW>
+int launch_lstm_bwd_tc2w(const float* U, const int32_t* slot_row, const uint8_t* slot_mask,
+                         int64_t R, int L, const float* save, const float* dh_out, float* dgx,
+                         int rnd, float* bias_partial, cudaStream_t s) {
+  CUtensorMap m;
+  int rc = make_map(&m, U, H, 4 * H, 4 * H, 32, H / 2, false);
+  if (rc) return rc;
+  constexpr int RPW = 32 / (EW / 4);
+  const size_t smem = (size_t)kBwdAStages * BM * 128 + (size_t)kBwdBStages * (H / 2) * 128 +
+                      (size_t)EW * (RPW > 1 ? RPW : 1) * 33 * 4 + 1024 + 512;
+  auto kern = lstm_bwd_tc2w_kernel<H, EW>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_bwd_tc2w: set smem");
+  const int grid = 2 * (int)((R + BM - 1) / BM);
+  kern<<<grid, 64 + 32 * EW, smem, s>>>(m, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
+                                        bias_partial, rnn_prefetch_distance());
+  DGC_CHECK_LAUNCH("lstm_bwd_tc2w_kernel");
+  return DGC_OK;
+}
+
 template <int H>
 int launch_lstm_bwd_tc2(const float* U, const int32_t* slot_row, const uint8_t* slot_mask,
                         int64_t R, int L, const float* save, const float* dh_out, float* dgx,
@@ -966,7 +1825,7 @@ int launch_lstm_bwd_tc2(const float* U, const int32_t* slot_row, const uint8_t* 
   if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_bwd_tc2: set smem");
   const int grid = 2 * (int)((R + BM - 1) / BM);
   kern<<<grid, kBwdThreads, smem, s>>>(m, slot_row, slot_mask, R, L, save, dh_out, dgx, dc_scr,
-                                       rnd, bias_partial);
+                                       rnd, bias_partial, rnn_prefetch_distance());
   DGC_CHECK_LAUNCH("lstm_bwd_tc2_kernel");
   return DGC_OK;
 }
@@ -1029,8 +1888,14 @@ extern "C" int dgc_rnn_fwd_tc(int32_t cell, const float* gx, const float* Ut,
         return launch_lstm_tc2<64>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
       return launch_lstm_tc<64>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
     case 128:
-      if (!getenv("DGC_NO_CLUSTER_RNN"))
+      if (!getenv("DGC_NO_CLUSTER_RNN")) {
+        const char* ew = getenv("DGC_FWD_EW");
+        if (!ew)
+          return launch_lstm_tc2v<128>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
+        if (atoi(ew) == 16)
+          return launch_lstm_tc2w<128, 16>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
         return launch_lstm_tc2<128>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
+      }
       return launch_lstm_tc<128>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
     default: return dgc::fail(DGC_ERR_ARG, "rnn_fwd_tc: H must be 32, 64 or 128");
   }
@@ -1054,8 +1919,15 @@ extern "C" int dgc_rnn_bwd_tc(int32_t cell_flags, const float* U, const int32_t*
     case 32: return launch_lstm_bwd_tc<32>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
     case 64: return launch_lstm_bwd_tc<64>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
     case 128:
-      if (!getenv("DGC_NO_CLUSTER_RNN"))
+      if (!getenv("DGC_NO_CLUSTER_RNN")) {
+        const char* ew = getenv("DGC_BWD_EW");
+        const int nw = ew ? atoi(ew) : 16;
+        if (nw == 16)
+          return launch_lstm_bwd_tc2w<128, 16>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, rnd, bias_partial, s);
+        if (nw == 8)
+          return launch_lstm_bwd_tc2w<128, 8>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, rnd, bias_partial, s);
         return launch_lstm_bwd_tc2<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
+      }
       return launch_lstm_bwd_tc<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
     default: return dgc::fail(DGC_ERR_ARG, "rnn_bwd_tc: H must be 32, 64 or 128");
   }
