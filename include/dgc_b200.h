@@ -154,6 +154,17 @@ int dgc_gemm_tf32_segmented(const float* A, int64_t lda, const float* B, int64_t
                             const int32_t* kitems, int32_t n_kitems, const int32_t* item_ptr,
                             int32_t n_seg, float* partial, float* colsum_partial, void* stream);
 
+/* Stacked-A GEMM: op(A) = [op(A0) ; op(A1)] along M (rows [0, M0) from A0,
+ * [M0, M) from A1; M0 % 128 == 0), every other argument as dgc_gemm_tf32.
+ * One launch for the two LSTM weight gradients that share B = dgx:
+ * [dWx ; dU] = [x ; h_in]^T dgx, so the 4H-wide dgx is streamed once (the
+ * split-K CTAs of both row tiles read each B k-block concurrently, L2 dedups).
+ * C is [M, N] (dWx and dU are adjacent in the flat gradient buffer). */
+int dgc_gemm_tf32_stacked_a(const float* A0, int64_t lda0, const float* A1, int64_t lda1,
+                            int64_t M0, const float* B, int64_t ldb, float* C, int64_t ldc,
+                            int64_t M, int64_t N, int64_t K, int32_t a_mn, int32_t b_mn,
+                            int32_t precision, int32_t k_splits, float* partial, void* stream);
+
 /* EvolveGCN-O weight evolution (matrix GRU in the reference gate form of
  * GruCell.step, fusion.py:409-413, input = hidden = W_{t-1}):
  *   R = s(S_r W + B_r), Z = s(S_z W + B_z), C = tanh(P_c W + Q_c (R*W) + B_c),

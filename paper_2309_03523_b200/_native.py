@@ -43,6 +43,8 @@ _SIGS = {
     "dgc_gemm_tf32": (_i32, [_p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _i32, _i32, _i32,
                               _p, _p, _i32, _i32, _p, _p, _p]),
     "dgc_gemm_splits": (_i32, [_i64, _i32, _i32]),
+    "dgc_gemm_tf32_stacked_a": (_i32, [_p, _i64, _p, _i64, _i64, _p, _i64, _p, _i64, _i64, _i64,
+                                       _i64, _i32, _i32, _i32, _i32, _p, _p]),
     "dgc_gemm_tf32_segmented": (_i32, [_p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _i32, _i32,
                                         _i32, _p, _p, _p, _i32, _p, _i32, _p, _i32, _p, _p, _p]),
     "dgc_evolve_fwd": (_i32, [_i32, _i32, _i32] + [_p] * 14 + [_i32, _p]),

@@ -30,6 +30,7 @@ template <bool A_MN, bool B_MN, bool SPLIT3>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC, int tma_store,
+                     const __grid_constant__ CUtensorMap tmA2, int64_t a2_row0,
                      float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, int bn, int stages,
                      int kb_total, int kb_per_split, int m_tiles, int n_tiles, int splits,
                      const float* __restrict__ bias, const float* __restrict__ relu_src,
@@ -80,6 +81,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    if (a2_row0 < M) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA2) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -139,12 +141,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int k0 = (kb0 + kb) * BK;
           // row-segmented B (one weight matrix per snapshot block of 128-row tiles)
           const int boff = seg_of_mtile ? seg_of_mtile[m0 / BM] * b_seg_rows : 0;
+          // stacked A: rows >= a2_row0 come from the second operand
+          const CUtensorMap* mA = m0 >= a2_row0 ? &tmA2 : &tmA;
+          const int am0 = (int)(m0 >= a2_row0 ? m0 - a2_row0 : m0);
           if (!A_MN) {
-            tma_load_2d(sa, &tmA, k0, (int)m0, &full[s]);
+            tma_load_2d(sa, mA, k0, am0, &full[s]);
           } else {
 #pragma unroll
             for (int i = 0; i < BM / 32; ++i)
-              tma_load_2d(sa + i * 4096, &tmA, (int)m0 + 32 * i, k0, &full[s]);
+              tma_load_2d(sa + i * 4096, mA, am0 + 32 * i, k0, &full[s]);
           }
           if (!b_res) {
             if (!B_MN) {
@@ -250,10 +255,44 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 32 * chalf; c < bn; c += 32 * (kEpiWarps / 4)) {
           float v[32];
           tmem_ld32(tmem_base + (uint32_t)a * acc_cols + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
+          const int64_t nb = n0 + c;
           if (bias) {
-            const int64_t nb = n0 + c;
 #pragma unroll
             for (int u = 0; u < 32; ++u) v[u] += (nb + u < N) ? __ldg(bias + nb + u) : 0.f;
+          }
+          const int64_t row = m0 + q * 32 + lane;
+          if (relu_src || colsum_partial) {
+            // ReLU mask from the forward activation (thread = row, 128-B row segment)
+            const bool rok = row < M;
+            if (relu_src) {
+              const float4* rs = reinterpret_cast<const float4*>(relu_src + row * ldc + nb);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float4 m = (rok && nb + 4 * j < N) ? __ldg(rs + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+                if (!(m.x > 0.f)) v[4 * j] = 0.f;
+                if (!(m.y > 0.f)) v[4 * j + 1] = 0.f;
+                if (!(m.z > 0.f)) v[4 * j + 2] = 0.f;
+                if (!(m.w > 0.f)) v[4 * j + 3] = 0.f;
+              }
+            }
+            if (colsum_partial) {
+              // column sums of this warp's 32 rows: butterfly transpose-reduction
+              // (31 shuffles; lane u ends with column u), fixed order
+              float x[32];
+#pragma unroll
+              for (int u = 0; u < 32; ++u) x[u] = rok ? v[u] : 0.f;
+#pragma unroll
+              for (int sft = 16; sft >= 1; sft >>= 1) {
+                const bool up = (lane & sft) != 0;
+#pragma unroll
+                for (int i = 0; i < sft; ++i) {
+                  const float send = up ? x[i] : x[i + sft];
+                  const float keep = up ? x[i + sft] : x[i];
+                  x[i] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+                }
+              }
+              if (nb + lane < N) colsum_partial[((m0 / BM) * 4 + q) * N + nb + lane] = x[0];
+            }
           }
           if (lane == 0) bulk_wait_read<0>();  // previous chunk's store has left the box
           __syncwarp();
@@ -368,10 +407,14 @@ struct SegOpts {
   int n_kitems = 0;
   const int32_t* item_ptr = nullptr;      // items of each segment
   int n_seg = 0;
+  const float* a2 = nullptr;              // stacked A: rows [a2_row0, M) of op(A)
+  int64_t lda2 = 0;
+  int64_t a2_row0 = 0;
 };
 
 template <bool A_MN, bool B_MN, bool SPLIT3>
 int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, int tma_store,
+                const CUtensorMap& ma2, int64_t a2_row0,
                 float* C, int64_t ldc, int64_t M,
                 int64_t N, int bn, int ntiles, int kb_total, int splits, int kb_per,
                 const float* bias, const float* relu_src, int accumulate, float* partial,
@@ -399,7 +442,7 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   const int total = m_tiles * ntiles * splits;
   int grid = (dgc::kNumSMs / ntiles) * ntiles;  // multiple of n_tiles: fixed n per CTA
   if (grid > total) grid = total;
-  kern<<<grid, kThreads, smem, s>>>(ma, mb, mc, tma_store, C, ldc, M, N, bn, stages, kb_total, kb_per, m_tiles,
+  kern<<<grid, kThreads, smem, s>>>(ma, mb, mc, tma_store, ma2, a2_row0, C, ldc, M, N, bn, stages, kb_total, kb_per, m_tiles,
                                     ntiles, splits, bias, relu_src, accumulate, partial,
                                     colsum_partial, b_res, so.seg_of_mtile, so.b_seg_rows,
                                     so.kitems);
@@ -448,6 +491,19 @@ static int gemm_impl(const float* A, int64_t lda, const float* B, int64_t ldb, f
   int rc = a_mn ? make_map(&ma, A, K, M, lda, 32, 32, true)
                  : make_map(&ma, A, M, K, lda, 32, BM, false);
   if (rc) return rc;
+  CUtensorMap ma2 = ma;
+  int64_t a2_row0 = INT64_MAX;
+  if (so.a2) {
+    DGC_REQUIRE(so.a2_row0 > 0 && so.a2_row0 % BM == 0 && so.a2_row0 < M,
+                "gemm: stacked A needs a 128-aligned split row inside M");
+    a2_row0 = so.a2_row0;
+    rc = a_mn ? make_map(&ma2, so.a2, K, M - a2_row0, so.lda2, 32, 32, true)
+              : make_map(&ma2, so.a2, M - a2_row0, K, so.lda2, 32, BM, false);
+    if (rc) return rc;
+    rc = a_mn ? make_map(&ma, A, K, a2_row0, lda, 32, 32, true)
+              : make_map(&ma, A, a2_row0, K, lda, 32, BM, false);
+    if (rc) return rc;
+  }
   const int64_t nseg = so.b_nseg > 0 ? so.b_nseg : 1;
   rc = b_mn ? make_map(&mb, B, K * nseg, N, ldb, 32, 32, true)
             : make_map(&mb, B, N * nseg, K, ldb, 32, (uint32_t)bn, false);
@@ -456,7 +512,7 @@ static int gemm_impl(const float* A, int64_t lda, const float* B, int64_t ldb, f
   const bool s3 = precision == 3;
   // plain / bias-only outputs leave through TMA stores (box 32 cols x 32 rows)
   CUtensorMap mc;
-  int tma_store = (!part && !relu_src && !accumulate && !colsum_partial &&
+  int tma_store = (!part && !accumulate && ((ldc * 4) % 16 == 0) && (!relu_src || N % 4 == 0) &&
                    !getenv("DGC_GEMM_NO_TMA_STORE")) ? 1 : 0;
   if (tma_store && make_map(&mc, C, M, N, ldc, 32, 32, false) != DGC_OK) tma_store = 0;
   if (so.kitems && splits == 0) {
@@ -464,7 +520,8 @@ static int gemm_impl(const float* A, int64_t lda, const float* B, int64_t ldb, f
   } else {
 #define DGC_GEMM_CASE(AM, BMN, S3)                                                               \
   if ((bool)a_mn == AM && (bool)b_mn == BMN && s3 == S3)                                          \
-    rc = launch_gemm<AM, BMN, S3>(ma, mb, mc, tma_store, C, ldc, M, N, bn, ntiles, kb_total,     \
+    rc = launch_gemm<AM, BMN, S3>(ma, mb, mc, tma_store, ma2, a2_row0, C, ldc, M, N, bn, ntiles, \
+                                  kb_total,                                                      \
                                   splits, kb_per,                                                \
                                   part ? nullptr : bias, part ? nullptr : relu_src,              \
                                   part ? 0 : accumulate, part, colsum_partial, so, s);
@@ -522,4 +579,17 @@ extern "C" int dgc_gemm_tf32_segmented(const float* A, int64_t lda, const float*
   so.n_seg = n_seg;
   return gemm_impl(A, lda, B, ldb, C, ldc, M, N, K, a_mn, b_mn, precision, bias, relu_src, 0, 1,
                    partial, colsum_partial, so, stream);
+}
+
+extern "C" int dgc_gemm_tf32_stacked_a(const float* A0, int64_t lda0, const float* A1, int64_t lda1,
+                                       int64_t M0, const float* B, int64_t ldb, float* C,
+                                       int64_t ldc, int64_t M, int64_t N, int64_t K, int32_t a_mn,
+                                       int32_t b_mn, int32_t precision, int32_t k_splits,
+                                       float* partial, void* stream) {
+  SegOpts so;
+  so.a2 = A1;
+  so.lda2 = lda1;
+  so.a2_row0 = M0;
+  return gemm_impl(A0, lda0, B, ldb, C, ldc, M, N, K, a_mn, b_mn, precision, nullptr, nullptr, 0,
+                   k_splits, partial, nullptr, so, stream);
 }

@@ -117,6 +117,30 @@ def gemm(A, B, C, M, N, K, *, a_mn=False, b_mn=True, lda=None, ldb=None, ldc=Non
     return C
 
 
+def gemm_stacked_a(A0, A1, B, C, M0, M, N, K, *, a_mn=False, b_mn=True, lda0=None, lda1=None,
+                   ldb=None, ldc=None, precision=3, k_splits=1, partial=None):
+    """K2 with op(A) = [op(A0); op(A1)] along M (dgc_gemm_tf32_stacked_a): one
+    launch for [dWx; dU] = [x; h_in]^T dgx."""
+    for t, nm in ((A0, "A0"), (A1, "A1"), (B, "B"), (C, "C")):
+        _req(t, torch.float32, nm)
+    if partial is None and gemm_splits(K, precision, k_splits) > 1:
+        raise ValueError("gemm_stacked_a: split-K needs a partial buffer")
+    lda0 = lda0 if lda0 is not None else (M0 if a_mn else K)
+    lda1 = lda1 if lda1 is not None else ((M - M0) if a_mn else K)
+    ldb = ldb if ldb is not None else (N if b_mn else K)
+    ldc = ldc if ldc is not None else N
+    splits = gemm_splits(K, precision, k_splits)
+    nb = 4 * (M * K + K * N + M * N)
+    gname = "gemm_tf32" if precision == 1 else "gemm_3xtf32"
+    if _prof_detail:
+        gname += f"[{M}x{N}x{K} a{int(a_mn)}b{int(b_mn)} s{splits} stacked]"
+    _run(gname, lambda: _native.check(_native.lib().dgc_gemm_tf32_stacked_a(
+        _p(A0), lda0, _p(A1), lda1, M0, _p(B), ldb, _p(C), ldc, M, N, K, int(a_mn), int(b_mn),
+        precision, k_splits, _p(partial), _stream()), "dgc_gemm_tf32_stacked_a"),
+        nb, 2.0 * M * N * K, 1 + int(splits > 1))
+    return C
+
+
 def gemm_segmented(A, B, C, M, N, K, *, a_mn=False, b_mn=True, lda=None, ldb=None, ldc=None,
                    precision=3, bias=None, relu_src=None, seg_of_mtile=None, b_nseg=1,
                    kitems=None, n_kitems=0, item_ptr=None, n_seg=0, partial=None,

@@ -181,7 +181,7 @@ class Shard:
         kb = max(1, (n + 31) // 32)
         self.ksplit = max(1, min(148, kb // 4))
         n_split = ops.gemm_splits(max(n, 1), self.prec, self.ksplit)
-        self.partial = torch.zeros(n_split * max(F, H) * max(GH, H, cfg.C), **f32)
+        self.partial = torch.zeros(n_split * max(F, 2 * H) * max(GH, H, cfg.C), **f32)
         # stale caches (spatial per GCN layer, temporal per RNN layer)
         stale_on = stale.mode is not StaleMode.OFF and self.D > 1
         self.stale_on = stale_on
@@ -411,18 +411,25 @@ class Shard:
                             H, self.save[k], self.dh, self.dgx, bias_partial=self.bias_partial)
                 ops.reduce_rows(self.bias_partial, self.rnn_prows, GH, self.g(f"br{k}"))
             xin, ldxin = (self.Hl[1], H) if k == 0 else (self.hbuf[k - 1], self.hw)
-            ops.gemm(xin, self.dgx, self.g(f"Wx{k}"), H, GH, n, a_mn=True, lda=ldxin,
-                     precision=prec, k_splits=ks, partial=part)
             gU = self.g(f"U{k}")
-            if cell == 0:
-                ops.gemm(self.save[k], self.dgx, gU, H, 2 * H, n, a_mn=True, lda=self.sf,
-                         ldb=GH, ldc=GH, precision=prec, k_splits=ks, partial=part)
-                ops.gemm(self.save[k][:, H:], self.dgx[:, 2 * H:], gU[:, 2 * H:], H, H, n,
-                         a_mn=True, lda=self.sf, ldb=GH, ldc=GH, precision=prec, k_splits=ks,
-                         partial=part)
+            if cell == 1 and H % 128 == 0:
+                # [dWx; dU] = [x; h_in]^T dgx in ONE launch: dgx is streamed once
+                # (Wx{k} and U{k} are adjacent in the flat gradient buffer)
+                ops.gemm_stacked_a(xin, self.save[k], self.dgx, self.g(f"Wx{k}"), H, 2 * H, GH, n,
+                                   a_mn=True, lda0=ldxin, lda1=self.sf, ldb=GH, ldc=GH,
+                                   precision=prec, k_splits=ks, partial=part)
             else:
-                ops.gemm(self.save[k], self.dgx, gU, H, GH, n, a_mn=True, lda=self.sf, ldb=GH,
-                         ldc=GH, precision=prec, k_splits=ks, partial=part)
+                ops.gemm(xin, self.dgx, self.g(f"Wx{k}"), H, GH, n, a_mn=True, lda=ldxin,
+                         precision=prec, k_splits=ks, partial=part)
+                if cell == 0:
+                    ops.gemm(self.save[k], self.dgx, gU, H, 2 * H, n, a_mn=True, lda=self.sf,
+                             ldb=GH, ldc=GH, precision=prec, k_splits=ks, partial=part)
+                    ops.gemm(self.save[k][:, H:], self.dgx[:, 2 * H:], gU[:, 2 * H:], H, H, n,
+                             a_mn=True, lda=self.sf, ldb=GH, ldc=GH, precision=prec, k_splits=ks,
+                             partial=part)
+                else:
+                    ops.gemm(self.save[k], self.dgx, gU, H, GH, n, a_mn=True, lda=self.sf,
+                             ldb=GH, ldc=GH, precision=prec, k_splits=ks, partial=part)
             relu_src = self.Hl[1] if k == 0 else None
             ops.gemm(self.dgx, self.pr(f"Wx{k}"), self.dh2, n, H, GH, b_mn=False, ldb=GH,
                      precision=prec, relu_src=relu_src,

@@ -79,6 +79,49 @@ def test_gemm_epilogues_and_strides():
     close(C.cpu().numpy(), ref, 2e-6, "epilogue")
 
 
+@pytest.mark.parametrize("M,N,K", [(700, 64, 32), (1000, 128, 128), (333, 512, 128)])
+@pytest.mark.parametrize("relu", [False, True])
+def test_gemm_tma_store_epilogue(M, N, K, relu):
+    """TMA-store epilogue (plain / bias / ReLU mask / fused column sums):
+    C = relu_mask(A B + bias); colsum partials reduce to the column sums of C."""
+    from paper_2309_03523_b200 import ops
+    rng = np.random.default_rng(M + N + int(relu))
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((K, N)).astype(np.float32)
+    bias = rng.standard_normal(N).astype(np.float32)
+    mask = rng.standard_normal((M, N)).astype(np.float32)
+    ref = A.astype(np.float64) @ B + bias
+    if relu:
+        ref = ref * (mask > 0)
+    C = torch.full((M, N), 3.0, device=dev)
+    tiles = (M + 127) // 128
+    cs = torch.zeros((4 * tiles, N), device=dev)
+    ops.gemm(t(A), t(B), C, M, N, K, precision=3, bias=t(bias),
+             relu_src=t(mask) if relu else None, colsum_partial=cs)
+    close(C.cpu().numpy(), ref, 2e-6, "tma-store epilogue")
+    out = torch.zeros(N, device=dev)
+    ops.reduce_rows(cs, 4 * tiles, N, out)
+    close(out.cpu().numpy(), ref.sum(0), 2e-5, "fused column sums")
+
+
+@pytest.mark.parametrize("prec,tol", [(3, 5e-6), (1, 2e-3)])
+def test_gemm_stacked_a(prec, tol):
+    """[dWx; dU] = [x; h_in]^T dgx in one launch (two A operands with their own
+    row strides), split-K, vs fp64."""
+    from paper_2309_03523_b200 import ops
+    rng = np.random.default_rng(11)
+    n, H, G = 20000, 128, 4
+    X = rng.standard_normal((n, 2 * H)).astype(np.float32)     # x with ld 2H (an h|c buffer)
+    S = rng.standard_normal((n, 7 * H)).astype(np.float32)     # save, h_in in the first H
+    dG = rng.standard_normal((n, G * H)).astype(np.float32)
+    ref = np.concatenate([X[:, :H].astype(np.float64).T @ dG, S[:, :H].astype(np.float64).T @ dG])
+    C = torch.zeros((2 * H, G * H), device=dev)
+    part = torch.zeros(ops.gemm_splits(n, prec, 96) * 2 * H * G * H, device=dev)
+    ops.gemm_stacked_a(t(X), t(S), t(dG), C, H, 2 * H, G * H, n, a_mn=True, lda0=2 * H,
+                       lda1=7 * H, ldb=G * H, ldc=G * H, precision=prec, k_splits=96, partial=part)
+    close(C.cpu().numpy(), ref, tol, "stacked A")
+
+
 def _csr(n_rows, n_cols, rng, max_deg=40):
     deg = rng.integers(0, max_deg, size=n_rows)
     deg[rng.random(n_rows) < 0.2] = 0
