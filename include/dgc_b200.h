@@ -212,13 +212,17 @@ int dgc_rnn_fwd_tc(int32_t cell, const float* gx, const float* Ut, const int32_t
                    int64_t n_rows, int32_t row_len, int32_t H, int64_t ld_out, float* h_out,
                    float* c_out, float* save, void* stream);
 /* Tensor-core BPTT (LSTM, H in {32,64,128}): takes U itself [H, 4H] (the
- * K-major B operand of dh = da U^T), dc_scratch [dgc_rnn_tc_tiles(n_rows)*128,
- * H] floats; bias_partial [dgc_rnn_tc_tiles(n_rows), 4H] (may be NULL). */
+ * K-major B operand of dh = da U^T), dc_scratch [ceil(n_rows/128)*128, H]
+ * floats; bias_partial [dgc_rnn_tc_tiles(n_rows, H), 4H] (may be NULL). */
 int dgc_rnn_bwd_tc(int32_t cell, const float* U, const int32_t* slot_row,
                    const uint8_t* slot_mask, int64_t n_rows, int32_t row_len, int32_t H,
                    const float* save, const float* dh_out, float* dgx, float* dc_scratch,
                    float* bias_partial, void* stream);
-int64_t dgc_rnn_tc_tiles(int64_t n_rows);
+/* Row tiles of the tensor-core BPTT for this H = rows of its bias_partial:
+ * 128 packed rows per tile (single-CTA kernels), or 4*rq rows per 2-CTA
+ * cluster (H = 128: rq = ceil(n_rows / 296) rows per TMEM lane quadrant, so
+ * the recurrence spans up to 74 clusters = all 148 SMs). */
+int64_t dgc_rnn_tc_tiles(int64_t n_rows, int32_t H);
 /* BPTT over the same packing (Ut = U^T, [G*H, H], see dgc_transpose): dh_out [n_inst,H] -> dgx [n_inst,G*H]
  * (d pre-activations; dWx = x^T dgx, db = colsum(dgx), dx = dgx Wx^T,
  * dU = save-operand^T dgx by K2). Carries from other devices are constants. */

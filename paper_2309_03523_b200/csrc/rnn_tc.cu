@@ -29,12 +29,6 @@ constexpr int kStages = 2;     // B ring: one (k-block, 256-column part) of U^T 
 constexpr int kChunk = 16;     // units per TMEM load / smem transpose
 constexpr int kStgStride = 17; // padded row stride of the transpose buffer (floats)
 constexpr int kStgFloats = 4 * 32 * kStgStride;  // 4 gates x 32 rows per warp
-// L2 prefetch distance (positions) of the cluster kernels; < 0 disables
-int rnn_prefetch_distance() {
-  const char* e = getenv("DGC_RNN_PF");
-  return e ? atoi(e) : 1;
-}
-
 __device__ __forceinline__ float tanh_fast(float x) {
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -199,11 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int prev = __shfl_sync(0xffffffffu, my_prev, rl);
             const float* gr = gx + (int64_t)max(inst[t], 0) * G4 + j;
 #pragma unroll
-#ifndef DGC_EXP_NOGX
             for (int gi = 0; gi < 4; ++gi) xg[t][gi] = inst[t] >= 0 ? __ldg(gr + gi * H) : 0.f;
-#else
-            for (int gi = 0; gi < 4; ++gi) xg[t][gi] = 0.f;
-#endif
             cin[t] = ci >= 0 ? carry[(int64_t)ci * 2 * H + H + j]
                              : (prev >= 0 ? c_out[(int64_t)prev * ld + j] : 0.f);
           }
@@ -224,7 +214,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float tc = tanh_fast(cn);
               hn = rna_tf32(og * tc);
               float* sv = save + (int64_t)inst[t] * 7 * H + j;
-#ifndef DGC_EXP_NOSAVE
               sv[0] = hin;
               sv[H] = cin[t];
               sv[2 * H] = ig;
@@ -232,7 +221,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               sv[4 * H] = gg;
               sv[5 * H] = og;
               sv[6 * H] = tc;
-#endif
               h_out[(int64_t)inst[t] * ld + j] = hn;
               c_out[(int64_t)inst[t] * ld + j] = cn;
             }
@@ -255,479 +243,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
 }
 
-// ---------------------------------------------------------------------------
-// Forward, 2-CTA cluster variant: the two CTAs of a cluster share one 128-row
-// tile and each owns HALF of the hidden units (all four gates of them), so the
-// epilogue-bound recurrence runs on twice the SMs. Each CTA's MMA computes its
-// 2H gate columns from the FULL h tile; the epilogues write their h halves into
-// both CTAs' A tiles (DSMEM st.shared::cluster) and arrive on both CTAs'
-// a_full; MMA completion is multicast to both CTAs' acc_full, so neither
-// epilogue overwrites an h tile the partner's MMA is still reading.
-template <int H>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    lstm_fwd_tc2_kernel(const __grid_constant__ CUtensorMap tmUt, const float* __restrict__ gx,
-                        const int32_t* __restrict__ slot_row, const uint8_t* __restrict__ slot_mask,
-                        const int32_t* __restrict__ slot_carry, const float* __restrict__ carry,
-                        int64_t R, int L, int64_t ld, float* __restrict__ h_out,
-                        float* __restrict__ c_out, float* __restrict__ save, int kPf) {
-  constexpr int G4 = 4 * H;
-  constexpr int HU = H / 2;                  // units owned by this CTA
-  constexpr int NP = 4 * HU;                 // MMA N: 4 gates x HU units (<= 256)
-  constexpr int KB = H / BK;
-  constexpr int kABytes = KB * BM * 128;
-  constexpr int kBStage = NP * 128;
-  constexpr int kUnits = HU / 2;             // units per epilogue warp (2 warps per quadrant)
-  constexpr uint32_t kTmemCols = NP <= 128 ? 128 : 256;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~(uintptr_t)1023);
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + kABytes;
-  float* stg_all = reinterpret_cast<float*>(sB + kStages * kBStage);
-  uint64_t* b_full = reinterpret_cast<uint64_t*>(stg_all + kEpiWarps * kStgFloats);
-  uint64_t* b_empty = b_full + kStages;
-  uint64_t* a_full = b_empty + kStages;
-  uint64_t* acc_full = a_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t crank = cluster_rank(), peer = crank ^ 1u;
-  const int64_t row0 = (int64_t)(blockIdx.x >> 1) * BM;
-  const int u0 = (int)crank * HU;
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&b_full[s], 1);
-      mbar_init(&b_empty[s], 1);
-    }
-    mbar_init(a_full, 2 * kEpiThreads);  // local + partner epilogue threads
-    mbar_init(acc_full, 2);              // both CTAs' MMAs (multicast commit)
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmUt) : "memory");
-  }
-  if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
-  fence_before();
-  __syncthreads();
-  cluster_sync_all();  // barriers of both CTAs initialised before any remote access
-  fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      for (int g = 0; g < L * KB; ++g) {
-        const int s = g % kStages;
-        mbar_wait(&b_empty[s], ((g / kStages) & 1) ^ 1);
-        const int kb = g % KB;
-        mbar_expect_tx(&b_full[s], (uint32_t)kBStage);
-#pragma unroll
-        for (int gi = 0; gi < 4; ++gi)  // U^T rows of gate gi, this CTA's units
-          tma_load_2d(sB + s * kBStage + gi * HU * 128, &tmUt, kb * BK, gi * H + u0, &b_full[s]);
-      }
-    }
-  } else if (warp == 1) {
-    const uint32_t idesc = idesc_tf32(NP, false, false);
-    const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
-    for (int p = 0; p < L; ++p) {
-      mbar_wait_cluster(a_full, p & 1);
-      fence_after();
-      for (int kb = 0; kb < KB; ++kb) {
-        const int g = p * KB + kb;
-        const int s = g % kStages;
-        mbar_wait(&b_full[s], (g / kStages) & 1);
-        fence_after();
-        if (lane == 0) {
-#pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk)
-            mma_tf32(tmem_base, kdesc(a_base + kb * BM * 128 + kk * 32),
-                     kdesc(b_base + s * kBStage + kk * 32), idesc, (kb > 0 || kk > 0) ? 1u : 0u);
-          mma_commit(&b_empty[s]);
-          if (kb == KB - 1) mma_commit_mc(acc_full, (uint16_t)0x3);
-        }
-        __syncwarp();
-      }
-    }
-  } else {
-    const int ew = warp - 2;
-    const int q = warp & 3;
-    const int ul0 = (ew >> 2) * kUnits;     // local unit range of this warp
-    float* stg = stg_all + ew * kStgFloats;
-    const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
-    const int uu = lane & 15, rr = lane >> 4;
-    const uint32_t sA_peer = map_peer(sA, peer);
-    auto a_off = [&](int r, int k) { return (uint32_t)((k / BK) * BM * 128) + sw128_offset(r, k % BK); };
-    auto put_h = [&](int r, int k, float v) {  // both CTAs' h tiles
-      const uint32_t off = a_off(r, k);
-      *reinterpret_cast<float*>(sA + off) = v;
-      st_cluster_f32(sA_peer + off, v);
-    };
-    for (int it = 0; it < 16; ++it) {
-      const int r = q * 32 + it * 2 + rr;
-      const int64_t row = row0 + r;
-      const int ci = row < R ? slot_carry[row * L] : -1;
-      for (int ul = ul0 + uu; ul < ul0 + kUnits; ul += 16) {
-        const int j = u0 + ul;
-        put_h(r, j, ci >= 0 ? rna_tf32(carry[(int64_t)ci * 2 * H + j]) : 0.f);
-      }
-    }
-    asm volatile("fence.proxy.async;" ::: "memory");
-    mbar_arrive(a_full);
-    mbar_arrive_cluster(map_peer(a_full, peer));
-    // L2 prefetch of the gx rows kPf positions ahead (each CTA of the pair pulls
-    // half of every row; the unit-half-0 warps issue it, one row per lane)
-    const int64_t pf_row = row0 + q * 32 + lane;
-    auto prefetch_pos = [&](int pp) {
-      if (kPf < 0 || ul0 != 0 || pp >= L || pf_row >= R) return;
-      const int inst = slot_row[pf_row * L + pp];
-      if (inst >= 0) prefetch_l2_bulk(gx + (int64_t)inst * G4 + crank * (G4 / 2), G4 * 2);
-    };
-    for (int pp = 0; pp <= kPf; ++pp) prefetch_pos(pp);
-    for (int p = 0; p < L; ++p) {
-      const bool has_next = p + 1 < L;
-      prefetch_pos(p + kPf + 1);
-      const int64_t my_row = row0 + q * 32 + lane;
-      const bool my_ok = my_row < R;
-      const int64_t my_s = my_row * L + p;
-      const int my_inst = my_ok ? slot_row[my_s] : -1;
-      const bool my_mk = my_ok && slot_mask[my_s];
-      const int my_ci = my_ok ? slot_carry[my_s] : -1;
-      const int my_prev = (p > 0 && my_mk) ? slot_row[my_s - 1] : -1;
-      const float my_mnext = (has_next && my_ok) ? (float)slot_mask[my_s + 1] : 0.f;
-      const int my_cnext = (has_next && my_ok) ? slot_carry[my_s + 1] : -1;
-      mbar_wait_cluster(acc_full, p & 1);
-      fence_after();
-#pragma unroll 1
-      for (int c0 = ul0; c0 < ul0 + kUnits; c0 += kChunk) {
-#pragma unroll
-        for (int gi = 0; gi < 4; ++gi) {
-          float a[16];
-          tmem_ld16(tl + gi * HU + c0, a);
-#pragma unroll
-          for (int u = 0; u < 16; ++u) stg[(gi * 32 + lane) * kStgStride + u] = a[u];
-        }
-        __syncwarp();
-        const int j = u0 + c0 + uu;  // global unit of this lane
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          float xg[8][4], cin[8];
-          int inst[8];
-#pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            const int rl = (half * 8 + t) * 2 + rr;
-            inst[t] = __shfl_sync(0xffffffffu, my_inst, rl);
-            const int ci = __shfl_sync(0xffffffffu, my_ci, rl);
-            const int prev = __shfl_sync(0xffffffffu, my_prev, rl);
-            const float* gr = gx + (int64_t)max(inst[t], 0) * G4 + j;
-#pragma unroll
-            for (int gi = 0; gi < 4; ++gi) xg[t][gi] = inst[t] >= 0 ? __ldg(gr + gi * H) : 0.f;
-            cin[t] = ci >= 0 ? carry[(int64_t)ci * 2 * H + H + j]
-                             : (prev >= 0 ? c_out[(int64_t)prev * ld + j] : 0.f);
-          }
-#pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            const int rl = (half * 8 + t) * 2 + rr;
-            const int r = q * 32 + rl;
-            const float m_next = __shfl_sync(0xffffffffu, my_mnext, rl);
-            const int c_next = __shfl_sync(0xffffffffu, my_cnext, rl);
-            const float hin = *reinterpret_cast<const float*>(sA + a_off(r, j));
-            float hn = 0.f;
-            if (inst[t] >= 0) {
-              const float ig = sigm(stg[(0 * 32 + rl) * kStgStride + uu] + xg[t][0]);
-              const float fg = sigm(stg[(1 * 32 + rl) * kStgStride + uu] + xg[t][1]);
-              const float gg = tanh_fast(stg[(2 * 32 + rl) * kStgStride + uu] + xg[t][2]);
-              const float og = sigm(stg[(3 * 32 + rl) * kStgStride + uu] + xg[t][3]);
-              const float cn = fg * cin[t] + ig * gg;
-              const float tc = tanh_fast(cn);
-              hn = rna_tf32(og * tc);
-              float* sv = save + (int64_t)inst[t] * 7 * H + j;
-              sv[0] = hin;
-              sv[H] = cin[t];
-              sv[2 * H] = ig;
-              sv[3 * H] = fg;
-              sv[4 * H] = gg;
-              sv[5 * H] = og;
-              sv[6 * H] = tc;
-              h_out[(int64_t)inst[t] * ld + j] = hn;
-              c_out[(int64_t)inst[t] * ld + j] = cn;
-            }
-            if (has_next)
-              put_h(r, j, c_next >= 0 ? rna_tf32(carry[(int64_t)c_next * 2 * H + j]) : hn * m_next);
-          }
-        }
-        __syncwarp();
-      }
-      if (has_next) {
-        fence_before();
-        asm volatile("fence.proxy.async;" ::: "memory");
-        mbar_arrive(a_full);
-        mbar_arrive_cluster(map_peer(a_full, peer));
-      }
-    }
-  }
-  fence_before();
-  __syncthreads();
-  cluster_sync_all();  // the partner may still be writing into our shared memory
-  if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
-}
-
-// Forward, 2-CTA cluster variant with EW epilogue warps: EW/4 warps per TMEM
-// lane quadrant, each owning 32/(EW/4) rows and all HU units of this CTA (16-unit
-// chunks, transposed through shared memory so lanes = (row parity, unit)). The
-// carried c of a cell stays in registers (a thread owns the same cells at every
-// position), so only run starts with a cross-device predecessor read memory.
-template <int H, int EW>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
-    lstm_fwd_tc2w_kernel(const __grid_constant__ CUtensorMap tmUt, const float* __restrict__ gx,
-                         const int32_t* __restrict__ slot_row, const uint8_t* __restrict__ slot_mask,
-                         const int32_t* __restrict__ slot_carry, const float* __restrict__ carry,
-                         int64_t R, int L, int64_t ld, float* __restrict__ h_out,
-                         float* __restrict__ c_out, float* __restrict__ save, int kPf) {
-  constexpr int kEpiT = 32 * EW;
-  constexpr int WPQ = EW / 4;
-  constexpr int RPW = 32 / WPQ;              // rows per warp (even)
-  constexpr int NT = RPW / 2;                // row pairs per chunk
-  constexpr int G4 = 4 * H;
-  constexpr int HU = H / 2;
-  constexpr int NCH = HU / kChunk;           // 16-unit chunks per CTA
-  constexpr int NP = 4 * HU;
-  constexpr int KB = H / BK;
-  constexpr int kABytes = KB * BM * 128;
-  constexpr int kBStage = NP * 128;
-  constexpr int kStgW = 4 * RPW * kStgStride;
-  constexpr uint32_t kTmemCols = NP <= 128 ? 128 : 256;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~(uintptr_t)1023);
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + kABytes;
-  float* stg_all = reinterpret_cast<float*>(sB + kStages * kBStage);
-  float* c_all = stg_all + EW * kStgW;       // carried c: [EW][NCH][NT][32]
-  uint64_t* b_full = reinterpret_cast<uint64_t*>(c_all + EW * NCH * NT * 32);
-  uint64_t* b_empty = b_full + kStages;
-  uint64_t* a_full = b_empty + kStages;
-  uint64_t* acc_full = a_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t crank = cluster_rank(), peer = crank ^ 1u;
-  const int64_t row0 = (int64_t)(blockIdx.x >> 1) * BM;
-  const int u0 = (int)crank * HU;
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&b_full[s], 1);
-      mbar_init(&b_empty[s], 1);
-    }
-    mbar_init(a_full, 2 * kEpiT);
-    mbar_init(acc_full, 2);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmUt) : "memory");
-  }
-  if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
-  fence_before();
-  __syncthreads();
-  cluster_sync_all();
-  fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      for (int g = 0; g < L * KB; ++g) {
-        const int s = g % kStages;
-        mbar_wait(&b_empty[s], ((g / kStages) & 1) ^ 1);
-        const int kb = g % KB;
-        mbar_expect_tx(&b_full[s], (uint32_t)kBStage);
-#pragma unroll
-        for (int gi = 0; gi < 4; ++gi)
-          tma_load_2d(sB + s * kBStage + gi * HU * 128, &tmUt, kb * BK, gi * H + u0, &b_full[s]);
-      }
-    }
-  } else if (warp == 1) {
-    const uint32_t idesc = idesc_tf32(NP, false, false);
-    const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
-    for (int p = 0; p < L; ++p) {
-      mbar_wait_cluster(a_full, p & 1);
-      fence_after();
-      if (blockIdx.x == 0 && lane == 0 && p < 256) g_lstm_ts[p][0] = globaltimer();
-      for (int kb = 0; kb < KB; ++kb) {
-        const int g = p * KB + kb;
-        const int s = g % kStages;
-        mbar_wait(&b_full[s], (g / kStages) & 1);
-        fence_after();
-        if (lane == 0) {
-#pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk)
-            mma_tf32(tmem_base, kdesc(a_base + kb * BM * 128 + kk * 32),
-                     kdesc(b_base + s * kBStage + kk * 32), idesc, (kb > 0 || kk > 0) ? 1u : 0u);
-          mma_commit(&b_empty[s]);
-          if (kb == KB - 1) mma_commit_mc(acc_full, (uint16_t)0x3);
-        }
-        __syncwarp();
-      }
-    }
-  } else {
-    const int ew = warp - 2;
-    const int q = warp & 3;
-    const int rb = (ew >> 2) * RPW;          // first quadrant row of this warp
-    float* stg = stg_all + ew * kStgW;
-    const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
-    const int uu = lane & 15, rr = lane >> 4;
-    const uint32_t sA_peer = map_peer(sA, peer);
-    auto a_off = [&](int r, int k) { return (uint32_t)((k / BK) * BM * 128) + sw128_offset(r, k % BK); };
-    auto put_h = [&](int r, int k, float v) {
-      const uint32_t off = a_off(r, k);
-      *reinterpret_cast<float*>(sA + off) = v;
-#ifndef DGC_EXP_NODSMEM
-      st_cluster_f32(sA_peer + off, v);
-#endif
-    };
-    const int64_t my_row = row0 + q * 32 + lane;
-    const bool my_ok = my_row < R;
-    // prologue: h_in of position 0 for this warp's rows (run start: carry or zero)
-#pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      const int r = q * 32 + rb + 2 * t + rr;
-      const int64_t row = row0 + r;
-      const int ci = row < R ? slot_carry[row * L] : -1;
-      for (int ul = uu; ul < HU; ul += 16) {
-        const int j = u0 + ul;
-        put_h(r, j, ci >= 0 ? rna_tf32(carry[(int64_t)ci * 2 * H + j]) : 0.f);
-      }
-    }
-    asm volatile("fence.proxy.async;" ::: "memory");
-    mbar_arrive(a_full);
-    mbar_arrive_cluster(map_peer(a_full, peer));
-    auto prefetch_pos = [&](int pp) {
-      if (kPf < 0 || pp >= L || !my_ok || (ew >> 2) != 0) return;
-      const int inst = slot_row[my_row * L + pp];
-      if (inst >= 0) prefetch_l2_bulk(gx + (int64_t)inst * G4 + crank * (G4 / 2), G4 * 2);
-    };
-    for (int pp = 0; pp <= kPf; ++pp) prefetch_pos(pp);
-    float* creg = c_all + ew * NCH * NT * 32 + lane;  // [ch][t] at (ch * NT + t) * 32
-    // per-row slot info (lane = quadrant row), loaded one position ahead
-    int n_inst = my_ok ? slot_row[my_row * L] : -1;
-    int n_mk = 0;  // mask of position 0 is always 0
-    int n_ci = my_ok ? slot_carry[my_row * L] : -1;
-    for (int p = 0; p < L; ++p) {
-      const bool has_next = p + 1 < L;
-      prefetch_pos(p + kPf + 1);
-      const int my_inst = n_inst, my_mk = n_mk, my_ci = n_ci;
-      if (has_next && my_ok) {
-        const int64_t s1 = my_row * L + p + 1;
-        n_inst = slot_row[s1];
-        n_mk = slot_mask[s1];
-        n_ci = slot_carry[s1];
-      } else {
-        n_inst = -1; n_mk = 0; n_ci = -1;
-      }
-      const float my_mnext = (float)n_mk;
-      const int my_cnext = n_ci;
-      mbar_wait_cluster(acc_full, p & 1);
-      fence_after();
-      if (blockIdx.x == 0 && threadIdx.x == 64 && p < 256) g_lstm_ts[p][1] = globaltimer();
-#pragma unroll 1
-      for (int ch = 0; ch < NCH; ++ch) {
-        const int c0 = ch * kChunk;
-#pragma unroll
-        for (int gi = 0; gi < 4; ++gi) {
-          float a[16];
-          tmem_ld16(tl + gi * HU + c0, a);
-          if (lane >= rb && lane < rb + RPW) {
-#pragma unroll
-            for (int u = 0; u < 16; ++u) stg[(gi * RPW + lane - rb) * kStgStride + u] = a[u];
-          }
-        }
-        __syncwarp();
-        const int j = u0 + c0 + uu;
-        float xg[NT][4], cin[NT];
-        int inst[NT];
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          const int rl = rb + 2 * t + rr;
-          inst[t] = __shfl_sync(0xffffffffu, my_inst, rl);
-          const int ci = __shfl_sync(0xffffffffu, my_ci, rl);
-          const int mk = __shfl_sync(0xffffffffu, my_mk, rl);
-          const float* gr = gx + (int64_t)max(inst[t], 0) * G4 + j;
-#pragma unroll
-#ifdef DGC_EXP_NOLOAD
-          for (int gi = 0; gi < 4; ++gi) xg[t][gi] = 0.01f * (float)((inst[t] + gi) & 7);
-#else
-          for (int gi = 0; gi < 4; ++gi) xg[t][gi] = inst[t] >= 0 ? __ldg(gr + gi * H) : 0.f;
-#endif
-          cin[t] = ci >= 0 ? carry[(int64_t)ci * 2 * H + H + j] : (mk ? creg[(ch * NT + t) * 32] : 0.f);
-        }
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          const int rl = rb + 2 * t + rr;
-          const int r = q * 32 + rl;
-          const int sl = 2 * t + rr;         // row within this warp's stg
-          const float m_next = __shfl_sync(0xffffffffu, my_mnext, rl);
-          const int c_next = __shfl_sync(0xffffffffu, my_cnext, rl);
-          const float hin = *reinterpret_cast<const float*>(sA + a_off(r, j));
-          float hn = 0.f, cn = 0.f;
-          if (inst[t] >= 0) {
-            const float ig = sigm(stg[(0 * RPW + sl) * kStgStride + uu] + xg[t][0]);
-            const float fg = sigm(stg[(1 * RPW + sl) * kStgStride + uu] + xg[t][1]);
-            const float gg = tanh_fast(stg[(2 * RPW + sl) * kStgStride + uu] + xg[t][2]);
-            const float og = sigm(stg[(3 * RPW + sl) * kStgStride + uu] + xg[t][3]);
-            cn = fg * cin[t] + ig * gg;
-            const float tc = tanh_fast(cn);
-            hn = rna_tf32(og * tc);
-#ifndef DGC_EXP_NOSTORE
-            float* sv = save + (int64_t)inst[t] * 7 * H + j;
-            sv[0] = hin;
-            sv[H] = cin[t];
-            sv[2 * H] = ig;
-            sv[3 * H] = fg;
-            sv[4 * H] = gg;
-            sv[5 * H] = og;
-            sv[6 * H] = tc;
-            h_out[(int64_t)inst[t] * ld + j] = hn;
-            c_out[(int64_t)inst[t] * ld + j] = cn;
-#else
-            if (hn + hin + tc == 1234.5f) save[0] = hn;
-#endif
-          }
-          creg[(ch * NT + t) * 32] = cn;
-          if (has_next)
-            put_h(r, j, c_next >= 0 ? rna_tf32(carry[(int64_t)c_next * 2 * H + j]) : hn * m_next);
-        }
-        __syncwarp();
-      }
-      if (blockIdx.x == 0 && threadIdx.x == 64 && p < 256) g_lstm_ts[p][2] = globaltimer();
-      if (has_next) {
-        fence_before();
-        asm volatile("fence.proxy.async;" ::: "memory");
-        mbar_arrive(a_full);
-        mbar_arrive_cluster(map_peer(a_full, peer));
-      }
-    }
-  }
-  fence_before();
-  __syncthreads();
-  cluster_sync_all();
-  if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
-}
-
-template <int H, int EW>
-int launch_lstm_tc2w(const float* gx, const float* Ut, const int32_t* slot_row,
-                     const uint8_t* slot_mask, const int32_t* slot_carry, const float* carry,
-                     int64_t R, int L, int64_t ld, float* h_out, float* c_out, float* save,
-                     cudaStream_t s) {
-  CUtensorMap m;
-  int rc = make_map(&m, Ut, 4 * H, H, H, 32, H / 2, false);
-  if (rc) return rc;
-  constexpr int RPW = 32 / (EW / 4);
-  const size_t smem = (size_t)(H / BK) * BM * 128 + (size_t)kStages * 2 * H * 128 +
-                      (size_t)EW * 4 * RPW * kStgStride * 4 + (size_t)EW * (H / 32) * (RPW / 2) * 128 +
-                      1024 + 256;
-  auto kern = lstm_fwd_tc2w_kernel<H, EW>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_fwd_tc2w: set smem");
-  const int grid = 2 * (int)((R + BM - 1) / BM);
-  kern<<<grid, 64 + 32 * EW, smem, s>>>(m, gx, slot_row, slot_mask, slot_carry, carry, R, L, ld,
-                                        h_out, c_out, save, rnn_prefetch_distance());
-  DGC_CHECK_LAUNCH("lstm_fwd_tc2w_kernel");
-  return DGC_OK;
-}
-
 // Forward, 2-CTA cluster, vectorised epilogue (16 warps = 4 per TMEM lane
 // quadrant, 8 rows each). A lane owns one row and 4 consecutive units of a
 // 16-unit chunk (lane = 8 rows x 4 unit quads), so every global / shared / DSMEM
@@ -735,6 +250,17 @@ int launch_lstm_tc2w(const float* gx, const float* Ut, const int32_t* slot_row,
 // shuffles). The carried c stays in shared memory per lane (same cells at every
 // position); the next chunk's gx loads are issued before the current chunk's math.
 constexpr int kVEW = 16;
+// Row tiling of the 2-CTA cluster kernels: a cluster owns 4 x rq packed rows
+// (rq per TMEM lane quadrant, rows q*32 + [0, rq) of its 128-row MMA tile) with
+// rq = ceil(R / (4 * 74)) <= 32, so R rows spread over <= 74 clusters = 148 SMs.
+inline int cluster_rows_per_quadrant(int64_t R) {
+  const int64_t per = (R + 4 * (dgc::kNumSMs / 2) - 1) / (4 * (dgc::kNumSMs / 2));
+  return (int)(per < 1 ? 1 : per > 32 ? 32 : per);
+}
+inline int64_t cluster_tiles(int64_t R) {
+  const int64_t rows = 4 * (int64_t)cluster_rows_per_quadrant(R);
+  return (R + rows - 1) / rows;
+}
 __device__ __forceinline__ float4 f4(const float* p) { return *reinterpret_cast<const float4*>(p); }
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 __device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
@@ -746,7 +272,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
                          const int32_t* __restrict__ slot_row, const uint8_t* __restrict__ slot_mask,
                          const int32_t* __restrict__ slot_carry, const float* __restrict__ carry,
                          int64_t R, int L, int64_t ld, float* __restrict__ h_out,
-                         float* __restrict__ c_out, float* __restrict__ save) {
+                         float* __restrict__ c_out, float* __restrict__ save, int rq) {
   constexpr int kEpiT = 32 * kVEW;
   constexpr int G4 = 4 * H;
   constexpr int HU = H / 2;
@@ -772,14 +298,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cluster_rank(), peer = crank ^ 1u;
-  const int64_t row0 = (int64_t)(blockIdx.x >> 1) * BM;
+  // the cluster's packed rows: rq per TMEM lane quadrant (rq <= 32), so the
+  // recurrence spreads over ~all SMs instead of R/128 tiles
+  const int64_t row0 = (int64_t)(blockIdx.x >> 1) * 4 * rq;
   const int u0 = (int)crank * HU;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&b_full[s], 1);
       mbar_init(&b_empty[s], 1);
     }
-    mbar_init(a_full, 2 * kEpiT);
+    // local epilogue threads arrive (CTA scope); the peer's half of the h tile
+    // lands by st.async (complete_tx), expected by one local arrive.expect_tx
+    mbar_init(a_full, kEpiT);
     mbar_init(acc_full, 2);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmUt) : "memory");
@@ -807,8 +337,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
     const uint32_t idesc = idesc_tf32(NP, false, false);
     const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
     for (int p = 0; p < L; ++p) {
-      mbar_wait_cluster(a_full, p & 1);
+      mbar_wait(a_full, p & 1);
       fence_after();
+      // generic-proxy writes (local st.shared, peer st.async) -> async proxy (MMA)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       if (blockIdx.x == 0 && lane == 0 && p < 256) g_lstm_ts[p][0] = globaltimer();
       for (int kb = 0; kb < KB; ++kb) {
         const int g = p * KB + kb;
@@ -831,23 +363,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
     const int q = warp & 3;                  // TMEM lane quadrant (warp id % 4)
     const int rb = (ew >> 2) * 8;            // first quadrant row of this warp
     const int r8 = lane >> 2, uq = lane & 3;
-    const int r = q * 32 + rb + r8;          // tile row of this lane
-    const int64_t grow = row0 + r;
-    const bool ok = grow < R;
+    const int r = q * 32 + rb + r8;          // tile (TMEM lane / A) row of this lane
+    const int64_t grow = row0 + q * rq + rb + r8;
+    const bool ok = rb + r8 < rq && grow < R;
+    const bool active = rb < rq;             // warps with no rows only keep the protocol
     float* stg = stg_all + ew * kStgW;
     float* creg = c_all + (ew * NCH * 32 + lane) * 4;  // + ch * 128
     const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
     const uint32_t sA_peer = map_peer(sA, peer);
+    const uint32_t afull_peer = map_peer(a_full, peer);
     auto a_off = [&](int k) { return (uint32_t)((k / BK) * BM * 128) + sw128_offset(r, k % BK); };
     auto put_h = [&](int k, float4 v) {
       const uint32_t off = a_off(k);
       st4(reinterpret_cast<float*>(sA + off), v);
-#ifndef DGC_EXP_NODSMEM
-      st_cluster_v4(sA_peer + off, v);
-#endif
+      st_async_v4(sA_peer + off, v, afull_peer);
+    };
+    // bytes of the peer's half of the h tile it writes into ours: 8 rows x HU
+    // units per active warp (4 quadrants x ceil(rq / 8) warps)
+    const uint32_t kPeerBytes = 4u * (uint32_t)((rq + 7) / 8) * 8u * HU * 4u;
+    auto publish = [&]() {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (ew == 0 && lane == 0) mbar_arrive_expect_tx(a_full, kPeerBytes);
+      else mbar_arrive(a_full);
     };
     // prologue: h_in of position 0 (run start: carry or zero)
-    {
+    if (active) {
       const int ci = ok ? slot_carry[grow * L] : -1;
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) {
@@ -861,9 +401,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
         st4(creg + ch * 128, zero4());
       }
     }
-    asm volatile("fence.proxy.async;" ::: "memory");
-    mbar_arrive(a_full);
-    mbar_arrive_cluster(map_peer(a_full, peer));
+    publish();
     int n_inst = ok ? slot_row[grow * L] : -1, n_mk = 0, n_ci = ok ? slot_carry[grow * L] : -1;
     for (int p = 0; p < L; ++p) {
       const bool has_next = p + 1 < L;
@@ -877,14 +415,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
         n_inst = -1; n_mk = 0; n_ci = -1;
       }
       const float m_next = (float)n_mk;
+      if (!active) {  // keep the a_full phase order: step p's MMA done first
+        mbar_wait(acc_full, p & 1);
+        if (has_next) publish();
+        continue;
+      }
       const float* gxr = gx + (int64_t)max(inst, 0) * G4 + u0 + uq * 4;
       float4 xg[4];
 #pragma unroll
       for (int gi = 0; gi < 4; ++gi) xg[gi] = inst >= 0 ? ldg4(gxr + gi * H) : zero4();
-#ifdef DGC_EXP_NOLOAD
-      for (int gi = 0; gi < 4; ++gi) xg[gi] = make_float4(0.01f * gi, 0.02f, 0.03f * (inst & 3), 0.f);
-#endif
-      mbar_wait_cluster(acc_full, p & 1);
+      mbar_wait(acc_full, p & 1);
       fence_after();
       if (blockIdx.x == 0 && threadIdx.x == 64 && p < 256) g_lstm_ts[p][1] = globaltimer();
 #pragma unroll 1
@@ -893,12 +433,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
         const int j = u0 + c0 + uq * 4;
         {
           float a[64];
-#ifndef DGC_EXP_NOTMEM
           tmem_ld16x4(tl + c0, tl + HU + c0, tl + 2 * HU + c0, tl + 3 * HU + c0, a);
-#else
-#pragma unroll
-          for (int u = 0; u < 64; ++u) a[u] = 0.01f * (float)((lane + u) & 7);
-#endif
           if (lane >= rb && lane < rb + 8) {
 #pragma unroll
             for (int gi = 0; gi < 4; ++gi) {
@@ -918,11 +453,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
         float4 xn[4];
 #pragma unroll
         for (int gi = 0; gi < 4; ++gi)
-#ifndef DGC_EXP_NOLOAD
           xn[gi] = (inst >= 0 && ch + 1 < NCH) ? ldg4(gxr + gi * H + c0 + 16) : zero4();
-#else
-          xn[gi] = make_float4(0.01f * gi, 0.02f * ch, 0.03f * (inst & 3), 0.f);
-#endif
         float4 cin = zero4();
         if (ci >= 0) cin = f4(carry + (int64_t)ci * 2 * H + H + j);
         else if (mk) cin = f4(creg + ch * 128);
@@ -940,7 +471,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   hn.c = rna_tf32(og.c * tc.c);
           DGC_LSTM_CELL(x) DGC_LSTM_CELL(y) DGC_LSTM_CELL(z) DGC_LSTM_CELL(w)
 #undef DGC_LSTM_CELL
-#ifndef DGC_EXP_NOSTORE
           float* sv = save + (int64_t)inst * 7 * H + j;
           st4(sv, hin);
           st4(sv + H, cin);
@@ -951,9 +481,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           st4(sv + 6 * H, tc);
           st4(h_out + (int64_t)inst * ld + j, hn);
           st4(c_out + (int64_t)inst * ld + j, cn);
-#else
-          if (hn.x + tc.y + hin.z + og.w + ig.x + fg.y + gg.z == 1234.5f) save[0] = 1.f;
-#endif
         }
         st4(creg + ch * 128, cn);
         if (has_next) {
@@ -973,9 +500,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       if (blockIdx.x == 0 && threadIdx.x == 64 && p < 256) g_lstm_ts[p][2] = globaltimer();
       if (has_next) {
         fence_before();
-        asm volatile("fence.proxy.async;" ::: "memory");
-        mbar_arrive(a_full);
-        mbar_arrive_cluster(map_peer(a_full, peer));
+        publish();
       }
     }
   }
@@ -999,30 +524,11 @@ int launch_lstm_tc2v(const float* gx, const float* Ut, const int32_t* slot_row,
   auto kern = lstm_fwd_tc2v_kernel<H>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_fwd_tc2v: set smem");
-  const int grid = 2 * (int)((R + BM - 1) / BM);
+  const int rq = cluster_rows_per_quadrant(R);
+  const int grid = 2 * (int)cluster_tiles(R);
   kern<<<grid, 64 + 32 * kVEW, smem, s>>>(m, gx, slot_row, slot_mask, slot_carry, carry, R, L, ld,
-                                          h_out, c_out, save);
+                                          h_out, c_out, save, rq);
   DGC_CHECK_LAUNCH("lstm_fwd_tc2v_kernel");
-  return DGC_OK;
-}
-
-template <int H>
-int launch_lstm_tc2(const float* gx, const float* Ut, const int32_t* slot_row,
-                    const uint8_t* slot_mask, const int32_t* slot_carry, const float* carry,
-                    int64_t R, int L, int64_t ld, float* h_out, float* c_out, float* save,
-                    cudaStream_t s) {
-  CUtensorMap m;
-  int rc = make_map(&m, Ut, 4 * H, H, H, 32, H / 2, false);
-  if (rc) return rc;
-  const size_t smem = (size_t)(H / BK) * BM * 128 + (size_t)kStages * 2 * H * 128 +
-                      (size_t)kEpiWarps * kStgFloats * 4 + 1024 + 256;
-  auto kern = lstm_fwd_tc2_kernel<H>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_fwd_tc2: set smem");
-  const int grid = 2 * (int)((R + BM - 1) / BM);
-  kern<<<grid, kThreads, smem, s>>>(m, gx, slot_row, slot_mask, slot_carry, carry, R, L, ld,
-                                    h_out, c_out, save, rnn_prefetch_distance());
-  DGC_CHECK_LAUNCH("lstm_fwd_tc2_kernel");
   return DGC_OK;
 }
 
@@ -1264,288 +770,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 }
 
 // Backward, 2-CTA cluster variant (H = 128): CTA c owns hidden units
-// [c*H/2, (c+1)*H/2). Its epilogue computes da for those units (8 of the 16
-// da k-blocks per position) and writes them into BOTH CTAs' A rings (DSMEM);
-// each CTA's MMA then forms dh_prev for its own units only (N = H/2) from all
-// 16 k-blocks. Ring slots are released by a multicast commit from both MMAs.
-// k-block sequence per position interleaves the owners: chunk order 0, 2, 1, 3.
-template <int H>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBwdThreads, 1)
-    lstm_bwd_tc2_kernel(const __grid_constant__ CUtensorMap tmU, const int32_t* __restrict__ slot_row,
-                        const uint8_t* __restrict__ slot_mask, int64_t R, int L,
-                        const float* __restrict__ save, const float* __restrict__ dh_out,
-                        float* __restrict__ dgx, float* __restrict__ dc_scr, int rnd,
-                        float* __restrict__ bias_partial, int kPf) {
-  static_assert(H == 128, "cluster BPTT is specialised for H = 128");
-  constexpr int kRB = 8;                     // rows per load batch (memory-level parallelism)
-  constexpr int G4 = 4 * H;
-  constexpr int HU = H / 2;
-  constexpr int NC = H / 32;                 // 32-unit chunks (4)
-  constexpr int KB = G4 / BK;                // 16 da k-blocks per position
-  constexpr int kAStage = BM * 128;
-  constexpr int kBStage = HU * 128;          // HU rows of U x 32 k
-  constexpr uint32_t kTmemCols = 128;        // 2 x HU accumulators
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~(uintptr_t)1023);
-  uint8_t* sA = smem;
-  uint8_t* sB = sA + kBwdAStages * kAStage;
-  float* stg_all = reinterpret_cast<float*>(sB + kBwdBStages * kBStage);
-  uint64_t* a_full = reinterpret_cast<uint64_t*>(stg_all + kBwdEpiWarps * 32 * 33);
-  uint64_t* a_empty = a_full + kBwdAStages;
-  uint64_t* b_full = a_empty + kBwdAStages;
-  uint64_t* b_empty = b_full + kBwdBStages;
-  uint64_t* acc_full = b_empty + kBwdBStages;   // [2]
-  uint64_t* acc_empty = acc_full + 2;           // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t crank = cluster_rank(), peer = crank ^ 1u;
-  const int64_t tile = blockIdx.x >> 1;
-  const int64_t row0 = tile * BM;
-  const int u0 = (int)crank * HU;
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < kBwdAStages; ++s) {
-      mbar_init(&a_full[s], kBwdEpiThreads);  // all 8 epilogue warps of the owner CTA
-      mbar_init(&a_empty[s], 2);    // both MMAs (multicast commit)
-    }
-    for (int s = 0; s < kBwdBStages; ++s) {
-      mbar_init(&b_full[s], 1);
-      mbar_init(&b_empty[s], 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&acc_full[a], 1);
-      mbar_init(&acc_empty[a], kBwdEpiThreads);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmU) : "memory");
-  }
-  if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
-  fence_before();
-  __syncthreads();
-  cluster_sync_all();
-  fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  // sequence position m (0..NC-1) -> chunk (interleaved owners)
-  auto chunk_at = [](int m) { return (m & 1) * (NC / 2) + (m >> 1); };
-
-  if (warp == 0) {
-    if (lane == 0) {
-      for (int seq = 0; seq < L * KB; ++seq) {
-        const int s = seq % kBwdBStages;
-        mbar_wait(&b_empty[s], ((seq / kBwdBStages) & 1) ^ 1);
-        const int i = seq % KB, c = chunk_at(i >> 2), g = i & 3;
-        mbar_expect_tx(&b_full[s], (uint32_t)kBStage);
-        tma_load_2d(sB + s * kBStage, &tmU, g * H + 32 * c, u0, &b_full[s]);
-      }
-    }
-  } else if (warp == 1) {
-    const uint32_t idesc = idesc_tf32(HU, false, false);
-    const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
-    for (int t = 0; t < L; ++t) {
-      const int p = L - 1 - t;
-      const int a = p & 1;
-      mbar_wait(&acc_empty[a], ((t >> 1) & 1) ^ 1);
-      fence_after();
-      for (int i = 0; i < KB; ++i) {
-        const int seq = t * KB + i;
-        const int sa = seq % kBwdAStages, sb = seq % kBwdBStages;
-        mbar_wait_cluster(&a_full[sa], (seq / kBwdAStages) & 1);
-        mbar_wait(&b_full[sb], (seq / kBwdBStages) & 1);
-        fence_after();
-        if (lane == 0) {
-#pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk)
-            mma_tf32(tmem_base + a * HU, kdesc(a_base + sa * kAStage + kk * 32),
-                     kdesc(b_base + sb * kBStage + kk * 32), idesc, (i > 0 || kk > 0) ? 1u : 0u);
-          mma_commit_mc(&a_empty[sa], (uint16_t)0x3);
-          mma_commit(&b_empty[sb]);
-          if (i == KB - 1) mma_commit(&acc_full[a]);
-        }
-        __syncwarp();
-      }
-    }
-  } else {
-    // All 8 epilogue warps work on one 32-unit chunk at a time, in k-block
-    // sequence order (warp = quadrant q x row half h: 16 rows each), so a ring
-    // slot is never waited on by warps that could be working on another chunk.
-    const int ew = warp - 2;
-    const int q = warp & 3;
-    const int h = ew >> 2;                  // row half of the quadrant
-    float* stg = stg_all + ew * 32 * 33;
-    const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
-    const uint32_t sA_peer = map_peer(sA, peer);
-    const int64_t my_row = row0 + q * 32 + lane;
-    const bool my_ok = my_row < R;
-    float bsum[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-    // L2 prefetch kPf positions ahead (backwards): row-half-0 warps pull half of
-    // the saved-activation row, row-half-1 warps this CTA's half of dh_out
-    auto prefetch_pos = [&](int pp) {
-      if (kPf < 0 || pp < 0 || !my_ok) return;
-      const int inst = slot_row[my_row * L + pp];
-      if (inst < 0) return;
-      if (h == 0)
-        prefetch_l2_bulk(save + (int64_t)inst * 7 * H + crank * (7 * H / 2), 7 * H * 2);
-      else
-        prefetch_l2_bulk(dh_out + (int64_t)inst * H + u0, HU * 4);
-    };
-    for (int pp = L - 1; pp >= L - 1 - kPf; --pp) prefetch_pos(pp);
-    for (int t = 0; t < L; ++t) {
-      const int p = L - 1 - t;
-      const bool has_next = p + 1 < L;
-      prefetch_pos(p - kPf - 1);
-      const int64_t my_s = my_row * L + p;
-      const int my_inst = my_ok ? slot_row[my_s] : -1;
-      const float my_m = my_ok ? (float)slot_mask[my_s] : 0.f;
-      const float my_mnext = (has_next && my_ok) ? (float)slot_mask[my_s + 1] : 0.f;
-      if (blockIdx.x == 0 && threadIdx.x == 64 && t < 256) g_lstm_ts[t][0] = globaltimer();
-      if (has_next) {
-        mbar_wait(&acc_full[(p + 1) & 1], ((t - 1) >> 1) & 1);
-        fence_after();
-        if (blockIdx.x == 0 && threadIdx.x == 64 && t < 256) g_lstm_ts[t][1] = globaltimer();
-      }
-#pragma unroll 1
-      for (int lc = 0; lc < 2; ++lc) {
-        const int c = (int)crank * (NC / 2) + lc;  // global 32-unit chunk
-        const int m = 2 * lc + (int)crank;         // position in the k-block sequence
-        const int j = 32 * c + lane;
-        if (has_next) {
-          float v[32];
-          tmem_ld32(tl + ((p + 1) & 1) * HU + 32 * lc, v);
-#pragma unroll
-          for (int u = 0; u < 32; ++u) stg[lane * 33 + u] = v[u];
-        }
-        __syncwarp();
-        const int seq0 = t * KB + m * 4;
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          const int seq = seq0 + g;
-          mbar_wait(&a_empty[seq % kBwdAStages], ((seq / kBwdAStages) & 1) ^ 1);
-        }
-#pragma unroll 1
-        for (int r0 = 16 * h; r0 < 16 * h + 16; r0 += kRB) {
-          float ld[kRB][6], dhv[kRB], dcv[kRB];
-          int inst[kRB];
-#pragma unroll
-          for (int u = 0; u < kRB; ++u) {
-            const int rl = r0 + u;
-            inst[u] = __shfl_sync(0xffffffffu, my_inst, rl);
-            const float mn = __shfl_sync(0xffffffffu, my_mnext, rl);
-            const int64_t trow = row0 + q * 32 + rl;
-            dhv[u] = has_next ? mn * stg[rl * 33 + lane] : 0.f;
-#ifdef DGC_EXP_NOLOAD
-            dcv[u] = has_next ? 0.5f : 0.f;
-            if (inst[u] >= 0) {
-              dhv[u] += 0.25f * (float)(inst[u] & 7);
-#pragma unroll
-              for (int k = 0; k < 6; ++k) ld[u][k] = 0.1f * k + 1e-3f * (float)(inst[u] & 15);
-            } else {
-#else
-            dcv[u] = has_next ? dc_scr[trow * H + j] : 0.f;
-            if (inst[u] >= 0) {
-              dhv[u] += dh_out[(int64_t)inst[u] * H + j];
-              const float* sv = save + (int64_t)inst[u] * 7 * H + j;
-#pragma unroll
-              for (int k = 0; k < 6; ++k) ld[u][k] = sv[(k + 1) * H];
-            } else {
-#endif
-#pragma unroll
-              for (int k = 0; k < 6; ++k) ld[u][k] = 0.f;
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < kRB; ++u) {
-            const int rl = r0 + u;
-            const int r = q * 32 + rl;
-            const float mp = __shfl_sync(0xffffffffu, my_m, rl);
-            const int64_t trow = row0 + r;
-            float da[4] = {0.f, 0.f, 0.f, 0.f};
-            float dcp = 0.f;
-            if (inst[u] >= 0) {
-              const float c_in = ld[u][0], ig = ld[u][1], fg = ld[u][2], gg = ld[u][3],
-                          og = ld[u][4], tc = ld[u][5];
-              const float g_ = dhv[u];
-              const float d_o = g_ * tc;
-              const float dcn = dcv[u] + g_ * og * (1.f - tc * tc);
-              da[0] = dcn * gg * ig * (1.f - ig);
-              da[1] = dcn * c_in * fg * (1.f - fg);
-              da[2] = dcn * ig * (1.f - gg * gg);
-              da[3] = d_o * og * (1.f - og);
-              dcp = dcn * fg * mp;
-              float* o = dgx + (int64_t)inst[u] * G4 + j;
-#pragma unroll
-              for (int g = 0; g < 4; ++g) {
-                if (rnd) da[g] = rna_tf32(da[g]);
-#ifndef DGC_EXP_NOSTORE
-                o[g * H] = da[g];
-#endif
-                bsum[lc][g] += da[g];
-              }
-            }
-#ifndef DGC_EXP_NOSTORE
-            if (trow < R) dc_scr[trow * H + j] = dcp;
-#else
-            if (dcp == 1234.5f) dc_scr[0] = dcp;
-#endif
-#pragma unroll
-            for (int g = 0; g < 4; ++g) {
-              const uint32_t off =
-                  (uint32_t)(((seq0 + g) % kBwdAStages) * kAStage) + sw128_offset(r, lane);
-              *reinterpret_cast<float*>(sA + off) = da[g];
-#ifndef DGC_EXP_NODSMEM
-              st_cluster_f32(sA_peer + off, da[g]);
-#endif
-            }
-          }
-        }
-        asm volatile("fence.proxy.async;" ::: "memory");
-        if (lc == 1 && blockIdx.x == 0 && threadIdx.x == 64 && t < 256) g_lstm_ts[t][2] = globaltimer();
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          const int sl = (seq0 + g) % kBwdAStages;
-          mbar_arrive(&a_full[sl]);
-          mbar_arrive_cluster(map_peer(&a_full[sl], peer));
-        }
-        __syncwarp();
-      }
-      if (has_next) {
-        fence_before();
-        mbar_arrive(&acc_empty[(p + 1) & 1]);
-      }
-    }
-    if (bias_partial) {  // combine the 8 warps (4 quadrants x 2 halves) in fixed order
-      for (int lc = 0; lc < 2; ++lc) {
-        const int c = (int)crank * (NC / 2) + lc;
-        for (int g = 0; g < 4; ++g) {
-          stg[lane] = bsum[lc][g];
-          asm volatile("bar.sync 1, %0;" ::"r"(kBwdEpiThreads));
-          if (ew == 0) {
-            float acc = 0.f;
-            for (int w = 0; w < kBwdEpiWarps; ++w) acc += stg_all[w * 32 * 33 + lane];
-            bias_partial[tile * G4 + g * H + 32 * c + lane] = acc;
-          }
-          asm volatile("bar.sync 1, %0;" ::"r"(kBwdEpiThreads));
-        }
-      }
-    }
-  }
-  fence_before();
-  __syncthreads();
-  cluster_sync_all();
-  if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
-}
-
-// Backward, 2-CTA cluster variant with EW epilogue warps (EW/4 per TMEM lane
-// quadrant, 32/(EW/4) rows each; more warps = more loads in flight for this
-// latency-bound epilogue). The carried dc of a (row, unit) cell stays in
-// registers: a thread owns the same cells at every position.
+// [c*H/2, (c+1)*H/2). Its epilogue computes da for those units (8 of the 16 da
+// k-blocks per position) and writes them into BOTH CTAs' A rings (DSMEM); each
+// CTA's MMA then forms dh_prev for its own units only (N = H/2) from all 16
+// k-blocks; ring slots are released by a multicast commit from both MMAs
+// (k-block order interleaves the owners: chunks 0, 2, 1, 3). EW epilogue warps
+// (EW/4 per TMEM lane quadrant; more warps = more loads in flight for this
+// latency-bound epilogue); the carried dc of a (row, unit) cell stays in
+// registers (a thread owns the same cells at every position). Rows: rq per
+// lane quadrant (cluster_rows_per_quadrant), as the forward.
 template <int H, int EW>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
     lstm_bwd_tc2w_kernel(const __grid_constant__ CUtensorMap tmU, const int32_t* __restrict__ slot_row,
                          const uint8_t* __restrict__ slot_mask, int64_t R, int L,
                          const float* __restrict__ save, const float* __restrict__ dh_out,
                          float* __restrict__ dgx, int rnd, float* __restrict__ bias_partial,
-                         int kPf) {
+                         int rq) {
   static_assert(H == 128, "cluster BPTT is specialised for H = 128");
   constexpr int kEpiT = 32 * EW;
   constexpr int WPQ = EW / 4;                // warps per lane quadrant
@@ -1577,7 +817,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cluster_rank(), peer = crank ^ 1u;
   const int64_t tile = blockIdx.x >> 1;
-  const int64_t row0 = tile * BM;
+  const int64_t row0 = tile * 4 * rq;
   const int u0 = (int)crank * HU;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kBwdAStages; ++s) {
@@ -1647,26 +887,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
     float* stg = stg_all + ew * kStg;
     const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
     const uint32_t sA_peer = map_peer(sA, peer);
-    const int64_t my_row = row0 + q * 32 + lane;
-    const bool my_ok = my_row < R;
+    const int64_t my_row = row0 + q * rq + lane;  // lane = quadrant row
+    const bool my_ok = lane < rq && my_row < R;
+    const bool active = rb < rq;            // warps with no rows only keep the protocol
     float bsum[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
     float dcr[2][RPW];                      // carried dc of this thread's cells
 #pragma unroll
     for (int lc = 0; lc < 2; ++lc)
 #pragma unroll
       for (int u = 0; u < RPW; ++u) dcr[lc][u] = 0.f;
-    auto prefetch_pos = [&](int pp) {
-      if (kPf < 0 || pp < 0 || !my_ok || hq != 0) return;
-      const int inst = slot_row[my_row * L + pp];
-      if (inst < 0) return;
-      prefetch_l2_bulk(save + (int64_t)inst * 7 * H + crank * (7 * H / 2), 7 * H * 2);
-      prefetch_l2_bulk(dh_out + (int64_t)inst * H + u0, HU * 4);
-    };
-    for (int pp = L - 1; pp >= L - 1 - kPf; --pp) prefetch_pos(pp);
     for (int t = 0; t < L; ++t) {
       const int p = L - 1 - t;
       const bool has_next = p + 1 < L;
-      prefetch_pos(p - kPf - 1);
       const int64_t my_s = my_row * L + p;
       const int my_inst = my_ok ? slot_row[my_s] : -1;
       const float my_m = my_ok ? (float)slot_mask[my_s] : 0.f;
@@ -1682,7 +914,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
         const int c = (int)crank * (NC / 2) + lc;
         const int m = 2 * lc + (int)crank;
         const int j = 32 * c + lane;
-        if (has_next) {
+        if (has_next && active) {
           float v[32];
           tmem_ld32(tl + ((p + 1) & 1) * HU + 32 * lc, v);
           if (lane >= rb && lane < rb + RPW) {
@@ -1699,6 +931,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
         }
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
+          if (rb + b * kRB >= rq) continue;  // warp-uniform: no rows left
           float ld[kRB][6], dhv[kRB];
           int inst[kRB];
 #pragma unroll
@@ -1804,29 +1037,10 @@ int launch_lstm_bwd_tc2w(const float* U, const int32_t* slot_row, const uint8_t*
   auto kern = lstm_bwd_tc2w_kernel<H, EW>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_bwd_tc2w: set smem");
-  const int grid = 2 * (int)((R + BM - 1) / BM);
+  const int grid = 2 * (int)cluster_tiles(R);
   kern<<<grid, 64 + 32 * EW, smem, s>>>(m, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
-                                        bias_partial, rnn_prefetch_distance());
+                                        bias_partial, cluster_rows_per_quadrant(R));
   DGC_CHECK_LAUNCH("lstm_bwd_tc2w_kernel");
-  return DGC_OK;
-}
-
-template <int H>
-int launch_lstm_bwd_tc2(const float* U, const int32_t* slot_row, const uint8_t* slot_mask,
-                        int64_t R, int L, const float* save, const float* dh_out, float* dgx,
-                        float* dc_scr, int rnd, float* bias_partial, cudaStream_t s) {
-  CUtensorMap m;
-  int rc = make_map(&m, U, H, 4 * H, 4 * H, 32, H / 2, false);
-  if (rc) return rc;
-  const size_t smem = (size_t)kBwdAStages * BM * 128 + (size_t)kBwdBStages * (H / 2) * 128 +
-                      (size_t)kBwdEpiWarps * 32 * 33 * 4 + 1024 + 512;
-  auto kern = lstm_bwd_tc2_kernel<H>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_bwd_tc2: set smem");
-  const int grid = 2 * (int)((R + BM - 1) / BM);
-  kern<<<grid, kBwdThreads, smem, s>>>(m, slot_row, slot_mask, R, L, save, dh_out, dgx, dc_scr,
-                                       rnd, bias_partial, rnn_prefetch_distance());
-  DGC_CHECK_LAUNCH("lstm_bwd_tc2_kernel");
   return DGC_OK;
 }
 
@@ -1872,6 +1086,8 @@ int launch_lstm_tc(const float* gx, const float* Ut, const int32_t* slot_row,
 
 }  // namespace
 
+static bool cluster_rnn_enabled() { return getenv("DGC_NO_CLUSTER_RNN") == nullptr; }
+
 extern "C" int dgc_rnn_fwd_tc(int32_t cell, const float* gx, const float* Ut,
                               const int32_t* slot_row, const uint8_t* slot_mask,
                               const int32_t* slot_carry, const float* carry, int64_t n_rows,
@@ -1881,22 +1097,15 @@ extern "C" int dgc_rnn_fwd_tc(int32_t cell, const float* gx, const float* Ut,
   DGC_REQUIRE(c_out != nullptr, "rnn_fwd_tc: LSTM needs c_out");
   if (n_rows == 0 || row_len == 0) return DGC_OK;
   cudaStream_t s = dgc::as_stream(stream);
+  const bool cl = cluster_rnn_enabled();
   switch (H) {
     case 32: return launch_lstm_tc<32>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
     case 64:
-      if (!getenv("DGC_NO_CLUSTER_RNN"))
-        return launch_lstm_tc2<64>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
-      return launch_lstm_tc<64>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
+      return cl ? launch_lstm_tc2v<64>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s)
+                : launch_lstm_tc<64>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
     case 128:
-      if (!getenv("DGC_NO_CLUSTER_RNN")) {
-        const char* ew = getenv("DGC_FWD_EW");
-        if (!ew)
-          return launch_lstm_tc2v<128>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
-        if (atoi(ew) == 16)
-          return launch_lstm_tc2w<128, 16>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
-        return launch_lstm_tc2<128>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
-      }
-      return launch_lstm_tc<128>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
+      return cl ? launch_lstm_tc2v<128>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s)
+                : launch_lstm_tc<128>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
     default: return dgc::fail(DGC_ERR_ARG, "rnn_fwd_tc: H must be 32, 64 or 128");
   }
 }
@@ -1919,18 +1128,13 @@ extern "C" int dgc_rnn_bwd_tc(int32_t cell_flags, const float* U, const int32_t*
     case 32: return launch_lstm_bwd_tc<32>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
     case 64: return launch_lstm_bwd_tc<64>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
     case 128:
-      if (!getenv("DGC_NO_CLUSTER_RNN")) {
-        const char* ew = getenv("DGC_BWD_EW");
-        const int nw = ew ? atoi(ew) : 16;
-        if (nw == 16)
-          return launch_lstm_bwd_tc2w<128, 16>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, rnd, bias_partial, s);
-        if (nw == 8)
-          return launch_lstm_bwd_tc2w<128, 8>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, rnd, bias_partial, s);
-        return launch_lstm_bwd_tc2<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
-      }
-      return launch_lstm_bwd_tc<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
+      return cluster_rnn_enabled()
+                 ? launch_lstm_bwd_tc2w<128, 16>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, rnd, bias_partial, s)
+                 : launch_lstm_bwd_tc<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
     default: return dgc::fail(DGC_ERR_ARG, "rnn_bwd_tc: H must be 32, 64 or 128");
   }
 }
 
-extern "C" int64_t dgc_rnn_tc_tiles(int64_t n_rows) { return (n_rows + 127) / 128; }
+extern "C" int64_t dgc_rnn_tc_tiles(int64_t n_rows, int32_t H) {
+  return (H == 128 && cluster_rnn_enabled()) ? cluster_tiles(n_rows) : (n_rows + 127) / 128;
+}

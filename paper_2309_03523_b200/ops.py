@@ -229,8 +229,9 @@ def rnn_bwd_tc(cell, U, slot_row, slot_mask, n_rows, row_len, H, save, dh_out, d
         nb, 2.0 * n_rows * row_len * H * G * H)
 
 
-def rnn_tc_tiles(n_rows):
-    return _native.lib().dgc_rnn_tc_tiles(n_rows)
+def rnn_tc_tiles(n_rows, H):
+    """Rows of the tensor-core BPTT's bias partials (dgc_rnn_tc_tiles)."""
+    return _native.lib().dgc_rnn_tc_tiles(n_rows, H)
 
 
 def rnn_bwd_partial_rows(n_rows, H):

@@ -165,9 +165,8 @@ class Shard:
                        and os.environ.get("DGC_TC_RNN", "1") != "0")
         self.Ut_f = [torch.zeros((GH, H), **f32) for _ in range(cfg.n_rnn)] if self.tc_rnn else None
         if self.tc_rnn:
-            tiles = ops.rnn_tc_tiles(max(self.R, 1))
-            self.rnn_dc_scratch = torch.zeros((tiles * 128, H), **f32)
-            self.rnn_tc_prows = tiles
+            self.rnn_dc_scratch = torch.zeros(((max(self.R, 1) + 127) // 128 * 128, H), **f32)
+            self.rnn_tc_prows = ops.rnn_tc_tiles(max(self.R, 1), H)
         self.dYext = torch.zeros((self.nloc, H), **f32)
         self.colsum_scratch = torch.zeros(2 * 148 * max(GH, cfg.C, H), **f32)
         # fused bias-gradient partial sums (produced inside the kernels that write
@@ -175,7 +174,7 @@ class Shard:
         self.m_tiles = max(1, (n + 127) // 128)
         self.rnn_prows = ops.rnn_bwd_partial_rows(self.R, H) if self.R else 1
         self.dl_partial = torch.zeros(max(1, (n + 255) // 256) * cfg.C, **f32)
-        prows = max(self.rnn_prows, ops.rnn_tc_tiles(max(self.R, 1)))
+        prows = max(self.rnn_prows, ops.rnn_tc_tiles(max(self.R, 1), H))
         self.bias_partial = torch.zeros(max(prows * GH, 4 * self.m_tiles * H), **f32)
         # split-K for weight gradients: ~one wave of 148 SMs
         kb = max(1, (n + 31) // 32)

@@ -329,9 +329,9 @@ def test_lstm_bwd_tensor_core_matches_simt(H):
         dgx = torch.zeros((n, 4 * H), device=dev)
         sr, sm = t(slot_row, torch.int32), t(mask.reshape(-1), torch.uint8)
         if tc:
-            tiles = ops.rnn_tc_tiles(R)
+            tiles = ops.rnn_tc_tiles(R, H)
             bp = torch.zeros((tiles, 4 * H), device=dev)
-            scr = torch.zeros((tiles * 128, H), device=dev)
+            scr = torch.zeros(((R + 127) // 128 * 128, H), device=dev)
             ops.rnn_bwd_tc(1, t(U), sr, sm, R, L, H, t(save), t(dh), dgx, scr, bias_partial=bp)
             bias = bp.sum(0)
         else:

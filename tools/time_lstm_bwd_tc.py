@@ -15,8 +15,8 @@ U = torch.randn((H, 4 * H), device=dev) / H ** 0.5
 sr = torch.tensor(slot_row, device=dev); sm = torch.tensor(mask.reshape(-1), device=dev)
 save = torch.rand((n, 7 * H), device=dev); dh = torch.randn((n, H), device=dev)
 dgx = torch.zeros((n, 4 * H), device=dev)
-tiles = ops.rnn_tc_tiles(R)
-bp = torch.zeros((tiles, 4 * H), device=dev); scr = torch.zeros((tiles * 128, H), device=dev)
+tiles = ops.rnn_tc_tiles(R, H)
+bp = torch.zeros((tiles, 4 * H), device=dev); scr = torch.zeros(((R + 127) // 128 * 128, H), device=dev)
 fn = lambda: ops.rnn_bwd_tc(1, U, sr, sm, R, L, H, save, dh, dgx, scr, bias_partial=bp)
 fn(); torch.cuda.synchronize()
 s = torch.cuda.Event(enable_timing=True); e = torch.cuda.Event(enable_timing=True)
