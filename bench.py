@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--detail", action="store_true", help="per-shape kernel table on stderr")
     ap.add_argument("--cpu-sample-s", type=float, default=25.0)
+    ap.add_argument("--no-graph", action="store_true", help="eager epochs (no CUDA graph replay)")
     return ap.parse_args()
 
 
@@ -136,9 +137,9 @@ def model_cfg(args, pa):
 
 # -- CPU baseline: the fp64 oracle port on the host cores ---------------------
 
-def cpu_epoch_time(pa, cfg, budget_s):
-    """Time full epochs of the CPU oracle (oracle/dgnn.py, numpy fp64, all
-    host BLAS threads) on the same plan and model; bounded by budget_s."""
+def cpu_oracle(pa, cfg):
+    """The CPU oracle trainer (oracle/dgnn.py, numpy fp64, all host BLAS
+    threads) on the same plan and model."""
     import oracle.dgnn as od
     from paper_2309_03523_b200.layout import build_layout
     from paper_2309_03523_b200.model import init_params, synthetic_inputs
@@ -147,7 +148,12 @@ def cpu_epoch_time(pa, cfg, budget_s):
     T = int(pa.inst_t.max())
     ocfg = od.OracleConfig(F=cfg.F, H=cfg.H, C=cfg.C, rnn=cfg.rnn, n_rnn=cfg.n_rnn,
                            model=cfg.model, T=T, optimizer="adam", lr=1e-3)
-    orc = od.OracleDGNN(lays, X, y, init_params(cfg, 0), ocfg, inst_t=pa.inst_t)
+    return od.OracleDGNN(lays, X, y, init_params(cfg, 0), ocfg, inst_t=pa.inst_t)
+
+
+def cpu_epoch_time(pa, cfg, budget_s):
+    """Full CPU-oracle epochs, bounded by budget_s (at most 3): min seconds."""
+    orc = cpu_oracle(pa, cfg)
     times = []
     t_start = time.perf_counter()
     r = 0
@@ -162,6 +168,9 @@ def cpu_epoch_time(pa, cfg, budget_s):
 
 
 def run_reference(args):
+    """Reference arm: the CPU oracle port of the path on the host cores (rank 0
+    only; other ranks exit). One step = one full fp64 epoch of the same plan
+    and model."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
@@ -170,11 +179,13 @@ def run_reference(args):
     pa, _ = load_plan(args, 1)
     cfg = model_cfg(args, pa)
     cores = os.cpu_count()
-    vals = []
-    for _ in range(args.warmup + args.steps):
-        t, _ = cpu_epoch_time(pa, cfg, args.cpu_sample_s)
-        vals.append(t)
-    times = vals[args.warmup:] or vals
+    orc = cpu_oracle(pa, cfg)
+    times = []
+    for r in range(1, args.warmup + args.steps + 1):
+        t0 = time.perf_counter()
+        orc.epoch(r)
+        times.append(time.perf_counter() - t0)
+    times = times[args.warmup:] or times
     ep = statistics.mean(times)
     value = pa.n_spatial_edges / ep
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
@@ -185,9 +196,9 @@ def run_reference(args):
                                    f"{pa.n_spatial_edges} edges, {cfg.rnn.upper()}x{cfg.n_rnn}, "
                                    f"F={cfg.F} H={cfg.H}", "parallelism": "host CPU"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": "full epochs of the fp64 oracle (oracle/dgnn.py) on the "
-                                       "same plan/model; the reference (dynpart) has no DGNN "
-                                       "trainer and cannot run on the GPU box"},
+                             "sample": f"{args.steps} full epochs (after {args.warmup} warm-up) "
+                                       "of the fp64 oracle (oracle/dgnn.py) on the same plan/"
+                                       "model; the reference (dynpart) has no DGNN trainer"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -212,8 +223,10 @@ def run_ours(args):
     cfg = model_cfg(args, pa)
     X, y = synthetic_inputs(pa.n_instances, cfg.F, cfg.C, 0)
     distributed = world > 1 and scaling == "strong"
+    # single-device epochs replay one captured CUDA graph (same kernels, no
+    # per-launch host latency); multi-rank epochs have host-side count syncs
     tr = DGNNTrainer(pa, cfg, None, seed=0, device=dev, distributed=distributed, features=X,
-                     labels=y)
+                     labels=y, cuda_graph=not args.no_graph)
     sh = tr.shards[0]
     flush = torch.empty(320 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
 
@@ -226,16 +239,29 @@ def run_ours(args):
         tr.run_epoch()
     # ---- device-timed region (inputs resident in HBM) ----
     times = []
-    ops._prof_detail = args.detail
-    prof = ops.profile()
-    with ClockSampler(local) as clocks, prof:
+    with ClockSampler(local) as clocks:
         for _ in range(args.steps):
             flush.zero_()
             barrier()
             rep = tr.run_epoch()  # brackets the step with CUDA events (wall_ms)
             times.append(rep.wall_ms)
             barrier()
-    kern = prof.summary()
+    # ---- per-kernel table: separate eager epochs with CUDA events around every
+    # native launch on its stream (never inside the timed region) ----
+    ops._prof_detail = args.detail
+    prof = ops.profile()
+    graph_mode, tr.cuda_graph = tr.cuda_graph, False
+    n_prof = max(1, min(args.steps, 3))
+    with prof:
+        for _ in range(n_prof):
+            flush.zero_()
+            barrier()
+            tr.run_epoch()
+            barrier()
+    tr.cuda_graph = graph_mode
+    # per-step averages over the profiled epochs, expressed per `steps` epochs
+    kern = {k: {f: v[f] * args.steps / n_prof for f in ("ms", "launches", "kernels", "bytes", "flops")}
+            for k, v in prof.summary().items()}
     step_ms = float(np.mean(times))
     if world > 1:
         t = torch.tensor([step_ms], device=dev)

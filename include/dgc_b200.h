@@ -286,6 +286,10 @@ int dgc_sgd(float* p, const float* g, float* mom, int64_t n, float lr, float mom
             void* stream);
 int dgc_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, float beta1,
              float beta2, float eps, int32_t step, void* stream);
+/* Adam with the (already incremented) step count read from device memory, so
+ * an epoch can be captured once in a CUDA graph and replayed. */
+int dgc_adam_dev(float* p, const float* g, float* m, float* v, int64_t n, float lr, float beta1,
+                 float beta2, float eps, const int32_t* step_dev, void* stream);
 
 #ifdef __cplusplus
 }

@@ -69,6 +69,7 @@ _SIGS = {
     "dgc_relu_bwd": (_i32, [_p, _p, _p, _i64, _p]),
     "dgc_sgd": (_i32, [_p, _p, _p, _i64, _f32, _f32, _p]),
     "dgc_adam": (_i32, [_p, _p, _p, _p, _i64, _f32, _f32, _f32, _f32, _i32, _p]),
+    "dgc_adam_dev": (_i32, [_p, _p, _p, _p, _i64, _f32, _f32, _f32, _f32, _p, _p]),
 }
 
 _lib = None

@@ -137,7 +137,13 @@ __global__ void sgd_kernel(float* __restrict__ p, const float* __restrict__ g,
 
 __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g,
                             float* __restrict__ m, float* __restrict__ v, int64_t n, float lr,
-                            float b1, float b2, float eps, float c1, float c2) {
+                            float b1, float b2, float eps, float c1, float c2,
+                            const int32_t* __restrict__ step_dev) {
+  if (step_dev) {  // step count in device memory (replayable in a CUDA graph)
+    const float st = (float)*step_dev;
+    c1 = 1.f - powf(b1, st);
+    c2 = 1.f - powf(b2, st);
+  }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const float gi = g[i];
@@ -257,7 +263,18 @@ extern "C" int dgc_adam(float* p, const float* g, float* m, float* v, int64_t n,
   if (n == 0) return DGC_OK;
   const float c1 = 1.f - powf(beta1, (float)step), c2 = 1.f - powf(beta2, (float)step);
   adam_kernel<<<dgc::grid_for(n, 256), 256, 0, dgc::as_stream(stream)>>>(p, g, m, v, n, lr, beta1,
-                                                                       beta2, eps, c1, c2);
+                                                                       beta2, eps, c1, c2, nullptr);
+  DGC_CHECK_LAUNCH("adam_kernel");
+  return DGC_OK;
+}
+
+extern "C" int dgc_adam_dev(float* p, const float* g, float* m, float* v, int64_t n, float lr,
+                            float beta1, float beta2, float eps, const int32_t* step_dev,
+                            void* stream) {
+  DGC_REQUIRE(step_dev != nullptr, "adam_dev: step_dev is NULL");
+  if (n == 0) return DGC_OK;
+  adam_kernel<<<dgc::grid_for(n, 256), 256, 0, dgc::as_stream(stream)>>>(p, g, m, v, n, lr, beta1,
+                                                                       beta2, eps, 1.f, 1.f, step_dev);
   DGC_CHECK_LAUNCH("adam_kernel");
   return DGC_OK;
 }

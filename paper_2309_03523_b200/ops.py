@@ -341,6 +341,13 @@ def sgd(p, g, mom, lr, momentum):
 
 
 def adam(p, g, m, v, lr, b1, b2, eps, step):
+    """dgc_adam (host step count) or dgc_adam_dev (step: int32 CUDA tensor)."""
+    if isinstance(step, torch.Tensor):
+        _req(step, torch.int32, "step")
+        _run("adam", lambda: _native.check(_native.lib().dgc_adam_dev(
+            _p(p), _p(g), _p(m), _p(v), p.numel(), float(lr), float(b1), float(b2), float(eps),
+            _p(step), _stream()), "dgc_adam_dev"), 28 * p.numel())
+        return
     _run("adam", lambda: _native.check(_native.lib().dgc_adam(
         _p(p), _p(g), _p(m), _p(v), p.numel(), float(lr), float(b1), float(b2), float(eps),
         int(step), _stream()), "dgc_adam"), 28 * p.numel())

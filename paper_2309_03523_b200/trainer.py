@@ -193,6 +193,7 @@ class Shard:
         self.fresh = [{} for _ in range(2)]  # layer -> {peer: (recv idx tensor)}
         self.sent = [{} for _ in range(2)]   # layer -> {peer: (send idx tensor or None, count)}
         self.step_count = 0
+        self.step_dev = torch.zeros(1, dtype=torch.int32, device=dev)
         self.events = None
 
     def _init_evolve(self, lay, cfg, dev):
@@ -384,7 +385,7 @@ class Shard:
                          self.loss_partial, round_tf32=self.tf32, dl_partial=self.dl_partial)
         loss_local = self.loss_partial.sum().reshape(1)
         loss = yield ("sum", loss_local)
-        info["loss"] = float(loss.item()) / self.n_total
+        info["loss_sum"] = loss  # device scalar; read once the epoch is enqueued
         # ---------------- backward ----------------
         self.grads.zero_()
         ks, part = self.ksplit, self.partial
@@ -482,8 +483,9 @@ class Shard:
             yield ("sum", self.grads)
         self.step_count += 1
         if cfg.optimizer == "adam":
+            self.step_dev.add_(1)  # device step count: the epoch is replayable as a graph
             ops.adam(self.params, self.grads, self.m, self.v, cfg.lr, cfg.beta1, cfg.beta2,
-                     cfg.eps, self.step_count)
+                     cfg.eps, self.step_dev)
         else:
             ops.sgd(self.params, self.grads, self.m, cfg.lr, cfg.momentum)
         if self.tf32:
@@ -612,8 +614,14 @@ class DGNNTrainer:
 
     def __init__(self, pa: PlanArrays, cfg: DGNNConfig, stale_config=None, seed: int = 0,
                  device=None, distributed: bool = False, features=None, labels=None,
-                 params=None):
+                 params=None, cuda_graph: bool = False):
         self.pa, self.cfg = pa, cfg
+        # cuda_graph: a single-device epoch without staleness is a fixed kernel
+        # sequence with no host sync; capture it once (after one eager epoch)
+        # and replay it, so the step is not bound by per-launch host latency
+        self.cuda_graph = cuda_graph
+        self._graph = None
+        self._graph_infos = None
         self.stale = StaleConfig.coerce(stale_config)
         self.device = torch.device(device or "cuda")
         self.trace = EpochLossTrace()
@@ -646,13 +654,24 @@ class DGNNTrainer:
         torch.cuda.synchronize(self.device)
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
+        graphable = (self.cuda_graph and len(self.shards) == 1 and self.pa.n_devices == 1
+                     and self.stale.mode is StaleMode.OFF and isinstance(self.runner, LocalRunner))
+        if graphable and r >= 2 and self._graph is None:
+            self._graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self._graph):
+                self._graph_infos = self.runner.run([s.step(r, self.trace) for s in self.shards])
+            torch.cuda.synchronize(self.device)
         t0.record()
-        infos = self.runner.run([s.step(r, self.trace) for s in self.shards])
+        if graphable and self._graph is not None:
+            self._graph.replay()
+            infos = self._graph_infos
+        else:
+            infos = self.runner.run([s.step(r, self.trace) for s in self.shards])
         t1.record()
         torch.cuda.synchronize(self.device)
         ms = t0.elapsed_time(t1)
         self.epoch_no = r
-        loss = infos[0]["loss"]
+        loss = float(infos[0]["loss_sum"].item()) / self.pa.n_instances
         self.trace.append(loss)
         return self._report(r, ms, infos, loss)
 
