@@ -100,13 +100,114 @@ __global__ void __launch_bounds__(256) colsum_stage1(const float* __restrict__ X
   }
 }
 
-__global__ void colsum_stage2(const float* __restrict__ scratch, int nblk, int width,
-                              float* __restrict__ out, int accumulate) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= width) return;
+// stage 2: out[j] (+)= sum of the nblk partial rows; block = 32 columns x 8
+// slab groups (each thread sums every 8th slab), combined in fixed order.
+__global__ void __launch_bounds__(256) colsum_stage2(const float* __restrict__ scratch, int nblk,
+                                                     int width, float* __restrict__ out,
+                                                     int accumulate) {
+  __shared__ float red[8][33];
+  const int j = blockIdx.x * 32 + threadIdx.x;
   float acc = 0.f;
-  for (int b = 0; b < nblk; ++b) acc += scratch[(int64_t)b * width + j];
-  out[j] = accumulate ? out[j] + acc : acc;
+  if (j < width)
+    for (int b = threadIdx.y; b < nblk; b += 8) acc += scratch[(int64_t)b * width + j];
+  red[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && j < width) {
+    float s = 0.f;
+    for (int g = 0; g < 8; ++g) s += red[g][threadIdx.x];
+    out[j] = accumulate ? out[j] + s : s;
+  }
+}
+
+// Readout softmax cross-entropy for C <= 32 classes: thread per row (logits in
+// registers, 16-byte loads/stores when C % 4 == 0), per-block loss and dlogits
+// column sums by warp shuffles + a fixed-order combine of the 8 warps.
+template <int CM>
+__global__ void __launch_bounds__(256) softmax_xent_small_kernel(
+    const float* __restrict__ logits, const int32_t* __restrict__ labels, int64_t n, int C,
+    float scale, int round_out, float* __restrict__ dlogits, double* __restrict__ loss_partial,
+    float* __restrict__ dl_partial) {
+  __shared__ double lred[8];
+  __shared__ float cred[8][CM];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const bool vec = (C & 3) == 0;
+  float x[CM];
+  double l = 0.0;
+  if (i < n) {
+    const float* row = logits + i * C;
+#pragma unroll
+    for (int c = 0; c < CM; c += 4) {
+      if (c < C) {
+        if (vec) {
+          const float4 v = *reinterpret_cast<const float4*>(row + c);
+          x[c] = v.x; x[c + 1] = v.y; x[c + 2] = v.z; x[c + 3] = v.w;
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) x[c + e] = (c + e < C) ? row[c + e] : 0.f;
+        }
+      }
+    }
+    float m = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < CM; ++c) if (c < C) m = fmaxf(m, x[c]);
+    const int y = labels[i];  // y < 0: padding row (no loss, no gradient)
+    float zy = 0.f;
+#pragma unroll
+    for (int c = 0; c < CM; ++c) if (c == y) zy = x[c];
+    float ssum = 0.f;
+#pragma unroll
+    for (int c = 0; c < CM; ++c) if (c < C) { x[c] = __expf(x[c] - m); ssum += x[c]; }
+    l = y >= 0 ? -(double)(zy - m - logf(ssum)) : 0.0;
+    const float inv = 1.f / ssum;
+#pragma unroll
+    for (int c = 0; c < CM; ++c) {
+      float p = x[c] * inv;
+      if (c == y) p -= 1.f;
+      if (y < 0) p = 0.f;
+      p *= scale;
+      x[c] = round_out ? dgc::rna_tf32_f(p) : p;
+    }
+    float* drow = dlogits + i * C;
+#pragma unroll
+    for (int c = 0; c < CM; c += 4) {
+      if (c < C) {
+        if (vec) {
+          *reinterpret_cast<float4*>(drow + c) = make_float4(x[c], x[c + 1], x[c + 2], x[c + 3]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) if (c + e < C) drow[c + e] = x[c + e];
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < CM; ++c) x[c] = 0.f;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+  if (lane == 0) lred[w] = l;
+  if (dl_partial) {
+#pragma unroll
+    for (int c = 0; c < CM; ++c) {
+      if (c >= C) break;
+      float v = x[c];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) cred[w][c] = v;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < 8; ++k) t += lred[k];
+    loss_partial[blockIdx.x] = t;
+  }
+  if (dl_partial && (int)threadIdx.x < C) {
+    float t = 0.f;
+    for (int k = 0; k < 8; ++k) t += cred[k][threadIdx.x];
+    dl_partial[(int64_t)blockIdx.x * C + threadIdx.x] = t;
+  }
 }
 
 __global__ void relu_bwd_kernel(const float4* __restrict__ dH, const float4* __restrict__ H,
@@ -163,9 +264,16 @@ extern "C" int dgc_softmax_xent(const float* logits, const int32_t* labels, int6
   DGC_REQUIRE(C >= 1, "softmax_xent: C must be >= 1");
   if (n == 0) return DGC_OK;
   const int blocks = (int)((n + 255) / 256);
-  softmax_xent_kernel<<<blocks, 256, 0, dgc::as_stream(stream)>>>(logits, labels, n, C, scale,
-                                                                 flags & 1, dlogits, loss_partial,
-                                                                 dl_partial);
+  const bool aligned = (reinterpret_cast<uintptr_t>(logits) & 15) == 0 &&
+                       (reinterpret_cast<uintptr_t>(dlogits) & 15) == 0;
+  if (C <= 32 && (aligned || (C & 3) != 0)) {
+    softmax_xent_small_kernel<32><<<blocks, 256, 0, dgc::as_stream(stream)>>>(
+        logits, labels, n, C, scale, flags & 1, dlogits, loss_partial, dl_partial);
+  } else {
+    softmax_xent_kernel<<<blocks, 256, 0, dgc::as_stream(stream)>>>(logits, labels, n, C, scale,
+                                                                   flags & 1, dlogits, loss_partial,
+                                                                   dl_partial);
+  }
   DGC_CHECK_LAUNCH("softmax_xent_kernel");
   return DGC_OK;
 }
@@ -182,7 +290,7 @@ extern "C" int dgc_colsum(const float* X, int64_t n, int32_t width, int64_t ld, 
     colsum_stage1<<<nblk, 256, 256 * sizeof(float4), s>>>(X, n, width, ld, rows_per, scratch);
     DGC_CHECK_LAUNCH("colsum_stage1");
   }
-  colsum_stage2<<<(width + 255) / 256, 256, 0, s>>>(scratch, nblk, width, out, accumulate);
+  colsum_stage2<<<(width + 31) / 32, dim3(32, 8), 0, s>>>(scratch, nblk, width, out, accumulate);
   DGC_CHECK_LAUNCH("colsum_stage2");
   return DGC_OK;
 }
@@ -228,7 +336,8 @@ extern "C" int dgc_reduce_rows(const float* partial, int64_t rows, int32_t width
     reduce_rows_stage1<<<grid, dim3(32, 8), 0, s>>>(partial, rows, width, slab, scratch);
     DGC_CHECK_LAUNCH("reduce_rows_stage1");
   }
-  colsum_stage2<<<(width + 255) / 256, 256, 0, s>>>(scratch, (int)slabs, width, out, accumulate);
+  colsum_stage2<<<(width + 31) / 32, dim3(32, 8), 0, s>>>(scratch, (int)slabs, width, out,
+                                                         accumulate);
   DGC_CHECK_LAUNCH("reduce_rows_stage2");
   return DGC_OK;
 }

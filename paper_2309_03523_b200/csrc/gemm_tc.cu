@@ -366,6 +366,47 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// Split-K reduction, fixed order. Block = 64 float4 column groups x 4 split
+// slices: thread (g, s) sums splits s, s+4, ... of 4 consecutive elements (16-B
+// loads, 4x the loads in flight of a thread-per-element loop), the 4 slices are
+// then combined in order through shared memory. Needs N % 4 == 0.
+__global__ void __launch_bounds__(256) splitk_reduce4_kernel(
+    const float* __restrict__ partial, int splits, int64_t M, int64_t N, float* __restrict__ C,
+    int64_t ldc, const float* __restrict__ bias, const float* __restrict__ relu_src,
+    int accumulate) {
+  __shared__ float4 red[4][64];
+  const int64_t total4 = M * N / 4;
+  const int64_t e4 = (int64_t)blockIdx.x * 64 + threadIdx.x;
+  const int sl = threadIdx.y;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (e4 < total4) {
+    const float4* p4 = reinterpret_cast<const float4*>(partial);
+    for (int z = sl; z < splits; z += 4) {
+      const float4 v = __ldg(p4 + (int64_t)z * total4 + e4);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+  }
+  red[sl][threadIdx.x] = acc;
+  __syncthreads();
+  if (sl != 0 || e4 >= total4) return;
+  float4 t = red[0][threadIdx.x];
+  for (int k = 1; k < 4; ++k) {
+    const float4 v = red[k][threadIdx.x];
+    t.x += v.x; t.y += v.y; t.z += v.z; t.w += v.w;
+  }
+  const int64_t e = e4 * 4, r = e / N, n = e % N;  // 4 elements of one row (N % 4 == 0)
+  float o[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    float* dst = C + r * ldc + n + k;
+    float a = o[k];
+    if (accumulate) a += *dst;
+    if (bias) a += bias[n + k];
+    if (relu_src && !(relu_src[r * ldc + n + k] > 0.f)) a = 0.f;
+    *dst = a;
+  }
+}
+
 __global__ void splitk_reduce_kernel(const float* __restrict__ partial, int splits, int64_t M,
                                      int64_t N, float* __restrict__ C, int64_t ldc,
                                      const float* __restrict__ bias,
@@ -476,6 +517,13 @@ static int gemm_impl(const float* A, int64_t lda, const float* B, int64_t ldb, f
   bn = (bn + align - 1) / align * align;
   if (bn > 256) bn = 256;
   const int kb_total = (int)((K + BK - 1) / BK);
+  // split-K only to fill the machine: ~one wave of (m-tile, n-tile, split) work
+  // items (the split-K partials cost 2 x splits x M x N x 4 bytes of traffic)
+  {
+    const int64_t tiles = ((M + BM - 1) / BM) * ntiles;
+    const int64_t cap = tiles >= dgc::kNumSMs ? 1 : dgc::kNumSMs / tiles;
+    if (k_splits > cap) k_splits = (int)cap;
+  }
   int kb_per = (kb_total + k_splits - 1) / k_splits;
   // The tcgen05 fp32 accumulator truncates (measured: a systematic -1.2e-4
   // relative bias after 625 k-blocks of 3xTF32, tools/debug_gemm.py), so the
@@ -541,8 +589,14 @@ static int gemm_impl(const float* A, int64_t lda, const float* B, int64_t ldb, f
         part, so.item_ptr, so.n_seg, M, N, C, ldc);
     DGC_CHECK_LAUNCH("seg_reduce_kernel");
   } else if (part) {
-    splitk_reduce_kernel<<<dgc::grid_for(M * N, 256), 256, 0, s>>>(part, splits, M, N, C, ldc,
-                                                                   bias, relu_src, accumulate);
+    if (N % 4 == 0 && (reinterpret_cast<uintptr_t>(part) & 15) == 0) {
+      const int64_t total4 = M * N / 4;
+      splitk_reduce4_kernel<<<(unsigned)((total4 + 63) / 64), dim3(64, 4), 0, s>>>(
+          part, splits, M, N, C, ldc, bias, relu_src, accumulate);
+    } else {
+      splitk_reduce_kernel<<<dgc::grid_for(M * N, 256), 256, 0, s>>>(part, splits, M, N, C, ldc,
+                                                                     bias, relu_src, accumulate);
+    }
     DGC_CHECK_LAUNCH("splitk_reduce_kernel");
   }
   return DGC_OK;
