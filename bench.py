@@ -297,8 +297,16 @@ def run_ours(args):
             dist.destroy_process_group()
         return
     hbm, tflops, src = peaks()
+    # DRAM traffic of the dominant kernel from the committed ncu --set full
+    # capture of this workload (profiles/ncu_traffic.json), per launch
+    traffic = None
+    tp = ROOT / "profiles" / "ncu_traffic.json"
+    if tp.exists():
+        rec = json.loads(tp.read_text()).get("kernels", {})
     top = max(((k.split("[")[0], v) for k, v in kern.items()), key=lambda kv: kv[1]["ms"])
     name, d = top
+    if tp.exists() and name in rec:
+        traffic = rec[name]["traffic_bytes"]
     avg_ms = d["ms"] / d["launches"]
     achieved = (d["bytes"] / d["launches"]) / (avg_ms / 1e3) / 1e9
     per_kernel = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
@@ -337,7 +345,7 @@ def run_ours(args):
                 "h2d_bytes_per_step": int(Xh.numel() * 4 + yh.numel() * 4),
                 "d2h_bytes_per_step": 8, "ms_per_step": e2e_step},
         "roofline": {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": hbm,
-                     "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                     "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                      "peak_source": src, "algorithmic_bytes_per_launch": d["bytes"] / d["launches"],
                      "avg_launch_ms": avg_ms},
         "kernels": per_kernel,

@@ -148,3 +148,30 @@ def test_trainer_evolvegcn_matches_oracle(artifacts_dir, precision, tol):
             ref = o["grads"][k]
             err = np.linalg.norm(g - ref) / max(np.linalg.norm(ref), 1e-30)
             assert err <= tol, f"epoch {r} grad {k}: {err:.2e}"
+
+
+@pytest.mark.parametrize("H,precision", [(128, "tf32"), (16, "fp32")])
+def test_cuda_graph_epochs_equal_eager(H, precision):
+    """A single-device epoch captured once as a CUDA graph and replayed gives
+    bitwise the same losses and parameters as eager epochs (same kernels, every
+    reduction in fixed order; the Adam step count lives in device memory)."""
+    from pathlib import Path
+    from paper_2309_03523_b200 import DGNNConfig, load_plan_npz, single_device
+    from paper_2309_03523_b200.trainer import DGNNTrainer
+    from paper_2309_03523_b200.model import init_params, synthetic_inputs
+    root = Path(__file__).resolve().parents[1]
+    pa = single_device(load_plan_npz(root / "artifacts" / "t4" / "plan.npz"))
+    cfg = DGNNConfig(F=H, H=H, C=16, rnn="lstm", n_rnn=2, optimizer="adam", lr=1e-3,
+                     precision=precision)
+    X, y = synthetic_inputs(pa.n_instances, cfg.F, cfg.C, 0)
+    params = init_params(cfg, 0)
+    runs = []
+    for graph in (False, True):
+        tr = DGNNTrainer(pa, cfg, None, features=X, labels=y, params=params, cuda_graph=graph)
+        losses = [tr.run_epoch().loss for _ in range(4)]
+        assert (tr._graph is not None) == graph
+        runs.append((losses, tr.params(0)))
+    (l0, p0), (l1, p1) = runs
+    assert l0 == l1
+    for k in p0:
+        assert np.array_equal(p0[k], p1[k]), k
