@@ -769,68 +769,75 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
 }
 
-// Backward, 2-CTA cluster variant (H = 128): CTA c owns hidden units
-// [c*H/2, (c+1)*H/2). Its epilogue computes da for those units (8 of the 16 da
-// k-blocks per position) and writes them into BOTH CTAs' A rings (DSMEM); each
-// CTA's MMA then forms dh_prev for its own units only (N = H/2) from all 16
-// k-blocks; ring slots are released by a multicast commit from both MMAs
-// (k-block order interleaves the owners: chunks 0, 2, 1, 3). EW epilogue warps
-// (EW/4 per TMEM lane quadrant; more warps = more loads in flight for this
-// latency-bound epilogue); the carried dc of a (row, unit) cell stays in
-// registers (a thread owns the same cells at every position). Rows: rq per
-// lane quadrant (cluster_rows_per_quadrant), as the forward.
-template <int H, int EW>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
-    lstm_bwd_tc2w_kernel(const __grid_constant__ CUtensorMap tmU, const int32_t* __restrict__ slot_row,
+// Backward, 2-CTA cluster, K-split (H = 128). CTA c owns hidden units
+// [c*H/2, (c+1)*H/2) and the 8 da k-blocks (4 gates x 2 chunks of 32 units) of
+// them. Its MMA forms a PARTIAL dh for ALL H units from its own k-blocks only
+// (M = 128 rows, N = H, K = 2H; B = the matching 32-column blocks of U), so the
+// A ring stays CTA-local (local arrivals, no cluster-scope fences). The two
+// CTAs then swap the halves that belong to the other CTA's units: 8 rows x H/2
+// floats per epilogue warp through st.async + complete_tx into the peer's
+// double-buffered receive tile (32 KB per position), and each CTA adds its own
+// half (TMEM) and the received half. 16 epilogue warps (4 per TMEM lane
+// quadrant, 8 rows each; lane = unit in the BPTT math), carried dc in
+// registers, rq rows per lane quadrant as the forward.
+constexpr int kKsAStages = 4;
+constexpr int kKsBStages = 3;
+template <int H>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
+    lstm_bwd_tc2k_kernel(const __grid_constant__ CUtensorMap tmU, const int32_t* __restrict__ slot_row,
                          const uint8_t* __restrict__ slot_mask, int64_t R, int L,
                          const float* __restrict__ save, const float* __restrict__ dh_out,
                          float* __restrict__ dgx, int rnd, float* __restrict__ bias_partial,
                          int rq) {
-  static_assert(H == 128, "cluster BPTT is specialised for H = 128");
+  static_assert(H == 128, "K-split cluster BPTT is specialised for H = 128");
+  constexpr int EW = kVEW;
   constexpr int kEpiT = 32 * EW;
-  constexpr int WPQ = EW / 4;                // warps per lane quadrant
-  constexpr int RPW = 32 / WPQ;              // rows per warp
-  constexpr int kRB = EW >= 16 ? 4 : 8;      // rows per load batch
-  constexpr int NB = RPW / kRB;              // batches per chunk
+  constexpr int RPW = 8;                     // rows per warp (4 warps per quadrant)
+  constexpr int kRB = 4;                     // rows per load batch
+  constexpr int NB = RPW / kRB;
   constexpr int G4 = 4 * H;
   constexpr int HU = H / 2;
-  constexpr int NC = H / 32;
-  constexpr int KB = G4 / BK;
-  constexpr int kAStage = BM * 128;
-  constexpr int kBStage = HU * 128;
-  constexpr uint32_t kTmemCols = 128;
+  constexpr int KBO = 8;                     // own da k-blocks per position
+  constexpr int kAStage = BM * 128;          // 128 rows x 32 gate columns
+  constexpr int kBStage = H * 128;           // H units x 32 gate columns of U
+  constexpr int kS = HU + 1;                 // own-half staging row stride (floats)
+  constexpr int kStgW = RPW * kS;
+  constexpr int kRecv = BM * HU;             // floats per receive tile
+  constexpr uint32_t kTmemCols = 2 * H;      // two N = H accumulators
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~(uintptr_t)1023);
   uint8_t* sA = smem;
-  uint8_t* sB = sA + kBwdAStages * kAStage;
-  float* stg_all = reinterpret_cast<float*>(sB + kBwdBStages * kBStage);
-  constexpr int kStg = (RPW > 1 ? RPW : 1) * 33;  // >= 32 floats (bias combine)
-  uint64_t* a_full = reinterpret_cast<uint64_t*>(stg_all + EW * kStg);
-  uint64_t* a_empty = a_full + kBwdAStages;
-  uint64_t* b_full = a_empty + kBwdAStages;
-  uint64_t* b_empty = b_full + kBwdBStages;
-  uint64_t* acc_full = b_empty + kBwdBStages;   // [2]
+  uint8_t* sB = sA + kKsAStages * kAStage;
+  float* recv = reinterpret_cast<float*>(sB + kKsBStages * kBStage);  // [2][128][HU]
+  float* stg_all = recv + 2 * kRecv;
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(stg_all + EW * kStgW);
+  uint64_t* a_empty = a_full + kKsAStages;
+  uint64_t* b_full = a_empty + kKsAStages;
+  uint64_t* b_empty = b_full + kKsBStages;
+  uint64_t* acc_full = b_empty + kKsBStages;    // [2]
   uint64_t* acc_empty = acc_full + 2;           // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* recv_full = acc_empty + 2;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recv_full + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cluster_rank(), peer = crank ^ 1u;
   const int64_t tile = blockIdx.x >> 1;
   const int64_t row0 = tile * 4 * rq;
-  const int u0 = (int)crank * HU;
+  const int u0 = (int)crank * HU, pu0 = (int)peer * HU;
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < kBwdAStages; ++s) {
+    for (int s = 0; s < kKsAStages; ++s) {
       mbar_init(&a_full[s], kEpiT);
-      mbar_init(&a_empty[s], 2);
+      mbar_init(&a_empty[s], 1);
     }
-    for (int s = 0; s < kBwdBStages; ++s) {
+    for (int s = 0; s < kKsBStages; ++s) {
       mbar_init(&b_full[s], 1);
       mbar_init(&b_empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
       mbar_init(&acc_empty[a], kEpiT);
+      mbar_init(&recv_full[a], 1);  // local arrive.expect_tx + the peer's st.async bytes
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmU) : "memory");
@@ -838,43 +845,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
   if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
   fence_before();
   __syncthreads();
-  cluster_sync_all();
+  cluster_sync_all();  // both CTAs' barriers initialised before any st.async
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  auto chunk_at = [](int m) { return (m & 1) * (NC / 2) + (m >> 1); };
+  // own k-block i of a position: chunk lc = i >> 2 (global chunk 2*crank + lc), gate g = i & 3
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int seq = 0; seq < L * KB; ++seq) {
-        const int s = seq % kBwdBStages;
-        mbar_wait(&b_empty[s], ((seq / kBwdBStages) & 1) ^ 1);
-        const int i = seq % KB, c = chunk_at(i >> 2), g = i & 3;
+      for (int seq = 0; seq < L * KBO; ++seq) {
+        const int s = seq % kKsBStages;
+        mbar_wait(&b_empty[s], ((seq / kKsBStages) & 1) ^ 1);
+        const int i = seq % KBO, c = 2 * (int)crank + (i >> 2), g = i & 3;
         mbar_expect_tx(&b_full[s], (uint32_t)kBStage);
-        tma_load_2d(sB + s * kBStage, &tmU, g * H + 32 * c, u0, &b_full[s]);
+        tma_load_2d(sB + s * kBStage, &tmU, g * H + 32 * c, 0, &b_full[s]);
       }
     }
   } else if (warp == 1) {
-    const uint32_t idesc = idesc_tf32(HU, false, false);
+    const uint32_t idesc = idesc_tf32(H, false, false);
     const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
     for (int t = 0; t < L; ++t) {
       const int p = L - 1 - t;
       const int a = p & 1;
       mbar_wait(&acc_empty[a], ((t >> 1) & 1) ^ 1);
       fence_after();
-      for (int i = 0; i < KB; ++i) {
-        const int seq = t * KB + i;
-        const int sa = seq % kBwdAStages, sb = seq % kBwdBStages;
-        mbar_wait_cluster(&a_full[sa], (seq / kBwdAStages) & 1);
-        mbar_wait(&b_full[sb], (seq / kBwdBStages) & 1);
+      for (int i = 0; i < KBO; ++i) {
+        const int seq = t * KBO + i;
+        const int sa = seq % kKsAStages, sb = seq % kKsBStages;
+        mbar_wait(&a_full[sa], (seq / kKsAStages) & 1);
+        mbar_wait(&b_full[sb], (seq / kKsBStages) & 1);
         fence_after();
         if (lane == 0) {
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk)
-            mma_tf32(tmem_base + a * HU, kdesc(a_base + sa * kAStage + kk * 32),
+            mma_tf32(tmem_base + a * H, kdesc(a_base + sa * kAStage + kk * 32),
                      kdesc(b_base + sb * kBStage + kk * 32), idesc, (i > 0 || kk > 0) ? 1u : 0u);
-          mma_commit_mc(&a_empty[sa], (uint16_t)0x3);
+          mma_commit(&a_empty[sa]);
           mma_commit(&b_empty[sb]);
-          if (i == KB - 1) mma_commit(&acc_full[a]);
+          if (i == KBO - 1) mma_commit(&acc_full[a]);
         }
         __syncwarp();
       }
@@ -882,16 +889,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
   } else {
     const int ew = warp - 2;
     const int q = warp & 3;                 // TMEM lane quadrant (warp id % 4)
-    const int hq = ew >> 2;                 // row group within the quadrant
-    const int rb = hq * RPW;                // first quadrant row of this warp
-    float* stg = stg_all + ew * kStg;
+    const int rb = (ew >> 2) * RPW;         // first quadrant row of this warp
+    float* stg = stg_all + ew * kStgW;
     const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
-    const uint32_t sA_peer = map_peer(sA, peer);
+    const uint32_t recv_peer = map_peer(recv, peer);
+    const uint32_t rfull_peer = map_peer(recv_full, peer);
     const int64_t my_row = row0 + q * rq + lane;  // lane = quadrant row
     const bool my_ok = lane < rq && my_row < R;
-    const bool active = rb < rq;            // warps with no rows only keep the protocol
+    const bool active = rb < rq;
+    // bytes the peer sends into our receive tile per position: 8 rows x HU per
+    // active peer warp (4 quadrants x ceil(rq / 8) warps)
+    const uint32_t kRecvBytes = 4u * (uint32_t)((rq + RPW - 1) / RPW) * RPW * HU * 4u;
     float bsum[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-    float dcr[2][RPW];                      // carried dc of this thread's cells
+    float dcr[2][RPW];
 #pragma unroll
     for (int lc = 0; lc < 2; ++lc)
 #pragma unroll
@@ -904,30 +914,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
       const float my_m = my_ok ? (float)slot_mask[my_s] : 0.f;
       const float my_mnext = (has_next && my_ok) ? (float)slot_mask[my_s + 1] : 0.f;
       if (blockIdx.x == 0 && threadIdx.x == 64 && t < 256) g_lstm_ts[t][0] = globaltimer();
+      const float* rv = recv + (t & 1) * kRecv;
       if (has_next) {
+        if (ew == 0 && lane == 0) mbar_arrive_expect_tx(&recv_full[t & 1], kRecvBytes);
         mbar_wait(&acc_full[(p + 1) & 1], ((t - 1) >> 1) & 1);
         fence_after();
         if (blockIdx.x == 0 && threadIdx.x == 64 && t < 256) g_lstm_ts[t][1] = globaltimer();
+        if (active) {
+          // partial dh of this warp's 8 rows: own units -> staging, the peer's
+          // units -> the peer's receive tile (thread = row = TMEM lane)
+          float v[64];
+          const uint32_t ta = tl + ((p + 1) & 1) * H;
+          tmem_ld16x4(ta + u0, ta + u0 + 16, ta + u0 + 32, ta + u0 + 48, v);
+          if (lane >= rb && lane < rb + RPW) {
+            float* d = stg + (lane - rb) * kS;
+#pragma unroll
+            for (int u = 0; u < HU; ++u) d[u] = v[u];
+          }
+          tmem_ld16x4(ta + pu0, ta + pu0 + 16, ta + pu0 + 32, ta + pu0 + 48, v);
+          if (lane >= rb && lane < rb + RPW) {
+            const uint32_t dst = recv_peer + (uint32_t)(((t & 1) * kRecv + (q * 32 + lane) * HU) * 4);
+#pragma unroll
+            for (int u = 0; u < HU; u += 4)
+              st_async_v4(dst + u * 4, make_float4(v[u], v[u + 1], v[u + 2], v[u + 3]),
+                          rfull_peer + (uint32_t)((t & 1) * 8));
+          }
+        }
+        fence_before();
+        mbar_arrive(&acc_empty[(p + 1) & 1]);  // this accumulator is fully read
+        mbar_wait(&recv_full[t & 1], ((t - 1) >> 1) & 1);
+        __syncwarp();
       }
 #pragma unroll
       for (int lc = 0; lc < 2; ++lc) {
-        const int c = (int)crank * (NC / 2) + lc;
-        const int m = 2 * lc + (int)crank;
-        const int j = 32 * c + lane;
-        if (has_next && active) {
-          float v[32];
-          tmem_ld32(tl + ((p + 1) & 1) * HU + 32 * lc, v);
-          if (lane >= rb && lane < rb + RPW) {
-#pragma unroll
-            for (int u = 0; u < 32; ++u) stg[(lane - rb) * 33 + u] = v[u];
-          }
-        }
-        __syncwarp();
-        const int seq0 = t * KB + m * 4;
+        const int c = 2 * (int)crank + lc;   // global 32-unit chunk
+        const int j = 32 * c + lane;         // this lane's hidden unit
+        const int seq0 = t * KBO + lc * 4;
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           const int seq = seq0 + g;
-          mbar_wait(&a_empty[seq % kBwdAStages], ((seq / kBwdAStages) & 1) ^ 1);
+          mbar_wait(&a_empty[seq % kKsAStages], ((seq / kKsAStages) & 1) ^ 1);
         }
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
@@ -939,7 +965,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
             const int rl = rb + b * kRB + u;
             inst[u] = __shfl_sync(0xffffffffu, my_inst, rl);
             const float mn = __shfl_sync(0xffffffffu, my_mnext, rl);
-            dhv[u] = has_next ? mn * stg[(b * kRB + u) * 33 + lane] : 0.f;
+            dhv[u] = has_next ? mn * (stg[(b * kRB + u) * kS + 32 * lc + lane] +
+                                      rv[(q * 32 + rl) * HU + 32 * lc + lane])
+                              : 0.f;
             if (inst[u] >= 0) {
               dhv[u] += dh_out[(int64_t)inst[u] * H + j];
               const float* sv = save + (int64_t)inst[u] * 7 * H + j;
@@ -980,37 +1008,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
             dc = dcp;
             const uint32_t off0 = sw128_offset(r, lane);
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-              const uint32_t off = (uint32_t)(((seq0 + g) % kBwdAStages) * kAStage) + off0;
-              *reinterpret_cast<float*>(sA + off) = da[g];
-              st_cluster_f32(sA_peer + off, da[g]);
-            }
+            for (int g = 0; g < 4; ++g)
+              *reinterpret_cast<float*>(sA + ((seq0 + g) % kKsAStages) * kAStage + off0) = da[g];
           }
         }
-        asm volatile("fence.proxy.async;" ::: "memory");
+        fence_async_smem();
         if (lc == 1 && blockIdx.x == 0 && threadIdx.x == 64 && t < 256) g_lstm_ts[t][2] = globaltimer();
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          const int sl = (seq0 + g) % kBwdAStages;
-          mbar_arrive(&a_full[sl]);
-          mbar_arrive_cluster(map_peer(&a_full[sl], peer));
-        }
+        for (int g = 0; g < 4; ++g) mbar_arrive(&a_full[(seq0 + g) % kKsAStages]);
         __syncwarp();
-      }
-      if (has_next) {
-        fence_before();
-        mbar_arrive(&acc_empty[(p + 1) & 1]);
       }
     }
     if (bias_partial) {  // combine the EW warps in fixed order
       for (int lc = 0; lc < 2; ++lc) {
-        const int c = (int)crank * (NC / 2) + lc;
+        const int c = 2 * (int)crank + lc;
         for (int g = 0; g < 4; ++g) {
           stg[lane] = bsum[lc][g];
           asm volatile("bar.sync 1, %0;" ::"r"(kEpiT));
           if (ew == 0) {
             float acc = 0.f;
-            for (int w = 0; w < EW; ++w) acc += stg_all[w * kStg + lane];
+            for (int w = 0; w < EW; ++w) acc += stg_all[w * kStgW + lane];
             bias_partial[tile * G4 + g * H + 32 * c + lane] = acc;
           }
           asm volatile("bar.sync 1, %0;" ::"r"(kEpiT));
@@ -1020,27 +1037,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
   }
   fence_before();
   __syncthreads();
-  cluster_sync_all();
+  cluster_sync_all();  // no st.async may still target this CTA's shared memory
   if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
 }
 
-template <int H, int EW>
-int launch_lstm_bwd_tc2w(const float* U, const int32_t* slot_row, const uint8_t* slot_mask,
+template <int H>
+int launch_lstm_bwd_tc2k(const float* U, const int32_t* slot_row, const uint8_t* slot_mask,
                          int64_t R, int L, const float* save, const float* dh_out, float* dgx,
                          int rnd, float* bias_partial, cudaStream_t s) {
   CUtensorMap m;
-  int rc = make_map(&m, U, H, 4 * H, 4 * H, 32, H / 2, false);
+  int rc = make_map(&m, U, H, 4 * H, 4 * H, 32, H, false);
   if (rc) return rc;
-  constexpr int RPW = 32 / (EW / 4);
-  const size_t smem = (size_t)kBwdAStages * BM * 128 + (size_t)kBwdBStages * (H / 2) * 128 +
-                      (size_t)EW * (RPW > 1 ? RPW : 1) * 33 * 4 + 1024 + 512;
-  auto kern = lstm_bwd_tc2w_kernel<H, EW>;
+  const size_t smem = (size_t)kKsAStages * BM * 128 + (size_t)kKsBStages * H * 128 +
+                      (size_t)2 * BM * (H / 2) * 4 + (size_t)kVEW * 8 * (H / 2 + 1) * 4 + 1024 + 512;
+  auto kern = lstm_bwd_tc2k_kernel<H>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_bwd_tc2w: set smem");
+  if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_bwd_tc2k: set smem");
   const int grid = 2 * (int)cluster_tiles(R);
-  kern<<<grid, 64 + 32 * EW, smem, s>>>(m, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
-                                        bias_partial, cluster_rows_per_quadrant(R));
-  DGC_CHECK_LAUNCH("lstm_bwd_tc2w_kernel");
+  kern<<<grid, 64 + 32 * kVEW, smem, s>>>(m, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
+                                          bias_partial, cluster_rows_per_quadrant(R));
+  DGC_CHECK_LAUNCH("lstm_bwd_tc2k_kernel");
   return DGC_OK;
 }
 
@@ -1129,7 +1145,7 @@ extern "C" int dgc_rnn_bwd_tc(int32_t cell_flags, const float* U, const int32_t*
     case 64: return launch_lstm_bwd_tc<64>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
     case 128:
       return cluster_rnn_enabled()
-                 ? launch_lstm_bwd_tc2w<128, 16>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, rnd, bias_partial, s)
+                 ? launch_lstm_bwd_tc2k<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, rnd, bias_partial, s)
                  : launch_lstm_bwd_tc<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
     default: return dgc::fail(DGC_ERR_ARG, "rnn_bwd_tc: H must be 32, 64 or 128");
   }
