@@ -5,7 +5,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O3
 SRC := paper_2309_03523_b200/csrc
 OUT := paper_2309_03523_b200/lib
 CU := common spmm stale exchange dense rnn gemm_tc rnn_tc evolve
-OBJS := $(addprefix build/,$(addsuffix .o,$(CU))) build/layout.o build/fusion_plan.o
+OBJS := $(addprefix build/,$(addsuffix .o,$(CU))) build/layout.o build/fusion_plan.o build/propagate.o
 
 all: $(OUT)/libdgc_b200.so
 
@@ -27,5 +27,9 @@ clean:
 .PHONY: all clean
 
 build/fusion_plan.o: $(SRC)/fusion_plan.cpp include/dgc_b200.h
+	@mkdir -p build
+	g++ -O3 -std=c++17 -fPIC -c $< -o $@
+
+build/propagate.o: $(SRC)/propagate.cpp include/dgc_b200.h
 	@mkdir -p build
 	g++ -O3 -std=c++17 -fPIC -c $< -o $@

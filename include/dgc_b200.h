@@ -85,6 +85,20 @@ int dgc_pack_sequences(const int32_t* lengths, int64_t n, int32_t row_len,
                        int64_t capacity_rows, int32_t* slot_seq, int32_t* slot_pos,
                        uint8_t* mask, int64_t* n_rows, int64_t* padding);
 
+/* Chunk generation (PGC weighted label propagation), bit-exact port of
+ * dynpart.partition.propagate's label computation (partition.py:200-270 with
+ * _propagation_edges :138-152, _greedy_coloring :155-168, _class_argmax
+ * :171-197). spatial_edges [n_spatial, 2] / temporal_links [n_temporal, 2] are
+ * DynamicGraph.spatial_edge_index() / temporal_link_index() (int64, reference
+ * order); spatial_weight = edge_traffic(profile, "spatial"); temporal_weights
+ * [n_temporal] = _temporal_link_weights(g, profile). labels [n] out (final
+ * label per instance; _build_chunk_graph turns them into chunks); rounds_run
+ * and n_colors (may be NULL) report the sweeps done and colour classes. */
+int dgc_propagate_labels(int64_t n, int64_t n_spatial, const int64_t* spatial_edges,
+                         int64_t n_temporal, const int64_t* temporal_links, int64_t spatial_weight,
+                         const int64_t* temporal_weights, int64_t size_cap, int32_t max_rounds,
+                         int64_t* labels, int32_t* rounds_run, int32_t* n_colors);
+
 /* Native bit-exact plan_spatial_fusion (fusion.py:108-203) for ONE device:
  * chunk stats (degree sums, halos over spatial edges + temporal links, inter-
  * chunk message bytes, partition.py:273-359) are derived from the graph
