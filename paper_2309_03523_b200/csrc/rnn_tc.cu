@@ -266,7 +266,7 @@ __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpre
 __device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
 __device__ __forceinline__ float4 zero4() { return make_float4(0.f, 0.f, 0.f, 0.f); }
 
-template <int H>
+template <int H, int kVEW>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
     lstm_fwd_tc2v_kernel(const __grid_constant__ CUtensorMap tmUt, const float* __restrict__ gx,
                          const int32_t* __restrict__ slot_row, const uint8_t* __restrict__ slot_mask,
@@ -510,6 +510,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
 }
 
+template <int H, int EW>
+int launch_lstm_tc2v_ew(const CUtensorMap& m, const float* gx, const int32_t* slot_row,
+                        const uint8_t* slot_mask, const int32_t* slot_carry, const float* carry,
+                        int64_t R, int L, int64_t ld, float* h_out, float* c_out, float* save,
+                        int rq, cudaStream_t s) {
+  const size_t smem = (size_t)(H / BK) * BM * 128 + (size_t)kStages * 2 * H * 128 +
+                      (size_t)EW * 4 * 8 * 16 * 4 + (size_t)EW * (H / 32) * 32 * 16 + 1024 + 256;
+  auto kern = lstm_fwd_tc2v_kernel<H, EW>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_fwd_tc2v: set smem");
+  const int grid = 2 * (int)cluster_tiles(R);
+  kern<<<grid, 64 + 32 * EW, smem, s>>>(m, gx, slot_row, slot_mask, slot_carry, carry, R, L, ld,
+                                        h_out, c_out, save, rq);
+  DGC_CHECK_LAUNCH("lstm_fwd_tc2v_kernel");
+  return DGC_OK;
+}
+
+// 12 epilogue warps (3 per lane quadrant = 24 rows) when rq <= 24: the idle
+// fourth warp's registers go to the others (128 instead of 96 per thread)
 template <int H>
 int launch_lstm_tc2v(const float* gx, const float* Ut, const int32_t* slot_row,
                      const uint8_t* slot_mask, const int32_t* slot_carry, const float* carry,
@@ -518,18 +537,12 @@ int launch_lstm_tc2v(const float* gx, const float* Ut, const int32_t* slot_row,
   CUtensorMap m;
   int rc = make_map(&m, Ut, 4 * H, H, H, 32, H / 2, false);
   if (rc) return rc;
-  const size_t smem = (size_t)(H / BK) * BM * 128 + (size_t)kStages * 2 * H * 128 +
-                      (size_t)kVEW * 4 * 8 * 16 * 4 + (size_t)kVEW * (H / 32) * 32 * 16 +
-                      1024 + 256;
-  auto kern = lstm_fwd_tc2v_kernel<H>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_fwd_tc2v: set smem");
   const int rq = cluster_rows_per_quadrant(R);
-  const int grid = 2 * (int)cluster_tiles(R);
-  kern<<<grid, 64 + 32 * kVEW, smem, s>>>(m, gx, slot_row, slot_mask, slot_carry, carry, R, L, ld,
-                                          h_out, c_out, save, rq);
-  DGC_CHECK_LAUNCH("lstm_fwd_tc2v_kernel");
-  return DGC_OK;
+  if (rq <= 24 && !getenv("DGC_RNN_EW16"))
+    return launch_lstm_tc2v_ew<H, 12>(m, gx, slot_row, slot_mask, slot_carry, carry, R, L, ld,
+                                      h_out, c_out, save, rq, s);
+  return launch_lstm_tc2v_ew<H, 16>(m, gx, slot_row, slot_mask, slot_carry, carry, R, L, ld,
+                                    h_out, c_out, save, rq, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -782,7 +795,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 // registers, rq rows per lane quadrant as the forward.
 constexpr int kKsAStages = 4;
 constexpr int kKsBStages = 3;
-template <int H>
+template <int H, int kVEW>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
     lstm_bwd_tc2k_kernel(const __grid_constant__ CUtensorMap tmU, const int32_t* __restrict__ slot_row,
                          const uint8_t* __restrict__ slot_mask, int64_t R, int L,
@@ -793,7 +806,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   constexpr int EW = kVEW;
   constexpr int kEpiT = 32 * EW;
   constexpr int RPW = 8;                     // rows per warp (4 warps per quadrant)
-  constexpr int kRB = 4;                     // rows per load batch
+  constexpr int kRB = kVEW <= 12 ? 8 : 4;    // rows per load batch (register budget)
   constexpr int NB = RPW / kRB;
   constexpr int G4 = 4 * H;
   constexpr int HU = H / 2;
@@ -1041,6 +1054,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
 }
 
+template <int H, int EW>
+int launch_lstm_bwd_tc2k_ew(const CUtensorMap& m, const int32_t* slot_row, const uint8_t* slot_mask,
+                            int64_t R, int L, const float* save, const float* dh_out, float* dgx,
+                            int rnd, float* bias_partial, int rq, cudaStream_t s) {
+  const size_t smem = (size_t)kKsAStages * BM * 128 + (size_t)kKsBStages * H * 128 +
+                      (size_t)2 * BM * (H / 2) * 4 + (size_t)EW * 8 * (H / 2 + 1) * 4 + 1024 + 512;
+  auto kern = lstm_bwd_tc2k_kernel<H, EW>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_bwd_tc2k: set smem");
+  const int grid = 2 * (int)cluster_tiles(R);
+  kern<<<grid, 64 + 32 * EW, smem, s>>>(m, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
+                                        bias_partial, rq);
+  DGC_CHECK_LAUNCH("lstm_bwd_tc2k_kernel");
+  return DGC_OK;
+}
+
 template <int H>
 int launch_lstm_bwd_tc2k(const float* U, const int32_t* slot_row, const uint8_t* slot_mask,
                          int64_t R, int L, const float* save, const float* dh_out, float* dgx,
@@ -1048,16 +1077,12 @@ int launch_lstm_bwd_tc2k(const float* U, const int32_t* slot_row, const uint8_t*
   CUtensorMap m;
   int rc = make_map(&m, U, H, 4 * H, 4 * H, 32, H, false);
   if (rc) return rc;
-  const size_t smem = (size_t)kKsAStages * BM * 128 + (size_t)kKsBStages * H * 128 +
-                      (size_t)2 * BM * (H / 2) * 4 + (size_t)kVEW * 8 * (H / 2 + 1) * 4 + 1024 + 512;
-  auto kern = lstm_bwd_tc2k_kernel<H>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_bwd_tc2k: set smem");
-  const int grid = 2 * (int)cluster_tiles(R);
-  kern<<<grid, 64 + 32 * kVEW, smem, s>>>(m, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
-                                          bias_partial, cluster_rows_per_quadrant(R));
-  DGC_CHECK_LAUNCH("lstm_bwd_tc2k_kernel");
-  return DGC_OK;
+  const int rq = cluster_rows_per_quadrant(R);
+  if (rq <= 24 && !getenv("DGC_RNN_EW16"))
+    return launch_lstm_bwd_tc2k_ew<H, 12>(m, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
+                                          bias_partial, rq, s);
+  return launch_lstm_bwd_tc2k_ew<H, 16>(m, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
+                                        bias_partial, rq, s);
 }
 
 template <int H>
