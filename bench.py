@@ -248,7 +248,7 @@ def run_ours(args):
             barrier()
     # ---- per-kernel table: separate eager epochs with CUDA events around every
     # native launch on its stream (never inside the timed region) ----
-    ops._prof_detail = args.detail
+    ops._prof_detail = True  # per-shape names: the dominant kernel is one (kernel, shape)
     prof = ops.profile()
     graph_mode, tr.cuda_graph = tr.cuda_graph, False
     n_prof = max(1, min(args.steps, 3))
@@ -303,10 +303,12 @@ def run_ours(args):
     tp = ROOT / "profiles" / "ncu_traffic.json"
     if tp.exists():
         rec = json.loads(tp.read_text()).get("kernels", {})
-    top = max(((k.split("[")[0], v) for k, v in kern.items()), key=lambda kv: kv[1]["ms"])
+    top = max(kern.items(), key=lambda kv: kv[1]["ms"])
     name, d = top
-    if tp.exists() and name in rec:
-        traffic = rec[name]["traffic_bytes"]
+    base = name.split("[")[0]
+    # the ncu capture's shape must be the dominant one for its traffic to apply
+    if tp.exists() and base in rec and rec[base].get("shape", name) == name:
+        traffic = rec[base]["traffic_bytes"]
     avg_ms = d["ms"] / d["launches"]
     achieved = (d["bytes"] / d["launches"]) / (avg_ms / 1e3) / 1e9
     per_kernel = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
