@@ -622,6 +622,10 @@ class DGNNTrainer:
         self.cuda_graph = cuda_graph
         self._graph = None
         self._graph_infos = None
+        # double-buffered input staging (stage_inputs / run_epoch(next_inputs=...))
+        self._copy_stream = None
+        self._staged_ev = None
+        self._stage_free_ev = None
         self.stale = StaleConfig.coerce(stale_config)
         self.device = torch.device(device or "cuda")
         self.trace = EpochLossTrace()
@@ -649,11 +653,62 @@ class DGNNTrainer:
         self.method = "pgc"
         self.epoch_no = 0
 
-    def run_epoch(self):
+    def host_inputs(self, features: np.ndarray, labels: np.ndarray):
+        """Per-shard pinned host tensors (own-row order; padding rows zero /
+        label -1) of global per-instance features and labels, for
+        stage_inputs / run_epoch(next_inputs=...)."""
+        xs, ys = [], []
+        for sh in self.shards:
+            real = sh.lay.own_gid >= 0
+            gid = np.maximum(sh.lay.own_gid, 0)
+            xs.append(torch.as_tensor(np.where(real[:, None], features[gid], 0).astype(np.float32)).pin_memory())
+            ys.append(torch.as_tensor(np.where(real, labels[gid], -1).astype(np.int32)).pin_memory())
+        return xs, ys
+
+    def stage_inputs(self, xs, ys):
+        """Start the host->device copy of the NEXT epoch's features / labels
+        (per-shard pinned host tensors, see host_inputs) into staging buffers
+        on a side stream; the next run_epoch() installs them first. The copy
+        overlaps whatever the compute stream is running (a prefetching input
+        pipeline: one 2-deep buffer per shard)."""
+        if self._copy_stream is None:
+            self._copy_stream = torch.cuda.Stream(self.device)
+            for sh in self.shards:
+                sh.X_stage = torch.empty_like(sh.X)
+                sh.y_stage = torch.empty_like(sh.y)
+        with torch.cuda.stream(self._copy_stream):
+            if self._stage_free_ev is not None:  # the previous staging was installed
+                self._copy_stream.wait_event(self._stage_free_ev)
+            for sh, x, y in zip(self.shards, xs, ys):
+                sh.X_stage.copy_(x, non_blocking=True)
+                sh.y_stage.copy_(y, non_blocking=True)
+            self._staged_ev = torch.cuda.Event()
+            self._staged_ev.record(self._copy_stream)
+
+    def _install_staged(self):
+        cur = torch.cuda.current_stream(self.device)
+        cur.wait_event(self._staged_ev)
+        for sh in self.shards:
+            if sh.tf32:  # tensor-core operands are kept TF32-rounded
+                ops.round_tf32(sh.X_stage, sh.X)
+            else:
+                sh.X.copy_(sh.X_stage)
+            sh.y.copy_(sh.y_stage)
+        self._stage_free_ev = torch.cuda.Event()
+        self._stage_free_ev.record(cur)
+        self._staged_ev = None
+
+    def run_epoch(self, next_inputs=None):
+        """One training epoch (simulate_epoch's role, sim.py:423-566) -> EpochReport.
+        If inputs were staged (stage_inputs) they are installed first;
+        next_inputs = (xs, ys) stages the following epoch's inputs so their
+        copy overlaps this epoch."""
         r = self.epoch_no + 1
         torch.cuda.synchronize(self.device)
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
+        if self._staged_ev is not None:
+            self._install_staged()
         graphable = (self.cuda_graph and len(self.shards) == 1 and self.pa.n_devices == 1
                      and self.stale.mode is StaleMode.OFF and isinstance(self.runner, LocalRunner))
         if graphable and r >= 2 and self._graph is None:
@@ -668,6 +723,8 @@ class DGNNTrainer:
         else:
             infos = self.runner.run([s.step(r, self.trace) for s in self.shards])
         t1.record()
+        if next_inputs is not None:
+            self.stage_inputs(*next_inputs)
         torch.cuda.synchronize(self.device)
         ms = t0.elapsed_time(t1)
         self.epoch_no = r

@@ -175,3 +175,30 @@ def test_cuda_graph_epochs_equal_eager(H, precision):
     assert l0 == l1
     for k in p0:
         assert np.array_equal(p0[k], p1[k]), k
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_staged_inputs_equal_resident(graph):
+    """Epochs fed through the double-buffered input pipeline (stage_inputs /
+    run_epoch(next_inputs=...)) equal epochs on resident inputs, bitwise."""
+    from pathlib import Path
+    from paper_2309_03523_b200 import DGNNConfig, load_plan_npz, single_device
+    from paper_2309_03523_b200.trainer import DGNNTrainer
+    from paper_2309_03523_b200.model import init_params, synthetic_inputs
+    root = Path(__file__).resolve().parents[1]
+    pa = single_device(load_plan_npz(root / "artifacts" / "t4" / "plan.npz"))
+    cfg = DGNNConfig(F=128, H=128, C=16, rnn="lstm", n_rnn=2, optimizer="adam", lr=1e-3,
+                     precision="tf32")
+    X, y = synthetic_inputs(pa.n_instances, cfg.F, cfg.C, 0)
+    params = init_params(cfg, 0)
+    a = DGNNTrainer(pa, cfg, None, features=X, labels=y, params=params, cuda_graph=graph)
+    la = [a.run_epoch().loss for _ in range(3)]
+    b = DGNNTrainer(pa, cfg, None, features=np.zeros_like(X), labels=np.zeros_like(y),
+                    params=params, cuda_graph=graph)
+    xs, ys = b.host_inputs(X, y)
+    b.stage_inputs(xs, ys)
+    lb = [b.run_epoch(next_inputs=(xs, ys)).loss for _ in range(3)]
+    assert la == lb
+    pa_, pb_ = a.params(0), b.params(0)
+    for k in pa_:
+        assert np.array_equal(pa_[k], pb_[k]), k
