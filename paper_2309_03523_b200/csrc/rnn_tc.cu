@@ -478,7 +478,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           st4(sv + 3 * H, fg);
           st4(sv + 4 * H, gg);
           st4(sv + 5 * H, og);
-          st4(sv + 6 * H, tc);
+          if (H != 128) st4(sv + 6 * H, tc);  // H = 128: the cluster BPTT recomputes tanh(c)
           st4(h_out + (int64_t)inst * ld + j, hn);
           st4(c_out + (int64_t)inst * ld + j, cn);
         }
@@ -971,7 +971,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
           if (rb + b * kRB >= rq) continue;  // warp-uniform: no rows left
-          float ld[kRB][6], dhv[kRB];
+          float ld[kRB][5], dhv[kRB];
           int inst[kRB];
 #pragma unroll
           for (int u = 0; u < kRB; ++u) {
@@ -985,10 +985,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
               dhv[u] += dh_out[(int64_t)inst[u] * H + j];
               const float* sv = save + (int64_t)inst[u] * 7 * H + j;
 #pragma unroll
-              for (int k = 0; k < 6; ++k) ld[u][k] = sv[(k + 1) * H];
+              for (int k = 0; k < 5; ++k) ld[u][k] = sv[(k + 1) * H];  // c_in, i, f, g, o
             } else {
 #pragma unroll
-              for (int k = 0; k < 6; ++k) ld[u][k] = 0.f;
+              for (int k = 0; k < 5; ++k) ld[u][k] = 0.f;
             }
           }
 #pragma unroll
@@ -1001,7 +1001,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
             float dcp = 0.f;
             if (inst[u] >= 0) {
               const float c_in = ld[u][0], ig = ld[u][1], fg = ld[u][2], gg = ld[u][3],
-                          og = ld[u][4], tc = ld[u][5];
+                          og = ld[u][4];
+              const float tc = tanh_fast(fg * c_in + ig * gg);  // the forward's tanh(c)
               const float g_ = dhv[u];
               const float d_o = g_ * tc;
               const float dcn = dc + g_ * og * (1.f - tc * tc);

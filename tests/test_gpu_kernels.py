@@ -303,7 +303,10 @@ def test_lstm_fwd_tensor_core_matches_simt(H):
         torch.cuda.synchronize()
         outs.append((hc.cpu().numpy(), save.cpu().numpy()))
     close(outs[1][0], outs[0][0], 2e-3, "lstm tc h|c")
-    close(outs[1][1], outs[0][1], 2e-3, "lstm tc save")
+    # the H = 128 cluster forward leaves the tanh(c) field (6) unwritten: its BPTT
+    # recomputes tanh(f c_in + i g) from the saved c_in, i, f, g
+    nf = 6 if H == 128 else 7
+    close(outs[1][1][:, :nf * H], outs[0][1][:, :nf * H], 2e-3, "lstm tc save")
 
 
 @pytest.mark.parametrize("H", [32, 64, 128])
@@ -322,7 +325,9 @@ def test_lstm_bwd_tensor_core_matches_simt(H):
     U = (rng.standard_normal((H, 4 * H)) / np.sqrt(H)).astype(np.float32)
     save = np.concatenate([rng.standard_normal((n, 2 * H)),            # h_in, c_in
                            rng.random((n, 4 * H)),                      # i, f, g, o
-                           np.tanh(rng.standard_normal((n, H)))], 1).astype(np.float32)
+                           np.zeros((n, H))], 1).astype(np.float32)
+    ci, ig, fg, gg = (save[:, k * H:(k + 1) * H] for k in (1, 2, 3, 4))
+    save[:, 6 * H:] = np.tanh(fg * ci + ig * gg)                       # tanh(c) of the forward
     dh = rng.standard_normal((n, H)).astype(np.float32)
     outs = []
     for tc in (False, True):
