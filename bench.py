@@ -215,10 +215,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # DGC_BENCH_BACKEND=gloo + DGC_BENCH_ONE_GPU=1: smoke-test the N>1 code
+    # path with every rank on cuda:0 (a one-GPU box); the real run is NCCL
+    gpu = 0 if os.environ.get("DGC_BENCH_ONE_GPU") == "1" else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("DGC_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     pa, scaling = load_plan(args, world)
     cfg = model_cfg(args, pa)
     X, y = synthetic_inputs(pa.n_instances, cfg.F, cfg.C, 0)
