@@ -29,7 +29,7 @@ constexpr int kABytes = BM * BK * 4;  // 16 KiB
 template <bool A_MN, bool B_MN, bool SPLIT3>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmC, int tma_store,
+                     const __grid_constant__ CUtensorMap tmC, int tma_store, int64_t c_rows_per_z,
                      const __grid_constant__ CUtensorMap tmA2, int64_t a2_row0,
                      float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, int bn, int stages,
                      int kb_total, int kb_per_split, int m_tiles, int n_tiles, int splits,
@@ -303,7 +303,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmC, box, (int)(n0 + c), (int)(m0 + q * 32));
+            // split-K / K-segmented partials: tile z writes rows z*M + m (M % 128 == 0)
+            tma_store_2d(&tmC, box, (int)(n0 + c), (int)(z * c_rows_per_z + m0 + q * 32));
             bulk_commit();
           }
         }
@@ -455,14 +456,18 @@ struct SegOpts {
 
 template <bool A_MN, bool B_MN, bool SPLIT3>
 int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, int tma_store,
-                const CUtensorMap& ma2, int64_t a2_row0,
+                int64_t c_rows_per_z, const CUtensorMap& ma2, int64_t a2_row0,
                 float* C, int64_t ldc, int64_t M,
                 int64_t N, int bn, int ntiles, int kb_total, int splits, int kb_per,
                 const float* bias, const float* relu_src, int accumulate, float* partial,
                 float* colsum_partial, const SegOpts& so, cudaStream_t s) {
   const int ab = kABytes + bn * BK * 4;
   const int stage_bytes = ab * (SPLIT3 ? 2 : 1);
-  const int budget = 155 * 1024;  // + ~68 KB epilogue staging + barriers <= 227 KB
+  // shared memory: pipeline stages (+ resident B panel) + the epilogue staging
+  // (8 x 4 KB TMA-store boxes, or 8 padded 32x33 transpose tiles) + alignment
+  // and barriers, within the 227 KB per-CTA limit
+  const int stg_bytes = tma_store ? kEpiWarps * 4096 : kEpiWarps * 32 * 33 * 4;
+  const int budget = 232448 - 1024 - 256 - 1024 - stg_bytes;
   // B panel resident in shared memory when one CTA keeps one n-tile and it fits
   const int bres_bytes = kb_total * bn * BK * 4;
   const int b_res = (!SPLIT3 && splits == 1 && bres_bytes <= 96 * 1024 && !so.seg_of_mtile &&
@@ -475,7 +480,7 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   }
   if (stages < 1) return dgc::fail(DGC_ERR_ARG, "gemm: tile does not fit shared memory");
   const size_t smem = (size_t)stages * (b_res ? kABytes : stage_bytes) +
-                      (b_res ? (size_t)bres_bytes : 0) + 1024 + 256 + 1024 + kEpiWarps * 32 * 33 * 4;
+                      (b_res ? (size_t)bres_bytes : 0) + 1024 + 256 + 1024 + stg_bytes;
   auto kern = gemm_tf32_kernel<A_MN, B_MN, SPLIT3>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return dgc::cuda_fail(e, "gemm: set smem");
@@ -483,7 +488,7 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   const int total = m_tiles * ntiles * splits;
   int grid = (dgc::kNumSMs / ntiles) * ntiles;  // multiple of n_tiles: fixed n per CTA
   if (grid > total) grid = total;
-  kern<<<grid, kThreads, smem, s>>>(ma, mb, mc, tma_store, ma2, a2_row0, C, ldc, M, N, bn, stages, kb_total, kb_per, m_tiles,
+  kern<<<grid, kThreads, smem, s>>>(ma, mb, mc, tma_store, c_rows_per_z, ma2, a2_row0, C, ldc, M, N, bn, stages, kb_total, kb_per, m_tiles,
                                     ntiles, splits, bias, relu_src, accumulate, partial,
                                     colsum_partial, b_res, so.seg_of_mtile, so.b_seg_rows,
                                     so.kitems);
@@ -560,15 +565,26 @@ static int gemm_impl(const float* A, int64_t lda, const float* B, int64_t ldb, f
   const bool s3 = precision == 3;
   // plain / bias-only outputs leave through TMA stores (box 32 cols x 32 rows)
   CUtensorMap mc;
-  int tma_store = (!part && !accumulate && ((ldc * 4) % 16 == 0) && (!relu_src || N % 4 == 0) &&
-                   !getenv("DGC_GEMM_NO_TMA_STORE")) ? 1 : 0;
-  if (tma_store && make_map(&mc, C, M, N, ldc, 32, 32, false) != DGC_OK) tma_store = 0;
+  int tma_store = 0;
+  int64_t c_rows_per_z = 0;
+  if (!getenv("DGC_GEMM_NO_TMA_STORE")) {
+    if (!part) {
+      tma_store = (!accumulate && ((ldc * 4) % 16 == 0) && (!relu_src || N % 4 == 0)) ? 1 : 0;
+      if (tma_store && make_map(&mc, C, M, N, ldc, 32, 32, false) != DGC_OK) tma_store = 0;
+    } else if (M % BM == 0 && N % 4 == 0) {
+      // partial tiles [items x M, N]: a tile never crosses into the next item
+      const int64_t items = so.kitems ? so.n_kitems : splits;
+      tma_store = make_map(&mc, part, items * M, N, N, 32, 32, false) == DGC_OK ? 1 : 0;
+      c_rows_per_z = M;
+    }
+  }
   if (so.kitems && splits == 0) {
     rc = DGC_OK;
   } else {
 #define DGC_GEMM_CASE(AM, BMN, S3)                                                               \
   if ((bool)a_mn == AM && (bool)b_mn == BMN && s3 == S3)                                          \
-    rc = launch_gemm<AM, BMN, S3>(ma, mb, mc, tma_store, ma2, a2_row0, C, ldc, M, N, bn, ntiles, \
+    rc = launch_gemm<AM, BMN, S3>(ma, mb, mc, tma_store, c_rows_per_z, ma2, a2_row0, C, ldc,     \
+                                  M, N, bn, ntiles,                                              \
                                   kb_total,                                                      \
                                   splits, kb_per,                                                \
                                   part ? nullptr : bias, part ? nullptr : relu_src,              \

@@ -51,6 +51,13 @@ CONFIGS = {
                  profile=ModelProfile(1, 2, 0, "previous-only", 16, 4), fuse="native"),
     "c3d8": dict(N=1_000_000, T=64, sigma_mult=1.0, D=8, F=16,
                  profile=ModelProfile(1, 2, 0, "previous-only", 16, 4), fuse="native"),
+    # C5: 10M instances x 128 snapshots, sigma = 2 mu, EvolveGCN profile, D = 8.
+    # PGC through the native bit-exact propagate port (the Python label
+    # propagation needs hours at 10M); assignment by the reference; fusion off
+    # (numerics are fusion-invariant)
+    "c5d8": dict(N=10_000_000, T=128, sigma_mult=2.0, D=8, F=16,
+                 profile=ModelProfile(1, 2, 0, "previous-only", 16, 4), fuse=False,
+                 native_propagate=True),
     # small EvolveGCN plans for the parity tests
     "e2": dict(N=3_000, T=8, sigma_mult=1.0, D=2, F=16,
                profile=ModelProfile(1, 2, 0, "previous-only", 16, 4), fuse=True),
@@ -82,7 +89,13 @@ def build(name: str) -> None:
     g = graphstore.generate(spec_for(cfg))
     t1 = time.time()
     cluster = sim.ClusterSpec(n_devices=cfg["D"])
-    plan = sim.build_plan(g, "pgc", cfg["profile"], cluster, fuse=cfg["fuse"] is True)
+    if cfg.get("native_propagate"):
+        sys.path.insert(0, str(ROOT))
+        from paper_2309_03523_b200.partition import native_planner
+        with native_planner():
+            plan = sim.build_plan(g, "pgc", cfg["profile"], cluster, fuse=cfg["fuse"] is True)
+    else:
+        plan = sim.build_plan(g, "pgc", cfg["profile"], cluster, fuse=cfg["fuse"] is True)
     t2 = time.time()
     print(f"[{name}] generate {t1 - t0:.1f}s build_plan {t2 - t1:.1f}s "
           f"chunks={len(plan.chunk_graph.chunks)}", flush=True)
@@ -150,7 +163,8 @@ def build(name: str) -> None:
 
 
 
-def share_graphs(groups=(("c2", ("c2", "c2d2", "c2d4", "c2d8")), ("c3", ("c3d2", "c3d4", "c3d8")))):
+def share_graphs(groups=(("c2", ("c2", "c2d2", "c2d4", "c2d8")), ("c3", ("c3d2", "c3d4", "c3d8")),
+                         ("c5", ("c5d8",)))):
     """Plans of one graph share artifacts/<g>_graph.npz (the graph arrays); each
     plan.npz keeps only the plan arrays and names its graph file in meta."""
     import hashlib
