@@ -473,11 +473,12 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   const int b_res = (!SPLIT3 && splits == 1 && bres_bytes <= 96 * 1024 && !so.seg_of_mtile &&
                      !so.kitems && !getenv("DGC_GEMM_NO_BRES")) ? 1 : 0;
   int stages = b_res ? (budget - bres_bytes) / kABytes : budget / stage_bytes;
-  stages = stages > 4 ? 4 : stages;
+  int max_stages = 4;
   if (const char* env = getenv("DGC_GEMM_MAX_STAGES")) {
     const int cap = atoi(env);
-    if (cap >= 1 && cap < stages) stages = cap;
+    if (cap >= 1) max_stages = cap;
   }
+  stages = stages > max_stages ? max_stages : stages;
   if (stages < 1) return dgc::fail(DGC_ERR_ARG, "gemm: tile does not fit shared memory");
   const size_t smem = (size_t)stages * (b_res ? kABytes : stage_bytes) +
                       (b_res ? (size_t)bres_bytes : 0) + 1024 + 256 + 1024 + stg_bytes;
