@@ -225,6 +225,18 @@ int dgc_rnn_fwd_tc(int32_t cell, const float* gx, const float* Ut, const int32_t
                    const uint8_t* slot_mask, const int32_t* slot_carry, const float* carry,
                    int64_t n_rows, int32_t row_len, int32_t H, int64_t ld_out, float* h_out,
                    float* c_out, float* save, void* stream);
+/* Tensor-core LSTM forward with the input projection fused (F = H = 128, the
+ * 2-CTA cluster kernel): gate pre-activations x Wx + h U + b accumulate in TMEM
+ * from TMA row gathers of x (tile::gather4 by slot_row) against WxT [4H, F]
+ * and the h tile against Ut [4H, H]; bias [4H]. x [n_x, F] (row stride ldx,
+ * TF32-rounded). Replaces the gx GEMM + dgc_rnn_fwd_tc pair; same outputs. */
+int dgc_rnn_fwd_tc_x(int32_t cell, const float* x, int64_t ldx, int64_t n_x, int32_t F,
+                     const float* WxT, const float* Ut, const float* bias,
+                     const int32_t* slot_row, const uint8_t* slot_mask, const int32_t* slot_carry,
+                     const float* carry, int64_t n_rows, int32_t row_len, int32_t H,
+                     int64_t ld_out, float* h_out, float* c_out, float* save, void* stream);
+/* 1 if dgc_rnn_fwd_tc_x serves this (F, H) in this process, else 0. */
+int dgc_rnn_fwd_tc_fused_available(int32_t F, int32_t H);
 /* Tensor-core BPTT (LSTM, H in {32,64,128}): takes U itself [H, 4H] (the
  * K-major B operand of dh = da U^T), dc_scratch [ceil(n_rows/128)*128, H]
  * floats; bias_partial [dgc_rnn_tc_tiles(n_rows, H), 4H] (may be NULL). */

@@ -39,6 +39,9 @@ _SIGS = {
     "dgc_plan_spatial_fusion": (_i32, [_i64, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _i64, _i64,
                                        _i64, _i64, _i64, _p, _p, _p, _p]),
     "dgc_propagate_labels": (_i32, [_i64, _i64, _p, _i64, _p, _i64, _p, _i64, _i32, _p, _p, _p]),
+    "dgc_rnn_fwd_tc_x": (_i32, [_i32, _p, _i64, _i64, _i32, _p, _p, _p, _p, _p, _p, _p, _i64, _i32,
+                                _i32, _i64, _p, _p, _p, _p]),
+    "dgc_rnn_fwd_tc_fused_available": (_i32, [_i32, _i32]),
     "dgc_pack_sequences": (_i32, [_p, _i64, _i32, _i64, _p, _p, _p, _p, _p]),
     "dgc_spmm_csr": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i32, _i32, _p]),
     "dgc_gemm_tf32": (_i32, [_p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _i32, _i32, _i32,

@@ -19,6 +19,7 @@ namespace {
 
 using namespace dgc::tc;
 using dgc::make_map;
+using dgc::make_gather_map;
 
 // warp 0 TMA, warp 1 MMA + TMEM, warps 2..9 epilogue: 2 warps per TMEM lane
 // quadrant (32 packed rows), each owning H/2 hidden units.
@@ -266,9 +267,19 @@ __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpre
 __device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
 __device__ __forceinline__ float4 zero4() { return make_float4(0.f, 0.f, 0.f, 0.f); }
 
-template <int H, int kVEW>
+// FX (fused input projection): the gate pre-activations x Wx + h U + b are
+// accumulated in TMEM from two operand pairs per position -- the x rows of the
+// position's packed slots, gathered by TMA (tile::gather4, rows given by
+// slot_row) against Wx^T, then the h tile against U^T -- into double-buffered
+// accumulators (2 x 256 columns), so the x part of position p+1 runs while the
+// epilogue drains position p. The gx GEMM and every per-position global load of
+// the epilogue disappear; the bias is added from L1.
+template <int H, int kVEW, bool FX>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
-    lstm_fwd_tc2v_kernel(const __grid_constant__ CUtensorMap tmUt, const float* __restrict__ gx,
+    lstm_fwd_tc2v_kernel(const __grid_constant__ CUtensorMap tmUt,
+                         const __grid_constant__ CUtensorMap tmWxT,
+                         const __grid_constant__ CUtensorMap tmX, const float* __restrict__ bias,
+                         const float* __restrict__ gx,
                          const int32_t* __restrict__ slot_row, const uint8_t* __restrict__ slot_mask,
                          const int32_t* __restrict__ slot_carry, const float* __restrict__ carry,
                          int64_t R, int L, int64_t ld, float* __restrict__ h_out,
@@ -282,19 +293,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   constexpr int kABytes = KB * BM * 128;
   constexpr int kBStage = NP * 128;
   constexpr int kStgW = 4 * 8 * 16;          // [gate][8 rows][16 units]
-  constexpr uint32_t kTmemCols = NP <= 128 ? 128 : 256;
+  constexpr uint32_t kAccCols = NP <= 128 ? 128 : 256;
+  constexpr uint32_t kTmemCols = FX ? 2 * kAccCols : kAccCols;
+  constexpr int kXStage = BM * 128;          // one x k-block: 128 rows x 32 fp32
+  static_assert(!FX || H == 128, "fused input projection: F = H = 128");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~(uintptr_t)1023);
   uint8_t* sA = smem;
   uint8_t* sB = smem + kABytes;
-  float* stg_all = reinterpret_cast<float*>(sB + kStages * kBStage);
+  uint8_t* sX = sB + kStages * kBStage;      // FX: x k-block ring
+  float* stg_all = reinterpret_cast<float*>(sX + (FX ? kStages * kXStage : 0));
   float* c_all = stg_all + kVEW * kStgW;     // carried c: [warp][chunk][lane] float4
   uint64_t* b_full = reinterpret_cast<uint64_t*>(c_all + kVEW * NCH * 32 * 4);
   uint64_t* b_empty = b_full + kStages;
   uint64_t* a_full = b_empty + kStages;
-  uint64_t* acc_full = a_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  uint64_t* acc_full = a_full + 1;           // [2] (FX: per accumulator)
+  uint64_t* acc_empty = acc_full + 2;        // [2] FX
+  uint64_t* x_full = acc_empty + 2;          // [kStages] FX
+  uint64_t* x_empty = x_full + kStages;      // [kStages] FX
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_empty + kStages);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cluster_rank(), peer = crank ^ 1u;
@@ -310,9 +328,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
     // local epilogue threads arrive (CTA scope); the peer's half of the h tile
     // lands by st.async (complete_tx), expected by one local arrive.expect_tx
     mbar_init(a_full, kEpiT);
-    mbar_init(acc_full, 2);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 2);  // both CTAs' MMAs (multicast commit)
+      mbar_init(&acc_empty[a], kEpiT);
+    }
+    for (int st = 0; st < kStages; ++st) {
+      mbar_init(&x_full[st], 1);
+      mbar_init(&x_empty[st], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmUt) : "memory");
+    if (FX) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmWxT) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
+    }
   }
   if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
   fence_before();
@@ -322,38 +351,109 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
-      for (int g = 0; g < L * KB; ++g) {
-        const int s = g % kStages;
-        mbar_wait(&b_empty[s], ((g / kStages) & 1) ^ 1);
-        const int kb = g % KB;
-        mbar_expect_tx(&b_full[s], (uint32_t)kBStage);
+    if (!FX) {
+      if (lane == 0) {
+        for (int g = 0; g < L * KB; ++g) {
+          const int s = g % kStages;
+          mbar_wait(&b_empty[s], ((g / kStages) & 1) ^ 1);
+          const int kb = g % KB;
+          mbar_expect_tx(&b_full[s], (uint32_t)kBStage);
 #pragma unroll
-        for (int gi = 0; gi < 4; ++gi)
-          tma_load_2d(sB + s * kBStage + gi * HU * 128, &tmUt, kb * BK, gi * H + u0, &b_full[s]);
+          for (int gi = 0; gi < 4; ++gi)
+            tma_load_2d(sB + s * kBStage + gi * HU * 128, &tmUt, kb * BK, gi * H + u0, &b_full[s]);
+        }
+      }
+    } else {
+      // per position: 4 x k-blocks (x rows gathered, Wx^T), then 4 h k-blocks (U^T).
+      // Lane g < 4 * ceil(rq/4) gathers rows [4i, 4i+4) of lane quadrant g / ceil(rq/4).
+      const int gpq = (rq + 3) / 4;                // gathers per lane quadrant
+      const int n_g = 4 * gpq;
+      const uint32_t x_bytes = (uint32_t)n_g * 4u * 128u;
+      const int gq = lane / gpq, gi0 = (lane % gpq) * 4;
+      int g = 0, gxs = 0;                          // B-ring and x-ring sequence numbers
+      for (int p = 0; p < L; ++p) {
+        int idx[4] = {0, 0, 0, 0};
+        if (lane < n_g) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int i = gi0 + e;
+            const int64_t prow = row0 + (int64_t)gq * rq + i;
+            const int inst = (i < rq && prow < R) ? slot_row[prow * L + p] : -1;
+            idx[e] = inst >= 0 ? inst : 0;  // padding slots read row 0 (result unused)
+          }
+        }
+        for (int kb = 0; kb < KB; ++kb, ++g, ++gxs) {
+          const int s = g % kStages, sx = gxs % kStages;
+          if (lane == 0) {
+            mbar_wait(&x_empty[sx], ((gxs / kStages) & 1) ^ 1);
+            mbar_expect_tx(&x_full[sx], x_bytes);
+            mbar_wait(&b_empty[s], ((g / kStages) & 1) ^ 1);
+            mbar_expect_tx(&b_full[s], (uint32_t)kBStage);
+#pragma unroll
+            for (int gi = 0; gi < 4; ++gi)
+              tma_load_2d(sB + s * kBStage + gi * HU * 128, &tmWxT, kb * BK, gi * H + u0, &b_full[s]);
+          }
+          __syncwarp();
+          if (lane < n_g)
+            tma_gather4(sX + sx * kXStage + (gq * 32 + gi0) * 128, &tmX, kb * BK, idx[0], idx[1],
+                        idx[2], idx[3], &x_full[sx]);
+        }
+        if (lane == 0) {
+          for (int kb = 0; kb < KB; ++kb, ++g) {
+            const int s = g % kStages;
+            mbar_wait(&b_empty[s], ((g / kStages) & 1) ^ 1);
+            mbar_expect_tx(&b_full[s], (uint32_t)kBStage);
+#pragma unroll
+            for (int gi = 0; gi < 4; ++gi)
+              tma_load_2d(sB + s * kBStage + gi * HU * 128, &tmUt, kb * BK, gi * H + u0, &b_full[s]);
+          }
+        }
+        __syncwarp();
       }
     }
   } else if (warp == 1) {
     const uint32_t idesc = idesc_tf32(NP, false, false);
-    const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+    const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB), x_base = smem_u32(sX);
+    int g = 0, gxs = 0;
     for (int p = 0; p < L; ++p) {
+      const int ab = FX ? (p & 1) : 0;
+      const uint32_t tacc = tmem_base + ab * kAccCols;
+      if (FX) {
+        mbar_wait(&acc_empty[ab], ((p >> 1) & 1) ^ 1);  // epilogue of p-2 drained it
+        fence_after();
+        for (int kb = 0; kb < KB; ++kb, ++g, ++gxs) {
+          const int s = g % kStages, sx = gxs % kStages;
+          mbar_wait(&x_full[sx], (gxs / kStages) & 1);
+          mbar_wait(&b_full[s], (g / kStages) & 1);
+          fence_after();
+          if (lane == 0) {
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk)
+              mma_tf32(tacc, kdesc(x_base + sx * kXStage + kk * 32),
+                       kdesc(b_base + s * kBStage + kk * 32), idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+            mma_commit(&x_empty[sx]);
+            mma_commit(&b_empty[s]);
+          }
+          __syncwarp();
+        }
+      }
       mbar_wait(a_full, p & 1);
       fence_after();
       // generic-proxy writes (local st.shared, peer st.async) -> async proxy (MMA)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       if (blockIdx.x == 0 && lane == 0 && p < 256) g_lstm_ts[p][0] = globaltimer();
-      for (int kb = 0; kb < KB; ++kb) {
-        const int g = p * KB + kb;
+      for (int kb = 0; kb < KB; ++kb, ++g) {
         const int s = g % kStages;
         mbar_wait(&b_full[s], (g / kStages) & 1);
         fence_after();
         if (lane == 0) {
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk)
-            mma_tf32(tmem_base, kdesc(a_base + kb * BM * 128 + kk * 32),
-                     kdesc(b_base + s * kBStage + kk * 32), idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+            mma_tf32(tacc, kdesc(a_base + kb * BM * 128 + kk * 32),
+                     kdesc(b_base + s * kBStage + kk * 32), idesc,
+                     (FX || kb > 0 || kk > 0) ? 1u : 0u);
           mma_commit(&b_empty[s]);
-          if (kb == KB - 1) mma_commit_mc(acc_full, (uint16_t)0x3);
+          if (kb == KB - 1) mma_commit_mc(&acc_full[ab], (uint16_t)0x3);
         }
         __syncwarp();
       }
@@ -415,16 +515,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
         n_inst = -1; n_mk = 0; n_ci = -1;
       }
       const float m_next = (float)n_mk;
-      if (!active) {  // keep the a_full phase order: step p's MMA done first
-        mbar_wait(acc_full, p & 1);
+      const int ab = FX ? (p & 1) : 0;
+      const uint32_t acc_par = FX ? ((p >> 1) & 1) : (p & 1);
+      if (!active) {  // keep the a_full / acc_empty phase order: step p's MMA done first
+        mbar_wait(&acc_full[ab], acc_par);
+        if (FX) mbar_arrive(&acc_empty[ab]);
         if (has_next) publish();
         continue;
       }
       const float* gxr = gx + (int64_t)max(inst, 0) * G4 + u0 + uq * 4;
       float4 xg[4];
 #pragma unroll
-      for (int gi = 0; gi < 4; ++gi) xg[gi] = inst >= 0 ? ldg4(gxr + gi * H) : zero4();
-      mbar_wait(acc_full, p & 1);
+      for (int gi = 0; gi < 4; ++gi)
+        xg[gi] = FX ? ldg4(bias + gi * H + u0 + uq * 4) : (inst >= 0 ? ldg4(gxr + gi * H) : zero4());
+      mbar_wait(&acc_full[ab], acc_par);
       fence_after();
       if (blockIdx.x == 0 && threadIdx.x == 64 && p < 256) g_lstm_ts[p][1] = globaltimer();
 #pragma unroll 1
@@ -433,7 +537,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
         const int j = u0 + c0 + uq * 4;
         {
           float a[64];
-          tmem_ld16x4(tl + c0, tl + HU + c0, tl + 2 * HU + c0, tl + 3 * HU + c0, a);
+          const uint32_t ta = tl + ab * kAccCols + c0;
+          tmem_ld16x4(ta, ta + HU, ta + 2 * HU, ta + 3 * HU, a);
           if (lane >= rb && lane < rb + 8) {
 #pragma unroll
             for (int gi = 0; gi < 4; ++gi) {
@@ -453,7 +558,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
         float4 xn[4];
 #pragma unroll
         for (int gi = 0; gi < 4; ++gi)
-          xn[gi] = (inst >= 0 && ch + 1 < NCH) ? ldg4(gxr + gi * H + c0 + 16) : zero4();
+          xn[gi] = ch + 1 >= NCH ? zero4()
+                   : FX ? ldg4(bias + gi * H + u0 + c0 + 16 + uq * 4)
+                        : (inst >= 0 ? ldg4(gxr + gi * H + c0 + 16) : zero4());
         float4 cin = zero4();
         if (ci >= 0) cin = f4(carry + (int64_t)ci * 2 * H + H + j);
         else if (mk) cin = f4(creg + ch * 128);
@@ -498,10 +605,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
         __syncwarp();
       }
       if (blockIdx.x == 0 && threadIdx.x == 64 && p < 256) g_lstm_ts[p][2] = globaltimer();
-      if (has_next) {
-        fence_before();
-        publish();
-      }
+      fence_before();
+      if (FX) mbar_arrive(&acc_empty[ab]);  // this accumulator is drained
+      if (has_next) publish();
     }
   }
   fence_before();
@@ -510,19 +616,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
 }
 
-template <int H, int EW>
-int launch_lstm_tc2v_ew(const CUtensorMap& m, const float* gx, const int32_t* slot_row,
+template <int H, int EW, bool FX>
+int launch_lstm_tc2v_ew(const CUtensorMap& m, const CUtensorMap& mwx, const CUtensorMap& mx,
+                        const float* bias, const float* gx, const int32_t* slot_row,
                         const uint8_t* slot_mask, const int32_t* slot_carry, const float* carry,
                         int64_t R, int L, int64_t ld, float* h_out, float* c_out, float* save,
                         int rq, cudaStream_t s) {
   const size_t smem = (size_t)(H / BK) * BM * 128 + (size_t)kStages * 2 * H * 128 +
-                      (size_t)EW * 4 * 8 * 16 * 4 + (size_t)EW * (H / 32) * 32 * 16 + 1024 + 256;
-  auto kern = lstm_fwd_tc2v_kernel<H, EW>;
+                      (FX ? (size_t)kStages * BM * 128 : 0) + (size_t)EW * 4 * 8 * 16 * 4 +
+                      (size_t)EW * (H / 32) * 32 * 16 + 1024 + 256;
+  auto kern = lstm_fwd_tc2v_kernel<H, EW, FX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_fwd_tc2v: set smem");
   const int grid = 2 * (int)cluster_tiles(R);
-  kern<<<grid, 64 + 32 * EW, smem, s>>>(m, gx, slot_row, slot_mask, slot_carry, carry, R, L, ld,
-                                        h_out, c_out, save, rq);
+  kern<<<grid, 64 + 32 * EW, smem, s>>>(m, mwx, mx, bias, gx, slot_row, slot_mask, slot_carry,
+                                        carry, R, L, ld, h_out, c_out, save, rq);
   DGC_CHECK_LAUNCH("lstm_fwd_tc2v_kernel");
   return DGC_OK;
 }
@@ -539,10 +647,30 @@ int launch_lstm_tc2v(const float* gx, const float* Ut, const int32_t* slot_row,
   if (rc) return rc;
   const int rq = cluster_rows_per_quadrant(R);
   if (rq <= 24 && !getenv("DGC_RNN_EW16"))
-    return launch_lstm_tc2v_ew<H, 12>(m, gx, slot_row, slot_mask, slot_carry, carry, R, L, ld,
-                                      h_out, c_out, save, rq, s);
-  return launch_lstm_tc2v_ew<H, 16>(m, gx, slot_row, slot_mask, slot_carry, carry, R, L, ld,
-                                    h_out, c_out, save, rq, s);
+    return launch_lstm_tc2v_ew<H, 12, false>(m, m, m, nullptr, gx, slot_row, slot_mask, slot_carry,
+                                             carry, R, L, ld, h_out, c_out, save, rq, s);
+  return launch_lstm_tc2v_ew<H, 16, false>(m, m, m, nullptr, gx, slot_row, slot_mask, slot_carry,
+                                           carry, R, L, ld, h_out, c_out, save, rq, s);
+}
+
+// Fused input projection (H = F = 128): x [n, F] (row stride ldx), WxT [4H, F],
+// Ut [4H, H], bias [4H]; no gx.
+int launch_lstm_tc2x(const float* x, int64_t ldx, int64_t n_x, const float* WxT, const float* Ut,
+                     const float* bias, const int32_t* slot_row, const uint8_t* slot_mask,
+                     const int32_t* slot_carry, const float* carry, int64_t R, int L, int64_t ld,
+                     float* h_out, float* c_out, float* save, cudaStream_t s) {
+  constexpr int H = 128;
+  CUtensorMap m, mwx, mx;
+  int rc = make_map(&m, Ut, 4 * H, H, H, 32, H / 2, false);
+  if (!rc) rc = make_map(&mwx, WxT, 4 * H, H, H, 32, H / 2, false);
+  if (!rc) rc = make_gather_map(&mx, x, n_x, H, ldx, 32);
+  if (rc) return rc;
+  const int rq = cluster_rows_per_quadrant(R);
+  if (rq <= 24 && !getenv("DGC_RNN_EW16"))
+    return launch_lstm_tc2v_ew<H, 12, true>(m, mwx, mx, bias, nullptr, slot_row, slot_mask,
+                                            slot_carry, carry, R, L, ld, h_out, c_out, save, rq, s);
+  return launch_lstm_tc2v_ew<H, 16, true>(m, mwx, mx, bias, nullptr, slot_row, slot_mask,
+                                          slot_carry, carry, R, L, ld, h_out, c_out, save, rq, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -1150,6 +1278,25 @@ extern "C" int dgc_rnn_fwd_tc(int32_t cell, const float* gx, const float* Ut,
                 : launch_lstm_tc<128>(gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row_len, ld_out, h_out, c_out, save, s);
     default: return dgc::fail(DGC_ERR_ARG, "rnn_fwd_tc: H must be 32, 64 or 128");
   }
+}
+
+extern "C" int dgc_rnn_fwd_tc_x(int32_t cell, const float* x, int64_t ldx, int64_t n_x, int32_t F,
+                                const float* WxT, const float* Ut, const float* bias,
+                                const int32_t* slot_row, const uint8_t* slot_mask,
+                                const int32_t* slot_carry, const float* carry, int64_t n_rows,
+                                int32_t row_len, int32_t H, int64_t ld_out, float* h_out,
+                                float* c_out, float* save, void* stream) {
+  DGC_REQUIRE(cell == 1, "rnn_fwd_tc_x: LSTM only");
+  DGC_REQUIRE(H == 128 && F == 128, "rnn_fwd_tc_x: fused input projection needs F = H = 128");
+  DGC_REQUIRE(cluster_rnn_enabled(), "rnn_fwd_tc_x: needs the cluster kernels (DGC_NO_CLUSTER_RNN set)");
+  DGC_REQUIRE(c_out != nullptr && bias != nullptr, "rnn_fwd_tc_x: c_out and bias required");
+  if (n_rows == 0 || row_len == 0) return DGC_OK;
+  return launch_lstm_tc2x(x, ldx, n_x, WxT, Ut, bias, slot_row, slot_mask, slot_carry, carry, n_rows,
+                          row_len, ld_out, h_out, c_out, save, dgc::as_stream(stream));
+}
+
+extern "C" int dgc_rnn_fwd_tc_fused_available(int32_t F, int32_t H) {
+  return (F == 128 && H == 128 && cluster_rnn_enabled() && !getenv("DGC_NO_FUSED_XPROJ")) ? 1 : 0;
 }
 
 extern "C" int dgc_debug_lstm_timestamps(unsigned long long* out, int n) {

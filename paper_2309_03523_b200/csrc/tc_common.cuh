@@ -54,6 +54,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+// TMA gather of 4 rows (row indices r0..r3) x one box of columns starting at
+// column c0 into shared memory (rows land consecutively; the map's swizzle
+// applies), completion on `bar` (tensor map box = {cols, 1}).
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, int c0, int r0, int r1,
+                                            int r2, int r3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
 // TMA store of a 2-D box from shared memory (bulk-group completion).
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
@@ -291,6 +302,25 @@ inline EncodeTiledFn encode_fn() {
       fn = reinterpret_cast<EncodeTiledFn>(p);
   }
   return fn;
+}
+
+// Row-gather map of a row-major [rows, cols] fp32 tensor: box = {box_cols, 1},
+// SWIZZLE_128B (tile::gather4 loads 4 given rows per instruction).
+inline int make_gather_map(CUtensorMap* map, const float* ptr, int64_t rows, int64_t cols,
+                           int64_t ld, uint32_t box_cols) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return dgc::fail(DGC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || ((ld * 4) & 15))
+    return dgc::fail(DGC_ERR_ARG, "gather map: 16-byte aligned base and row stride required");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {box_cols, 1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return dgc::fail(DGC_ERR_CUDA, "cuTensorMapEncodeTiled (gather) failed");
+  return DGC_OK;
 }
 
 // Row-major [rows, cols] fp32 tensor with row stride ld (elements).

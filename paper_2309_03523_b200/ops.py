@@ -215,6 +215,28 @@ def rnn_fwd_tc(cell, gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row
         "dgc_rnn_fwd_tc"), nb, 2.0 * n_rows * row_len * H * G * H)
 
 
+def rnn_fwd_tc_fused_available(F, H):
+    return bool(_native.lib().dgc_rnn_fwd_tc_fused_available(F, H))
+
+
+def rnn_fwd_tc_x(x, ldx, WxT, Ut, bias, slot_row, slot_mask, slot_carry, carry, n_rows, row_len,
+                 H, ld_out, h_out, c_out, save):
+    """K4 on tcgen05 with the input projection fused (dgc_rnn_fwd_tc_x): the
+    x rows of each position are TMA-gathered and multiplied by Wx^T in TMEM
+    next to h U^T; no gx round trip through HBM."""
+    _req(x, torch.float32, "x"); _req(WxT, torch.float32, "WxT"); _req(Ut, torch.float32, "Ut")
+    n_inst, F = h_out.shape[0], WxT.shape[1]
+    G = 4
+    sf = rnn_save_floats(1, H)
+    nb = 4 * n_inst * (F + (sf - 1) + 2 * H) + 9 * n_rows * row_len + 4 * G * H * (H + F)
+    _run("lstm_fwd_tc", lambda: _native.check(
+        _native.lib().dgc_rnn_fwd_tc_x(1, _p(x), ldx, x.shape[0], F, _p(WxT), _p(Ut), _p(bias),
+                                       _p(slot_row), _p(slot_mask), _p(slot_carry), _p(carry),
+                                       n_rows, row_len, H, ld_out, _p(h_out), _p(c_out), _p(save),
+                                       _stream()), "dgc_rnn_fwd_tc_x"),
+        nb, 2.0 * n_rows * row_len * H * G * (H + F))
+
+
 def rnn_bwd_tc(cell, U, slot_row, slot_mask, n_rows, row_len, H, save, dh_out, dgx, dc_scratch,
                bias_partial=None):
     """K4 BPTT on tcgen05 (dgc_rnn_bwd_tc): dh = da U^T on tensor cores."""

@@ -164,6 +164,10 @@ class Shard:
         self.tc_rnn = (cfg.precision == "tf32" and cfg.rnn == "lstm" and H in (32, 64, 128)
                        and os.environ.get("DGC_TC_RNN", "1") != "0")
         self.Ut_f = [torch.zeros((GH, H), **f32) for _ in range(cfg.n_rnn)] if self.tc_rnn else None
+        # fused input projection (F = H = 128 cluster recurrence): no gx tensor
+        self.fused_xproj = (self.tc_rnn and cfg.rnn == "lstm" and self.R > 0
+                            and ops.rnn_fwd_tc_fused_available(H, H))
+        self.WxT_f = [torch.zeros((GH, H), **f32) for _ in range(cfg.n_rnn)] if self.fused_xproj else None
         if self.tc_rnn:
             self.rnn_dc_scratch = torch.zeros(((max(self.R, 1) + 127) // 128 * 128, H), **f32)
             self.rnn_tc_prows = ops.rnn_tc_tiles(max(self.R, 1), H)
@@ -352,16 +356,25 @@ class Shard:
         # ---------------- forward: time encoder ----------------
         xr, ldx = self.Hl[1], H
         for k in range(cfg.n_rnn if not self.evolve else 0):
-            ops.gemm(xr, self.pr(f"Wx{k}"), self.gx, n, GH, H, lda=ldx, precision=prec,
-                     bias=self.p(f"br{k}"))
             hb = self.hbuf[k]
             c_out = hb[:, H:] if cell == 1 else None
-            if self.tc_rnn:
+            if self.fused_xproj:
+                # x Wx + h U + b in one tensor-core recurrence (no gx round trip)
+                ops.transpose(self.pr(f"U{k}"), self.Ut_f[k])
+                ops.transpose(self.pr(f"Wx{k}"), self.WxT_f[k])
+                ops.rnn_fwd_tc_x(xr, ldx, self.WxT_f[k], self.Ut_f[k], self.p(f"br{k}"),
+                                 self.slot_row, self.slot_mask, self.slot_carry, self.carry[k],
+                                 self.R, self.L, H, self.hw, hb, c_out, self.save[k])
+            elif self.tc_rnn:
+                ops.gemm(xr, self.pr(f"Wx{k}"), self.gx, n, GH, H, lda=ldx, precision=prec,
+                         bias=self.p(f"br{k}"))
                 ops.transpose(self.pr(f"U{k}"), self.Ut_f[k])
                 ops.rnn_fwd_tc(cell, self.gx, self.Ut_f[k], self.slot_row, self.slot_mask,
                                self.slot_carry, self.carry[k], self.R, self.L, H, self.hw, hb,
                                c_out, self.save[k])
             else:
+                ops.gemm(xr, self.pr(f"Wx{k}"), self.gx, n, GH, H, lda=ldx, precision=prec,
+                         bias=self.p(f"br{k}"))
                 ops.rnn_fwd(cell | rflag, self.gx, self.pr(f"U{k}"), self.slot_row,
                             self.slot_mask, self.slot_carry, self.carry[k], self.R, self.L, H,
                             self.hw, hb, c_out, self.save[k])

@@ -309,6 +309,57 @@ def test_lstm_fwd_tensor_core_matches_simt(H):
     close(outs[1][1][:, :nf * H], outs[0][1][:, :nf * H], 2e-3, "lstm tc save")
 
 
+@pytest.mark.parametrize("n_seq,carry_frac", [(700, 0.3), (9000, 0.0)])
+def test_lstm_fwd_fused_projection_matches_two_step(n_seq, carry_frac):
+    """The fused-projection forward (x rows TMA-gathered by slot_row, x Wx^T +
+    h U^T + b in TMEM) equals gx = x Wx + b (K2) followed by the unfused
+    tensor-core forward: h|c and every saved field, TF32 both ways."""
+    from paper_2309_03523_b200 import ops
+    from paper_2309_03523_b200.layout import pack_sequences_native
+    H = 128
+    if not ops.rnn_fwd_tc_fused_available(H, H):
+        pytest.skip("fused projection disabled in this process")
+    rng = np.random.default_rng(n_seq)
+    lengths = rng.integers(1, 20, size=n_seq)
+    seq, pos, mask, _ = pack_sequences_native(lengths)
+    R, L = seq.shape
+    offs = np.concatenate([[0], np.cumsum(lengths)])
+    n = int(offs[-1])
+    # instances not in slot order: a random permutation of the rows
+    perm = rng.permutation(n)
+    slot_row = np.where(seq >= 0, perm[offs[np.maximum(seq, 0)] + pos], -1).astype(np.int32)
+    run_carry = np.where(rng.random(len(lengths)) < carry_frac, 1, -1)
+    n_carry = int((run_carry > 0).sum())
+    run_carry[run_carry > 0] = np.arange(n_carry)
+    slot_carry = np.where((seq >= 0) & (pos == 0), run_carry[np.maximum(seq, 0)], -1).astype(np.int32)
+    rnd = lambda a: t(a)
+    x = t(rng.standard_normal((n, 2 * H)).astype(np.float32))   # ld 2H, like an h|c buffer
+    ops.round_tf32(x, x)
+    Wx = t((rng.standard_normal((H, 4 * H)) / np.sqrt(H)).astype(np.float32)); ops.round_tf32(Wx, Wx)
+    U = t((rng.standard_normal((H, 4 * H)) / np.sqrt(H)).astype(np.float32)); ops.round_tf32(U, U)
+    b = t(rng.standard_normal(4 * H).astype(np.float32) * 0.1)
+    carry = t(rng.standard_normal((max(n_carry, 1), 2 * H)).astype(np.float32))
+    sr, sm, sc = t(slot_row.reshape(-1), torch.int32), t(mask.reshape(-1), torch.uint8), \
+        t(slot_carry.reshape(-1), torch.int32)
+    Ut = U.t().contiguous()
+    WxT = Wx.t().contiguous()
+    outs = []
+    for fused in (False, True):
+        hc = torch.zeros((n, 2 * H), device=dev)
+        save = torch.zeros((n, 7 * H), device=dev)
+        if fused:
+            ops.rnn_fwd_tc_x(x, 2 * H, WxT, Ut, b, sr, sm, sc, carry, R, L, H, 2 * H, hc, hc[:, H:],
+                             save)
+        else:
+            gx = torch.zeros((n, 4 * H), device=dev)
+            ops.gemm(x, Wx, gx, n, 4 * H, H, lda=2 * H, precision=1, bias=b)
+            ops.rnn_fwd_tc(1, gx, Ut, sr, sm, sc, carry, R, L, H, 2 * H, hc, hc[:, H:], save)
+        torch.cuda.synchronize()
+        outs.append((hc.cpu().numpy(), save.cpu().numpy()))
+    close(outs[1][0], outs[0][0], 2e-3, "fused h|c")  # TF32 operand rounding differs
+    close(outs[1][1][:, :6 * H], outs[0][1][:, :6 * H], 2e-3, "fused save")
+
+
 @pytest.mark.parametrize("H", [32, 64, 128])
 def test_lstm_bwd_tensor_core_matches_simt(H):
     """K4 BPTT on tcgen05 (TF32) vs the fp32 SIMT BPTT on the same packed runs:
