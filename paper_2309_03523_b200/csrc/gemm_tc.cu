@@ -44,8 +44,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // streams; the n_tiles CTAs sharing an A tile run together (L2 dedups A).
   // Two TMEM accumulators let the epilogue drain tile i while the MMA runs i+1.
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~(uintptr_t)1023);
+  // 1024-B aligned base, derived from the __shared__ array (keeps shared-space
+  // addressing: STS/LDS instead of generic ST/LD)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int b_bytes = bn * BK * 4;
   const int ab_bytes = kABytes + b_bytes;
   const int ld_bytes = b_res ? kABytes : ab_bytes;  // bytes TMA-loaded per stage
@@ -59,8 +60,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* bres_full = tempty + 2;  // [1]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_full + 1);
   // epilogue staging (transpose buffers, or 4 KB SWIZZLE_128B boxes), 1024-B aligned
-  float* stg_base = reinterpret_cast<float*>(
-      (reinterpret_cast<uintptr_t>(tmem_slot + 4) + 1023) & ~(uintptr_t)1023);
+  uint8_t* stg_raw = reinterpret_cast<uint8_t*>(tmem_slot + 4);
+  float* stg_base = reinterpret_cast<float*>(stg_raw + ((1024u - (smem_u32(stg_raw) & 1023u)) & 1023u));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tiles_total = m_tiles * n_tiles * splits;

@@ -63,8 +63,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kUnits = H / 2;              // units per epilogue warp
   constexpr uint32_t kTmemCols = G4 <= 128 ? 128 : G4 <= 256 ? 256 : 512;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~(uintptr_t)1023);
+  // 1024-B aligned base, derived from the __shared__ array (keeps shared-space
+  // addressing: STS/LDS instead of generic ST/LD)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + kABytes;
   float* stg_all = reinterpret_cast<float*>(sB + kStages * kBStage);
@@ -298,8 +299,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   constexpr int kXStage = BM * 128;          // one x k-block: 128 rows x 32 fp32
   static_assert(!FX || H == 128, "fused input projection: F = H = 128");
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~(uintptr_t)1023);
+  // 1024-B aligned base, derived from the __shared__ array (keeps shared-space
+  // addressing: STS/LDS instead of generic ST/LD)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + kABytes;
   uint8_t* sX = sB + kStages * kBStage;      // FX: x k-block ring
@@ -467,15 +469,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
     const int64_t grow = row0 + q * rq + rb + r8;
     const bool ok = rb + r8 < rq && grow < R;
     const bool active = rb < rq;             // warps with no rows only keep the protocol
-    float* stg = stg_all + ew * kStgW;
-    float* creg = c_all + (ew * NCH * 32 + lane) * 4;  // + ch * 128
+    const uint32_t stg = smem_u32(stg_all + ew * kStgW);             // byte addresses
+    const uint32_t creg = smem_u32(c_all + (ew * NCH * 32 + lane) * 4);  // + ch * 512
+    const uint32_t sA_s = smem_u32(sA);
     const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
     const uint32_t sA_peer = map_peer(sA, peer);
     const uint32_t afull_peer = map_peer(a_full, peer);
     auto a_off = [&](int k) { return (uint32_t)((k / BK) * BM * 128) + sw128_offset(r, k % BK); };
     auto put_h = [&](int k, float4 v) {
       const uint32_t off = a_off(k);
-      st4(reinterpret_cast<float*>(sA + off), v);
+      sts4(sA_s + off, v);
       st_async_v4(sA_peer + off, v, afull_peer);
     };
     // bytes of the peer's half of the h tile it writes into ours: 8 rows x HU
@@ -498,7 +501,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           v = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
         }
         put_h(j, v);
-        st4(creg + ch * 128, zero4());
+        sts4(creg + ch * 512, zero4());
       }
     }
     publish();
@@ -542,18 +545,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           if (lane >= rb && lane < rb + 8) {
 #pragma unroll
             for (int gi = 0; gi < 4; ++gi) {
-              float* d = stg + (gi * 8 + lane - rb) * 16;
+              const uint32_t d = stg + (gi * 8 + lane - rb) * 64;
 #pragma unroll
               for (int u = 0; u < 16; u += 4)
-                st4(d + u, make_float4(a[gi * 16 + u], a[gi * 16 + u + 1], a[gi * 16 + u + 2],
-                                       a[gi * 16 + u + 3]));
+                sts4(d + u * 4, make_float4(a[gi * 16 + u], a[gi * 16 + u + 1], a[gi * 16 + u + 2],
+                                            a[gi * 16 + u + 3]));
             }
           }
         }
         __syncwarp();
         float4 pre[4];
 #pragma unroll
-        for (int gi = 0; gi < 4; ++gi) pre[gi] = f4(stg + (gi * 8 + r8) * 16 + uq * 4);
+        for (int gi = 0; gi < 4; ++gi) pre[gi] = lds4(stg + ((gi * 8 + r8) * 16 + uq * 4) * 4);
         // next chunk's gx in flight while this chunk computes
         float4 xn[4];
 #pragma unroll
@@ -563,8 +566,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
                         : (inst >= 0 ? ldg4(gxr + gi * H + c0 + 16) : zero4());
         float4 cin = zero4();
         if (ci >= 0) cin = f4(carry + (int64_t)ci * 2 * H + H + j);
-        else if (mk) cin = f4(creg + ch * 128);
-        const float4 hin = f4(reinterpret_cast<const float*>(sA + a_off(j)));
+        else if (mk) cin = lds4(creg + ch * 512);
+        const float4 hin = lds4(sA_s + a_off(j));
         float4 hn = zero4(), cn = zero4();
         if (inst >= 0) {
           float4 ig, fg, gg, og, tc;
@@ -589,7 +592,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           st4(h_out + (int64_t)inst * ld + j, hn);
           st4(c_out + (int64_t)inst * ld + j, cn);
         }
-        st4(creg + ch * 128, cn);
+        sts4(creg + ch * 512, cn);
         if (has_next) {
           float4 v;
           if (n_ci >= 0) {
@@ -703,8 +706,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   constexpr int kBStage = H * 128;           // H rows of U x 32 k
   constexpr uint32_t kTmemCols = 2 * H <= 32 ? 32 : 2 * H <= 64 ? 64 : 2 * H <= 128 ? 128 : 256;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~(uintptr_t)1023);
+  // 1024-B aligned base, derived from the __shared__ array (keeps shared-space
+  // addressing: STS/LDS instead of generic ST/LD)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = sA + kBwdAStages * kAStage;
   float* stg_all = reinterpret_cast<float*>(sB + kBwdBStages * kBStage);
@@ -946,8 +950,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   constexpr int kRecv = BM * HU;             // floats per receive tile
   constexpr uint32_t kTmemCols = 2 * H;      // two N = H accumulators
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~(uintptr_t)1023);
+  // 1024-B aligned base, derived from the __shared__ array (keeps shared-space
+  // addressing: STS/LDS instead of generic ST/LD)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = sA + kKsAStages * kAStage;
   float* recv = reinterpret_cast<float*>(sB + kKsBStages * kBStage);  // [2][128][HU]

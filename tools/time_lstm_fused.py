@@ -1,0 +1,33 @@
+"""Per-position timing of the fused-projection LSTM forward (C2 shape)."""
+import ctypes
+import sys
+sys.path.insert(0, ".")
+import numpy as np, torch
+from paper_2309_03523_b200 import ops, _native
+from paper_2309_03523_b200.layout import pack_sequences_native
+H = 128
+lengths = np.full(6250, 32)
+seq, pos, mask, _ = pack_sequences_native(lengths)
+R, L = seq.shape
+offs = np.concatenate([[0], np.cumsum(lengths)])
+n = int(offs[-1])
+slot_row = np.where(seq >= 0, offs[np.maximum(seq, 0)] + pos, -1).astype(np.int32).reshape(-1)
+dev = "cuda"
+x = torch.randn((n, H), device=dev); WxT = torch.randn((4 * H, H), device=dev) / H ** 0.5
+Ut = torch.randn((4 * H, H), device=dev) / H ** 0.5; b = torch.zeros(4 * H, device=dev)
+sr = torch.tensor(slot_row, device=dev); sm = torch.tensor(mask.reshape(-1), device=dev)
+sc = torch.full((R * L,), -1, dtype=torch.int32, device=dev); carry = torch.zeros((1, 2 * H), device=dev)
+hc = torch.zeros((n, 2 * H), device=dev); save = torch.zeros((n, 7 * H), device=dev)
+fn = lambda: ops.rnn_fwd_tc_x(x, H, WxT, Ut, b, sr, sm, sc, carry, R, L, H, 2 * H, hc, hc[:, H:], save)
+fn(); torch.cuda.synchronize()
+s = torch.cuda.Event(enable_timing=True); e = torch.cuda.Event(enable_timing=True)
+s.record()
+for _ in range(3): fn()
+e.record(); torch.cuda.synchronize()
+print(f"fused fwd H {H}: {s.elapsed_time(e) / 3:.3f} ms")
+fn(); torch.cuda.synchronize()
+buf = (ctypes.c_ulonglong * (256 * 3))()
+_native.lib().dgc_debug_lstm_timestamps(buf, 256 * 3)
+ts = np.array(buf[:L * 3], dtype=np.float64).reshape(L, 3)
+print("per-step us: h-ready->acc", np.mean(ts[:, 1] - ts[:, 0]) / 1e3, "epi", np.mean(ts[:, 2] - ts[:, 1]) / 1e3,
+      "epi_end->next h-ready", np.mean(ts[1:, 0] - ts[:-1, 2]) / 1e3, "step", np.mean(np.diff(ts[:, 0])) / 1e3)
