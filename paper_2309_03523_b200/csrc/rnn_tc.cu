@@ -1096,11 +1096,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
         const int c = 2 * (int)crank + lc;   // global 32-unit chunk
         const int j = 32 * c + lane;         // this lane's hidden unit
         const int seq0 = t * KBO + lc * 4;
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          const int seq = seq0 + g;
-          mbar_wait(&a_empty[seq % kKsAStages], ((seq / kKsAStages) & 1) ^ 1);
-        }
+        bool slots_free = false;  // ring slots are awaited once the first loads are in flight
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
           if (rb + b * kRB >= rq) continue;  // warp-uniform: no rows left
@@ -1123,6 +1119,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
 #pragma unroll
               for (int k = 0; k < 5; ++k) ld[u][k] = 0.f;
             }
+          }
+          if (!slots_free) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              const int seq = seq0 + g;
+              mbar_wait(&a_empty[seq % kKsAStages], ((seq / kKsAStages) & 1) ^ 1);
+            }
+            slots_free = true;
           }
 #pragma unroll
           for (int u = 0; u < kRB; ++u) {
@@ -1157,6 +1161,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
 #pragma unroll
             for (int g = 0; g < 4; ++g)
               *reinterpret_cast<float*>(sA + ((seq0 + g) % kKsAStages) * kAStage + off0) = da[g];
+          }
+        }
+        if (!slots_free) {  // no rows in this warp: keep the a_empty -> a_full phase order
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const int seq = seq0 + g;
+            mbar_wait(&a_empty[seq % kKsAStages], ((seq / kKsAStages) & 1) ^ 1);
           }
         }
         fence_async_smem();
