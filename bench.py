@@ -341,7 +341,7 @@ def run_ours(args):
         "scaling": scaling, "vs_baseline": None, "dtype": "tf32" if args.precision == "tf32" else "f32",
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {pa.n_instances} instances x {pa.T} snapshots, "
-                               f"{pa.n_spatial_edges} edges (power-law, sigma=mu), "
+                               f"{pa.n_spatial_edges} edges (power-law, sigma={'2mu' if args.config.startswith('c5') else 'mu'}), "
                                + (f"EvolveGCN-O (2 GCN, per-snapshot weights), F={cfg.F} H={cfg.H} "
                                   if cfg.model == "evolve" else
                                   f"{cfg.n_rnn}-layer {cfg.rnn.upper()} + 2 GCN, F={cfg.F} H={cfg.H} ")
