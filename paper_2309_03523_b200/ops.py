@@ -228,7 +228,9 @@ def rnn_fwd_tc_x(x, ldx, WxT, Ut, bias, slot_row, slot_mask, slot_carry, carry, 
     n_inst, F = h_out.shape[0], WxT.shape[1]
     G = 4
     sf = rnn_save_floats(1, H)
-    nb = 4 * n_inst * (F + (sf - 1) + 2 * H) + 9 * n_rows * row_len + 4 * G * H * (H + F)
+    # reads x (F); writes h_in, c_in, i, f, g, o (tanh(c) is recomputed by the
+    # BPTT) and h, c
+    nb = 4 * n_inst * (F + (sf - H) + 2 * H) + 9 * n_rows * row_len + 4 * G * H * (H + F)
     _run("lstm_fwd_tc", lambda: _native.check(
         _native.lib().dgc_rnn_fwd_tc_x(1, _p(x), ldx, x.shape[0], F, _p(WxT), _p(Ut), _p(bias),
                                        _p(slot_row), _p(slot_mask), _p(slot_carry), _p(carry),
@@ -242,8 +244,10 @@ def rnn_bwd_tc(cell, U, slot_row, slot_mask, n_rows, row_len, H, save, dh_out, d
     """K4 BPTT on tcgen05 (dgc_rnn_bwd_tc): dh = da U^T on tensor cores."""
     _req(dh_out, torch.float32, "dh_out"); _req(dgx, torch.float32, "dgx")
     n_inst, G = dgx.shape[0], 4
-    sf = rnn_save_floats(1, H)
-    nb = 4 * n_inst * (G * H + 6 * H + H) + 5 * n_rows * row_len + 4 * G * H * H
+    # reads the saved c_in, i, f, g, o (+ tanh(c) unless H = 128, where the
+    # cluster kernel recomputes it) and dh; writes dgx
+    n_saved = 5 if H == 128 else 6
+    nb = 4 * n_inst * (G * H + n_saved * H + H) + 5 * n_rows * row_len + 4 * G * H * H
     _run("lstm_bwd_tc", lambda: _native.check(
         _native.lib().dgc_rnn_bwd_tc(cell, _p(U), _p(slot_row), _p(slot_mask), n_rows, row_len, H,
                                      _p(save), _p(dh_out), _p(dgx), _p(dc_scratch),
