@@ -106,6 +106,7 @@ class Shard:
         self.nnz = lay.nnz
         self.key_rows = _dev_i32(lay.key_rows, dev)
         self.key_ncut = torch.as_tensor(lay.key_ncut.astype(np.int64), device=dev)
+        self.key_ncut_total = int(lay.key_ncut.sum())
         self.tkey_rows = _dev_i32(lay.tkey_rows, dev)
         peers = [p for p in range(self.D) if p != self.d]
         self.peers = peers
@@ -289,7 +290,10 @@ class Shard:
             sends.append(buf)
             idxs.append(idx)
             sent[p] = (idx, c)
-        recv = yield ("a2av", sends, idxs)
+        # without staleness every listed row is sent, so the receive counts are the
+        # plan's (no count exchange, no host sync)
+        rc = None if cache is not None else [recv_rows[p].numel() for p in self.peers]
+        recv = yield ("a2av", sends, idxs, rc)
         fresh = {}
         for p, (buf, idx) in zip(self.peers, zip(*recv)):
             ops.scatter_rows(buf, recv_rows[p], idx, idx.numel(), width, dst)
@@ -306,7 +310,8 @@ class Shard:
             ops.gather_rows(dYext, self.recv_slot[p], idx, idx.numel(), H, buf)
             sends.append(buf)
             idxs.append(idx)
-        recv = yield ("a2av", sends, idxs)
+        # the peers return gradients for exactly the rows they were sent
+        recv = yield ("a2av", sends, idxs, [self.sent[l][p][1] for p in self.peers])
         for p, (buf, _) in zip(self.peers, zip(*recv)):
             idx, c = self.sent[l][p]
             ops.scatter_rows(buf, self.send_rows[p], idx, c, H, dYext, add=True)
@@ -344,7 +349,7 @@ class Shard:
                     info["theta"][f"s{l}"], info["d_r"][f"s{l}"] = th, dr
                     billed = int((cache.send.to(torch.int64) * self.key_ncut).sum().item())
                 else:
-                    billed = int(self.key_ncut.sum().item()) if self.key_ncut.numel() else 0
+                    billed = self.key_ncut_total
                 info["billed_sp"] += billed
                 fresh, sent = yield from self._exchange_rows(
                     Y, H, self.send_pos, self.send_rows, Y, self.recv_slot, cache)
@@ -581,12 +586,14 @@ class NcclRunner:
                     dist.all_reduce(req[1], op=dist.ReduceOp.SUM, group=self.group)
                     out = req[1]
                 else:
-                    out = self._a2av(req[1], req[2])
+                    out = self._a2av(req[1], req[2], req[3] if len(req) > 3 else None)
                 req = g.send(out)
         except StopIteration as stop:
             return [stop.value]
 
-    def _a2av(self, bufs, idxs):
+    def _a2av(self, bufs, idxs, peer_recv_counts=None):
+        """Variable-count all-to-all. peer_recv_counts (per peer, in peer order)
+        skips the count exchange when the caller knows them (no host sync)."""
         dist = self.dist
         D = dist.get_world_size(self.group)
         me = dist.get_rank(self.group)
@@ -596,10 +603,15 @@ class NcclRunner:
         peers = [p for p in range(D) if p != me]
         for p, b in zip(peers, bufs):
             send_counts[p] = b.shape[0]
-        sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
-        rc = torch.empty_like(sc)
-        dist.all_to_all_single(rc, sc, group=self.group)
-        recv_counts = rc.tolist()
+        if peer_recv_counts is not None:
+            recv_counts = [0] * D
+            for p, c in zip(peers, peer_recv_counts):
+                recv_counts[p] = int(c)
+        else:
+            sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
+            rc = torch.empty_like(sc)
+            dist.all_to_all_single(rc, sc, group=self.group)
+            recv_counts = rc.tolist()
         send_f = torch.cat([b.reshape(-1) for b in bufs]) if bufs else torch.empty(0, device=dev)
         send_i = torch.cat(idxs) if idxs else torch.empty(0, dtype=torch.int32, device=dev)
         recv_f = torch.empty(sum(recv_counts) * width, dtype=torch.float32, device=dev)

@@ -22,7 +22,7 @@ def _cfg():
                       precision="fp32")
 
 
-def _run(distributed, plan="t2"):
+def _run(distributed, plan="t2", stale="relax"):
     from pathlib import Path
     from paper_2309_03523_b200 import StaleConfig, load_plan_npz
     from paper_2309_03523_b200.model import init_params, synthetic_inputs
@@ -30,33 +30,36 @@ def _run(distributed, plan="t2"):
     pa = load_plan_npz(Path(__file__).resolve().parents[1] / "artifacts" / plan / "plan.npz")
     cfg = _cfg()
     X, y = synthetic_inputs(pa.n_instances, cfg.F, cfg.C, 0)
-    tr = DGNNTrainer(pa, cfg, StaleConfig.adaptive(), features=X, labels=y,
+    scfg = StaleConfig.adaptive() if stale == "relax" else StaleConfig.off()
+    tr = DGNNTrainer(pa, cfg, scfg, features=X, labels=y,
                      params=init_params(cfg, 0), device="cuda:0", distributed=distributed)
     reps = [tr.run_epoch() for _ in range(EPOCHS)]
     sends = [{k: c.send.cpu().numpy().copy() for k, c in
               [(f"s{l}", sh.scache[l]) for l in range(2)] + [(f"t{k}", sh.tcache[k]) for k in range(cfg.n_rnn)]}
-             for sh in tr.shards]
+             if sh.stale_on else {} for sh in tr.shards]
     return ([r.loss for r in reps], [r.stale_sent_bytes for r in reps], tr.params(0), sends)
 
 
-def _worker(rank, world, plan, port, q):
+def _worker(rank, world, plan, stale, port, q):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        q.put((rank, _run(True, plan)))
+        q.put((rank, _run(True, plan, stale)))
     except Exception as e:  # surface the failure in the parent
         q.put((rank, repr(e)))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("plan,world,port", [("t2", 2, 29571), ("t4", 4, 29572)])
-def test_distributed_runner_equals_local_runner(plan, world, port):
+@pytest.mark.parametrize("plan,world,stale,port", [("t2", 2, "relax", 29571), ("t4", 4, "relax", 29572),
+                                                   ("t2", 2, "off", 29573), ("t4", 4, "off", 29574)])
+def test_distributed_runner_equals_local_runner(plan, world, stale, port):
+    """stale "off" exercises the static-count exchanges (no count all-to-all)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, plan, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, plan, stale, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     got = dict(q.get(timeout=600) for _ in procs)
@@ -64,7 +67,7 @@ def test_distributed_runner_equals_local_runner(plan, world, port):
         p.join(timeout=120)
     for r in range(world):
         assert not isinstance(got[r], str), got[r]
-    loss_l, sent_l, params_l, sends_l = _run(False, plan)
+    loss_l, sent_l, params_l, sends_l = _run(False, plan, stale)
     # 2 ranks: every all-reduce sums 2 operands (exact, order-free) -> bitwise
     # equal. 4 ranks: gloo's gradient SUM order differs from the local runner's
     # sequential order, so later epochs differ by float rounding (~1e-10)
