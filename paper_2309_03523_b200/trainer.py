@@ -641,9 +641,10 @@ class DGNNTrainer:
                  device=None, distributed: bool = False, features=None, labels=None,
                  params=None, cuda_graph: bool = False):
         self.pa, self.cfg = pa, cfg
-        # cuda_graph: a single-device epoch without staleness is a fixed kernel
-        # sequence with no host sync; capture it once (after one eager epoch)
-        # and replay it, so the step is not bound by per-launch host latency
+        # cuda_graph: a single-process epoch without staleness (any number of
+        # local shards) is a fixed kernel sequence with no host sync; capture it
+        # once (after one eager epoch) and replay it, so the step is not bound
+        # by per-launch host latency
         self.cuda_graph = cuda_graph
         self._graph = None
         self._graph_infos = None
@@ -734,8 +735,10 @@ class DGNNTrainer:
         t1 = torch.cuda.Event(enable_timing=True)
         if self._staged_ev is not None:
             self._install_staged()
-        graphable = (self.cuda_graph and len(self.shards) == 1 and self.pa.n_devices == 1
-                     and self.stale.mode is StaleMode.OFF and isinstance(self.runner, LocalRunner))
+        # one process, no staleness: the step (all D local shards and their
+        # exchanges) has no host synchronisation -> capturable
+        graphable = (self.cuda_graph and self.stale.mode is StaleMode.OFF
+                     and isinstance(self.runner, LocalRunner))
         if graphable and r >= 2 and self._graph is None:
             self._graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(self._graph):

@@ -150,8 +150,8 @@ def test_trainer_evolvegcn_matches_oracle(artifacts_dir, precision, tol):
             assert err <= tol, f"epoch {r} grad {k}: {err:.2e}"
 
 
-@pytest.mark.parametrize("H,precision", [(128, "tf32"), (16, "fp32")])
-def test_cuda_graph_epochs_equal_eager(H, precision):
+@pytest.mark.parametrize("H,precision,devices", [(128, "tf32", 1), (16, "fp32", 1), (16, "fp32", 4)])
+def test_cuda_graph_epochs_equal_eager(H, precision, devices):
     """A single-device epoch captured once as a CUDA graph and replayed gives
     bitwise the same losses and parameters as eager epochs (same kernels, every
     reduction in fixed order; the Adam step count lives in device memory)."""
@@ -160,7 +160,9 @@ def test_cuda_graph_epochs_equal_eager(H, precision):
     from paper_2309_03523_b200.trainer import DGNNTrainer
     from paper_2309_03523_b200.model import init_params, synthetic_inputs
     root = Path(__file__).resolve().parents[1]
-    pa = single_device(load_plan_npz(root / "artifacts" / "t4" / "plan.npz"))
+    pa = load_plan_npz(root / "artifacts" / "t4" / "plan.npz")  # D = 4
+    if devices == 1:
+        pa = single_device(pa)
     cfg = DGNNConfig(F=H, H=H, C=16, rnn="lstm", n_rnn=2, optimizer="adam", lr=1e-3,
                      precision=precision)
     X, y = synthetic_inputs(pa.n_instances, cfg.F, cfg.C, 0)
