@@ -215,6 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;           // TMEM lane quadrant this warp may access
     float* stg = stg_base + (warp - 2) * 32 * 33;
     int g = 0, i = 0;
+    int box_seq = 0;
     for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++i) {
       int64_t m0, n0;
       int z, kb0, nkb;
@@ -252,8 +253,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // TMEM -> registers (thread = row) [+ bias] -> this warp's SWIZZLE_128B
         // staging box [32 rows x 32 cols] -> one TMA store per chunk (the copy
         // engine writes the tile; the epilogue never issues global stores).
-        uint8_t* box = reinterpret_cast<uint8_t*>(stg_base + (warp - 2) * 1024);  // 4 KB, aligned
-        for (int c = 32 * chalf; c < bn; c += 32 * (kEpiWarps / 4)) {
+        // tma_store = number of 4 KB boxes per warp (2: ping-pong, a chunk never
+        // waits for the previous chunk's store to leave shared memory)
+        for (int c = 32 * chalf; c < bn; c += 32 * (kEpiWarps / 4), ++box_seq) {
+          uint8_t* box = reinterpret_cast<uint8_t*>(
+              stg_base + ((warp - 2) * tma_store + (box_seq % tma_store)) * 1024);
           float v[32];
           tmem_ld32(tmem_base + (uint32_t)a * acc_cols + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
           const int64_t nb = n0 + c;
@@ -295,7 +299,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (nb + lane < N) colsum_partial[((m0 / BM) * 4 + q) * N + nb + lane] = x[0];
             }
           }
-          if (lane == 0) bulk_wait_read<0>();  // previous chunk's store has left the box
+          if (lane == 0) {  // the store that last used this box has read it
+            if (tma_store == 2) bulk_wait_read<1>();
+            else bulk_wait_read<0>();
+          }
           __syncwarp();
 #pragma unroll
           for (int j = 0; j < 8; ++j)
@@ -467,7 +474,7 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   // shared memory: pipeline stages (+ resident B panel) + the epilogue staging
   // (8 x 4 KB TMA-store boxes, or 8 padded 32x33 transpose tiles) + alignment
   // and barriers, within the 227 KB per-CTA limit
-  const int stg_bytes = tma_store ? kEpiWarps * 4096 : kEpiWarps * 32 * 33 * 4;
+  int stg_bytes = tma_store ? kEpiWarps * 4096 : kEpiWarps * 32 * 33 * 4;
   const int budget = 232448 - 1024 - 256 - 1024 - stg_bytes;
   // B panel resident in shared memory when one CTA keeps one n-tile and it fits
   const int bres_bytes = kb_total * bn * BK * 4;
@@ -481,8 +488,13 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   }
   stages = stages > max_stages ? max_stages : stages;
   if (stages < 1) return dgc::fail(DGC_ERR_ARG, "gemm: tile does not fit shared memory");
-  const size_t smem = (size_t)stages * (b_res ? kABytes : stage_bytes) +
-                      (b_res ? (size_t)bres_bytes : 0) + 1024 + 256 + 1024 + stg_bytes;
+  const size_t pipe = (size_t)stages * (b_res ? kABytes : stage_bytes) + (b_res ? (size_t)bres_bytes : 0);
+  // a second TMA-store box per warp when it fits beside the pipeline
+  if (tma_store && pipe + 1024 + 256 + 1024 + 2 * stg_bytes <= 232448 && !getenv("DGC_GEMM_ONE_BOX")) {
+    tma_store = 2;
+    stg_bytes *= 2;
+  }
+  const size_t smem = pipe + 1024 + 256 + 1024 + stg_bytes;
   auto kern = gemm_tf32_kernel<A_MN, B_MN, SPLIT3>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return dgc::cuda_fail(e, "gemm: set smem");
