@@ -269,10 +269,13 @@ def test_softmax_xent_colsum_optimizers():
     close(pd.cpu().numpy(), ref, 1e-6, "adam")
 
 
-@pytest.mark.parametrize("H", [32, 64, 128])
-def test_lstm_fwd_tensor_core_matches_simt(H):
+@pytest.mark.parametrize("H,ew16", [(32, False), (64, False), (128, False), (128, True)])
+def test_lstm_fwd_tensor_core_matches_simt(H, ew16, monkeypatch):
     """K4 on tcgen05 (TF32) vs the fp32 SIMT kernel on the same packed runs,
-    with cross-device carries at some run starts."""
+    with cross-device carries at some run starts (ew16: the 16-epilogue-warp
+    cluster variant used when rq > 24)."""
+    if ew16:
+        monkeypatch.setenv("DGC_RNN_EW16", "1")
     from paper_2309_03523_b200 import ops
     from paper_2309_03523_b200.layout import pack_sequences_native
     rng = np.random.default_rng(H)
@@ -309,11 +312,13 @@ def test_lstm_fwd_tensor_core_matches_simt(H):
     close(outs[1][1][:, :nf * H], outs[0][1][:, :nf * H], 2e-3, "lstm tc save")
 
 
-@pytest.mark.parametrize("n_seq,carry_frac", [(700, 0.3), (9000, 0.0)])
+@pytest.mark.parametrize("n_seq,carry_frac", [(700, 0.3), (9000, 0.0), (16000, 0.1)])
 def test_lstm_fwd_fused_projection_matches_two_step(n_seq, carry_frac):
     """The fused-projection forward (x rows TMA-gathered by slot_row, x Wx^T +
     h U^T + b in TMEM) equals gx = x Wx + b (K2) followed by the unfused
-    tensor-core forward: h|c and every saved field, TF32 both ways."""
+    tensor-core forward: h|c and every saved field, TF32 both ways. 16000
+    sequences -> R > 7104 packed rows -> rq > 24 rows per lane quadrant (the
+    16-epilogue-warp variants)."""
     from paper_2309_03523_b200 import ops
     from paper_2309_03523_b200.layout import pack_sequences_native
     H = 128
@@ -360,10 +365,12 @@ def test_lstm_fwd_fused_projection_matches_two_step(n_seq, carry_frac):
     close(outs[1][1][:, :6 * H], outs[0][1][:, :6 * H], 2e-3, "fused save")
 
 
-@pytest.mark.parametrize("H", [32, 64, 128])
-def test_lstm_bwd_tensor_core_matches_simt(H):
+@pytest.mark.parametrize("H,ew16", [(32, False), (64, False), (128, False), (128, True)])
+def test_lstm_bwd_tensor_core_matches_simt(H, ew16, monkeypatch):
     """K4 BPTT on tcgen05 (TF32) vs the fp32 SIMT BPTT on the same packed runs:
-    dgx and the fused bias partial sums."""
+    dgx and the fused bias partial sums (ew16: the 16-warp cluster variant)."""
+    if ew16:
+        monkeypatch.setenv("DGC_RNN_EW16", "1")
     from paper_2309_03523_b200 import ops
     from paper_2309_03523_b200.layout import pack_sequences_native
     rng = np.random.default_rng(H + 1)
