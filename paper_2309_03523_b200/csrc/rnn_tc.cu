@@ -309,8 +309,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   float* c_all = stg_all + kVEW * kStgW;     // carried c: [warp][chunk][lane] float4
   uint64_t* b_full = reinterpret_cast<uint64_t*>(c_all + kVEW * NCH * 32 * 4);
   uint64_t* b_empty = b_full + kStages;
-  uint64_t* a_full = b_empty + kStages;
-  uint64_t* acc_full = a_full + 1;           // [2] (FX: per accumulator)
+  // h-tile readiness: FX (double-buffered accumulators) splits it into two
+  // halves -- k-blocks {0, 2} (both CTAs' first 32 units) and {1, 3} -- so the
+  // h U^T MMA of p+1 starts on the first half while the epilogues of p finish
+  constexpr int kHalves = (FX && KB == 4) ? 2 : 1;
+  uint64_t* a_full = b_empty + kStages;      // [2]
+  uint64_t* acc_full = a_full + 2;           // [2] (FX: per accumulator)
   uint64_t* acc_empty = acc_full + 2;        // [2] FX
   uint64_t* x_full = acc_empty + 2;          // [kStages] FX
   uint64_t* x_empty = x_full + kStages;      // [kStages] FX
@@ -329,7 +333,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
     }
     // local epilogue threads arrive (CTA scope); the peer's half of the h tile
     // lands by st.async (complete_tx), expected by one local arrive.expect_tx
-    mbar_init(a_full, kEpiT);
+    mbar_init(&a_full[0], kEpiT);
+    mbar_init(&a_full[1], kEpiT);
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 2);  // both CTAs' MMAs (multicast commit)
       mbar_init(&acc_empty[a], kEpiT);
@@ -401,7 +406,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
                         idx[2], idx[3], &x_full[sx]);
         }
         if (lane == 0) {
-          for (int kb = 0; kb < KB; ++kb, ++g) {
+          for (int i = 0; i < KB; ++i, ++g) {
+            const int kb = kHalves == 2 ? (i >> 1) + 2 * (i & 1) : i;  // 0, 2, 1, 3
             const int s = g % kStages;
             mbar_wait(&b_empty[s], ((g / kStages) & 1) ^ 1);
             mbar_expect_tx(&b_full[s], (uint32_t)kBStage);
@@ -439,12 +445,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           __syncwarp();
         }
       }
-      mbar_wait(a_full, p & 1);
-      fence_after();
-      // generic-proxy writes (local st.shared, peer st.async) -> async proxy (MMA)
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      if (blockIdx.x == 0 && lane == 0 && p < 256) g_lstm_ts[p][0] = globaltimer();
-      for (int kb = 0; kb < KB; ++kb, ++g) {
+      for (int i = 0; i < KB; ++i, ++g) {
+        const int kb = kHalves == 2 ? (i >> 1) + 2 * (i & 1) : i;  // 0, 2, 1, 3
+        if (i % (KB / kHalves) == 0) {
+          mbar_wait(&a_full[i / (KB / kHalves)], p & 1);
+          fence_after();
+          // generic-proxy writes (local st.shared, peer st.async) -> async proxy (MMA)
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          if (i == 0 && blockIdx.x == 0 && lane == 0 && p < 256) g_lstm_ts[p][0] = globaltimer();
+        }
         const int s = g % kStages;
         mbar_wait(&b_full[s], (g / kStages) & 1);
         fence_after();
@@ -453,9 +462,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           for (int kk = 0; kk < BK / 8; ++kk)
             mma_tf32(tacc, kdesc(a_base + kb * BM * 128 + kk * 32),
                      kdesc(b_base + s * kBStage + kk * 32), idesc,
-                     (FX || kb > 0 || kk > 0) ? 1u : 0u);
+                     (FX || i > 0 || kk > 0) ? 1u : 0u);
           mma_commit(&b_empty[s]);
-          if (kb == KB - 1) mma_commit_mc(&acc_full[ab], (uint16_t)0x3);
+          if (i == KB - 1) mma_commit_mc(&acc_full[ab], (uint16_t)0x3);
         }
         __syncwarp();
       }
@@ -476,18 +485,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
     const uint32_t sA_peer = map_peer(sA, peer);
     const uint32_t afull_peer = map_peer(a_full, peer);
     auto a_off = [&](int k) { return (uint32_t)((k / BK) * BM * 128) + sw128_offset(r, k % BK); };
+    // unit k of this CTA lies in h-tile half (k - u0) / 32 (kHalves == 2)
     auto put_h = [&](int k, float4 v) {
       const uint32_t off = a_off(k);
       sts4(sA_s + off, v);
-      st_async_v4(sA_peer + off, v, afull_peer);
+      const uint32_t half = kHalves == 2 ? (uint32_t)((k - u0) >> 5) : 0u;
+      st_async_v4(sA_peer + off, v, afull_peer + half * 8u);
     };
     // bytes of the peer's half of the h tile it writes into ours: 8 rows x HU
     // units per active warp (4 quadrants x ceil(rq / 8) warps)
     const uint32_t kPeerBytes = 4u * (uint32_t)((rq + 7) / 8) * 8u * HU * 4u;
-    auto publish = [&]() {
+    auto publish = [&](int half) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      if (ew == 0 && lane == 0) mbar_arrive_expect_tx(a_full, kPeerBytes);
-      else mbar_arrive(a_full);
+      if (ew == 0 && lane == 0) mbar_arrive_expect_tx(&a_full[half], kPeerBytes / kHalves);
+      else mbar_arrive(&a_full[half]);
+    };
+    auto publish_all = [&]() {
+      for (int h = 0; h < kHalves; ++h) publish(h);
     };
     // prologue: h_in of position 0 (run start: carry or zero)
     if (active) {
@@ -504,7 +518,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
         sts4(creg + ch * 512, zero4());
       }
     }
-    publish();
+    publish_all();
     int n_inst = ok ? slot_row[grow * L] : -1, n_mk = 0, n_ci = ok ? slot_carry[grow * L] : -1;
     for (int p = 0; p < L; ++p) {
       const bool has_next = p + 1 < L;
@@ -523,7 +537,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       if (!active) {  // keep the a_full / acc_empty phase order: step p's MMA done first
         mbar_wait(&acc_full[ab], acc_par);
         if (FX) mbar_arrive(&acc_empty[ab]);
-        if (has_next) publish();
+        if (has_next) publish_all();
         continue;
       }
       const float* gxr = gx + (int64_t)max(inst, 0) * G4 + u0 + uq * 4;
@@ -603,6 +617,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           }
           put_h(j, v);
         }
+        // first half of this CTA's units done: the MMA of p+1 may start on it
+        if (kHalves == 2 && has_next && ch == NCH / 2 - 1) publish(0);
 #pragma unroll
         for (int gi = 0; gi < 4; ++gi) xg[gi] = xn[gi];
         __syncwarp();
@@ -610,7 +626,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       if (blockIdx.x == 0 && threadIdx.x == 64 && p < 256) g_lstm_ts[p][2] = globaltimer();
       fence_before();
       if (FX) mbar_arrive(&acc_empty[ab]);  // this accumulator is drained
-      if (has_next) publish();
+      if (has_next) publish(kHalves - 1);
     }
   }
   fence_before();
