@@ -51,6 +51,11 @@ CONFIGS = {
                  profile=ModelProfile(1, 2, 0, "previous-only", 16, 4), fuse="native"),
     "c3d8": dict(N=1_000_000, T=64, sigma_mult=1.0, D=8, F=16,
                  profile=ModelProfile(1, 2, 0, "previous-only", 16, 4), fuse="native"),
+    # C4: the C3 graph on 8 devices planned with the GCN+GRU recurrent profile
+    # (an EvolveGCN plan is snapshot-local and cuts almost
+    # nothing); the staleness sweep runs on it (tools/stale_sweep.py --plan c4d8)
+    "c4d8": dict(N=1_000_000, T=64, sigma_mult=1.0, D=8, F=16,
+                 profile=ModelProfile.recurrent(16), fuse=False, native_propagate=True),
     # C5: 10M instances x 128 snapshots, sigma = 2 mu, EvolveGCN profile, D = 8.
     # PGC through the native bit-exact propagate port (the Python label
     # propagation needs hours at 10M); assignment by the reference; fusion off
@@ -163,7 +168,7 @@ def build(name: str) -> None:
 
 
 
-def share_graphs(groups=(("c2", ("c2", "c2d2", "c2d4", "c2d8")), ("c3", ("c3d2", "c3d4", "c3d8")),
+def share_graphs(groups=(("c2", ("c2", "c2d2", "c2d4", "c2d8")), ("c3", ("c3d2", "c3d4", "c3d8", "c4d8")),
                          ("c5", ("c5d8",)))):
     """Plans of one graph share artifacts/<g>_graph.npz (the graph arrays); each
     plan.npz keeps only the plan arrays and names its graph file in meta."""
