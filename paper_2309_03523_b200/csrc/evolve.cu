@@ -201,19 +201,14 @@ __global__ void __launch_bounds__(512) evolve_bwd_kernel(
 }
 
 // ---------------------------------------------------------------------------
-// Cluster kernels (the default at F_l = 128): the gate matrices live in shared
-// memory for the whole sequence. A 2-CTA cluster shares one group of NCOL
-// columns and splits the F_l rows in halves: each CTA keeps its row half of all
-// four gate matrices (8 F_l^2 bytes, 128 KB at F_l = 128), k-packed as
-// G[g][k/4][row][k%4] so one 16-byte load feeds four FMAs, and computes those
-// rows. The per-step column vectors every row needs (w and r*w forward; da_c,
-// da_r, da_z backward) are exchanged by st.async into the peer's shared memory
-// with complete_tx on its mbarrier, two exchanges per snapshot; each k-loop
-// runs over the CTA's own half first and waits for the peer's half after it,
-// so the exchange hides behind half of the loop (the halves are summed as
-// separate partials, so every row uses the same order). The L2-streamed
-// kernels above re-read 256 KB of gate matrices per snapshot and are
-// latency-bound on those loads; they remain for the other shapes.
+// Cluster kernels (the default at F_l = 128). A 2-CTA cluster shares one group
+// of NCOL columns and splits the F_l rows in halves; the per-step column
+// vectors every row needs (w and r*w forward; da_c, da_r, da_z backward) are
+// exchanged by st.async into the peer's shared memory with complete_tx on its
+// mbarrier, two exchanges per snapshot, and each lane's k-slice of its own half
+// is summed before it waits for the peer's. The L2-streamed kernels above
+// re-read 256 KB of gate matrices per snapshot and are latency-bound on those
+// loads (2.6 ms per launch at C3 vs 0.15 ms); they remain for other shapes.
 // ---------------------------------------------------------------------------
 using dgc::tc::cluster_rank;
 using dgc::tc::cluster_sync_all;
@@ -229,158 +224,167 @@ __device__ __forceinline__ void put_f32(float* local, uint32_t peer, uint32_t pe
                ::"r"(peer), "f"(v), "r"(peer_bar) : "memory");
 }
 
-// G[g][k/4][il][k%4] = M_g[k][row0 + il] (4-byte cp.async: the element
-// transpose happens in flight; every load of the CTA is issued before the wait).
-template <int RH>
-__device__ __forceinline__ void stage_gates(float* G, int row0, int tid, int nthr, const float* M0,
-                                            const float* M1, const float* M2, const float* M3) {
-  constexpr int FL = 2 * RH, PER = FL * RH;
-  for (int idx = tid; idx < 4 * PER; idx += nthr) {
-    const int g = idx / PER, rem = idx - g * PER, k = rem / RH, il = rem - k * RH;
-    const float* M = g == 0 ? M0 : g == 1 ? M1 : g == 2 ? M2 : M3;
-    const uint32_t dst = smem_u32(G + (((g * (FL / 4) + (k >> 2)) * RH + il) << 2) + (k & 3));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst),
-                 "l"(M + (int64_t)k * FL + row0 + il)
-                 : "memory");
-  }
-}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
-// acc[n] += sum_{k in [k0, k0 + RH)} G[k][il] * V[c0 + n][k]  for one gate.
-template <int NJ, int RH>
-__device__ __forceinline__ void dot_half(const float4* Gg, const float4* V, int k0, int c0,
-                                         float* acc) {
-  constexpr int FL = 2 * RH;
-#pragma unroll 4
-  for (int k4 = k0 / 4; k4 < (k0 + RH) / 4; ++k4) {
-    const float4 g = Gg[k4 * RH];
-#pragma unroll
-    for (int n = 0; n < NJ; ++n) {
-      const float4 v = V[(c0 + n) * (FL / 4) + k4];
-      acc[n] = fmaf(g.x, v.x, fmaf(g.y, v.y, fmaf(g.z, v.z, fmaf(g.w, v.w, acc[n]))));
-    }
-  }
+// four independent partial chains (k mod 4) keep the FMA pipe fed, summed at the end
+__device__ __forceinline__ void fma4(float4& a, const float4& g, const float4& v) {
+  a.x = fmaf(g.x, v.x, a.x);
+  a.y = fmaf(g.y, v.y, a.y);
+  a.z = fmaf(g.z, v.z, a.z);
+  a.w = fmaf(g.w, v.w, a.w);
 }
-// three gates against one vector set (forward phase A)
-template <int NJ, int RH>
-__device__ __forceinline__ void dot3_half(const float4* G0, const float4* G1, const float4* G2,
-                                          const float4* V, int k0, int c0, float* a0, float* a1,
-                                          float* a2) {
-  constexpr int FL = 2 * RH;
-#pragma unroll 4
-  for (int k4 = k0 / 4; k4 < (k0 + RH) / 4; ++k4) {
-    const float4 g0 = G0[k4 * RH], g1 = G1[k4 * RH], g2 = G2[k4 * RH];
-#pragma unroll
-    for (int n = 0; n < NJ; ++n) {
-      const float4 v = V[(c0 + n) * (FL / 4) + k4];
-      a0[n] = fmaf(g0.x, v.x, fmaf(g0.y, v.y, fmaf(g0.z, v.z, fmaf(g0.w, v.w, a0[n]))));
-      a1[n] = fmaf(g1.x, v.x, fmaf(g1.y, v.y, fmaf(g1.z, v.z, fmaf(g1.w, v.w, a1[n]))));
-      a2[n] = fmaf(g2.x, v.x, fmaf(g2.y, v.y, fmaf(g2.z, v.z, fmaf(g2.w, v.w, a2[n]))));
-    }
+__device__ __forceinline__ float hsum(const float4& a) { return (a.x + a.y) + (a.z + a.w); }
+
+// ---------------------------------------------------------------------------
+// Register-resident variant (the default): the CTA's row half of the four
+// gate matrices lives in REGISTERS (128 per thread), so the per-step k-loops
+// read only the exchanged column vectors from shared memory. Thread
+// (row il, slice q) owns k in {own0 + 16q .. +16} and {peer0 + 16q .. +16}
+// (own slice first, the peer's after its mbarrier), the four slice partials
+// of a row are combined with two xor-shuffles (lanes 4il..4il+3), and every
+// lane of the quad then holds the full sums. Vectors are stored with a
+// 20-float pitch per 16-k slice so the four slices of a quad hit disjoint banks.
+// ---------------------------------------------------------------------------
+constexpr int kRR_RH = 64, kRR_FL = 128, kRR_SP = 20, kRR_VP = 8 * kRR_SP;  // 160 floats
+__device__ __forceinline__ int rr_pos(int k) { return (k >> 4) * kRR_SP + (k & 15); }
+
+// one gate's row half -> registers g[0..15] (own slice), g[16..31] (peer slice)
+__device__ __forceinline__ void rr_load_gate(float* stage, const float* M, int own0, int peer0,
+                                             int il, int q, int tid, float* g) {
+  // stage[k][il] = M[k][own0 + il]
+  for (int idx = tid; idx < kRR_FL * kRR_RH; idx += 256) {
+    const int k = idx / kRR_RH, i = idx - k * kRR_RH;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(stage + idx)),
+                 "l"(M + (int64_t)k * kRR_FL + own0 + i)
+                 : "memory");
   }
+  cp_async_wait_all();
+  __syncthreads();
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    g[m] = stage[(own0 + 16 * q + m) * kRR_RH + il];
+    g[16 + m] = stage[(peer0 + 16 * q + m) * kRR_RH + il];
+  }
+  __syncthreads();
 }
 
-template <int NJ, int CB, int RH>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RH * CB) evolve_fwd_cl_kernel(
+// partial dot of 16 gate registers with 16 vector entries starting at slice base
+__device__ __forceinline__ float rr_dot16(const float* g, const float* v) {
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int m = 0; m < 4; ++m) fma4(a, make_float4(g[4 * m], g[4 * m + 1], g[4 * m + 2], g[4 * m + 3]),
+                                   reinterpret_cast<const float4*>(v)[m]);
+  return hsum(a);
+}
+__device__ __forceinline__ float quad_sum(float x) {
+  x += __shfl_xor_sync(0xffffffffu, x, 1);
+  return x + __shfl_xor_sync(0xffffffffu, x, 2);
+}
+
+template <int NCOL>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) evolve_fwd_rr_kernel(
     int Hl, int T, const float* __restrict__ W0, const float* __restrict__ SrT,
     const float* __restrict__ SzT, const float* __restrict__ PcT, const float* __restrict__ QcT,
     const float* __restrict__ Br, const float* __restrict__ Bz, const float* __restrict__ Bc,
     float* __restrict__ Wstack, float* __restrict__ sv_r, float* __restrict__ sv_z,
     float* __restrict__ sv_c, float* __restrict__ sv_w, float* __restrict__ sv_rw, int rnd) {
-  constexpr int FL = 2 * RH, NCOL = CB * NJ, NT = RH * CB;
+  constexpr int RH = kRR_RH, FL = kRR_FL;
   extern __shared__ __align__(16) float sm[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm);  // [0] r*w arrived, [1] w arrived
-  float* G = sm + 4;                                 // [4][FL/4][RH][4]: Sr Sz Pc Qc rows
-  float* w_s = G + 4 * FL * RH;                      // [NCOL][FL]
-  float* rw_s = w_s + NCOL * FL;                     // [NCOL][FL]
+  float* w_s = sm + 4;                               // [NCOL][VP]
+  float* rw_s = w_s + NCOL * kRR_VP;                 // [NCOL][VP]
+  float* stage = rw_s + NCOL * kRR_VP;               // [FL][RH] staging of one gate
   const uint32_t rank = cluster_rank(), peer = rank ^ 1u;
-  const int il = threadIdx.x, jj = threadIdx.y, gi = (int)rank * RH + il;
-  const int c0 = jj * NJ, j0 = (blockIdx.x >> 1) * NCOL, jb = j0 + c0;
-  const int tid = threadIdx.y * RH + threadIdx.x;
-  const int own0 = (int)rank * RH, peer0 = (int)peer * RH;
+  const int tid = threadIdx.x, q = tid & 3, il = tid >> 2, gi = (int)rank * RH + il;
+  const int own0 = (int)rank * RH, peer0 = (int)peer * RH, j0 = (blockIdx.x >> 1) * NCOL;
+  const bool lo = rank == 0;
   if (tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  stage_gates<RH>(G, own0, tid, NT, SrT, SzT, PcT, QcT);
-  for (int idx = tid; idx < FL * NCOL; idx += NT) {  // W_0 for all rows of the group
+  for (int idx = tid; idx < FL * NCOL; idx += 256) {  // W_0 for all rows of the group
     const int k = idx / NCOL, c = idx - k * NCOL, j = j0 + c;
-    w_s[c * FL + k] = j < Hl ? __ldg(W0 + (int64_t)k * Hl + j) : 0.f;
+    w_s[c * kRR_VP + rr_pos(k)] = j < Hl ? __ldg(W0 + (int64_t)k * Hl + j) : 0.f;
   }
-  cp_async_wait_all();
-  cluster_sync_all();  // barriers initialised in both CTAs, shared memory staged
-  const uint32_t rw_peer = map_peer(rw_s + c0 * FL + gi, peer);
-  const uint32_t w_peer = map_peer(w_s + c0 * FL + gi, peer);
+  float gr[32], gz[32], gp[32], gq[32];
+  rr_load_gate(stage, SrT, own0, peer0, il, q, tid, gr);
+  rr_load_gate(stage, SzT, own0, peer0, il, q, tid, gz);
+  rr_load_gate(stage, PcT, own0, peer0, il, q, tid, gp);
+  rr_load_gate(stage, QcT, own0, peer0, il, q, tid, gq);
+  cluster_sync_all();
+  const uint32_t rw_peer = map_peer(rw_s + rr_pos(gi), peer);
+  const uint32_t w_peer = map_peer(w_s + rr_pos(gi), peer);
   const uint32_t bar_rw_peer = map_peer(&bar[0], peer), bar_w_peer = map_peer(&bar[1], peer);
   constexpr uint32_t kXBytes = RH * NCOL * sizeof(float);
-  const float4* G4 = reinterpret_cast<const float4*>(G) + il;
-  const float4* Gr = G4;
-  const float4* Gz = G4 + (FL / 4) * RH;
-  const float4* Gp = G4 + 2 * (FL / 4) * RH;
-  const float4* Gq = G4 + 3 * (FL / 4) * RH;
-  const float4* w4 = reinterpret_cast<const float4*>(w_s);
-  const float4* rw4 = reinterpret_cast<const float4*>(rw_s);
-  float w[NJ], br[NJ], bz[NJ], bc[NJ];
+  const int own_off = rr_pos(own0 + 16 * q), peer_off = rr_pos(peer0 + 16 * q);
+  float w[NCOL], br[NCOL], bz[NCOL], bc[NCOL];
 #pragma unroll
-  for (int n = 0; n < NJ; ++n) {
-    const int j = jb + n;
+  for (int c = 0; c < NCOL; ++c) {
+    const int j = j0 + c;
     const bool ok = j < Hl;
-    w[n] = w_s[(c0 + n) * FL + gi];
-    if (ok) Wstack[(int64_t)gi * Hl + j] = rnd ? dgc::rna_tf32_f(w[n]) : w[n];
-    br[n] = ok ? Br[(int64_t)gi * Hl + j] : 0.f;
-    bz[n] = ok ? Bz[(int64_t)gi * Hl + j] : 0.f;
-    bc[n] = ok ? Bc[(int64_t)gi * Hl + j] : 0.f;
+    w[c] = w_s[c * kRR_VP + rr_pos(gi)];
+    if (ok && (c & 3) == q) Wstack[(int64_t)gi * Hl + j] = rnd ? dgc::rna_tf32_f(w[c]) : w[c];
+    br[c] = ok ? __ldg(Br + (int64_t)gi * Hl + j) : 0.f;
+    bz[c] = ok ? __ldg(Bz + (int64_t)gi * Hl + j) : 0.f;
+    bc[c] = ok ? __ldg(Bc + (int64_t)gi * Hl + j) : 0.f;
   }
   for (int t = 0; t < T; ++t) {
-    // phase A: [Sr; Sz; Pc] w  (own row half of w first, then the peer's)
-    float ar[NJ], az[NJ], ap[NJ], ar2[NJ], az2[NJ], ap2[NJ];
+    // phase A: [Sr; Sz; Pc] w over this lane's own-half slice, then the peer's
+    float pr[NCOL], pz[NCOL], pp[NCOL];
 #pragma unroll
-    for (int n = 0; n < NJ; ++n) ar[n] = az[n] = ap[n] = ar2[n] = az2[n] = ap2[n] = 0.f;
-    dot3_half<NJ, RH>(Gr, Gz, Gp, w4, own0, c0, ar, az, ap);
+    for (int c = 0; c < NCOL; ++c) {
+      const float* v = w_s + c * kRR_VP + own_off;
+      pr[c] = rr_dot16(gr, v);
+      pz[c] = rr_dot16(gz, v);
+      pp[c] = rr_dot16(gp, v);
+    }
     if (t > 0) mbar_wait(&bar[1], (t - 1) & 1);
-    dot3_half<NJ, RH>(Gr, Gz, Gp, w4, peer0, c0, ar2, az2, ap2);
-    float r[NJ], z[NJ], rw[NJ], aq[NJ], aq2[NJ];
+    float r[NCOL], z[NCOL], rw[NCOL], aq[NCOL];
 #pragma unroll
-    for (int n = 0; n < NJ; ++n) {
-      const bool lo = rank == 0;  // partial over rows [0, RH) + partial over [RH, FL)
-      r[n] = sgm((lo ? ar[n] + ar2[n] : ar2[n] + ar[n]) + br[n]);
-      z[n] = sgm((lo ? az[n] + az2[n] : az2[n] + az[n]) + bz[n]);
-      aq[n] = (lo ? ap[n] + ap2[n] : ap2[n] + ap[n]) + bc[n];
-      rw[n] = r[n] * w[n];
-      put_f32(rw_s + (c0 + n) * FL + gi, rw_peer + (uint32_t)(n * FL * 4), bar_rw_peer, rw[n]);
+    for (int c = 0; c < NCOL; ++c) {
+      const float* v = w_s + c * kRR_VP + peer_off;
+      const float xr = rr_dot16(gr + 16, v), xz = rr_dot16(gz + 16, v), xp = rr_dot16(gp + 16, v);
+      r[c] = sgm(quad_sum(lo ? pr[c] + xr : xr + pr[c]) + br[c]);
+      z[c] = sgm(quad_sum(lo ? pz[c] + xz : xz + pz[c]) + bz[c]);
+      aq[c] = quad_sum(lo ? pp[c] + xp : xp + pp[c]) + bc[c];
+      rw[c] = r[c] * w[c];
+      if ((c & 3) == q)
+        put_f32(rw_s + c * kRR_VP + rr_pos(gi), rw_peer + (uint32_t)(c * kRR_VP * 4), bar_rw_peer,
+                rw[c]);
     }
     if (tid == 0) mbar_arrive_expect_tx(&bar[0], kXBytes);
     __syncthreads();
     // phase B: Qc (r * w)
+    float pq[NCOL];
 #pragma unroll
-    for (int n = 0; n < NJ; ++n) ap[n] = ap2[n] = 0.f;
-    dot_half<NJ, RH>(Gq, rw4, own0, c0, ap);
+    for (int c = 0; c < NCOL; ++c) pq[c] = rr_dot16(gq, rw_s + c * kRR_VP + own_off);
     mbar_wait(&bar[0], t & 1);
-    dot_half<NJ, RH>(Gq, rw4, peer0, c0, ap2);
 #pragma unroll
-    for (int n = 0; n < NJ; ++n) {
-      aq2[n] = rank == 0 ? ap[n] + ap2[n] : ap2[n] + ap[n];
-      const int j = jb + n;
-      const float c = tanhf(aq[n] + aq2[n]);
-      const float wn = (1.f - z[n]) * c + z[n] * w[n];
-      if (j < Hl) {
+    for (int c = 0; c < NCOL; ++c) {
+      const float xq = rr_dot16(gq + 16, rw_s + c * kRR_VP + peer_off);
+      const float cc = tanhf(aq[c] + quad_sum(lo ? pq[c] + xq : xq + pq[c]));
+      const float wn = (1.f - z[c]) * cc + z[c] * w[c];
+      const int j = j0 + c;
+      if (j < Hl && (c & 3) == q) {
         const int64_t sidx = ((int64_t)gi * T + t) * Hl + j;  // [Fl][T][Hl]
-        sv_r[sidx] = r[n];
-        sv_z[sidx] = z[n];
-        sv_c[sidx] = c;
-        sv_w[sidx] = rnd ? dgc::rna_tf32_f(w[n]) : w[n];
-        sv_rw[sidx] = rnd ? dgc::rna_tf32_f(rw[n]) : rw[n];
+        sv_r[sidx] = r[c];
+        sv_z[sidx] = z[c];
+        sv_c[sidx] = cc;
+        sv_w[sidx] = rnd ? dgc::rna_tf32_f(w[c]) : w[c];
+        sv_rw[sidx] = rnd ? dgc::rna_tf32_f(rw[c]) : rw[c];
         Wstack[((int64_t)(t + 1) * FL + gi) * Hl + j] = rnd ? dgc::rna_tf32_f(wn) : wn;
       }
-      w[n] = wn;
+      w[c] = wn;
     }
     if (t + 1 < T) {
 #pragma unroll
-      for (int n = 0; n < NJ; ++n)
-        put_f32(w_s + (c0 + n) * FL + gi, w_peer + (uint32_t)(n * FL * 4), bar_w_peer, w[n]);
+      for (int c = 0; c < NCOL; ++c)
+        if ((c & 3) == q)
+          put_f32(w_s + c * kRR_VP + rr_pos(gi), w_peer + (uint32_t)(c * kRR_VP * 4), bar_w_peer,
+                  w[c]);
       if (tid == 0) mbar_arrive_expect_tx(&bar[1], kXBytes);
       __syncthreads();
     }
@@ -388,171 +392,168 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RH * CB) evolve_fwd_
   cluster_sync_all();  // no st.async may still target this CTA's shared memory
 }
 
-template <int NJ, int CB, int RH>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RH * CB) evolve_bwd_cl_kernel(
+template <int NCOL>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) evolve_bwd_rr_kernel(
     int Hl, int T, const float* __restrict__ Sr, const float* __restrict__ Sz,
     const float* __restrict__ Pc, const float* __restrict__ Qc, const float* __restrict__ sv_r,
     const float* __restrict__ sv_z, const float* __restrict__ sv_c, const float* __restrict__ sv_w,
     const float* __restrict__ dW_direct, float* __restrict__ dW0, float* __restrict__ da_r,
     float* __restrict__ da_z, float* __restrict__ da_c, float* __restrict__ dBr,
     float* __restrict__ dBz, float* __restrict__ dBc, int rnd) {
-  constexpr int FL = 2 * RH, NCOL = CB * NJ, NT = RH * CB;
+  constexpr int RH = kRR_RH, FL = kRR_FL;
   extern __shared__ __align__(16) float sm[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm);  // [0] da_c arrived, [1] da_r/da_z arrived
-  float* G = sm + 4;                                 // [4][FL/4][RH][4]: Qc^T Pc^T Sr^T Sz^T rows
-  float* dac_s = G + 4 * FL * RH;                    // [NCOL][FL]
-  float* dar_s = dac_s + NCOL * FL;
-  float* daz_s = dar_s + NCOL * FL;
+  float* dac_s = sm + 4;                             // [NCOL][VP]
+  float* dar_s = dac_s + NCOL * kRR_VP;
+  float* daz_s = dar_s + NCOL * kRR_VP;
+  float* stage = daz_s + NCOL * kRR_VP;
   const uint32_t rank = cluster_rank(), peer = rank ^ 1u;
-  const int il = threadIdx.x, jj = threadIdx.y, gi = (int)rank * RH + il;
-  const int c0 = jj * NJ, jb = (blockIdx.x >> 1) * NCOL + c0;
-  const int tid = threadIdx.y * RH + threadIdx.x;
-  const int own0 = (int)rank * RH, peer0 = (int)peer * RH;
+  const int tid = threadIdx.x, q = tid & 3, il = tid >> 2, gi = (int)rank * RH + il;
+  const int own0 = (int)rank * RH, peer0 = (int)peer * RH, j0 = (blockIdx.x >> 1) * NCOL;
+  const bool lo = rank == 0;
   if (tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  stage_gates<RH>(G, own0, tid, NT, Qc, Pc, Sr, Sz);
-  // inputs of the first BPTT step (t = T - 1) in flight with the staging
-  float nxt_d[NJ], nxt_r[NJ], nxt_z[NJ], nxt_c[NJ], nxt_w[NJ];
+  // gate g's column gi over k: M_g[k][gi] (untransposed source) -> the same staging
+  float gq[32], gp[32], gr[32], gz[32];
+  rr_load_gate(stage, Qc, own0, peer0, il, q, tid, gq);
+  rr_load_gate(stage, Pc, own0, peer0, il, q, tid, gp);
+  rr_load_gate(stage, Sr, own0, peer0, il, q, tid, gr);
+  rr_load_gate(stage, Sz, own0, peer0, il, q, tid, gz);
+  float nd[NCOL], nr[NCOL], nz[NCOL], nc[NCOL], nw[NCOL];
   auto fetch = [&](int t) {
 #pragma unroll
-    for (int n = 0; n < NJ; ++n) {
-      const int j = jb + n;
+    for (int c = 0; c < NCOL; ++c) {
+      const int j = j0 + c;
       const int64_t sidx = ((int64_t)gi * T + t) * Hl + j;
       const bool ok = j < Hl;
-      nxt_d[n] = ok ? __ldg(dW_direct + ((int64_t)t * FL + gi) * Hl + j) : 0.f;
-      nxt_r[n] = ok ? __ldg(sv_r + sidx) : 0.f;
-      nxt_z[n] = ok ? __ldg(sv_z + sidx) : 0.f;
-      nxt_c[n] = ok ? __ldg(sv_c + sidx) : 0.f;
-      nxt_w[n] = ok ? __ldg(sv_w + sidx) : 0.f;
+      nd[c] = ok ? __ldg(dW_direct + ((int64_t)t * FL + gi) * Hl + j) : 0.f;
+      nr[c] = ok ? __ldg(sv_r + sidx) : 0.f;
+      nz[c] = ok ? __ldg(sv_z + sidx) : 0.f;
+      nc[c] = ok ? __ldg(sv_c + sidx) : 0.f;
+      nw[c] = ok ? __ldg(sv_w + sidx) : 0.f;
     }
   };
   fetch(T - 1);
-  cp_async_wait_all();
   cluster_sync_all();
-  const uint32_t dac_peer = map_peer(dac_s + c0 * FL + gi, peer);
-  const uint32_t dar_peer = map_peer(dar_s + c0 * FL + gi, peer);
-  const uint32_t daz_peer = map_peer(daz_s + c0 * FL + gi, peer);
+  const uint32_t dac_peer = map_peer(dac_s + rr_pos(gi), peer);
+  const uint32_t dar_peer = map_peer(dar_s + rr_pos(gi), peer);
+  const uint32_t daz_peer = map_peer(daz_s + rr_pos(gi), peer);
   const uint32_t bar_c_peer = map_peer(&bar[0], peer), bar_rz_peer = map_peer(&bar[1], peer);
   constexpr uint32_t kXBytes = RH * NCOL * sizeof(float);
-  const float4* G4 = reinterpret_cast<const float4*>(G) + il;
-  const float4* Gq = G4;
-  const float4* Gp = G4 + (FL / 4) * RH;
-  const float4* Gr = G4 + 2 * (FL / 4) * RH;
-  const float4* Gz = G4 + 3 * (FL / 4) * RH;
-  const float4* dac4 = reinterpret_cast<const float4*>(dac_s);
-  const float4* dar4 = reinterpret_cast<const float4*>(dar_s);
-  const float4* daz4 = reinterpret_cast<const float4*>(daz_s);
-  const bool lo = rank == 0;
-  float carry[NJ], sbr[NJ], sbz[NJ], sbc[NJ];
+  const int own_off = rr_pos(own0 + 16 * q), peer_off = rr_pos(peer0 + 16 * q);
+  float carry[NCOL], sbr[NCOL], sbz[NCOL], sbc[NCOL];
 #pragma unroll
-  for (int n = 0; n < NJ; ++n) carry[n] = sbr[n] = sbz[n] = sbc[n] = 0.f;
+  for (int c = 0; c < NCOL; ++c) carry[c] = sbr[c] = sbz[c] = sbc[c] = 0.f;
   for (int t = T - 1, s = 0; t >= 0; --t, ++s) {
-    float r[NJ], z[NJ], w[NJ], dz[NJ], dw[NJ], dac[NJ];
+    float r[NCOL], z[NCOL], w[NCOL], dz[NCOL], dw[NCOL], dac[NCOL];
 #pragma unroll
-    for (int n = 0; n < NJ; ++n) {
-      const float g = carry[n] + nxt_d[n];  // grad wrt W_{t+1} (snapshot t+1)
-      const float c = nxt_c[n];
-      r[n] = nxt_r[n];
-      z[n] = nxt_z[n];
-      w[n] = nxt_w[n];
-      dz[n] = g * (w[n] - c);
-      dw[n] = g * z[n];
-      dac[n] = g * (1.f - z[n]) * (1.f - c * c);
-      put_f32(dac_s + (c0 + n) * FL + gi, dac_peer + (uint32_t)(n * FL * 4), bar_c_peer, dac[n]);
+    for (int c = 0; c < NCOL; ++c) {
+      const float g = carry[c] + nd[c];  // grad wrt W_{t+1} (snapshot t+1)
+      const float cc = nc[c];
+      r[c] = nr[c];
+      z[c] = nz[c];
+      w[c] = nw[c];
+      dz[c] = g * (w[c] - cc);
+      dw[c] = g * z[c];
+      dac[c] = g * (1.f - z[c]) * (1.f - cc * cc);
+      if ((c & 3) == q)
+        put_f32(dac_s + c * kRR_VP + rr_pos(gi), dac_peer + (uint32_t)(c * kRR_VP * 4), bar_c_peer,
+                dac[c]);
     }
     if (t > 0) fetch(t - 1);  // next step's inputs stream in under this step
     if (tid == 0) mbar_arrive_expect_tx(&bar[0], kXBytes);
     __syncthreads();
-    float drw[NJ], dpc[NJ], drw2[NJ], dpc2[NJ];
+    float pq[NCOL], pp[NCOL];
 #pragma unroll
-    for (int n = 0; n < NJ; ++n) drw[n] = dpc[n] = drw2[n] = dpc2[n] = 0.f;
-    dot_half<NJ, RH>(Gq, dac4, own0, c0, drw);
-    dot_half<NJ, RH>(Gp, dac4, own0, c0, dpc);
+    for (int c = 0; c < NCOL; ++c) {
+      const float* v = dac_s + c * kRR_VP + own_off;
+      pq[c] = rr_dot16(gq, v);
+      pp[c] = rr_dot16(gp, v);
+    }
     mbar_wait(&bar[0], s & 1);
-    dot_half<NJ, RH>(Gq, dac4, peer0, c0, drw2);
-    dot_half<NJ, RH>(Gp, dac4, peer0, c0, dpc2);
-    float dar[NJ], daz[NJ];
+    float dar[NCOL], daz[NCOL];
 #pragma unroll
-    for (int n = 0; n < NJ; ++n) {
-      const float drw_t = lo ? drw[n] + drw2[n] : drw2[n] + drw[n];
-      const float dpc_t = lo ? dpc[n] + dpc2[n] : dpc2[n] + dpc[n];
-      const float dr = drw_t * w[n];
-      dw[n] = fmaf(drw_t, r[n], dw[n]) + dpc_t;
-      dar[n] = dr * r[n] * (1.f - r[n]);
-      daz[n] = dz[n] * z[n] * (1.f - z[n]);
-      put_f32(dar_s + (c0 + n) * FL + gi, dar_peer + (uint32_t)(n * FL * 4), bar_rz_peer, dar[n]);
-      put_f32(daz_s + (c0 + n) * FL + gi, daz_peer + (uint32_t)(n * FL * 4), bar_rz_peer, daz[n]);
+    for (int c = 0; c < NCOL; ++c) {
+      const float* v = dac_s + c * kRR_VP + peer_off;
+      const float xq = rr_dot16(gq + 16, v), xp = rr_dot16(gp + 16, v);
+      const float drw = quad_sum(lo ? pq[c] + xq : xq + pq[c]);
+      const float dpc = quad_sum(lo ? pp[c] + xp : xp + pp[c]);
+      dw[c] = fmaf(drw, r[c], dw[c]) + dpc;
+      dar[c] = drw * w[c] * r[c] * (1.f - r[c]);
+      daz[c] = dz[c] * z[c] * (1.f - z[c]);
+      if ((c & 3) == q) {
+        put_f32(dar_s + c * kRR_VP + rr_pos(gi), dar_peer + (uint32_t)(c * kRR_VP * 4), bar_rz_peer,
+                dar[c]);
+        put_f32(daz_s + c * kRR_VP + rr_pos(gi), daz_peer + (uint32_t)(c * kRR_VP * 4), bar_rz_peer,
+                daz[c]);
+      }
     }
     if (tid == 0) mbar_arrive_expect_tx(&bar[1], 2 * kXBytes);
     __syncthreads();
-    float e1[NJ], e2[NJ], f1[NJ], f2[NJ];
+    float pr[NCOL], pz[NCOL];
 #pragma unroll
-    for (int n = 0; n < NJ; ++n) e1[n] = e2[n] = f1[n] = f2[n] = 0.f;
-    dot_half<NJ, RH>(Gr, dar4, own0, c0, e1);
-    dot_half<NJ, RH>(Gz, daz4, own0, c0, f1);
+    for (int c = 0; c < NCOL; ++c) {
+      pr[c] = rr_dot16(gr, dar_s + c * kRR_VP + own_off);
+      pz[c] = rr_dot16(gz, daz_s + c * kRR_VP + own_off);
+    }
     mbar_wait(&bar[1], s & 1);
-    dot_half<NJ, RH>(Gr, dar4, peer0, c0, e2);
-    dot_half<NJ, RH>(Gz, daz4, peer0, c0, f2);
 #pragma unroll
-    for (int n = 0; n < NJ; ++n) {
-      const float er = lo ? e1[n] + e2[n] : e2[n] + e1[n];
-      const float ez = lo ? f1[n] + f2[n] : f2[n] + f1[n];
-      dw[n] += er + ez;
-      const int j = jb + n;
-      if (j < Hl) {
+    for (int c = 0; c < NCOL; ++c) {
+      const float xr = rr_dot16(gr + 16, dar_s + c * kRR_VP + peer_off);
+      const float xz = rr_dot16(gz + 16, daz_s + c * kRR_VP + peer_off);
+      const float er = quad_sum(lo ? pr[c] + xr : xr + pr[c]);
+      const float ez = quad_sum(lo ? pz[c] + xz : xz + pz[c]);
+      dw[c] += er + ez;
+      const int j = j0 + c;
+      if (j < Hl && (c & 3) == q) {
         const int64_t sidx = ((int64_t)gi * T + t) * Hl + j;
-        da_r[sidx] = rnd ? dgc::rna_tf32_f(dar[n]) : dar[n];
-        da_z[sidx] = rnd ? dgc::rna_tf32_f(daz[n]) : daz[n];
-        da_c[sidx] = rnd ? dgc::rna_tf32_f(dac[n]) : dac[n];
+        da_r[sidx] = rnd ? dgc::rna_tf32_f(dar[c]) : dar[c];
+        da_z[sidx] = rnd ? dgc::rna_tf32_f(daz[c]) : daz[c];
+        da_c[sidx] = rnd ? dgc::rna_tf32_f(dac[c]) : dac[c];
       }
-      sbr[n] += dar[n];
-      sbz[n] += daz[n];
-      sbc[n] += dac[n];
-      carry[n] = dw[n];
+      sbr[c] += dar[c];
+      sbz[c] += daz[c];
+      sbc[c] += dac[c];
+      carry[c] = dw[c];
     }
   }
 #pragma unroll
-  for (int n = 0; n < NJ; ++n) {
-    const int j = jb + n;
-    if (j < Hl) {
-      dW0[(int64_t)gi * Hl + j] = carry[n];
-      dBr[(int64_t)gi * Hl + j] = sbr[n];
-      dBz[(int64_t)gi * Hl + j] = sbz[n];
-      dBc[(int64_t)gi * Hl + j] = sbc[n];
+  for (int c = 0; c < NCOL; ++c) {
+    const int j = j0 + c;
+    if (j < Hl && (c & 3) == q) {
+      dW0[(int64_t)gi * Hl + j] = carry[c];
+      dBr[(int64_t)gi * Hl + j] = sbr[c];
+      dBz[(int64_t)gi * Hl + j] = sbz[c];
+      dBc[(int64_t)gi * Hl + j] = sbc[c];
     }
   }
   cluster_sync_all();
 }
 
-// Cluster-kernel shape: NJ columns per thread x CB column groups per CTA
-// (DGC_EVOLVE_CL="NJ,CB" in {1,1 1,2 1,4 2,2}; "0" selects the L2-streamed kernels).
-int evolve_cl_variant() {
-  const char* e = getenv("DGC_EVOLVE_CL");
-  if (!e) return 12;
-  int nj = 0, cb = 1;
-  if (sscanf(e, "%d,%d", &nj, &cb) < 1 || nj == 0) return 0;
-  const int v = nj * 10 + cb;
-  return (v == 11 || v == 12 || v == 14 || v == 22) ? v : 12;
-}
-
-template <int NJ, int CB, int NX>
-constexpr size_t evolve_cl_smem() {
-  return 16 + (size_t)(4 * 128 * 64 + NX * NJ * CB * 128) * sizeof(float);
-}
-
-template <int NJ, int CB, int NX, typename Kern, typename... Args>
-int launch_cl(Kern kern, int Hl, cudaStream_t st, const char* name, Args... args) {
-  constexpr int NCOL = NJ * CB;
-  constexpr size_t smem = evolve_cl_smem<NJ, CB, NX>();
+template <int NCOL, int NX, typename Kern, typename... Args>
+int launch_rr(Kern kern, int Hl, cudaStream_t st, const char* name, Args... args) {
+  constexpr size_t smem = 16 + (size_t)(NX * NCOL * kRR_VP + kRR_FL * kRR_RH) * sizeof(float);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return dgc::fail(DGC_ERR_CUDA, std::string(name) + ": " + cudaGetErrorString(e));
   const unsigned groups = (unsigned)((Hl + NCOL - 1) / NCOL);
-  kern<<<2 * groups, dim3(64, CB), smem, st>>>(args...);
+  kern<<<2 * groups, 256, smem, st>>>(args...);
   DGC_CHECK_LAUNCH(name);
   return DGC_OK;
+}
+
+// Weight-evolution kernel: DGC_EVOLVE_CL = "rr1" | "rr2" (default) | "rr4" columns
+// per cluster for the register-resident kernels, "0" for the L2-streamed ones.
+int evolve_rr_cols() {
+  const char* e = getenv("DGC_EVOLVE_CL");
+  if (!e) return 2;
+  if (e[0] == 'r' && e[1] == 'r') {
+    const int n = atoi(e + 2);
+    return n == 1 || n == 4 ? n : 2;
+  }
+  return 0;
 }
 
 int evolve_nj() {
@@ -583,17 +584,14 @@ extern "C" int dgc_evolve_fwd(int32_t Fl, int32_t Hl, int32_t T, const float* W0
                               float* sv_r, float* sv_z, float* sv_c, float* sv_w, float* sv_rw,
                               int32_t flags, void* stream) {
   DGC_REQUIRE(Fl >= 1 && Fl <= 512 && Hl >= 1, "evolve_fwd: bad shape (F <= 512)");
-  const int v = evolve_cl_variant();
-  if (Fl == 128 && v) {
+  const int nc = evolve_rr_cols();
+  if (Fl == 128 && nc) {  // register-resident cluster kernels
     cudaStream_t st = dgc::as_stream(stream);
-#define DGC_FWD_ARGS Hl, T, W0, SrT, SzT, PcT, QcT, Br, Bz, Bc, Wstack, sv_r, sv_z, sv_c, sv_w, sv_rw, flags & 1
-#define DGC_FWD(NJ, CB) launch_cl<NJ, CB, 2>(evolve_fwd_cl_kernel<NJ, CB, 64>, Hl, st, "evolve_fwd_cl", DGC_FWD_ARGS)
-    if (v == 11) return DGC_FWD(1, 1);
-    if (v == 14) return DGC_FWD(1, 4);
-    if (v == 22) return DGC_FWD(2, 2);
-    return DGC_FWD(1, 2);
-#undef DGC_FWD
-#undef DGC_FWD_ARGS
+#define DGC_FWD_RR(N)                                                                           \
+  launch_rr<N, 2>(evolve_fwd_rr_kernel<N>, Hl, st, "evolve_fwd_rr", Hl, T, W0, SrT, SzT, PcT, \
+                  QcT, Br, Bz, Bc, Wstack, sv_r, sv_z, sv_c, sv_w, sv_rw, flags & 1)
+    return nc == 1 ? DGC_FWD_RR(1) : nc == 4 ? DGC_FWD_RR(4) : DGC_FWD_RR(2);
+#undef DGC_FWD_RR
   }
   DGC_EVOLVE_DISPATCH(evolve_fwd_kernel, 2, Fl, Hl, T, W0, SrT, SzT, PcT, QcT, Br, Bz, Bc, Wstack,
                       sv_r, sv_z, sv_c, sv_w, sv_rw, flags & 1);
@@ -608,17 +606,14 @@ extern "C" int dgc_evolve_bwd(int32_t Fl, int32_t Hl, int32_t T, const float* Sr
                               float* da_c, float* dBr, float* dBz, float* dBc, int32_t flags,
                               void* stream) {
   DGC_REQUIRE(Fl >= 1 && Fl <= 512 && Hl >= 1, "evolve_bwd: bad shape (F <= 512)");
-  const int v = evolve_cl_variant();
-  if (Fl == 128 && v) {
+  const int nc = evolve_rr_cols();
+  if (Fl == 128 && nc) {
     cudaStream_t st = dgc::as_stream(stream);
-#define DGC_BWD_ARGS Hl, T, Sr, Sz, Pc, Qc, sv_r, sv_z, sv_c, sv_w, dW_direct, dW0, da_r, da_z, da_c, dBr, dBz, dBc, flags & 1
-#define DGC_BWD(NJ, CB) launch_cl<NJ, CB, 3>(evolve_bwd_cl_kernel<NJ, CB, 64>, Hl, st, "evolve_bwd_cl", DGC_BWD_ARGS)
-    if (v == 11) return DGC_BWD(1, 1);
-    if (v == 14) return DGC_BWD(1, 4);
-    if (v == 22) return DGC_BWD(2, 2);
-    return DGC_BWD(1, 2);
-#undef DGC_BWD
-#undef DGC_BWD_ARGS
+#define DGC_BWD_RR(N)                                                                              \
+  launch_rr<N, 3>(evolve_bwd_rr_kernel<N>, Hl, st, "evolve_bwd_rr", Hl, T, Sr, Sz, Pc, Qc, sv_r, \
+                  sv_z, sv_c, sv_w, dW_direct, dW0, da_r, da_z, da_c, dBr, dBz, dBc, flags & 1)
+    return nc == 1 ? DGC_BWD_RR(1) : nc == 4 ? DGC_BWD_RR(4) : DGC_BWD_RR(2);
+#undef DGC_BWD_RR
   }
   DGC_EVOLVE_DISPATCH(evolve_bwd_kernel, 3, Fl, Hl, T, Sr, Sz, Pc, Qc, sv_r, sv_z, sv_c, sv_w,
                       dW_direct, dW0, da_r, da_z, da_c, dBr, dBz, dBc, flags & 1);
