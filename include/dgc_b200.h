@@ -183,14 +183,14 @@ int dgc_gemm_tf32_stacked_a(const float* A0, int64_t lda0, const float* A1, int6
  * GruCell.step, fusion.py:409-413, input = hidden = W_{t-1}):
  *   R = s(S_r W + B_r), Z = s(S_z W + B_z), C = tanh(P_c W + Q_c (R*W) + B_c),
  *   W_t = (1-Z)*C + Z*W_{t-1}.  W, B_* [Fl, Hl]; S_r, S_z, P_c, Q_c [Fl, Fl].
- * fwd takes the TRANSPOSED gate matrices; writes Wstack [T+1, Fl, Hl]
+ * fwd and bwd take the gate matrices as they are; fwd writes Wstack [T+1, Fl, Hl]
  * (Wstack[0] = W0) and saves r, z, c, w_prev, r*w_prev laid out [Fl, T, Hl].
- * bwd takes the gate matrices as is and dW_direct [T, Fl, Hl] (d loss / d W_t
+ * bwd takes dW_direct [T, Fl, Hl] (d loss / d W_t
  * from the snapshot-t GCN rows); writes dW0 [Fl, Hl], pre-activation grads
  * da_r, da_z, da_c [Fl, T, Hl] (then dS_r = da_r w^T etc. are K2 GEMMs with
  * K = T*Hl) and the bias grads dB_* [Fl, Hl]. flags bit 0: TF32-round saves. */
-int dgc_evolve_fwd(int32_t Fl, int32_t Hl, int32_t T, const float* W0, const float* SrT,
-                   const float* SzT, const float* PcT, const float* QcT, const float* Br,
+int dgc_evolve_fwd(int32_t Fl, int32_t Hl, int32_t T, const float* W0, const float* Sr,
+                   const float* Sz, const float* Pc, const float* Qc, const float* Br,
                    const float* Bz, const float* Bc, float* Wstack, float* sv_r, float* sv_z,
                    float* sv_c, float* sv_w, float* sv_rw, int32_t flags, void* stream);
 int dgc_evolve_bwd(int32_t Fl, int32_t Hl, int32_t T, const float* Sr, const float* Sz,

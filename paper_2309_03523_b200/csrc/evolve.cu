@@ -25,8 +25,8 @@ __device__ __forceinline__ float sgm(float x) { return 1.f / (1.f + __expf(-x));
 // per-column state lives in registers.
 template <int NJ>
 __global__ void __launch_bounds__(512) evolve_fwd_kernel(
-    int Fl, int Hl, int T, const float* __restrict__ W0, const float* __restrict__ SrT,
-    const float* __restrict__ SzT, const float* __restrict__ PcT, const float* __restrict__ QcT,
+    int Fl, int Hl, int T, const float* __restrict__ W0, const float* __restrict__ Sr,
+    const float* __restrict__ Sz, const float* __restrict__ Pc, const float* __restrict__ Qc,
     const float* __restrict__ Br, const float* __restrict__ Bz, const float* __restrict__ Bc,
     float* __restrict__ Wstack, float* __restrict__ sv_r, float* __restrict__ sv_z,
     float* __restrict__ sv_c, float* __restrict__ sv_w, float* __restrict__ sv_rw, int rnd) {
@@ -54,8 +54,8 @@ __global__ void __launch_bounds__(512) evolve_fwd_kernel(
 #pragma unroll
     for (int n = 0; n < NJ; ++n) { ar[n] = br[n]; az[n] = bz[n]; ap[n] = bc[n]; }
     for (int k = 0; k < Fl; ++k) {
-      const float sr = __ldg(SrT + (int64_t)k * Fl + i), sz = __ldg(SzT + (int64_t)k * Fl + i),
-                  pc = __ldg(PcT + (int64_t)k * Fl + i);
+      const float sr = __ldg(Sr + (int64_t)i * Fl + k), sz = __ldg(Sz + (int64_t)i * Fl + k),
+                  pc = __ldg(Pc + (int64_t)i * Fl + k);
 #pragma unroll
       for (int n = 0; n < NJ; ++n) {
         const float wk = w_s[(jj * NJ + n) * Fl + k];
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(512) evolve_fwd_kernel(
 #pragma unroll
     for (int n = 0; n < NJ; ++n) aq[n] = ap[n];
     for (int k = 0; k < Fl; ++k) {
-      const float qc = __ldg(QcT + (int64_t)k * Fl + i);
+      const float qc = __ldg(Qc + (int64_t)i * Fl + k);
 #pragma unroll
       for (int n = 0; n < NJ; ++n) aq[n] = fmaf(qc, rw_s[(jj * NJ + n) * Fl + k], aq[n]);
     }
@@ -250,22 +250,35 @@ __device__ __forceinline__ float hsum(const float4& a) { return (a.x + a.y) + (a
 constexpr int kRR_RH = 64, kRR_FL = 128, kRR_SP = 20, kRR_VP = 8 * kRR_SP;  // 160 floats
 __device__ __forceinline__ int rr_pos(int k) { return (k >> 4) * kRR_SP + (k & 15); }
 
-// one gate's row half -> registers g[0..15] (own slice), g[16..31] (peer slice)
+// One gate's row half -> registers g[0..15] (own slice), g[16..31] (peer slice):
+// g[m] = A[own0 + il][k_m] where A = M (ROWS) or A = M^T (COLUMNS). The staging
+// tile has pitch RH + 1 so both the in-flight transpose and the reads are
+// conflict-free.
+enum class RrSrc { kRows, kColumns };
+template <RrSrc SRC>
 __device__ __forceinline__ void rr_load_gate(float* stage, const float* M, int own0, int peer0,
                                              int il, int q, int tid, float* g) {
-  // stage[k][il] = M[k][own0 + il]
+  constexpr int P = kRR_RH + 1;
   for (int idx = tid; idx < kRR_FL * kRR_RH; idx += 256) {
-    const int k = idx / kRR_RH, i = idx - k * kRR_RH;
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(stage + idx)),
-                 "l"(M + (int64_t)k * kRR_FL + own0 + i)
+    int k, i;
+    const float* src;
+    if constexpr (SRC == RrSrc::kRows) {  // row own0 + i of M, coalesced along k
+      i = idx / kRR_FL, k = idx - i * kRR_FL;
+      src = M + (int64_t)(own0 + i) * kRR_FL + k;
+    } else {  // column own0 + i of M, coalesced along i
+      k = idx / kRR_RH, i = idx - k * kRR_RH;
+      src = M + (int64_t)k * kRR_FL + own0 + i;
+    }
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(stage + k * P + i)),
+                 "l"(src)
                  : "memory");
   }
   cp_async_wait_all();
   __syncthreads();
 #pragma unroll
   for (int m = 0; m < 16; ++m) {
-    g[m] = stage[(own0 + 16 * q + m) * kRR_RH + il];
-    g[16 + m] = stage[(peer0 + 16 * q + m) * kRR_RH + il];
+    g[m] = stage[(own0 + 16 * q + m) * P + il];
+    g[16 + m] = stage[(peer0 + 16 * q + m) * P + il];
   }
   __syncthreads();
 }
@@ -285,8 +298,8 @@ __device__ __forceinline__ float quad_sum(float x) {
 
 template <int NCOL>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) evolve_fwd_rr_kernel(
-    int Hl, int T, const float* __restrict__ W0, const float* __restrict__ SrT,
-    const float* __restrict__ SzT, const float* __restrict__ PcT, const float* __restrict__ QcT,
+    int Hl, int T, const float* __restrict__ W0, const float* __restrict__ Sr,
+    const float* __restrict__ Sz, const float* __restrict__ Pc, const float* __restrict__ Qc,
     const float* __restrict__ Br, const float* __restrict__ Bz, const float* __restrict__ Bc,
     float* __restrict__ Wstack, float* __restrict__ sv_r, float* __restrict__ sv_z,
     float* __restrict__ sv_c, float* __restrict__ sv_w, float* __restrict__ sv_rw, int rnd) {
@@ -310,10 +323,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) evolve_fwd_r
     w_s[c * kRR_VP + rr_pos(k)] = j < Hl ? __ldg(W0 + (int64_t)k * Hl + j) : 0.f;
   }
   float gr[32], gz[32], gp[32], gq[32];
-  rr_load_gate(stage, SrT, own0, peer0, il, q, tid, gr);
-  rr_load_gate(stage, SzT, own0, peer0, il, q, tid, gz);
-  rr_load_gate(stage, PcT, own0, peer0, il, q, tid, gp);
-  rr_load_gate(stage, QcT, own0, peer0, il, q, tid, gq);
+  rr_load_gate<RrSrc::kRows>(stage, Sr, own0, peer0, il, q, tid, gr);
+  rr_load_gate<RrSrc::kRows>(stage, Sz, own0, peer0, il, q, tid, gz);
+  rr_load_gate<RrSrc::kRows>(stage, Pc, own0, peer0, il, q, tid, gp);
+  rr_load_gate<RrSrc::kRows>(stage, Qc, own0, peer0, il, q, tid, gq);
   cluster_sync_all();
   const uint32_t rw_peer = map_peer(rw_s + rr_pos(gi), peer);
   const uint32_t w_peer = map_peer(w_s + rr_pos(gi), peer);
@@ -416,12 +429,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) evolve_bwd_r
     mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // gate g's column gi over k: M_g[k][gi] (untransposed source) -> the same staging
+  // gate g's column gi over k: M_g[k][gi]
   float gq[32], gp[32], gr[32], gz[32];
-  rr_load_gate(stage, Qc, own0, peer0, il, q, tid, gq);
-  rr_load_gate(stage, Pc, own0, peer0, il, q, tid, gp);
-  rr_load_gate(stage, Sr, own0, peer0, il, q, tid, gr);
-  rr_load_gate(stage, Sz, own0, peer0, il, q, tid, gz);
+  rr_load_gate<RrSrc::kColumns>(stage, Qc, own0, peer0, il, q, tid, gq);
+  rr_load_gate<RrSrc::kColumns>(stage, Pc, own0, peer0, il, q, tid, gp);
+  rr_load_gate<RrSrc::kColumns>(stage, Sr, own0, peer0, il, q, tid, gr);
+  rr_load_gate<RrSrc::kColumns>(stage, Sz, own0, peer0, il, q, tid, gz);
   float nd[NCOL], nr[NCOL], nz[NCOL], nc[NCOL], nw[NCOL];
   auto fetch = [&](int t) {
 #pragma unroll
@@ -535,7 +548,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) evolve_bwd_r
 
 template <int NCOL, int NX, typename Kern, typename... Args>
 int launch_rr(Kern kern, int Hl, cudaStream_t st, const char* name, Args... args) {
-  constexpr size_t smem = 16 + (size_t)(NX * NCOL * kRR_VP + kRR_FL * kRR_RH) * sizeof(float);
+  constexpr size_t smem = 16 + (size_t)(NX * NCOL * kRR_VP + kRR_FL * (kRR_RH + 1)) * sizeof(float);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return dgc::fail(DGC_ERR_CUDA, std::string(name) + ": " + cudaGetErrorString(e));
   const unsigned groups = (unsigned)((Hl + NCOL - 1) / NCOL);
@@ -578,8 +591,8 @@ int evolve_nj() {
     else KERN<4><<<grid, block, shm, st>>>(__VA_ARGS__);                                   \
   } while (0)
 
-extern "C" int dgc_evolve_fwd(int32_t Fl, int32_t Hl, int32_t T, const float* W0, const float* SrT,
-                              const float* SzT, const float* PcT, const float* QcT,
+extern "C" int dgc_evolve_fwd(int32_t Fl, int32_t Hl, int32_t T, const float* W0, const float* Sr,
+                              const float* Sz, const float* Pc, const float* Qc,
                               const float* Br, const float* Bz, const float* Bc, float* Wstack,
                               float* sv_r, float* sv_z, float* sv_c, float* sv_w, float* sv_rw,
                               int32_t flags, void* stream) {
@@ -588,12 +601,12 @@ extern "C" int dgc_evolve_fwd(int32_t Fl, int32_t Hl, int32_t T, const float* W0
   if (Fl == 128 && nc) {  // register-resident cluster kernels
     cudaStream_t st = dgc::as_stream(stream);
 #define DGC_FWD_RR(N)                                                                           \
-  launch_rr<N, 2>(evolve_fwd_rr_kernel<N>, Hl, st, "evolve_fwd_rr", Hl, T, W0, SrT, SzT, PcT, \
-                  QcT, Br, Bz, Bc, Wstack, sv_r, sv_z, sv_c, sv_w, sv_rw, flags & 1)
+  launch_rr<N, 2>(evolve_fwd_rr_kernel<N>, Hl, st, "evolve_fwd_rr", Hl, T, W0, Sr, Sz, Pc, \
+                  Qc, Br, Bz, Bc, Wstack, sv_r, sv_z, sv_c, sv_w, sv_rw, flags & 1)
     return nc == 1 ? DGC_FWD_RR(1) : nc == 4 ? DGC_FWD_RR(4) : DGC_FWD_RR(2);
 #undef DGC_FWD_RR
   }
-  DGC_EVOLVE_DISPATCH(evolve_fwd_kernel, 2, Fl, Hl, T, W0, SrT, SzT, PcT, QcT, Br, Bz, Bc, Wstack,
+  DGC_EVOLVE_DISPATCH(evolve_fwd_kernel, 2, Fl, Hl, T, W0, Sr, Sz, Pc, Qc, Br, Bz, Bc, Wstack,
                       sv_r, sv_z, sv_c, sv_w, sv_rw, flags & 1);
   DGC_CHECK_LAUNCH("evolve_fwd_kernel");
   return DGC_OK;

@@ -161,10 +161,10 @@ def gemm_segmented(A, B, C, M, N, K, *, a_mn=False, b_mn=True, lda=None, ldb=Non
     return C
 
 
-def evolve_fwd(Fl, Hl, T, W0, SrT, SzT, PcT, QcT, Br, Bz, Bc, Wstack, sv, rnd=False):
+def evolve_fwd(Fl, Hl, T, W0, Sr, Sz, Pc, Qc, Br, Bz, Bc, Wstack, sv, rnd=False):
     """EvolveGCN-O weight evolution forward (dgc_evolve_fwd); sv = (r, z, c, w, rw)."""
     _run("evolve_fwd", lambda: _native.check(_native.lib().dgc_evolve_fwd(
-        Fl, Hl, T, _p(W0), _p(SrT), _p(SzT), _p(PcT), _p(QcT), _p(Br), _p(Bz), _p(Bc),
+        Fl, Hl, T, _p(W0), _p(Sr), _p(Sz), _p(Pc), _p(Qc), _p(Br), _p(Bz), _p(Bc),
         _p(Wstack), *[_p(x) for x in sv], int(rnd), _stream()), "dgc_evolve_fwd"),
         4 * T * Fl * Hl * 6 + 16 * T * Fl * Fl, 8.0 * T * Fl * Fl * Hl)
 

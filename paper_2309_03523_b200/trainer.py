@@ -212,13 +212,20 @@ class Shard:
         for t in range(T):
             tile_seg[seg[t] // 128:seg[t + 1] // 128] = t
         self.seg_of_mtile = torch.as_tensor(tile_seg, device=dev)
-        # K-segmented work items for dW_t = X_t^T dY_t (chain <= 16 k-blocks in fp32 mode)
-        cap = 16 if self.prec == 3 else 1 << 30
+        # K-segmented work items for dW_t = X_t^T dY_t: chain <= 16 k-blocks in fp32 mode;
+        # in TF32 mode each snapshot's K is split evenly so the items fill two waves of
+        # the 148 SMs (one item per snapshot would leave 84 of them idle at T = 64)
+        total_kb = max(1, int(seg[T] // 32))
         items, item_ptr = [], [0]
         for t in range(T):
             kb0, kb1 = seg[t] // 32, seg[t + 1] // 32
-            for a in range(kb0, kb1, cap):
-                items.append((a, min(cap, kb1 - a)))
+            if self.prec == 3:
+                chunk = 16
+            else:
+                parts = max(1, int(round((kb1 - kb0) * 296 / total_kb)))
+                chunk = max(16, -(-(kb1 - kb0) // parts))
+            for a in range(kb0, kb1, chunk):
+                items.append((a, min(chunk, kb1 - a)))
             item_ptr.append(len(items))
         self.kitems = torch.as_tensor(np.asarray(items, np.int32).reshape(-1), device=dev)
         self.n_kitems = len(items)
@@ -230,7 +237,6 @@ class Shard:
             e = dict(Fl=Fl,
                      Wstack=torch.zeros(((T + 1) * Fl, H), **f32),
                      sv=[torch.zeros((Fl, T * H), **f32) for _ in range(5)],  # r z c w rw
-                     gT=[torch.zeros((Fl, Fl), **f32) for _ in range(4)],      # SrT SzT PcT QcT
                      dW_direct=torch.zeros((T * Fl, H), **f32),
                      da=[torch.zeros((Fl, T * H), **f32) for _ in range(3)])
             self.evo.append(e)
@@ -328,9 +334,8 @@ class Shard:
         # ---------------- forward: structure encoder ----------------
         if self.evolve:  # EvolveGCN-O: W_t for every snapshot, per layer
             for l, e in enumerate(self.evo, start=1):
-                for gi, k in enumerate(("Sr", "Sz", "Pc", "Qc")):
-                    ops.transpose(self.p(f"{k}{l}"), e["gT"][gi])
-                ops.evolve_fwd(e["Fl"], H, cfg.T, self.p(f"W{l}_0"), *e["gT"], self.p(f"Br{l}"),
+                ops.evolve_fwd(e["Fl"], H, cfg.T, self.p(f"W{l}_0"),
+                               *[self.p(f"{k}{l}") for k in ("Sr", "Sz", "Pc", "Qc")], self.p(f"Br{l}"),
                                self.p(f"Bz{l}"), self.p(f"Bc{l}"), e["Wstack"], e["sv"],
                                rnd=self.tf32)
         hin, ldin, kin = self.X, cfg.F, cfg.F

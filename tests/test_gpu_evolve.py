@@ -28,7 +28,6 @@ def _run(variant, Fl, Hl, T, prob):
     W0, Sr, Sz, Pc, Qc, Br, Bz, Bc, dWd = prob
     dev = torch.device("cuda:0")
     f = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float32, device=dev)
-    gT = [f(M.T) for M in (Sr, Sz, Pc, Qc)]
     Wstack = torch.zeros(((T + 1) * Fl, Hl), dtype=torch.float32, device=dev)
     sv = [torch.zeros((Fl, T * Hl), dtype=torch.float32, device=dev) for _ in range(5)]
     da = [torch.zeros((Fl, T * Hl), dtype=torch.float32, device=dev) for _ in range(3)]
@@ -38,7 +37,7 @@ def _run(variant, Fl, Hl, T, prob):
     if variant is not None:
         os.environ["DGC_EVOLVE_CL"] = variant
     try:
-        ops.evolve_fwd(Fl, Hl, T, f(W0), *gT, f(Br), f(Bz), f(Bc), Wstack, sv)
+        ops.evolve_fwd(Fl, Hl, T, f(W0), f(Sr), f(Sz), f(Pc), f(Qc), f(Br), f(Bz), f(Bc), Wstack, sv)
         ops.evolve_bwd(Fl, Hl, T, f(Sr), f(Sz), f(Pc), f(Qc), sv, f(dWd.reshape(T * Fl, Hl)),
                        dW0, da, dB)
         torch.cuda.synchronize()
