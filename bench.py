@@ -53,8 +53,11 @@ def parse():
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
-        d = json.loads(p.read_text())
-        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+        try:
+            d = json.loads(p.read_text())
+            return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+        except (ValueError, KeyError, TypeError):
+            pass
     return 6650.0, 1590.0, "fallback"
 
 
@@ -315,8 +318,9 @@ def run_ours(args):
     name, d = top
     base = name.split("[")[0]
     # the ncu capture's shape must be the dominant one for its traffic to apply
-    if tp.exists() and base in rec and rec[base].get("shape", name) == name:
-        traffic = rec[base]["traffic_bytes"]
+    key = f"{args.config}/{base}"  # records are per workload (config) and shape
+    if tp.exists() and key in rec and rec[key].get("shape", name) == name:
+        traffic = rec[key]["traffic_bytes"]
     avg_ms = d["ms"] / d["launches"]
     achieved = (d["bytes"] / d["launches"]) / (avg_ms / 1e3) / 1e9
     per_kernel = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
