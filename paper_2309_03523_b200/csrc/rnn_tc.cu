@@ -948,9 +948,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
     lstm_bwd_tc2k_kernel(const __grid_constant__ CUtensorMap tmU, const int32_t* __restrict__ slot_row,
                          const uint8_t* __restrict__ slot_mask, int64_t R, int L,
                          const float* __restrict__ save, const float* __restrict__ dh_out,
-                         float* __restrict__ dgx, int rnd, float* __restrict__ bias_partial,
+                         float* __restrict__ dgx, int rnd_pf, float* __restrict__ bias_partial,
                          int rq) {
   static_assert(H == 128, "K-split cluster BPTT is specialised for H = 128");
+  const int rnd = rnd_pf & 1, pf = (rnd_pf >> 1) & 3;  // pf: 1 = L2, 2 = L1 prefetch of the saves
   constexpr int EW = kVEW;
   constexpr int kEpiT = 32 * EW;
   constexpr int RPW = 8;                     // rows per warp (4 warps per quadrant)
@@ -1075,6 +1076,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       const int my_inst = my_ok ? slot_row[my_s] : -1;
       const float my_m = my_ok ? (float)slot_mask[my_s] : 0.f;
       const float my_mnext = (has_next && my_ok) ? (float)slot_mask[my_s + 1] : 0.f;
+      if (pf && my_inst >= 0) {
+        // this row's saved c_in, i, f, g, o and dh_out (the CTA's 64 units) start
+        // streaming in while the position waits for its dh partials
+        const float* sv = save + (int64_t)my_inst * 7 * H + 64 * crank;
+        const float* dd = dh_out + (int64_t)my_inst * H + 64 * crank;
+        if (pf == 1) {
+#pragma unroll
+          for (int k = 1; k <= 5; ++k) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(sv + k * H));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(sv + k * H + 32));
+          }
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(dd));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(dd + 32));
+        } else {
+#pragma unroll
+          for (int k = 1; k <= 5; ++k) {
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(sv + k * H));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(sv + k * H + 32));
+          }
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(dd));
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(dd + 32));
+        }
+      }
       if (blockIdx.x == 0 && threadIdx.x == 64 && t < 256) g_lstm_ts[t][0] = globaltimer();
       const float* rv = recv + (t & 1) * kRecv;
       if (has_next) {
@@ -1239,10 +1263,12 @@ int launch_lstm_bwd_tc2k(const float* U, const int32_t* slot_row, const uint8_t*
   int rc = make_map(&m, U, H, 4 * H, 4 * H, 32, H, false);
   if (rc) return rc;
   const int rq = cluster_rows_per_quadrant(R);
+  static const int pf = getenv("DGC_BWD_PF") ? atoi(getenv("DGC_BWD_PF")) & 3 : 2;
+  const int rnd_pf = (rnd & 1) | (pf << 1);
   if (rq <= 24 && !getenv("DGC_RNN_EW16"))
-    return launch_lstm_bwd_tc2k_ew<H, 12>(m, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
+    return launch_lstm_bwd_tc2k_ew<H, 12>(m, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd_pf,
                                           bias_partial, rq, s);
-  return launch_lstm_bwd_tc2k_ew<H, 16>(m, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
+  return launch_lstm_bwd_tc2k_ew<H, 16>(m, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd_pf,
                                         bias_partial, rq, s);
 }
 
