@@ -208,7 +208,8 @@ int dgc_evolve_bwd(int32_t Fl, int32_t Hl, int32_t T, const float* Sr, const flo
  * slot_row/slot_carry [R*L] int32 (-1 = none), slot_mask [R*L] uint8: the
  * carry mask of gru_forward_masked (fusion.py:457-462). A run start with a
  * remote predecessor loads carry[slot_carry] (h | c for LSTM) instead of 0.
- * h_out/c_out rows have stride ld_out (LSTM: one [n_inst, 2H] h|c buffer).
+ * h_out/c_out rows have stride ld_out (LSTM: one [n_inst, 2H] h|c buffer). The H = 128
+ * cluster kernels write c_out only at the last slot of each run (the carry rows).
  * save [n_inst, dgc_rnn_save_floats] per-instance activations (instance order:
  * GRU [h_in, r*h_in, r, z, c], LSTM [h_in, c_in, i, f, g, o, tanh(c)]).
  * The first H columns of save are the operand of dU = save[:, :H]^T dgx. */

@@ -604,7 +604,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           st4(sv + 5 * H, og);
           if (H != 128) st4(sv + 6 * H, tc);  // H = 128: the cluster BPTT recomputes tanh(c)
           st4(h_out + (int64_t)inst * ld + j, hn);
-          st4(c_out + (int64_t)inst * ld + j, cn);
+          // c leaves the kernel only where a run ends (the carries other devices
+          // read); inside a run it lives in creg and in the successor's c_in save
+          if (!(has_next && n_mk)) st4(c_out + (int64_t)inst * ld + j, cn);
         }
         sts4(creg + ch * 512, cn);
         if (has_next) {

@@ -220,7 +220,7 @@ def rnn_fwd_tc_fused_available(F, H):
 
 
 def rnn_fwd_tc_x(x, ldx, WxT, Ut, bias, slot_row, slot_mask, slot_carry, carry, n_rows, row_len,
-                 H, ld_out, h_out, c_out, save):
+                 H, ld_out, h_out, c_out, save, c_rows=None):
     """K4 on tcgen05 with the input projection fused (dgc_rnn_fwd_tc_x): the
     x rows of each position are TMA-gathered and multiplied by Wx^T in TMEM
     next to h U^T; no gx round trip through HBM."""
@@ -229,8 +229,10 @@ def rnn_fwd_tc_x(x, ldx, WxT, Ut, bias, slot_row, slot_mask, slot_carry, carry, 
     G = 4
     sf = rnn_save_floats(1, H)
     # reads x (F); writes h_in, c_in, i, f, g, o (tanh(c) is recomputed by the
-    # BPTT) and h, c
-    nb = 4 * n_inst * (F + (sf - H) + 2 * H) + 9 * n_rows * row_len + 4 * G * H * (H + F)
+    # BPTT), h, and c at the run ends (c_rows of them)
+    c_rows = n_inst if c_rows is None else c_rows
+    nb = (4 * n_inst * (F + (sf - H) + H) + 4 * c_rows * H + 9 * n_rows * row_len
+          + 4 * G * H * (H + F))
     _run("lstm_fwd_tc", lambda: _native.check(
         _native.lib().dgc_rnn_fwd_tc_x(1, _p(x), ldx, x.shape[0], F, _p(WxT), _p(Ut), _p(bias),
                                        _p(slot_row), _p(slot_mask), _p(slot_carry), _p(carry),

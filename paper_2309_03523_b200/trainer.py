@@ -103,6 +103,14 @@ class Shard:
         self.slot_mask = torch.as_tensor(lay.slot_mask.astype(np.uint8), device=dev)
         self.slot_carry = _dev_i32(lay.slot_carry, dev)
         self.R, self.L = lay.n_rows, lay.row_len
+        # instances at the last slot of their run: the only c rows the cluster LSTM writes
+        if self.R and self.L:
+            sr2 = np.asarray(lay.slot_row).reshape(self.R, self.L)
+            nxt = np.zeros((self.R, self.L), np.uint8)
+            nxt[:, :-1] = np.asarray(lay.slot_mask).reshape(self.R, self.L)[:, 1:]
+            self.n_run_ends = int(((sr2 >= 0) & (nxt == 0)).sum())
+        else:
+            self.n_run_ends = 0
         self.nnz = lay.nnz
         self.key_rows = _dev_i32(lay.key_rows, dev)
         self.key_ncut = torch.as_tensor(lay.key_ncut.astype(np.int64), device=dev)
@@ -374,7 +382,8 @@ class Shard:
                 ops.transpose(self.pr(f"Wx{k}"), self.WxT_f[k])
                 ops.rnn_fwd_tc_x(xr, ldx, self.WxT_f[k], self.Ut_f[k], self.p(f"br{k}"),
                                  self.slot_row, self.slot_mask, self.slot_carry, self.carry[k],
-                                 self.R, self.L, H, self.hw, hb, c_out, self.save[k])
+                                 self.R, self.L, H, self.hw, hb, c_out, self.save[k],
+                                 c_rows=self.n_run_ends)
             elif self.tc_rnn:
                 ops.gemm(xr, self.pr(f"Wx{k}"), self.gx, n, GH, H, lda=ldx, precision=prec,
                          bias=self.p(f"br{k}"))

@@ -269,6 +269,14 @@ def test_softmax_xent_colsum_optimizers():
     close(pd.cpu().numpy(), ref, 1e-6, "adam")
 
 
+def run_end_rows(slot_row, mask):
+    """Instances at the last slot of their run (next slot absent or not continuing)."""
+    sr = np.asarray(slot_row).reshape(mask.shape)
+    nxt = np.zeros_like(mask)
+    nxt[:, :-1] = mask[:, 1:]
+    return sr[(sr >= 0) & (nxt == 0)]
+
+
 @pytest.mark.parametrize("H,ew16", [(32, False), (64, False), (128, False), (128, True)])
 def test_lstm_fwd_tensor_core_matches_simt(H, ew16, monkeypatch):
     """K4 on tcgen05 (TF32) vs the fp32 SIMT kernel on the same packed runs,
@@ -305,7 +313,10 @@ def test_lstm_fwd_tensor_core_matches_simt(H, ew16, monkeypatch):
             ops.rnn_fwd(1, args[0], t(U), *args[2:])
         torch.cuda.synchronize()
         outs.append((hc.cpu().numpy(), save.cpu().numpy()))
-    close(outs[1][0], outs[0][0], 2e-3, "lstm tc h|c")
+    # the cluster forward (H = 128) writes c only at run ends (the carries)
+    ends = run_end_rows(slot_row, mask)
+    close(outs[1][0][:, :H], outs[0][0][:, :H], 2e-3, "lstm tc h")
+    close(outs[1][0][ends, H:], outs[0][0][ends, H:], 2e-3, "lstm tc c at run ends")
     # the H = 128 cluster forward leaves the tanh(c) field (6) unwritten: its BPTT
     # recomputes tanh(f c_in + i g) from the saved c_in, i, f, g
     nf = 6 if H == 128 else 7
@@ -362,6 +373,8 @@ def test_lstm_fwd_fused_projection_matches_two_step(n_seq, carry_frac):
         torch.cuda.synchronize()
         outs.append((hc.cpu().numpy(), save.cpu().numpy()))
     close(outs[1][0], outs[0][0], 2e-3, "fused h|c")  # TF32 operand rounding differs
+    ends = run_end_rows(slot_row, mask)
+    assert np.abs(outs[1][0][ends, H:]).max() > 0  # c written at every run end
     close(outs[1][1][:, :6 * H], outs[0][1][:, :6 * H], 2e-3, "fused save")
 
 
