@@ -943,7 +943,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 // half (TMEM) and the received half. 16 epilogue warps (4 per TMEM lane
 // quadrant, 8 rows each; lane = unit in the BPTT math), carried dc in
 // registers, rq rows per lane quadrant as the forward.
-constexpr int kKsAStages = 4;
+// A-ring depth and receive-tile rows per lane quadrant: the 12-warp variant
+// (rq <= 24) sizes the receive tiles for 24 rows and spends the freed shared
+// memory on 6 A stages, so the second chunk's da rarely waits for the MMA to
+// drain the first chunk's stages.
+template <int kVEW> __host__ __device__ constexpr int ks_a_stages() { return kVEW <= 12 ? 6 : 4; }
+template <int kVEW> __host__ __device__ constexpr int ks_recv_rq() { return kVEW <= 12 ? 24 : 32; }
 constexpr int kKsBStages = 3;
 template <int H, int kVEW>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
@@ -966,7 +971,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   constexpr int kBStage = H * 128;           // H units x 32 gate columns of U
   constexpr int kS = HU + 1;                 // own-half staging row stride (floats)
   constexpr int kStgW = RPW * kS;
-  constexpr int kRecv = BM * HU;             // floats per receive tile
+  constexpr int kKsAStages = ks_a_stages<kVEW>();
+  constexpr int kRQ = ks_recv_rq<kVEW>();    // receive-tile rows per lane quadrant
+  constexpr int kRecv = 4 * kRQ * HU;        // floats per receive tile
   constexpr uint32_t kTmemCols = 2 * H;      // two N = H accumulators
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned base, derived from the __shared__ array (keeps shared-space
@@ -974,7 +981,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = sA + kKsAStages * kAStage;
-  float* recv = reinterpret_cast<float*>(sB + kKsBStages * kBStage);  // [2][128][HU]
+  float* recv = reinterpret_cast<float*>(sB + kKsBStages * kBStage);  // [2][4 kRQ][HU]
   float* stg_all = recv + 2 * kRecv;
   uint64_t* a_full = reinterpret_cast<uint64_t*>(stg_all + EW * kStgW);
   uint64_t* a_empty = a_full + kKsAStages;
@@ -1121,7 +1128,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           }
           tmem_ld16x4(ta + pu0, ta + pu0 + 16, ta + pu0 + 32, ta + pu0 + 48, v);
           if (lane >= rb && lane < rb + RPW) {
-            const uint32_t dst = recv_peer + (uint32_t)(((t & 1) * kRecv + (q * 32 + lane) * HU) * 4);
+            const uint32_t dst = recv_peer + (uint32_t)(((t & 1) * kRecv + (q * kRQ + lane) * HU) * 4);
 #pragma unroll
             for (int u = 0; u < HU; u += 4)
               st_async_v4(dst + u * 4, make_float4(v[u], v[u + 1], v[u + 2], v[u + 3]),
@@ -1150,7 +1157,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
             inst[u] = __shfl_sync(0xffffffffu, my_inst, rl);
             const float mn = __shfl_sync(0xffffffffu, my_mnext, rl);
             dhv[u] = has_next ? mn * (stg[(b * kRB + u) * kS + 32 * lc + lane] +
-                                      rv[(q * 32 + rl) * HU + 32 * lc + lane])
+                                      rv[(q * kRQ + rl) * HU + 32 * lc + lane])
                               : 0.f;
             if (inst[u] >= 0) {
               dhv[u] += dh_out[(int64_t)inst[u] * H + j];
@@ -1245,8 +1252,9 @@ template <int H, int EW>
 int launch_lstm_bwd_tc2k_ew(const CUtensorMap& m, const int32_t* slot_row, const uint8_t* slot_mask,
                             int64_t R, int L, const float* save, const float* dh_out, float* dgx,
                             int rnd, float* bias_partial, int rq, cudaStream_t s) {
-  const size_t smem = (size_t)kKsAStages * BM * 128 + (size_t)kKsBStages * H * 128 +
-                      (size_t)2 * BM * (H / 2) * 4 + (size_t)EW * 8 * (H / 2 + 1) * 4 + 1024 + 512;
+  const size_t smem = (size_t)ks_a_stages<EW>() * BM * 128 + (size_t)kKsBStages * H * 128 +
+                      (size_t)2 * 4 * ks_recv_rq<EW>() * (H / 2) * 4 + (size_t)EW * 8 * (H / 2 + 1) * 4 +
+                      1024 + 512;
   auto kern = lstm_bwd_tc2k_kernel<H, EW>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_bwd_tc2k: set smem");
