@@ -142,6 +142,8 @@ int dgc_spmm_csr(const int32_t* row_ptr, const int32_t* col, const float* dinv,
  * exceeds 16 k-blocks (512 K): the tensor-core fp32 accumulator truncates,
  * which biases long chains. dgc_gemm_splits() returns the split count a call
  * will use, to size `partial` (splits * M * N floats).
+ * accumulate: bit 0 = add into C; bit 1 = ReLU on the output; bit 2 = round the
+ * output to TF32 (bits 1-2 need an unsplit K; applied after bias / relu_src).
  * Replaces the x@W / h@U products of GruCell.step (fusion.py:410-412). */
 int dgc_gemm_splits(int64_t K, int32_t precision, int32_t k_splits);
 int dgc_gemm_tf32(const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
@@ -166,7 +168,10 @@ int dgc_gemm_tf32_segmented(const float* A, int64_t lda, const float* B, int64_t
                             int32_t b_mn, int32_t precision, const float* bias,
                             const float* relu_src, const int32_t* seg_of_mtile, int32_t b_nseg,
                             const int32_t* kitems, int32_t n_kitems, const int32_t* item_ptr,
-                            int32_t n_seg, float* partial, float* colsum_partial, void* stream);
+                            int32_t n_seg, float* partial, float* colsum_partial, int32_t act,
+                            void* stream);
+/* act: bit 0 ReLU, bit 1 TF32-round the output (row-segmented calls; as bits 1-2
+ * of dgc_gemm_tf32's accumulate). */
 
 /* Stacked-A GEMM: op(A) = [op(A0) ; op(A1)] along M (rows [0, M0) from A0,
  * [M0, M) from A1; M0 % 128 == 0), every other argument as dgc_gemm_tf32.

@@ -50,7 +50,8 @@ _SIGS = {
     "dgc_gemm_tf32_stacked_a": (_i32, [_p, _i64, _p, _i64, _i64, _p, _i64, _p, _i64, _i64, _i64,
                                        _i64, _i32, _i32, _i32, _i32, _p, _p]),
     "dgc_gemm_tf32_segmented": (_i32, [_p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _i32, _i32,
-                                        _i32, _p, _p, _p, _i32, _p, _i32, _p, _i32, _p, _p, _p]),
+                                        _i32, _p, _p, _p, _i32, _p, _i32, _p, _i32, _p, _p, _i32,
+                                        _p]),
     "dgc_evolve_fwd": (_i32, [_i32, _i32, _i32] + [_p] * 14 + [_i32, _p]),
     "dgc_evolve_bwd": (_i32, [_i32, _i32, _i32] + [_p] * 16 + [_i32, _p]),
     "dgc_rnn_save_floats": (_i32, [_i32, _i32]),

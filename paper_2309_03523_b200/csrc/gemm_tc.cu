@@ -47,6 +47,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // 1024-B aligned base, derived from the __shared__ array (keeps shared-space
   // addressing: STS/LDS instead of generic ST/LD)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  // accumulate: bit 0 add into C; output activation bits: 1 ReLU, 2 round to TF32
+  const int out_act = accumulate >> 1;
+  accumulate &= 1;
   const int b_bytes = bn * BK * 4;
   const int ab_bytes = kABytes + b_bytes;
   const int ld_bytes = b_res ? kABytes : ab_bytes;  // bytes TMA-loaded per stage
@@ -265,6 +268,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int u = 0; u < 32; ++u) v[u] += (nb + u < N) ? __ldg(bias + nb + u) : 0.f;
           }
+          if (out_act) {
+#pragma unroll
+            for (int u = 0; u < 32; ++u) {
+              if (out_act & 1) v[u] = fmaxf(v[u], 0.f);
+              if (out_act & 2) v[u] = dgc::rna_tf32_f(v[u]);
+            }
+          }
           const int64_t row = m0 + q * 32 + lane;
           if (relu_src || colsum_partial) {
             // ReLU mask from the forward activation (thread = row, 128-B row segment)
@@ -353,6 +363,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else {
               float y = x[u] + acc_in[u] + bn_v;
               if (relu_src && !(aux[u] > 0.f)) y = 0.f;
+              if (out_act & 1) y = fmaxf(y, 0.f);
+              if (out_act & 2) y = dgc::rna_tf32_f(y);
               C[row * ldc + n] = y;
               csum += y;
             }
@@ -526,6 +538,8 @@ static int gemm_impl(const float* A, int64_t lda, const float* B, int64_t ldb, f
                      int32_t accumulate, int32_t k_splits, float* partial, float* colsum_partial,
                      const SegOpts& so, void* stream) {
   DGC_REQUIRE(M >= 0 && N >= 0 && K >= 1, "gemm: bad shape");
+  const int out_act = (accumulate >> 1) & 3;  // bit 1 ReLU, bit 2 TF32-round the output
+  accumulate &= 1;
   DGC_REQUIRE(precision == 1 || precision == 3, "gemm: precision must be 1 (TF32) or 3 (3xTF32)");
   DGC_REQUIRE(k_splits >= 1, "gemm: k_splits >= 1");
   if (M == 0 || N == 0) return DGC_OK;
@@ -576,6 +590,7 @@ static int gemm_impl(const float* A, int64_t lda, const float* B, int64_t ldb, f
             : make_map(&mb, B, N * nseg, K, ldb, 32, (uint32_t)bn, false);
   if (rc) return rc;
   float* part = (splits > 1 || so.kitems) ? partial : nullptr;
+  DGC_REQUIRE(!(part && out_act), "gemm: an output activation needs an unsplit K");
   const bool s3 = precision == 3;
   // plain / bias-only outputs leave through TMA stores (box 32 cols x 32 rows)
   CUtensorMap mc;
@@ -602,7 +617,8 @@ static int gemm_impl(const float* A, int64_t lda, const float* B, int64_t ldb, f
                                   kb_total,                                                      \
                                   splits, kb_per,                                                \
                                   part ? nullptr : bias, part ? nullptr : relu_src,              \
-                                  part ? 0 : accumulate, part, colsum_partial, so, s);
+                                  part ? 0 : (accumulate | (out_act << 1)), part, colsum_partial,\
+                                  so, s);
     DGC_GEMM_CASE(false, false, false)
     DGC_GEMM_CASE(false, true, false)
     DGC_GEMM_CASE(true, false, false)
@@ -648,7 +664,7 @@ extern "C" int dgc_gemm_tf32_segmented(const float* A, int64_t lda, const float*
                                        const int32_t* seg_of_mtile, int32_t b_nseg,
                                        const int32_t* kitems, int32_t n_kitems,
                                        const int32_t* item_ptr, int32_t n_seg, float* partial,
-                                       float* colsum_partial, void* stream) {
+                                       float* colsum_partial, int32_t act, void* stream) {
   DGC_REQUIRE(!(seg_of_mtile && kitems), "gemm_segmented: row- and K-segmentation are exclusive");
   // stacked per-segment B: a 32-row TMA box must not run into the next matrix
   DGC_REQUIRE(!seg_of_mtile || (b_mn ? K % 32 == 0 : N % 16 == 0),
@@ -661,8 +677,8 @@ extern "C" int dgc_gemm_tf32_segmented(const float* A, int64_t lda, const float*
   so.n_kitems = n_kitems;
   so.item_ptr = item_ptr;
   so.n_seg = n_seg;
-  return gemm_impl(A, lda, B, ldb, C, ldc, M, N, K, a_mn, b_mn, precision, bias, relu_src, 0, 1,
-                   partial, colsum_partial, so, stream);
+  return gemm_impl(A, lda, B, ldb, C, ldc, M, N, K, a_mn, b_mn, precision, bias, relu_src,
+                   (act & 3) << 1, 1, partial, colsum_partial, so, stream);
 }
 
 extern "C" int dgc_gemm_tf32_stacked_a(const float* A0, int64_t lda0, const float* A1, int64_t lda1,

@@ -93,8 +93,9 @@ def spmm_csr(row_ptr, col, dinv, Y, bias, out, act: int, nnz=0, n_cols=0):
 
 def gemm(A, B, C, M, N, K, *, a_mn=False, b_mn=True, lda=None, ldb=None, ldc=None,
          precision=3, bias=None, relu_src=None, accumulate=False, k_splits=1, partial=None,
-         colsum_partial=None):
-    """K2 dgc_gemm_tf32 (tcgen05). Defaults: A [M,K] row-major, B [K,N] row-major."""
+         colsum_partial=None, act=0):
+    """K2 dgc_gemm_tf32 (tcgen05). Defaults: A [M,K] row-major, B [K,N] row-major.
+    act: bit 0 ReLU on the output, bit 1 round the output to TF32."""
     for t, nm in ((A, "A"), (B, "B"), (C, "C")):
         _req(t, torch.float32, nm)
     if partial is None and gemm_splits(K, precision, k_splits) > 1:
@@ -111,8 +112,8 @@ def gemm(A, B, C, M, N, K, *, a_mn=False, b_mn=True, lda=None, ldb=None, ldc=Non
     _run(gname, lambda: _native.check(
         _native.lib().dgc_gemm_tf32(
             _p(A), lda, _p(B), ldb, _p(C), ldc, M, N, K, int(a_mn), int(b_mn), precision,
-            _p(bias), _p(relu_src), int(accumulate), k_splits, _p(partial),
-            _p(colsum_partial), _stream()),
+            _p(bias), _p(relu_src), int(accumulate) | ((int(act) & 3) << 1), k_splits,
+            _p(partial), _p(colsum_partial), _stream()),
         "dgc_gemm_tf32"), nb, 2.0 * M * N * K, 1 + int(splits > 1))
     return C
 
@@ -144,8 +145,8 @@ def gemm_stacked_a(A0, A1, B, C, M0, M, N, K, *, a_mn=False, b_mn=True, lda0=Non
 def gemm_segmented(A, B, C, M, N, K, *, a_mn=False, b_mn=True, lda=None, ldb=None, ldc=None,
                    precision=3, bias=None, relu_src=None, seg_of_mtile=None, b_nseg=1,
                    kitems=None, n_kitems=0, item_ptr=None, n_seg=0, partial=None,
-                   colsum_partial=None):
-    """K2 for per-snapshot weights (dgc_gemm_tf32_segmented)."""
+                   colsum_partial=None, act=0):
+    """K2 for per-snapshot weights (dgc_gemm_tf32_segmented); act as in gemm()."""
     lda = lda if lda is not None else (M if a_mn else K)
     ldb = ldb if ldb is not None else (N if b_mn else K)
     ldc = ldc if ldc is not None else N
@@ -156,7 +157,8 @@ def gemm_segmented(A, B, C, M, N, K, *, a_mn=False, b_mn=True, lda=None, ldb=Non
     _run(gname, lambda: _native.check(_native.lib().dgc_gemm_tf32_segmented(
         _p(A), lda, _p(B), ldb, _p(C), ldc, M, N, K, int(a_mn), int(b_mn), precision, _p(bias),
         _p(relu_src), _p(seg_of_mtile), int(b_nseg), _p(kitems), int(n_kitems), _p(item_ptr),
-        int(n_seg), _p(partial), _p(colsum_partial), _stream()), "dgc_gemm_tf32_segmented"),
+        int(n_seg), _p(partial), _p(colsum_partial), int(act), _stream()),
+        "dgc_gemm_tf32_segmented"),
         nb, 2.0 * M * N * K, 1 + int(kitems is not None))
     return C
 

@@ -95,7 +95,7 @@ def test_trainer_stale_schedule_matches_oracle(artifacts_dir, mode):
     assert out[-1][0].stale_reduction_pct > 0.0
 
 
-@pytest.mark.parametrize("name,H", [("t4", 64), ("t2", 128)])
+@pytest.mark.parametrize("name,H", [("t4", 64), ("t2", 128), ("t2-single", 128)])
 def test_trainer_tf32_tensor_core_path(artifacts_dir, name, H):
     """TF32 perf mode (tcgen05 GEMMs + tensor-core LSTM recurrence, TF32-rounded
     operands) against the fp64 oracle. Loss and the time-encoder/readout
@@ -104,11 +104,14 @@ def test_trainer_tf32_tensor_core_path(artifacts_dir, name, H):
     with strong cancellation (|sum| ~ 2-5% of sum|terms| at initialisation),
     which amplifies the ~5e-4 per-element TF32 error of their inputs; they are
     held to 5e-2 in tensor norm (the fp32 mode meets 1e-4 on all of them)."""
-    from paper_2309_03523_b200 import load_plan_npz
-    pa = load_plan_npz(artifacts_dir / name / "plan.npz")
+    from paper_2309_03523_b200 import load_plan_npz, single_device
+    pa = load_plan_npz(artifacts_dir / name.split("-")[0] / "plan.npz")
+    if name.endswith("-single"):  # one device: layer 1 runs aggregate-first
+        pa = single_device(pa)
     out, tr, _ = run_pair(pa, dict(F=32, H=H, C=16, rnn="lstm", n_rnn=2), "off", epochs=2,
                           precision="tf32")
     assert tr.shards[0].tc_rnn
+    assert tr.shards[0].agg_first == name.endswith("-single")
     for rep, o, grads in out:
         assert rep.loss == pytest.approx(o["loss"], rel=2e-2)
         for k, g in grads.items():
@@ -121,20 +124,47 @@ def test_trainer_tf32_tensor_core_path(artifacts_dir, name, H):
                 assert err <= 2e-2, f"epoch {rep.epoch} grad {k}: {err:.2e}"
 
 
-@pytest.mark.parametrize("precision,tol", [("fp32", 1e-4), ("tf32", 5e-2)])
-def test_trainer_evolvegcn_matches_oracle(artifacts_dir, precision, tol):
+def test_trainer_aggregate_first_fp32(artifacts_dir, monkeypatch):
+    """Layer 1 as relu((A X) W1 + b1) (the single-device TF32 default, forced
+    here in fp32 mode) against the oracle's relu(A (X W1) + b1). Loss and every
+    gradient except W1/b1 within 1e-4; W1/b1 in norm, because the reassociated
+    sum can flip a ReLU whose pre-activation lies within rounding of 0 (one flip
+    moves single entries of W1/b1 by ~1e-3 of their max)."""
+    monkeypatch.setenv("DGC_AGG_FIRST", "1")
+    from paper_2309_03523_b200 import load_plan_npz, single_device
+    pa = single_device(load_plan_npz(artifacts_dir / "t2" / "plan.npz"))
+    out, tr, _ = run_pair(pa, dict(F=32, H=64, C=16, rnn="lstm", n_rnn=2), "off", epochs=2)
+    assert tr.shards[0].agg_first
+    for rep, o, grads in out:
+        assert rep.loss == pytest.approx(o["loss"], rel=1e-4)
+        for k, g in grads.items():
+            ref = o["grads"][k]
+            if k in ("W1", "b1"):
+                err = np.linalg.norm(g - ref) / np.linalg.norm(ref)
+                assert err <= 1e-3, f"epoch {rep.epoch} grad {k}: rel-norm {err:.2e}"
+            else:
+                err = np.abs(g - ref).max() / max(np.abs(ref).max(), 1e-30)
+                assert err <= 1e-4, f"epoch {rep.epoch} grad {k}: {err:.2e}"
+
+
+@pytest.mark.parametrize("precision,tol,single", [("fp32", 1e-4, False), ("tf32", 5e-2, False),
+                                                  ("tf32", 5e-2, True)])
+def test_trainer_evolvegcn_matches_oracle(artifacts_dir, precision, tol, single):
     """C3 model (EvolveGCN-O weight evolution + per-snapshot GCN on snapshot-
     segmented layouts) on the reference's 2-device EvolveGCN plan vs the oracle."""
-    from paper_2309_03523_b200 import DGNNConfig, load_plan_npz
+    from paper_2309_03523_b200 import DGNNConfig, load_plan_npz, single_device
     from paper_2309_03523_b200.model import init_params, synthetic_inputs
     from paper_2309_03523_b200.trainer import DGNNTrainer
     pa = load_plan_npz(artifacts_dir / "e2" / "plan.npz")
+    if single:  # one device: layer 1 aggregate-first on the per-snapshot weights
+        pa = single_device(pa)
     T = int(pa.inst_t.max())
     cfg = DGNNConfig(F=32, H=32, C=8, model="evolve", n_rnn=0, T=T, optimizer="sgd", lr=0.05,
                      precision=precision)
     X, y = synthetic_inputs(pa.n_instances, cfg.F, cfg.C, 0)
     params = init_params(cfg, 0)
     tr = DGNNTrainer(pa, cfg, None, features=X, labels=y, params=params)
+    assert tr.shards[0].agg_first == single
     lays = build_layouts(pa.n_instances, pa.inst_entity, pa.inst_t, pa.spatial_edges,
                          pa.temporal_links, pa.structure_device, pa.chunk_of, pa.n_devices,
                          pa.group_device, pa.group_ptr, pa.group_chunks)
