@@ -250,6 +250,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int a = i & 1;
       const uint32_t aph = (i >> 1) & 1;
+      if (relu_src && tma_store) {
+        // this thread's row of the ReLU mask streams into L1 while the tile's
+        // MMAs finish (thread = row; its chunks of the tile's columns)
+        const int64_t row = m0 + q * 32 + lane;
+        if (row < M)
+          for (int c = 32 * chalf; c < bn; c += 32 * (kEpiWarps / 4))
+            if (n0 + c < N)
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(relu_src + row * ldc + n0 + c));
+      }
       mbar_wait(&tfull[a], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (tma_store) {
