@@ -237,14 +237,25 @@ class Shard:
         # in TF32 mode each snapshot's K is split evenly so the items fill two waves of
         # the 148 SMs (one item per snapshot would leave 84 of them idle at T = 64)
         total_kb = max(1, int(seg[T] // 32))
+        kbs = [int(seg[t + 1] // 32 - seg[t] // 32) for t in range(T)]
+        # TF32: a whole number of waves (2 x 148 items when T <= 296), split by
+        # largest remainder so every item has ~total/target k-blocks
+        target = 2 * 148 if T <= 296 else -(-T // 148) * 148
+        share = [k * target / total_kb for k in kbs]
+        parts = [max(1, int(x)) if k else 0 for x, k in zip(share, kbs)]
+        order = sorted(range(T), key=lambda t: -(share[t] - int(share[t])))
+        for t in order:
+            if sum(parts) >= target:
+                break
+            if kbs[t] > parts[t]:
+                parts[t] += 1
         items, item_ptr = [], [0]
         for t in range(T):
             kb0, kb1 = seg[t] // 32, seg[t + 1] // 32
             if self.prec == 3:
                 chunk = 16
             else:
-                parts = max(1, int(round((kb1 - kb0) * 296 / total_kb)))
-                chunk = max(16, -(-(kb1 - kb0) // parts))
+                chunk = max(1, -(-(kb1 - kb0) // max(1, parts[t])))
             for a in range(kb0, kb1, chunk):
                 items.append((a, min(chunk, kb1 - a)))
             item_ptr.append(len(items))
