@@ -270,11 +270,18 @@ class Shard:
                      Wstack=torch.zeros(((T + 1) * Fl, H), **f32),
                      sv=[torch.zeros((Fl, T * H), **f32) for _ in range(5)],  # r z c w rw
                      dW_direct=torch.zeros((T * Fl, H), **f32),
-                     da=[torch.zeros((Fl, T * H), **f32) for _ in range(3)])
+                     da_all=torch.zeros((3 * Fl, T * H), **f32))
+            e["da"] = [e["da_all"][i * Fl:(i + 1) * Fl] for i in range(3)]  # r z c, contiguous
             self.evo.append(e)
         self.evo_gsplit = max(1, min(64, (T * H) // 128))
         self.evo_gpartial = torch.zeros(
-            ops.gemm_splits(T * H, self.prec, self.evo_gsplit) * Fmax * Fmax, **f32)
+            ops.gemm_splits(T * H, self.prec, self.evo_gsplit) * 3 * Fmax * Fmax, **f32)
+        # dS_r, dS_z, dP_c share the operand w: one M = 3 F_l GEMM when their
+        # gradients are adjacent in the flat buffer (param_shapes order Sr Sz Pc Qc)
+        self.evo_stack3 = all(
+            self.offs[f"Sz{l}"][0] == self.offs[f"Sr{l}"][0] + Fl * Fl
+            and self.offs[f"Pc{l}"][0] == self.offs[f"Sz{l}"][0] + Fl * Fl
+            for l, Fl in ((1, cfg.F), (2, H)))
 
     def p(self, name):
         o, shape = self.offs[name]
@@ -553,8 +560,16 @@ class Shard:
                                self.g(f"W{l}_0"), e["da"],
                                (self.g(f"Br{l}"), self.g(f"Bz{l}"), self.g(f"Bc{l}")),
                                rnd=self.tf32)
-                for k, da, op in (("Sr", e["da"][0], e["sv"][3]), ("Sz", e["da"][1], e["sv"][3]),
-                                  ("Pc", e["da"][2], e["sv"][3]), ("Qc", e["da"][2], e["sv"][4])):
+                if self.evo_stack3:  # [dS_r; dS_z; dP_c] = [da_r; da_z; da_c] w^T
+                    gS = self.grads[self.offs[f"Sr{l}"][0]:self.offs[f"Sr{l}"][0] + 3 * Fl * Fl]
+                    ops.gemm(e["da_all"], e["sv"][3], gS.view(3 * Fl, Fl), 3 * Fl, Fl, TH,
+                             b_mn=False, ldb=TH, precision=prec, k_splits=self.evo_gsplit,
+                             partial=self.evo_gpartial)
+                    pairs = (("Qc", e["da"][2], e["sv"][4]),)
+                else:
+                    pairs = (("Sr", e["da"][0], e["sv"][3]), ("Sz", e["da"][1], e["sv"][3]),
+                             ("Pc", e["da"][2], e["sv"][3]), ("Qc", e["da"][2], e["sv"][4]))
+                for k, da, op in pairs:
                     ops.gemm(da, op, self.g(f"{k}{l}"), Fl, Fl, TH, b_mn=False, ldb=TH,
                              precision=prec, k_splits=self.evo_gsplit, partial=self.evo_gpartial)
         # ---------------- gradient all-reduce + update ----------------
