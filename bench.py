@@ -356,8 +356,11 @@ def run_ours(args):
                    "parallelism": f"chunk-sharded x{world}" if distributed else
                    ("replicas" if world > 1 else "1 GPU")},
         "e2e": {"value": edges_total / (e2e_step / 1e3), "unit": UNIT,
-                "h2d_bytes_per_step": int(sum(x.numel() * 4 + t.numel() * 4 for x, t in zip(xs, ys))),
-                "pipeline": "inputs double-buffered: step i+1's H2D overlaps step i on a copy stream",
+                "h2d_bytes_per_step": int(sum(x.numel() * x.element_size() + t.numel() * t.element_size()
+                                              for x, t in zip(xs, ys))),
+                "pipeline": ("inputs double-buffered: step i+1's H2D overlaps step i on a copy stream; "
+                             "TF32 mode ships the TF32-rounded features as their 3 significant bytes "
+                             "(bit-identical to on-device rounding)"),
                 "d2h_bytes_per_step": 8, "ms_per_step": e2e_step},
         "roofline": {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": hbm,
                      "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,

@@ -302,6 +302,11 @@ int dgc_softmax_xent(const float* logits, const int32_t* labels, int64_t n, int3
 int dgc_reduce_rows(const float* partial, int64_t rows, int32_t width, float* out,
                     int32_t accumulate, void* stream);
 /* out[i] = in[i] rounded to the nearest TF32 (weights / inputs of TF32 mode) */
+/* TF32 input pipeline: n values (n % 4 == 0) shipped as 3 bytes each (the top
+ * three bytes of the fp32 after round-to-nearest-away to TF32, whose low byte is
+ * zero) -> fp32; bit-identical to dgc_round_tf32 of the original values.
+ * in: 4-byte aligned, out: 16-byte aligned. */
+int dgc_unpack_tf32x24(const uint8_t* in, float* out, int64_t n, void* stream);
 int dgc_round_tf32(const float* in, float* out, int64_t n, void* stream);
 /* Deterministic column sums out[j] (+)= sum_i X[i, j] (bias gradients);
  * scratch >= 296*width floats (<= 2 row blocks per SM). */

@@ -226,6 +226,24 @@ __global__ void round_tf32_kernel(const float* __restrict__ in, float* __restric
     out[i] = dgc::rna_tf32_f(in[i]);
 }
 
+// TF32 features shipped as 3 bytes per value (the host rounds to TF32 with the
+// same round-to-nearest-away as cvt.rna.tf32, whose low 13 mantissa bits -- the
+// whole low byte -- are zero): out = the 24-bit value << 8. Thread = 4 values
+// (three 32-bit words in, one float4 out).
+__global__ void unpack_tf32x24_kernel(const uint32_t* __restrict__ in, float4* __restrict__ out,
+                                      int64_t n4) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t w0 = __ldg(in + 3 * i), w1 = __ldg(in + 3 * i + 1), w2 = __ldg(in + 3 * i + 2);
+    float4 o;
+    o.x = __uint_as_float((w0 & 0x00ffffffu) << 8);
+    o.y = __uint_as_float(((w0 >> 24) | ((w1 & 0xffffu) << 8)) << 8);
+    o.z = __uint_as_float(((w1 >> 16) | ((w2 & 0xffu) << 16)) << 8);
+    o.w = __uint_as_float(w2 & 0xffffff00u);
+    out[i] = o;
+  }
+}
+
 __global__ void sgd_kernel(float* __restrict__ p, const float* __restrict__ g,
                            float* __restrict__ mom, int64_t n, float lr, float mu) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -349,6 +367,17 @@ extern "C" int dgc_relu_bwd(const float* dH, const float* H, float* dZ, int64_t 
       reinterpret_cast<const float4*>(dH), reinterpret_cast<const float4*>(H),
       reinterpret_cast<float4*>(dZ), n / 4);
   DGC_CHECK_LAUNCH("relu_bwd_kernel");
+  return DGC_OK;
+}
+
+extern "C" int dgc_unpack_tf32x24(const uint8_t* in, float* out, int64_t n, void* stream) {
+  DGC_REQUIRE(n % 4 == 0, "unpack_tf32x24: n must be a multiple of 4");
+  DGC_REQUIRE((reinterpret_cast<uintptr_t>(in) & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0,
+              "unpack_tf32x24: misaligned buffers");
+  if (n == 0) return DGC_OK;
+  unpack_tf32x24_kernel<<<dgc::grid_for(n / 4, 256), 256, 0, dgc::as_stream(stream)>>>(
+      reinterpret_cast<const uint32_t*>(in), reinterpret_cast<float4*>(out), n / 4);
+  DGC_CHECK_LAUNCH("unpack_tf32x24_kernel");
   return DGC_OK;
 }
 

@@ -7,6 +7,7 @@ fallback path.
 """
 from __future__ import annotations
 
+import numpy as np
 import torch
 
 from . import _native
@@ -342,6 +343,25 @@ def softmax_xent(logits, labels, C, scale, dlogits, loss_partial, round_tf32=Fal
     _run("softmax_xent", lambda: _native.check(_native.lib().dgc_softmax_xent(
         _p(logits), _p(labels), n, C, float(scale), int(round_tf32), _p(dlogits),
         _p(loss_partial), _p(dl_partial), _stream()), "dgc_softmax_xent"), n * (8 * C + 4))
+
+
+def pack_tf32x24(x: np.ndarray) -> np.ndarray:
+    """Host side of the TF32 input pipeline: round fp32 values to TF32 (round to
+    nearest, ties away: cvt.rna.tf32) and keep the top three bytes of each
+    (the low byte is zero) -> uint8 [3 * x.size]."""
+    u = np.ascontiguousarray(x, dtype=np.float32).reshape(-1).view(np.uint32)
+    finite = (u & np.uint32(0x7F800000)) != np.uint32(0x7F800000)
+    r = np.where(finite, (u + np.uint32(0x1000)) & np.uint32(0xFFFFE000), u).astype(np.uint32)
+    return np.ascontiguousarray(r.view(np.uint8).reshape(-1, 4)[:, 1:]).reshape(-1)
+
+
+def unpack_tf32x24(packed, out):
+    """dgc_unpack_tf32x24: out (fp32) from pack_tf32x24's 3-byte values."""
+    _req(out, torch.float32, "out")
+    n = out.numel()
+    _run("unpack_tf32x24", lambda: _native.check(_native.lib().dgc_unpack_tf32x24(
+        _p(packed), _p(out), n, _stream()), "dgc_unpack_tf32x24"), 7 * n)
+    return out
 
 
 def round_tf32(x, out):

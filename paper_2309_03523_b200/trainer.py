@@ -763,7 +763,13 @@ class DGNNTrainer:
         for sh in self.shards:
             real = sh.lay.own_gid >= 0
             gid = np.maximum(sh.lay.own_gid, 0)
-            xs.append(torch.as_tensor(np.where(real[:, None], features[gid], 0).astype(np.float32)).pin_memory())
+            x = np.where(real[:, None], features[gid], 0).astype(np.float32)
+            if sh.tf32 and x.size % 4 == 0:
+                # TF32 mode: the features are consumed TF32-rounded, so they ship as
+                # the 3 significant bytes of the rounded value (25% fewer PCIe bytes;
+                # bit-identical to the device-side rounding of the fp32 values)
+                x = ops.pack_tf32x24(x)
+            xs.append(torch.as_tensor(x).pin_memory())
             ys.append(torch.as_tensor(np.where(real, labels[gid], -1).astype(np.int32)).pin_memory())
         return xs, ys
 
@@ -775,8 +781,8 @@ class DGNNTrainer:
         pipeline: one 2-deep buffer per shard)."""
         if self._copy_stream is None:
             self._copy_stream = torch.cuda.Stream(self.device)
-            for sh in self.shards:
-                sh.X_stage = torch.empty_like(sh.X)
+            for sh, x in zip(self.shards, xs):
+                sh.X_stage = torch.empty(x.shape, dtype=x.dtype, device=self.device)
                 sh.y_stage = torch.empty_like(sh.y)
         with torch.cuda.stream(self._copy_stream):
             if self._stage_free_ev is not None:  # the previous staging was installed
@@ -791,7 +797,9 @@ class DGNNTrainer:
         cur = torch.cuda.current_stream(self.device)
         cur.wait_event(self._staged_ev)
         for sh in self.shards:
-            if sh.tf32:  # tensor-core operands are kept TF32-rounded
+            if sh.X_stage.dtype == torch.uint8:  # TF32 values shipped in 3 bytes
+                ops.unpack_tf32x24(sh.X_stage, sh.X)
+            elif sh.tf32:  # tensor-core operands are kept TF32-rounded
                 ops.round_tf32(sh.X_stage, sh.X)
             else:
                 sh.X.copy_(sh.X_stage)

@@ -419,3 +419,24 @@ def test_lstm_bwd_tensor_core_matches_simt(H, ew16, monkeypatch):
         outs.append((dgx.cpu().numpy(), bias.cpu().numpy()))
     close(outs[1][0], outs[0][0], 3e-3, "lstm bwd tc dgx")
     close(outs[1][1], outs[0][1], 3e-3, "lstm bwd tc bias")
+
+
+def test_tf32x24_input_pipeline_is_bit_exact():
+    """Host pack (round-to-nearest-away to TF32, keep 3 bytes) + device unpack
+    equals the device's cvt.rna.tf32 rounding of the fp32 values, bit for bit,
+    including ties, carries into the exponent, subnormals, zeros and infinities."""
+    from paper_2309_03523_b200 import ops
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal(1 << 16).astype(np.float32)
+    special = np.array([0.0, -0.0, 1.0, -1.0, np.inf, -np.inf, 1e-40, -1e-40, 3.4e38, -3.4e38],
+                       np.float32)
+    ties = (np.arange(1, 1 + 64, dtype=np.uint32) << 13 | 0x1000).view(np.float32)  # exact halves
+    near = (np.uint32(0x3FFFF000) + np.arange(64, dtype=np.uint32)).view(np.float32)  # carry into exp
+    x = np.concatenate([x, special, ties, -ties, near, np.zeros(2, np.float32)])
+    x = x[: len(x) // 4 * 4]
+    ref = torch.empty(len(x), device=dev)
+    ops.round_tf32(t(x), ref)
+    out = torch.empty(len(x), device=dev)
+    ops.unpack_tf32x24(torch.as_tensor(ops.pack_tf32x24(x)).to(dev), out)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.cpu().numpy().view(np.uint32))
