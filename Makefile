@@ -2,6 +2,10 @@
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O3
+# make DGC_TS=1: per-position LSTM timestamps for tools/time_lstm_*.py
+ifeq ($(DGC_TS),1)
+NVFLAGS += -DDGC_LSTM_TIMESTAMPS
+endif
 SRC := paper_2309_03523_b200/csrc
 OUT := paper_2309_03523_b200/lib
 CU := common spmm stale exchange dense rnn gemm_tc rnn_tc evolve

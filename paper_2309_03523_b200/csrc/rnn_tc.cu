@@ -43,9 +43,21 @@ __device__ __forceinline__ float rna_tf32(float x) {
   return __uint_as_float(r);
 }
 
-// Per-position timestamps of CTA 0 (ns, globaltimer) for profiling:
+// Per-position timestamps of CTA 0 (ns, globaltimer) for tools/time_lstm_*.py:
 // [p][0] MMA issue start, [p][1] accumulator ready, [p][2] epilogue done.
+// Compiled in only with -DDGC_LSTM_TIMESTAMPS (make DGC_TS=1): the production
+// kernels carry no probe.
 __device__ unsigned long long g_lstm_ts[256][3];
+#ifdef DGC_LSTM_TIMESTAMPS
+#define DGC_TS(cond, p, k) \
+  do {                     \
+    if (cond) g_lstm_ts[p][k] = globaltimer(); \
+  } while (0)
+#else
+#define DGC_TS(cond, p, k) \
+  do {                     \
+  } while (0)
+#endif
 
 template <int H>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -110,7 +122,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int p = 0; p < L; ++p) {
       mbar_wait(a_full, p & 1);
       fence_after();
-      if (blockIdx.x == 0 && lane == 0 && p < 256) g_lstm_ts[p][0] = globaltimer();
+      DGC_TS(blockIdx.x == 0 && lane == 0 && p < 256, p, 0);
       for (int u = 0; u < kUnitsPerStep; ++u) {
         const int g = p * kUnitsPerStep + u;
         const int s = g % kStages;
@@ -169,7 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int my_cnext = (has_next && my_ok) ? slot_carry[my_s + 1] : -1;
       mbar_wait(acc_full, p & 1);
       fence_after();
-      if (blockIdx.x == 0 && threadIdx.x == 64 && p < 256) g_lstm_ts[p][1] = globaltimer();
+      DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && p < 256, p, 1);
 #pragma unroll 1
       for (int j0 = u_lo; j0 < u_lo + kUnits; j0 += kChunk) {
         // TMEM (thread = row) -> smem [gate][row][unit]
@@ -232,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
       }
-      if (blockIdx.x == 0 && threadIdx.x == 64 && p < 256) g_lstm_ts[p][2] = globaltimer();
+      DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && p < 256, p, 2);
       if (has_next) {
         fence_before();
         fence_async_smem();
@@ -452,7 +464,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           fence_after();
           // generic-proxy writes (local st.shared, peer st.async) -> async proxy (MMA)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          if (i == 0 && blockIdx.x == 0 && lane == 0 && p < 256) g_lstm_ts[p][0] = globaltimer();
+          DGC_TS(i == 0 && blockIdx.x == 0 && lane == 0 && p < 256, p, 0);
         }
         const int s = g % kStages;
         mbar_wait(&b_full[s], (g / kStages) & 1);
@@ -547,7 +559,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
         xg[gi] = FX ? ldg4(bias + gi * H + u0 + uq * 4) : (inst >= 0 ? ldg4(gxr + gi * H) : zero4());
       mbar_wait(&acc_full[ab], acc_par);
       fence_after();
-      if (blockIdx.x == 0 && threadIdx.x == 64 && p < 256) g_lstm_ts[p][1] = globaltimer();
+      DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && p < 256, p, 1);
 #pragma unroll 1
       for (int ch = 0; ch < NCH; ++ch) {
         const int c0 = ch * 16;
@@ -625,7 +637,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
         for (int gi = 0; gi < 4; ++gi) xg[gi] = xn[gi];
         __syncwarp();
       }
-      if (blockIdx.x == 0 && threadIdx.x == 64 && p < 256) g_lstm_ts[p][2] = globaltimer();
+      DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && p < 256, p, 2);
       fence_before();
       if (FX) mbar_arrive(&acc_empty[ab]);  // this accumulator is drained
       if (has_next) publish(kHalves - 1);
@@ -1108,13 +1120,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           asm volatile("prefetch.global.L1 [%0];" ::"l"(dd + 32));
         }
       }
-      if (blockIdx.x == 0 && threadIdx.x == 64 && t < 256) g_lstm_ts[t][0] = globaltimer();
+      DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 0);
       const float* rv = recv + (t & 1) * kRecv;
       if (has_next) {
         if (ew == 0 && lane == 0) mbar_arrive_expect_tx(&recv_full[t & 1], kRecvBytes);
         mbar_wait(&acc_full[(p + 1) & 1], ((t - 1) >> 1) & 1);
         fence_after();
-        if (blockIdx.x == 0 && threadIdx.x == 64 && t < 256) g_lstm_ts[t][1] = globaltimer();
+        DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 1);
         if (active) {
           // partial dh of this warp's 8 rows: own units -> staging, the peer's
           // units -> the peer's receive tile (thread = row = TMEM lane)
@@ -1220,7 +1232,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           }
         }
         fence_async_smem();
-        if (lc == 1 && blockIdx.x == 0 && threadIdx.x == 64 && t < 256) g_lstm_ts[t][2] = globaltimer();
+        DGC_TS(lc == 1 && blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 2);
 #pragma unroll
         for (int g = 0; g < 4; ++g) mbar_arrive(&a_full[(seq0 + g) % kKsAStages]);
         __syncwarp();

@@ -1,4 +1,5 @@
 """Per-position timing of the fused-projection LSTM forward (C2 shape)."""
+# per-position timestamps need a build with them compiled in: make clean && make DGC_TS=1
 import ctypes
 import sys
 sys.path.insert(0, ".")

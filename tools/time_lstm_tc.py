@@ -1,4 +1,5 @@
 import sys, time
+# per-position timestamps need a build with them compiled in: make clean && make DGC_TS=1
 sys.path.insert(0, ".")
 import numpy as np, torch
 from paper_2309_03523_b200 import ops
