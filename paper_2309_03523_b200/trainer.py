@@ -722,12 +722,13 @@ class DGNNTrainer:
         # once (after one eager epoch) and replay it, so the step is not bound
         # by per-launch host latency
         self.cuda_graph = cuda_graph
-        self._graph = None
-        self._graph_infos = None
+        self._graphs = {}
+        self._loss_host = None
+        self._epoch_ev = None
+        self._alt_free_ev = None
         # double-buffered input staging (stage_inputs / run_epoch(next_inputs=...))
         self._copy_stream = None
         self._staged_ev = None
-        self._stage_free_ev = None
         self.stale = StaleConfig.coerce(stale_config)
         self.device = torch.device(device or "cuda")
         self.trace = EpochLossTrace()
@@ -775,37 +776,39 @@ class DGNNTrainer:
 
     def stage_inputs(self, xs, ys):
         """Start the host->device copy of the NEXT epoch's features / labels
-        (per-shard pinned host tensors, see host_inputs) into staging buffers
-        on a side stream; the next run_epoch() installs them first. The copy
-        overlaps whatever the compute stream is running (a prefetching input
-        pipeline: one 2-deep buffer per shard)."""
+        (per-shard pinned host tensors, see host_inputs) on a side stream and
+        expand them there (TF32 unpack / rounding) into each shard's second
+        input buffer; the next run_epoch() switches to that buffer (and to the
+        CUDA graph captured for it) after a stream wait. Copy and expansion
+        overlap whatever the compute stream is running: a prefetching input
+        pipeline, two input buffers per shard."""
         if self._copy_stream is None:
             self._copy_stream = torch.cuda.Stream(self.device)
             for sh, x in zip(self.shards, xs):
                 sh.X_stage = torch.empty(x.shape, dtype=x.dtype, device=self.device)
-                sh.y_stage = torch.empty_like(sh.y)
+                sh.X_alt = torch.empty_like(sh.X)
+                sh.y_alt = torch.empty_like(sh.y)
         with torch.cuda.stream(self._copy_stream):
-            if self._stage_free_ev is not None:  # the previous staging was installed
-                self._copy_stream.wait_event(self._stage_free_ev)
+            # the second buffers were last read by the epoch before the running one
+            if self._alt_free_ev is not None:
+                self._copy_stream.wait_event(self._alt_free_ev)
             for sh, x, y in zip(self.shards, xs, ys):
                 sh.X_stage.copy_(x, non_blocking=True)
-                sh.y_stage.copy_(y, non_blocking=True)
+                if sh.X_stage.dtype == torch.uint8:  # TF32 values shipped in 3 bytes
+                    ops.unpack_tf32x24(sh.X_stage, sh.X_alt)
+                elif sh.tf32:  # tensor-core operands are kept TF32-rounded
+                    ops.round_tf32(sh.X_stage, sh.X_alt)
+                else:
+                    sh.X_alt.copy_(sh.X_stage)
+                sh.y_alt.copy_(y, non_blocking=True)
             self._staged_ev = torch.cuda.Event()
             self._staged_ev.record(self._copy_stream)
 
     def _install_staged(self):
-        cur = torch.cuda.current_stream(self.device)
-        cur.wait_event(self._staged_ev)
+        torch.cuda.current_stream(self.device).wait_event(self._staged_ev)
         for sh in self.shards:
-            if sh.X_stage.dtype == torch.uint8:  # TF32 values shipped in 3 bytes
-                ops.unpack_tf32x24(sh.X_stage, sh.X)
-            elif sh.tf32:  # tensor-core operands are kept TF32-rounded
-                ops.round_tf32(sh.X_stage, sh.X)
-            else:
-                sh.X.copy_(sh.X_stage)
-            sh.y.copy_(sh.y_stage)
-        self._stage_free_ev = torch.cuda.Event()
-        self._stage_free_ev.record(cur)
+            sh.X, sh.X_alt = sh.X_alt, sh.X
+            sh.y, sh.y_alt = sh.y_alt, sh.y
         self._staged_ev = None
 
     def run_epoch(self, next_inputs=None):
@@ -814,7 +817,9 @@ class DGNNTrainer:
         next_inputs = (xs, ys) stages the following epoch's inputs so their
         copy overlaps this epoch."""
         r = self.epoch_no + 1
-        torch.cuda.synchronize(self.device)
+        # (no host synchronisation here: the previous epoch ended with one, and
+        # staged inputs are ordered by stream events, so the install and the
+        # epoch are enqueued while the device may still be draining earlier work)
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         if self._staged_ev is not None:
@@ -823,24 +828,34 @@ class DGNNTrainer:
         # exchanges) has no host synchronisation -> capturable
         graphable = (self.cuda_graph and self.stale.mode is StaleMode.OFF
                      and isinstance(self.runner, LocalRunner))
-        if graphable and r >= 2 and self._graph is None:
-            self._graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(self._graph):
-                self._graph_infos = self.runner.run([s.step(r, self.trace) for s in self.shards])
+        # one captured graph per input buffer set (the staged inputs alternate)
+        key = tuple(sh.X.data_ptr() for sh in self.shards)
+        if graphable and r >= 2 and key not in self._graphs:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                infos_g = self.runner.run([s.step(r, self.trace) for s in self.shards])
+            self._graphs[key] = (g, infos_g)
             torch.cuda.synchronize(self.device)
         t0.record()
-        if graphable and self._graph is not None:
-            self._graph.replay()
-            infos = self._graph_infos
+        if graphable and key in self._graphs:
+            g, infos = self._graphs[key]
+            g.replay()
         else:
             infos = self.runner.run([s.step(r, self.trace) for s in self.shards])
         t1.record()
+        if self._loss_host is None:
+            self._loss_host = torch.empty(1, dtype=infos[0]["loss_sum"].dtype, pin_memory=True)
+        self._loss_host.copy_(infos[0]["loss_sum"].reshape(1), non_blocking=True)
+        # this epoch's input buffers become the next staging target only after
+        # the epoch that follows it; the previous epoch's are free once it is done
+        self._alt_free_ev, self._epoch_ev = self._epoch_ev, torch.cuda.Event()
+        self._epoch_ev.record()
         if next_inputs is not None:
             self.stage_inputs(*next_inputs)
         torch.cuda.synchronize(self.device)
         ms = t0.elapsed_time(t1)
         self.epoch_no = r
-        loss = float(infos[0]["loss_sum"].item()) / self.pa.n_instances
+        loss = float(self._loss_host[0]) / self.pa.n_instances
         self.trace.append(loss)
         return self._report(r, ms, infos, loss)
 
