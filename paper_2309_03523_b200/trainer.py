@@ -859,14 +859,28 @@ class DGNNTrainer:
         self.trace.append(loss)
         return self._report(r, ms, infos, loss)
 
+    def _report_static(self):
+        """Plan-constant report fields (computed once)."""
+        if getattr(self, "_static_rep", None) is None:
+            cfg = self.cfg
+            per_msg = self.blocks * cfg.H * self.s_bytes
+            self._static_rep = dict(
+                per_msg=per_msg,
+                full_sp=2 * sum(int(l.key_ncut.sum()) for l in self.layouts) * per_msg,
+                full_tm=cfg.n_rnn * sum(len(l.tkey_rows) for l in self.layouts) * per_msg,
+                loading=sum(l.loaded_rows for l in self.layouts) * self.pa.feature_dim * self.s_bytes,
+                padding=sum(l.padding for l in self.layouts),
+                naive_padding=sum(l.naive_padding for l in self.layouts))
+        return self._static_rep
+
     def _report(self, r, ms, infos, loss):
         cfg = self.cfg
-        H, s = cfg.H, self.s_bytes
-        per_msg = self.blocks * H * s  # one layer's share of a reference message
+        H = cfg.H
+        st = self._report_static()
+        per_msg = st["per_msg"]  # one layer's share of a reference message
         billed_sp = sum(i["billed_sp"] for i in infos) * per_msg
         billed_tm = sum(i["billed_tm"] for i in infos) * per_msg
-        full_sp = 2 * sum(int(l.key_ncut.sum()) for l in self.layouts) * per_msg
-        full_tm = cfg.n_rnn * sum(len(l.tkey_rows) for l in self.layouts) * per_msg
+        full_sp, full_tm = st["full_sp"], st["full_tm"]
         if len(self.shards) == 1 and self.pa.n_devices > 1:
             import torch.distributed as dist
             t = torch.tensor([billed_sp, billed_tm, full_sp, full_tm], dtype=torch.float64,
@@ -878,14 +892,13 @@ class DGNNTrainer:
         avoided = full - sent
         theta = infos[0]["theta"].get("s0", 0.0)
         d_r = infos[0]["d_r"].get("s0", 0.0)
-        loading = sum(l.loaded_rows for l in self.layouts) * self.pa.feature_dim * s
+        loading = st["loading"]
         walls = [ms] * len(self.shards)
         return EpochReport(
             method=self.method, epoch=r, per_device_compute_ms=walls, per_device_wall_ms=walls,
             spatial_traffic_bytes=billed_sp, temporal_traffic_bytes=billed_tm, shuffle_bytes=0,
             loading_bytes=loading if r == 1 else 0,
-            padding_slots=sum(l.padding for l in self.layouts),
-            naive_padding_slots=sum(l.naive_padding for l in self.layouts),
+            padding_slots=st["padding"], naive_padding_slots=st["naive_padding"],
             load_divergence=1.0, wall_ms=ms, stale_theta=theta, stale_d=d_r,
             stale_sent_bytes=sent if self.stale.mode is not StaleMode.OFF else 0,
             stale_avoided_bytes=avoided if self.stale.mode is not StaleMode.OFF else 0,
