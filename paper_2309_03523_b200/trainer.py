@@ -36,6 +36,36 @@ from .stale import (EmbeddingCacheGPU, EpochLossTrace, StaleConfig, StaleMode, c
                     filter_transmissions_gpu, threshold)
 
 
+def k_segment_items(seg, T: int, fp32_chain: bool, n_sms: int = 148):
+    """Work items (first k-block, k-blocks) of the K-segmented per-snapshot
+    weight-gradient GEMM dW_t = X_t^T dY_t, seg = row offsets of the T snapshot
+    segments (multiples of 32). fp32 (3xTF32) mode caps every TMEM chain at 16
+    k-blocks; TF32 mode splits each snapshot's K evenly so the items form a
+    whole number of waves (2 x n_sms when T <= 2 n_sms), the parts per snapshot
+    by largest remainder. Returns (items, item_ptr) with item_ptr[t] the first
+    item of snapshot t."""
+    seg = np.asarray(seg, dtype=np.int64)
+    total_kb = max(1, int(seg[T] // 32))
+    kbs = [int(seg[t + 1] // 32 - seg[t] // 32) for t in range(T)]
+    target = 2 * n_sms if T <= 2 * n_sms else -(-T // n_sms) * n_sms
+    share = [k * target / total_kb for k in kbs]
+    parts = [max(1, int(x)) if k else 0 for x, k in zip(share, kbs)]
+    order = sorted(range(T), key=lambda t: -(share[t] - int(share[t])))
+    for t in order:
+        if sum(parts) >= target:
+            break
+        if kbs[t] > parts[t]:
+            parts[t] += 1
+    items, item_ptr = [], [0]
+    for t in range(T):
+        kb0, kb1 = int(seg[t] // 32), int(seg[t + 1] // 32)
+        chunk = 16 if fp32_chain else max(1, -(-(kb1 - kb0) // max(1, parts[t])))
+        for a in range(kb0, kb1, chunk):
+            items.append((a, min(chunk, kb1 - a)))
+        item_ptr.append(len(items))
+    return items, item_ptr
+
+
 @dataclass
 class EpochReport:
     """Fields of the reference EpochReport (sim.py:259-303), filled with
@@ -233,32 +263,7 @@ class Shard:
         for t in range(T):
             tile_seg[seg[t] // 128:seg[t + 1] // 128] = t
         self.seg_of_mtile = torch.as_tensor(tile_seg, device=dev)
-        # K-segmented work items for dW_t = X_t^T dY_t: chain <= 16 k-blocks in fp32 mode;
-        # in TF32 mode each snapshot's K is split evenly so the items fill two waves of
-        # the 148 SMs (one item per snapshot would leave 84 of them idle at T = 64)
-        total_kb = max(1, int(seg[T] // 32))
-        kbs = [int(seg[t + 1] // 32 - seg[t] // 32) for t in range(T)]
-        # TF32: a whole number of waves (2 x 148 items when T <= 296), split by
-        # largest remainder so every item has ~total/target k-blocks
-        target = 2 * 148 if T <= 296 else -(-T // 148) * 148
-        share = [k * target / total_kb for k in kbs]
-        parts = [max(1, int(x)) if k else 0 for x, k in zip(share, kbs)]
-        order = sorted(range(T), key=lambda t: -(share[t] - int(share[t])))
-        for t in order:
-            if sum(parts) >= target:
-                break
-            if kbs[t] > parts[t]:
-                parts[t] += 1
-        items, item_ptr = [], [0]
-        for t in range(T):
-            kb0, kb1 = seg[t] // 32, seg[t + 1] // 32
-            if self.prec == 3:
-                chunk = 16
-            else:
-                chunk = max(1, -(-(kb1 - kb0) // max(1, parts[t])))
-            for a in range(kb0, kb1, chunk):
-                items.append((a, min(chunk, kb1 - a)))
-            item_ptr.append(len(items))
+        items, item_ptr = k_segment_items(seg, T, self.prec == 3)
         self.kitems = torch.as_tensor(np.asarray(items, np.int32).reshape(-1), device=dev)
         self.n_kitems = len(items)
         self.item_ptr = torch.as_tensor(np.asarray(item_ptr, np.int32), device=dev)
