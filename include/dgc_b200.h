@@ -301,6 +301,11 @@ int dgc_softmax_xent(const float* logits, const int32_t* labels, int64_t n, int3
 /* out[j] (+)= sum_r partial[r, j] in fixed row order (deterministic). */
 int dgc_reduce_rows(const float* partial, int64_t rows, int32_t width, float* out,
                     int32_t accumulate, void* stream);
+/* n_jobs (<= 8) row reductions out_j[c] = sum_r partial_j[r, c] in two launches,
+ * bitwise equal to separate dgc_reduce_rows calls (host arrays of pointers /
+ * sizes; accumulate not supported). */
+int dgc_reduce_rows_batched(int32_t n_jobs, const float* const* partials, const int64_t* rows,
+                            const int32_t* widths, float* const* outs, void* stream);
 /* out[i] = in[i] rounded to the nearest TF32 (weights / inputs of TF32 mode) */
 /* TF32 input pipeline: n values (n % 4 == 0) shipped as 3 bytes each (the top
  * three bytes of the fp32 after round-to-nearest-away to TF32, whose low byte is

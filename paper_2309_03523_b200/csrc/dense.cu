@@ -333,6 +333,106 @@ __global__ void __launch_bounds__(256) reduce_rows_stage1(const float* __restric
   }
 }
 
+// Several row reductions in two launches (the bias gradients of one step):
+// stage 1 = reduce_rows_stage1 over every job's (32-column block, slab) pairs,
+// stage 2 = colsum_stage2 over every job's column blocks; same fixed order as
+// dgc_reduce_rows, so the results are bitwise those of separate calls.
+constexpr int kRRMaxJobs = 8;
+struct RRJobs {
+  const float* in[kRRMaxJobs];
+  float* out[kRRMaxJobs];
+  int64_t rows[kRRMaxJobs];
+  int64_t slab[kRRMaxJobs];
+  int64_t scr[kRRMaxJobs];   // scratch offset (floats)
+  int width[kRRMaxJobs];
+  int nslab[kRRMaxJobs];
+  int blk1[kRRMaxJobs + 1];  // stage-1 block prefix
+  int blk2[kRRMaxJobs + 1];  // stage-2 block prefix
+  int n;
+};
+
+__global__ void __launch_bounds__(256) reduce_rows_batched_stage1(RRJobs J, float* __restrict__ scratch) {
+  __shared__ float red[8][33];
+  int j = 0;
+  while (j + 1 < J.n && (int)blockIdx.x >= J.blk1[j + 1]) ++j;
+  const int local = blockIdx.x - J.blk1[j];
+  const int ncb = (J.width[j] + 31) / 32;
+  const int cb = local % ncb, sl = local / ncb;
+  const int width = J.width[j];
+  const int c = cb * 32 + threadIdx.x;
+  const int64_t r0 = (int64_t)sl * J.slab[j], r1 = min(r0 + J.slab[j], J.rows[j]);
+  float acc = 0.f;
+  if (c < width)
+    for (int64_t r = r0 + threadIdx.y; r < r1; r += 8) acc += J.in[j][r * width + c];
+  red[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < width) {
+    float s = 0.f;
+    for (int g = 0; g < 8; ++g) s += red[g][threadIdx.x];
+    scratch[J.scr[j] + (int64_t)sl * width + c] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) reduce_rows_batched_stage2(RRJobs J, const float* __restrict__ scratch) {
+  __shared__ float red[8][33];
+  int j = 0;
+  while (j + 1 < J.n && (int)blockIdx.x >= J.blk2[j + 1]) ++j;
+  const int width = J.width[j];
+  const int c = (blockIdx.x - J.blk2[j]) * 32 + threadIdx.x;
+  float acc = 0.f;
+  if (c < width)
+    for (int b = threadIdx.y; b < J.nslab[j]; b += 8) acc += scratch[J.scr[j] + (int64_t)b * width + c];
+  red[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < width) {
+    float s = 0.f;
+    for (int g = 0; g < 8; ++g) s += red[g][threadIdx.x];
+    J.out[j][c] = s;
+  }
+}
+
+extern "C" int dgc_reduce_rows_batched(int32_t n_jobs, const float* const* partials,
+                                       const int64_t* rows, const int32_t* widths,
+                                       float* const* outs, void* stream) {
+  DGC_REQUIRE(n_jobs >= 1 && n_jobs <= kRRMaxJobs, "reduce_rows_batched: 1..8 jobs");
+  RRJobs J{};
+  J.n = n_jobs;
+  int64_t scr = 0;
+  J.blk1[0] = J.blk2[0] = 0;
+  for (int j = 0; j < n_jobs; ++j) {
+    DGC_REQUIRE(widths[j] >= 1 && rows[j] >= 1, "reduce_rows_batched: empty job");
+    J.in[j] = partials[j];
+    J.out[j] = outs[j];
+    J.rows[j] = rows[j];
+    J.width[j] = widths[j];
+    int64_t slabs = rows[j] < 256 ? rows[j] : 256;  // as dgc_reduce_rows
+    const int64_t slab = (rows[j] + slabs - 1) / slabs;
+    slabs = (rows[j] + slab - 1) / slab;
+    J.slab[j] = slab;
+    J.nslab[j] = (int)slabs;
+    J.scr[j] = scr;
+    scr += slabs * widths[j];
+    const int ncb = (widths[j] + 31) / 32;
+    J.blk1[j + 1] = J.blk1[j] + ncb * (int)slabs;
+    J.blk2[j + 1] = J.blk2[j] + ncb;
+  }
+  // fixed-size scratch, allocated once and never freed: captured CUDA graphs
+  // keep pointing at it (<= 8 jobs x 256 slabs x 4096 columns)
+  constexpr int64_t kScratch = (int64_t)kRRMaxJobs * 256 * 4096;
+  DGC_REQUIRE(scr <= kScratch, "reduce_rows_batched: jobs too wide");
+  static float* scratch = nullptr;
+  if (!scratch) {
+    cudaError_t e = cudaMalloc(&scratch, kScratch * sizeof(float));
+    if (e != cudaSuccess) return dgc::cuda_fail(e, "reduce_rows_batched scratch");
+  }
+  cudaStream_t s = dgc::as_stream(stream);
+  reduce_rows_batched_stage1<<<J.blk1[n_jobs], dim3(32, 8), 0, s>>>(J, scratch);
+  DGC_CHECK_LAUNCH("reduce_rows_batched_stage1");
+  reduce_rows_batched_stage2<<<J.blk2[n_jobs], dim3(32, 8), 0, s>>>(J, scratch);
+  DGC_CHECK_LAUNCH("reduce_rows_batched_stage2");
+  return DGC_OK;
+}
+
 extern "C" int dgc_reduce_rows(const float* partial, int64_t rows, int32_t width, float* out,
                                int32_t accumulate, void* stream) {
   if (width == 0) return DGC_OK;

@@ -277,6 +277,21 @@ def reduce_rows(partial, rows, width, out, accumulate=False):
     return out
 
 
+def reduce_rows_batched(jobs):
+    """dgc_reduce_rows_batched: jobs = [(partial, rows, width, out), ...] (<= 8),
+    bitwise the same as reduce_rows per job, in two launches."""
+    import ctypes
+    n = len(jobs)
+    P = (ctypes.c_void_p * n)(*[p.data_ptr() for p, _, _, _ in jobs])
+    R = (ctypes.c_int64 * n)(*[int(r) for _, r, _, _ in jobs])
+    W = (ctypes.c_int32 * n)(*[int(w) for _, _, w, _ in jobs])
+    O = (ctypes.c_void_p * n)(*[o.data_ptr() for _, _, _, o in jobs])
+    _run("reduce_rows", lambda: _native.check(_native.lib().dgc_reduce_rows_batched(
+        n, ctypes.addressof(P), ctypes.addressof(R), ctypes.addressof(W), ctypes.addressof(O),
+        _stream()), "dgc_reduce_rows_batched"),
+        sum(4 * r * w for _, r, w, _ in jobs), 0, 2)
+
+
 def rnn_bwd(cell, Ut, slot_row, slot_mask, n_rows, row_len, H, save, dh_out, dgx,
             bias_partial=None):
     """K3/K4 dgc_rnn_bwd (BPTT over packed runs)."""

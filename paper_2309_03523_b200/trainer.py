@@ -231,7 +231,10 @@ class Shard:
         self.rnn_prows = ops.rnn_bwd_partial_rows(self.R, H) if self.R else 1
         self.dl_partial = torch.zeros(max(1, (n + 255) // 256) * cfg.C, **f32)
         prows = max(self.rnn_prows, ops.rnn_tc_tiles(max(self.R, 1), H))
-        self.bias_partial = torch.zeros(max(prows * GH, 4 * self.m_tiles * H), **f32)
+        # one partial buffer per bias gradient: their fixed-order reductions run
+        # together at the end of the backward (dgc_reduce_rows_batched, 2 launches)
+        self.bp_b = [torch.zeros(4 * self.m_tiles * H, **f32) for _ in range(2)]      # b1, b2
+        self.bp_r = [torch.zeros(prows * GH, **f32) for _ in range(max(cfg.n_rnn, 1))]  # br_k
         # split-K for weight gradients: ~one wave of 148 SMs
         kb = max(1, (n + 31) // 32)
         self.ksplit = max(1, min(148, kb // 4))
@@ -472,11 +475,11 @@ class Shard:
         ks, part = self.ksplit, self.partial
         ops.gemm(xr, self.dlogits, self.g("Wo"), H, cfg.C, n, a_mn=True, lda=ldx, precision=prec,
                  k_splits=ks, partial=part)
-        ops.reduce_rows(self.dl_partial, max(1, (n + 255) // 256), cfg.C, self.g("bo"))
+        rjobs = [(self.dl_partial, max(1, (n + 255) // 256), cfg.C, self.g("bo"))]
         if self.evolve:  # no time encoder: dZ2 = (dlogits Wo^T) * (H2 > 0), b2 fused
             ops.gemm(self.dlogits, self.pr("Wo"), self.dh, n, H, cfg.C, b_mn=False, ldb=cfg.C,
-                     precision=prec, relu_src=self.Hl[1], colsum_partial=self.bias_partial)
-            ops.reduce_rows(self.bias_partial, 4 * self.m_tiles, H, self.g("b2"))
+                     precision=prec, relu_src=self.Hl[1], colsum_partial=self.bp_b[1])
+            rjobs.append((self.bp_b[1], 4 * self.m_tiles, H, self.g("b2")))
         else:
             ops.gemm(self.dlogits, self.pr("Wo"), self.dh, n, H, cfg.C, b_mn=False, ldb=cfg.C,
                      precision=prec)
@@ -484,13 +487,13 @@ class Shard:
             if self.tc_rnn:
                 ops.rnn_bwd_tc(cell | rflag, self.pr(f"U{k}"), self.slot_row, self.slot_mask,
                                self.R, self.L, H, self.save[k], self.dh, self.dgx,
-                               self.rnn_dc_scratch, bias_partial=self.bias_partial)
-                ops.reduce_rows(self.bias_partial, self.rnn_tc_prows, GH, self.g(f"br{k}"))
+                               self.rnn_dc_scratch, bias_partial=self.bp_r[k])
+                rjobs.append((self.bp_r[k], self.rnn_tc_prows, GH, self.g(f"br{k}")))
             else:
                 ops.transpose(self.pr(f"U{k}"), self.Ut)
                 ops.rnn_bwd(cell | rflag, self.Ut, self.slot_row, self.slot_mask, self.R, self.L,
-                            H, self.save[k], self.dh, self.dgx, bias_partial=self.bias_partial)
-                ops.reduce_rows(self.bias_partial, self.rnn_prows, GH, self.g(f"br{k}"))
+                            H, self.save[k], self.dh, self.dgx, bias_partial=self.bp_r[k])
+                rjobs.append((self.bp_r[k], self.rnn_prows, GH, self.g(f"br{k}")))
             xin, ldxin = (self.Hl[1], H) if k == 0 else (self.hbuf[k - 1], self.hw)
             gU = self.g(f"U{k}")
             if cell == 1 and H % 128 == 0:
@@ -514,9 +517,9 @@ class Shard:
             relu_src = self.Hl[1] if k == 0 else None
             ops.gemm(self.dgx, self.pr(f"Wx{k}"), self.dh2, n, H, GH, b_mn=False, ldb=GH,
                      precision=prec, relu_src=relu_src,
-                     colsum_partial=self.bias_partial if k == 0 else None)
+                     colsum_partial=self.bp_b[1] if k == 0 else None)
             if k == 0:  # dZ2 = dH2 * (H2 > 0): its column sums are the b2 gradient
-                ops.reduce_rows(self.bias_partial, 4 * self.m_tiles, H, self.g("b2"))
+                rjobs.append((self.bp_b[1], 4 * self.m_tiles, H, self.g("b2")))
             self.dh, self.dh2 = self.dh2, self.dh
         dZ = self.dh  # = dH2 * (H2 > 0), fused into the last GEMM epilogue
         for l in (1, 0):
@@ -546,16 +549,16 @@ class Shard:
                     ops.gemm_segmented(self.dYext, e["Wstack"][kin_l:], self.dh2, n, H, H,
                                        b_mn=False, ldb=H, precision=prec, relu_src=self.Hl[0],
                                        seg_of_mtile=self.seg_of_mtile, b_nseg=cfg.T,
-                                       colsum_partial=self.bias_partial)
-                    ops.reduce_rows(self.bias_partial, 4 * self.m_tiles, H, self.g("b1"))
+                                       colsum_partial=self.bp_b[0])
+                    rjobs.append((self.bp_b[0], 4 * self.m_tiles, H, self.g("b1")))
                     dZ = self.dh2
                 continue
             ops.gemm(hin_l, self.dYext, self.g(W), kin_l, H, n, a_mn=True, lda=ldin_l, ldb=H,
                      precision=prec, k_splits=ks, partial=part)
             if l == 1:
                 ops.gemm(self.dYext, self.pr("W2"), self.dh2, n, H, H, b_mn=False, ldb=H,
-                         precision=prec, relu_src=self.Hl[0], colsum_partial=self.bias_partial)
-                ops.reduce_rows(self.bias_partial, 4 * self.m_tiles, H, self.g("b1"))
+                         precision=prec, relu_src=self.Hl[0], colsum_partial=self.bp_b[0])
+                rjobs.append((self.bp_b[0], 4 * self.m_tiles, H, self.g("b1")))
                 dZ = self.dh2
         if self.evolve:  # BPTT through the weight evolution, gate-matrix grads by K2
             for l, e in enumerate(self.evo, start=1):
@@ -577,6 +580,8 @@ class Shard:
                 for k, da, op in pairs:
                     ops.gemm(da, op, self.g(f"{k}{l}"), Fl, Fl, TH, b_mn=False, ldb=TH,
                              precision=prec, k_splits=self.evo_gsplit, partial=self.evo_gpartial)
+        for j0 in range(0, len(rjobs), 8):  # bias gradients, fixed order, 2 launches
+            ops.reduce_rows_batched(rjobs[j0:j0 + 8])
         # ---------------- gradient all-reduce + update ----------------
         if D > 1:
             yield ("sum", self.grads)

@@ -440,3 +440,19 @@ def test_tf32x24_input_pipeline_is_bit_exact():
     ops.unpack_tf32x24(torch.as_tensor(ops.pack_tf32x24(x)).to(dev), out)
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.cpu().numpy().view(np.uint32))
+
+
+def test_reduce_rows_batched_equals_separate_calls():
+    """The batched bias-gradient reduction is bitwise the per-job dgc_reduce_rows."""
+    from paper_2309_03523_b200 import ops
+    rng = np.random.default_rng(11)
+    shapes = [(782, 16), (6252, 128), (144, 512), (1, 64), (300, 33)]
+    ins = [t(rng.standard_normal((r, w)).astype(np.float32)) for r, w in shapes]
+    sep = [torch.zeros(w, device=dev) for _, w in shapes]
+    bat = [torch.zeros(w, device=dev) for _, w in shapes]
+    for x, (r, w), o in zip(ins, shapes, sep):
+        ops.reduce_rows(x, r, w, o)
+    ops.reduce_rows_batched([(x, r, w, o) for x, (r, w), o in zip(ins, shapes, bat)])
+    torch.cuda.synchronize()
+    for a, b in zip(sep, bat):
+        assert np.array_equal(a.cpu().numpy(), b.cpu().numpy())
