@@ -628,6 +628,8 @@ class LocalRunner:
             m = torch.stack([r[1].reshape(-1)[0] for r in reqs]).max().reshape(1)
             return [m.clone() for _ in reqs]
         if kind == "sum":
+            if D == 1:  # nothing to combine
+                return [reqs[0][1]]
             acc = reqs[0][1].clone()
             for r in reqs[1:]:
                 acc += r[1]
