@@ -37,3 +37,11 @@ build/fusion_plan.o: $(SRC)/fusion_plan.cpp include/dgc_b200.h
 build/propagate.o: $(SRC)/propagate.cpp include/dgc_b200.h
 	@mkdir -p build
 	g++ -O3 -std=c++17 -fPIC -c $< -o $@
+
+# microbenchmark probes (built on demand, never committed)
+probes: tools/probes/gather4
+
+tools/probes/gather4: tools/probes/gather4.cu
+	$(NVCC) $(ARCH) -O3 -std=c++17 -o $@ $<
+
+.PHONY: probes

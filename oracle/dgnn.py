@@ -153,6 +153,7 @@ class OracleDGNN:
         self.vel = {k: np.zeros_like(v) for k, v in self.p.items()}
         self.step_count = 0
         self.tie_log: list[dict] = []
+        self.relu_log: list[dict] = []
 
     # -- staleness (stale.py) ------------------------------------------------
     def _decide(self, r, values, cache, cached, forced=None, tag=""):
@@ -193,10 +194,17 @@ class OracleDGNN:
         return sends, theta, d_r
 
     # -- forward/backward of one epoch ---------------------------------------
-    def epoch(self, r, forced=None):
+    def epoch(self, r, forced=None, forced_relu=None):
         """One epoch; ``forced`` = {cache tag: per-device send masks} replays
-        externally made stale decisions (see _decide)."""
+        externally made stale decisions (see _decide). ``forced_relu`` =
+        {GCN layer 0/1: per-device bool (n_own, H) masks} replays another
+        implementation's ReLU decisions the same way: the oracle's own
+        pre-activation z is still computed, and every element where
+        (z > 0) differs from the forced mask is logged in self.relu_log with
+        z and the layer's max|z| (tests assert they are near-ties, i.e. the
+        discontinuity of relu' at 0 sits inside the other side's rounding)."""
         forced = forced or {}
+        forced_relu = forced_relu or {}
         cfg, D, G, H = self.cfg, self.D, self.G, self.cfg.H
         out = {"send": {}, "theta": {}, "d_r": {}}
         hin = self.X
@@ -239,11 +247,23 @@ class OracleDGNN:
             out["send"][f"s{l}"] = sends
             out["theta"][f"s{l}"] = theta
             out["d_r"][f"s{l}"] = d_r
-            Hl = []
+            Hl, masks = [], []
             for d in range(D):
                 Yext = np.concatenate([Y[d], self.halo[l][d]])
-                Hl.append(np.maximum(self.A[d] @ Yext + self.p[b], 0.0))
-            acts.append((hin, Hl))
+                z = self.A[d] @ Yext + self.p[b]
+                m = z > 0
+                if l in forced_relu:
+                    f = np.asarray(forced_relu[l][d], bool)
+                    diff = np.flatnonzero((f != m).reshape(-1))
+                    if len(diff):
+                        zs = float(np.abs(z).max())
+                        for i in diff:
+                            self.relu_log.append(dict(epoch=r, layer=l, device=d, index=int(i),
+                                                      z=float(z.reshape(-1)[i]), scale=zs))
+                    m = f
+                Hl.append(np.where(m, z, 0.0))
+                masks.append(m)
+            acts.append((hin, Hl, masks))
             fresh_all.append(fresh)
             hin = Hl
         # time encoder
@@ -320,11 +340,11 @@ class OracleDGNN:
             dh = dx
         for l in (1, 0):
             W, b = ("W1", "b1") if l == 0 else ("W2", "b2")
-            hin_l, hout_l = acts[l]
+            hin_l, hout_l, mask_l = acts[l]
             dY_own = []
             dY_halo = []
             for d in range(D):
-                dz = dh[d] * (hout_l[d] > 0)
+                dz = dh[d] * mask_l[d]
                 grads[b] += dz.sum(axis=0)
                 dYext = self.A[d].T @ dz
                 dY_own.append(dYext[:self.L[d].n_own].copy())

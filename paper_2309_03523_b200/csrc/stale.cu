@@ -18,27 +18,36 @@ __global__ void stale_distance_kernel(const float* __restrict__ Y, const int32_t
                                       const float* __restrict__ cache,
                                       const uint8_t* __restrict__ cached, int64_t n_keys, int width,
                                       float* __restrict__ dist, unsigned int* __restrict__ dmax) {
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int lane = (int)(tid % LPR);
-  const int64_t stride = ((int64_t)gridDim.x * blockDim.x) / LPR;
+  // 32/LPR keys per warp and iteration; the loop bound is warp-uniform (every
+  // lane of the warp runs every iteration, so the full-mask shuffles below are
+  // always converged), keys past n_keys contribute acc = 0 and store nothing
+  constexpr int KPW = 32 / LPR;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = (int)(threadIdx.x & 31) % LPR;
+  const int sub = (int)(threadIdx.x & 31) / LPR;
   const int w4 = width / 4;
   unsigned int local_max = 0u;
-  for (int64_t k = tid / LPR; k < n_keys; k += stride) {
-    const float4* y = reinterpret_cast<const float4*>(Y + (int64_t)__ldg(keys + k) * width);
-    const float4* c = reinterpret_cast<const float4*>(cache + k * width);
+  for (int64_t base = warp * KPW; base < n_keys; base += nwarps * KPW) {
+    const int64_t k = base + sub;
+    const bool valid = k < n_keys;
     float acc = 0.f;
-    for (int j = lane; j < w4; j += LPR) {
-      const float4 a = __ldg(y + j), b = __ldg(c + j);
-      const float dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z, dw = a.w - b.w;
-      acc = fmaf(dx, dx, acc);
-      acc = fmaf(dy, dy, acc);
-      acc = fmaf(dz, dz, acc);
-      acc = fmaf(dw, dw, acc);
+    if (valid) {
+      const float4* y = reinterpret_cast<const float4*>(Y + (int64_t)__ldg(keys + k) * width);
+      const float4* c = reinterpret_cast<const float4*>(cache + k * width);
+      for (int j = lane; j < w4; j += LPR) {
+        const float4 a = __ldg(y + j), b = __ldg(c + j);
+        const float dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z, dw = a.w - b.w;
+        acc = fmaf(dx, dx, acc);
+        acc = fmaf(dy, dy, acc);
+        acc = fmaf(dz, dz, acc);
+        acc = fmaf(dw, dw, acc);
+      }
     }
 #pragma unroll
     for (int off = LPR / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
     const float d = sqrtf(acc);
-    if (lane == 0) {
+    if (valid && lane == 0) {
       dist[k] = d;
       if (cached[k]) local_max = max(local_max, __float_as_uint(d));
     }

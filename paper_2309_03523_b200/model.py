@@ -46,6 +46,12 @@ class DGNNConfig:
     @classmethod
     def for_profile(cls, profile: dict, F: int, H: int | None = None, C: int = 16, **kw):
         """Model of a reference ModelProfile (costmodel.py:50-92)."""
+        if profile.get("temporal_fanout", "previous-only") != "previous-only":
+            # the all-snapshots (attention-style) fanout bills every ordered
+            # same-entity pair (costmodel.py:125-131); only the previous-only
+            # recurrences (GRU/LSTM, EvolveGCN) are modelled
+            raise ValueError("only the previous-only temporal fanout is modelled, got "
+                             f"{profile.get('temporal_fanout')!r}")
         if profile.get("spatial_msgs_per_block", 2) != 2 or profile.get("blocks", 1) != 1:
             raise ValueError("only the 1-block, 2-GCN-layer profiles of C1/C2 are modelled")
         n_rnn = int(profile.get("temporal_msgs_per_block", 1))

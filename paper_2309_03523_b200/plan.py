@@ -158,7 +158,17 @@ def from_reference_artifacts(directory) -> PlanArrays:
 
 
 def from_dynpart(g, plan) -> PlanArrays:
-    """Duck-typed adapter for a live reference DynamicGraph + Plan."""
+    """Duck-typed adapter for a live reference DynamicGraph + Plan.
+
+    The B200 step runs the time encoder on the structure device (the chunk
+    plans of the reference, ``Plan.time_device is None``, sim.py:119-121); a
+    pss-ts plan, whose time phase moves instances to other devices
+    (sim.py:243-252), is rejected instead of being silently re-homed."""
+    tdev = getattr(plan, "time_device", None)
+    if tdev is not None and not np.array_equal(np.asarray(tdev), np.asarray(plan.structure_device)):
+        raise ValueError(f"plan method {getattr(plan, 'method', '?')!r} has a separate time-phase "
+                         "device map (pss-ts); the B200 step runs the time encoder on the "
+                         "structure device")
     inst = np.asarray(g.instances, dtype=np.int64).reshape(-1, 2)
     chunk_of = np.empty(g.n_instances, np.int64)
     for c in plan.chunk_graph.chunks:
@@ -179,7 +189,8 @@ def from_dynpart(g, plan) -> PlanArrays:
                     temporal_links=_i32(g.temporal_link_index()),
                     structure_device=_i32(plan.structure_device), chunk_of=_i32(chunk_of),
                     n_devices=int(plan.n_devices), group_device=gd, group_ptr=gp,
-                    group_chunks=gc, profile=prof)
+                    group_chunks=gc, profile=prof,
+                    meta={"method": str(getattr(plan, "method", "pgc"))})
     pa.validate()
     return pa
 

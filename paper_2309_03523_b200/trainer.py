@@ -927,6 +927,21 @@ class DGNNTrainer:
         sh = self.shards[shard]
         return {k: sh.g(k).detach().cpu().numpy().copy() for k in sh.offs}
 
+    def optimizer_state(self, shard: int = 0):
+        """(first moments, second moments, step count) per parameter name."""
+        sh = self.shards[shard]
+
+        def view(buf, k):
+            o, shape = sh.offs[k]
+            return buf[o:o + int(np.prod(shape))].view(*shape).detach().cpu().numpy().copy()
+        return ({k: view(sh.m, k) for k in sh.offs}, {k: view(sh.v, k) for k in sh.offs},
+                int(sh.step_dev.item()) if self.cfg.optimizer == "adam" else sh.step_count)
+
+    def relu_masks(self, shard: int = 0):
+        """{GCN layer: bool (n_own, H)} -- this epoch's ReLU decisions (H_l > 0)."""
+        sh = self.shards[shard]
+        return {l: (sh.Hl[l] > 0).cpu().numpy() for l in range(2)}
+
 
 def run_epochs(g, plan=None, profile=None, cluster=None, epochs: int = 1, stale_config=None,
                drift_spec=None, seed: int = 0, coeffs=None, initial_loss=None, loss_decay=None,

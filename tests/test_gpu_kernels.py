@@ -213,6 +213,33 @@ def test_stale_filter_matches_reference_golden(golden_dir):
             trace.append(2.0 * 0.9 ** (r - 1))
 
 
+@pytest.mark.parametrize("width,n_keys", [(64, 1001), (32, 4099), (16, 7), (128, 333),
+                                          (256, 5), (12, 1003)])
+def test_stale_distance_all_widths(width, n_keys):
+    """K5 distance at every sub-warp width (LPR 1/8/32), including the LPR = 8
+    path (widths 32-124: four keys per warp) with n_keys not a multiple of 4,
+    against numpy fp64: distances, D_r = max over cached keys, and the send
+    decision (the tail warp used to shuffle unconverged)."""
+    from paper_2309_03523_b200 import stale as st
+    rng = np.random.default_rng(width + n_keys)
+    n_rows = n_keys + 50
+    Y = rng.standard_normal((n_rows, width)).astype(np.float32)
+    keys = rng.permutation(n_rows)[:n_keys].astype(np.int32)
+    cache = st.EmbeddingCacheGPU(n_keys, width, dev)
+    cv = (Y[keys] + 0.1 * rng.standard_normal((n_keys, width))).astype(np.float32)
+    cached = (rng.random(n_keys) < 0.8).astype(np.uint8)
+    cache.values.copy_(t(cv))
+    cache.cached.copy_(t(cached, torch.uint8))
+    dmax = float(st.cache_gap_gpu(t(Y), t(keys, torch.int32), cache).item())
+    ref = np.sqrt(((Y[keys].astype(np.float64) - cv) ** 2).sum(axis=1))
+    np.testing.assert_allclose(cache.dist.cpu().numpy(), ref, rtol=1e-5)
+    assert dmax == pytest.approx(ref[cached.astype(bool)].max(), rel=1e-5)
+    theta = float(np.median(ref))
+    s = st.filter_transmissions_gpu(t(Y), t(keys, torch.int32), cache, theta).cpu().numpy()
+    exp = (~cached.astype(bool)) | (cache.dist.cpu().numpy() > theta)
+    np.testing.assert_array_equal(s.astype(bool), exp)
+
+
 def test_exchange_pack_unpack():
     from paper_2309_03523_b200 import ops
     rng = np.random.default_rng(9)

@@ -41,12 +41,41 @@ def run_pair(pa, cfg_kw, stale_mode="off", epochs=3, fraction=0.5, seed=0, preci
                       for l in range(2)}
             forced.update({f"t{k}": [sh.tcache[k].send.cpu().numpy().astype(bool)
                                      for sh in tr.shards] for k in range(cfg.n_rnn)})
-        o = orc.epoch(r, forced)
+        # replay the GPU's ReLU decisions too (near-ties logged in orc.relu_log,
+        # checked against the precision's tie band by check_epochs)
+        o = orc.epoch(r, forced, forced_relu=oracle_relu_masks(tr, lays))
         out.append((rep, o, tr.grads(0)))
+    orc.precision = precision
     return out, tr, orc
 
 
-def check_epochs(out, rtol=1e-4):
+def oracle_relu_masks(tr, lays):
+    """The GPU's ReLU decisions of this epoch in the oracle layouts' row order
+    (GPU layouts may carry snapshot padding rows: EvolveGCN segments)."""
+    out = {0: [], 1: []}
+    for i, lay in enumerate(lays):
+        gl = tr.layouts[i].own_gid
+        pos = np.full(max(int(gl.max()) + 1, 1), -1, np.int64)
+        pos[gl[gl >= 0]] = np.flatnonzero(gl >= 0)
+        rows = pos[np.asarray(lay.own_gid)]
+        assert (rows >= 0).all()
+        for l, m in tr.relu_masks(i).items():
+            out[l].append(m[rows])
+    return out
+
+
+# ReLU tie band (|z| / max|z| of the layer) per precision; see test_gpu_c2_parity.py
+RELU_BAND = {"fp32": 5e-7, "tf32": 2e-3}
+
+
+def check_relu_ties(orc):
+    for e in orc.relu_log:
+        assert abs(e["z"]) <= RELU_BAND[orc.precision] * e["scale"], e
+
+
+def check_epochs(out, rtol=1e-4, orc=None):
+    if orc is not None:
+        check_relu_ties(orc)
     for rep, o, grads in out:
         assert rep.loss == pytest.approx(o["loss"], rel=rtol)
         for k, g in grads.items():
@@ -63,15 +92,15 @@ def check_epochs(out, rtol=1e-4):
 def test_trainer_matches_oracle_stale_off(artifacts_dir, name, cfg_kw):
     from paper_2309_03523_b200 import load_plan_npz
     pa = load_plan_npz(artifacts_dir / name / "plan.npz")
-    out, _, _ = run_pair(pa, cfg_kw, "off", epochs=3)
-    check_epochs(out)
+    out, _, orc = run_pair(pa, cfg_kw, "off", epochs=3)
+    check_epochs(out, orc=orc)
 
 
 def test_trainer_single_device_wide(artifacts_dir):
     from paper_2309_03523_b200 import load_plan_npz, single_device
     pa = single_device(load_plan_npz(artifacts_dir / "t2" / "plan.npz"))
-    out, _, _ = run_pair(pa, dict(F=32, H=64, C=16, rnn="lstm", n_rnn=2), "off", epochs=2)
-    check_epochs(out)
+    out, _, orc = run_pair(pa, dict(F=32, H=64, C=16, rnn="lstm", n_rnn=2), "off", epochs=2)
+    check_epochs(out, orc=orc)
 
 
 @pytest.mark.parametrize("mode", ["relax", "tighten", "static"])
@@ -80,7 +109,7 @@ def test_trainer_stale_schedule_matches_oracle(artifacts_dir, mode):
     pa = load_plan_npz(artifacts_dir / "t2" / "plan.npz")
     out, tr, orc = run_pair(pa, dict(F=16, H=16, C=16, rnn="gru", n_rnn=1), mode, epochs=4,
                             fraction=0.3)
-    check_epochs(out, rtol=1e-4)
+    check_epochs(out, rtol=1e-4, orc=orc)
     for rep, o, _ in out:
         for key, th in o["theta"].items():
             if key in rep.stale_detail["theta"]:
@@ -98,57 +127,36 @@ def test_trainer_stale_schedule_matches_oracle(artifacts_dir, mode):
 @pytest.mark.parametrize("name,H", [("t4", 64), ("t2", 128), ("t2-single", 128)])
 def test_trainer_tf32_tensor_core_path(artifacts_dir, name, H):
     """TF32 perf mode (tcgen05 GEMMs + tensor-core LSTM recurrence, TF32-rounded
-    operands) against the fp64 oracle. Loss and the time-encoder/readout
-    gradients are held to the north star's 2e-2 class (max-normalised). The
-    structure-encoder gradients (W1, b1, W2, b2) are sums over all instances
-    with strong cancellation (|sum| ~ 2-5% of sum|terms| at initialisation),
-    which amplifies the ~5e-4 per-element TF32 error of their inputs; they are
-    held to 5e-2 in tensor norm (the fp32 mode meets 1e-4 on all of them)."""
+    operands) against the fp64 oracle: loss and EVERY gradient within the
+    north star's 2e-2 (max-normalised), with the GPU's ReLU decisions replayed
+    and every disagreement inside the TF32 tie band (test_gpu_c2_parity.py)."""
     from paper_2309_03523_b200 import load_plan_npz, single_device
     pa = load_plan_npz(artifacts_dir / name.split("-")[0] / "plan.npz")
     if name.endswith("-single"):  # one device: layer 1 runs aggregate-first
         pa = single_device(pa)
-    out, tr, _ = run_pair(pa, dict(F=32, H=H, C=16, rnn="lstm", n_rnn=2), "off", epochs=2,
-                          precision="tf32")
+    out, tr, orc = run_pair(pa, dict(F=32, H=H, C=16, rnn="lstm", n_rnn=2), "off", epochs=2,
+                            precision="tf32")
     assert tr.shards[0].tc_rnn
     assert tr.shards[0].agg_first == name.endswith("-single")
-    for rep, o, grads in out:
-        assert rep.loss == pytest.approx(o["loss"], rel=2e-2)
-        for k, g in grads.items():
-            ref = o["grads"][k]
-            if k in ("W1", "b1", "W2", "b2"):
-                err = np.linalg.norm(g - ref) / np.linalg.norm(ref)
-                assert err <= 5e-2, f"epoch {rep.epoch} grad {k}: rel-norm {err:.2e}"
-            else:
-                err = np.abs(g - ref).max() / np.abs(ref).max()
-                assert err <= 2e-2, f"epoch {rep.epoch} grad {k}: {err:.2e}"
+    check_epochs(out, rtol=2e-2, orc=orc)
 
 
 def test_trainer_aggregate_first_fp32(artifacts_dir, monkeypatch):
     """Layer 1 as relu((A X) W1 + b1) (the single-device TF32 default, forced
-    here in fp32 mode) against the oracle's relu(A (X W1) + b1). Loss and every
-    gradient except W1/b1 within 1e-4; W1/b1 in norm, because the reassociated
-    sum can flip a ReLU whose pre-activation lies within rounding of 0 (one flip
-    moves single entries of W1/b1 by ~1e-3 of their max)."""
+    here in fp32 mode) against the oracle's relu(A (X W1) + b1): the
+    reassociated sum differs in rounding only, so with the ReLU decisions
+    replayed (near-ties inside the fp32 band) loss and every gradient are
+    within 1e-4."""
     monkeypatch.setenv("DGC_AGG_FIRST", "1")
     from paper_2309_03523_b200 import load_plan_npz, single_device
     pa = single_device(load_plan_npz(artifacts_dir / "t2" / "plan.npz"))
-    out, tr, _ = run_pair(pa, dict(F=32, H=64, C=16, rnn="lstm", n_rnn=2), "off", epochs=2)
+    out, tr, orc = run_pair(pa, dict(F=32, H=64, C=16, rnn="lstm", n_rnn=2), "off", epochs=2)
     assert tr.shards[0].agg_first
-    for rep, o, grads in out:
-        assert rep.loss == pytest.approx(o["loss"], rel=1e-4)
-        for k, g in grads.items():
-            ref = o["grads"][k]
-            if k in ("W1", "b1"):
-                err = np.linalg.norm(g - ref) / np.linalg.norm(ref)
-                assert err <= 1e-3, f"epoch {rep.epoch} grad {k}: rel-norm {err:.2e}"
-            else:
-                err = np.abs(g - ref).max() / max(np.abs(ref).max(), 1e-30)
-                assert err <= 1e-4, f"epoch {rep.epoch} grad {k}: {err:.2e}"
+    check_epochs(out, rtol=1e-4, orc=orc)
 
 
-@pytest.mark.parametrize("precision,tol,single", [("fp32", 1e-4, False), ("tf32", 5e-2, False),
-                                                  ("tf32", 5e-2, True)])
+@pytest.mark.parametrize("precision,tol,single", [("fp32", 1e-4, False), ("tf32", 2e-2, False),
+                                                  ("tf32", 2e-2, True)])
 def test_trainer_evolvegcn_matches_oracle(artifacts_dir, precision, tol, single):
     """C3 model (EvolveGCN-O weight evolution + per-snapshot GCN on snapshot-
     segmented layouts) on the reference's 2-device EvolveGCN plan vs the oracle."""
@@ -170,14 +178,21 @@ def test_trainer_evolvegcn_matches_oracle(artifacts_dir, precision, tol, single)
                          pa.group_device, pa.group_ptr, pa.group_chunks)
     ocfg = OracleConfig(F=32, H=32, C=8, model="evolve", T=T, n_rnn=0, optimizer="sgd", lr=0.05)
     orc = OracleDGNN(lays, X, y, params, ocfg, inst_t=pa.inst_t)
+    orc.precision = precision
+    worst = {}
     for r in (1, 2, 3):
         rep = tr.run_epoch()
-        o = orc.epoch(r)
+        o = orc.epoch(r, forced_relu=oracle_relu_masks(tr, lays))
         assert rep.loss == pytest.approx(o["loss"], rel=tol)
         for k, g in tr.grads(0).items():
             ref = o["grads"][k]
-            err = np.linalg.norm(g - ref) / max(np.linalg.norm(ref), 1e-30)
-            assert err <= tol, f"epoch {r} grad {k}: {err:.2e}"
+            err = np.abs(g - ref).max() / max(np.abs(ref).max(), 1e-30)
+            worst[k] = max(worst.get(k, 0.0), err)
+    print(f"\nevolve {precision} single={single}: "
+          + ", ".join(f"{k}={v:.1e}" for k, v in worst.items()))
+    check_relu_ties(orc)
+    bad = {k: v for k, v in worst.items() if not v <= tol}
+    assert not bad, bad
 
 
 @pytest.mark.parametrize("H,precision,devices", [(128, "tf32", 1), (16, "fp32", 1), (16, "fp32", 4)])
