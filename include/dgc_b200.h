@@ -131,6 +131,17 @@ int dgc_spmm_csr(const int32_t* row_ptr, const int32_t* col, const float* dinv,
                  const float* Y, const float* bias, float* out,
                  int64_t n_rows, int32_t width, int32_t act, void* stream);
 
+/* K1 over a row subset: rows != NULL -> the rows rows[0..n_rows); rows ==
+ * NULL -> the range [row_begin, row_begin + n_rows). Same per-row arithmetic
+ * and reduction order as dgc_spmm_csr (bitwise identical rows). Used to split
+ * a device's rows into interior rows (no halo column; run while the boundary
+ * exchange is in flight) and boundary rows (after it lands), and the
+ * transposed backward into its halo block (sent back first) and own block. */
+int dgc_spmm_csr_rows(const int32_t* row_ptr, const int32_t* col, const float* dinv,
+                      const float* Y, const float* bias, float* out, const int32_t* rows,
+                      int64_t n_rows, int64_t row_begin, int32_t width, int32_t act,
+                      void* stream);
+
 /* K2: tcgen05 TF32 GEMM (TMA -> SMEM -> TMEM), fp32 storage, fp32 accumulate.
  *   C[M,N] = (accumulate ? C : 0) + op(A) op(B)  (+ bias[N]) (* (relu_src > 0))
  *   a_mn = 0: A is [M,K] (row stride lda); a_mn = 1: A stored as [K,M] (A^T)
@@ -278,6 +289,47 @@ int dgc_stale_distance(const float* Y, const int32_t* key_rows, const float* cac
 int dgc_stale_select(const float* Y, const int32_t* key_rows, const float* dist, float theta,
                      float* cache, uint8_t* cached, uint8_t* send, int64_t n_keys,
                      int32_t width, void* stream);
+
+/* dgc_stale_select2: the same decision with theta = coef * dmax[0] read from
+ * device memory (dmax = the MAX all-reduce of dgc_stale_distance's D_r;
+ * threshold() of stale.py:97-108 is D_r times a factor the host knows at the
+ * start of the epoch), compared in fp64; dmax == NULL uses `theta`. When ncut
+ * != NULL, *billed += sum of ncut[k] over sent keys (the reference-billed cut
+ * messages of sim.py:464-469 for this send mask). No host round trip. */
+int dgc_stale_select2(const float* Y, const int32_t* key_rows, const float* dist, double theta,
+                      const float* dmax, double coef, float* cache, uint8_t* cached,
+                      uint8_t* send, int64_t n_keys, int32_t width, const int64_t* ncut,
+                      uint64_t* billed, void* stream);
+
+/* K6': one-buffer exchange data plane (all peers per launch). Entries =
+ * the per-peer send lists concatenated peer-major: ent_key[e] = key index,
+ * ent_idx[e] = position in its peer's list, ent_ptr[D+1] = peer segments.
+ * A send buffer holds one record [int32 list position, 3 pad | width floats]
+ * per sent entry, peer-major -> ONE all-to-allv with split p = count_p.
+ * dgc_exchange_rank: stale compaction on the device (send[key] != 0):
+ *   ent_slot[e] = ordinal among sent entries or -1, counts[p] per peer. */
+int dgc_exchange_rank(const int32_t* ent_key, int64_t n_ent, const int32_t* ent_ptr, int32_t D,
+                      const uint8_t* send, int32_t* ent_slot, int32_t* counts, void* stream);
+/* record ent_slot[e] (ent_slot NULL: e) = (ent_idx[e], Y[key_rows[ent_key[e]]]) */
+int dgc_exchange_pack(const float* Y, int32_t width, const int32_t* key_rows,
+                      const int32_t* ent_key, const int32_t* ent_idx, const int32_t* ent_slot,
+                      int64_t n_ent, float* sendbuf, void* stream);
+/* received records (rcounts[p] from peer p, peer-major; at most n_max):
+ * dst[rlist[rlist_ptr[p] + j]] = row, j = the record's list position */
+int dgc_exchange_unpack(const float* recvbuf, int32_t width, const int32_t* rcounts, int32_t D,
+                        const int32_t* rlist, const int32_t* rlist_ptr, int64_t n_max,
+                        float* dst, void* stream);
+/* reverse direction: backbuf[i] = dY[rlist[rlist_ptr[p] + j_i]] for the i-th
+ * record received in the forward (rows only, width floats each) */
+int dgc_exchange_pack_back(const float* fwd_recvbuf, int32_t width, const int32_t* rcounts,
+                           int32_t D, const int32_t* rlist, const int32_t* rlist_ptr,
+                           int64_t n_max, const float* dY, float* backbuf, void* stream);
+/* dY[key_rows[k]] += backbuf[ent_slot[e]] over the key's entries e in
+ * kent[kent_ptr[k]..kent_ptr[k+1]) (ascending peer; skipped when -1):
+ * fixed-order accumulation of the returned halo gradients */
+int dgc_exchange_add_back(const float* backbuf, int32_t width, const int32_t* key_rows,
+                          const int32_t* kent_ptr, const int32_t* kent, const int32_t* ent_slot,
+                          int64_t n_keys, float* dY, void* stream);
 
 /* K6: exchange pack/unpack (boundary rows; bytes billed as sim.py:514-543).
  * dgc_compact_sent: out_pos = [i for i in 0..n) if send[pos[i]]] in order,

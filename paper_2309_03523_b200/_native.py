@@ -65,6 +65,14 @@ _SIGS = {
     "dgc_stale_distance": (_i32, [_p, _p, _p, _p, _i64, _i32, _p, _p, _p]),
     "dgc_stale_select": (_i32, [_p, _p, _p, _f32, _p, _p, _p, _i64, _i32, _p]),
     "dgc_compact_sent": (_i32, [_p, _i64, _p, _p, _p, _p]),
+    "dgc_spmm_csr_rows": (_i32, [_p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i32, _i32, _p]),
+    "dgc_stale_select2": (_i32, [_p, _p, _p, C.c_double, _p, C.c_double, _p, _p, _p, _i64, _i32,
+                                 _p, _p, _p]),
+    "dgc_exchange_rank": (_i32, [_p, _i64, _p, _i32, _p, _p, _p, _p]),
+    "dgc_exchange_pack": (_i32, [_p, _i32, _p, _p, _p, _p, _i64, _p, _p]),
+    "dgc_exchange_unpack": (_i32, [_p, _i32, _p, _i32, _p, _p, _i64, _p, _p]),
+    "dgc_exchange_pack_back": (_i32, [_p, _i32, _p, _i32, _p, _p, _i64, _p, _p, _p]),
+    "dgc_exchange_add_back": (_i32, [_p, _i32, _p, _p, _p, _p, _i64, _p, _p]),
     "dgc_gather_rows": (_i32, [_p, _p, _p, _i64, _i32, _p, _p]),
     "dgc_scatter_rows": (_i32, [_p, _p, _p, _i64, _i32, _p, _i32, _p]),
     "dgc_softmax_xent": (_i32, [_p, _p, _i64, _i32, _f32, _i32, _p, _p, _p, _p]),

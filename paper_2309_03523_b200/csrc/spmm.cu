@@ -21,12 +21,14 @@ template <int LPR, int NV>
 __global__ void __launch_bounds__(256) spmm_csr_kernel(
     const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
     const float* __restrict__ dinv, const float4* __restrict__ Y,
-    const float* __restrict__ bias, float4* __restrict__ out, int64_t n_rows, int act) {
+    const float* __restrict__ bias, float4* __restrict__ out, const int32_t* __restrict__ rows,
+    int64_t n_rows, int64_t row_begin, int act) {
   constexpr int W4 = LPR * NV;  // float4 per row
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = (int)(tid % LPR);
   const int64_t stride = ((int64_t)gridDim.x * blockDim.x) / LPR;
-  for (int64_t row = tid / LPR; row < n_rows; row += stride) {
+  for (int64_t i = tid / LPR; i < n_rows; i += stride) {
+    const int64_t row = rows ? (int64_t)__ldg(rows + i) : row_begin + i;
     const int beg = __ldg(row_ptr + row), end = __ldg(row_ptr + row + 1);
     float4 acc[NV];
 #pragma unroll
@@ -96,33 +98,45 @@ __global__ void __launch_bounds__(256) spmm_csr_kernel(
 
 template <int LPR, int NV>
 int launch(const int32_t* rp, const int32_t* col, const float* dinv, const float* Y,
-           const float* bias, float* out, int64_t n, int act, cudaStream_t s) {
+           const float* bias, float* out, const int32_t* rows, int64_t n, int64_t row_begin,
+           int act, cudaStream_t s) {
   const int block = 256;
   const int grid = dgc::grid_for(n * LPR, block, 8);
   spmm_csr_kernel<LPR, NV><<<grid, block, 0, s>>>(rp, col, dinv,
                                                   reinterpret_cast<const float4*>(Y), bias,
-                                                  reinterpret_cast<float4*>(out), n, act);
+                                                  reinterpret_cast<float4*>(out), rows, n,
+                                                  row_begin, act);
   DGC_CHECK_LAUNCH("spmm_csr_kernel");
   return DGC_OK;
 }
 
 }  // namespace
 
-extern "C" int dgc_spmm_csr(const int32_t* row_ptr, const int32_t* col, const float* dinv,
-                            const float* Y, const float* bias, float* out, int64_t n_rows,
-                            int32_t width, int32_t act, void* stream) {
+extern "C" int dgc_spmm_csr_rows(const int32_t* row_ptr, const int32_t* col, const float* dinv,
+                                 const float* Y, const float* bias, float* out,
+                                 const int32_t* rows, int64_t n_rows, int64_t row_begin,
+                                 int32_t width, int32_t act, void* stream) {
   DGC_REQUIRE(width > 0 && width % 4 == 0, "spmm: width must be a positive multiple of 4");
   if (n_rows == 0) return DGC_OK;
   cudaStream_t s = dgc::as_stream(stream);
+#define DGC_SPMM_L(LPR, NV) launch<LPR, NV>(row_ptr, col, dinv, Y, bias, out, rows, n_rows, row_begin, act, s)
   switch (width) {
-    case 4: return launch<1, 1>(row_ptr, col, dinv, Y, bias, out, n_rows, act, s);
-    case 8: return launch<2, 1>(row_ptr, col, dinv, Y, bias, out, n_rows, act, s);
-    case 16: return launch<4, 1>(row_ptr, col, dinv, Y, bias, out, n_rows, act, s);
-    case 32: return launch<8, 1>(row_ptr, col, dinv, Y, bias, out, n_rows, act, s);
-    case 64: return launch<16, 1>(row_ptr, col, dinv, Y, bias, out, n_rows, act, s);
-    case 128: return launch<32, 1>(row_ptr, col, dinv, Y, bias, out, n_rows, act, s);
-    case 256: return launch<32, 2>(row_ptr, col, dinv, Y, bias, out, n_rows, act, s);
-    case 512: return launch<32, 4>(row_ptr, col, dinv, Y, bias, out, n_rows, act, s);
+    case 4: return DGC_SPMM_L(1, 1);
+    case 8: return DGC_SPMM_L(2, 1);
+    case 16: return DGC_SPMM_L(4, 1);
+    case 32: return DGC_SPMM_L(8, 1);
+    case 64: return DGC_SPMM_L(16, 1);
+    case 128: return DGC_SPMM_L(32, 1);
+    case 256: return DGC_SPMM_L(32, 2);
+    case 512: return DGC_SPMM_L(32, 4);
     default: return dgc::fail(DGC_ERR_ARG, "spmm: unsupported width (use 4..512, power of two)");
   }
+#undef DGC_SPMM_L
+}
+
+extern "C" int dgc_spmm_csr(const int32_t* row_ptr, const int32_t* col, const float* dinv,
+                            const float* Y, const float* bias, float* out, int64_t n_rows,
+                            int32_t width, int32_t act, void* stream) {
+  return dgc_spmm_csr_rows(row_ptr, col, dinv, Y, bias, out, nullptr, n_rows, 0, width, act,
+                           stream);
 }

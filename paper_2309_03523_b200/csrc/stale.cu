@@ -60,18 +60,28 @@ __global__ void stale_distance_kernel(const float* __restrict__ Y, const int32_t
 }
 
 __global__ void stale_select_kernel(const float* __restrict__ Y, const int32_t* __restrict__ keys,
-                                    const float* __restrict__ dist, float theta,
+                                    const float* __restrict__ dist, double theta_host,
+                                    const float* __restrict__ dmax, double coef,
                                     float* __restrict__ cache, uint8_t* __restrict__ cached,
-                                    uint8_t* __restrict__ send, int64_t n_keys, int width) {
+                                    uint8_t* __restrict__ send, int64_t n_keys, int width,
+                                    const int64_t* __restrict__ ncut,
+                                    unsigned long long* __restrict__ billed) {
+  // theta = coef * D_r (threshold(), stale.py:97-108: every mode is D_r times a
+  // factor known on the host at the start of the epoch) with D_r read from
+  // device memory (the MAX all-reduce result): no host round trip. The
+  // comparison is in fp64 like the reference's (stale.py:169, strict >).
+  const double theta = dmax ? coef * (double)*dmax : theta_host;
   // one warp per key: decision by lane 0, broadcast, then a coalesced copy
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long bill = 0;
   for (int64_t k = warp; k < n_keys; k += nwarps) {
-    const bool s = (theta < 0.f) || !cached[k] || (dist[k] > theta);  // strict, stale.py:169
+    const bool s = (theta < 0.0) || !cached[k] || ((double)dist[k] > theta);
     if (lane == 0) {
       send[k] = s ? 1 : 0;
       if (s) cached[k] = 1;
+      if (s && ncut) bill += (unsigned long long)ncut[k];
     }
     if (s) {
       const float* y = Y + (int64_t)keys[k] * width;
@@ -79,6 +89,8 @@ __global__ void stale_select_kernel(const float* __restrict__ Y, const int32_t* 
       for (int j = lane; j < width; j += 32) c[j] = y[j];
     }
   }
+  // reference-billed messages of the sent keys (integer atomics: exact)
+  if (billed && lane == 0 && bill) atomicAdd(billed, bill);
 }
 
 }  // namespace
@@ -108,14 +120,23 @@ extern "C" int dgc_stale_distance(const float* Y, const int32_t* key_rows, const
   return DGC_OK;
 }
 
-extern "C" int dgc_stale_select(const float* Y, const int32_t* key_rows, const float* dist,
-                                float theta, float* cache, uint8_t* cached, uint8_t* send,
-                                int64_t n_keys, int32_t width, void* stream) {
+extern "C" int dgc_stale_select2(const float* Y, const int32_t* key_rows, const float* dist,
+                                 double theta, const float* dmax, double coef, float* cache,
+                                 uint8_t* cached, uint8_t* send, int64_t n_keys, int32_t width,
+                                 const int64_t* ncut, uint64_t* billed, void* stream) {
   if (n_keys == 0) return DGC_OK;
   cudaStream_t s = dgc::as_stream(stream);
   const int block = 256;
   stale_select_kernel<<<dgc::grid_for(n_keys * 32, block), block, 0, s>>>(
-      Y, key_rows, dist, theta, cache, cached, send, n_keys, width);
+      Y, key_rows, dist, theta, dmax, coef, cache, cached, send, n_keys, width, ncut,
+      reinterpret_cast<unsigned long long*>(billed));
   DGC_CHECK_LAUNCH("stale_select_kernel");
   return DGC_OK;
+}
+
+extern "C" int dgc_stale_select(const float* Y, const int32_t* key_rows, const float* dist,
+                                float theta, float* cache, uint8_t* cached, uint8_t* send,
+                                int64_t n_keys, int32_t width, void* stream) {
+  return dgc_stale_select2(Y, key_rows, dist, (double)theta, nullptr, 0.0, cache, cached, send,
+                           n_keys, width, nullptr, nullptr, stream);
 }

@@ -92,6 +92,69 @@ def spmm_csr(row_ptr, col, dinv, Y, bias, out, act: int, nnz=0, n_cols=0):
     return out
 
 
+def spmm_csr_rows(row_ptr, col, dinv, Y, bias, out, act: int, rows=None, n_rows=0, row_begin=0,
+                  nnz=0, n_cols=0, name="spmm_csr"):
+    """K1 over a row subset (dgc_spmm_csr_rows): the rows of the int32 list
+    ``rows``, or the range [row_begin, row_begin + n_rows). nnz / n_cols: the
+    subset's nonzeros and distinct gathered columns (algorithmic bytes)."""
+    _req(row_ptr, torch.int32, "row_ptr"); _req(col, torch.int32, "col")
+    _req(Y, torch.float32, "Y"); _req(out, torch.float32, "out"); _req(rows, torch.int32, "rows")
+    n = rows.numel() if rows is not None else int(n_rows)
+    W = out.shape[-1] if out.dim() > 1 else 1
+    nb = 4 * W * (n_cols + n) + 8 * n + 4 * nnz + 4 * n_cols
+    _run(name, lambda: _native.check(_native.lib().dgc_spmm_csr_rows(
+        _p(row_ptr), _p(col), _p(dinv), _p(Y), _p(bias), _p(out), _p(rows), n, int(row_begin), W,
+        act, _stream()), "dgc_spmm_csr_rows"), nb, 2 * nnz * W)
+    return out
+
+
+def stale_select_dev(Y, key_rows, dist, dmax, coef, cache, cached, send, width, ncut=None,
+                     billed=None, theta=0.0):
+    """K5 decision with theta = coef * dmax[0] on the device (dgc_stale_select2);
+    dmax None: the host theta. Accumulates the billed cut messages of sent keys."""
+    k = key_rows.numel()
+    _run("stale_select", lambda: _native.check(_native.lib().dgc_stale_select2(
+        _p(Y), _p(key_rows), _p(dist), float(theta), _p(dmax), float(coef), _p(cache),
+        _p(cached), _p(send), k, width, _p(ncut), _p(billed), _stream()), "dgc_stale_select2"),
+        k * 18)
+
+
+def exchange_rank(ent_key, ent_ptr, D, send, ent_slot, counts):
+    """dgc_exchange_rank: stale compaction of every peer's send list at once."""
+    n = ent_key.numel()
+    _run("exchange_rank", lambda: _native.check(_native.lib().dgc_exchange_rank(
+        _p(ent_key), n, _p(ent_ptr), int(D), _p(send), _p(ent_slot), _p(counts), _stream()),
+        "dgc_exchange_rank"), 13 * n)
+
+
+def exchange_pack(Y, width, key_rows, ent_key, ent_idx, ent_slot, sendbuf, n_sent=None):
+    """dgc_exchange_pack: one record per sent entry, all peers in one buffer."""
+    n = ent_key.numel()
+    rows = n if n_sent is None else n_sent
+    _run("exchange_pack", lambda: _native.check(_native.lib().dgc_exchange_pack(
+        _p(Y), int(width), _p(key_rows), _p(ent_key), _p(ent_idx), _p(ent_slot), n,
+        _p(sendbuf), _stream()), "dgc_exchange_pack"), 12 * n + rows * (8 * width + 16))
+
+
+def exchange_unpack(recvbuf, width, rcounts, D, rlist, rlist_ptr, n_max, dst):
+    _run("exchange_unpack", lambda: _native.check(_native.lib().dgc_exchange_unpack(
+        _p(recvbuf), int(width), _p(rcounts), int(D), _p(rlist), _p(rlist_ptr), int(n_max),
+        _p(dst), _stream()), "dgc_exchange_unpack"), n_max * (8 * width + 20))
+
+
+def exchange_pack_back(fwd_recvbuf, width, rcounts, D, rlist, rlist_ptr, n_max, dY, backbuf):
+    _run("exchange_pack_back", lambda: _native.check(_native.lib().dgc_exchange_pack_back(
+        _p(fwd_recvbuf), int(width), _p(rcounts), int(D), _p(rlist), _p(rlist_ptr), int(n_max),
+        _p(dY), _p(backbuf), _stream()), "dgc_exchange_pack_back"), n_max * (8 * width + 20))
+
+
+def exchange_add_back(backbuf, width, key_rows, kent_ptr, kent, ent_slot, dY):
+    n = key_rows.numel()
+    _run("exchange_add_back", lambda: _native.check(_native.lib().dgc_exchange_add_back(
+        _p(backbuf), int(width), _p(key_rows), _p(kent_ptr), _p(kent), _p(ent_slot), n, _p(dY),
+        _stream()), "dgc_exchange_add_back"), n * 12 * width)
+
+
 def gemm(A, B, C, M, N, K, *, a_mn=False, b_mn=True, lda=None, ldb=None, ldc=None,
          precision=3, bias=None, relu_src=None, accumulate=False, k_splits=1, partial=None,
          colsum_partial=None, act=0):

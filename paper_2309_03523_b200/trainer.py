@@ -107,6 +107,53 @@ def _dev_i32(a, device):
     return torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32), device=device)
 
 
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+class ExchangePlan:
+    """Index arrays and persistent buffers of one boundary exchange (one GCN
+    layer's halo rows, or one RNN layer's carries) for the one-buffer data
+    plane (csrc/exchange.cu): the per-peer send lists concatenated peer-major
+    ("entries"), the per-peer receive lists, and a key -> entries CSR in
+    ascending peer order for the fixed-order gradient return."""
+
+    def __init__(self, D, send_ptr, send_pos, recv_ptr, recv_slot, width, dev, n_keys,
+                 backward=True):
+        send_ptr = np.asarray(send_ptr, np.int64)
+        recv_ptr = np.asarray(recv_ptr, np.int64)
+        n_ent = int(send_ptr[-1])
+        n_recv = int(recv_ptr[-1])
+        self.n_ent, self.n_recv = n_ent, n_recv
+        peer_of = np.repeat(np.arange(D), np.diff(send_ptr))
+        self.ent_key = _dev_i32(np.asarray(send_pos)[:n_ent], dev)
+        self.ent_ptr = _dev_i32(send_ptr, dev)
+        self.ent_idx = _dev_i32(np.arange(n_ent) - send_ptr[peer_of], dev)
+        self.rlist = _dev_i32(np.asarray(recv_slot)[:n_recv], dev)
+        self.rlist_ptr = _dev_i32(recv_ptr, dev)
+        self.send_static = [int(x) for x in np.diff(send_ptr)]
+        self.recv_static = [int(x) for x in np.diff(recv_ptr)]
+        self.sent_host, self.recv_host = list(self.send_static), list(self.recv_static)
+        order = np.argsort(np.asarray(send_pos)[:n_ent], kind="stable")  # (key, peer) order
+        keys_sorted = np.asarray(send_pos)[:n_ent][order]
+        self.kent = _dev_i32(order, dev)
+        self.kent_ptr = _dev_i32(np.searchsorted(keys_sorted, np.arange(n_keys + 1)), dev)
+        i32 = dict(dtype=torch.int32, device=dev)
+        f32 = dict(dtype=torch.float32, device=dev)
+        self.ent_slot = torch.zeros(max(1, n_ent), **i32)
+        self.counts = torch.as_tensor(np.asarray(self.send_static, np.int32), device=dev)
+        self.rcounts = torch.as_tensor(np.asarray(self.recv_static, np.int32), device=dev)
+        self.sendbuf = torch.zeros(max(1, n_ent) * (width + 4), **f32)
+        self.recvbuf = torch.zeros(max(1, n_recv) * (width + 4), **f32)
+        if backward:
+            self.backsend = torch.zeros(max(1, n_recv) * width, **f32)
+            self.backrecv = torch.zeros(max(1, n_ent) * width, **f32)
+
+
 class Shard:
     """One device's state: layout tensors, activations, caches, parameters."""
 
@@ -148,14 +195,6 @@ class Shard:
         self.tkey_rows = _dev_i32(lay.tkey_rows, dev)
         peers = [p for p in range(self.D) if p != self.d]
         self.peers = peers
-        sp, rp = lay.send_ptr, lay.recv_ptr
-        tsp, trp = lay.tsend_ptr, lay.trecv_ptr
-        self.send_pos = {p: _dev_i32(lay.send_pos[sp[p]:sp[p + 1]], dev) for p in peers}
-        self.send_rows = {p: _dev_i32(lay.key_rows[lay.send_pos[sp[p]:sp[p + 1]]], dev) for p in peers}
-        self.recv_slot = {p: _dev_i32(lay.recv_slot[rp[p]:rp[p + 1]], dev) for p in peers}
-        self.tsend_pos = {p: _dev_i32(lay.tsend_pos[tsp[p]:tsp[p + 1]], dev) for p in peers}
-        self.tsend_rows = {p: _dev_i32(lay.tkey_rows[lay.tsend_pos[tsp[p]:tsp[p + 1]]], dev) for p in peers}
-        self.trecv_carry = {p: _dev_i32(lay.trecv_carry[trp[p]:trp[p + 1]], dev) for p in peers}
         # data (snapshot padding rows of EvolveGCN layouts: zero features, label -1)
         real = lay.own_gid >= 0
         gid = np.maximum(lay.own_gid, 0)
@@ -248,12 +287,33 @@ class Shard:
         self.evolve = cfg.model == "evolve"
         if self.evolve:
             self._init_evolve(lay, cfg, dev)
-        self.compact_idx = torch.zeros(max(1, len(lay.key_rows), len(lay.tkey_rows)), dtype=torch.int32, device=dev)
-        self.fresh = [{} for _ in range(2)]  # layer -> {peer: (recv idx tensor)}
-        self.sent = [{} for _ in range(2)]   # layer -> {peer: (send idx tensor or None, count)}
+        # exchange data plane (D > 1): one record buffer per exchange, all peers
+        # per launch; interior rows (no halo column) aggregate while it is in
+        # flight, boundary rows after it lands
+        if self.D > 1:
+            rp = np.asarray(lay.row_ptr, np.int64)
+            bnd_nnz = np.zeros(n, bool)
+            if nh:
+                hit = np.asarray(lay.col) >= n
+                bnd_nnz = np.add.reduceat(hit.astype(np.int64), rp[:-1]) > 0 if len(hit) else bnd_nnz
+                bnd_nnz &= np.diff(rp) > 0
+            self.rows_bnd = _dev_i32(np.flatnonzero(bnd_nnz), dev)
+            self.rows_int = _dev_i32(np.flatnonzero(~bnd_nnz), dev)
+            deg = np.diff(rp)
+            self.nnz_bnd, self.nnz_int = int(deg[bnd_nnz].sum()), int(deg[~bnd_nnz].sum())
+            self.xs = [ExchangePlan(self.D, lay.send_ptr, lay.send_pos, lay.recv_ptr, lay.recv_slot,
+                                    H, dev, len(lay.key_rows)) for _ in range(2)]
+            self.xt = [ExchangePlan(self.D, lay.tsend_ptr, lay.tsend_pos, lay.trecv_ptr,
+                                    lay.trecv_carry, self.hw, dev, len(lay.tkey_rows), backward=False)
+                       for _ in range(cfg.n_rnn)]
+            self.tkey_ncut = torch.ones(max(1, len(lay.tkey_rows)), dtype=torch.int64, device=dev)
+            # device counters: reference-billed cut messages (spatial, temporal) of
+            # this epoch's send masks; D_r per cache (read once per epoch)
+            self.billed_dev = torch.zeros(2, dtype=torch.int64, device=dev)
         self.step_count = 0
         self.step_dev = torch.zeros(1, dtype=torch.int32, device=dev)
         self.events = None
+        self.timing = None  # list of (start, end) events of compute-stream stalls
 
     def _init_evolve(self, lay, cfg, dev):
         """Per-snapshot weight machinery of EvolveGCN-O (C3)."""
@@ -312,62 +372,69 @@ class Shard:
         return self.offs[name][0]
 
     # -- exchanges ------------------------------------------------------------
-    def _decide(self, r, trace, Y, keys, cache, key):
-        """Stale decision of one cache: returns (theta, d_r) and leaves the send
-        mask in cache.send. Yields one MAX all-reduce for the global D_r."""
-        d_r = 0.0
-        theta = 0.0
+    def _stale_select(self, r, trace, Y, keys, cache, ncut, billed):
+        """Stale decision of one cache on the device (K5): distances, one MAX
+        all-reduce of D_r (the reference's one global cache, sim.py:455-459),
+        theta = coef * D_r in the select kernel (threshold(), stale.py:97-108,
+        with coef from the loss trace known on the host), billed messages
+        accumulated on the device. No host round trip. Returns (coef, D_r
+        device tensor or None); the send mask is left in cache.send."""
         if r >= 2:
+            coef = threshold(trace, r, 1.0, self.stale)  # threshold is linear in D_r
             cache_gap_gpu(Y, keys, cache)
             dmax = yield ("max", cache.dmax)
-            d_r = float(dmax.item())
-            theta = threshold(trace, r, d_r, self.stale)
-        filter_transmissions_gpu(Y, keys, cache, theta)
-        return theta, d_r
+            ops.stale_select_dev(Y, keys, cache.dist, dmax, coef, cache.values, cache.cached,
+                                 cache.send, cache.width, ncut=ncut, billed=billed)
+            return coef, dmax
+        ops.stale_select_dev(Y, keys, cache.dist, None, 0.0, cache.values, cache.cached,
+                             cache.send, cache.width, ncut=ncut, billed=billed, theta=0.0)
+        return 0.0, None
 
-    def _exchange_rows(self, Y, width, send_pos, send_rows, dst, recv_rows, cache):
-        """Pack the (stale-filtered) rows per peer, all-to-allv, unpack.
-        Returns {peer: received idx tensor} and {peer: (sent idx, count)}."""
-        sends, idxs, sent = [], [], {}
-        for p in self.peers:
-            if cache is not None:
-                cnt = torch.zeros(1, dtype=torch.int32, device=self.device)
-                ops.compact_sent(send_pos[p], cache.send, self.compact_idx, cnt)
-                c = int(cnt.item())
-                idx = self.compact_idx[:c].clone()
-            else:
-                c = send_pos[p].numel()
-                idx = torch.arange(c, dtype=torch.int32, device=self.device)
-            buf = torch.empty((c, width), dtype=torch.float32, device=self.device)
-            ops.gather_rows(Y, send_rows[p], idx, c, width, buf)
-            sends.append(buf)
-            idxs.append(idx)
-            sent[p] = (idx, c)
-        # without staleness every listed row is sent, so the receive counts are the
-        # plan's (no count exchange, no host sync)
-        rc = None if cache is not None else [recv_rows[p].numel() for p in self.peers]
-        recv = yield ("a2av", sends, idxs, rc)
-        fresh = {}
-        for p, (buf, idx) in zip(self.peers, zip(*recv)):
-            ops.scatter_rows(buf, recv_rows[p], idx, idx.numel(), width, dst)
-            fresh[p] = idx
-        return fresh, sent
+    def _send(self, xp: "ExchangePlan", Y, width, keys, cache):
+        """Pack this exchange's records (stale-compacted on the device when a
+        cache is given) and start the all-to-allv. Returns the runner token."""
+        slot = None
+        if cache is not None:
+            ops.exchange_rank(xp.ent_key, xp.ent_ptr, self.D, cache.send, xp.ent_slot, xp.counts)
+            slot = xp.ent_slot
+        ops.exchange_pack(Y, width, keys, xp.ent_key, xp.ent_idx, slot, xp.sendbuf)
+        tok = yield ("a2a_start", xp.sendbuf, None if cache is not None else xp.send_static,
+                     xp.counts, xp.recvbuf, width + 4, xp.recv_static, xp.rcounts)
+        return tok
 
-    def _exchange_back(self, l, dYext, H):
-        """Reverse all-to-allv of the gradients of fresh halo rows
-        (Appendix B.4: reused rows return nothing)."""
-        sends, idxs = [], []
-        for p in self.peers:
-            idx = self.fresh[l][p]
-            buf = torch.empty((idx.numel(), H), dtype=torch.float32, device=self.device)
-            ops.gather_rows(dYext, self.recv_slot[p], idx, idx.numel(), H, buf)
-            sends.append(buf)
-            idxs.append(idx)
-        # the peers return gradients for exactly the rows they were sent
-        recv = yield ("a2av", sends, idxs, [self.sent[l][p][1] for p in self.peers])
-        for p, (buf, _) in zip(self.peers, zip(*recv)):
-            idx, c = self.sent[l][p]
-            ops.scatter_rows(buf, self.send_rows[p], idx, c, H, dYext, add=True)
+    def _land(self, xp: "ExchangePlan", tok, width, dst):
+        """Finish an all-to-allv and unpack it into dst (on the runner's comm
+        stream when it has one: overlaps the compute stream). Returns the
+        event the consumer waits on (None: same stream)."""
+        res = yield ("a2a_finish", tok)
+        xp.sent_host, xp.recv_host = res["send_counts"], res["recv_counts"]
+        st = res.get("stream")
+        ctx = torch.cuda.stream(st) if st is not None else _nullctx()
+        with ctx:
+            ops.exchange_unpack(xp.recvbuf, width, xp.rcounts, self.D, xp.rlist, xp.rlist_ptr,
+                                sum(xp.recv_host), dst)
+            ev = None
+            if st is not None:
+                ev = torch.cuda.Event()
+                ev.record(st)
+        return ev
+
+    def _wait(self, ev):
+        if ev is not None:
+            self._stall(lambda: torch.cuda.current_stream(self.device).wait_event(ev))
+
+    def _stall(self, fn):
+        """Run fn (a stream wait / blocking collective on the compute stream),
+        timing the compute stream's stall when per-device timing is on."""
+        if self.timing is None:
+            return fn()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        out = fn()
+        b.record()
+        self.timing.append((a, b))
+        return out
 
     # -- one training step ----------------------------------------------------
     def step(self, r: int, trace: EpochLossTrace):
@@ -376,8 +443,11 @@ class Shard:
         cell = 0 if cfg.rnn == "gru" else 1
         rflag = 0x100 if self.tf32 else 0   # DGC_RNN_ROUND_TF32
         rnd2 = 2 if self.tf32 else 0        # spmm: round output to TF32
-        info = {"theta": {}, "d_r": {}, "billed_sp": 0, "billed_tm": 0, "rows": 0}
+        info = {"coef": {}, "d_r": {}, "rows": 0, "xbytes": 0}
         D = self.D
+        pending_t = []  # temporal carry exchanges: landed at the end of the step
+        if D > 1 and self.stale_on:
+            self.billed_dev.zero_()
         # ---------------- forward: structure encoder ----------------
         if self.evolve:  # EvolveGCN-O: W_t for every snapshot, per layer
             for l, e in enumerate(self.evo, start=1):
@@ -409,19 +479,26 @@ class Shard:
                 ops.gemm(hin, self.pr(W), Y, n, H, kin, lda=ldin, precision=self.prec_gcn)
             if D > 1:
                 cache = self.scache[l] if self.stale_on else None
+                xp = self.xs[l]
                 if cache is not None:
-                    th, dr = yield from self._decide(r, trace, Y, self.key_rows, cache, f"s{l}")
-                    info["theta"][f"s{l}"], info["d_r"][f"s{l}"] = th, dr
-                    billed = int((cache.send.to(torch.int64) * self.key_ncut).sum().item())
-                else:
-                    billed = self.key_ncut_total
-                info["billed_sp"] += billed
-                fresh, sent = yield from self._exchange_rows(
-                    Y, H, self.send_pos, self.send_rows, Y, self.recv_slot, cache)
-                self.fresh[l], self.sent[l] = fresh, sent
-                info["rows"] += sum(c for _, c in sent.values())
-            ops.spmm_csr(self.row_ptr, self.col, self.dinv, Y, self.p(b), self.Hl[l], act=1 | rnd2,
-                         nnz=self.nnz, n_cols=self.nloc)
+                    coef, dr = yield from self._stale_select(r, trace, Y, self.key_rows, cache,
+                                                             self.key_ncut, self.billed_dev[0:1])
+                    info["coef"][f"s{l}"], info["d_r"][f"s{l}"] = coef, dr
+                tok = yield from self._send(xp, Y, H, self.key_rows, cache)
+                # interior rows need no halo row: they aggregate while the exchange flies
+                ops.spmm_csr_rows(self.row_ptr, self.col, self.dinv, Y, self.p(b), self.Hl[l],
+                                  act=1 | rnd2, rows=self.rows_int, nnz=self.nnz_int,
+                                  n_cols=self.rows_int.numel())
+                ev = yield from self._land(xp, tok, H, Y)
+                info["rows"] += sum(xp.sent_host)
+                info["xbytes"] += sum(xp.sent_host) * (H + 4) * 4
+                self._wait(ev)
+                ops.spmm_csr_rows(self.row_ptr, self.col, self.dinv, Y, self.p(b), self.Hl[l],
+                                  act=1 | rnd2, rows=self.rows_bnd, nnz=self.nnz_bnd,
+                                  n_cols=self.nh + self.rows_bnd.numel())
+            else:
+                ops.spmm_csr(self.row_ptr, self.col, self.dinv, Y, self.p(b), self.Hl[l],
+                             act=1 | rnd2, nnz=self.nnz, n_cols=self.nloc)
             hin, ldin, kin = self.Hl[l], H, H
         # ---------------- forward: time encoder ----------------
         xr, ldx = self.Hl[1], H
@@ -450,26 +527,21 @@ class Shard:
                             self.slot_mask, self.slot_carry, self.carry[k], self.R, self.L, H,
                             self.hw, hb, c_out, self.save[k])
             if D > 1:
+                # carries for the NEXT epoch (carry-from-cache): the exchange is
+                # landed at the end of the step, overlapping everything after it
                 cache = self.tcache[k] if self.stale_on else None
                 if cache is not None:
-                    th, dr = yield from self._decide(r, trace, hb, self.tkey_rows, cache, f"t{k}")
-                    info["theta"][f"t{k}"], info["d_r"][f"t{k}"] = th, dr
-                    info["billed_tm"] += int(cache.send.to(torch.int64).sum().item())
-                else:
-                    info["billed_tm"] += int(self.tkey_rows.numel())
-                _, tsent = yield from self._exchange_rows(
-                    hb, self.hw, self.tsend_pos, self.tsend_rows, self.carry[k], self.trecv_carry,
-                    cache)
-                info["rows"] += sum(c for _, c in tsent.values())
+                    coef, dr = yield from self._stale_select(r, trace, hb, self.tkey_rows, cache,
+                                                             self.tkey_ncut, self.billed_dev[1:2])
+                    info["coef"][f"t{k}"], info["d_r"][f"t{k}"] = coef, dr
+                tok = yield from self._send(self.xt[k], hb, self.hw, self.tkey_rows, cache)
+                pending_t.append((k, tok))
             xr, ldx = hb, self.hw
         # ---------------- readout + loss ----------------
         ops.gemm(xr, self.pr("Wo"), self.logits, n, cfg.C, H, lda=ldx, precision=prec,
                  bias=self.p("bo"))
         ops.softmax_xent(self.logits, self.y, cfg.C, 1.0 / self.n_total, self.dlogits,
                          self.loss_partial, round_tf32=self.tf32, dl_partial=self.dl_partial)
-        loss_local = self.loss_partial.sum().reshape(1)
-        loss = yield ("sum", loss_local)
-        info["loss_sum"] = loss  # device scalar; read once the epoch is enqueued
         # ---------------- backward ----------------
         self.grads.zero_()
         ks, part = self.ksplit, self.partial
@@ -534,10 +606,30 @@ class Shard:
                     ops.gemm(self.AX, dZ, self.g(W), cfg.F, H, n, a_mn=True, lda=cfg.F, ldb=H,
                              precision=prec, k_splits=ks, partial=part)
                 continue
-            ops.spmm_csr(self.t_row_ptr, self.t_col, self.dinv, dZ, None, self.dYext, act=rnd2,
-                         nnz=self.nnz, n_cols=n)
             if D > 1:
-                yield from self._exchange_back(l, self.dYext, H)
+                # halo block first: its gradients go back to their owners while
+                # the own block aggregates (Appendix B.4: only fresh rows return)
+                xp = self.xs[l]
+                ops.spmm_csr_rows(self.t_row_ptr, self.t_col, self.dinv, dZ, None, self.dYext,
+                                  act=rnd2, n_rows=self.nh, row_begin=n, name="spmm_csr_t")
+                ops.exchange_pack_back(xp.recvbuf, H, xp.rcounts, D, xp.rlist, xp.rlist_ptr,
+                                       sum(xp.recv_host), self.dYext, xp.backsend)
+                tok = yield ("a2a_start", xp.backsend, list(xp.recv_host), None, xp.backrecv, H,
+                             list(xp.sent_host), None)
+                ops.spmm_csr_rows(self.t_row_ptr, self.t_col, self.dinv, dZ, None, self.dYext,
+                                  act=rnd2, n_rows=n, row_begin=0, nnz=self.nnz, n_cols=n,
+                                  name="spmm_csr_t")
+                res = yield ("a2a_finish", tok)
+                info["xbytes"] += sum(xp.recv_host) * H * 4
+                if res.get("stream") is not None:
+                    ev = torch.cuda.Event()
+                    ev.record(res["stream"])
+                    self._wait(ev)
+                ops.exchange_add_back(xp.backrecv, H, self.key_rows, xp.kent_ptr, xp.kent,
+                                      xp.ent_slot if self.stale_on else None, self.dYext)
+            else:
+                ops.spmm_csr(self.t_row_ptr, self.t_col, self.dinv, dZ, None, self.dYext,
+                             act=rnd2, nnz=self.nnz, n_cols=n)
             hin_l, ldin_l, kin_l = (self.X, cfg.F, cfg.F) if l == 0 else (self.Hl[0], H, H)
             if self.evolve:
                 e = self.evo[l]
@@ -582,7 +674,15 @@ class Shard:
                              precision=prec, k_splits=self.evo_gsplit, partial=self.evo_gpartial)
         for j0 in range(0, len(rjobs), 8):  # bias gradients, fixed order, 2 launches
             ops.reduce_rows_batched(rjobs[j0:j0 + 8])
-        # ---------------- gradient all-reduce + update ----------------
+        # ---------------- land the carries, all-reduces, update ----------------
+        for k, tok in pending_t:
+            xp = self.xt[k]
+            ev = yield from self._land(xp, tok, self.hw, self.carry[k])
+            info["rows"] += sum(xp.sent_host)
+            info["xbytes"] += sum(xp.sent_host) * (self.hw + 4) * 4
+            self._wait(ev)
+        loss_local = self.loss_partial.sum().reshape(1)
+        info["loss_sum"] = (yield ("sum", loss_local)) if D > 1 else loss_local
         if D > 1:
             yield ("sum", self.grads)
         self.step_count += 1
@@ -600,33 +700,57 @@ class Shard:
 # -- runners ------------------------------------------------------------------
 
 class LocalRunner:
-    """Services the collectives of all shards of one process by direct copies
-    (virtual devices on one GPU)."""
+    """Services the collectives of all shards of one process by direct device
+    copies (D virtual devices on one GPU). The shards advance in lock-step:
+    every shard yields the same request kind at the same point of the step.
+
+    With ``timing`` (a list per shard), each shard's generator segments are
+    bracketed by CUDA events: its compute time is the sum of its segments."""
+
+    def __init__(self):
+        self.timing = None
+        self._tokens = {}
 
     def run(self, gens):
         results = [None] * len(gens)
-        reqs = []
-        for g in gens:
-            reqs.append(next(g))
+        reqs = [self._advance(i, g, None, first=True) for i, g in enumerate(gens)]
         live = [True] * len(gens)
+        for i, r in enumerate(reqs):
+            if isinstance(r, _Done):
+                results[i], live[i] = r.value, False
         while any(live):
             kind = next(r for r, a in zip(reqs, live) if a)[0]
-            outs = self._service(kind, [r for r in reqs])
+            outs = self._service(kind, reqs)
             for i, g in enumerate(gens):
                 if not live[i]:
                     continue
-                try:
-                    reqs[i] = g.send(outs[i])
-                except StopIteration as stop:
-                    results[i] = stop.value
-                    live[i] = False
+                r = self._advance(i, g, outs[i])
+                if isinstance(r, _Done):
+                    results[i], live[i] = r.value, False
+                else:
+                    reqs[i] = r
         return results
+
+    def _advance(self, i, g, value, first=False):
+        a = b = None
+        if self.timing is not None:
+            a = torch.cuda.Event(enable_timing=True)
+            a.record()
+        try:
+            out = next(g) if first else g.send(value)
+        except StopIteration as stop:
+            out = _Done(stop.value)
+        if a is not None:
+            b = torch.cuda.Event(enable_timing=True)
+            b.record()
+            self.timing[i].append((a, b))
+        return out
 
     def _service(self, kind, reqs):
         D = len(reqs)
         if kind == "max":
             m = torch.stack([r[1].reshape(-1)[0] for r in reqs]).max().reshape(1)
-            return [m.clone() for _ in reqs]
+            return [m for _ in reqs]
         if kind == "sum":
             if D == 1:  # nothing to combine
                 return [reqs[0][1]]
@@ -636,28 +760,61 @@ class LocalRunner:
             for r in reqs:
                 r[1].copy_(acc)
             return [r[1] for r in reqs]
-        if kind == "a2av":
+        if kind == "a2a_start":
+            # (sendbuf, send_counts|None, counts_dev, recvbuf, rw, recv_counts|None, rcounts_dev)
+            sc = [list(r[2]) if r[2] is not None else [int(x) for x in r[3].tolist()] for r in reqs]
             outs = []
             for d in range(D):
-                bufs, idxs = [], []
+                rw, recvbuf = reqs[d][5], reqs[d][4]
+                roff = 0
                 for p in range(D):
-                    if p == d:
-                        continue
-                    j = d if d < p else d - 1  # position of d among p's peers
-                    bufs.append(reqs[p][1][j])
-                    idxs.append(reqs[p][2][j])
-                outs.append((bufs, idxs))
+                    n = sc[p][d] if p != d else 0
+                    if n:
+                        off = sum(sc[p][:d])
+                        recvbuf[roff * rw:(roff + n) * rw].copy_(reqs[p][1][off * rw:(off + n) * rw])
+                    roff += n
+                rc = [sc[p][d] if p != d else 0 for p in range(D)]
+                if reqs[d][2] is None and reqs[d][7] is not None:  # dynamic counts -> device
+                    reqs[d][7].copy_(torch.stack([reqs[p][3][d] for p in range(D)]))
+                outs.append(dict(send_counts=sc[d], recv_counts=rc, stream=None))
             return outs
+        if kind == "a2a_finish":
+            return [r[1] for r in reqs]
         raise ValueError(kind)
 
 
+class _Done:
+    def __init__(self, value):
+        self.value = value
+
+
 class NcclRunner:
-    """One shard per process; collectives through torch.distributed (NCCL)."""
+    """One shard per process; collectives through torch.distributed (NCCL).
+
+    Boundary all-to-allvs run on a dedicated comm stream: "a2a_start" makes
+    the comm stream wait for the packed send buffer only, so the compute
+    stream keeps running (interior rows) while the transfer is in flight;
+    "a2a_finish" hands the comm stream back to the shard, which unpacks on it
+    and joins. Stale-filtered (device-counted) exchanges first swap their
+    per-peer counts (one int per peer) and read them once on the host."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
         self.dist = dist
         self.group = group
+        self.timing = None
+        self.comm = None
+
+    def _stall(self, fn):
+        if self.timing is None:
+            return fn()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        out = fn()
+        b.record()
+        self.timing[0].append((a, b))
+        return out
 
     def run(self, gens):
         (g,) = gens
@@ -668,52 +825,66 @@ class NcclRunner:
                 kind = req[0]
                 if kind == "max":
                     t = req[1].clone()
-                    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+                    self._stall(lambda: dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group))
                     out = t
                 elif kind == "sum":
-                    dist.all_reduce(req[1], op=dist.ReduceOp.SUM, group=self.group)
+                    self._stall(lambda: dist.all_reduce(req[1], op=dist.ReduceOp.SUM,
+                                                        group=self.group))
                     out = req[1]
+                elif kind == "a2a_start":
+                    out = self._start(*req[1:])
+                elif kind == "a2a_finish":
+                    out = self._finish(req[1])
                 else:
-                    out = self._a2av(req[1], req[2], req[3] if len(req) > 3 else None)
+                    raise ValueError(kind)
                 req = g.send(out)
         except StopIteration as stop:
             return [stop.value]
 
-    def _a2av(self, bufs, idxs, peer_recv_counts=None):
-        """Variable-count all-to-all. peer_recv_counts (per peer, in peer order)
-        skips the count exchange when the caller knows them (no host sync)."""
+    def _start(self, sendbuf, sc, counts_dev, recvbuf, rw, rc, rcounts_dev):
         dist = self.dist
-        D = dist.get_world_size(self.group)
-        me = dist.get_rank(self.group)
-        dev = bufs[0].device if bufs else idxs[0].device
-        width = bufs[0].shape[1] if bufs else 1
-        send_counts = [0] * D
-        peers = [p for p in range(D) if p != me]
-        for p, b in zip(peers, bufs):
-            send_counts[p] = b.shape[0]
-        if peer_recv_counts is not None:
-            recv_counts = [0] * D
-            for p, c in zip(peers, peer_recv_counts):
-                recv_counts[p] = int(c)
-        else:
-            sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
-            rc = torch.empty_like(sc)
-            dist.all_to_all_single(rc, sc, group=self.group)
-            recv_counts = rc.tolist()
-        send_f = torch.cat([b.reshape(-1) for b in bufs]) if bufs else torch.empty(0, device=dev)
-        send_i = torch.cat(idxs) if idxs else torch.empty(0, dtype=torch.int32, device=dev)
-        recv_f = torch.empty(sum(recv_counts) * width, dtype=torch.float32, device=dev)
-        recv_i = torch.empty(sum(recv_counts), dtype=torch.int32, device=dev)
-        dist.all_to_all_single(recv_f, send_f, [c * width for c in recv_counts],
-                               [c * width for c in send_counts], group=self.group)
-        dist.all_to_all_single(recv_i, send_i, recv_counts, send_counts, group=self.group)
-        out_b, out_i, off = [], [], 0
-        for p in peers:
-            c = recv_counts[p]
-            out_b.append(recv_f[off * width:(off + c) * width].view(c, width))
-            out_i.append(recv_i[off:off + c])
-            off += c
-        return out_b, out_i
+        tok = dict(sendbuf=sendbuf, recvbuf=recvbuf, rw=rw, sc=sc, rc=rc, cuda=sendbuf.is_cuda)
+        if tok["cuda"] and self.comm is None:
+            self.comm = torch.cuda.Stream()
+        ctx = _nullctx()
+        if tok["cuda"]:
+            ev = torch.cuda.Event()
+            ev.record()
+            ctx = torch.cuda.stream(self.comm)
+        with ctx:
+            if tok["cuda"]:
+                self.comm.wait_event(ev)
+            if sc is None:  # device-counted (stale-filtered): swap the counts first
+                dist.all_to_all_single(rcounts_dev, counts_dev, group=self.group)
+                pin = torch.empty(2, counts_dev.numel(), dtype=torch.int32,
+                                  pin_memory=tok["cuda"])
+                pin[0].copy_(counts_dev, non_blocking=True)
+                pin[1].copy_(rcounts_dev, non_blocking=True)
+                tok["pin"] = pin
+                if tok["cuda"]:
+                    tok["ev"] = torch.cuda.Event()
+                    tok["ev"].record(self.comm)
+            else:
+                self._payload(tok)
+        return tok
+
+    def _payload(self, tok):
+        rw, sc, rc = tok["rw"], tok["sc"], tok["rc"]
+        with torch.cuda.stream(self.comm) if tok["cuda"] else _nullctx():
+            self.dist.all_to_all_single(tok["recvbuf"][:sum(rc) * rw], tok["sendbuf"][:sum(sc) * rw],
+                                        [c * rw for c in rc], [c * rw for c in sc],
+                                        group=self.group)
+        tok["done"] = True
+
+    def _finish(self, tok):
+        if not tok.get("done"):
+            if tok["cuda"]:
+                tok["ev"].synchronize()  # the only host wait: one per stale-filtered exchange
+            tok["sc"] = [int(x) for x in tok["pin"][0].tolist()]
+            tok["rc"] = [int(x) for x in tok["pin"][1].tolist()]
+            self._payload(tok)
+        return dict(send_counts=tok["sc"], recv_counts=tok["rc"],
+                    stream=self.comm if tok["cuda"] else None)
 
 
 # -- the trainer ----------------------------------------------------------------
@@ -765,7 +936,7 @@ class DGNNTrainer:
         prof = pa.profile or {}
         self.s_bytes = int(prof.get("bytes_per_scalar", 4))
         self.blocks = int(prof.get("blocks", 1))
-        self.method = "pgc"
+        self.method = str(pa.meta.get("method", "pgc"))
         self.epoch_no = 0
 
     def host_inputs(self, features: np.ndarray, labels: np.ndarray):
@@ -848,13 +1019,23 @@ class DGNNTrainer:
                 infos_g = self.runner.run([s.step(r, self.trace) for s in self.shards])
             self._graphs[key] = (g, infos_g)
             torch.cuda.synchronize(self.device)
+        replay = graphable and key in self._graphs
+        # per-device times (EpochReport.per_device_*): eager epochs bracket every
+        # shard's work / stalls with events; a replayed graph reuses the last
+        # eager measurement (single device: the epoch itself)
+        timed = not replay and len(self.shards) + (self.pa.n_devices > 1) > 1
+        if timed:
+            self.runner.timing = [[] for _ in self.shards]
+            for sh in self.shards:
+                sh.timing = []
         t0.record()
-        if graphable and key in self._graphs:
+        if replay:
             g, infos = self._graphs[key]
             g.replay()
         else:
             infos = self.runner.run([s.step(r, self.trace) for s in self.shards])
         t1.record()
+        self.runner.timing = None if not timed else self.runner.timing
         if self._loss_host is None:
             self._loss_host = torch.empty(1, dtype=infos[0]["loss_sum"].dtype, pin_memory=True)
         self._loss_host.copy_(infos[0]["loss_sum"].reshape(1), non_blocking=True)
@@ -866,58 +1047,101 @@ class DGNNTrainer:
             self.stage_inputs(*next_inputs)
         torch.cuda.synchronize(self.device)
         ms = t0.elapsed_time(t1)
+        if timed:
+            self._device_times(ms)
+            self.runner.timing = None
+            for sh in self.shards:
+                sh.timing = None
         self.epoch_no = r
         loss = float(self._loss_host[0]) / self.pa.n_instances
         self.trace.append(loss)
         return self._report(r, ms, infos, loss)
 
+    def _device_times(self, ms):
+        """Per-device compute and wall ms of the epoch just measured.
+        NCCL (one shard per rank): wall = the rank's epoch, compute = wall minus
+        the compute stream's stalls on collectives / exchange arrivals;
+        all-gathered over ranks. Local shards: compute = the sum of the shard's
+        own segments, wall = compute + the exchange service time."""
+        if isinstance(self.runner, NcclRunner):
+            sh = self.shards[0]
+            stall = sum(a.elapsed_time(b) for a, b in (sh.timing or []) + self.runner.timing[0])
+            import torch.distributed as dist
+            mine = torch.tensor([max(ms - stall, 0.0), ms], dtype=torch.float64, device=self.device)
+            out = [torch.zeros_like(mine) for _ in range(dist.get_world_size())]
+            dist.all_gather(out, mine)
+            vals = torch.stack(out).cpu().numpy()
+            self._dev_times = ([float(v) for v in vals[:, 0]], [float(v) for v in vals[:, 1]])
+            return
+        comp = [sum(a.elapsed_time(b) for a, b in seg) for seg in self.runner.timing]
+        service = max(ms - sum(comp), 0.0)
+        self._dev_times = (comp, [c + service for c in comp])
+
     def _report_static(self):
-        """Plan-constant report fields (computed once)."""
+        """Plan-constant report fields (computed once). Billing follows the
+        reference's MessageSet bytes (costmodel.py:95-103): per message and GCN
+        (RNN) layer, blocks * profile.embedding_dim * bytes_per_scalar."""
         if getattr(self, "_static_rep", None) is None:
             cfg = self.cfg
-            per_msg = self.blocks * cfg.H * self.s_bytes
+            prof = self.pa.profile or {}
+            emb = int(prof.get("embedding_dim", cfg.H))
+            per_msg = self.blocks * emb * self.s_bytes
+            lays = self.layouts
+            full = np.asarray([2 * sum(int(l.key_ncut.sum()) for l in lays),
+                               cfg.n_rnn * sum(len(l.tkey_rows) for l in lays)], np.int64)
             self._static_rep = dict(
-                per_msg=per_msg,
-                full_sp=2 * sum(int(l.key_ncut.sum()) for l in self.layouts) * per_msg,
-                full_tm=cfg.n_rnn * sum(len(l.tkey_rows) for l in self.layouts) * per_msg,
-                loading=sum(l.loaded_rows for l in self.layouts) * self.pa.feature_dim * self.s_bytes,
-                padding=sum(l.padding for l in self.layouts),
-                naive_padding=sum(l.naive_padding for l in self.layouts))
+                per_msg=per_msg, full=full,
+                loading=sum(l.loaded_rows for l in lays) * self.pa.feature_dim * self.s_bytes,
+                padding=sum(l.padding for l in lays),
+                naive_padding=sum(l.naive_padding for l in lays))
         return self._static_rep
 
     def _report(self, r, ms, infos, loss):
         cfg = self.cfg
-        H = cfg.H
         st = self._report_static()
-        per_msg = st["per_msg"]  # one layer's share of a reference message
-        billed_sp = sum(i["billed_sp"] for i in infos) * per_msg
-        billed_tm = sum(i["billed_tm"] for i in infos) * per_msg
-        full_sp, full_tm = st["full_sp"], st["full_tm"]
-        if len(self.shards) == 1 and self.pa.n_devices > 1:
+        per_msg = st["per_msg"]
+        stale_on = self.stale.mode is not StaleMode.OFF and self.pa.n_devices > 1
+        full = st["full"].copy()
+        if self.pa.n_devices > 1 and len(self.shards) == 1:  # NCCL: this rank's share
+            full = np.asarray([2 * int(self.layouts[0].key_ncut.sum()),
+                               cfg.n_rnn * len(self.layouts[0].tkey_rows)], np.int64)
+        if stale_on:
+            billed = torch.stack([sh.billed_dev for sh in self.shards]).sum(0)
+        else:
+            billed = torch.as_tensor(full, device=self.device)
+        rows = torch.tensor([sum(i["rows"] for i in infos), sum(i["xbytes"] for i in infos)],
+                            dtype=torch.int64, device=self.device)
+        acc = torch.cat([billed.to(torch.int64), torch.as_tensor(full, device=self.device), rows])
+        if self.pa.n_devices > 1 and len(self.shards) == 1:
             import torch.distributed as dist
-            t = torch.tensor([billed_sp, billed_tm, full_sp, full_tm], dtype=torch.float64,
-                             device=self.device)
-            dist.all_reduce(t)
-            billed_sp, billed_tm, full_sp, full_tm = (int(x) for x in t.tolist())
+            dist.all_reduce(acc)
+        acc = [int(x) for x in acc.tolist()]
+        billed_sp, billed_tm = acc[0] * per_msg, acc[1] * per_msg
+        full_b = (acc[2] + acc[3]) * per_msg
+        n_rows, xbytes = acc[4], acc[5]
         sent = billed_sp + billed_tm
-        full = full_sp + full_tm
-        avoided = full - sent
-        theta = infos[0]["theta"].get("s0", 0.0)
-        d_r = infos[0]["d_r"].get("s0", 0.0)
-        loading = st["loading"]
-        walls = [ms] * len(self.shards)
+        avoided = full_b - sent
+        i0 = infos[0]
+        d_r = {k: (float(v.reshape(-1)[0].item()) if v is not None else 0.0)
+               for k, v in i0["d_r"].items()}
+        theta = {k: i0["coef"][k] * d_r[k] for k in d_r}
+        comp, walls = getattr(self, "_dev_times", ([ms], [ms]))
+        if self.pa.n_devices == 1:
+            comp, walls = [ms], [ms]
+        lam = max(walls) / min(walls) if walls and min(walls) > 0 else 1.0
         return EpochReport(
-            method=self.method, epoch=r, per_device_compute_ms=walls, per_device_wall_ms=walls,
+            method=self.method, epoch=r, per_device_compute_ms=list(comp),
+            per_device_wall_ms=list(walls),
             spatial_traffic_bytes=billed_sp, temporal_traffic_bytes=billed_tm, shuffle_bytes=0,
-            loading_bytes=loading if r == 1 else 0,
+            loading_bytes=st["loading"] if r == 1 else 0,
             padding_slots=st["padding"], naive_padding_slots=st["naive_padding"],
-            load_divergence=1.0, wall_ms=ms, stale_theta=theta, stale_d=d_r,
-            stale_sent_bytes=sent if self.stale.mode is not StaleMode.OFF else 0,
-            stale_avoided_bytes=avoided if self.stale.mode is not StaleMode.OFF else 0,
-            stale_reduction_pct=(100.0 * avoided / full if full and self.stale.mode is not StaleMode.OFF else 0.0),
-            loss=loss, exchanged_rows=sum(i["rows"] for i in infos),
-            exchanged_bytes=sum(i["rows"] for i in infos) * H * 4,
-            stale_detail={"theta": infos[0]["theta"], "d_r": infos[0]["d_r"]})
+            load_divergence=lam, wall_ms=ms, stale_theta=theta.get("s0", 0.0),
+            stale_d=d_r.get("s0", 0.0),
+            stale_sent_bytes=sent if stale_on else 0,
+            stale_avoided_bytes=avoided if stale_on else 0,
+            stale_reduction_pct=(100.0 * avoided / full_b if full_b and stale_on else 0.0),
+            loss=loss, exchanged_rows=n_rows, exchanged_bytes=xbytes,
+            stale_detail={"theta": theta, "d_r": d_r})
 
     def params(self, shard: int = 0) -> dict:
         sh = self.shards[shard]

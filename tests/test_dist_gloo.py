@@ -12,23 +12,31 @@ import torch.multiprocessing as mp
 
 
 def mock_step(d, D):
-    """Mimics Shard.step's collective protocol on CPU tensors."""
+    """Mimics Shard.step's collective protocol on CPU tensors: MAX all-reduce,
+    a device-counted (stale-filtered) one-buffer all-to-allv, a static-count
+    one (the temporal carries: other record width), SUM all-reduce."""
     out = {}
     m = yield ("max", torch.tensor([float(d * 3 % 5)]))
-    out["max"] = float(m.item())
-    peers = [p for p in range(D) if p != d]
-    bufs, idxs = [], []
-    for p in peers:
-        c = (d * 7 + p * 3) % 5  # includes empty sends
-        bufs.append(torch.arange(c * 4, dtype=torch.float32).view(c, 4) + 100 * d + 10 * p)
-        idxs.append(torch.arange(c, dtype=torch.int32) * 2 + d)
-    rb, ri = yield ("a2av", bufs, idxs)
-    out["recv"] = {p: (b.clone().numpy(), i.clone().numpy()) for p, b, i in zip(peers, rb, ri)}
-    # second exchange with different widths (the temporal carry path: 2H wide)
-    bufs2 = [torch.full((1, 8), float(d * 10 + p)) for p in peers]
-    idx2 = [torch.tensor([p], dtype=torch.int32) for p in peers]
-    rb2, ri2 = yield ("a2av", bufs2, idx2)
-    out["recv2"] = {p: (b.clone().numpy(), i.clone().numpy()) for p, b, i in zip(peers, rb2, ri2)}
+    out["max"] = float(m.reshape(-1)[0])
+    rw = 4 + 4  # 16-byte header + 4 floats
+    cnt = [(d * 7 + p * 3) % 5 if p != d else 0 for p in range(D)]  # includes empty sends
+    send = torch.cat([torch.arange(c * rw, dtype=torch.float32) + 100 * d + 10 * p
+                      for p, c in enumerate(cnt)] + [torch.zeros(3 * rw)])  # spare capacity
+    counts = torch.tensor(cnt, dtype=torch.int32)
+    recv = torch.full((5 * D * rw,), -1.0)
+    rcounts = torch.zeros(D, dtype=torch.int32)
+    tok = yield ("a2a_start", send, None, counts, recv, rw, None, rcounts)
+    res = yield ("a2a_finish", tok)
+    out["recv"] = (list(res["recv_counts"]), recv[:sum(res["recv_counts"]) * rw].clone().numpy(),
+                   rcounts.clone().numpy(), list(res["send_counts"]))
+    # static counts (known to both sides), width 8 + header
+    rw2 = 8 + 4
+    sc = [1 if p != d else 0 for p in range(D)]
+    send2 = torch.cat([torch.full((rw2,), float(d * 10 + p)) for p in range(D) if p != d])
+    recv2 = torch.zeros((D - 1) * rw2)
+    tok2 = yield ("a2a_start", send2, sc, None, recv2, rw2, list(sc), None)
+    res2 = yield ("a2a_finish", tok2)
+    out["recv2"] = (list(res2["recv_counts"]), recv2.clone().numpy())
     g = torch.full((6,), float(d + 1))
     s = yield ("sum", g)
     out["sum"] = s.clone().numpy()
@@ -64,13 +72,22 @@ def test_nccl_runner_equals_local_runner(world, port):
         assert a["max"] == b["max"] == max(float(r * 3 % 5) for r in range(world))
         np.testing.assert_array_equal(a["sum"], b["sum"])
         for key in ("recv", "recv2"):
-            for p in a[key]:
-                np.testing.assert_array_equal(a[key][p][0], b[key][p][0])
-                np.testing.assert_array_equal(a[key][p][1], b[key][p][1])
-                # sender p's payload for d arrives intact
-                if key == "recv":
-                    c = (p * 7 + d * 3) % 5
-                    assert a[key][p][0].shape == (c, 4)
+            assert a[key][0] == b[key][0]
+            for x, y in zip(a[key][1:], b[key][1:]):
+                np.testing.assert_array_equal(x, y)
+        # sender p's records for d arrive intact, peer-major
+        rc = a["recv"][0]
+        assert rc == [(p * 7 + d * 3) % 5 if p != d else 0 for p in range(world)]
+        np.testing.assert_array_equal(a["recv"][2], rc)
+        off = 0
+        for p in range(world):
+            if rc[p]:
+                sc_p = [(p * 7 + q * 3) % 5 if q != p else 0 for q in range(world)]
+                first = 100 * p + 10 * d + 0.0
+                assert a["recv"][1][off * 8] == first
+                assert a["recv"][1][(off + rc[p]) * 8 - 1] == first + rc[p] * 8 - 1
+                assert sum(sc_p[:d]) >= 0
+            off += rc[p]
 
 
 @pytest.mark.parametrize("name", ["t2", "t4", "c1"])

@@ -266,6 +266,119 @@ def test_exchange_pack_unpack():
     np.testing.assert_array_equal(dst.cpu().numpy(), exp)
 
 
+@pytest.mark.parametrize("W,stale", [(16, True), (128, True), (64, False), (8, True)])
+def test_exchange_data_plane(W, stale):
+    """One-buffer exchange (csrc/exchange.cu) for D = 4 virtual devices vs
+    numpy: device compaction of every peer's list, records, unpack into halo
+    rows, reverse pack of the fresh rows' gradients and the fixed-order
+    add-back (ascending peer)."""
+    from paper_2309_03523_b200 import ops
+    from paper_2309_03523_b200.trainer import ExchangePlan
+    rng = np.random.default_rng(W)
+    D, me, n_keys, n_own = 4, 1, 700, 2000
+    key_rows = np.sort(rng.choice(n_own, n_keys, replace=False)).astype(np.int32)
+    lists = [np.sort(rng.choice(n_keys, int(rng.integers(0, 400)), replace=False)) if p != me
+             else np.zeros(0, np.int64) for p in range(D)]
+    send_ptr = np.cumsum([0] + [len(l) for l in lists])
+    send_pos = np.concatenate(lists).astype(np.int32)
+    halo_owner = rng.integers(0, D, 900)  # every halo row has one owner (disjoint lists)
+    rl = [np.flatnonzero((halo_owner == p) & (rng.random(900) < 0.7)) + n_own if p != me
+          else np.zeros(0, np.int64) for p in range(D)]
+    recv_ptr = np.cumsum([0] + [len(l) for l in rl])
+    recv_slot = np.concatenate(rl).astype(np.int32)
+    xp = ExchangePlan(D, send_ptr, send_pos, recv_ptr, recv_slot, W, dev, n_keys)
+    Y = rng.standard_normal((n_own + 900, W)).astype(np.float32)
+    send = (rng.random(n_keys) < 0.6).astype(np.uint8) if stale else np.ones(n_keys, np.uint8)
+    slot = None
+    if stale:
+        ops.exchange_rank(xp.ent_key, xp.ent_ptr, D, t(send, torch.uint8), xp.ent_slot, xp.counts)
+        slot = xp.ent_slot
+    Yt = t(Y)
+    ops.exchange_pack(Yt, W, t(key_rows, torch.int32), xp.ent_key, xp.ent_idx, slot, xp.sendbuf)
+    cnt = xp.counts.cpu().numpy()
+    rec = xp.sendbuf.cpu().numpy()
+    o = 0
+    for p in range(D):
+        sel = [j for j, k in enumerate(lists[p]) if send[k]]
+        assert cnt[p] == len(sel)
+        for j in sel:
+            r = rec[o * (W + 4):(o + 1) * (W + 4)]
+            assert r[:1].view(np.int32)[0] == j
+            np.testing.assert_array_equal(r[4:], Y[key_rows[lists[p][j]]])
+            o += 1
+    # receive: records from the peers for my recv lists (every other fresh)
+    rcnt = np.zeros(D, np.int32)
+    recs, fresh = [], []
+    for p in range(D):
+        js = [j for j in range(len(rl[p])) if j % 2 == 0]
+        rcnt[p] = len(js)
+        for j in js:
+            v = rng.standard_normal(W).astype(np.float32)
+            recs.append(np.concatenate([np.asarray([j, 0, 0, 0], np.int32).view(np.float32), v]))
+            fresh.append((rl[p][j], v))
+    rbuf = t(np.concatenate(recs) if recs else np.zeros(W + 4, np.float32))
+    dst = Yt.clone()
+    ops.exchange_unpack(rbuf, W, t(rcnt, torch.int32), D, xp.rlist, xp.rlist_ptr, len(recs), dst)
+    exp = Y.copy()
+    for s_, v in fresh:
+        exp[s_] = v
+    np.testing.assert_array_equal(dst.cpu().numpy(), exp)
+    # reverse: gradient rows of the fresh halo rows, in received order
+    dY = rng.standard_normal((n_own + 900, W)).astype(np.float32)
+    back = torch.zeros(max(1, len(recs)) * W, device=dev)
+    ops.exchange_pack_back(rbuf, W, t(rcnt, torch.int32), D, xp.rlist, xp.rlist_ptr, len(recs),
+                           t(dY), back)
+    np.testing.assert_array_equal(back.cpu().numpy()[:len(recs) * W].reshape(-1, W),
+                                  np.asarray([dY[s_] for s_, _ in fresh]).reshape(-1, W))
+    # add-back: the gradients returned for my sent records, fixed peer order
+    n_sent = int(cnt.sum())
+    g = rng.standard_normal((max(1, n_sent), W)).astype(np.float32)
+    dYt = t(dY)
+    ops.exchange_add_back(t(g), W, t(key_rows, torch.int32), xp.kent_ptr, xp.kent, slot, dYt)
+    exp = dY.copy()
+    acc = {}
+    o = 0
+    for p in range(D):
+        for j, k in enumerate(lists[p]):
+            if send[k]:
+                acc.setdefault(int(k), []).append(g[o])
+                o += 1
+    for k, gs in acc.items():
+        v = exp[key_rows[k]].copy()
+        for x in gs:  # ascending peer
+            v = v + x
+        exp[key_rows[k]] = v
+    np.testing.assert_array_equal(dYt.cpu().numpy(), exp)
+
+
+def test_spmm_row_subsets_equal_full():
+    """dgc_spmm_csr_rows on interior / boundary row lists and on row ranges
+    is bitwise the full dgc_spmm_csr."""
+    from paper_2309_03523_b200 import ops
+    rng = np.random.default_rng(3)
+    n, nc, W = 3000, 3500, 128
+    deg = rng.integers(1, 30, n)
+    row_ptr = np.concatenate([[0], np.cumsum(deg)]).astype(np.int32)
+    col = np.concatenate([np.sort(rng.choice(nc, d, replace=False)) for d in deg]).astype(np.int32)
+    dinv = rng.random(nc).astype(np.float32)
+    Y = t(rng.standard_normal((nc, W)).astype(np.float32))
+    b = t(rng.standard_normal(W).astype(np.float32))
+    full = torch.zeros((n, W), device=dev)
+    ops.spmm_csr(t(row_ptr, torch.int32), t(col, torch.int32), t(dinv), Y, b, full, act=1)
+    bnd = np.asarray([(col[row_ptr[i]:row_ptr[i + 1]] >= n).any() for i in range(n)])
+    part = torch.zeros((n, W), device=dev)
+    for rows in (np.flatnonzero(~bnd), np.flatnonzero(bnd)):
+        ops.spmm_csr_rows(t(row_ptr, torch.int32), t(col, torch.int32), t(dinv), Y, b, part, act=1,
+                          rows=t(rows, torch.int32))
+    assert torch.equal(part, full)
+    part.zero_()
+    ops.spmm_csr_rows(t(row_ptr, torch.int32), t(col, torch.int32), t(dinv), Y, b, part, act=1,
+                      n_rows=1234, row_begin=n - 1234)
+    ops.spmm_csr_rows(t(row_ptr, torch.int32), t(col, torch.int32), t(dinv), Y, b, part, act=1,
+                      n_rows=n - 1234, row_begin=0)
+    assert torch.equal(part, full)
+
+
 def test_softmax_xent_colsum_optimizers():
     from paper_2309_03523_b200 import ops
     rng = np.random.default_rng(10)
