@@ -116,6 +116,28 @@ class ClockSampler:
                 "samples": len(sm), "sm_min_mhz": min(sm)}
 
 
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def workload(args, pa, cfg) -> str:
+    """config.workload: byte-identical in both arms (same plan, same model)."""
+    sigma = "2mu" if args.config.startswith("c5") else "mu"
+    model = (f"EvolveGCN-O (2 GCN, per-snapshot weights), F={cfg.F} H={cfg.H} "
+             if cfg.model == "evolve" else
+             f"{cfg.n_rnn}-layer {cfg.rnn.upper()} + 2 GCN, F={cfg.F} H={cfg.H} ")
+    return (f"{args.config}: {pa.n_instances} instances x {pa.T} snapshots, "
+            f"{pa.n_spatial_edges} edges (power-law, sigma={sigma}), {model}C={cfg.C}, "
+            f"chunk plan of the reference planner ({'fused' if pa.fused else 'unfused'}, "
+            f"D={pa.n_devices})")
+
+
 def load_plan(args, world):
     from paper_2309_03523_b200 import load_plan_npz, single_device
     if world == 1:
@@ -126,10 +148,16 @@ def load_plan(args, world):
             pa.meta["note"] = "single-device restatement of the D=8 plan"
             return pa, "strong"
         return load_plan_npz(p), "strong"
-    p = ROOT / "artifacts" / f"{args.config}d{world}" / "plan.npz"
-    if p.exists():
-        return load_plan_npz(p), "strong"
-    return load_plan_npz(ROOT / "artifacts" / args.config / "plan.npz"), "weak"
+    # N ranks: the reference planner's D = N plan of the same graph, one shard
+    # per rank (strong scaling: the graph is fixed, sim.py:76-105 n_devices = N)
+    for p in (ROOT / "artifacts" / f"{args.config}d{world}" / "plan.npz",
+              ROOT / "artifacts" / args.config / "plan.npz"):
+        if p.exists():
+            pa = load_plan_npz(p)
+            if pa.n_devices == world:
+                return pa, "strong"
+    raise SystemExit(f"bench.py: no {world}-device plan of {args.config} "
+                     f"(artifacts/{args.config}d{world}/plan.npz; tools/make_artifacts.py)")
 
 
 def model_cfg(args, pa):
@@ -142,12 +170,16 @@ def model_cfg(args, pa):
 
 def cpu_oracle(pa, cfg):
     """The CPU oracle trainer (oracle/dgnn.py, numpy fp64, all host BLAS
-    threads) on the same plan and model."""
+    threads) on the same plan and model, with its per-device layouts from the
+    independent Python restatement oracle/layout.py (no product code: the
+    native library is never loaded on this arm)."""
     import oracle.dgnn as od
-    from paper_2309_03523_b200.layout import build_layout
+    from oracle.layout import build_layouts
     from paper_2309_03523_b200.model import init_params, synthetic_inputs
     X, y = synthetic_inputs(pa.n_instances, cfg.F, cfg.C, 0)
-    lays = [build_layout(pa, d) for d in range(pa.n_devices)]
+    lays = build_layouts(pa.n_instances, pa.inst_entity, pa.inst_t, pa.spatial_edges,
+                         pa.temporal_links, pa.structure_device, pa.chunk_of, pa.n_devices,
+                         pa.group_device, pa.group_ptr, pa.group_chunks)
     T = int(pa.inst_t.max())
     ocfg = od.OracleConfig(F=cfg.F, H=cfg.H, C=cfg.C, rnn=cfg.rnn, n_rnn=cfg.n_rnn,
                            model=cfg.model, T=T, optimizer="adam", lr=1e-3)
@@ -173,16 +205,17 @@ def cpu_epoch_time(pa, cfg, budget_s):
 def run_reference(args):
     """Reference arm: the CPU oracle port of the path on the host cores (rank 0
     only; other ranks exit). One step = one full fp64 epoch of the same plan
-    and model."""
+    (the D = N plan at N ranks) and model as our arm."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    import torch  # noqa: F401  (threads)
-    pa, _ = load_plan(args, 1)
+    pa, scaling = load_plan(args, world)
     cfg = model_cfg(args, pa)
     cores = os.cpu_count()
+    t_build = time.perf_counter()
     orc = cpu_oracle(pa, cfg)
+    t_build = time.perf_counter() - t_build
     times = []
     for r in range(1, args.warmup + args.steps + 1):
         t0 = time.perf_counter()
@@ -191,17 +224,21 @@ def run_reference(args):
     times = times[args.warmup:] or times
     ep = statistics.mean(times)
     value = pa.n_spatial_edges / ep
+    loaded = [Path(l.split()[-1]).name for l in Path("/proc/self/maps").read_text().splitlines()
+              if "libdgc_b200" in l] if Path("/proc/self/maps").exists() else []
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ep * 1e3, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": ep * 1e3, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {pa.n_instances} instances x {pa.T} snapshots, "
-                                   f"{pa.n_spatial_edges} edges, {cfg.rnn.upper()}x{cfg.n_rnn}, "
-                                   f"F={cfg.F} H={cfg.H}", "parallelism": "host CPU"},
+            "config": {"workload": workload(args, pa, cfg), "parallelism": "host CPU"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "cpu_model": cpu_model(), "epoch_s": ep,
                              "sample": f"{args.steps} full epochs (after {args.warmup} warm-up) "
                                        "of the fp64 oracle (oracle/dgnn.py) on the same plan/"
-                                       "model; the reference (dynpart) has no DGNN trainer"},
+                                       "model, layouts from oracle/layout.py "
+                                       f"({t_build:.0f} s to build, untimed); the reference "
+                                       "(dynpart) has no DGNN trainer",
+                             "native_libs_loaded": sorted(set(loaded))},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -255,6 +292,7 @@ def run_ours(args):
             barrier()
             rep = tr.run_epoch()  # brackets the step with CUDA events (wall_ms)
             times.append(rep.wall_ms)
+            rep_last = rep
             barrier()
     # ---- per-kernel table: separate eager epochs with CUDA events around every
     # native launch on its stream (never inside the timed region) ----
@@ -262,6 +300,8 @@ def run_ours(args):
     prof = ops.profile()
     graph_mode, tr.cuda_graph = tr.cuda_graph, False
     n_prof = max(1, min(args.steps, 3))
+    if distributed:
+        tr.runner.comm_timing = []
     with prof:
         for _ in range(n_prof):
             flush.zero_()
@@ -269,6 +309,25 @@ def run_ours(args):
             tr.run_epoch()
             barrier()
     tr.cuda_graph = graph_mode
+    exchange = None
+    if distributed:
+        # payload all-to-allvs on the comm stream (overlapped with compute), per
+        # step; NVLink 5 = 900 GB/s per direction per GPU
+        ct = tr.runner.comm_timing
+        tr.runner.comm_timing = None
+        torch.cuda.synchronize()
+        x_ms = sum(a.elapsed_time(b) for a, b, _, _ in ct) / n_prof
+        x_out = sum(o for _, _, o, _ in ct) / n_prof
+        x_in = sum(i for _, _, _, i in ct) / n_prof
+        t = torch.tensor([x_ms, x_out, x_in], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        x_ms, x_out, x_in = t.tolist()
+        gbs = max(x_out, x_in) / (x_ms / 1e3) / 1e9 if x_ms > 0 else 0.0
+        exchange = {"bytes_out_per_step": x_out, "bytes_in_per_step": x_in,
+                    "a2a_ms_per_step": x_ms, "GBps": gbs, "peak_GBps": 900.0,
+                    "frac": gbs / 900.0,
+                    "note": "busiest rank; NCCL all-to-allv time on the comm stream, which "
+                            "overlaps interior-row SpMM (not on the critical path when hidden)"}
     # per-step averages over the profiled epochs, expressed per `steps` epochs
     kern = {k: {f: v[f] * args.steps / n_prof for f in ("ms", "launches", "kernels", "bytes", "flops")}
             for k, v in prof.summary().items()}
@@ -336,7 +395,7 @@ def run_ours(args):
     if world == 1 and not args.no_cpu_baseline:
         t_cpu, n_ep = cpu_epoch_time(pa, cfg, args.cpu_sample_s)
         cpu = {"value": pa.n_spatial_edges / t_cpu, "unit": UNIT, "cores": os.cpu_count(),
-               "kind": "port", "epoch_s": t_cpu,
+               "kind": "port", "epoch_s": t_cpu, "cpu_model": cpu_model(),
                "sample": f"{n_ep} full epoch(s) of the fp64 numpy oracle (oracle/dgnn.py) on the "
                          f"same plan and model, all host BLAS threads"}
     line = {
@@ -344,14 +403,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
         "scaling": scaling, "vs_baseline": None, "dtype": "tf32" if args.precision == "tf32" else "f32",
         "data": "synthetic",
-        "config": {"workload": f"{args.config}: {pa.n_instances} instances x {pa.T} snapshots, "
-                               f"{pa.n_spatial_edges} edges (power-law, sigma={'2mu' if args.config.startswith('c5') else 'mu'}), "
-                               + (f"EvolveGCN-O (2 GCN, per-snapshot weights), F={cfg.F} H={cfg.H} "
-                                  if cfg.model == "evolve" else
-                                  f"{cfg.n_rnn}-layer {cfg.rnn.upper()} + 2 GCN, F={cfg.F} H={cfg.H} ")
-                               + 
-                               f"C={cfg.C}, chunk plan of the reference planner "
-                               f"({'fused' if pa.fused else 'unfused'}, D={pa.n_devices})",
+        "config": {"workload": workload(args, pa, cfg),
                    "epoch_ms": step_ms, "l2": "flushed (320 MB write) before every timed step",
                    "parallelism": f"chunk-sharded x{world}" if distributed else
                    ("replicas" if world > 1 else "1 GPU")},
@@ -368,6 +420,13 @@ def run_ours(args):
                      "avg_launch_ms": avg_ms},
         "kernels": per_kernel,
         "gpu_launches": gpu_launches,
+        "exchange": exchange,
+        "epoch_report": {"per_device_compute_ms": rep_last.per_device_compute_ms,
+                         "per_device_wall_ms": rep_last.per_device_wall_ms,
+                         "load_divergence": rep_last.load_divergence,
+                         "spatial_traffic_bytes": rep_last.spatial_traffic_bytes,
+                         "temporal_traffic_bytes": rep_last.temporal_traffic_bytes,
+                         "exchanged_bytes": rep_last.exchanged_bytes},
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
     }
@@ -376,8 +435,26 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def spawn(args) -> int:
+    """`python bench.py --gpus N` without a launcher: re-run this script under
+    torchrun, one rank per GPU (rendezvous on 127.0.0.1); rank 0 prints the
+    line."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 if __name__ == "__main__":
     a = parse()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn(a))
+    if int(os.environ.get("WORLD_SIZE", "1")) != a.gpus:
+        raise SystemExit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE')}")
     if a.impl == "reference":
         run_reference(a)
     else:

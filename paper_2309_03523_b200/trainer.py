@@ -804,6 +804,9 @@ class NcclRunner:
         self.group = group
         self.timing = None
         self.comm = None
+        # optional [(start, end, bytes out, bytes in)] of every payload
+        # all-to-allv on the comm stream (bench.py: exchange GB/s vs NVLink)
+        self.comm_timing = None
 
     def _stall(self, fn):
         if self.timing is None:
@@ -870,10 +873,18 @@ class NcclRunner:
 
     def _payload(self, tok):
         rw, sc, rc = tok["rw"], tok["sc"], tok["rc"]
+        timed = self.comm_timing is not None and tok["cuda"]
         with torch.cuda.stream(self.comm) if tok["cuda"] else _nullctx():
+            if timed:
+                a = torch.cuda.Event(enable_timing=True)
+                a.record(self.comm)
             self.dist.all_to_all_single(tok["recvbuf"][:sum(rc) * rw], tok["sendbuf"][:sum(sc) * rw],
                                         [c * rw for c in rc], [c * rw for c in sc],
                                         group=self.group)
+            if timed:
+                b = torch.cuda.Event(enable_timing=True)
+                b.record(self.comm)
+                self.comm_timing.append((a, b, 4 * rw * sum(sc), 4 * rw * sum(rc)))
         tok["done"] = True
 
     def _finish(self, tok):
