@@ -16,7 +16,8 @@ __version__ = "0.1.0"
 
 def __getattr__(name):
     # GPU-facing pieces load the native library lazily (fail loudly if absent)
-    if name in ("DGNNTrainer", "EpochReport", "run_epochs"):
+    if name in ("DGNNTrainer", "EpochReport", "run_epochs", "simulate_epoch", "StaleState",
+                "reference_billed_messages"):
         from . import trainer
         return getattr(trainer, name)
     if name in ("GruCell", "PackedBatch", "pack_sequences", "gru_forward_masked"):

@@ -1178,19 +1178,94 @@ class DGNNTrainer:
         return {l: (sh.Hl[l] > 0).cpu().numpy() for l in range(2)}
 
 
+def reference_billed_messages(layouts, spatial_sends, temporal_sends):
+    """Host restatement of the reference's billing for given send masks:
+    the cut messages whose source is sent (sim.py:464-469,
+    ``msgs.nbytes[cut & send[src]]``), counted per GCN layer (spatial) and per
+    RNN layer (temporal). ``spatial_sends[l][d]`` / ``temporal_sends[k][d]``:
+    bool per key of device d (layouts' key_rows / tkey_rows). Returns
+    (spatial messages, temporal messages); bytes = messages * blocks *
+    embedding_dim * bytes_per_scalar (costmodel.py:95-103)."""
+    sp = sum(int(np.asarray(lay.key_ncut)[np.asarray(m[d], bool)].sum())
+             for m in spatial_sends for d, lay in enumerate(layouts))
+    tm = sum(int(np.asarray(m[d], bool).sum()) for m in temporal_sends for d in range(len(layouts)))
+    return sp, tm
+
+
+class StaleState:
+    """Cross-epoch state of the B200 step, the role of sim.StaleState
+    (sim.py:306-324): the trainer (parameters, optimizer moments, embedding
+    caches, halo rows, carries, the real epoch-loss trace). Built once from
+    the reference graph + plan (or a PlanArrays) and threaded through
+    simulate_epoch calls."""
+
+    def __init__(self, g, plan=None, profile=None, cluster=None, stale_config=None, seed=0, *,
+                 cfg: DGNNConfig | None = None, F: int | None = None, H: int | None = None,
+                 distributed: bool = False, device=None, cuda_graph: bool = False):
+        from .plan import from_dynpart
+        pa = g if isinstance(g, PlanArrays) else from_dynpart(g, plan)
+        prof = profile.to_dict() if hasattr(profile, "to_dict") else (profile or pa.profile)
+        pa.profile = dict(prof or {})
+        if cfg is None:
+            cfg = DGNNConfig.for_profile(pa.profile, F=F or pa.feature_dim, H=H)
+        self.pa, self.cfg = pa, cfg
+        self.trainer = DGNNTrainer(pa, cfg, stale_config, seed=seed, device=device,
+                                   distributed=distributed, cuda_graph=cuda_graph)
+
+    @property
+    def trace(self):
+        return self.trainer.trace
+
+
+def _check_plan(g, plan, cluster):
+    """The reference's guards (sim.py:433-437), raised before any GPU work."""
+    from .plan import PlanGraphMismatch
+    n_inst = g.n_instances
+    sdev = plan.structure_device if plan is not None else g.structure_device
+    if len(sdev) != n_inst:
+        raise PlanGraphMismatch(f"plan covers {len(sdev)} instances, graph has {n_inst}")
+    n_dev = plan.n_devices if plan is not None else g.n_devices
+    c_dev = getattr(cluster, "n_devices", cluster)
+    if c_dev is not None and int(c_dev) != int(n_dev):
+        raise PlanGraphMismatch("plan and cluster disagree on device count")
+
+
+def simulate_epoch(g, plan, profile=None, cluster=None, stale_config=None, epoch: int = 1,
+                   coeffs=None, stale_state: StaleState | None = None, **kw):
+    """Drop-in for dynpart.sim.simulate_epoch (sim.py:423-432): same
+    positional signature; one REAL training epoch (fwd + bwd + exchange +
+    all-reduce + update) on the B200 step, reported in the reference's
+    EpochReport fields (sim.py:259-303) with measured per-device times,
+    lambda = max/min of the per-device walls (assign.py:98-104) and the
+    reference-billed bytes of the actual send masks. ``g``/``plan``: a dynpart
+    DynamicGraph + Plan (converted unchanged) or a PlanArrays (plan=None).
+    Without ``stale_state`` a fresh state is built (epoch 1 from the initial
+    parameters); threading one state through consecutive epochs trains.
+    ``coeffs`` (the reference's analytic cost coefficients) is unused: times are
+    measured."""
+    _check_plan(g, plan, cluster)
+    state = stale_state if stale_state is not None else StaleState(
+        g, plan, profile, cluster, stale_config, **kw)
+    tr = state.trainer
+    if epoch != tr.epoch_no + 1:
+        raise ValueError(f"epoch {epoch} requested, the state is at epoch {tr.epoch_no}")
+    if stale_config is not None and StaleConfig.coerce(stale_config) != tr.stale:
+        raise ValueError("stale_config differs from the one the state was built with")
+    return tr.run_epoch()
+
+
 def run_epochs(g, plan=None, profile=None, cluster=None, epochs: int = 1, stale_config=None,
                drift_spec=None, seed: int = 0, coeffs=None, initial_loss=None, loss_decay=None,
                *, cfg: DGNNConfig | None = None, F: int | None = None, H: int | None = None,
-               distributed: bool = False, device=None):
+               distributed: bool = False, device=None, cuda_graph: bool = False):
     """Drop-in for dynpart.sim.run_epochs (sim.py:569-599): same positional
-    signature, real training. ``g``/``plan`` may be a dynpart DynamicGraph +
-    Plan (converted unchanged) or a PlanArrays (plan=None). drift_spec,
-    coeffs, initial_loss and loss_decay drive the reference's simulated
-    embeddings/loss and are ignored: the embeddings and the loss trace are real."""
-    from .plan import from_dynpart
-    pa = g if isinstance(g, PlanArrays) else from_dynpart(g, plan)
-    prof = profile.to_dict() if hasattr(profile, "to_dict") else (profile or pa.profile)
-    if cfg is None:
-        cfg = DGNNConfig.for_profile(prof, F=F or pa.feature_dim, H=H)
-    trainer = DGNNTrainer(pa, cfg, stale_config, seed=seed, device=device, distributed=distributed)
-    return [trainer.run_epoch() for _ in range(epochs)]
+    signature, real training through simulate_epoch with one StaleState.
+    drift_spec, coeffs, initial_loss and loss_decay drive the reference's
+    simulated embeddings/loss and are unused: the embeddings and the loss
+    trace are real."""
+    if plan is not None or not isinstance(g, PlanArrays):
+        _check_plan(g, plan, cluster)
+    state = StaleState(g, plan, profile, cluster, stale_config, seed, cfg=cfg, F=F, H=H,
+                       distributed=distributed, device=device, cuda_graph=cuda_graph)
+    return [simulate_epoch(g, plan, profile, cluster, stale_config, r, coeffs, state)
+            for r in range(1, epochs + 1)]

@@ -249,3 +249,40 @@ def test_staged_inputs_equal_resident(graph):
     pa_, pb_ = a.params(0), b.params(0)
     for k in pa_:
         assert np.array_equal(pa_[k], pb_[k]), k
+
+
+@pytest.mark.parametrize("plan,rnn,n_rnn", [("t4", "lstm", 2), ("c1", "gru", 1)])
+def test_simulate_epoch_report_fields(artifacts_dir, plan, rnn, n_rnn):
+    """simulate_epoch (sim.py:423-432 signature) threaded through one StaleState
+    for 3 adaptive-relax epochs: the device-accumulated billing equals the
+    host restatement of the reference accounting (sim.py:464-469) for the
+    GPU's own send masks, per-device times are measured (one per device,
+    compute <= wall) and lambda = max/min of the walls (assign.py:98-104)."""
+    from paper_2309_03523_b200 import DGNNConfig, StaleConfig, load_plan_npz
+    from paper_2309_03523_b200.trainer import StaleState, reference_billed_messages, simulate_epoch
+    pa = load_plan_npz(artifacts_dir / plan / "plan.npz")
+    cfg = DGNNConfig(F=16, H=16, C=16, rnn=rnn, n_rnn=n_rnn, optimizer="adam", lr=1e-2)
+    scfg = StaleConfig.adaptive()
+    state = StaleState(pa, None, pa.profile, pa.n_devices, scfg, cfg=cfg)
+    tr = state.trainer
+    prof = pa.profile
+    per_msg = prof.get("blocks", 1) * prof["embedding_dim"] * prof["bytes_per_scalar"]
+    for r in (1, 2, 3):
+        rep = simulate_epoch(pa, None, pa.profile, pa.n_devices, scfg, r, None, state)
+        sp = [[sh.scache[l].send.cpu().numpy().astype(bool) for sh in tr.shards] for l in range(2)]
+        tm = [[sh.tcache[k].send.cpu().numpy().astype(bool) for sh in tr.shards]
+              for k in range(n_rnn)]
+        n_sp, n_tm = reference_billed_messages(tr.layouts, sp, tm)
+        assert rep.spatial_traffic_bytes == n_sp * per_msg
+        assert rep.temporal_traffic_bytes == n_tm * per_msg
+        assert rep.stale_sent_bytes == (n_sp + n_tm) * per_msg
+        assert len(rep.per_device_wall_ms) == len(rep.per_device_compute_ms) == pa.n_devices
+        assert all(0 < c <= w for c, w in zip(rep.per_device_compute_ms, rep.per_device_wall_ms))
+        assert rep.load_divergence == pytest.approx(max(rep.per_device_wall_ms)
+                                                    / min(rep.per_device_wall_ms))
+        assert rep.exchanged_rows > 0 and rep.exchanged_bytes > 0
+        if r >= 2:
+            assert rep.stale_theta > 0 and rep.stale_d > 0
+    assert rep.stale_avoided_bytes > 0
+    with pytest.raises(ValueError):
+        simulate_epoch(pa, None, pa.profile, pa.n_devices, scfg, 7, None, state)
