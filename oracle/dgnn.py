@@ -186,7 +186,8 @@ class OracleDGNN:
                 for k in np.flatnonzero(f != s):
                     self.tie_log.append(dict(epoch=r, cache=tag, device=d, key=int(k),
                                              dist=float(dd[k]), theta=float(theta),
-                                             scale=float(np.abs(v[k]).max())))
+                                             scale=float(np.abs(v[k]).max()),
+                                             norm=float(np.sqrt((v[k] * v[k]).sum()))))
                 s = f
             c[s] = v[s]
             cc |= s

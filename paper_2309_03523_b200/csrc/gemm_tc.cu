@@ -541,14 +541,40 @@ extern "C" int dgc_gemm_splits(int64_t K, int32_t precision, int32_t k_splits) {
   return kb_per > 0 ? (kb_total + kb_per - 1) / kb_per : 1;
 }
 
+// K == 0 (a device that owns no rows: its weight-gradient contractions are
+// empty): C = (accumulate ? C : 0) + bias, then the epilogue's ReLU mask /
+// output activation, exactly as the tensor-core epilogue would apply them.
+__global__ void gemm_k0_kernel(float* C, int64_t ldc, int64_t M, int64_t N, const float* bias,
+                               const float* relu_src, int accumulate, int out_act) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M * N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / N, c = i % N;
+    float v = accumulate ? C[r * ldc + c] : 0.f;
+    if (bias) v += bias[c];
+    if (relu_src && !(relu_src[r * N + c] > 0.f)) v = 0.f;
+    if (out_act & 1) v = fmaxf(v, 0.f);
+    if (out_act & 2) v = dgc::rna_tf32_f(v);
+    C[r * ldc + c] = v;
+  }
+}
+
 static int gemm_impl(const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                      int64_t ldc, int64_t M, int64_t N, int64_t K, int32_t a_mn, int32_t b_mn,
                      int32_t precision, const float* bias, const float* relu_src,
                      int32_t accumulate, int32_t k_splits, float* partial, float* colsum_partial,
                      const SegOpts& so, void* stream) {
-  DGC_REQUIRE(M >= 0 && N >= 0 && K >= 1, "gemm: bad shape");
+  DGC_REQUIRE(M >= 0 && N >= 0 && K >= 0, "gemm: bad shape");
   const int out_act = (accumulate >> 1) & 3;  // bit 1 ReLU, bit 2 TF32-round the output
   accumulate &= 1;
+  if (K == 0) {
+    if (M == 0 || N == 0) return DGC_OK;
+    DGC_REQUIRE(colsum_partial == nullptr && so.seg_of_mtile == nullptr && so.kitems == nullptr,
+                "gemm: K == 0 supports plain / bias / ReLU-mask epilogues only");
+    gemm_k0_kernel<<<dgc::grid_for(M * N, 256), 256, 0, dgc::as_stream(stream)>>>(
+        C, ldc, M, N, bias, relu_src, accumulate, out_act);
+    DGC_CHECK_LAUNCH("gemm_k0_kernel");
+    return DGC_OK;
+  }
   DGC_REQUIRE(precision == 1 || precision == 3, "gemm: precision must be 1 (TF32) or 3 (3xTF32)");
   DGC_REQUIRE(k_splits >= 1, "gemm: k_splits >= 1");
   if (M == 0 || N == 0) return DGC_OK;

@@ -55,7 +55,7 @@ def oracle_relu_masks(tr, lays):
     out = {0: [], 1: []}
     for i, lay in enumerate(lays):
         gl = tr.layouts[i].own_gid
-        pos = np.full(max(int(gl.max()) + 1, 1), -1, np.int64)
+        pos = np.full(max(int(gl.max(initial=-1)) + 1, 1), -1, np.int64)
         pos[gl[gl >= 0]] = np.flatnonzero(gl >= 0)
         rows = pos[np.asarray(lay.own_gid)]
         assert (rows >= 0).all()
@@ -103,25 +103,57 @@ def test_trainer_single_device_wide(artifacts_dir):
     check_epochs(out, orc=orc)
 
 
-@pytest.mark.parametrize("mode", ["relax", "tighten", "static"])
-def test_trainer_stale_schedule_matches_oracle(artifacts_dir, mode):
+def subsample_plan(pa, t_max):
+    """The plan restricted to snapshots 1..t_max (same devices, chunks and
+    instance order; spatial edges are snapshot-local, temporal links kept when
+    both ends are)."""
+    from paper_2309_03523_b200.plan import PlanArrays
+    keep = pa.inst_t <= t_max
+    new = np.full(pa.n_instances, -1, np.int64)
+    new[keep] = np.arange(int(keep.sum()))
+    se = pa.spatial_edges[keep[pa.spatial_edges].all(axis=1)]
+    tl = pa.temporal_links[keep[pa.temporal_links].all(axis=1)]
+    return PlanArrays(T=t_max, feature_dim=pa.feature_dim, inst_entity=pa.inst_entity[keep],
+                      inst_t=pa.inst_t[keep], spatial_edges=new[se].astype(np.int32),
+                      temporal_links=new[tl].astype(np.int32),
+                      structure_device=pa.structure_device[keep], chunk_of=pa.chunk_of[keep],
+                      n_devices=pa.n_devices, profile=dict(pa.profile), meta=dict(pa.meta))
+
+
+@pytest.mark.parametrize("plan,cfg_kw,mode", [
+    ("t2", dict(F=16, H=16, C=16, rnn="gru", n_rnn=1), "relax"),
+    ("t2", dict(F=16, H=16, C=16, rnn="gru", n_rnn=1), "tighten"),
+    ("t2", dict(F=16, H=16, C=16, rnn="gru", n_rnn=1), "static"),
+    # LSTM temporal carries (h|c, width 2H) through their own caches, D = 4
+    ("t4", dict(F=16, H=16, C=16, rnn="lstm", n_rnn=2), "relax"),
+    ("t4", dict(F=16, H=64, C=16, rnn="lstm", n_rnn=2), "static"),
+    # the C4 sweep's plan (1M x 64, GCN+GRU, D = 8), snapshots 1-6 (40k instances)
+    ("c4d8-sub", dict(F=16, H=16, C=16, rnn="gru", n_rnn=1), "relax"),
+])
+def test_trainer_stale_schedule_matches_oracle(artifacts_dir, plan, cfg_kw, mode):
     from paper_2309_03523_b200 import load_plan_npz
-    pa = load_plan_npz(artifacts_dir / "t2" / "plan.npz")
-    out, tr, orc = run_pair(pa, dict(F=16, H=16, C=16, rnn="gru", n_rnn=1), mode, epochs=4,
-                            fraction=0.3)
+    pa = load_plan_npz(artifacts_dir / plan.split("-")[0] / "plan.npz")
+    if plan.endswith("-sub"):
+        pa = subsample_plan(pa, 6)
+    out, tr, orc = run_pair(pa, cfg_kw, mode, epochs=4, fraction=0.3)
     check_epochs(out, rtol=1e-4, orc=orc)
     for rep, o, _ in out:
         for key, th in o["theta"].items():
             if key in rep.stale_detail["theta"]:
                 assert rep.stale_detail["theta"][key] == pytest.approx(th, rel=1e-4, abs=2e-6)
     # staleness schedule: the GPU's send sets equal the oracle's fp64 decisions
-    # except keys inside the fp32 tie band |dist - theta| <= 1e-5 * |value|
-    # (SURVEY.md §7 (ii)); report the band population.
+    # except keys inside the fp32 tie band (SURVEY.md §7 (ii)). The fp32 distance
+    # of two nearly equal rows carries the rows' absolute rounding (~1e-7 of
+    # their norm each), so the band is |dist - theta| <= 1e-6 * max(1, ||row||);
+    # when the rows barely move (layer-0 embeddings, dist ~ 1e-5) that band is a
+    # few 1e-3 of theta and holds a few tenths of a percent of the keys.
     n_keys = sum(len(sh.key_rows) for sh in tr.shards) * 2 * len(out)
     for t_ in orc.tie_log:
-        assert abs(t_["dist"] - t_["theta"]) <= 1e-5 * max(1.0, t_["scale"]), t_
-    assert len(orc.tie_log) <= max(2, n_keys // 1000), orc.tie_log
+        assert abs(t_["dist"] - t_["theta"]) <= 1e-6 * max(1.0, t_["norm"]), t_
+    assert len(orc.tie_log) <= max(2, n_keys // 100), len(orc.tie_log)
     assert out[-1][0].stale_reduction_pct > 0.0
+    print(f"\n{plan} {mode}: {len(orc.tie_log)} tie-band keys; stale reduction "
+          + ", ".join(f"{rep.stale_reduction_pct:.1f}%" for rep, _, _ in out))
 
 
 @pytest.mark.parametrize("name,H", [("t4", 64), ("t2", 128), ("t2-single", 128)])
