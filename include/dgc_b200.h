@@ -265,6 +265,9 @@ int dgc_rnn_bwd_tc(int32_t cell, const float* U, const int32_t* slot_row,
  * 128 packed rows per tile (single-CTA kernels), or 4*rq rows per 2-CTA
  * cluster (H = 128: rq = ceil(n_rows / 296) rows per TMEM lane quadrant, so
  * the recurrence spans up to 74 clusters = all 148 SMs). */
+/* Save-row width (floats) of the tensor-core LSTM kernels: 3.5 H at H = 128
+ * with the cluster kernels (h_in fp32 | c_in, i, f, g, o fp16), else 7 H. */
+int32_t dgc_rnn_tc_save_floats(int32_t H);
 int64_t dgc_rnn_tc_tiles(int64_t n_rows, int32_t H);
 /* BPTT over the same packing (Ut = U^T, [G*H, H], see dgc_transpose): dh_out [n_inst,H] -> dgx [n_inst,G*H]
  * (d pre-activations; dWx = x^T dgx, db = colsum(dgx), dx = dgx Wx^T,

@@ -60,6 +60,7 @@ _SIGS = {
     "dgc_rnn_bwd": (_i32, [_i32, _p, _p, _p, _i64, _i32, _i32, _p, _p, _p, _p, _p]),
     "dgc_rnn_bwd_tc": (_i32, [_i32, _p, _p, _p, _i64, _i32, _i32, _p, _p, _p, _p, _p, _p]),
     "dgc_rnn_tc_tiles": (_i64, [_i64, _i32]),
+    "dgc_rnn_tc_save_floats": (_i32, [_i32]),
     "dgc_rnn_bwd_partial_rows": (_i64, [_i64, _i32]),
     "dgc_transpose": (_i32, [_p, _i64, _i64, _p, _p]),
     "dgc_stale_distance": (_i32, [_p, _p, _p, _p, _i64, _i32, _p, _p, _p]),

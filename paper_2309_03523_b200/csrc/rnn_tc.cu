@@ -13,9 +13,28 @@
 //           the NEXT position's masked h_in (carry mask, or the cross-device carry
 //           at a run start) straight into the swizzled A tile.
 // The input projection x Wx + b of all slots is one K2 GEMM ahead of this kernel.
+#include <cuda_fp16.h>
+
 #include "tc_common.cuh"
 
 namespace {
+
+// Compact save row of the H = 128 cluster kernels (forward writes, BPTT
+// reads): [h_in fp32 (H) | c_in, i, f, g, o fp16 (5 x H)] = 3.5 H floats per
+// instance (1792 B at H = 128; 16-B multiple, so h_in stays a TMA operand of
+// the stacked weight-gradient GEMM). fp16 keeps the 10 explicit mantissa bits
+// of the TF32 path's operands (gates in (0,1) / (-1,1), |c| <= L), and halves
+// the bytes of the five BPTT-only fields (28 H -> 14 H bytes per instance).
+template <int H> __host__ __device__ constexpr int tc_save_floats() {
+  return H == 128 ? H + 5 * H / 2 : 7 * H;
+}
+__device__ __forceinline__ void sth4(__half* p, float4 v) {
+  const __half2 a = __floats2half2_rn(v.x, v.y), b = __floats2half2_rn(v.z, v.w);
+  uint2 u;
+  u.x = *reinterpret_cast<const uint32_t*>(&a);
+  u.y = *reinterpret_cast<const uint32_t*>(&b);
+  *reinterpret_cast<uint2*>(p) = u;
+}
 
 using namespace dgc::tc;
 using dgc::make_map;
@@ -607,14 +626,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   hn.c = rna_tf32(og.c * tc.c);
           DGC_LSTM_CELL(x) DGC_LSTM_CELL(y) DGC_LSTM_CELL(z) DGC_LSTM_CELL(w)
 #undef DGC_LSTM_CELL
-          float* sv = save + (int64_t)inst * 7 * H + j;
+          constexpr int kSF = tc_save_floats<H>();
+          float* sv = save + (int64_t)inst * kSF + j;
           st4(sv, hin);
-          st4(sv + H, cin);
-          st4(sv + 2 * H, ig);
-          st4(sv + 3 * H, fg);
-          st4(sv + 4 * H, gg);
-          st4(sv + 5 * H, og);
-          if (H != 128) st4(sv + 6 * H, tc);  // H = 128: the cluster BPTT recomputes tanh(c)
+          if (H == 128) {  // compact row: fp16 c_in, i, f, g, o; the BPTT recomputes tanh(c)
+            __half* sh = reinterpret_cast<__half*>(save + (int64_t)inst * kSF + H) + j;
+            sth4(sh, cin);
+            sth4(sh + H, ig);
+            sth4(sh + 2 * H, fg);
+            sth4(sh + 3 * H, gg);
+            sth4(sh + 4 * H, og);
+          } else {
+            st4(sv + H, cin);
+            st4(sv + 2 * H, ig);
+            st4(sv + 3 * H, fg);
+            st4(sv + 4 * H, gg);
+            st4(sv + 5 * H, og);
+            st4(sv + 6 * H, tc);
+          }
           st4(h_out + (int64_t)inst * ld + j, hn);
           // c leaves the kernel only where a run ends (the carries other devices
           // read); inside a run it lives in creg and in the successor's c_in save
@@ -987,6 +1016,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   constexpr int kRQ = ks_recv_rq<kVEW>();    // receive-tile rows per lane quadrant
   constexpr int kRecv = 4 * kRQ * HU;        // floats per receive tile
   constexpr uint32_t kTmemCols = 2 * H;      // two N = H accumulators
+  constexpr int kSF = tc_save_floats<H>();   // compact save row (floats)
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned base, derived from the __shared__ array (keeps shared-space
   // addressing: STS/LDS instead of generic ST/LD)
@@ -1100,22 +1130,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       if (pf && my_inst >= 0) {
         // this row's saved c_in, i, f, g, o and dh_out (the CTA's 64 units) start
         // streaming in while the position waits for its dh partials
-        const float* sv = save + (int64_t)my_inst * 7 * H + 64 * crank;
+        // compact row: the CTA's 64 units of each fp16 field = one 128-B line
+        const __half* sv = reinterpret_cast<const __half*>(save + (int64_t)my_inst * kSF + H) +
+                           64 * crank;
         const float* dd = dh_out + (int64_t)my_inst * H + 64 * crank;
         if (pf == 1) {
 #pragma unroll
-          for (int k = 1; k <= 5; ++k) {
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(sv + k * H));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(sv + k * H + 32));
-          }
+          for (int k = 0; k < 5; ++k) asm volatile("prefetch.global.L2 [%0];" ::"l"(sv + k * H));
           asm volatile("prefetch.global.L2 [%0];" ::"l"(dd));
           asm volatile("prefetch.global.L2 [%0];" ::"l"(dd + 32));
         } else {
 #pragma unroll
-          for (int k = 1; k <= 5; ++k) {
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(sv + k * H));
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(sv + k * H + 32));
-          }
+          for (int k = 0; k < 5; ++k) asm volatile("prefetch.global.L1 [%0];" ::"l"(sv + k * H));
           asm volatile("prefetch.global.L1 [%0];" ::"l"(dd));
           asm volatile("prefetch.global.L1 [%0];" ::"l"(dd + 32));
         }
@@ -1161,7 +1187,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
           if (rb + b * kRB >= rq) continue;  // warp-uniform: no rows left
-          float ld[kRB][5], dhv[kRB];
+          // raw fp16 fields: converted at use, so the loads of all kRB rows are in
+          // flight together (a conversion right after each row's loads would
+          // serialise the rows on the load latency)
+          __half ld[kRB][5];
+          float dhv[kRB];
           int inst[kRB];
 #pragma unroll
           for (int u = 0; u < kRB; ++u) {
@@ -1173,12 +1203,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
                               : 0.f;
             if (inst[u] >= 0) {
               dhv[u] += dh_out[(int64_t)inst[u] * H + j];
-              const float* sv = save + (int64_t)inst[u] * 7 * H + j;
+              const __half* sv = reinterpret_cast<const __half*>(save + (int64_t)inst[u] * kSF + H) + j;
 #pragma unroll
-              for (int k = 0; k < 5; ++k) ld[u][k] = sv[(k + 1) * H];  // c_in, i, f, g, o
+              for (int k = 0; k < 5; ++k) ld[u][k] = sv[k * H];  // c_in, i, f, g, o
             } else {
 #pragma unroll
-              for (int k = 0; k < 5; ++k) ld[u][k] = 0.f;
+              for (int k = 0; k < 5; ++k) ld[u][k] = __ushort_as_half((unsigned short)0);
             }
           }
           if (!slots_free) {
@@ -1198,8 +1228,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
             float da[4] = {0.f, 0.f, 0.f, 0.f};
             float dcp = 0.f;
             if (inst[u] >= 0) {
-              const float c_in = ld[u][0], ig = ld[u][1], fg = ld[u][2], gg = ld[u][3],
-                          og = ld[u][4];
+              const float c_in = __half2float(ld[u][0]), ig = __half2float(ld[u][1]),
+                          fg = __half2float(ld[u][2]), gg = __half2float(ld[u][3]),
+                          og = __half2float(ld[u][4]);
               const float tc = tanh_fast(fg * c_in + ig * gg);  // the forward's tanh(c)
               const float g_ = dhv[u];
               const float d_o = g_ * tc;
@@ -1402,6 +1433,10 @@ extern "C" int dgc_rnn_bwd_tc(int32_t cell_flags, const float* U, const int32_t*
                  : launch_lstm_bwd_tc<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
     default: return dgc::fail(DGC_ERR_ARG, "rnn_bwd_tc: H must be 32, 64 or 128");
   }
+}
+
+extern "C" int32_t dgc_rnn_tc_save_floats(int32_t H) {
+  return (H == 128 && cluster_rnn_enabled()) ? tc_save_floats<128>() : 7 * H;
 }
 
 extern "C" int64_t dgc_rnn_tc_tiles(int64_t n_rows, int32_t H) {

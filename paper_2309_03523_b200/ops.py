@@ -281,6 +281,12 @@ def rnn_fwd_tc(cell, gx, Ut, slot_row, slot_mask, slot_carry, carry, n_rows, row
         "dgc_rnn_fwd_tc"), nb, 2.0 * n_rows * row_len * H * G * H)
 
 
+def rnn_tc_save_floats(H):
+    """Save-row width of the tensor-core LSTM (dgc_rnn_tc_save_floats): 3.5 H
+    (h_in fp32 + five fp16 fields) for the H = 128 cluster kernels, else 7 H."""
+    return _native.lib().dgc_rnn_tc_save_floats(H)
+
+
 def rnn_fwd_tc_fused_available(F, H):
     return bool(_native.lib().dgc_rnn_fwd_tc_fused_available(F, H))
 
@@ -294,10 +300,11 @@ def rnn_fwd_tc_x(x, ldx, WxT, Ut, bias, slot_row, slot_mask, slot_carry, carry, 
     n_inst, F = h_out.shape[0], WxT.shape[1]
     G = 4
     sf = rnn_save_floats(1, H)
-    # reads x (F); writes h_in, c_in, i, f, g, o (tanh(c) is recomputed by the
-    # BPTT), h, and c at the run ends (c_rows of them)
+    # reads x (F); writes the save row (h_in fp32 + c_in, i, f, g, o fp16: sf
+    # floats; tanh(c) is recomputed by the BPTT), h, and c at the run ends
+    sf = rnn_tc_save_floats(H)
     c_rows = n_inst if c_rows is None else c_rows
-    nb = (4 * n_inst * (F + (sf - H) + H) + 4 * c_rows * H + 9 * n_rows * row_len
+    nb = (4 * n_inst * (F + sf + H) + 4 * c_rows * H + 9 * n_rows * row_len
           + 4 * G * H * (H + F))
     _run("lstm_fwd_tc", lambda: _native.check(
         _native.lib().dgc_rnn_fwd_tc_x(1, _p(x), ldx, x.shape[0], F, _p(WxT), _p(Ut), _p(bias),
@@ -312,10 +319,10 @@ def rnn_bwd_tc(cell, U, slot_row, slot_mask, n_rows, row_len, H, save, dh_out, d
     """K4 BPTT on tcgen05 (dgc_rnn_bwd_tc): dh = da U^T on tensor cores."""
     _req(dh_out, torch.float32, "dh_out"); _req(dgx, torch.float32, "dgx")
     n_inst, G = dgx.shape[0], 4
-    # reads the saved c_in, i, f, g, o (+ tanh(c) unless H = 128, where the
-    # cluster kernel recomputes it) and dh; writes dgx
-    n_saved = 5 if H == 128 else 6
-    nb = 4 * n_inst * (G * H + n_saved * H + H) + 5 * n_rows * row_len + 4 * G * H * H
+    # reads the saved c_in, i, f, g, o (fp16 in the H = 128 cluster kernel, which
+    # recomputes tanh(c); fp32 + tanh(c) otherwise) and dh; writes dgx
+    saved_bytes = 2 * 5 * H if rnn_tc_save_floats(H) < 7 * H else 4 * 6 * H
+    nb = n_inst * (4 * G * H + saved_bytes + 4 * H) + 5 * n_rows * row_len + 4 * G * H * H
     _run("lstm_bwd_tc", lambda: _native.check(
         _native.lib().dgc_rnn_bwd_tc(cell, _p(U), _p(slot_row), _p(slot_mask), n_rows, row_len, H,
                                      _p(save), _p(dh_out), _p(dgx), _p(dc_scratch),

@@ -241,7 +241,11 @@ class Shard:
         self.hw = cfg.carry_width
         self.gx = torch.zeros((n, GH), **f32)
         self.hbuf = [torch.zeros((n, self.hw), **f32) for _ in range(cfg.n_rnn)]
-        self.sf = ops.rnn_save_floats(0 if cfg.rnn == "gru" else 1, H)
+        # tensor-core recurrence: TF32 mode, LSTM, H in {32, 64, 128}
+        self.tc_rnn = (cfg.precision == "tf32" and cfg.rnn == "lstm" and H in (32, 64, 128)
+                       and os.environ.get("DGC_TC_RNN", "1") != "0")
+        self.sf = (ops.rnn_tc_save_floats(H) if self.tc_rnn
+                   else ops.rnn_save_floats(0 if cfg.rnn == "gru" else 1, H))
         self.save = [torch.zeros((n, self.sf), **f32) for _ in range(cfg.n_rnn)]
         self.carry = [torch.zeros((max(lay.n_carry, 1), self.hw), **f32) for _ in range(cfg.n_rnn)]
         self.logits = torch.zeros((n, cfg.C), **f32)
@@ -251,9 +255,6 @@ class Shard:
         self.dh2 = torch.zeros((n, H), **f32)
         self.dgx = torch.zeros((n, GH), **f32)
         self.Ut = torch.zeros((GH, H), **f32)
-        # tensor-core recurrence: TF32 mode, LSTM, H in {32, 64, 128}
-        self.tc_rnn = (cfg.precision == "tf32" and cfg.rnn == "lstm" and H in (32, 64, 128)
-                       and os.environ.get("DGC_TC_RNN", "1") != "0")
         self.Ut_f = [torch.zeros((GH, H), **f32) for _ in range(cfg.n_rnn)] if self.tc_rnn else None
         # fused input projection (F = H = 128 cluster recurrence): no gx tensor
         self.fused_xproj = (self.tc_rnn and cfg.rnn == "lstm" and self.R > 0

@@ -409,6 +409,32 @@ def test_softmax_xent_colsum_optimizers():
     close(pd.cpu().numpy(), ref, 1e-6, "adam")
 
 
+def tc_save_decode(save, H):
+    """The tensor-core LSTM save rows as [n, 6H] fp32 (h_in, c_in, i, f, g, o):
+    the compact H = 128 cluster layout (h_in fp32 | five fp16 fields, 3.5 H
+    floats per row) or the 7 H fp32 layout."""
+    from paper_2309_03523_b200 import ops
+    save = np.ascontiguousarray(save, np.float32)
+    sf = ops.rnn_tc_save_floats(H)
+    if sf == 7 * H:
+        return save[:, :6 * H]
+    half = save[:, H:sf].copy().view(np.float16).astype(np.float32)  # [n, 5H]
+    return np.concatenate([save[:, :H], half], 1)
+
+
+def tc_save_encode(fields, H):
+    """Inverse of tc_save_decode for [n, 7H] fp32 inputs (tanh(c) dropped when compact)."""
+    from paper_2309_03523_b200 import ops
+    sf = ops.rnn_tc_save_floats(H)
+    if sf == 7 * H:
+        return np.ascontiguousarray(fields, np.float32)
+    n = fields.shape[0]
+    out = np.zeros((n, sf), np.float32)
+    out[:, :H] = fields[:, :H]
+    out[:, H:] = np.ascontiguousarray(fields[:, H:6 * H].astype(np.float16)).view(np.float32)
+    return out
+
+
 def run_end_rows(slot_row, mask):
     """Instances at the last slot of their run (next slot absent or not continuing)."""
     sr = np.asarray(slot_row).reshape(mask.shape)
@@ -443,7 +469,7 @@ def test_lstm_fwd_tensor_core_matches_simt(H, ew16, monkeypatch):
     outs = []
     for tc in (False, True):
         hc = torch.zeros((n, 2 * H), device=dev)
-        save = torch.zeros((n, 7 * H), device=dev)
+        save = torch.zeros((n, ops.rnn_tc_save_floats(H) if tc else 7 * H), device=dev)
         args = (t(gx), None, t(slot_row.reshape(-1), torch.int32), t(mask.reshape(-1), torch.uint8),
                 t(slot_carry.reshape(-1), torch.int32), t(carry), R, L, H, 2 * H, hc, hc[:, H:], save)
         if tc:
@@ -452,15 +478,15 @@ def test_lstm_fwd_tensor_core_matches_simt(H, ew16, monkeypatch):
         else:
             ops.rnn_fwd(1, args[0], t(U), *args[2:])
         torch.cuda.synchronize()
-        outs.append((hc.cpu().numpy(), save.cpu().numpy()))
+        sv = save.cpu().numpy()
+        outs.append((hc.cpu().numpy(), tc_save_decode(sv, H) if tc else sv[:, :6 * H]))
     # the cluster forward (H = 128) writes c only at run ends (the carries)
     ends = run_end_rows(slot_row, mask)
     close(outs[1][0][:, :H], outs[0][0][:, :H], 2e-3, "lstm tc h")
     close(outs[1][0][ends, H:], outs[0][0][ends, H:], 2e-3, "lstm tc c at run ends")
-    # the H = 128 cluster forward leaves the tanh(c) field (6) unwritten: its BPTT
-    # recomputes tanh(f c_in + i g) from the saved c_in, i, f, g
-    nf = 6 if H == 128 else 7
-    close(outs[1][1][:, :nf * H], outs[0][1][:, :nf * H], 2e-3, "lstm tc save")
+    # h_in .. o (the H = 128 cluster forward stores no tanh(c): its BPTT recomputes
+    # tanh(f c_in + i g), and keeps c_in, i, f, g, o in fp16)
+    close(outs[1][1], outs[0][1], 2e-3, "lstm tc save")
 
 
 @pytest.mark.parametrize("n_seq,carry_frac", [(700, 0.3), (9000, 0.0), (16000, 0.1)])
@@ -502,7 +528,7 @@ def test_lstm_fwd_fused_projection_matches_two_step(n_seq, carry_frac):
     outs = []
     for fused in (False, True):
         hc = torch.zeros((n, 2 * H), device=dev)
-        save = torch.zeros((n, 7 * H), device=dev)
+        save = torch.zeros((n, ops.rnn_tc_save_floats(H)), device=dev)
         if fused:
             ops.rnn_fwd_tc_x(x, 2 * H, WxT, Ut, b, sr, sm, sc, carry, R, L, H, 2 * H, hc, hc[:, H:],
                              save)
@@ -515,7 +541,7 @@ def test_lstm_fwd_fused_projection_matches_two_step(n_seq, carry_frac):
     close(outs[1][0], outs[0][0], 2e-3, "fused h|c")  # TF32 operand rounding differs
     ends = run_end_rows(slot_row, mask)
     assert np.abs(outs[1][0][ends, H:]).max() > 0  # c written at every run end
-    close(outs[1][1][:, :6 * H], outs[0][1][:, :6 * H], 2e-3, "fused save")
+    close(tc_save_decode(outs[1][1], H), tc_save_decode(outs[0][1], H), 2e-3, "fused save")
 
 
 @pytest.mark.parametrize("H,ew16", [(32, False), (64, False), (128, False), (128, True)])
@@ -548,7 +574,8 @@ def test_lstm_bwd_tensor_core_matches_simt(H, ew16, monkeypatch):
             tiles = ops.rnn_tc_tiles(R, H)
             bp = torch.zeros((tiles, 4 * H), device=dev)
             scr = torch.zeros(((R + 127) // 128 * 128, H), device=dev)
-            ops.rnn_bwd_tc(1, t(U), sr, sm, R, L, H, t(save), t(dh), dgx, scr, bias_partial=bp)
+            ops.rnn_bwd_tc(1, t(U), sr, sm, R, L, H, t(tc_save_encode(save, H)), t(dh), dgx, scr,
+                           bias_partial=bp)
             bias = bp.sum(0)
         else:
             rows = ops.rnn_bwd_partial_rows(R, H)
