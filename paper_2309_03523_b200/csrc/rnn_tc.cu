@@ -20,20 +20,30 @@
 namespace {
 
 // Compact save row of the H = 128 cluster kernels (forward writes, BPTT
-// reads): [h_in fp32 (H) | c_in, i, f, g, o fp16 (5 x H)] = 3.5 H floats per
-// instance (1792 B at H = 128; 16-B multiple, so h_in stays a TMA operand of
-// the stacked weight-gradient GEMM). fp16 keeps the 10 explicit mantissa bits
-// of the TF32 path's operands (gates in (0,1) / (-1,1), |c| <= L), and halves
-// the bytes of the five BPTT-only fields (28 H -> 14 H bytes per instance).
+// reads): [h_in fp32 (H) | c_in fp16 (H) | i, f, g, o fp16 interleaved per unit
+// (4 H: unit j at halves 4j .. 4j+3)] = 3.5 H floats per instance (1792 B at
+// H = 128; 16-B multiple, so h_in stays a TMA operand of the stacked
+// weight-gradient GEMM). fp16 keeps the 10 explicit mantissa bits of the TF32
+// path's operands (gates in (0,1) / (-1,1), |c| <= L). Interleaving the gates
+// makes a BPTT lane's four units one 32-B load and the forward's one 32-B store.
 template <int H> __host__ __device__ constexpr int tc_save_floats() {
   return H == 128 ? H + 5 * H / 2 : 7 * H;
 }
+__device__ __forceinline__ uint32_t h2u(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
 __device__ __forceinline__ void sth4(__half* p, float4 v) {
-  const __half2 a = __floats2half2_rn(v.x, v.y), b = __floats2half2_rn(v.z, v.w);
-  uint2 u;
-  u.x = *reinterpret_cast<const uint32_t*>(&a);
-  u.y = *reinterpret_cast<const uint32_t*>(&b);
-  *reinterpret_cast<uint2*>(p) = u;
+  *reinterpret_cast<uint2*>(p) = make_uint2(h2u(v.x, v.y), h2u(v.z, v.w));
+}
+// the gates of 4 consecutive units, interleaved: 32 B at p (16-B aligned)
+__device__ __forceinline__ void st_ifgo(__half* p, float4 i, float4 f, float4 g, float4 o) {
+  uint4* q = reinterpret_cast<uint4*>(p);
+  q[0] = make_uint4(h2u(i.x, f.x), h2u(g.x, o.x), h2u(i.y, f.y), h2u(g.y, o.y));
+  q[1] = make_uint4(h2u(i.z, f.z), h2u(g.z, o.z), h2u(i.w, f.w), h2u(g.w, o.w));
+}
+__device__ __forceinline__ float2 u2h(uint32_t u) {
+  return __half22float2(*reinterpret_cast<const __half2*>(&u));
 }
 
 using namespace dgc::tc;
@@ -66,7 +76,7 @@ __device__ __forceinline__ float rna_tf32(float x) {
 // [p][0] MMA issue start, [p][1] accumulator ready, [p][2] epilogue done.
 // Compiled in only with -DDGC_LSTM_TIMESTAMPS (make DGC_TS=1): the production
 // kernels carry no probe.
-__device__ unsigned long long g_lstm_ts[256][3];
+__device__ unsigned long long g_lstm_ts[256][8];
 #ifdef DGC_LSTM_TIMESTAMPS
 #define DGC_TS(cond, p, k) \
   do {                     \
@@ -630,12 +640,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           float* sv = save + (int64_t)inst * kSF + j;
           st4(sv, hin);
           if (H == 128) {  // compact row: fp16 c_in, i, f, g, o; the BPTT recomputes tanh(c)
-            __half* sh = reinterpret_cast<__half*>(save + (int64_t)inst * kSF + H) + j;
-            sth4(sh, cin);
-            sth4(sh + H, ig);
-            sth4(sh + 2 * H, fg);
-            sth4(sh + 3 * H, gg);
-            sth4(sh + 4 * H, og);
+            __half* sh = reinterpret_cast<__half*>(save + (int64_t)inst * kSF + H);
+            sth4(sh + j, cin);
+            st_ifgo(sh + H + 4 * j, ig, fg, gg, og);
           } else {
             st4(sv + H, cin);
             st4(sv + 2 * H, ig);
@@ -665,6 +672,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
 #pragma unroll
         for (int gi = 0; gi < 4; ++gi) xg[gi] = xn[gi];
         __syncwarp();
+        DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && p < 256 && ch < 3, p, 3 + ch);
       }
       DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && p < 256, p, 2);
       fence_before();
@@ -980,10 +988,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 // A ring stays CTA-local (local arrivals, no cluster-scope fences). The two
 // CTAs then swap the halves that belong to the other CTA's units: 8 rows x H/2
 // floats per epilogue warp through st.async + complete_tx into the peer's
-// double-buffered receive tile (32 KB per position), and each CTA adds its own
-// half (TMEM) and the received half. 16 epilogue warps (4 per TMEM lane
-// quadrant, 8 rows each; lane = unit in the BPTT math), carried dc in
-// registers, rq rows per lane quadrant as the forward.
+// double-buffered receive tile, and each CTA adds its own half (TMEM, staged in
+// shared memory) and the received half. rq rows per lane quadrant as the
+// forward; 8 rows per epilogue warp (12 warps when rq <= 24, else 16).
+// Vectorised epilogue: a lane owns 4 consecutive units of 2 rows per 32-unit
+// chunk (lane = 4 rows x 8 unit quads), so its saved gates are one 32-B load
+// (the interleaved compact row), c_in 8 B, dh_out / dgx / the da A-tile 16-B
+// vectors; in the 12-warp variant every load of a position is issued at its
+// start, under the wait for the position's dh partials. Carried dc in registers.
 // A-ring depth and receive-tile rows per lane quadrant: the 12-warp variant
 // (rq <= 24) sizes the receive tiles for 24 rows and spends the freed shared
 // memory on 6 A stages, so the second chunk's da rarely waits for the MMA to
@@ -991,27 +1003,27 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 template <int kVEW> __host__ __device__ constexpr int ks_a_stages() { return kVEW <= 12 ? 6 : 4; }
 template <int kVEW> __host__ __device__ constexpr int ks_recv_rq() { return kVEW <= 12 ? 24 : 32; }
 constexpr int kKsBStages = 3;
+constexpr int kKsStgStride = 64 + 4;  // own-half staging row stride (floats, 16-B aligned)
 template <int H, int kVEW>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
     lstm_bwd_tc2k_kernel(const __grid_constant__ CUtensorMap tmU, const int32_t* __restrict__ slot_row,
                          const uint8_t* __restrict__ slot_mask, int64_t R, int L,
                          const float* __restrict__ save, const float* __restrict__ dh_out,
-                         float* __restrict__ dgx, int rnd_pf, float* __restrict__ bias_partial,
+                         float* __restrict__ dgx, int rnd, float* __restrict__ bias_partial,
                          int rq) {
   static_assert(H == 128, "K-split cluster BPTT is specialised for H = 128");
-  const int rnd = rnd_pf & 1, pf = (rnd_pf >> 1) & 3;  // pf: 1 = L2, 2 = L1 prefetch of the saves
   constexpr int EW = kVEW;
   constexpr int kEpiT = 32 * EW;
-  constexpr int RPW = 8;                     // rows per warp (4 warps per quadrant)
-  constexpr int kRB = kVEW <= 12 ? 8 : 4;    // rows per load batch (register budget)
-  constexpr int NB = RPW / kRB;
+  constexpr int RPW = 8;                     // rows per warp
+  constexpr bool kHoist = EW <= 12;          // all of a position's loads issued at its start
   constexpr int G4 = 4 * H;
   constexpr int HU = H / 2;
   constexpr int KBO = 8;                     // own da k-blocks per position
   constexpr int kAStage = BM * 128;          // 128 rows x 32 gate columns
   constexpr int kBStage = H * 128;           // H units x 32 gate columns of U
-  constexpr int kS = HU + 1;                 // own-half staging row stride (floats)
+  constexpr int kS = kKsStgStride;
   constexpr int kStgW = RPW * kS;
+  static_assert(kStgW >= 8 * 32, "staging must hold the warp's bias partials");
   constexpr int kKsAStages = ks_a_stages<kVEW>();
   constexpr int kRQ = ks_recv_rq<kVEW>();    // receive-tile rows per lane quadrant
   constexpr int kRecv = 4 * kRQ * HU;        // floats per receive tile
@@ -1104,184 +1116,231 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
     const int ew = warp - 2;
     const int q = warp & 3;                 // TMEM lane quadrant (warp id % 4)
     const int rb = (ew >> 2) * RPW;         // first quadrant row of this warp
-    float* stg = stg_all + ew * kStgW;
+    const int r4 = lane >> 3, u8 = lane & 7;  // vector lane: rows rb + 4 it + r4, units 4 u8 .. +3
+    const uint32_t stg_s = smem_u32(stg_all + ew * kStgW);
+    const uint32_t sA_s = smem_u32(sA), recv_s = smem_u32(recv);
     const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
     const uint32_t recv_peer = map_peer(recv, peer);
     const uint32_t rfull_peer = map_peer(recv_full, peer);
-    const int64_t my_row = row0 + q * rq + lane;  // lane = quadrant row
-    const bool my_ok = lane < rq && my_row < R;
     const bool active = rb < rq;
     // bytes the peer sends into our receive tile per position: 8 rows x HU per
     // active peer warp (4 quadrants x ceil(rq / 8) warps)
     const uint32_t kRecvBytes = 4u * (uint32_t)((rq + RPW - 1) / RPW) * RPW * HU * 4u;
-    float bsum[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-    float dcr[2][RPW];
+    int sbase[2];  // first slot of each of this lane's rows (R * L < 2^31), -1: no row
+    int inst[2], mk[2];
 #pragma unroll
-    for (int lc = 0; lc < 2; ++lc)
+    for (int it = 0; it < 2; ++it) {
+      const int rl = rb + 4 * it + r4;
+      const int64_t vrow = row0 + q * rq + rl;
+      sbase[it] = (rl < rq && vrow < R) ? (int)(vrow * L) : -1;
+      inst[it] = sbase[it] >= 0 ? slot_row[sbase[it] + L - 1] : -1;
+      mk[it] = sbase[it] >= 0 ? slot_mask[sbase[it] + L - 1] : 0;
+    }
+    float mnext[2] = {0.f, 0.f};
+    float4 bsum[2][4], dcr[2][2];
 #pragma unroll
-      for (int u = 0; u < RPW; ++u) dcr[lc][u] = 0.f;
+    for (int lc = 0; lc < 2; ++lc) {
+#pragma unroll
+      for (int g = 0; g < 4; ++g) bsum[lc][g] = zero4();
+      dcr[lc][0] = dcr[lc][1] = zero4();
+    }
+    // this lane's saved fields of (chunk lc, row it): dh_out (4 units), c_in, i/f/g/o
+    auto load_fields = [&](int lc, int it, float4& dho, uint2& cv, uint4& g0, uint4& g1) {
+      const int j = u0 + 32 * lc + 4 * u8;
+      if (inst[it] >= 0) {
+        dho = ldg4(dh_out + (int64_t)inst[it] * H + j);
+        const __half* sv = reinterpret_cast<const __half*>(save + (int64_t)inst[it] * kSF + H);
+        cv = __ldg(reinterpret_cast<const uint2*>(sv + j));
+        g0 = __ldg(reinterpret_cast<const uint4*>(sv + H + 4 * j));
+        g1 = __ldg(reinterpret_cast<const uint4*>(sv + H + 4 * j + 8));
+      } else {
+        dho = zero4();
+        cv = make_uint2(0u, 0u);
+        g0 = g1 = make_uint4(0u, 0u, 0u, 0u);
+      }
+    };
     for (int t = 0; t < L; ++t) {
       const int p = L - 1 - t;
       const bool has_next = p + 1 < L;
-      const int64_t my_s = my_row * L + p;
-      const int my_inst = my_ok ? slot_row[my_s] : -1;
-      const float my_m = my_ok ? (float)slot_mask[my_s] : 0.f;
-      const float my_mnext = (has_next && my_ok) ? (float)slot_mask[my_s + 1] : 0.f;
-      if (pf && my_inst >= 0) {
-        // this row's saved c_in, i, f, g, o and dh_out (the CTA's 64 units) start
-        // streaming in while the position waits for its dh partials
-        // compact row: the CTA's 64 units of each fp16 field = one 128-B line
-        const __half* sv = reinterpret_cast<const __half*>(save + (int64_t)my_inst * kSF + H) +
-                           64 * crank;
-        const float* dd = dh_out + (int64_t)my_inst * H + 64 * crank;
-        if (pf == 1) {
+      DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 0);
+      float4 dho[2][2];
+      uint2 cvv[2][2];
+      uint4 gv0[2][2], gv1[2][2];
+      if (kHoist) {  // chunk 0 now; chunk 1's lines into L2 (loaded before chunk 1's math)
 #pragma unroll
-          for (int k = 0; k < 5; ++k) asm volatile("prefetch.global.L2 [%0];" ::"l"(sv + k * H));
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(dd));
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(dd + 32));
-        } else {
-#pragma unroll
-          for (int k = 0; k < 5; ++k) asm volatile("prefetch.global.L1 [%0];" ::"l"(sv + k * H));
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(dd));
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(dd + 32));
+        for (int it = 0; it < 2; ++it) {
+          load_fields(0, it, dho[0][it], cvv[0][it], gv0[0][it], gv1[0][it]);
+          if (inst[it] >= 0) {
+            const int j = u0 + 32 + 4 * u8;
+            const __half* sv = reinterpret_cast<const __half*>(save + (int64_t)inst[it] * kSF + H);
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(sv + H + 4 * j));
+            if (u8 == 0) {
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(sv + j));
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(dh_out + (int64_t)inst[it] * H + j));
+            }
+          }
         }
       }
-      DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 0);
-      const float* rv = recv + (t & 1) * kRecv;
+      // the next position's slots (consumed one position later)
+      int n_inst[2], n_mk[2];
+#pragma unroll
+      for (int it = 0; it < 2; ++it) {
+        const bool ok = sbase[it] >= 0 && p > 0;
+        n_inst[it] = ok ? slot_row[sbase[it] + p - 1] : -1;
+        n_mk[it] = ok ? slot_mask[sbase[it] + p - 1] : 0;
+      }
+      DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 6);
       if (has_next) {
         if (ew == 0 && lane == 0) mbar_arrive_expect_tx(&recv_full[t & 1], kRecvBytes);
         mbar_wait(&acc_full[(p + 1) & 1], ((t - 1) >> 1) & 1);
         fence_after();
         DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 1);
         if (active) {
-          // partial dh of this warp's 8 rows: own units -> staging, the peer's
-          // units -> the peer's receive tile (thread = row = TMEM lane)
-          float v[64];
+          // partial dh of this warp's 8 rows (thread = row = TMEM lane): own
+          // units -> staging, the peer's units -> the peer's receive tile
           const uint32_t ta = tl + ((p + 1) & 1) * H;
-          tmem_ld16x4(ta + u0, ta + u0 + 16, ta + u0 + 32, ta + u0 + 48, v);
-          if (lane >= rb && lane < rb + RPW) {
-            float* d = stg + (lane - rb) * kS;
+          const bool mine = lane >= rb && lane < rb + RPW;
 #pragma unroll
-            for (int u = 0; u < HU; ++u) d[u] = v[u];
+          for (int h4 = 0; h4 < 4; ++h4) {
+            float v[16];
+            tmem_ld16(ta + u0 + 16 * h4, v);
+            if (mine) {
+              const uint32_t d = stg_s + (uint32_t)(((lane - rb) * kS + 16 * h4) * 4);
+#pragma unroll
+              for (int u = 0; u < 16; u += 4)
+                sts4(d + u * 4, make_float4(v[u], v[u + 1], v[u + 2], v[u + 3]));
+            }
           }
-          tmem_ld16x4(ta + pu0, ta + pu0 + 16, ta + pu0 + 32, ta + pu0 + 48, v);
-          if (lane >= rb && lane < rb + RPW) {
-            const uint32_t dst = recv_peer + (uint32_t)(((t & 1) * kRecv + (q * kRQ + lane) * HU) * 4);
 #pragma unroll
-            for (int u = 0; u < HU; u += 4)
-              st_async_v4(dst + u * 4, make_float4(v[u], v[u + 1], v[u + 2], v[u + 3]),
-                          rfull_peer + (uint32_t)((t & 1) * 8));
+          for (int h4 = 0; h4 < 4; ++h4) {
+            float v[16];
+            tmem_ld16(ta + pu0 + 16 * h4, v);
+            if (mine) {
+              const uint32_t dst =
+                  recv_peer + (uint32_t)(((t & 1) * kRecv + (q * kRQ + lane) * HU + 16 * h4) * 4);
+#pragma unroll
+              for (int u = 0; u < 16; u += 4)
+                st_async_v4(dst + u * 4, make_float4(v[u], v[u + 1], v[u + 2], v[u + 3]),
+                            rfull_peer + (uint32_t)((t & 1) * 8));
+            }
           }
         }
         fence_before();
         mbar_arrive(&acc_empty[(p + 1) & 1]);  // this accumulator is fully read
+        DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 3);
         mbar_wait(&recv_full[t & 1], ((t - 1) >> 1) & 1);
+        DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 4);
         __syncwarp();
       }
 #pragma unroll
       for (int lc = 0; lc < 2; ++lc) {
-        const int c = 2 * (int)crank + lc;   // global 32-unit chunk
-        const int j = 32 * c + lane;         // this lane's hidden unit
         const int seq0 = t * KBO + lc * 4;
-        bool slots_free = false;  // ring slots are awaited once the first loads are in flight
+        const int jo = 32 * lc + 4 * u8;     // own unit index of this lane's 4 units
+        if (!kHoist || lc == 1) {
 #pragma unroll
-        for (int b = 0; b < NB; ++b) {
-          if (rb + b * kRB >= rq) continue;  // warp-uniform: no rows left
-          // raw fp16 fields: converted at use, so the loads of all kRB rows are in
-          // flight together (a conversion right after each row's loads would
-          // serialise the rows on the load latency)
-          __half ld[kRB][5];
-          float dhv[kRB];
-          int inst[kRB];
+          for (int it = 0; it < 2; ++it)
+            load_fields(lc, it, dho[lc][it], cvv[lc][it], gv0[lc][it], gv1[lc][it]);
+        }
 #pragma unroll
-          for (int u = 0; u < kRB; ++u) {
-            const int rl = rb + b * kRB + u;
-            inst[u] = __shfl_sync(0xffffffffu, my_inst, rl);
-            const float mn = __shfl_sync(0xffffffffu, my_mnext, rl);
-            dhv[u] = has_next ? mn * (stg[(b * kRB + u) * kS + 32 * lc + lane] +
-                                      rv[(q * kRQ + rl) * HU + 32 * lc + lane])
-                              : 0.f;
-            if (inst[u] >= 0) {
-              dhv[u] += dh_out[(int64_t)inst[u] * H + j];
-              const __half* sv = reinterpret_cast<const __half*>(save + (int64_t)inst[u] * kSF + H) + j;
+        for (int g = 0; g < 4; ++g) {
+          const int seq = seq0 + g;
+          mbar_wait(&a_empty[seq % kKsAStages], ((seq / kKsAStages) & 1) ^ 1);
+        }
 #pragma unroll
-              for (int k = 0; k < 5; ++k) ld[u][k] = sv[k * H];  // c_in, i, f, g, o
-            } else {
 #pragma unroll
-              for (int k = 0; k < 5; ++k) ld[u][k] = __ushort_as_half((unsigned short)0);
-            }
+        for (int it = 0; it < 2; ++it) {
+          const int rl = rb + 4 * it + r4;
+          const int r = q * 32 + rl;
+          float4 dh = zero4();
+          if (has_next) {
+            const float4 a = lds4(stg_s + (uint32_t)(((4 * it + r4) * kS + jo) * 4));
+            const float4 b = lds4(recv_s + (uint32_t)((((t & 1) * kRecv) + (q * kRQ + rl) * HU + jo) * 4));
+            const float mn = mnext[it];
+            dh = make_float4(mn * (a.x + b.x), mn * (a.y + b.y), mn * (a.z + b.z), mn * (a.w + b.w));
           }
-          if (!slots_free) {
+          float4 da[4] = {zero4(), zero4(), zero4(), zero4()};
+          float4 dcp = zero4();
+          if (inst[it] >= 0) {
+            const float4 ho = dho[lc][it];
+            dh = make_float4(dh.x + ho.x, dh.y + ho.y, dh.z + ho.z, dh.w + ho.w);
+            const float2 c01 = u2h(cvv[lc][it].x), c23 = u2h(cvv[lc][it].y);
+            const float cin[4] = {c01.x, c01.y, c23.x, c23.y};
+            const uint32_t gw[8] = {gv0[lc][it].x, gv0[lc][it].y, gv0[lc][it].z, gv0[lc][it].w,
+                                    gv1[lc][it].x, gv1[lc][it].y, gv1[lc][it].z, gv1[lc][it].w};
+            const float dhk[4] = {dh.x, dh.y, dh.z, dh.w};
+            const float dck[4] = {dcr[lc][it].x, dcr[lc][it].y, dcr[lc][it].z, dcr[lc][it].w};
+            const float mp = (float)mk[it];
+            float dak[4][4], dcpk[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float2 if_ = u2h(gw[2 * k]), go = u2h(gw[2 * k + 1]);
+              const float ig = if_.x, fg = if_.y, gg = go.x, og = go.y;
+              const float tc = tanh_fast(fg * cin[k] + ig * gg);  // the forward's tanh(c)
+              const float g_ = dhk[k];
+              const float d_o = g_ * tc;
+              const float dcn = dck[k] + g_ * og * (1.f - tc * tc);
+              dak[0][k] = dcn * gg * ig * (1.f - ig);
+              dak[1][k] = dcn * cin[k] * fg * (1.f - fg);
+              dak[2][k] = dcn * ig * (1.f - gg * gg);
+              dak[3][k] = d_o * og * (1.f - og);
+              dcpk[k] = dcn * fg * mp;
+            }
+            dcp = make_float4(dcpk[0], dcpk[1], dcpk[2], dcpk[3]);
+            float* o = dgx + (int64_t)inst[it] * G4 + u0 + jo;
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
-              const int seq = seq0 + g;
-              mbar_wait(&a_empty[seq % kKsAStages], ((seq / kKsAStages) & 1) ^ 1);
+              float4 v = make_float4(dak[g][0], dak[g][1], dak[g][2], dak[g][3]);
+              if (rnd) v = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
+              da[g] = v;
+              st4(o + g * H, v);
+              bsum[lc][g] = make_float4(bsum[lc][g].x + v.x, bsum[lc][g].y + v.y,
+                                        bsum[lc][g].z + v.z, bsum[lc][g].w + v.w);
             }
-            slots_free = true;
           }
+          dcr[lc][it] = dcp;
+          const uint32_t off0 = sw128_offset(r, 4 * u8);
 #pragma unroll
-          for (int u = 0; u < kRB; ++u) {
-            const int rl = rb + b * kRB + u;
-            const int r = q * 32 + rl;
-            const float mp = __shfl_sync(0xffffffffu, my_m, rl);
-            float& dc = dcr[lc][b * kRB + u];
-            float da[4] = {0.f, 0.f, 0.f, 0.f};
-            float dcp = 0.f;
-            if (inst[u] >= 0) {
-              const float c_in = __half2float(ld[u][0]), ig = __half2float(ld[u][1]),
-                          fg = __half2float(ld[u][2]), gg = __half2float(ld[u][3]),
-                          og = __half2float(ld[u][4]);
-              const float tc = tanh_fast(fg * c_in + ig * gg);  // the forward's tanh(c)
-              const float g_ = dhv[u];
-              const float d_o = g_ * tc;
-              const float dcn = dc + g_ * og * (1.f - tc * tc);
-              da[0] = dcn * gg * ig * (1.f - ig);
-              da[1] = dcn * c_in * fg * (1.f - fg);
-              da[2] = dcn * ig * (1.f - gg * gg);
-              da[3] = d_o * og * (1.f - og);
-              dcp = dcn * fg * mp;
-              float* o = dgx + (int64_t)inst[u] * G4 + j;
-#pragma unroll
-              for (int g = 0; g < 4; ++g) {
-                if (rnd) da[g] = rna_tf32(da[g]);
-                o[g * H] = da[g];
-                bsum[lc][g] += da[g];
-              }
-            }
-            dc = dcp;
-            const uint32_t off0 = sw128_offset(r, lane);
-#pragma unroll
-            for (int g = 0; g < 4; ++g)
-              *reinterpret_cast<float*>(sA + ((seq0 + g) % kKsAStages) * kAStage + off0) = da[g];
-          }
-        }
-        if (!slots_free) {  // no rows in this warp: keep the a_empty -> a_full phase order
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            const int seq = seq0 + g;
-            mbar_wait(&a_empty[seq % kKsAStages], ((seq / kKsAStages) & 1) ^ 1);
-          }
+          for (int g = 0; g < 4; ++g)
+            sts4(sA_s + (uint32_t)(((seq0 + g) % kKsAStages) * kAStage) + off0, da[g]);
         }
         fence_async_smem();
         DGC_TS(lc == 1 && blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 2);
+        DGC_TS(lc == 0 && blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 5);
 #pragma unroll
         for (int g = 0; g < 4; ++g) mbar_arrive(&a_full[(seq0 + g) % kKsAStages]);
         __syncwarp();
       }
+#pragma unroll
+      for (int it = 0; it < 2; ++it) {
+        mnext[it] = (float)mk[it];
+        inst[it] = n_inst[it];
+        mk[it] = n_mk[it];
+      }
     }
-    if (bias_partial) {  // combine the EW warps in fixed order
-      for (int lc = 0; lc < 2; ++lc) {
-        const int c = 2 * (int)crank + lc;
+    if (bias_partial) {
+      // the 4 row lanes of each unit quad (xor 8, 16), then the EW warps in fixed order
+#pragma unroll
+      for (int lc = 0; lc < 2; ++lc)
+#pragma unroll
         for (int g = 0; g < 4; ++g) {
-          stg[lane] = bsum[lc][g];
-          asm volatile("bar.sync 1, %0;" ::"r"(kEpiT));
-          if (ew == 0) {
-            float acc = 0.f;
-            for (int w = 0; w < EW; ++w) acc += stg_all[w * kStgW + lane];
-            bias_partial[tile * G4 + g * H + 32 * c + lane] = acc;
+          float4 v = bsum[lc][g];
+#pragma unroll
+          for (int m = 8; m <= 16; m <<= 1) {
+            v.x += __shfl_xor_sync(0xffffffffu, v.x, m);
+            v.y += __shfl_xor_sync(0xffffffffu, v.y, m);
+            v.z += __shfl_xor_sync(0xffffffffu, v.z, m);
+            v.w += __shfl_xor_sync(0xffffffffu, v.w, m);
           }
-          asm volatile("bar.sync 1, %0;" ::"r"(kEpiT));
+          if (r4 == 0) sts4(stg_s + (uint32_t)(((lc * 4 + g) * 32 + 4 * u8) * 4), v);
         }
+      asm volatile("bar.sync 1, %0;" ::"r"(kEpiT));
+      if (ew == 0) {
+        for (int lc = 0; lc < 2; ++lc)
+          for (int g = 0; g < 4; ++g) {
+            float acc = 0.f;
+            for (int w = 0; w < EW; ++w) acc += stg_all[w * kStgW + (lc * 4 + g) * 32 + lane];
+            bias_partial[tile * G4 + g * H + u0 + 32 * lc + lane] = acc;
+          }
       }
     }
   }
@@ -1296,7 +1355,7 @@ int launch_lstm_bwd_tc2k_ew(const CUtensorMap& m, const int32_t* slot_row, const
                             int64_t R, int L, const float* save, const float* dh_out, float* dgx,
                             int rnd, float* bias_partial, int rq, cudaStream_t s) {
   const size_t smem = (size_t)ks_a_stages<EW>() * BM * 128 + (size_t)kKsBStages * H * 128 +
-                      (size_t)2 * 4 * ks_recv_rq<EW>() * (H / 2) * 4 + (size_t)EW * 8 * (H / 2 + 1) * 4 +
+                      (size_t)2 * 4 * ks_recv_rq<EW>() * (H / 2) * 4 + (size_t)EW * 8 * kKsStgStride * 4 +
                       1024 + 512;
   auto kern = lstm_bwd_tc2k_kernel<H, EW>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1315,13 +1374,12 @@ int launch_lstm_bwd_tc2k(const float* U, const int32_t* slot_row, const uint8_t*
   CUtensorMap m;
   int rc = make_map(&m, U, H, 4 * H, 4 * H, 32, H, false);
   if (rc) return rc;
+  DGC_REQUIRE(R * (int64_t)L < (int64_t)INT32_MAX, "lstm_bwd_tc2k: R * L must fit int32");
   const int rq = cluster_rows_per_quadrant(R);
-  static const int pf = getenv("DGC_BWD_PF") ? atoi(getenv("DGC_BWD_PF")) & 3 : 2;
-  const int rnd_pf = (rnd & 1) | (pf << 1);
   if (rq <= 24 && !getenv("DGC_RNN_EW16"))
-    return launch_lstm_bwd_tc2k_ew<H, 12>(m, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd_pf,
+    return launch_lstm_bwd_tc2k_ew<H, 12>(m, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
                                           bias_partial, rq, s);
-  return launch_lstm_bwd_tc2k_ew<H, 16>(m, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd_pf,
+  return launch_lstm_bwd_tc2k_ew<H, 16>(m, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
                                         bias_partial, rq, s);
 }
 
@@ -1411,7 +1469,7 @@ extern "C" int dgc_rnn_fwd_tc_fused_available(int32_t F, int32_t H) {
 }
 
 extern "C" int dgc_debug_lstm_timestamps(unsigned long long* out, int n) {
-  if (n > 256 * 3) n = 256 * 3;
+  if (n > 256 * 8) n = 256 * 8;
   cudaError_t e = cudaMemcpyFromSymbol(out, g_lstm_ts, n * sizeof(unsigned long long));
   return e == cudaSuccess ? DGC_OK : dgc::cuda_fail(e, "debug timestamps");
 }

@@ -411,15 +411,17 @@ def test_softmax_xent_colsum_optimizers():
 
 def tc_save_decode(save, H):
     """The tensor-core LSTM save rows as [n, 6H] fp32 (h_in, c_in, i, f, g, o):
-    the compact H = 128 cluster layout (h_in fp32 | five fp16 fields, 3.5 H
-    floats per row) or the 7 H fp32 layout."""
+    the compact H = 128 cluster layout (h_in fp32 | c_in fp16 | i, f, g, o fp16
+    interleaved per unit, 3.5 H floats per row) or the 7 H fp32 layout."""
     from paper_2309_03523_b200 import ops
     save = np.ascontiguousarray(save, np.float32)
     sf = ops.rnn_tc_save_floats(H)
     if sf == 7 * H:
         return save[:, :6 * H]
     half = save[:, H:sf].copy().view(np.float16).astype(np.float32)  # [n, 5H]
-    return np.concatenate([save[:, :H], half], 1)
+    n = save.shape[0]
+    ifgo = half[:, H:].reshape(n, H, 4).transpose(0, 2, 1).reshape(n, 4 * H)  # unit-interleaved
+    return np.concatenate([save[:, :H], half[:, :H], ifgo], 1)
 
 
 def tc_save_encode(fields, H):
@@ -431,7 +433,9 @@ def tc_save_encode(fields, H):
     n = fields.shape[0]
     out = np.zeros((n, sf), np.float32)
     out[:, :H] = fields[:, :H]
-    out[:, H:] = np.ascontiguousarray(fields[:, H:6 * H].astype(np.float16)).view(np.float32)
+    ifgo = fields[:, 2 * H:6 * H].reshape(n, 4, H).transpose(0, 2, 1).reshape(n, 4 * H)
+    half = np.concatenate([fields[:, H:2 * H], ifgo], 1).astype(np.float16)
+    out[:, H:] = np.ascontiguousarray(half).view(np.float32)
     return out
 
 

@@ -29,8 +29,8 @@ import ctypes
 from paper_2309_03523_b200 import _native
 lib = _native.lib()
 fn(); torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * (256 * 3))()
-lib.dgc_debug_lstm_timestamps(buf, 256 * 3)
+buf = (ctypes.c_ulonglong * (256 * 8))()
+lib.dgc_debug_lstm_timestamps(buf, 256 * 8)
 ts = np.array(buf[:L * 3], dtype=np.float64).reshape(L, 3)
 t0 = ts[0, 0]
 for t in range(1, 6):

@@ -27,8 +27,10 @@ for _ in range(3): fn()
 e.record(); torch.cuda.synchronize()
 print(f"fused fwd H {H}: {s.elapsed_time(e) / 3:.3f} ms")
 fn(); torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * (256 * 3))()
-_native.lib().dgc_debug_lstm_timestamps(buf, 256 * 3)
-ts = np.array(buf[:L * 3], dtype=np.float64).reshape(L, 3)
+buf = (ctypes.c_ulonglong * (256 * 8))()
+_native.lib().dgc_debug_lstm_timestamps(buf, 256 * 8)
+ts = np.array(buf[:L * 8], dtype=np.float64).reshape(L, 8)
 print("per-step us: h-ready->acc", np.mean(ts[:, 1] - ts[:, 0]) / 1e3, "epi", np.mean(ts[:, 2] - ts[:, 1]) / 1e3,
       "epi_end->next h-ready", np.mean(ts[1:, 0] - ts[:-1, 2]) / 1e3, "step", np.mean(np.diff(ts[:, 0])) / 1e3)
+ch = [ts[:, 1], ts[:, 3], ts[:, 4], ts[:, 5], ts[:, 2]]
+print("per-chunk epilogue us:", [round(float(np.mean(ch[i + 1] - ch[i])) / 1e3, 2) for i in range(4)])

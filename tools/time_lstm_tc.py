@@ -34,8 +34,8 @@ import ctypes
 from paper_2309_03523_b200 import _native
 lib = _native.lib()
 ops.rnn_fwd_tc(1, gx, Ut, sr, sm, sc, carry, R, L, H, 2 * H, hc, hc[:, H:], save); torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * (256 * 3))()
-lib.dgc_debug_lstm_timestamps(buf, 256 * 3)
+buf = (ctypes.c_ulonglong * (256 * 8))()
+lib.dgc_debug_lstm_timestamps(buf, 256 * 8)
 ts = np.array(buf[:L * 3], dtype=np.float64).reshape(L, 3)
 t0 = ts[0, 0]
 for p in range(min(L, 6)):
