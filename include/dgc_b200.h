@@ -26,10 +26,6 @@ extern "C" {
 #define DGC_ERR_CUDA -2
 #define DGC_ERR_PLAN -3 /* plan/graph mismatch, cf. sim.py:108 PlanGraphMismatch */
 
-/* element types of operands that have more than one storage format */
-#define DGC_F32 0
-#define DGC_BF16 1
-
 int dgc_version(void);
 const char* dgc_last_error(void);
 
@@ -145,15 +141,6 @@ int dgc_spmm_csr_rows(const int32_t* row_ptr, const int32_t* col, const float* d
                       const float* Y, const float* bias, float* out, const int32_t* rows,
                       int64_t n_rows, int64_t row_begin, int32_t width, int32_t act,
                       void* stream);
-
-/* K1 with the gathered operand in either storage format: y_dtype DGC_F32
- * (parity mode) or DGC_BF16 (TF32 mode: the neighbour-row gathers are the
- * kernel's dominant byte stream). Accumulation, bias, dinv and `out` are fp32;
- * rows / row_begin as dgc_spmm_csr_rows. */
-int dgc_spmm_csr_ex(const int32_t* row_ptr, const int32_t* col, const float* dinv,
-                    const void* Y, int32_t y_dtype, const float* bias, float* out,
-                    const int32_t* rows, int64_t n_rows, int64_t row_begin, int32_t width,
-                    int32_t act, void* stream);
 
 /* K2: tcgen05 TF32 GEMM (TMA -> SMEM -> TMEM), fp32 storage, fp32 accumulate.
  *   C[M,N] = (accumulate ? C : 0) + op(A) op(B)  (+ bias[N]) (* (relu_src > 0))

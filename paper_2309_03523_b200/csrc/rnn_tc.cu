@@ -485,6 +485,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           }
           __syncwarp();
         }
+        DGC_TS(blockIdx.x == 0 && lane == 0 && p < 256, p, 6);
       }
       for (int i = 0; i < KB; ++i, ++g) {
         const int kb = kHalves == 2 ? (i >> 1) + 2 * (i & 1) : i;  // 0, 2, 1, 3
@@ -498,6 +499,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
         const int s = g % kStages;
         mbar_wait(&b_full[s], (g / kStages) & 1);
         fence_after();
+        DGC_TS(i == 2 && blockIdx.x == 0 && lane == 0 && p < 256, p, 7);
         if (lane == 0) {
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk)
@@ -597,21 +599,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           float a[64];
           const uint32_t ta = tl + ab * kAccCols + c0;
           tmem_ld16x4(ta, ta + HU, ta + 2 * HU, ta + 3 * HU, a);
+          // staging row k (64 B) holds its 16-B quads XOR-swizzled by (k >> 1) & 3:
+          // the 8 writing lanes and the 8 lanes of every read phase hit 8
+          // distinct bank quads (conflict-free both ways)
           if (lane >= rb && lane < rb + 8) {
+            const int k = lane - rb;
 #pragma unroll
             for (int gi = 0; gi < 4; ++gi) {
-              const uint32_t d = stg + (gi * 8 + lane - rb) * 64;
+              const uint32_t d = stg + (gi * 8 + k) * 64;
 #pragma unroll
               for (int u = 0; u < 16; u += 4)
-                sts4(d + u * 4, make_float4(a[gi * 16 + u], a[gi * 16 + u + 1], a[gi * 16 + u + 2],
-                                            a[gi * 16 + u + 3]));
+                sts4(d + ((((u >> 2) ^ (k >> 1)) & 3) << 4),
+                     make_float4(a[gi * 16 + u], a[gi * 16 + u + 1], a[gi * 16 + u + 2],
+                                 a[gi * 16 + u + 3]));
             }
           }
         }
         __syncwarp();
         float4 pre[4];
 #pragma unroll
-        for (int gi = 0; gi < 4; ++gi) pre[gi] = lds4(stg + ((gi * 8 + r8) * 16 + uq * 4) * 4);
+        for (int gi = 0; gi < 4; ++gi)
+          pre[gi] = lds4(stg + (gi * 8 + r8) * 64 + (((uq ^ (r8 >> 1)) & 3) << 4));
         // next chunk's gx in flight while this chunk computes
         float4 xn[4];
 #pragma unroll

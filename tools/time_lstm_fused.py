@@ -34,3 +34,7 @@ print("per-step us: h-ready->acc", np.mean(ts[:, 1] - ts[:, 0]) / 1e3, "epi", np
       "epi_end->next h-ready", np.mean(ts[1:, 0] - ts[:-1, 2]) / 1e3, "step", np.mean(np.diff(ts[:, 0])) / 1e3)
 ch = [ts[:, 1], ts[:, 3], ts[:, 4], ts[:, 5], ts[:, 2]]
 print("per-chunk epilogue us:", [round(float(np.mean(ch[i + 1] - ch[i])) / 1e3, 2) for i in range(4)])
+print("MMA warp (us rel. to h-ready[p]): x-part issued for p (before h-ready)", np.mean(ts[:, 6] - ts[:, 0]) / 1e3,
+      "U kb2 ready", np.mean(ts[:, 7] - ts[:, 0]) / 1e3, "acc ready", np.mean(ts[:, 1] - ts[:, 0]) / 1e3)
+for p in range(1, 6):
+    print(p, " ".join(f"{(ts[p, k] - ts[p, 0]) / 1e3:6.2f}" for k in (6, 0, 7, 1, 3, 4, 5, 2)))
