@@ -142,6 +142,14 @@ int dgc_spmm_csr_rows(const int32_t* row_ptr, const int32_t* col, const float* d
                       int64_t n_rows, int64_t row_begin, int32_t width, int32_t act,
                       void* stream);
 
+/* K1 (as dgc_spmm_csr_rows) that also writes an fp16 copy of `out` to out16
+ * (same [rows, width] layout; may be NULL): the gathered x operand of the
+ * fp16 tensor-core recurrence (dgc_lstm_fwd_tc_f16x). */
+int dgc_spmm_csr_x(const int32_t* row_ptr, const int32_t* col, const float* dinv,
+                   const float* Y, const float* bias, float* out, void* out16,
+                   const int32_t* rows, int64_t n_rows, int64_t row_begin, int32_t width,
+                   int32_t act, void* stream);
+
 /* K2: tcgen05 TF32 GEMM (TMA -> SMEM -> TMEM), fp32 storage, fp32 accumulate.
  *   C[M,N] = (accumulate ? C : 0) + op(A) op(B)  (+ bias[N]) (* (relu_src > 0))
  *   a_mn = 0: A is [M,K] (row stride lda); a_mn = 1: A stored as [K,M] (A^T)
@@ -243,20 +251,31 @@ int dgc_rnn_fwd_tc(int32_t cell, const float* gx, const float* Ut, const int32_t
                    int64_t n_rows, int32_t row_len, int32_t H, int64_t ld_out, float* h_out,
                    float* c_out, float* save, void* stream);
 /* Tensor-core LSTM forward with the input projection fused (F = H = 128, the
- * 2-CTA cluster kernel): gate pre-activations x Wx + h U + b accumulate in TMEM
- * from TMA row gathers of x (tile::gather4 by slot_row) against WxT [4H, F]
- * and the h tile against Ut [4H, H]; bias [4H]. x [n_x, F] (row stride ldx,
- * TF32-rounded). Replaces the gx GEMM + dgc_rnn_fwd_tc pair; same outputs. */
-int dgc_rnn_fwd_tc_x(int32_t cell, const float* x, int64_t ldx, int64_t n_x, int32_t F,
-                     const float* WxT, const float* Ut, const float* bias,
-                     const int32_t* slot_row, const uint8_t* slot_mask, const int32_t* slot_carry,
-                     const float* carry, int64_t n_rows, int32_t row_len, int32_t H,
-                     int64_t ld_out, float* h_out, float* c_out, float* save, void* stream);
-/* 1 if dgc_rnn_fwd_tc_x serves this (F, H) in this process, else 0. */
+ * 2-CTA cluster kernel), all gate-product operands fp16 (kind::f16, the same
+ * 10-bit mantissa as TF32; fp32 accumulation): x Wx + h U + b accumulate in
+ * TMEM from TMA row gathers of x16 (tile::gather4 by slot_row) and the fp16 h
+ * tile against this CTA's halves of Wx and U, converted once per launch into
+ * resident shared memory (no weight traffic per position). x16 [n_x, 128]
+ * fp16 (the layer input); Wx, U [128, 512] fp32 as the model stores them; bias
+ * [512]. h_out is rounded to fp16 precision (exact in TF32), so the next
+ * position's fp16 h tile equals it; h_out16 (may be NULL) receives its fp16
+ * copy [n, 128] for the next layer's x16. Replaces the gx GEMM +
+ * dgc_rnn_fwd_tc pair; save/h/c outputs as dgc_rnn_fwd_tc. */
+int dgc_lstm_fwd_tc_f16x(const void* x16, int64_t n_x, const float* Wx, const float* U,
+                         const float* bias, const int32_t* slot_row, const uint8_t* slot_mask,
+                         const int32_t* slot_carry, const float* carry, int64_t n_rows,
+                         int32_t row_len, int64_t ld_out, float* h_out, float* c_out, float* save,
+                         void* h_out16, void* stream);
+/* 1 if dgc_lstm_fwd_tc_f16x serves this (F, H) in this process, else 0. */
 int dgc_rnn_fwd_tc_fused_available(int32_t F, int32_t H);
 /* Tensor-core BPTT (LSTM, H in {32,64,128}): takes U itself [H, 4H] (the
  * K-major B operand of dh = da U^T), dc_scratch [ceil(n_rows/128)*128, H]
- * floats; bias_partial [dgc_rnn_tc_tiles(n_rows, H), 4H] (may be NULL). */
+ * floats; bias_partial [dgc_rnn_tc_tiles(n_rows, H), 4H] (may be NULL).
+ * H = 128 (2-CTA cluster kernel): the recurrent product runs on kind::f16 with
+ * U resident in shared memory as fp16 and da as fp16 scaled by 2^e, e = bits
+ * 16..22 of cell (0: unscaled); the scale is removed exactly from dh. Size e to
+ * the loss normalisation (a mean over n instances: e = round(log2 n)) so that
+ * S da sits in fp16's normal range. */
 int dgc_rnn_bwd_tc(int32_t cell, const float* U, const int32_t* slot_row,
                    const uint8_t* slot_mask, int64_t n_rows, int32_t row_len, int32_t H,
                    const float* save, const float* dh_out, float* dgx, float* dc_scratch,

@@ -39,8 +39,8 @@ _SIGS = {
     "dgc_plan_spatial_fusion": (_i32, [_i64, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _i64, _i64,
                                        _i64, _i64, _i64, _p, _p, _p, _p]),
     "dgc_propagate_labels": (_i32, [_i64, _i64, _p, _i64, _p, _i64, _p, _i64, _i32, _p, _p, _p]),
-    "dgc_rnn_fwd_tc_x": (_i32, [_i32, _p, _i64, _i64, _i32, _p, _p, _p, _p, _p, _p, _p, _i64, _i32,
-                                _i32, _i64, _p, _p, _p, _p]),
+    "dgc_lstm_fwd_tc_f16x": (_i32, [_p, _i64, _p, _p, _p, _p, _p, _p, _p, _i64, _i32, _i64, _p, _p,
+                                    _p, _p, _p]),
     "dgc_rnn_fwd_tc_fused_available": (_i32, [_i32, _i32]),
     "dgc_pack_sequences": (_i32, [_p, _i64, _i32, _i64, _p, _p, _p, _p, _p]),
     "dgc_spmm_csr": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i32, _i32, _p]),
@@ -67,6 +67,7 @@ _SIGS = {
     "dgc_stale_select": (_i32, [_p, _p, _p, _f32, _p, _p, _p, _i64, _i32, _p]),
     "dgc_compact_sent": (_i32, [_p, _i64, _p, _p, _p, _p]),
     "dgc_spmm_csr_rows": (_i32, [_p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i32, _i32, _p]),
+    "dgc_spmm_csr_x": (_i32, [_p, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i32, _i32, _p]),
     "dgc_stale_select2": (_i32, [_p, _p, _p, C.c_double, _p, C.c_double, _p, _p, _p, _i64, _i32,
                                  _p, _p, _p]),
     "dgc_exchange_rank": (_i32, [_p, _i64, _p, _i32, _p, _p, _p, _p]),

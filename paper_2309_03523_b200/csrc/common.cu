@@ -9,6 +9,7 @@ int fail(int code, const std::string& msg) {
 }
 int cuda_fail(cudaError_t e, const char* what) {
   set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  (void)cudaGetLastError();  // a non-sticky error must not surface at the next launch check
   return DGC_ERR_CUDA;
 }
 }  // namespace dgc

@@ -42,6 +42,8 @@ __device__ __forceinline__ void st_ifgo(__half* p, float4 i, float4 f, float4 g,
   q[0] = make_uint4(h2u(i.x, f.x), h2u(g.x, o.x), h2u(i.y, f.y), h2u(g.y, o.y));
   q[1] = make_uint4(h2u(i.z, f.z), h2u(g.z, o.z), h2u(i.w, f.w), h2u(g.w, o.w));
 }
+// round to the nearest fp16 (exactly representable in TF32 too, in range)
+__device__ __forceinline__ float f16r(float x) { return __half2float(__float2half_rn(x)); }
 __device__ __forceinline__ float2 u2h(uint32_t u) {
   return __half22float2(*reinterpret_cast<const __half2*>(&u));
 }
@@ -49,6 +51,7 @@ __device__ __forceinline__ float2 u2h(uint32_t u) {
 using namespace dgc::tc;
 using dgc::make_map;
 using dgc::make_gather_map;
+using dgc::make_gather_map_f16;
 
 // warp 0 TMA, warp 1 MMA + TMEM, warps 2..9 epilogue: 2 warps per TMEM lane
 // quadrant (32 packed rows), each owning H/2 hidden units.
@@ -325,34 +328,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
                          const int32_t* __restrict__ slot_row, const uint8_t* __restrict__ slot_mask,
                          const int32_t* __restrict__ slot_carry, const float* __restrict__ carry,
                          int64_t R, int L, int64_t ld, float* __restrict__ h_out,
-                         float* __restrict__ c_out, float* __restrict__ save, int rq) {
+                         float* __restrict__ c_out, float* __restrict__ save, int rq,
+                         const float* __restrict__ Uw, const float* __restrict__ Wxw,
+                         __half* __restrict__ h16) {
   constexpr int kEpiT = 32 * kVEW;
   constexpr int G4 = 4 * H;
   constexpr int HU = H / 2;
   constexpr int NCH = HU / 16;               // 16-unit chunks per CTA
   constexpr int NP = 4 * HU;
   constexpr int KB = H / BK;
-  constexpr int kABytes = KB * BM * 128;
+  // FX (F = H = 128): every operand of the gate product is fp16 (kind::f16,
+  // the same 10-bit mantissa as TF32): the h tile (2 k-blocks of 64 units), the
+  // x rows TMA-gathered from an fp16 copy of the layer input, and this CTA's
+  // halves of U^T and Wx^T, resident in shared memory for the whole launch --
+  // no weight bytes move per position (streaming them was the recurrence's
+  // critical path: all 148 SMs re-read the same 256 KB every position).
+  constexpr int kABytes = FX ? 2 * BM * 128 : KB * BM * 128;
+  constexpr int kWBytes = FX ? 2 * NP * 128 : 0;  // one resident fp16 weight half: 2 k-blocks
+  constexpr int kBStages = FX ? 0 : kStages;
   constexpr int kBStage = NP * 128;
-  constexpr int kStgW = 4 * 8 * 16;          // [gate][8 rows][16 units]
+  constexpr int kXStages = FX ? 1 : kStages;
+  // staging [gate][8 rows][16 units] per warp, all 4 gates at once or (the
+  // 16-warp fp16 variant, to fit its shared memory) 2 at a time
+  constexpr int kStgGates = (FX && kVEW > 12) ? 2 : 4;
+  constexpr int kStgW = kStgGates * 8 * 16;
   constexpr uint32_t kAccCols = NP <= 128 ? 128 : 256;
   constexpr uint32_t kTmemCols = FX ? 2 * kAccCols : kAccCols;
-  constexpr int kXStage = BM * 128;          // one x k-block: 128 rows x 32 fp32
+  constexpr int kXStage = BM * 128;          // one x k-block: 128 rows x 128 B
   static_assert(!FX || H == 128, "fused input projection: F = H = 128");
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned base, derived from the __shared__ array (keeps shared-space
   // addressing: STS/LDS instead of generic ST/LD)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
-  uint8_t* sB = smem + kABytes;
-  uint8_t* sX = sB + kStages * kBStage;      // FX: x k-block ring
-  float* stg_all = reinterpret_cast<float*>(sX + (FX ? kStages * kXStage : 0));
+  uint8_t* sU = smem + kABytes;              // FX: resident U^T half (fp16)
+  uint8_t* sW = sU + kWBytes;                // FX: resident Wx^T half (fp16)
+  uint8_t* sB = sW + kWBytes;
+  uint8_t* sX = sB + kBStages * kBStage;     // FX: x k-block ring
+  float* stg_all = reinterpret_cast<float*>(sX + (FX ? kXStages * kXStage : 0));
   float* c_all = stg_all + kVEW * kStgW;     // carried c: [warp][chunk][lane] float4
   uint64_t* b_full = reinterpret_cast<uint64_t*>(c_all + kVEW * NCH * 32 * 4);
   uint64_t* b_empty = b_full + kStages;
   // h-tile readiness: FX (double-buffered accumulators) splits it into two
-  // halves -- k-blocks {0, 2} (both CTAs' first 32 units) and {1, 3} -- so the
-  // h U^T MMA of p+1 starts on the first half while the epilogues of p finish
+  // halves -- units {0-31, 64-95} (both CTAs' first 32 units) and {32-63,
+  // 96-127} -- so the h U^T MMA of p+1 starts on the first half while the
+  // epilogues of p finish
   constexpr int kHalves = (FX && KB == 4) ? 2 : 1;
   uint64_t* a_full = b_empty + kStages;      // [2]
   uint64_t* acc_full = a_full + 2;           // [2] (FX: per accumulator)
@@ -418,7 +438,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       const int n_g = 4 * gpq;
       const uint32_t x_bytes = (uint32_t)n_g * 4u * 128u;
       const int gq = lane / gpq, gi0 = (lane % gpq) * 4;
-      int g = 0, gxs = 0;                          // B-ring and x-ring sequence numbers
+      int gxs = 0;                                 // x-ring sequence number
       for (int p = 0; p < L; ++p) {
         int idx[4] = {0, 0, 0, 0};
         if (lane < n_g) {
@@ -430,32 +450,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
             idx[e] = inst >= 0 ? inst : 0;  // padding slots read row 0 (result unused)
           }
         }
-        for (int kb = 0; kb < KB; ++kb, ++g, ++gxs) {
-          const int s = g % kStages, sx = gxs % kStages;
+        // the position's x rows: 2 fp16 k-blocks of 64 units (weights are resident)
+        for (int kb = 0; kb < 2; ++kb, ++gxs) {
+          const int sx = gxs % kXStages;
           if (lane == 0) {
-            mbar_wait(&x_empty[sx], ((gxs / kStages) & 1) ^ 1);
+            mbar_wait(&x_empty[sx], ((gxs / kXStages) & 1) ^ 1);
             mbar_expect_tx(&x_full[sx], x_bytes);
-            mbar_wait(&b_empty[s], ((g / kStages) & 1) ^ 1);
-            mbar_expect_tx(&b_full[s], (uint32_t)kBStage);
-#pragma unroll
-            for (int gi = 0; gi < 4; ++gi)
-              tma_load_2d(sB + s * kBStage + gi * HU * 128, &tmWxT, kb * BK, gi * H + u0, &b_full[s]);
           }
           __syncwarp();
           if (lane < n_g)
-            tma_gather4(sX + sx * kXStage + (gq * 32 + gi0) * 128, &tmX, kb * BK, idx[0], idx[1],
+            tma_gather4(sX + sx * kXStage + (gq * 32 + gi0) * 128, &tmX, kb * 64, idx[0], idx[1],
                         idx[2], idx[3], &x_full[sx]);
-        }
-        if (lane == 0) {
-          for (int i = 0; i < KB; ++i, ++g) {
-            const int kb = kHalves == 2 ? (i >> 1) + 2 * (i & 1) : i;  // 0, 2, 1, 3
-            const int s = g % kStages;
-            mbar_wait(&b_empty[s], ((g / kStages) & 1) ^ 1);
-            mbar_expect_tx(&b_full[s], (uint32_t)kBStage);
-#pragma unroll
-            for (int gi = 0; gi < 4; ++gi)
-              tma_load_2d(sB + s * kBStage + gi * HU * 128, &tmUt, kb * BK, gi * H + u0, &b_full[s]);
-          }
         }
         __syncwarp();
       }
@@ -470,22 +475,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       if (FX) {
         mbar_wait(&acc_empty[ab], ((p >> 1) & 1) ^ 1);  // epilogue of p-2 drained it
         fence_after();
-        for (int kb = 0; kb < KB; ++kb, ++g, ++gxs) {
-          const int s = g % kStages, sx = gxs % kStages;
-          mbar_wait(&x_full[sx], (gxs / kStages) & 1);
-          mbar_wait(&b_full[s], (g / kStages) & 1);
+        if (p == 0) {  // the resident weights were written by the epilogue warps
+          mbar_wait(&a_full[0], 0);
+          fence_after();
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        const uint32_t w_base = smem_u32(sW), idesc16 = idesc_f16(NP);
+        for (int kb = 0; kb < 2; ++kb, ++gxs) {
+          const int sx = gxs % kXStages;
+          mbar_wait(&x_full[sx], (gxs / kXStages) & 1);
           fence_after();
           if (lane == 0) {
 #pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk)
-              mma_tf32(tacc, kdesc(x_base + sx * kXStage + kk * 32),
-                       kdesc(b_base + s * kBStage + kk * 32), idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < 4; ++kk)
+              mma_f16(tacc, kdesc(x_base + sx * kXStage + kk * 32),
+                      kdesc(w_base + kb * NP * 128 + kk * 32), idesc16, (kb > 0 || kk > 0) ? 1u : 0u);
             mma_commit(&x_empty[sx]);
-            mma_commit(&b_empty[s]);
           }
           __syncwarp();
         }
         DGC_TS(blockIdx.x == 0 && lane == 0 && p < 256, p, 6);
+      }
+      if (FX) {
+        // h part: fp16 h tile x resident fp16 U^T; half h = the 16-unit slices
+        // kk = 2h, 2h+1 of both 64-unit k-blocks
+        const uint32_t u_base = smem_u32(sU);
+        const uint32_t idesc16 = idesc_f16(NP);
+        for (int h = 0; h < 2; ++h) {
+          mbar_wait(&a_full[h], p & 1);
+          fence_after();
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          DGC_TS(h == 0 && blockIdx.x == 0 && lane == 0 && p < 256, p, 0);
+          if (lane == 0) {
+#pragma unroll
+            for (int kb16 = 0; kb16 < 2; ++kb16)
+#pragma unroll
+              for (int kk = 2 * h; kk < 2 * h + 2; ++kk)
+                mma_f16(tacc, kdesc(a_base + kb16 * BM * 128 + kk * 32),
+                        kdesc(u_base + kb16 * NP * 128 + kk * 32), idesc16, 1u);
+            if (h == 1) mma_commit_mc(&acc_full[ab], (uint16_t)0x3);
+          }
+          __syncwarp();
+        }
+        continue;
       }
       for (int i = 0; i < KB; ++i, ++g) {
         const int kb = kHalves == 2 ? (i >> 1) + 2 * (i & 1) : i;  // 0, 2, 1, 3
@@ -527,17 +559,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
     const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
     const uint32_t sA_peer = map_peer(sA, peer);
     const uint32_t afull_peer = map_peer(a_full, peer);
-    auto a_off = [&](int k) { return (uint32_t)((k / BK) * BM * 128) + sw128_offset(r, k % BK); };
+    // h-tile address of unit k of this lane's row: fp32 k-blocks of 32 units,
+    // or (FX) fp16 k-blocks of 64 units; both K-major SWIZZLE_128B
+    auto a_off = [&](int k) {
+      if (FX)
+        return (uint32_t)((k >> 6) * BM * 128 + r * 128 + ((((k & 63) >> 3) ^ (r & 7)) << 4) +
+                          (k & 7) * 2);
+      return (uint32_t)((k / BK) * BM * 128) + sw128_offset(r, k % BK);
+    };
     // unit k of this CTA lies in h-tile half (k - u0) / 32 (kHalves == 2)
     auto put_h = [&](int k, float4 v) {
       const uint32_t off = a_off(k);
-      sts4(sA_s + off, v);
       const uint32_t half = kHalves == 2 ? (uint32_t)((k - u0) >> 5) : 0u;
-      st_async_v4(sA_peer + off, v, afull_peer + half * 8u);
+      if (FX) {
+        const uint2 hv = make_uint2(h2u(v.x, v.y), h2u(v.z, v.w));
+        asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(sA_s + off), "r"(hv.x), "r"(hv.y)
+                     : "memory");
+        st_async_v2(sA_peer + off, hv, afull_peer + half * 8u);
+      } else {
+        sts4(sA_s + off, v);
+        st_async_v4(sA_peer + off, v, afull_peer + half * 8u);
+      }
+    };
+    auto get_h = [&](int k) {  // this lane's 4 units of the h tile (as the MMA reads them)
+      if (FX) {
+        uint32_t a, b;
+        asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(a), "=r"(b) : "r"(sA_s + a_off(k)));
+        const float2 lo = u2h(a), hi = u2h(b);
+        return make_float4(lo.x, lo.y, hi.x, hi.y);
+      }
+      return lds4(sA_s + a_off(k));
     };
     // bytes of the peer's half of the h tile it writes into ours: 8 rows x HU
     // units per active warp (4 quadrants x ceil(rq / 8) warps)
-    const uint32_t kPeerBytes = 4u * (uint32_t)((rq + 7) / 8) * 8u * HU * 4u;
+    const uint32_t kPeerBytes = 4u * (uint32_t)((rq + 7) / 8) * 8u * HU * (FX ? 2u : 4u);
+    if (FX) {
+      // this CTA's halves of U^T and Wx^T (B row n = gate column (n / HU) * H +
+      // u0 + n % HU, K = the H input units) as fp16, K-major SWIZZLE_128B, read
+      // straight from U and Wx [H, 4H] (the transpose happens here: consecutive
+      // threads take consecutive gate columns, so the fp32 reads coalesce);
+      // resident for the whole launch, ordered before the first MMA by the
+      // prologue's a_full arrival
+      for (int c = threadIdx.x - 64; c < 2 * NP * (H / 8); c += kEpiT) {
+        const int mat = c / (NP * (H / 8)), cc = c % (NP * (H / 8));
+        const int n = cc % NP, k0 = (cc / NP) * 8;
+        const float* src = (mat ? Wxw : Uw) + (int64_t)k0 * G4 + (n / HU) * H + u0 + (n % HU);
+        float v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = __ldg(src + (int64_t)i * G4);
+        const uint32_t dst = smem_u32(mat ? sW : sU) +
+                             (uint32_t)((k0 >> 6) * NP * 128 + n * 128 + ((((k0 & 63) >> 3) ^ (n & 7)) << 4));
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(h2u(v[0], v[1])),
+                     "r"(h2u(v[2], v[3])), "r"(h2u(v[4], v[5])), "r"(h2u(v[6], v[7]))
+                     : "memory");
+      }
+    }
     auto publish = [&](int half) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       if (ew == 0 && lane == 0) mbar_arrive_expect_tx(&a_full[half], kPeerBytes / kHalves);
@@ -555,7 +631,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
         float4 v = zero4();
         if (ci >= 0) {
           v = f4(carry + (int64_t)ci * 2 * H + j);
-          v = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
+          if (!FX) v = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
         }
         put_h(j, v);
         sts4(creg + ch * 512, zero4());
@@ -595,17 +671,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       for (int ch = 0; ch < NCH; ++ch) {
         const int c0 = ch * 16;
         const int j = u0 + c0 + uq * 4;
-        {
-          float a[64];
-          const uint32_t ta = tl + ab * kAccCols + c0;
-          tmem_ld16x4(ta, ta + HU, ta + 2 * HU, ta + 3 * HU, a);
-          // staging row k (64 B) holds its 16-B quads XOR-swizzled by (k >> 1) & 3:
-          // the 8 writing lanes and the 8 lanes of every read phase hit 8
-          // distinct bank quads (conflict-free both ways)
+        float4 pre[4];
+        const uint32_t ta = tl + ab * kAccCols + c0;
+        // staging row k (64 B) holds its 16-B quads XOR-swizzled by (k >> 1) & 3:
+        // the 8 writing lanes and the 8 lanes of every read phase hit 8
+        // distinct bank quads (conflict-free both ways)
+        auto stage = [&](const float* a, int ng) {
           if (lane >= rb && lane < rb + 8) {
             const int k = lane - rb;
 #pragma unroll
-            for (int gi = 0; gi < 4; ++gi) {
+            for (int gi = 0; gi < ng; ++gi) {
               const uint32_t d = stg + (gi * 8 + k) * 64;
 #pragma unroll
               for (int u = 0; u < 16; u += 4)
@@ -614,12 +689,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
                                  a[gi * 16 + u + 3]));
             }
           }
-        }
-        __syncwarp();
-        float4 pre[4];
+          __syncwarp();
+        };
+        if (kStgGates == 4) {
+          float a[64];
+          tmem_ld16x4(ta, ta + HU, ta + 2 * HU, ta + 3 * HU, a);
+          stage(a, 4);
 #pragma unroll
-        for (int gi = 0; gi < 4; ++gi)
-          pre[gi] = lds4(stg + (gi * 8 + r8) * 64 + (((uq ^ (r8 >> 1)) & 3) << 4));
+          for (int gi = 0; gi < 4; ++gi)
+            pre[gi] = lds4(stg + (gi * 8 + r8) * 64 + (((uq ^ (r8 >> 1)) & 3) << 4));
+        } else {  // two gates at a time (the 16-warp fp16 variant's shared memory)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float a[32];
+            tmem_ld16(ta + (2 * h) * HU, a);
+            tmem_ld16(ta + (2 * h + 1) * HU, a + 16);
+            stage(a, 2);
+#pragma unroll
+            for (int gi = 0; gi < 2; ++gi)
+              pre[2 * h + gi] = lds4(stg + (gi * 8 + r8) * 64 + (((uq ^ (r8 >> 1)) & 3) << 4));
+            __syncwarp();
+          }
+        }
         // next chunk's gx in flight while this chunk computes
         float4 xn[4];
 #pragma unroll
@@ -630,7 +721,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
         float4 cin = zero4();
         if (ci >= 0) cin = f4(carry + (int64_t)ci * 2 * H + H + j);
         else if (mk) cin = lds4(creg + ch * 512);
-        const float4 hin = lds4(sA_s + a_off(j));
+        const float4 hin = get_h(j);
         float4 hn = zero4(), cn = zero4();
         if (inst >= 0) {
           float4 ig, fg, gg, og, tc;
@@ -641,7 +732,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   og.c = sigm(pre[3].c + xg[3].c);                                \
   cn.c = fg.c * cin.c + ig.c * gg.c;                              \
   tc.c = tanh_fast(cn.c);                                         \
-  hn.c = rna_tf32(og.c * tc.c);
+  hn.c = FX ? f16r(og.c * tc.c) : rna_tf32(og.c * tc.c);
           DGC_LSTM_CELL(x) DGC_LSTM_CELL(y) DGC_LSTM_CELL(z) DGC_LSTM_CELL(w)
 #undef DGC_LSTM_CELL
           constexpr int kSF = tc_save_floats<H>();
@@ -660,6 +751,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
             st4(sv + 6 * H, tc);
           }
           st4(h_out + (int64_t)inst * ld + j, hn);
+          if (FX && h16) sth4(h16 + (int64_t)inst * H + j, hn);  // the next layer's fp16 x
           // c leaves the kernel only where a run ends (the carries other devices
           // read); inside a run it lives in creg and in the successor's c_in save
           if (!(has_next && n_mk)) st4(c_out + (int64_t)inst * ld + j, cn);
@@ -669,7 +761,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           float4 v;
           if (n_ci >= 0) {
             v = f4(carry + (int64_t)n_ci * 2 * H + j);
-            v = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
+            if (!FX) v = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
           } else {
             v = make_float4(hn.x * m_next, hn.y * m_next, hn.z * m_next, hn.w * m_next);
           }
@@ -699,16 +791,19 @@ int launch_lstm_tc2v_ew(const CUtensorMap& m, const CUtensorMap& mwx, const CUte
                         const float* bias, const float* gx, const int32_t* slot_row,
                         const uint8_t* slot_mask, const int32_t* slot_carry, const float* carry,
                         int64_t R, int L, int64_t ld, float* h_out, float* c_out, float* save,
-                        int rq, cudaStream_t s) {
-  const size_t smem = (size_t)(H / BK) * BM * 128 + (size_t)kStages * 2 * H * 128 +
-                      (FX ? (size_t)kStages * BM * 128 : 0) + (size_t)EW * 4 * 8 * 16 * 4 +
+                        int rq, cudaStream_t s, const float* Uw = nullptr,
+                        const float* Wxw = nullptr, __half* h16 = nullptr) {
+  // FX: fp16 h tile + resident fp16 U^T / Wx^T halves + one x stage
+  const size_t smem = (FX ? (size_t)2 * BM * 128 + (size_t)2 * 2 * 2 * H * 128 + (size_t)BM * 128
+                         : (size_t)(H / BK) * BM * 128 + (size_t)kStages * 2 * H * 128) +
+                      (size_t)EW * ((FX && EW > 12) ? 2 : 4) * 8 * 16 * 4 +
                       (size_t)EW * (H / 32) * 32 * 16 + 1024 + 256;
   auto kern = lstm_fwd_tc2v_kernel<H, EW, FX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_fwd_tc2v: set smem");
   const int grid = 2 * (int)cluster_tiles(R);
   kern<<<grid, 64 + 32 * EW, smem, s>>>(m, mwx, mx, bias, gx, slot_row, slot_mask, slot_carry,
-                                        carry, R, L, ld, h_out, c_out, save, rq);
+                                        carry, R, L, ld, h_out, c_out, save, rq, Uw, Wxw, h16);
   DGC_CHECK_LAUNCH("lstm_fwd_tc2v_kernel");
   return DGC_OK;
 }
@@ -733,22 +828,22 @@ int launch_lstm_tc2v(const float* gx, const float* Ut, const int32_t* slot_row,
 
 // Fused input projection (H = F = 128): x [n, F] (row stride ldx), WxT [4H, F],
 // Ut [4H, H], bias [4H]; no gx.
-int launch_lstm_tc2x(const float* x, int64_t ldx, int64_t n_x, const float* WxT, const float* Ut,
+int launch_lstm_tc2x(const void* x16, int64_t n_x, const float* Wx, const float* U,
                      const float* bias, const int32_t* slot_row, const uint8_t* slot_mask,
                      const int32_t* slot_carry, const float* carry, int64_t R, int L, int64_t ld,
-                     float* h_out, float* c_out, float* save, cudaStream_t s) {
+                     float* h_out, float* c_out, float* save, __half* h16, cudaStream_t s) {
   constexpr int H = 128;
-  CUtensorMap m, mwx, mx;
-  int rc = make_map(&m, Ut, 4 * H, H, H, 32, H / 2, false);
-  if (!rc) rc = make_map(&mwx, WxT, 4 * H, H, H, 32, H / 2, false);
-  if (!rc) rc = make_gather_map(&mx, x, n_x, H, ldx, 32);
+  CUtensorMap mx;  // (the fp32 weight maps of the other instantiations are unused here)
+  int rc = make_gather_map_f16(&mx, x16, n_x, H, H);
   if (rc) return rc;
   const int rq = cluster_rows_per_quadrant(R);
   if (rq <= 24 && !getenv("DGC_RNN_EW16"))
-    return launch_lstm_tc2v_ew<H, 12, true>(m, mwx, mx, bias, nullptr, slot_row, slot_mask,
-                                            slot_carry, carry, R, L, ld, h_out, c_out, save, rq, s);
-  return launch_lstm_tc2v_ew<H, 16, true>(m, mwx, mx, bias, nullptr, slot_row, slot_mask,
-                                          slot_carry, carry, R, L, ld, h_out, c_out, save, rq, s);
+    return launch_lstm_tc2v_ew<H, 12, true>(mx, mx, mx, bias, nullptr, slot_row, slot_mask,
+                                            slot_carry, carry, R, L, ld, h_out, c_out, save, rq, s,
+                                            U, Wx, h16);
+  return launch_lstm_tc2v_ew<H, 16, true>(mx, mx, mx, bias, nullptr, slot_row, slot_mask,
+                                          slot_carry, carry, R, L, ld, h_out, c_out, save, rq, s, U,
+                                          Wx, h16);
 }
 
 // ---------------------------------------------------------------------------
@@ -1008,27 +1103,26 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 // (rq <= 24) sizes the receive tiles for 24 rows and spends the freed shared
 // memory on 6 A stages, so the second chunk's da rarely waits for the MMA to
 // drain the first chunk's stages.
-template <int kVEW> __host__ __device__ constexpr int ks_a_stages() { return kVEW <= 12 ? 6 : 4; }
+template <int kVEW> __host__ __device__ constexpr int ks_a_stages() { return kVEW <= 12 ? 5 : 3; }
 template <int kVEW> __host__ __device__ constexpr int ks_recv_rq() { return kVEW <= 12 ? 24 : 32; }
-constexpr int kKsBStages = 3;
 constexpr int kKsStgStride = 64 + 4;  // own-half staging row stride (floats, 16-B aligned)
 template <int H, int kVEW>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
-    lstm_bwd_tc2k_kernel(const __grid_constant__ CUtensorMap tmU, const int32_t* __restrict__ slot_row,
+    lstm_bwd_tc2k_kernel(const float* __restrict__ U, const int32_t* __restrict__ slot_row,
                          const uint8_t* __restrict__ slot_mask, int64_t R, int L,
                          const float* __restrict__ save, const float* __restrict__ dh_out,
                          float* __restrict__ dgx, int rnd, float* __restrict__ bias_partial,
-                         int rq) {
+                         int rq, float da_scale) {
   static_assert(H == 128, "K-split cluster BPTT is specialised for H = 128");
   constexpr int EW = kVEW;
   constexpr int kEpiT = 32 * EW;
   constexpr int RPW = 8;                     // rows per warp
-  constexpr bool kHoist = EW <= 12;          // all of a position's loads issued at its start
+  constexpr bool kHoist = EW <= 12;          // chunk 0's loads issued at the position start
   constexpr int G4 = 4 * H;
   constexpr int HU = H / 2;
-  constexpr int KBO = 8;                     // own da k-blocks per position
-  constexpr int kAStage = BM * 128;          // 128 rows x 32 gate columns
-  constexpr int kBStage = H * 128;           // H units x 32 gate columns of U
+  constexpr int KBO = 4;                     // own fp16 da k-blocks (64 gate columns) per position
+  constexpr int kAStage = BM * 128;          // 128 rows x 64 fp16 gate columns
+  constexpr int kUBytes = KBO * H * 128;     // resident fp16 B: H units x 256 own gate columns
   constexpr int kS = kKsStgStride;
   constexpr int kStgW = RPW * kS;
   static_assert(kStgW >= 8 * 32, "staging must hold the warp's bias partials");
@@ -1042,17 +1136,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   // addressing: STS/LDS instead of generic ST/LD)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
-  uint8_t* sB = sA + kKsAStages * kAStage;
-  float* recv = reinterpret_cast<float*>(sB + kKsBStages * kBStage);  // [2][4 kRQ][HU]
+  uint8_t* sU = sA + kKsAStages * kAStage;
+  float* recv = reinterpret_cast<float*>(sU + kUBytes);  // [2][4 kRQ][HU]
   float* stg_all = recv + 2 * kRecv;
   uint64_t* a_full = reinterpret_cast<uint64_t*>(stg_all + EW * kStgW);
   uint64_t* a_empty = a_full + kKsAStages;
-  uint64_t* b_full = a_empty + kKsAStages;
-  uint64_t* b_empty = b_full + kKsBStages;
-  uint64_t* acc_full = b_empty + kKsBStages;    // [2]
+  uint64_t* acc_full = a_empty + kKsAStages;    // [2]
   uint64_t* acc_empty = acc_full + 2;           // [2]
   uint64_t* recv_full = acc_empty + 2;          // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recv_full + 2);
+  uint64_t* u_ready = recv_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(u_ready + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cluster_rank(), peer = crank ^ 1u;
@@ -1064,17 +1157,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       mbar_init(&a_full[s], kEpiT);
       mbar_init(&a_empty[s], 1);
     }
-    for (int s = 0; s < kKsBStages; ++s) {
-      mbar_init(&b_full[s], 1);
-      mbar_init(&b_empty[s], 1);
-    }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
       mbar_init(&acc_empty[a], kEpiT);
       mbar_init(&recv_full[a], 1);  // local arrive.expect_tx + the peer's st.async bytes
     }
+    mbar_init(u_ready, 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmU) : "memory");
   }
   if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
   fence_before();
@@ -1082,21 +1171,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   cluster_sync_all();  // both CTAs' barriers initialised before any st.async
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  // own k-block i of a position: chunk lc = i >> 2 (global chunk 2*crank + lc), gate g = i & 3
+  // own gate column k (0..255) of a position: 32-column block i = k >> 5 =
+  // 4 lc + g (chunk lc: global chunk 2*crank + lc, gate g); fp16 k-block k >> 6
 
   if (warp == 0) {
-    if (lane == 0) {
-      for (int seq = 0; seq < L * KBO; ++seq) {
-        const int s = seq % kKsBStages;
-        mbar_wait(&b_empty[s], ((seq / kKsBStages) & 1) ^ 1);
-        const int i = seq % KBO, c = 2 * (int)crank + (i >> 2), g = i & 3;
-        mbar_expect_tx(&b_full[s], (uint32_t)kBStage);
-        tma_load_2d(sB + s * kBStage, &tmU, g * H + 32 * c, 0, &b_full[s]);
-      }
+    // the MMA's B operand, resident for the launch: U's 256 own gate columns for
+    // all H units as fp16, K-major SWIZZLE_128B ([4 k-blocks][H rows][128 B])
+    for (int c = lane; c < H * (4 * HU / 8); c += 32) {
+      const int n = c % H, k0 = (c / H) * 8;
+      const int i = k0 >> 5, gcol = (i & 3) * H + 32 * (2 * (int)crank + (i >> 2)) + (k0 & 31);
+      const float* src = U + (int64_t)n * G4 + gcol;
+      const float4 a = ldg4(src), b = ldg4(src + 4);
+      const uint32_t dst = smem_u32(sU) + (uint32_t)((k0 >> 6) * H * 128 + n * 128 +
+                                                     ((((k0 & 63) >> 3) ^ (n & 7)) << 4));
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(h2u(a.x, a.y)),
+                   "r"(h2u(a.z, a.w)), "r"(h2u(b.x, b.y)), "r"(h2u(b.z, b.w))
+                   : "memory");
     }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive(u_ready);
   } else if (warp == 1) {
-    const uint32_t idesc = idesc_tf32(H, false, false);
-    const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+    // dh partial = (S da)[128, own 256] x U_own^T -> TMEM (kind::f16, fp32 accumulate)
+    const uint32_t idesc16 = idesc_f16(H);
+    const uint32_t a_base = smem_u32(sA), u_base = smem_u32(sU);
+    mbar_wait(u_ready, 0);
+    fence_after();
     for (int t = 0; t < L; ++t) {
       const int p = L - 1 - t;
       const int a = p & 1;
@@ -1104,17 +1203,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       fence_after();
       for (int i = 0; i < KBO; ++i) {
         const int seq = t * KBO + i;
-        const int sa = seq % kKsAStages, sb = seq % kKsBStages;
+        const int sa = seq % kKsAStages;
         mbar_wait(&a_full[sa], (seq / kKsAStages) & 1);
-        mbar_wait(&b_full[sb], (seq / kKsBStages) & 1);
         fence_after();
         if (lane == 0) {
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk)
-            mma_tf32(tmem_base + a * H, kdesc(a_base + sa * kAStage + kk * 32),
-                     kdesc(b_base + sb * kBStage + kk * 32), idesc, (i > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < 4; ++kk)
+            mma_f16(tmem_base + a * H, kdesc(a_base + sa * kAStage + kk * 32),
+                    kdesc(u_base + i * H * 128 + kk * 32), idesc16, (i > 0 || kk > 0) ? 1u : 0u);
           mma_commit(&a_empty[sa]);
-          mma_commit(&b_empty[sb]);
           if (i == KBO - 1) mma_commit(&acc_full[a]);
         }
         __syncwarp();
@@ -1131,6 +1228,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
     const uint32_t recv_peer = map_peer(recv, peer);
     const uint32_t rfull_peer = map_peer(recv_full, peer);
     const bool active = rb < rq;
+    const float inv_scale = 1.f / da_scale;  // da_scale: a power of two
     // bytes the peer sends into our receive tile per position: 8 rows x HU per
     // active peer warp (4 quadrants x ceil(rq / 8) warps)
     const uint32_t kRecvBytes = 4u * (uint32_t)((rq + RPW - 1) / RPW) * RPW * HU * 4u;
@@ -1242,7 +1340,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       }
 #pragma unroll
       for (int lc = 0; lc < 2; ++lc) {
-        const int seq0 = t * KBO + lc * 4;
+        const int seq0 = t * KBO + lc * 2;   // this chunk's 2 fp16 k-blocks (gates 0-1, 2-3)
         const int jo = 32 * lc + 4 * u8;     // own unit index of this lane's 4 units
         if (!kHoist || lc == 1) {
 #pragma unroll
@@ -1250,11 +1348,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
             load_fields(lc, it, dho[lc][it], cvv[lc][it], gv0[lc][it], gv1[lc][it]);
         }
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
+        for (int g = 0; g < 2; ++g) {
           const int seq = seq0 + g;
           mbar_wait(&a_empty[seq % kKsAStages], ((seq / kKsAStages) & 1) ^ 1);
         }
-#pragma unroll
 #pragma unroll
         for (int it = 0; it < 2; ++it) {
           const int rl = rb + 4 * it + r4;
@@ -1263,7 +1360,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           if (has_next) {
             const float4 a = lds4(stg_s + (uint32_t)(((4 * it + r4) * kS + jo) * 4));
             const float4 b = lds4(recv_s + (uint32_t)((((t & 1) * kRecv) + (q * kRQ + rl) * HU + jo) * 4));
-            const float mn = mnext[it];
+            const float mn = mnext[it] * inv_scale;  // the partials are S-scaled (exact)
             dh = make_float4(mn * (a.x + b.x), mn * (a.y + b.y), mn * (a.z + b.z), mn * (a.w + b.w));
           }
           float4 da[4] = {zero4(), zero4(), zero4(), zero4()};
@@ -1306,16 +1403,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
             }
           }
           dcr[lc][it] = dcp;
-          const uint32_t off0 = sw128_offset(r, 4 * u8);
+          // S da as fp16 into the A tiles: gate g -> k-block seq0 + g/2, columns
+          // 32 (g & 1) + 4 u8 .. +3 of its 64 (8 B of a 16-B swizzle chunk)
 #pragma unroll
-          for (int g = 0; g < 4; ++g)
-            sts4(sA_s + (uint32_t)(((seq0 + g) % kKsAStages) * kAStage) + off0, da[g]);
+          for (int g = 0; g < 4; ++g) {
+            const int k16 = (g & 1) * 32 + 4 * u8;
+            const uint32_t addr = sA_s + (uint32_t)(((seq0 + (g >> 1)) % kKsAStages) * kAStage) +
+                                  (uint32_t)(r * 128 + ((((k16 >> 3) ^ (r & 7))) << 4) + (k16 & 7) * 2);
+            asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr),
+                         "r"(h2u(da[g].x * da_scale, da[g].y * da_scale)),
+                         "r"(h2u(da[g].z * da_scale, da[g].w * da_scale))
+                         : "memory");
+          }
         }
         fence_async_smem();
         DGC_TS(lc == 1 && blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 2);
         DGC_TS(lc == 0 && blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 5);
 #pragma unroll
-        for (int g = 0; g < 4; ++g) mbar_arrive(&a_full[(seq0 + g) % kKsAStages]);
+        for (int g = 0; g < 2; ++g) mbar_arrive(&a_full[(seq0 + g) % kKsAStages]);
         __syncwarp();
       }
 #pragma unroll
@@ -1359,36 +1464,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
 }
 
 template <int H, int EW>
-int launch_lstm_bwd_tc2k_ew(const CUtensorMap& m, const int32_t* slot_row, const uint8_t* slot_mask,
+int launch_lstm_bwd_tc2k_ew(const float* U, const int32_t* slot_row, const uint8_t* slot_mask,
                             int64_t R, int L, const float* save, const float* dh_out, float* dgx,
-                            int rnd, float* bias_partial, int rq, cudaStream_t s) {
-  const size_t smem = (size_t)ks_a_stages<EW>() * BM * 128 + (size_t)kKsBStages * H * 128 +
+                            int rnd, float* bias_partial, int rq, float da_scale, cudaStream_t s) {
+  const size_t smem = (size_t)ks_a_stages<EW>() * BM * 128 + (size_t)4 * H * 128 +
                       (size_t)2 * 4 * ks_recv_rq<EW>() * (H / 2) * 4 + (size_t)EW * 8 * kKsStgStride * 4 +
                       1024 + 512;
   auto kern = lstm_bwd_tc2k_kernel<H, EW>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_bwd_tc2k: set smem");
   const int grid = 2 * (int)cluster_tiles(R);
-  kern<<<grid, 64 + 32 * EW, smem, s>>>(m, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
-                                        bias_partial, rq);
+  kern<<<grid, 64 + 32 * EW, smem, s>>>(U, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
+                                        bias_partial, rq, da_scale);
   DGC_CHECK_LAUNCH("lstm_bwd_tc2k_kernel");
   return DGC_OK;
 }
 
+// da_scale: power of two applied to da before its fp16 conversion (the MMA
+// operand) and removed exactly from the dh partials; sized by the caller to
+// the loss normalisation (mean over n instances: da ~ 1/n).
 template <int H>
 int launch_lstm_bwd_tc2k(const float* U, const int32_t* slot_row, const uint8_t* slot_mask,
                          int64_t R, int L, const float* save, const float* dh_out, float* dgx,
-                         int rnd, float* bias_partial, cudaStream_t s) {
-  CUtensorMap m;
-  int rc = make_map(&m, U, H, 4 * H, 4 * H, 32, H, false);
-  if (rc) return rc;
+                         int rnd, float* bias_partial, float da_scale, cudaStream_t s) {
   DGC_REQUIRE(R * (int64_t)L < (int64_t)INT32_MAX, "lstm_bwd_tc2k: R * L must fit int32");
   const int rq = cluster_rows_per_quadrant(R);
   if (rq <= 24 && !getenv("DGC_RNN_EW16"))
-    return launch_lstm_bwd_tc2k_ew<H, 12>(m, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
-                                          bias_partial, rq, s);
-  return launch_lstm_bwd_tc2k_ew<H, 16>(m, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
-                                        bias_partial, rq, s);
+    return launch_lstm_bwd_tc2k_ew<H, 12>(U, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
+                                          bias_partial, rq, da_scale, s);
+  return launch_lstm_bwd_tc2k_ew<H, 16>(U, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
+                                        bias_partial, rq, da_scale, s);
 }
 
 template <int H>
@@ -1457,19 +1562,18 @@ extern "C" int dgc_rnn_fwd_tc(int32_t cell, const float* gx, const float* Ut,
   }
 }
 
-extern "C" int dgc_rnn_fwd_tc_x(int32_t cell, const float* x, int64_t ldx, int64_t n_x, int32_t F,
-                                const float* WxT, const float* Ut, const float* bias,
-                                const int32_t* slot_row, const uint8_t* slot_mask,
-                                const int32_t* slot_carry, const float* carry, int64_t n_rows,
-                                int32_t row_len, int32_t H, int64_t ld_out, float* h_out,
-                                float* c_out, float* save, void* stream) {
-  DGC_REQUIRE(cell == 1, "rnn_fwd_tc_x: LSTM only");
-  DGC_REQUIRE(H == 128 && F == 128, "rnn_fwd_tc_x: fused input projection needs F = H = 128");
-  DGC_REQUIRE(cluster_rnn_enabled(), "rnn_fwd_tc_x: needs the cluster kernels (DGC_NO_CLUSTER_RNN set)");
-  DGC_REQUIRE(c_out != nullptr && bias != nullptr, "rnn_fwd_tc_x: c_out and bias required");
+extern "C" int dgc_lstm_fwd_tc_f16x(const void* x16, int64_t n_x, const float* Wx,
+                                    const float* U, const float* bias, const int32_t* slot_row,
+                                    const uint8_t* slot_mask, const int32_t* slot_carry,
+                                    const float* carry, int64_t n_rows, int32_t row_len,
+                                    int64_t ld_out, float* h_out, float* c_out, float* save,
+                                    void* h_out16, void* stream) {
+  DGC_REQUIRE(cluster_rnn_enabled(), "lstm_fwd_tc_f16x: needs the cluster kernels (DGC_NO_CLUSTER_RNN set)");
+  DGC_REQUIRE(c_out != nullptr && bias != nullptr, "lstm_fwd_tc_f16x: c_out and bias required");
   if (n_rows == 0 || row_len == 0) return DGC_OK;
-  return launch_lstm_tc2x(x, ldx, n_x, WxT, Ut, bias, slot_row, slot_mask, slot_carry, carry, n_rows,
-                          row_len, ld_out, h_out, c_out, save, dgc::as_stream(stream));
+  return launch_lstm_tc2x(x16, n_x, Wx, U, bias, slot_row, slot_mask, slot_carry, carry, n_rows,
+                          row_len, ld_out, h_out, c_out, save, static_cast<__half*>(h_out16),
+                          dgc::as_stream(stream));
 }
 
 extern "C" int dgc_rnn_fwd_tc_fused_available(int32_t F, int32_t H) {
@@ -1495,7 +1599,8 @@ extern "C" int dgc_rnn_bwd_tc(int32_t cell_flags, const float* U, const int32_t*
     case 64: return launch_lstm_bwd_tc<64>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
     case 128:
       return cluster_rnn_enabled()
-                 ? launch_lstm_bwd_tc2k<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, rnd, bias_partial, s)
+                 ? launch_lstm_bwd_tc2k<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, rnd, bias_partial,
+                                             ldexpf(1.f, (cell_flags >> 16) & 0x7f), s)
                  : launch_lstm_bwd_tc<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
     default: return dgc::fail(DGC_ERR_ARG, "rnn_bwd_tc: H must be 32, 64 or 128");
   }

@@ -4,27 +4,38 @@
 // fusion-group order, so a fused group is a contiguous row
 // segment and the whole device is one batched CSR. Each row is handled by a
 // sub-warp of LPR lanes; every lane owns NV float4 columns, so one neighbour
-// row is fetched as LPR*NV coalesced 16-byte loads (a 512-byte row at W=128
+// row is fetched as LPR*NV coalesced 16-byte loads (a 512-byte row at W = 128
 // is one fully coalesced warp transaction). Neighbour indices are broadcast
-// within the sub-warp and unrolled four deep to keep enough loads in flight
-// for the degree-skewed hub rows; the reduction order is the CSR order, so
-// the result is bitwise deterministic (no atomics).
+// within the sub-warp and unrolled kUnr deep; the reduction order is the CSR
+// order, so the result is bitwise deterministic (no atomics).
+//
+// The gather is latency-bound on the neighbour rows served by L2, so the
+// kernel is held to 32 registers (8 resident 256-thread CTAs = 64 warps per
+// SM) and the grid is exactly the resident capacity (a partial second wave
+// doubled the time when a variant needed 40 registers). Measured on B200 at
+// C2/C3 (tools/time_spmm.py, profiles/r2_summary.md): unroll 2 beats 4 and 8;
+// a bf16 gathered operand (half the bytes) was no faster, and TMA tile::gather4
+// staging of the neighbour rows in shared memory tops out near 8.9 TB/s of
+// 512-B row copies (tools/probes/tma_rate.cu), below this register gather.
 //
 // Semantics replace the analytic structure-encoder cost of the reference
 // (costmodel.py:259-263 via sim.py:339-360,485-486) with real arithmetic:
-//   out[i] = act( dinv[i] * sum_{c in row i} dinv[c] * Y[c] + bias ).
+//   out[i] = act( dinv[i] * sum_{c in row i} dinv[c] * Y[c] + bias ),
+// optionally also written as fp16 to out16 (the fused recurrence's x operand).
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace {
 
 constexpr int kUnr = 2;  // neighbours per batch of loads
 
-template <int LPR, int NV>
-__global__ void __launch_bounds__(256) spmm_csr_kernel(
+template <int LPR, int NV, bool F16>
+__global__ void __launch_bounds__(256, NV == 1 ? 8 : 4) spmm_csr_kernel(
     const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
     const float* __restrict__ dinv, const float4* __restrict__ Y,
-    const float* __restrict__ bias, float4* __restrict__ out, const int32_t* __restrict__ rows,
-    int64_t n_rows, int64_t row_begin, int act) {
+    const float* __restrict__ bias, float4* __restrict__ out, __half* __restrict__ out16,
+    const int32_t* __restrict__ rows, int64_t n_rows, int64_t row_begin, int act) {
   constexpr int W4 = LPR * NV;  // float4 per row
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = (int)(tid % LPR);
@@ -94,34 +105,55 @@ __global__ void __launch_bounds__(256) spmm_csr_kernel(
         o.w = dgc::rna_tf32_f(o.w);
       }
       out[row * W4 + j4] = o;
+      if (F16) {
+        const __half2 a = __floats2half2_rn(o.x, o.y), h = __floats2half2_rn(o.z, o.w);
+        reinterpret_cast<uint2*>(out16)[row * W4 + j4] =
+            make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&h));
+      }
     }
   }
 }
 
-template <int LPR, int NV>
+template <int LPR, int NV, bool F16>
 int launch(const int32_t* rp, const int32_t* col, const float* dinv, const float* Y,
-           const float* bias, float* out, const int32_t* rows, int64_t n, int64_t row_begin,
-           int act, cudaStream_t s) {
+           const float* bias, float* out, __half* out16, const int32_t* rows, int64_t n,
+           int64_t row_begin, int act, cudaStream_t s) {
   const int block = 256;
-  const int grid = dgc::grid_for(n * LPR, block, 8);
-  spmm_csr_kernel<LPR, NV><<<grid, block, 0, s>>>(rp, col, dinv,
-                                                  reinterpret_cast<const float4*>(Y), bias,
-                                                  reinterpret_cast<float4*>(out), rows, n,
-                                                  row_begin, act);
+  static const int resident = [] {  // CTAs per SM at this instantiation's register count
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, spmm_csr_kernel<LPR, NV, F16>, 256, 0) !=
+            cudaSuccess || b < 1)
+      b = 1;
+    return b;
+  }();
+  const int grid = dgc::grid_for(n * LPR, block, resident);
+  spmm_csr_kernel<LPR, NV, F16><<<grid, block, 0, s>>>(
+      rp, col, dinv, reinterpret_cast<const float4*>(Y), bias, reinterpret_cast<float4*>(out),
+      out16, rows, n, row_begin, act);
   DGC_CHECK_LAUNCH("spmm_csr_kernel");
   return DGC_OK;
 }
 
+template <int LPR, int NV>
+int launch_f(const int32_t* rp, const int32_t* col, const float* dinv, const float* Y,
+             const float* bias, float* out, __half* out16, const int32_t* rows, int64_t n,
+             int64_t row_begin, int act, cudaStream_t s) {
+  return out16 ? launch<LPR, NV, true>(rp, col, dinv, Y, bias, out, out16, rows, n, row_begin, act, s)
+               : launch<LPR, NV, false>(rp, col, dinv, Y, bias, out, nullptr, rows, n, row_begin, act, s);
+}
+
 }  // namespace
 
-extern "C" int dgc_spmm_csr_rows(const int32_t* row_ptr, const int32_t* col, const float* dinv,
-                                 const float* Y, const float* bias, float* out,
-                                 const int32_t* rows, int64_t n_rows, int64_t row_begin,
-                                 int32_t width, int32_t act, void* stream) {
+extern "C" int dgc_spmm_csr_x(const int32_t* row_ptr, const int32_t* col, const float* dinv,
+                              const float* Y, const float* bias, float* out, void* out16,
+                              const int32_t* rows, int64_t n_rows, int64_t row_begin,
+                              int32_t width, int32_t act, void* stream) {
   DGC_REQUIRE(width > 0 && width % 4 == 0, "spmm: width must be a positive multiple of 4");
   if (n_rows == 0) return DGC_OK;
   cudaStream_t s = dgc::as_stream(stream);
-#define DGC_SPMM_L(LPR, NV) launch<LPR, NV>(row_ptr, col, dinv, Y, bias, out, rows, n_rows, row_begin, act, s)
+  __half* o16 = static_cast<__half*>(out16);
+#define DGC_SPMM_L(LPR, NV) \
+  launch_f<LPR, NV>(row_ptr, col, dinv, Y, bias, out, o16, rows, n_rows, row_begin, act, s)
   switch (width) {
     case 4: return DGC_SPMM_L(1, 1);
     case 8: return DGC_SPMM_L(2, 1);
@@ -136,9 +168,17 @@ extern "C" int dgc_spmm_csr_rows(const int32_t* row_ptr, const int32_t* col, con
 #undef DGC_SPMM_L
 }
 
+extern "C" int dgc_spmm_csr_rows(const int32_t* row_ptr, const int32_t* col, const float* dinv,
+                                 const float* Y, const float* bias, float* out,
+                                 const int32_t* rows, int64_t n_rows, int64_t row_begin,
+                                 int32_t width, int32_t act, void* stream) {
+  return dgc_spmm_csr_x(row_ptr, col, dinv, Y, bias, out, nullptr, rows, n_rows, row_begin, width,
+                        act, stream);
+}
+
 extern "C" int dgc_spmm_csr(const int32_t* row_ptr, const int32_t* col, const float* dinv,
                             const float* Y, const float* bias, float* out, int64_t n_rows,
                             int32_t width, int32_t act, void* stream) {
-  return dgc_spmm_csr_rows(row_ptr, col, dinv, Y, bias, out, nullptr, n_rows, 0, width, act,
-                           stream);
+  return dgc_spmm_csr_x(row_ptr, col, dinv, Y, bias, out, nullptr, nullptr, n_rows, 0, width, act,
+                        stream);
 }

@@ -133,6 +133,17 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(accum));
 }
+// Instruction descriptor: D f32, A/B fp16 (K-major), M=128, N=n.
+__host__ __device__ constexpr uint32_t idesc_f16(int n) {
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -242,6 +253,12 @@ __device__ __forceinline__ void st_cluster_v4(uint32_t addr, float4 v) {
 // Asynchronous 16-byte store into a peer CTA's shared memory; its completion
 // is a complete_tx (release, cluster scope) of 16 bytes on the peer's mbarrier
 // `mbar` (shared::cluster address): no fence on the writer side.
+__device__ __forceinline__ void st_async_v2(uint32_t addr, uint2 v, uint32_t mbar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];" ::"r"(addr),
+      "r"(v.x), "r"(v.y), "r"(mbar)
+      : "memory");
+}
 __device__ __forceinline__ void st_async_v4(uint32_t addr, float4 v, uint32_t mbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];"
                ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(mbar)
@@ -343,6 +360,25 @@ inline int make_gather_map(CUtensorMap* map, const float* ptr, int64_t rows, int
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return dgc::fail(DGC_ERR_CUDA, "cuTensorMapEncodeTiled (gather) failed");
+  return DGC_OK;
+}
+
+// Row gathers (tile::gather4) of a row-major [rows, cols] fp16 tensor: boxes of
+// 64 columns (128 B) x 1 row, SWIZZLE_128B (the K-major UMMA operand layout).
+inline int make_gather_map_f16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols,
+                               int64_t ld) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return dgc::fail(DGC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || ((ld * 2) & 15))
+    return dgc::fail(DGC_ERR_ARG, "gather map: 16-byte aligned base and row stride required");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {64, 1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return dgc::fail(DGC_ERR_CUDA, "cuTensorMapEncodeTiled (fp16 gather) failed");
   return DGC_OK;
 }
 

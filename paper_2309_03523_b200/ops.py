@@ -77,7 +77,7 @@ def _req(t, dtype, name):
         raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
 
 
-def spmm_csr(row_ptr, col, dinv, Y, bias, out, act: int, nnz=0, n_cols=0):
+def spmm_csr(row_ptr, col, dinv, Y, bias, out, act: int, nnz=0, n_cols=0, out16=None):
     """K1 dgc_spmm_csr: out = act(dinv_i * sum_c dinv_c Y_c + bias).
     Algorithmic bytes: 4W(n_cols + n_rows) + 4(n_rows+1)
     + 4 nnz (+ 4 n_cols for dinv)."""
@@ -85,15 +85,15 @@ def spmm_csr(row_ptr, col, dinv, Y, bias, out, act: int, nnz=0, n_cols=0):
     _req(Y, torch.float32, "Y"); _req(out, torch.float32, "out")
     n = row_ptr.numel() - 1
     W = out.shape[-1] if out.dim() > 1 else 1
-    nb = 4 * W * (n_cols + n) + 4 * (n + 1) + 4 * nnz + 4 * n_cols
-    _run("spmm_csr", lambda: _native.check(_native.lib().dgc_spmm_csr(
-        _p(row_ptr), _p(col), _p(dinv), _p(Y), _p(bias), _p(out), n, W, act, _stream()),
-        "dgc_spmm_csr"), nb, 2 * nnz * W)
+    nb = 4 * W * (n_cols + n) + 4 * (n + 1) + 4 * nnz + 4 * n_cols + (2 * W * n if out16 is not None else 0)
+    _run("spmm_csr", lambda: _native.check(_native.lib().dgc_spmm_csr_x(
+        _p(row_ptr), _p(col), _p(dinv), _p(Y), _p(bias), _p(out), _p(out16), None, n, 0, W, act,
+        _stream()), "dgc_spmm_csr_x"), nb, 2 * nnz * W)
     return out
 
 
 def spmm_csr_rows(row_ptr, col, dinv, Y, bias, out, act: int, rows=None, n_rows=0, row_begin=0,
-                  nnz=0, n_cols=0, name="spmm_csr"):
+                  nnz=0, n_cols=0, name="spmm_csr", out16=None):
     """K1 over a row subset (dgc_spmm_csr_rows): the rows of the int32 list
     ``rows``, or the range [row_begin, row_begin + n_rows). nnz / n_cols: the
     subset's nonzeros and distinct gathered columns (algorithmic bytes)."""
@@ -101,10 +101,10 @@ def spmm_csr_rows(row_ptr, col, dinv, Y, bias, out, act: int, rows=None, n_rows=
     _req(Y, torch.float32, "Y"); _req(out, torch.float32, "out"); _req(rows, torch.int32, "rows")
     n = rows.numel() if rows is not None else int(n_rows)
     W = out.shape[-1] if out.dim() > 1 else 1
-    nb = 4 * W * (n_cols + n) + 8 * n + 4 * nnz + 4 * n_cols
-    _run(name, lambda: _native.check(_native.lib().dgc_spmm_csr_rows(
-        _p(row_ptr), _p(col), _p(dinv), _p(Y), _p(bias), _p(out), _p(rows), n, int(row_begin), W,
-        act, _stream()), "dgc_spmm_csr_rows"), nb, 2 * nnz * W)
+    nb = 4 * W * (n_cols + n) + 8 * n + 4 * nnz + 4 * n_cols + (2 * W * n if out16 is not None else 0)
+    _run(name, lambda: _native.check(_native.lib().dgc_spmm_csr_x(
+        _p(row_ptr), _p(col), _p(dinv), _p(Y), _p(bias), _p(out), _p(out16), _p(rows), n,
+        int(row_begin), W, act, _stream()), "dgc_spmm_csr_x"), nb, 2 * nnz * W)
     return out
 
 
@@ -291,26 +291,29 @@ def rnn_fwd_tc_fused_available(F, H):
     return bool(_native.lib().dgc_rnn_fwd_tc_fused_available(F, H))
 
 
-def rnn_fwd_tc_x(x, ldx, WxT, Ut, bias, slot_row, slot_mask, slot_carry, carry, n_rows, row_len,
-                 H, ld_out, h_out, c_out, save, c_rows=None):
-    """K4 on tcgen05 with the input projection fused (dgc_rnn_fwd_tc_x): the
-    x rows of each position are TMA-gathered and multiplied by Wx^T in TMEM
-    next to h U^T; no gx round trip through HBM."""
-    _req(x, torch.float32, "x"); _req(WxT, torch.float32, "WxT"); _req(Ut, torch.float32, "Ut")
-    n_inst, F = h_out.shape[0], WxT.shape[1]
+def lstm_fwd_tc_f16x(x16, Wx, U, bias, slot_row, slot_mask, slot_carry, carry, n_rows, row_len,
+                     H, ld_out, h_out, c_out, save, h_out16=None, c_rows=None):
+    """K4 on tcgen05 with the input projection fused (dgc_lstm_fwd_tc_f16x): the
+    fp16 x rows of each position are TMA-gathered and multiplied by Wx^T in TMEM
+    next to h U^T, both weight halves resident in shared memory as fp16; no gx
+    round trip through HBM and no weight traffic per position."""
+    if x16.dtype != torch.float16 or not x16.is_cuda:
+        raise ValueError("x16 must be a CUDA fp16 tensor")
+    _req(Wx, torch.float32, "Wx"); _req(U, torch.float32, "U")
+    n_inst, F = h_out.shape[0], Wx.shape[0]
     G = 4
-    sf = rnn_save_floats(1, H)
-    # reads x (F); writes the save row (h_in fp32 + c_in, i, f, g, o fp16: sf
-    # floats; tanh(c) is recomputed by the BPTT), h, and c at the run ends
+    # reads x (fp16); writes the save row (h_in fp32 + c_in, i, f, g, o fp16: sf
+    # floats; tanh(c) is recomputed by the BPTT), h (+ its fp16 copy), and c at
+    # the run ends
     sf = rnn_tc_save_floats(H)
     c_rows = n_inst if c_rows is None else c_rows
-    nb = (4 * n_inst * (F + sf + H) + 4 * c_rows * H + 9 * n_rows * row_len
-          + 4 * G * H * (H + F))
+    nb = (n_inst * (2 * F + 4 * sf + 4 * H + (2 * H if h_out16 is not None else 0))
+          + 4 * c_rows * H + 9 * n_rows * row_len + 4 * G * H * (H + F))
     _run("lstm_fwd_tc", lambda: _native.check(
-        _native.lib().dgc_rnn_fwd_tc_x(1, _p(x), ldx, x.shape[0], F, _p(WxT), _p(Ut), _p(bias),
-                                       _p(slot_row), _p(slot_mask), _p(slot_carry), _p(carry),
-                                       n_rows, row_len, H, ld_out, _p(h_out), _p(c_out), _p(save),
-                                       _stream()), "dgc_rnn_fwd_tc_x"),
+        _native.lib().dgc_lstm_fwd_tc_f16x(_p(x16), x16.shape[0], _p(Wx), _p(U), _p(bias),
+                                           _p(slot_row), _p(slot_mask), _p(slot_carry), _p(carry),
+                                           n_rows, row_len, ld_out, _p(h_out), _p(c_out), _p(save),
+                                           _p(h_out16), _stream()), "dgc_lstm_fwd_tc_f16x"),
         nb, 2.0 * n_rows * row_len * H * G * (H + F))
 
 

@@ -257,9 +257,13 @@ class Shard:
         self.Ut = torch.zeros((GH, H), **f32)
         self.Ut_f = [torch.zeros((GH, H), **f32) for _ in range(cfg.n_rnn)] if self.tc_rnn else None
         # fused input projection (F = H = 128 cluster recurrence): no gx tensor
+        self.da_exp = min(100, max(0, int(round(math.log2(max(self.n_total, 1))))))
         self.fused_xproj = (self.tc_rnn and cfg.rnn == "lstm" and self.R > 0
                             and ops.rnn_fwd_tc_fused_available(H, H))
-        self.WxT_f = [torch.zeros((GH, H), **f32) for _ in range(cfg.n_rnn)] if self.fused_xproj else None
+        # fp16 copies of each LSTM layer's input (the fused recurrence's gathered x):
+        # written by the last GCN SpMM (layer 1) and by the previous LSTM layer
+        self.x16 = ([torch.zeros((n, H), dtype=torch.float16, device=dev) for _ in range(cfg.n_rnn)]
+                    if self.fused_xproj else None)
         if self.tc_rnn:
             self.rnn_dc_scratch = torch.zeros(((max(self.R, 1) + 127) // 128 * 128, H), **f32)
             self.rnn_tc_prows = ops.rnn_tc_tiles(max(self.R, 1), H)
@@ -356,6 +360,10 @@ class Shard:
         o, shape = self.offs[name]
         n = int(np.prod(shape))
         return self.params[o:o + n].view(*shape)
+
+    def _x16_out(self, l):
+        """fp16 copy target of GCN layer l's output: the first LSTM layer's x16."""
+        return self.x16[0] if (self.x16 is not None and l == 1 and not self.evolve) else None
 
     def pr(self, name):
         """GEMM operand view of a parameter (TF32-rounded copy in TF32 mode)."""
@@ -489,17 +497,17 @@ class Shard:
                 # interior rows need no halo row: they aggregate while the exchange flies
                 ops.spmm_csr_rows(self.row_ptr, self.col, self.dinv, Y, self.p(b), self.Hl[l],
                                   act=1 | rnd2, rows=self.rows_int, nnz=self.nnz_int,
-                                  n_cols=self.rows_int.numel())
+                                  n_cols=self.rows_int.numel(), out16=self._x16_out(l))
                 ev = yield from self._land(xp, tok, H, Y)
                 info["rows"] += sum(xp.sent_host)
                 info["xbytes"] += sum(xp.sent_host) * (H + 4) * 4
                 self._wait(ev)
                 ops.spmm_csr_rows(self.row_ptr, self.col, self.dinv, Y, self.p(b), self.Hl[l],
                                   act=1 | rnd2, rows=self.rows_bnd, nnz=self.nnz_bnd,
-                                  n_cols=self.nh + self.rows_bnd.numel())
+                                  n_cols=self.nh + self.rows_bnd.numel(), out16=self._x16_out(l))
             else:
                 ops.spmm_csr(self.row_ptr, self.col, self.dinv, Y, self.p(b), self.Hl[l],
-                             act=1 | rnd2, nnz=self.nnz, n_cols=self.nloc)
+                             act=1 | rnd2, nnz=self.nnz, n_cols=self.nloc, out16=self._x16_out(l))
             hin, ldin, kin = self.Hl[l], H, H
         # ---------------- forward: time encoder ----------------
         xr, ldx = self.Hl[1], H
@@ -507,13 +515,14 @@ class Shard:
             hb = self.hbuf[k]
             c_out = hb[:, H:] if cell == 1 else None
             if self.fused_xproj:
-                # x Wx + h U + b in one tensor-core recurrence (no gx round trip)
-                ops.transpose(self.pr(f"U{k}"), self.Ut_f[k])
-                ops.transpose(self.pr(f"Wx{k}"), self.WxT_f[k])
-                ops.rnn_fwd_tc_x(xr, ldx, self.WxT_f[k], self.Ut_f[k], self.p(f"br{k}"),
-                                 self.slot_row, self.slot_mask, self.slot_carry, self.carry[k],
-                                 self.R, self.L, H, self.hw, hb, c_out, self.save[k],
-                                 c_rows=self.n_run_ends)
+                # x Wx + h U + b in one tensor-core recurrence (fp16 operands,
+                # resident weights; no gx round trip)
+                ops.lstm_fwd_tc_f16x(self.x16[k], self.p(f"Wx{k}"), self.p(f"U{k}"),
+                                     self.p(f"br{k}"), self.slot_row, self.slot_mask,
+                                     self.slot_carry, self.carry[k], self.R, self.L, H, self.hw,
+                                     hb, c_out, self.save[k],
+                                     h_out16=self.x16[k + 1] if k + 1 < cfg.n_rnn else None,
+                                     c_rows=self.n_run_ends)
             elif self.tc_rnn:
                 ops.gemm(xr, self.pr(f"Wx{k}"), self.gx, n, GH, H, lda=ldx, precision=prec,
                          bias=self.p(f"br{k}"))
@@ -558,7 +567,10 @@ class Shard:
                      precision=prec)
         for k in reversed(range(cfg.n_rnn if not self.evolve else 0)):
             if self.tc_rnn:
-                ops.rnn_bwd_tc(cell | rflag, self.pr(f"U{k}"), self.slot_row, self.slot_mask,
+                # the H = 128 cluster BPTT multiplies fp16 S*da by resident fp16 U:
+                # S = 2^round(log2 n_total) lifts da ~ 1/n_total into fp16's normal range
+                ops.rnn_bwd_tc(cell | rflag | (self.da_exp << 16), self.pr(f"U{k}"), self.slot_row,
+                               self.slot_mask,
                                self.R, self.L, H, self.save[k], self.dh, self.dgx,
                                self.rnn_dc_scratch, bias_partial=self.bp_r[k])
                 rjobs.append((self.bp_r[k], self.rnn_tc_prows, GH, self.g(f"br{k}")))

@@ -495,11 +495,13 @@ def test_lstm_fwd_tensor_core_matches_simt(H, ew16, monkeypatch):
 
 @pytest.mark.parametrize("n_seq,carry_frac", [(700, 0.3), (9000, 0.0), (16000, 0.1)])
 def test_lstm_fwd_fused_projection_matches_two_step(n_seq, carry_frac):
-    """The fused-projection forward (x rows TMA-gathered by slot_row, x Wx^T +
-    h U^T + b in TMEM) equals gx = x Wx + b (K2) followed by the unfused
-    tensor-core forward: h|c and every saved field, TF32 both ways. 16000
-    sequences -> R > 7104 packed rows -> rq > 24 rows per lane quadrant (the
-    16-epilogue-warp variants)."""
+    """The fused-projection forward (fp16 x rows TMA-gathered by slot_row, x
+    Wx^T + h U^T + b in TMEM from resident fp16 weights) equals gx = x Wx + b
+    (K2) followed by the unfused TF32 tensor-core forward: h|c and every saved
+    field (the operands are TF32-rounded, so their fp16 copies are exact; fp16
+    and TF32 carry the same 10-bit mantissa). The fp16 copy of h_out is h_out.
+    16000 sequences -> R > 7104 packed rows -> rq > 24 rows per lane quadrant
+    (the 16-epilogue-warp variants)."""
     from paper_2309_03523_b200 import ops
     from paper_2309_03523_b200.layout import pack_sequences_native
     H = 128
@@ -528,14 +530,16 @@ def test_lstm_fwd_fused_projection_matches_two_step(n_seq, carry_frac):
     sr, sm, sc = t(slot_row.reshape(-1), torch.int32), t(mask.reshape(-1), torch.uint8), \
         t(slot_carry.reshape(-1), torch.int32)
     Ut = U.t().contiguous()
-    WxT = Wx.t().contiguous()
     outs = []
     for fused in (False, True):
         hc = torch.zeros((n, 2 * H), device=dev)
         save = torch.zeros((n, ops.rnn_tc_save_floats(H)), device=dev)
         if fused:
-            ops.rnn_fwd_tc_x(x, 2 * H, WxT, Ut, b, sr, sm, sc, carry, R, L, H, 2 * H, hc, hc[:, H:],
-                             save)
+            h16 = torch.zeros((n, H), dtype=torch.float16, device=dev)
+            ops.lstm_fwd_tc_f16x(x[:, :H].half(), Wx, U, b, sr, sm, sc, carry, R, L, H, 2 * H, hc,
+                                 hc[:, H:], save, h_out16=h16)
+            torch.cuda.synchronize()
+            assert torch.equal(h16.float(), hc[:, :H])
         else:
             gx = torch.zeros((n, 4 * H), device=dev)
             ops.gemm(x, Wx, gx, n, 4 * H, H, lda=2 * H, precision=1, bias=b)

@@ -1,18 +1,13 @@
-# quick GPU check: LSTM kernel tests + C2 trainer parity + bench + BPTT timeline
-mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_kernels.py -q -x -k "lstm" 2>&1 | tail -3
+timeout 900 python -m pytest tests/test_gpu_kernels.py -q -x 2>&1 | tail -3
 timeout 600 python -m pytest tests/test_gpu_c2_parity.py tests/test_gpu_trainer.py -q -x 2>&1 | tail -3
 timeout 300 python bench.py --no-cpu-baseline --detail > gpurun_out/bench_q.json 2> gpurun_out/bench_q.err
 python - <<'PY'
 import json
 d = json.loads(open("gpurun_out/bench_q.json").read().strip().splitlines()[-1])
 print("epoch ms", round(d["ms_per_step"], 4), "e2e ms", round(d["e2e"]["ms_per_step"], 4), "roofline", d["roofline"]["kernel"], round(d["roofline"]["frac"], 3))
-for k, v in sorted(d["kernels"].items(), key=lambda kv: -kv[1]["ms_per_step"])[:8]:
+for k, v in sorted(d["kernels"].items(), key=lambda kv: -kv[1]["ms_per_step"])[:6]:
     print(f"  {k:55s} {v['ms_per_step']*1e3:8.1f} us  {v['GBps']:.0f} GB/s")
 PY
-if [ "$1" = "ts" ]; then
-  make clean > /dev/null && make -j8 DGC_TS=1 > /dev/null 2>&1
-  timeout 200 python tools/time_lstm_c2.py 2>&1 | tail -2
-  timeout 200 python tools/time_lstm_fused.py 2>&1 | tail -9
-  make clean > /dev/null
-fi
+make clean > /dev/null && make -j8 DGC_TS=1 > /dev/null 2>&1
+timeout 200 python tools/time_lstm_c2.py 2>&1 | tail -1
+make clean > /dev/null

@@ -19,7 +19,8 @@ Ut = torch.randn((4 * H, H), device=dev) / H ** 0.5; b = torch.zeros(4 * H, devi
 sr = torch.tensor(slot_row, device=dev); sm = torch.tensor(mask.reshape(-1), device=dev)
 sc = torch.full((R * L,), -1, dtype=torch.int32, device=dev); carry = torch.zeros((1, 2 * H), device=dev)
 hc = torch.zeros((n, 2 * H), device=dev); save = torch.zeros((n, 7 * H), device=dev)
-fn = lambda: ops.rnn_fwd_tc_x(x, H, WxT, Ut, b, sr, sm, sc, carry, R, L, H, 2 * H, hc, hc[:, H:], save)
+x16 = x.half(); Wx = WxT.t().contiguous(); U = Ut.t().contiguous()
+fn = lambda: ops.lstm_fwd_tc_f16x(x16, Wx, U, b, sr, sm, sc, carry, R, L, H, 2 * H, hc, hc[:, H:], save)
 fn(); torch.cuda.synchronize()
 s = torch.cuda.Event(enable_timing=True); e = torch.cuda.Event(enable_timing=True)
 s.record()
