@@ -9,7 +9,7 @@ endif
 SRC := paper_2309_03523_b200/csrc
 OUT := paper_2309_03523_b200/lib
 CU := common spmm stale exchange dense rnn gemm_tc rnn_tc evolve
-OBJS := $(addprefix build/,$(addsuffix .o,$(CU))) build/layout.o build/fusion_plan.o build/propagate.o
+OBJS := $(addprefix build/,$(addsuffix .o,$(CU))) build/layout.o build/fusion_plan.o build/propagate.o build/generate.o
 
 all: $(OUT)/libdgc_b200.so
 
@@ -31,6 +31,10 @@ clean:
 .PHONY: all clean
 
 build/fusion_plan.o: $(SRC)/fusion_plan.cpp include/dgc_b200.h
+	@mkdir -p build
+	g++ -O3 -std=c++17 -fPIC -c $< -o $@
+
+build/generate.o: $(SRC)/generate.cpp include/dgc_b200.h
 	@mkdir -p build
 	g++ -O3 -std=c++17 -fPIC -c $< -o $@
 

@@ -56,6 +56,35 @@ typedef struct dgc_plan_view {
                                      (per-snapshot weights, EvolveGCN) */
 } dgc_plan_view;
 
+/* Native synthetic generator, the contract of
+ * dynpart.graphstore.generate (graphstore.py:525-579) with its own random
+ * stream: presence lengths from the LengthDistribution (graphstore.py:367-382)
+ * until they sum to total_vertices, uniform starts, clipped-normal per-snapshot
+ * edge counts renormalised by largest remainder, uniform or preferential
+ * distinct-pair sampling per snapshot. Outputs (caller-allocated): presences
+ * [total_vertices][2] = (entity, t) grouped by entity, t ascending; edges
+ * [total_edges][3] = (t, u, v), u < v, by snapshot, sorted pairs. Returns
+ * DGC_ERR_ARG for an invalid spec or a snapshot that cannot host its quota. */
+#define DGC_LEN_CONSTANT 0
+#define DGC_LEN_UNIFORM 1
+#define DGC_LEN_BIMODAL 2
+#define DGC_LEN_GEOMETRIC 3
+typedef struct dgc_length_dist {
+  int32_t kind;
+  int32_t value, low, high, long_low, long_high;
+  double long_fraction, mean;
+} dgc_length_dist;
+typedef struct dgc_synthetic_spec {
+  int64_t total_vertices, total_edges;
+  int32_t T;
+  double edges_per_snapshot_mean, edges_per_snapshot_stddev;
+  dgc_length_dist length;
+  uint64_t rng_seed;
+  int32_t preferential; /* edge_attachment == "preferential" */
+} dgc_synthetic_spec;
+int dgc_generate_graph(const dgc_synthetic_spec* spec, int32_t* presences, int32_t* edges,
+                       int64_t* n_entities, int32_t n_threads);
+
 typedef struct dgc_layout dgc_layout;
 
 /* Field ids of dgc_layout_field(); all fields are int64 arrays. */

@@ -32,6 +32,7 @@ class PlanView(C.Structure):
 
 _SIGS = {
     "dgc_version": (_i32, []),
+    "dgc_generate_graph": (_i32, [_p, _p, _p, _p, _i32]),
     "dgc_last_error": (C.c_char_p, []),
     "dgc_layout_build": (_i32, [C.POINTER(PlanView), _i32, C.POINTER(_p)]),
     "dgc_layout_field": (_i64, [_p, _i32, C.POINTER(C.POINTER(_i64))]),

@@ -62,7 +62,7 @@ CONFIGS = {
     # (numerics are fusion-invariant)
     "c5d8": dict(N=10_000_000, T=128, sigma_mult=2.0, D=8, F=16,
                  profile=ModelProfile(1, 2, 0, "previous-only", 16, 4), fuse=False,
-                 native_propagate=True),
+                 native_propagate=True, native_generate=True),
     # small EvolveGCN plans for the parity tests
     "e2": dict(N=3_000, T=8, sigma_mult=1.0, D=2, F=16,
                profile=ModelProfile(1, 2, 0, "previous-only", 16, 4), fuse=True),
@@ -91,7 +91,14 @@ def build(name: str) -> None:
     out = ROOT / "artifacts" / name
     out.mkdir(parents=True, exist_ok=True)
     t0 = time.time()
-    g = graphstore.generate(spec_for(cfg))
+    if cfg.get("native_generate"):
+        # the native generator (csrc/generate.cpp): seconds
+        # instead of ~25 min; the reference DynamicGraph validates its output
+        sys.path.insert(0, str(ROOT))
+        from paper_2309_03523_b200.generate import generate as native_generate
+        g = native_generate(spec_for(cfg)).to_dynamic_graph()
+    else:
+        g = graphstore.generate(spec_for(cfg))
     t1 = time.time()
     cluster = sim.ClusterSpec(n_devices=cfg["D"])
     if cfg.get("native_propagate"):
@@ -140,6 +147,7 @@ def build(name: str) -> None:
         "n_devices": cfg["D"], "profile": cfg["profile"].to_dict(),
         "fused": bool(groups), "fusion_source": fusion_src,
         "generate_s": t1 - t0, "build_plan_s": t2 - t1,
+        "generator": "native (csrc/generate.cpp)" if cfg.get("native_generate") else "reference",
         "reference": "dynpart " + dynpart.__version__,
     }
     np.savez_compressed(
