@@ -339,24 +339,34 @@ def run_ours(args):
     edges_total = pa.n_spatial_edges * (world if scaling == "weak" else 1)
     value = edges_total / (step_ms / 1e3)
     # ---- end-to-end through the public API with host buffers: every step
-    # installs inputs copied from pinned host memory and reads the loss back;
-    # the next step's 103 MB H2D copy runs on a copy stream during this step's
-    # epoch (double-buffered input pipeline, trainer.stage_inputs) ----
+    # installs inputs copied from pinned host memory (the next step's copy runs
+    # on a copy stream during this step: trainer.stage_inputs) and reads its
+    # loss back to the host. Software-pipelined like a training loop: step i+1
+    # is submitted before step i's loss is read, so the host read overlaps the
+    # device; the timed region covers K submissions, K H2D copies and K loss
+    # reads (the last read and every queued copy drained before the end event).
     xs, ys = tr.host_inputs(X, y)
     tr.stage_inputs(xs, ys)
-    e2e_ms = []
-    for i in range(args.warmup + args.steps):
-        flush.zero_()
-        barrier()
-        s = torch.cuda.Event(enable_timing=True)
-        e = torch.cuda.Event(enable_timing=True)
-        s.record()
-        rep = tr.run_epoch(next_inputs=(xs, ys))
-        loss_host = float(rep.loss)  # D2H read of the step result
-        e.record()
-        barrier()
-        if i >= args.warmup:
-            e2e_ms.append(s.elapsed_time(e))
+
+    def pipelined(k):
+        prev = None
+        for _ in range(k):
+            p = tr.submit_epoch(next_inputs=(xs, ys))
+            if prev is not None:
+                float(prev.result().loss)  # D2H read of the step result
+            prev = p
+        float(prev.result().loss)
+        torch.cuda.synchronize()
+
+    pipelined(args.warmup)
+    barrier()
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    s.record()
+    pipelined(args.steps)
+    e.record()
+    barrier()
+    e2e_ms = [s.elapsed_time(e) / args.steps]
     e2e_step = float(np.mean(e2e_ms))
     if world > 1:
         t = torch.tensor([e2e_step], device=dev)
@@ -411,9 +421,17 @@ def run_ours(args):
                 "h2d_bytes_per_step": int(sum(x.numel() * x.element_size() + t.numel() * t.element_size()
                                               for x, t in zip(xs, ys))),
                 "pipeline": ("inputs double-buffered: step i+1's H2D overlaps step i on a copy stream; "
-                             "TF32 mode ships the TF32-rounded features as their 3 significant bytes "
-                             "(bit-identical to on-device rounding)"),
-                "d2h_bytes_per_step": 8, "ms_per_step": e2e_step},
+                             + ("TF32 mode consumes in-range features at fp16 precision and ships "
+                                "them as fp16 (bit-identical to on-device rounding); the host-side "
+                                "fp32->fp16 conversion happens once, outside the timed region"
+                                if sh.x_f16 else
+                                "TF32 mode ships the TF32-rounded features as their 3 significant "
+                                "bytes (bit-identical to on-device rounding); the host-side packing "
+                                "happens once, outside the timed region")),
+                "d2h_bytes_per_step": 8, "ms_per_step": e2e_step,
+                "loop": ("software-pipelined: step i+1 submitted before step i's loss is read "
+                         "(trainer.submit_epoch); time = K steps / K"),
+                "l2": "not flushed between pipelined steps; per-step working set (> 2 GB) >> 126 MB L2"},
         "roofline": {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": hbm,
                      "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                      "peak_source": src, "algorithmic_bytes_per_launch": d["bytes"] / d["launches"],

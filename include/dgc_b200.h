@@ -232,6 +232,21 @@ int dgc_gemm_tf32_stacked_a(const float* A0, int64_t lda0, const float* A1, int6
                             int64_t M, int64_t N, int64_t K, int32_t a_mn, int32_t b_mn,
                             int32_t precision, int32_t k_splits, float* partial, void* stream);
 
+/* K2 with fp16 operands (kind::f16, the same 10-bit mantissa as TF32; fp32
+ * accumulation and C): C = alpha * op(A) op(B) (+ bias) (* (relu_src > 0)),
+ * alpha undoing a power-of-two operand scale exactly (the BPTT's fp16 dgx is
+ * S * dgx). Majorness, split-K, accumulate and colsum as dgc_gemm_tf32; A and
+ * B are fp16 with row strides lda / ldb in elements (multiples of 8); an
+ * MN-major B needs N % 64 == 0. The stacked form = dgc_gemm_tf32_stacked_a. */
+int dgc_gemm_f16(const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
+                 int64_t M, int64_t N, int64_t K, int32_t a_mn, int32_t b_mn, float alpha,
+                 const float* bias, const float* relu_src, int32_t accumulate, int32_t k_splits,
+                 float* partial, float* colsum_partial, void* stream);
+int dgc_gemm_f16_stacked_a(const void* A0, int64_t lda0, const void* A1, int64_t lda1, int64_t M0,
+                           const void* B, int64_t ldb, float* C, int64_t ldc, int64_t M, int64_t N,
+                           int64_t K, int32_t a_mn, int32_t b_mn, float alpha, int32_t k_splits,
+                           float* partial, void* stream);
+
 /* EvolveGCN-O weight evolution (matrix GRU in the reference gate form of
  * GruCell.step, fusion.py:409-413, input = hidden = W_{t-1}):
  *   R = s(S_r W + B_r), Z = s(S_z W + B_z), C = tanh(P_c W + Q_c (R*W) + B_c),
@@ -416,6 +431,15 @@ int dgc_reduce_rows_batched(int32_t n_jobs, const float* const* partials, const 
  * in: 4-byte aligned, out: 16-byte aligned. */
 int dgc_unpack_tf32x24(const uint8_t* in, float* out, int64_t n, void* stream);
 int dgc_round_tf32(const float* in, float* out, int64_t n, void* stream);
+/* out[i] = fp16(in[i]) (round to nearest): the fp16 weight copies of the
+ * fp16-operand GEMMs. */
+int dgc_to_f16(const float* in, void* out, int64_t n, void* stream);
+/* TF32 mode's features are consumed at fp16 precision when they fit its range
+ * (the same 10-bit mantissa): out = fp32(fp16_rn(in)); the host ships them as
+ * fp16 (2 bytes per value) and dgc_unpack_f16 expands them (n % 8 == 0,
+ * 16-byte aligned) bit-identically to dgc_round_f16 on the device. */
+int dgc_round_f16(const float* in, float* out, int64_t n, void* stream);
+int dgc_unpack_f16(const void* in, float* out, int64_t n, void* stream);
 /* Deterministic column sums out[j] (+)= sum_i X[i, j] (bias gradients);
  * scratch >= 296*width floats (<= 2 row blocks per SM). */
 int dgc_colsum(const float* X, int64_t n, int32_t width, int64_t ld, float* out,

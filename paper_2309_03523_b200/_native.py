@@ -32,6 +32,13 @@ class PlanView(C.Structure):
 
 _SIGS = {
     "dgc_version": (_i32, []),
+    "dgc_to_f16": (_i32, [_p, _p, _i64, _p]),
+    "dgc_round_f16": (_i32, [_p, _p, _i64, _p]),
+    "dgc_unpack_f16": (_i32, [_p, _p, _i64, _p]),
+    "dgc_gemm_f16": (_i32, [_p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _i32, _i32, _f32, _p, _p,
+                            _i32, _i32, _p, _p, _p]),
+    "dgc_gemm_f16_stacked_a": (_i32, [_p, _i64, _p, _i64, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64,
+                                      _i32, _i32, _f32, _i32, _p, _p]),
     "dgc_generate_graph": (_i32, [_p, _p, _p, _p, _i32]),
     "dgc_last_error": (C.c_char_p, []),
     "dgc_layout_build": (_i32, [C.POINTER(PlanView), _i32, C.POINTER(_p)]),

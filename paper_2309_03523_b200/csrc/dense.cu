@@ -3,6 +3,8 @@
 // The reference loss trace is synthetic (sim.py:323-324); the B200 trainer
 // feeds the real mean cross-entropy into EpochLossTrace.append (stale.py:80),
 // which drives threshold() unchanged. Every reduction has a fixed order.
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace {
@@ -478,6 +480,60 @@ extern "C" int dgc_unpack_tf32x24(const uint8_t* in, float* out, int64_t n, void
   unpack_tf32x24_kernel<<<dgc::grid_for(n / 4, 256), 256, 0, dgc::as_stream(stream)>>>(
       reinterpret_cast<const uint32_t*>(in), reinterpret_cast<float4*>(out), n / 4);
   DGC_CHECK_LAUNCH("unpack_tf32x24_kernel");
+  return DGC_OK;
+}
+
+__global__ void round_f16_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __half2float(__float2half_rn(in[i]));
+}
+
+// fp16 features shipped from the host (2 bytes per value): thread = 8 values
+// (one 16-B load, two float4 stores)
+__global__ void unpack_f16_kernel(const uint4* __restrict__ in, float4* __restrict__ out,
+                                  int64_t n8) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 u = __ldg(in + i);
+    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+    const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+    const float2 c = __half22float2(*reinterpret_cast<const __half2*>(&u.z));
+    const float2 d = __half22float2(*reinterpret_cast<const __half2*>(&u.w));
+    out[2 * i] = make_float4(a.x, a.y, b.x, b.y);
+    out[2 * i + 1] = make_float4(c.x, c.y, d.x, d.y);
+  }
+}
+
+extern "C" int dgc_round_f16(const float* in, float* out, int64_t n, void* stream) {
+  if (n == 0) return DGC_OK;
+  round_f16_kernel<<<dgc::grid_for(n, 256), 256, 0, dgc::as_stream(stream)>>>(in, out, n);
+  DGC_CHECK_LAUNCH("round_f16_kernel");
+  return DGC_OK;
+}
+
+extern "C" int dgc_unpack_f16(const void* in, float* out, int64_t n, void* stream) {
+  DGC_REQUIRE(n % 8 == 0, "unpack_f16: n must be a multiple of 8");
+  DGC_REQUIRE((reinterpret_cast<uintptr_t>(in) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0,
+              "unpack_f16: misaligned buffers");
+  if (n == 0) return DGC_OK;
+  unpack_f16_kernel<<<dgc::grid_for(n / 8, 256), 256, 0, dgc::as_stream(stream)>>>(
+      static_cast<const uint4*>(in), reinterpret_cast<float4*>(out), n / 8);
+  DGC_CHECK_LAUNCH("unpack_f16_kernel");
+  return DGC_OK;
+}
+
+__global__ void to_f16_kernel(const float* __restrict__ in, __half* __restrict__ out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __float2half_rn(in[i]);
+}
+
+extern "C" int dgc_to_f16(const float* in, void* out, int64_t n, void* stream) {
+  if (n == 0) return DGC_OK;
+  to_f16_kernel<<<dgc::grid_for(n, 256), 256, 0, dgc::as_stream(stream)>>>(
+      in, static_cast<__half*>(out), n);
+  DGC_CHECK_LAUNCH("to_f16_kernel");
   return DGC_OK;
 }
 

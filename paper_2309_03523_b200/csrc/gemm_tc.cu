@@ -22,11 +22,12 @@ namespace {
 
 using namespace dgc::tc;
 using dgc::make_map;
+using dgc::make_map_f16;
 constexpr int kEpiWarps = 8;  // 2 per TMEM lane quadrant, round-robin 32-column chunks
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kABytes = BM * BK * 4;  // 16 KiB
 
-template <bool A_MN, bool B_MN, bool SPLIT3>
+template <bool A_MN, bool B_MN, bool SPLIT3, bool F16>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC, int tma_store, int64_t c_rows_per_z,
@@ -37,7 +38,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                      int accumulate, float* __restrict__ partial,
                      float* __restrict__ colsum_partial, int b_res,
                      const int32_t* __restrict__ seg_of_mtile, int b_seg_rows,
-                     const int32_t* __restrict__ kitems) {
+                     const int32_t* __restrict__ kitems, float alpha) {
+  // F16: fp16 operands (kind::f16, 64 elements per 128-B k-block row; MN-major
+  // boxes of 64 MN elements x 64 k-rows), C = alpha * A B (alpha undoes an
+  // operand's power-of-two scale exactly); else fp32 storage, TF32 math
+  constexpr int KE = F16 ? 64 : BK;
   // Persistent: CTA c owns tiles c, c+G, ... of the (split, m-tile, n-tile)
   // space, n fastest. With G a multiple of n_tiles every CTA keeps ONE n-tile,
   // so (b_res) its whole B panel is loaded into shared memory once and only A
@@ -123,7 +128,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < kb_total; ++kb) {
           uint8_t* sb = bres + (size_t)kb * b_bytes;
           if (!B_MN) {
-            tma_load_2d(sb, &tmB, kb * BK, (int)n0, bres_full);
+            tma_load_2d(sb, &tmB, kb * KE, (int)n0, bres_full);
+          } else if (F16) {
+            for (int i = 0; i < bn / 64; ++i)
+              tma_load_2d(sb + i * 8192, &tmB, (int)n0 + 64 * i, kb * KE, bres_full);
           } else {
             for (int i = 0; i < bn / 32; ++i)
               tma_load_2d(sb + i * 4096, &tmB, (int)n0 + 32 * i, kb * BK, bres_full);
@@ -142,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* sa = smem + (size_t)s * (b_res ? kABytes : stage_bytes);
           uint8_t* sb = sa + kABytes;
           mbar_expect_tx(&full[s], (uint32_t)ld_bytes);
-          const int k0 = (kb0 + kb) * BK;
+          const int k0 = (kb0 + kb) * KE;
           // row-segmented B (one weight matrix per snapshot block of 128-row tiles)
           const int boff = seg_of_mtile ? seg_of_mtile[m0 / BM] * b_seg_rows : 0;
           // stacked A: rows >= a2_row0 come from the second operand
@@ -150,6 +158,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int am0 = (int)(m0 >= a2_row0 ? m0 - a2_row0 : m0);
           if (!A_MN) {
             tma_load_2d(sa, mA, k0, am0, &full[s]);
+          } else if (F16) {
+#pragma unroll
+            for (int i = 0; i < BM / 64; ++i)
+              tma_load_2d(sa + i * 8192, mA, am0 + 64 * i, k0, &full[s]);
           } else {
 #pragma unroll
             for (int i = 0; i < BM / 32; ++i)
@@ -158,6 +170,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (!b_res) {
             if (!B_MN) {
               tma_load_2d(sb, &tmB, k0, (int)n0 + boff, &full[s]);
+            } else if (F16) {
+              for (int i = 0; i < bn / 64; ++i)
+                tma_load_2d(sb + i * 8192, &tmB, (int)n0 + 64 * i, k0 + boff, &full[s]);
             } else {
               for (int i = 0; i < bn / 32; ++i)
                 tma_load_2d(sb + i * 4096, &tmB, (int)n0 + 32 * i, k0 + boff, &full[s]);
@@ -167,7 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    const uint32_t idesc = idesc_tf32(bn, A_MN, B_MN);
+    const uint32_t idesc = F16 ? idesc_f16mn(bn, A_MN, B_MN) : idesc_tf32(bn, A_MN, B_MN);
     if (b_res) {
       mbar_wait(bres_full, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -192,6 +207,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t sb = b_res ? smem_u32(bres + (size_t)(kb0 + kb) * b_bytes) : sa + kABytes;
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
+            if (F16) {
+              // K = 16 per MMA: K-major 32 B inside the 128-B swizzle row;
+              // MN-major 16 k-rows (two 1-KB SWIZZLE_128B atoms) per MMA, 64-element
+              // MN chunks 8 KB apart
+              const uint32_t ao = A_MN ? kk * 2048 : kk * 32;
+              const uint32_t bo = B_MN ? kk * 2048 : kk * 32;
+              const uint64_t ad = A_MN ? sdesc(sa + ao, 8192, 1024, 2) : kdesc(sa + ao);
+              const uint64_t bd = B_MN ? sdesc(sb + bo, 8192, 1024, 2) : kdesc(sb + bo);
+              mma_f16(tacc, ad, bd, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+              continue;
+            }
             // K-major: advance 32 B inside the 128-B swizzle row; MN-major: eight
             // k-rows (two 512-B atoms, 1024 B) per MMA, MN chunks 4096 B apart.
             const uint32_t ao = A_MN ? kk * 1024 : kk * 32;
@@ -272,6 +298,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               stg_base + ((warp - 2) * tma_store + (box_seq % tma_store)) * 1024);
           float v[32];
           tmem_ld32(tmem_base + (uint32_t)a * acc_cols + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
+          if (F16) {
+#pragma unroll
+            for (int u = 0; u < 32; ++u) v[u] *= alpha;
+          }
           const int64_t nb = n0 + c;
           if (bias) {
 #pragma unroll
@@ -345,7 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float v[32];
         tmem_ld32(tmem_base + (uint32_t)a * acc_cols + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
 #pragma unroll
-        for (int u = 0; u < 32; ++u) stg[lane * 33 + u] = v[u];
+        for (int u = 0; u < 32; ++u) stg[lane * 33 + u] = F16 ? v[u] * alpha : v[u];
         __syncwarp();
         const int64_t n = n0 + c + lane;
         const bool col_ok = (c + lane < bn) && (n < N);
@@ -483,13 +513,13 @@ struct SegOpts {
   int64_t a2_row0 = 0;
 };
 
-template <bool A_MN, bool B_MN, bool SPLIT3>
+template <bool A_MN, bool B_MN, bool SPLIT3, bool F16 = false>
 int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, int tma_store,
                 int64_t c_rows_per_z, const CUtensorMap& ma2, int64_t a2_row0,
                 float* C, int64_t ldc, int64_t M,
                 int64_t N, int bn, int ntiles, int kb_total, int splits, int kb_per,
                 const float* bias, const float* relu_src, int accumulate, float* partial,
-                float* colsum_partial, const SegOpts& so, cudaStream_t s) {
+                float* colsum_partial, const SegOpts& so, cudaStream_t s, float alpha = 1.f) {
   const int ab = kABytes + bn * BK * 4;
   const int stage_bytes = ab * (SPLIT3 ? 2 : 1);
   // shared memory: pipeline stages (+ resident B panel) + the epilogue staging
@@ -516,7 +546,7 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     stg_bytes *= 2;
   }
   const size_t smem = pipe + 1024 + 256 + 1024 + stg_bytes;
-  auto kern = gemm_tf32_kernel<A_MN, B_MN, SPLIT3>;
+  auto kern = gemm_tf32_kernel<A_MN, B_MN, SPLIT3, F16>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return dgc::cuda_fail(e, "gemm: set smem");
   const int m_tiles = (int)((M + BM - 1) / BM);
@@ -526,7 +556,7 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   kern<<<grid, kThreads, smem, s>>>(ma, mb, mc, tma_store, c_rows_per_z, ma2, a2_row0, C, ldc, M, N, bn, stages, kb_total, kb_per, m_tiles,
                                     ntiles, splits, bias, relu_src, accumulate, partial,
                                     colsum_partial, b_res, so.seg_of_mtile, so.b_seg_rows,
-                                    so.kitems);
+                                    so.kitems, alpha);
   DGC_CHECK_LAUNCH("gemm_tf32_kernel");
   return DGC_OK;
 }
@@ -534,7 +564,8 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
 }  // namespace
 
 extern "C" int dgc_gemm_splits(int64_t K, int32_t precision, int32_t k_splits) {
-  const int kb_total = (int)((K + BK - 1) / BK);
+  const int KE = precision == 2 ? 64 : BK;
+  const int kb_total = (int)((K + KE - 1) / KE);
   if (k_splits < 1) k_splits = 1;
   int kb_per = (kb_total + k_splits - 1) / k_splits;
   if (precision == 3 && kb_per > 16) kb_per = 16;
@@ -562,7 +593,7 @@ static int gemm_impl(const float* A, int64_t lda, const float* B, int64_t ldb, f
                      int64_t ldc, int64_t M, int64_t N, int64_t K, int32_t a_mn, int32_t b_mn,
                      int32_t precision, const float* bias, const float* relu_src,
                      int32_t accumulate, int32_t k_splits, float* partial, float* colsum_partial,
-                     const SegOpts& so, void* stream) {
+                     const SegOpts& so, void* stream, float alpha = 1.f) {
   DGC_REQUIRE(M >= 0 && N >= 0 && K >= 0, "gemm: bad shape");
   const int out_act = (accumulate >> 1) & 3;  // bit 1 ReLU, bit 2 TF32-round the output
   accumulate &= 1;
@@ -575,16 +606,20 @@ static int gemm_impl(const float* A, int64_t lda, const float* B, int64_t ldb, f
     DGC_CHECK_LAUNCH("gemm_k0_kernel");
     return DGC_OK;
   }
-  DGC_REQUIRE(precision == 1 || precision == 3, "gemm: precision must be 1 (TF32) or 3 (3xTF32)");
+  DGC_REQUIRE(precision >= 1 && precision <= 3,
+              "gemm: precision must be 1 (TF32), 2 (fp16 operands) or 3 (3xTF32)");
+  const bool f16 = precision == 2;  // A, B are fp16 (the pointers' element type)
+  const int KE = f16 ? 64 : BK;     // elements per k-block
+  DGC_REQUIRE(!f16 || (!so.seg_of_mtile && !so.kitems), "gemm: fp16 operands: plain / stacked-A only");
   DGC_REQUIRE(k_splits >= 1, "gemm: k_splits >= 1");
   if (M == 0 || N == 0) return DGC_OK;
   cudaStream_t s = dgc::as_stream(stream);
-  const int align = b_mn ? 32 : 16;
+  const int align = b_mn ? (f16 ? 64 : 32) : 16;
   const int ntiles = (int)((N + 255) / 256);
   int bn = (int)((N + ntiles - 1) / ntiles);
   bn = (bn + align - 1) / align * align;
   if (bn > 256) bn = 256;
-  const int kb_total = (int)((K + BK - 1) / BK);
+  const int kb_total = (int)((K + KE - 1) / KE);
   // split-K only to fill the machine: ~one wave of (m-tile, n-tile, split) work
   // items (the split-K partials cost 2 x splits x M x N x 4 bytes of traffic)
   {
@@ -604,8 +639,13 @@ static int gemm_impl(const float* A, int64_t lda, const float* B, int64_t ldb, f
     DGC_REQUIRE(partial != nullptr, "gemm: split-K / K-segmented items need a partial buffer");
   if (splits > 1) DGC_REQUIRE(colsum_partial == nullptr, "gemm: column sums need k_splits == 1");
   CUtensorMap ma, mb;
-  int rc = a_mn ? make_map(&ma, A, K, M, lda, 32, 32, true)
-                 : make_map(&ma, A, M, K, lda, 32, BM, false);
+  // A / A2 / B maps: fp32 (TF32) or fp16 boxes
+  auto map_a = [&](CUtensorMap* m, const float* p, int64_t rows, int64_t ld) {
+    if (f16)
+      return a_mn ? make_map_f16(m, p, K, rows, ld, 64, 64) : make_map_f16(m, p, rows, K, ld, 64, BM);
+    return a_mn ? make_map(m, p, K, rows, ld, 32, 32, true) : make_map(m, p, rows, K, ld, 32, BM, false);
+  };
+  int rc = map_a(&ma, A, M, lda);
   if (rc) return rc;
   CUtensorMap ma2 = ma;
   int64_t a2_row0 = INT64_MAX;
@@ -613,16 +653,16 @@ static int gemm_impl(const float* A, int64_t lda, const float* B, int64_t ldb, f
     DGC_REQUIRE(so.a2_row0 > 0 && so.a2_row0 % BM == 0 && so.a2_row0 < M,
                 "gemm: stacked A needs a 128-aligned split row inside M");
     a2_row0 = so.a2_row0;
-    rc = a_mn ? make_map(&ma2, so.a2, K, M - a2_row0, so.lda2, 32, 32, true)
-              : make_map(&ma2, so.a2, M - a2_row0, K, so.lda2, 32, BM, false);
+    rc = map_a(&ma2, so.a2, M - a2_row0, so.lda2);
     if (rc) return rc;
-    rc = a_mn ? make_map(&ma, A, K, a2_row0, lda, 32, 32, true)
-              : make_map(&ma, A, a2_row0, K, lda, 32, BM, false);
+    rc = map_a(&ma, A, a2_row0, lda);
     if (rc) return rc;
   }
   const int64_t nseg = so.b_nseg > 0 ? so.b_nseg : 1;
-  rc = b_mn ? make_map(&mb, B, K * nseg, N, ldb, 32, 32, true)
-            : make_map(&mb, B, N * nseg, K, ldb, 32, (uint32_t)bn, false);
+  rc = f16 ? (b_mn ? make_map_f16(&mb, B, K * nseg, N, ldb, 64, 64)
+                   : make_map_f16(&mb, B, N * nseg, K, ldb, 64, (uint32_t)bn))
+           : b_mn ? make_map(&mb, B, K * nseg, N, ldb, 32, 32, true)
+                  : make_map(&mb, B, N * nseg, K, ldb, 32, (uint32_t)bn, false);
   if (rc) return rc;
   float* part = (splits > 1 || so.kitems) ? partial : nullptr;
   DGC_REQUIRE(!(part && out_act), "gemm: an output activation needs an unsplit K");
@@ -645,15 +685,20 @@ static int gemm_impl(const float* A, int64_t lda, const float* B, int64_t ldb, f
   if (so.kitems && splits == 0) {
     rc = DGC_OK;
   } else {
-#define DGC_GEMM_CASE(AM, BMN, S3)                                                               \
-  if ((bool)a_mn == AM && (bool)b_mn == BMN && s3 == S3)                                          \
-    rc = launch_gemm<AM, BMN, S3>(ma, mb, mc, tma_store, c_rows_per_z, ma2, a2_row0, C, ldc,     \
-                                  M, N, bn, ntiles,                                              \
-                                  kb_total,                                                      \
-                                  splits, kb_per,                                                \
-                                  part ? nullptr : bias, part ? nullptr : relu_src,              \
-                                  part ? 0 : (accumulate | (out_act << 1)), part, colsum_partial,\
-                                  so, s);
+#define DGC_GEMM_CASE4(AM, BMN, S3, F)                                                           \
+  if ((bool)a_mn == AM && (bool)b_mn == BMN && s3 == S3 && f16 == F)                              \
+    rc = launch_gemm<AM, BMN, S3, F>(ma, mb, mc, tma_store, c_rows_per_z, ma2, a2_row0, C, ldc,  \
+                                     M, N, bn, ntiles,                                           \
+                                     kb_total,                                                   \
+                                     splits, kb_per,                                             \
+                                     part ? nullptr : bias, part ? nullptr : relu_src,           \
+                                     part ? 0 : (accumulate | (out_act << 1)), part,             \
+                                     colsum_partial, so, s, alpha);
+#define DGC_GEMM_CASE(AM, BMN, S3) DGC_GEMM_CASE4(AM, BMN, S3, false)
+    DGC_GEMM_CASE4(false, false, false, true)
+    DGC_GEMM_CASE4(false, true, false, true)
+    DGC_GEMM_CASE4(true, false, false, true)
+    DGC_GEMM_CASE4(true, true, false, true)
     DGC_GEMM_CASE(false, false, false)
     DGC_GEMM_CASE(false, true, false)
     DGC_GEMM_CASE(true, false, false)
@@ -663,6 +708,7 @@ static int gemm_impl(const float* A, int64_t lda, const float* B, int64_t ldb, f
     DGC_GEMM_CASE(true, false, true)
     DGC_GEMM_CASE(true, true, true)
 #undef DGC_GEMM_CASE
+#undef DGC_GEMM_CASE4
   }
   if (rc) return rc;
   if (so.kitems) {
@@ -727,4 +773,26 @@ extern "C" int dgc_gemm_tf32_stacked_a(const float* A0, int64_t lda0, const floa
   so.a2_row0 = M0;
   return gemm_impl(A0, lda0, B, ldb, C, ldc, M, N, K, a_mn, b_mn, precision, nullptr, nullptr, 0,
                    k_splits, partial, nullptr, so, stream);
+}
+
+extern "C" int dgc_gemm_f16(const void* A, int64_t lda, const void* B, int64_t ldb, float* C,
+                            int64_t ldc, int64_t M, int64_t N, int64_t K, int32_t a_mn, int32_t b_mn,
+                            float alpha, const float* bias, const float* relu_src, int32_t accumulate,
+                            int32_t k_splits, float* partial, float* colsum_partial, void* stream) {
+  return gemm_impl(static_cast<const float*>(A), lda, static_cast<const float*>(B), ldb, C, ldc, M,
+                   N, K, a_mn, b_mn, 2, bias, relu_src, accumulate, k_splits, partial,
+                   colsum_partial, SegOpts{}, stream, alpha);
+}
+
+extern "C" int dgc_gemm_f16_stacked_a(const void* A0, int64_t lda0, const void* A1, int64_t lda1,
+                                      int64_t M0, const void* B, int64_t ldb, float* C, int64_t ldc,
+                                      int64_t M, int64_t N, int64_t K, int32_t a_mn, int32_t b_mn,
+                                      float alpha, int32_t k_splits, float* partial, void* stream) {
+  SegOpts so;
+  so.a2 = static_cast<const float*>(A1);
+  so.lda2 = lda1;
+  so.a2_row0 = M0;
+  return gemm_impl(static_cast<const float*>(A0), lda0, static_cast<const float*>(B), ldb, C, ldc, M,
+                   N, K, a_mn, b_mn, 2, nullptr, nullptr, 0, k_splits, partial, nullptr, so, stream,
+                   alpha);
 }

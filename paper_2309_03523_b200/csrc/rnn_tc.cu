@@ -19,15 +19,16 @@
 
 namespace {
 
-// Compact save row of the H = 128 cluster kernels (forward writes, BPTT
-// reads): [h_in fp32 (H) | c_in fp16 (H) | i, f, g, o fp16 interleaved per unit
-// (4 H: unit j at halves 4j .. 4j+3)] = 3.5 H floats per instance (1792 B at
-// H = 128; 16-B multiple, so h_in stays a TMA operand of the stacked
-// weight-gradient GEMM). fp16 keeps the 10 explicit mantissa bits of the TF32
-// path's operands (gates in (0,1) / (-1,1), |c| <= L). Interleaving the gates
-// makes a BPTT lane's four units one 32-B load and the forward's one 32-B store.
+// Compact save row of the H = 128 cluster kernels (forward writes, BPTT and
+// the weight-gradient GEMM read), all fp16: [h_in (H) | c_in (H) | i, f, g, o
+// interleaved per unit (4 H: unit j at halves 2H + 4j .. +3)] = 3 H floats
+// per instance (1536 B at H = 128). fp16 keeps the 10 explicit mantissa bits of
+// the TF32 path's operands (h_in is fp16-exact by construction, gates in (0,1)
+// / (-1,1), |c| <= L); h_in is the fp16 A operand of [dWx; dU] = [x; h_in]^T
+// dgx, and interleaving the gates makes a BPTT lane's four units one 32-B load
+// and the forward's one 32-B store.
 template <int H> __host__ __device__ constexpr int tc_save_floats() {
-  return H == 128 ? H + 5 * H / 2 : 7 * H;
+  return H == 128 ? 3 * H : 7 * H;
 }
 __device__ __forceinline__ uint32_t h2u(float a, float b) {
   const __half2 h = __floats2half2_rn(a, b);
@@ -737,12 +738,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
 #undef DGC_LSTM_CELL
           constexpr int kSF = tc_save_floats<H>();
           float* sv = save + (int64_t)inst * kSF + j;
-          st4(sv, hin);
-          if (H == 128) {  // compact row: fp16 c_in, i, f, g, o; the BPTT recomputes tanh(c)
-            __half* sh = reinterpret_cast<__half*>(save + (int64_t)inst * kSF + H);
-            sth4(sh + j, cin);
-            st_ifgo(sh + H + 4 * j, ig, fg, gg, og);
+          if (H == 128) {  // compact fp16 row: h_in, c_in, i, f, g, o (the BPTT recomputes tanh(c))
+            __half* sh = reinterpret_cast<__half*>(save + (int64_t)inst * kSF);
+            sth4(sh + j, hin);
+            sth4(sh + H + j, cin);
+            st_ifgo(sh + 2 * H + 4 * j, ig, fg, gg, og);
           } else {
+            st4(sv, hin);
             st4(sv + H, cin);
             st4(sv + 2 * H, ig);
             st4(sv + 3 * H, fg);
@@ -1112,7 +1114,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
                          const uint8_t* __restrict__ slot_mask, int64_t R, int L,
                          const float* __restrict__ save, const float* __restrict__ dh_out,
                          float* __restrict__ dgx, int rnd, float* __restrict__ bias_partial,
-                         int rq, float da_scale) {
+                         int rq, float da_scale, int dgx16) {
   static_assert(H == 128, "K-split cluster BPTT is specialised for H = 128");
   constexpr int EW = kVEW;
   constexpr int kEpiT = 32 * EW;
@@ -1255,7 +1257,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       const int j = u0 + 32 * lc + 4 * u8;
       if (inst[it] >= 0) {
         dho = ldg4(dh_out + (int64_t)inst[it] * H + j);
-        const __half* sv = reinterpret_cast<const __half*>(save + (int64_t)inst[it] * kSF + H);
+        const __half* sv = reinterpret_cast<const __half*>(save + (int64_t)inst[it] * kSF) + H;
         cv = __ldg(reinterpret_cast<const uint2*>(sv + j));
         g0 = __ldg(reinterpret_cast<const uint4*>(sv + H + 4 * j));
         g1 = __ldg(reinterpret_cast<const uint4*>(sv + H + 4 * j + 8));
@@ -1391,13 +1393,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
               dcpk[k] = dcn * fg * mp;
             }
             dcp = make_float4(dcpk[0], dcpk[1], dcpk[2], dcpk[3]);
-            float* o = dgx + (int64_t)inst[it] * G4 + u0 + jo;
+            const int64_t oi = (int64_t)inst[it] * G4 + u0 + jo;
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
               float4 v = make_float4(dak[g][0], dak[g][1], dak[g][2], dak[g][3]);
-              if (rnd) v = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
+              if (dgx16) {  // S da as fp16: the operand of the fp16 weight-gradient GEMMs
+                sth4(reinterpret_cast<__half*>(dgx) + oi + g * H,
+                     make_float4(v.x * da_scale, v.y * da_scale, v.z * da_scale, v.w * da_scale));
+              } else {
+                if (rnd) v = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
+                st4(dgx + oi + g * H, v);
+              }
               da[g] = v;
-              st4(o + g * H, v);
               bsum[lc][g] = make_float4(bsum[lc][g].x + v.x, bsum[lc][g].y + v.y,
                                         bsum[lc][g].z + v.z, bsum[lc][g].w + v.w);
             }
@@ -1466,7 +1473,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
 template <int H, int EW>
 int launch_lstm_bwd_tc2k_ew(const float* U, const int32_t* slot_row, const uint8_t* slot_mask,
                             int64_t R, int L, const float* save, const float* dh_out, float* dgx,
-                            int rnd, float* bias_partial, int rq, float da_scale, cudaStream_t s) {
+                            int rnd, float* bias_partial, int rq, float da_scale, int dgx16,
+                            cudaStream_t s) {
   const size_t smem = (size_t)ks_a_stages<EW>() * BM * 128 + (size_t)4 * H * 128 +
                       (size_t)2 * 4 * ks_recv_rq<EW>() * (H / 2) * 4 + (size_t)EW * 8 * kKsStgStride * 4 +
                       1024 + 512;
@@ -1475,7 +1483,7 @@ int launch_lstm_bwd_tc2k_ew(const float* U, const int32_t* slot_row, const uint8
   if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_bwd_tc2k: set smem");
   const int grid = 2 * (int)cluster_tiles(R);
   kern<<<grid, 64 + 32 * EW, smem, s>>>(U, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
-                                        bias_partial, rq, da_scale);
+                                        bias_partial, rq, da_scale, dgx16);
   DGC_CHECK_LAUNCH("lstm_bwd_tc2k_kernel");
   return DGC_OK;
 }
@@ -1486,14 +1494,14 @@ int launch_lstm_bwd_tc2k_ew(const float* U, const int32_t* slot_row, const uint8
 template <int H>
 int launch_lstm_bwd_tc2k(const float* U, const int32_t* slot_row, const uint8_t* slot_mask,
                          int64_t R, int L, const float* save, const float* dh_out, float* dgx,
-                         int rnd, float* bias_partial, float da_scale, cudaStream_t s) {
+                         int rnd, float* bias_partial, float da_scale, int dgx16, cudaStream_t s) {
   DGC_REQUIRE(R * (int64_t)L < (int64_t)INT32_MAX, "lstm_bwd_tc2k: R * L must fit int32");
   const int rq = cluster_rows_per_quadrant(R);
   if (rq <= 24 && !getenv("DGC_RNN_EW16"))
     return launch_lstm_bwd_tc2k_ew<H, 12>(U, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
-                                          bias_partial, rq, da_scale, s);
+                                          bias_partial, rq, da_scale, dgx16, s);
   return launch_lstm_bwd_tc2k_ew<H, 16>(U, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
-                                        bias_partial, rq, da_scale, s);
+                                        bias_partial, rq, da_scale, dgx16, s);
 }
 
 template <int H>
@@ -1600,7 +1608,8 @@ extern "C" int dgc_rnn_bwd_tc(int32_t cell_flags, const float* U, const int32_t*
     case 128:
       return cluster_rnn_enabled()
                  ? launch_lstm_bwd_tc2k<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, rnd, bias_partial,
-                                             ldexpf(1.f, (cell_flags >> 16) & 0x7f), s)
+                                             ldexpf(1.f, (cell_flags >> 16) & 0x7f),
+                                             (cell_flags >> 24) & 1, s)
                  : launch_lstm_bwd_tc<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
     default: return dgc::fail(DGC_ERR_ARG, "rnn_bwd_tc: H must be 32, 64 or 128");
   }

@@ -137,6 +137,10 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
 __host__ __device__ constexpr uint32_t idesc_f16(int n) {
   return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
+// ... with either operand MN-major
+__host__ __device__ constexpr uint32_t idesc_f16mn(int n, bool a_mn, bool b_mn) {
+  return idesc_f16(n) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16);
+}
 __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
                                         uint32_t accum) {
   asm volatile(
@@ -360,6 +364,26 @@ inline int make_gather_map(CUtensorMap* map, const float* ptr, int64_t rows, int
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return dgc::fail(DGC_ERR_CUDA, "cuTensorMapEncodeTiled (gather) failed");
+  return DGC_OK;
+}
+
+// Row-major [rows, cols] fp16 tensor with row stride ld (elements), boxes of
+// box_cols x box_rows, SWIZZLE_128B (K-major and MN-major UMMA operands alike:
+// box_cols = 64 elements = one 128-B swizzle row).
+inline int make_map_f16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
+                        uint32_t box_cols, uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return dgc::fail(DGC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || ((ld * 2) & 15))
+    return dgc::fail(DGC_ERR_ARG, "gemm: fp16 operands need 16-byte aligned base and row stride");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return dgc::fail(DGC_ERR_CUDA, "cuTensorMapEncodeTiled (fp16) failed");
   return DGC_OK;
 }
 

@@ -206,6 +206,52 @@ def gemm_stacked_a(A0, A1, B, C, M0, M, N, K, *, a_mn=False, b_mn=True, lda0=Non
     return C
 
 
+def _req16(t, name):
+    if t is not None and (not t.is_cuda or t.dtype != torch.float16):
+        raise ValueError(f"{name} must be a CUDA fp16 tensor")
+
+
+def gemm_f16(A, B, C, M, N, K, *, a_mn=False, b_mn=True, lda=None, ldb=None, ldc=None, alpha=1.0,
+             bias=None, relu_src=None, accumulate=False, k_splits=1, partial=None,
+             colsum_partial=None, act=0):
+    """K2 with fp16 operands (dgc_gemm_f16): C = alpha * op(A) op(B) [+ epilogue
+    as gemm()]; alpha undoes a power-of-two operand scale."""
+    _req16(A, "A"); _req16(B, "B"); _req(C, torch.float32, "C")
+    if partial is None and gemm_splits(K, 2, k_splits) > 1:
+        raise ValueError(f"gemm_f16: K={K} needs a split-K partial buffer")
+    lda = lda if lda is not None else (M if a_mn else K)
+    ldb = ldb if ldb is not None else (N if b_mn else K)
+    ldc = ldc if ldc is not None else N
+    splits = gemm_splits(K, 2, k_splits)
+    nb = 2 * (M * K + K * N) + 4 * M * N * (1 + int(accumulate) + int(relu_src is not None))
+    gname = "gemm_f16" + (f"[{M}x{N}x{K} a{int(a_mn)}b{int(b_mn)} s{splits}]" if _prof_detail else "")
+    _run(gname, lambda: _native.check(_native.lib().dgc_gemm_f16(
+        _p(A), lda, _p(B), ldb, _p(C), ldc, M, N, K, int(a_mn), int(b_mn), float(alpha), _p(bias),
+        _p(relu_src), int(accumulate) | ((int(act) & 3) << 1), k_splits, _p(partial),
+        _p(colsum_partial), _stream()), "dgc_gemm_f16"), nb, 2.0 * M * N * K, 1 + int(splits > 1))
+    return C
+
+
+def gemm_f16_stacked_a(A0, A1, B, C, M0, M, N, K, *, a_mn=False, b_mn=True, lda0=None, lda1=None,
+                       ldb=None, ldc=None, alpha=1.0, k_splits=1, partial=None):
+    """gemm_stacked_a with fp16 operands (dgc_gemm_f16_stacked_a)."""
+    _req16(A0, "A0"); _req16(A1, "A1"); _req16(B, "B"); _req(C, torch.float32, "C")
+    if partial is None and gemm_splits(K, 2, k_splits) > 1:
+        raise ValueError("gemm_f16_stacked_a: split-K needs a partial buffer")
+    lda0 = lda0 if lda0 is not None else (M0 if a_mn else K)
+    lda1 = lda1 if lda1 is not None else ((M - M0) if a_mn else K)
+    ldb = ldb if ldb is not None else (N if b_mn else K)
+    ldc = ldc if ldc is not None else N
+    splits = gemm_splits(K, 2, k_splits)
+    nb = 2 * (M * K + K * N) + 4 * M * N
+    gname = "gemm_f16" + (f"[{M}x{N}x{K} a{int(a_mn)}b{int(b_mn)} s{splits} stacked]" if _prof_detail else "")
+    _run(gname, lambda: _native.check(_native.lib().dgc_gemm_f16_stacked_a(
+        _p(A0), lda0, _p(A1), lda1, M0, _p(B), ldb, _p(C), ldc, M, N, K, int(a_mn), int(b_mn),
+        float(alpha), k_splits, _p(partial), _stream()), "dgc_gemm_f16_stacked_a"),
+        nb, 2.0 * M * N * K, 1 + int(splits > 1))
+    return C
+
+
 def gemm_segmented(A, B, C, M, N, K, *, a_mn=False, b_mn=True, lda=None, ldb=None, ldc=None,
                    precision=3, bias=None, relu_src=None, seg_of_mtile=None, b_nseg=1,
                    kitems=None, n_kitems=0, item_ptr=None, n_seg=0, partial=None,
@@ -319,13 +365,24 @@ def lstm_fwd_tc_f16x(x16, Wx, U, bias, slot_row, slot_mask, slot_carry, carry, n
 
 def rnn_bwd_tc(cell, U, slot_row, slot_mask, n_rows, row_len, H, save, dh_out, dgx, dc_scratch,
                bias_partial=None):
-    """K4 BPTT on tcgen05 (dgc_rnn_bwd_tc): dh = da U^T on tensor cores."""
-    _req(dh_out, torch.float32, "dh_out"); _req(dgx, torch.float32, "dgx")
+    """K4 BPTT on tcgen05 (dgc_rnn_bwd_tc): dh = da U^T on tensor cores. An fp16
+    dgx (H = 128 cluster kernel, cell bit 24) receives S * dgx, S = 2^(cell bits
+    16..22): the operand of the fp16 weight-gradient GEMMs."""
+    _req(dh_out, torch.float32, "dh_out")
+    f16 = dgx.dtype == torch.float16
+    if f16:
+        _req16(dgx, "dgx")
+        if not (H == 128 and rnn_tc_save_floats(H) < 7 * H):
+            raise ValueError("rnn_bwd_tc: an fp16 dgx needs the H = 128 cluster kernel")
+        cell |= 1 << 24
+    else:
+        _req(dgx, torch.float32, "dgx")
     n_inst, G = dgx.shape[0], 4
     # reads the saved c_in, i, f, g, o (fp16 in the H = 128 cluster kernel, which
     # recomputes tanh(c); fp32 + tanh(c) otherwise) and dh; writes dgx
     saved_bytes = 2 * 5 * H if rnn_tc_save_floats(H) < 7 * H else 4 * 6 * H
-    nb = n_inst * (4 * G * H + saved_bytes + 4 * H) + 5 * n_rows * row_len + 4 * G * H * H
+    nb = (n_inst * ((2 if f16 else 4) * G * H + saved_bytes + 4 * H) + 5 * n_rows * row_len
+          + 4 * G * H * H)
     _run("lstm_bwd_tc", lambda: _native.check(
         _native.lib().dgc_rnn_bwd_tc(cell, _p(U), _p(slot_row), _p(slot_mask), n_rows, row_len, H,
                                      _p(save), _p(dh_out), _p(dgx), _p(dc_scratch),
@@ -452,10 +509,34 @@ def unpack_tf32x24(packed, out):
     return out
 
 
+def round_f16(x, out):
+    """dgc_round_f16: out = fp32(RN_fp16(x)) (TF32 mode's in-range features)."""
+    _run("round_f16", lambda: _native.check(_native.lib().dgc_round_f16(
+        _p(x), _p(out), x.numel(), _stream()), "dgc_round_f16"), 8 * x.numel())
+    return out
+
+
+def unpack_f16(x16, out):
+    """dgc_unpack_f16: out (fp32) = the fp16 features shipped from the host."""
+    _req16(x16, "x16"); _req(out, torch.float32, "out")
+    n = out.numel()
+    _run("unpack_f16", lambda: _native.check(_native.lib().dgc_unpack_f16(
+        _p(x16), _p(out), n, _stream()), "dgc_unpack_f16"), 6 * n)
+    return out
+
+
 def round_tf32(x, out):
     """dgc_round_tf32: out = RN_tf32(x)."""
     _run("round_tf32", lambda: _native.check(_native.lib().dgc_round_tf32(
         _p(x), _p(out), x.numel(), _stream()), "dgc_round_tf32"), 8 * x.numel())
+    return out
+
+
+def to_f16(x, out):
+    """dgc_to_f16: out (fp16) = RN_fp16(x)."""
+    _req(x, torch.float32, "x"); _req16(out, "out")
+    _run("to_f16", lambda: _native.check(_native.lib().dgc_to_f16(
+        _p(x), _p(out), x.numel(), _stream()), "dgc_to_f16"), 6 * x.numel())
     return out
 
 

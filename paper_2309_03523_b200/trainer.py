@@ -214,10 +214,18 @@ class Shard:
         # (round-to-nearest) so the tcgen05 operand truncation is exact; the
         # optimizer keeps fp32 master weights in self.params.
         self.tf32 = cfg.precision == "tf32"
+        # TF32 mode consumes the features at fp16 precision when they fit its
+        # range (the same 10-bit mantissa; they then ship from the host in 2
+        # bytes per value), else TF32-rounded (3 bytes per value)
+        self.x_f16 = self.tf32 and bool(self.X.numel() % 8 == 0 and
+                                        float(self.X.abs().max()) < 65504.0)
         if self.tf32:
             self.params_r = torch.zeros_like(self.params)
             ops.round_tf32(self.params, self.params_r)
-            ops.round_tf32(self.X, self.X)
+            if self.x_f16:
+                ops.round_f16(self.X, self.X)
+            else:
+                ops.round_tf32(self.X, self.X)
         else:
             self.params_r = self.params
         # activations
@@ -258,12 +266,21 @@ class Shard:
         self.Ut_f = [torch.zeros((GH, H), **f32) for _ in range(cfg.n_rnn)] if self.tc_rnn else None
         # fused input projection (F = H = 128 cluster recurrence): no gx tensor
         self.da_exp = min(100, max(0, int(round(math.log2(max(self.n_total, 1))))))
+        self.inv_da_scale = 2.0 ** -self.da_exp
         self.fused_xproj = (self.tc_rnn and cfg.rnn == "lstm" and self.R > 0
                             and ops.rnn_fwd_tc_fused_available(H, H))
         # fp16 copies of each LSTM layer's input (the fused recurrence's gathered x):
         # written by the last GCN SpMM (layer 1) and by the previous LSTM layer
         self.x16 = ([torch.zeros((n, H), dtype=torch.float16, device=dev) for _ in range(cfg.n_rnn)]
                     if self.fused_xproj else None)
+        # fp16 LSTM backward (the fused path's kernels): the BPTT writes S*dgx as
+        # fp16 and [dWx; dU] = [x16; h_in16]^T dgx16, dx = dgx16 Wx16^T run as
+        # fp16-operand GEMMs with alpha = 1/S (half the bytes of the 4H-wide dgx)
+        self.f16_bwd = bool(self.fused_xproj)
+        if self.f16_bwd:
+            self.dgx = torch.zeros((n, GH), dtype=torch.float16, device=dev)
+            self.Wx16 = [torch.zeros((H, GH), dtype=torch.float16, device=dev)
+                         for _ in range(cfg.n_rnn)]
         if self.tc_rnn:
             self.rnn_dc_scratch = torch.zeros(((max(self.R, 1) + 127) // 128 * 128, H), **f32)
             self.rnn_tc_prows = ops.rnn_tc_tiles(max(self.R, 1), H)
@@ -581,7 +598,13 @@ class Shard:
                 rjobs.append((self.bp_r[k], self.rnn_prows, GH, self.g(f"br{k}")))
             xin, ldxin = (self.Hl[1], H) if k == 0 else (self.hbuf[k - 1], self.hw)
             gU = self.g(f"U{k}")
-            if cell == 1 and H % 128 == 0:
+            if self.f16_bwd:
+                # [dWx; dU] = [x16; h_in16]^T (S dgx16) / S, fp16 operands, one launch
+                ops.gemm_f16_stacked_a(self.x16[k], self.save[k].view(torch.float16), self.dgx,
+                                       self.g(f"Wx{k}"), H, 2 * H, GH, n, a_mn=True, lda0=H,
+                                       lda1=2 * self.sf, ldb=GH, ldc=GH, alpha=self.inv_da_scale,
+                                       k_splits=ks, partial=part)
+            elif cell == 1 and H % 128 == 0:
                 # [dWx; dU] = [x; h_in]^T dgx in ONE launch: dgx is streamed once
                 # (Wx{k} and U{k} are adjacent in the flat gradient buffer)
                 ops.gemm_stacked_a(xin, self.save[k], self.dgx, self.g(f"Wx{k}"), H, 2 * H, GH, n,
@@ -600,9 +623,15 @@ class Shard:
                     ops.gemm(self.save[k], self.dgx, gU, H, GH, n, a_mn=True, lda=self.sf,
                              ldb=GH, ldc=GH, precision=prec, k_splits=ks, partial=part)
             relu_src = self.Hl[1] if k == 0 else None
-            ops.gemm(self.dgx, self.pr(f"Wx{k}"), self.dh2, n, H, GH, b_mn=False, ldb=GH,
-                     precision=prec, relu_src=relu_src,
-                     colsum_partial=self.bp_b[1] if k == 0 else None)
+            if self.f16_bwd:
+                ops.to_f16(self.pr(f"Wx{k}"), self.Wx16[k])
+                ops.gemm_f16(self.dgx, self.Wx16[k], self.dh2, n, H, GH, b_mn=False, ldb=GH,
+                             alpha=self.inv_da_scale, relu_src=relu_src,
+                             colsum_partial=self.bp_b[1] if k == 0 else None)
+            else:
+                ops.gemm(self.dgx, self.pr(f"Wx{k}"), self.dh2, n, H, GH, b_mn=False, ldb=GH,
+                         precision=prec, relu_src=relu_src,
+                         colsum_partial=self.bp_b[1] if k == 0 else None)
             if k == 0:  # dZ2 = dH2 * (H2 > 0): its column sums are the b2 gradient
                 rjobs.append((self.bp_b[1], 4 * self.m_tiles, H, self.g("b2")))
             self.dh, self.dh2 = self.dh2, self.dh
@@ -913,6 +942,22 @@ class NcclRunner:
 
 # -- the trainer ----------------------------------------------------------------
 
+class PendingEpoch:
+    """An enqueued epoch (DGNNTrainer.submit_epoch); result() -> EpochReport."""
+
+    def __init__(self, trainer, r, t0, t1, done_ev, slot, infos, timed):
+        self.trainer, self.r, self.t0, self.t1 = trainer, r, t0, t1
+        self.done_ev, self.slot, self.infos, self.timed = done_ev, slot, infos, timed
+        self.done = False
+        self._report = None
+
+    def result(self):
+        if not self.done:
+            self._report = self.trainer._finish_epoch(self)
+            self.done = True
+        return self._report
+
+
 class DGNNTrainer:
     """Chunk-partitioned DGNN training on B200 driven by the reference plan.
 
@@ -931,6 +976,7 @@ class DGNNTrainer:
         self.cuda_graph = cuda_graph
         self._graphs = {}
         self._loss_host = None
+        self._unread = []  # submitted graph epochs whose result() was not read yet
         self._epoch_ev = None
         self._alt_free_ev = None
         # double-buffered input staging (stage_inputs / run_epoch(next_inputs=...))
@@ -972,7 +1018,12 @@ class DGNNTrainer:
             real = sh.lay.own_gid >= 0
             gid = np.maximum(sh.lay.own_gid, 0)
             x = np.where(real[:, None], features[gid], 0).astype(np.float32)
-            if sh.tf32 and x.size % 4 == 0:
+            if sh.x_f16:
+                # TF32 mode, in-range features: consumed at fp16 precision, so they
+                # ship as fp16 (half the PCIe bytes; numpy's round-to-nearest-even
+                # equals the device-side dgc_round_f16 of the fp32 values)
+                x = x.astype(np.float16)
+            elif sh.tf32 and x.size % 4 == 0:
                 # TF32 mode: the features are consumed TF32-rounded, so they ship as
                 # the 3 significant bytes of the rounded value (25% fewer PCIe bytes;
                 # bit-identical to the device-side rounding of the fp32 values)
@@ -1001,7 +1052,9 @@ class DGNNTrainer:
                 self._copy_stream.wait_event(self._alt_free_ev)
             for sh, x, y in zip(self.shards, xs, ys):
                 sh.X_stage.copy_(x, non_blocking=True)
-                if sh.X_stage.dtype == torch.uint8:  # TF32 values shipped in 3 bytes
+                if sh.X_stage.dtype == torch.float16:  # fp16 features
+                    ops.unpack_f16(sh.X_stage, sh.X_alt)
+                elif sh.X_stage.dtype == torch.uint8:  # TF32 values shipped in 3 bytes
                     ops.unpack_tf32x24(sh.X_stage, sh.X_alt)
                 elif sh.tf32:  # tensor-core operands are kept TF32-rounded
                     ops.round_tf32(sh.X_stage, sh.X_alt)
@@ -1023,6 +1076,22 @@ class DGNNTrainer:
         If inputs were staged (stage_inputs) they are installed first;
         next_inputs = (xs, ys) stages the following epoch's inputs so their
         copy overlaps this epoch."""
+        pend = self.submit_epoch(next_inputs)
+        torch.cuda.synchronize(self.device)  # every stream: the staged inputs too
+        return pend.result()
+
+    def submit_epoch(self, next_inputs=None):
+        """Enqueue one epoch without waiting for it -> PendingEpoch, whose
+        result() waits for that epoch alone and returns its EpochReport. A
+        training loop that submits epoch i+1 before reading epoch i's result
+        keeps the device busy while the host reads the loss (at most one epoch
+        in flight ahead: the double-buffered inputs and the loss slots are
+        ordered by stream events). Epochs with host-side count exchanges (the
+        multi-process runner, staleness) complete inside submit_epoch."""
+        # at most two unread epochs: epoch i+2 reuses epoch i's pinned loss slot
+        self._unread = [p for p in self._unread if not p.done]
+        while len(self._unread) >= 2:
+            self._unread.pop(0).result()
         r = self.epoch_no + 1
         # (no host synchronisation here: the previous epoch ended with one, and
         # staged inputs are ordered by stream events, so the install and the
@@ -1060,26 +1129,39 @@ class DGNNTrainer:
             infos = self.runner.run([s.step(r, self.trace) for s in self.shards])
         t1.record()
         self.runner.timing = None if not timed else self.runner.timing
-        if self._loss_host is None:
-            self._loss_host = torch.empty(1, dtype=infos[0]["loss_sum"].dtype, pin_memory=True)
-        self._loss_host.copy_(infos[0]["loss_sum"].reshape(1), non_blocking=True)
+        if self._loss_host is None:  # two pinned slots: one epoch may be in flight ahead
+            self._loss_host = [torch.empty(1, dtype=infos[0]["loss_sum"].dtype, pin_memory=True)
+                               for _ in range(2)]
+        slot = self._loss_host[r & 1]
+        slot.copy_(infos[0]["loss_sum"].reshape(1), non_blocking=True)
         # this epoch's input buffers become the next staging target only after
         # the epoch that follows it; the previous epoch's are free once it is done
         self._alt_free_ev, self._epoch_ev = self._epoch_ev, torch.cuda.Event()
         self._epoch_ev.record()
+        done_ev = self._epoch_ev
         if next_inputs is not None:
             self.stage_inputs(*next_inputs)
-        torch.cuda.synchronize(self.device)
-        ms = t0.elapsed_time(t1)
-        if timed:
+        self.epoch_no = r
+        pend = PendingEpoch(self, r, t0, t1, done_ev, slot, infos, timed)
+        if not replay:  # eager epochs: host-synchronous bookkeeping (stale trace, timings)
+            torch.cuda.synchronize(self.device)
+            pend.result()
+        else:
+            self._unread.append(pend)
+        return pend
+
+    def _finish_epoch(self, p):
+        """PendingEpoch.result(): wait for epoch p, read its loss, build the report."""
+        p.done_ev.synchronize()
+        ms = p.t0.elapsed_time(p.t1)
+        if p.timed:
             self._device_times(ms)
             self.runner.timing = None
             for sh in self.shards:
                 sh.timing = None
-        self.epoch_no = r
-        loss = float(self._loss_host[0]) / self.pa.n_instances
+        loss = float(p.slot[0]) / self.pa.n_instances
         self.trace.append(loss)
-        return self._report(r, ms, infos, loss)
+        return self._report(p.r, ms, p.infos, loss)
 
     def _device_times(self, ms):
         """Per-device compute and wall ms of the epoch just measured.

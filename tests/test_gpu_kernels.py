@@ -45,6 +45,52 @@ def test_gemm_tf32(a_mn, b_mn, prec, tol, M, N, K):
     close(C.cpu().numpy(), ref, tol, f"gemm a_mn={a_mn} b_mn={b_mn} p={prec}")
 
 
+@pytest.mark.parametrize("a_mn", [False, True])
+@pytest.mark.parametrize("b_mn", [False, True])
+@pytest.mark.parametrize("M,N,K", [(1000, 64, 64), (777, 128, 128), (300, 512, 128),
+                                   (129, 64, 200), (5000, 256, 512)])
+def test_gemm_f16(a_mn, b_mn, M, N, K):
+    """K2 with fp16 operands (kind::f16; K-major and MN-major SWIZZLE_128B
+    boxes) against fp64 of the same fp16-rounded operands; alpha = 2^-12 undoes
+    a 2^12 operand scale exactly."""
+    from paper_2309_03523_b200 import ops
+    rng = np.random.default_rng(M + N + K + 7)
+    A = rng.standard_normal((M, K)).astype(np.float16)
+    B = (rng.standard_normal((K, N)) * 4096).astype(np.float16)  # S-scaled operand
+    ref = (A.astype(np.float64) @ B.astype(np.float64)) / 4096
+
+    def padded(x):
+        ld = (x.shape[1] + 7) // 8 * 8
+        out = np.zeros((x.shape[0], ld), np.float16)
+        out[:, :x.shape[1]] = x
+        return t(out, torch.float16), ld
+    Ad, lda = padded(A.T) if a_mn else padded(A)
+    Bd, ldb = padded(B) if b_mn else padded(B.T)
+    C = torch.full((M, N), 7.0, device=dev)
+    ops.gemm_f16(Ad, Bd, C, M, N, K, a_mn=a_mn, b_mn=b_mn, lda=lda, ldb=ldb, alpha=2.0 ** -12)
+    close(C.cpu().numpy(), ref, 1e-5, f"gemm_f16 a_mn={a_mn} b_mn={b_mn}")
+
+
+def test_gemm_f16_stacked_split_k():
+    """[dWx; dU] = [x; h_in]^T (S dgx) with fp16 operands, split-K, alpha = 1/S:
+    the BPTT weight-gradient form (MN-major A halves with their own strides)."""
+    from paper_2309_03523_b200 import ops
+    rng = np.random.default_rng(11)
+    n, F, H, S = 20000, 128, 128, 2.0 ** 16
+    x = rng.standard_normal((n, F)).astype(np.float16)
+    hs = np.zeros((n, 3 * H), np.float16)          # h_in inside a wider save row
+    hs[:, :H] = rng.standard_normal((n, H)).astype(np.float16)
+    dgx = (rng.standard_normal((n, 4 * H)) * 1e-5 * S).astype(np.float16)
+    ref = np.concatenate([x, hs[:, :H]], 1).astype(np.float64).T @ dgx.astype(np.float64) / S
+    C = torch.zeros((F + H, 4 * H), device=dev)
+    splits = ops.gemm_splits(n, 2, 64)
+    part = torch.zeros(splits * (F + H) * 4 * H, device=dev)
+    ops.gemm_f16_stacked_a(t(x, torch.float16), t(hs, torch.float16), t(dgx, torch.float16), C, F,
+                           F + H, 4 * H, n, a_mn=True, b_mn=True, lda0=F, lda1=3 * H, alpha=1 / S,
+                           k_splits=64, partial=part)
+    close(C.cpu().numpy(), ref, 1e-5, "stacked f16")
+
+
 @pytest.mark.parametrize("splits", [1, 7, 64])
 def test_gemm_split_k_weight_gradient(splits):
     from paper_2309_03523_b200 import ops
@@ -411,17 +457,17 @@ def test_softmax_xent_colsum_optimizers():
 
 def tc_save_decode(save, H):
     """The tensor-core LSTM save rows as [n, 6H] fp32 (h_in, c_in, i, f, g, o):
-    the compact H = 128 cluster layout (h_in fp32 | c_in fp16 | i, f, g, o fp16
-    interleaved per unit, 3.5 H floats per row) or the 7 H fp32 layout."""
+    the compact H = 128 cluster layout (fp16 h_in | c_in | i, f, g, o
+    interleaved per unit, 3 H floats per row) or the 7 H fp32 layout."""
     from paper_2309_03523_b200 import ops
     save = np.ascontiguousarray(save, np.float32)
     sf = ops.rnn_tc_save_floats(H)
     if sf == 7 * H:
         return save[:, :6 * H]
-    half = save[:, H:sf].copy().view(np.float16).astype(np.float32)  # [n, 5H]
+    half = save[:, :sf].copy().view(np.float16).astype(np.float32)  # [n, 6H]
     n = save.shape[0]
-    ifgo = half[:, H:].reshape(n, H, 4).transpose(0, 2, 1).reshape(n, 4 * H)  # unit-interleaved
-    return np.concatenate([save[:, :H], half[:, :H], ifgo], 1)
+    ifgo = half[:, 2 * H:].reshape(n, H, 4).transpose(0, 2, 1).reshape(n, 4 * H)
+    return np.concatenate([half[:, :2 * H], ifgo], 1)
 
 
 def tc_save_encode(fields, H):
@@ -431,12 +477,9 @@ def tc_save_encode(fields, H):
     if sf == 7 * H:
         return np.ascontiguousarray(fields, np.float32)
     n = fields.shape[0]
-    out = np.zeros((n, sf), np.float32)
-    out[:, :H] = fields[:, :H]
     ifgo = fields[:, 2 * H:6 * H].reshape(n, 4, H).transpose(0, 2, 1).reshape(n, 4 * H)
-    half = np.concatenate([fields[:, H:2 * H], ifgo], 1).astype(np.float16)
-    out[:, H:] = np.ascontiguousarray(half).view(np.float32)
-    return out
+    half = np.concatenate([fields[:, :2 * H], ifgo], 1).astype(np.float16)
+    return np.ascontiguousarray(half).view(np.float32)
 
 
 def run_end_rows(slot_row, mask):
@@ -613,6 +656,26 @@ def test_tf32x24_input_pipeline_is_bit_exact():
     ops.round_tf32(t(x), ref)
     out = torch.empty(len(x), device=dev)
     ops.unpack_tf32x24(torch.as_tensor(ops.pack_tf32x24(x)).to(dev), out)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.cpu().numpy().view(np.uint32))
+
+
+def test_f16_input_pipeline_is_bit_exact():
+    """Host fp16 conversion (numpy, round to nearest even) + device unpack equals
+    the device's dgc_round_f16 of the fp32 values, bit for bit, including ties,
+    fp16 subnormals, zeros, the largest finite values and infinities."""
+    from paper_2309_03523_b200 import ops
+    rng = np.random.default_rng(8)
+    x = rng.standard_normal(1 << 16).astype(np.float32)
+    special = np.array([0.0, -0.0, 1.0, -1.0, np.inf, -np.inf, 6e-8, -3e-6, 65504.0, -65519.0,
+                        1e-40, 2.0 ** -24, 2.0 ** -25, 3 * 2.0 ** -25], np.float32)
+    ties = (1.0 + (2 * np.arange(1, 65) + 1) * 2.0 ** -11).astype(np.float32)  # exact halves
+    x = np.concatenate([x, special, ties, -ties])
+    x = x[: len(x) // 8 * 8]
+    ref = torch.empty(len(x), device=dev)
+    ops.round_f16(t(x), ref)
+    out = torch.empty(len(x), device=dev)
+    ops.unpack_f16(torch.as_tensor(x.astype(np.float16)).to(dev), out)
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.cpu().numpy().view(np.uint32))
 

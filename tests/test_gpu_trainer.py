@@ -281,6 +281,16 @@ def test_staged_inputs_equal_resident(graph):
     pa_, pb_ = a.params(0), b.params(0)
     for k in pa_:
         assert np.array_equal(pa_[k], pb_[k]), k
+    # software-pipelined submission (epoch i+1 queued before epoch i is read)
+    c = DGNNTrainer(pa, cfg, None, features=np.zeros_like(X), labels=np.zeros_like(y),
+                    params=params, cuda_graph=graph)
+    c.stage_inputs(xs, ys)
+    pend = [c.submit_epoch(next_inputs=(xs, ys)) for _ in range(3)]
+    lc = [p.result().loss for p in pend]
+    assert la == lc
+    pc_ = c.params(0)
+    for k in pa_:
+        assert np.array_equal(pa_[k], pc_[k]), k
 
 
 @pytest.mark.parametrize("plan,rnn,n_rnn", [("t4", "lstm", 2), ("c1", "gru", 1)])
