@@ -173,11 +173,16 @@ int dgc_spmm_csr_rows(const int32_t* row_ptr, const int32_t* col, const float* d
 
 /* K1 (as dgc_spmm_csr_rows) that also writes an fp16 copy of `out` to out16
  * (same [rows, width] layout; may be NULL): the gathered x operand of the
- * fp16 tensor-core recurrence (dgc_lstm_fwd_tc_f16x). */
+ * fp16 tensor-core recurrence (dgc_lstm_fwd_tc_f16x). work (may be NULL): two
+ * int32 zeros in device memory; on large graphs (>= 256 rows per resident
+ * warp) the warps then take rows in order from this counter (the rows in
+ * flight stay one compact window, so their neighbour rows stay L2-resident)
+ * and the kernel leaves it zeroed. One counter pair per stream (launches
+ * sharing it must be stream-ordered). */
 int dgc_spmm_csr_x(const int32_t* row_ptr, const int32_t* col, const float* dinv,
                    const float* Y, const float* bias, float* out, void* out16,
                    const int32_t* rows, int64_t n_rows, int64_t row_begin, int32_t width,
-                   int32_t act, void* stream);
+                   int32_t act, int32_t* work, void* stream);
 
 /* K2: tcgen05 TF32 GEMM (TMA -> SMEM -> TMEM), fp32 storage, fp32 accumulate.
  *   C[M,N] = (accumulate ? C : 0) + op(A) op(B)  (+ bias[N]) (* (relu_src > 0))

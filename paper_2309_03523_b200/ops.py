@@ -77,7 +77,7 @@ def _req(t, dtype, name):
         raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
 
 
-def spmm_csr(row_ptr, col, dinv, Y, bias, out, act: int, nnz=0, n_cols=0, out16=None):
+def spmm_csr(row_ptr, col, dinv, Y, bias, out, act: int, nnz=0, n_cols=0, out16=None, work=None):
     """K1 dgc_spmm_csr: out = act(dinv_i * sum_c dinv_c Y_c + bias).
     Algorithmic bytes: 4W(n_cols + n_rows) + 4(n_rows+1)
     + 4 nnz (+ 4 n_cols for dinv)."""
@@ -88,12 +88,12 @@ def spmm_csr(row_ptr, col, dinv, Y, bias, out, act: int, nnz=0, n_cols=0, out16=
     nb = 4 * W * (n_cols + n) + 4 * (n + 1) + 4 * nnz + 4 * n_cols + (2 * W * n if out16 is not None else 0)
     _run("spmm_csr", lambda: _native.check(_native.lib().dgc_spmm_csr_x(
         _p(row_ptr), _p(col), _p(dinv), _p(Y), _p(bias), _p(out), _p(out16), None, n, 0, W, act,
-        _stream()), "dgc_spmm_csr_x"), nb, 2 * nnz * W)
+        _p(work), _stream()), "dgc_spmm_csr_x"), nb, 2 * nnz * W)
     return out
 
 
 def spmm_csr_rows(row_ptr, col, dinv, Y, bias, out, act: int, rows=None, n_rows=0, row_begin=0,
-                  nnz=0, n_cols=0, name="spmm_csr", out16=None):
+                  nnz=0, n_cols=0, name="spmm_csr", out16=None, work=None):
     """K1 over a row subset (dgc_spmm_csr_rows): the rows of the int32 list
     ``rows``, or the range [row_begin, row_begin + n_rows). nnz / n_cols: the
     subset's nonzeros and distinct gathered columns (algorithmic bytes)."""
@@ -104,7 +104,7 @@ def spmm_csr_rows(row_ptr, col, dinv, Y, bias, out, act: int, rows=None, n_rows=
     nb = 4 * W * (n_cols + n) + 8 * n + 4 * nnz + 4 * n_cols + (2 * W * n if out16 is not None else 0)
     _run(name, lambda: _native.check(_native.lib().dgc_spmm_csr_x(
         _p(row_ptr), _p(col), _p(dinv), _p(Y), _p(bias), _p(out), _p(out16), _p(rows), n,
-        int(row_begin), W, act, _stream()), "dgc_spmm_csr_x"), nb, 2 * nnz * W)
+        int(row_begin), W, act, _p(work), _stream()), "dgc_spmm_csr_x"), nb, 2 * nnz * W)
     return out
 
 

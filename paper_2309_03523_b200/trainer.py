@@ -285,6 +285,8 @@ class Shard:
             self.rnn_dc_scratch = torch.zeros(((max(self.R, 1) + 127) // 128 * 128, H), **f32)
             self.rnn_tc_prows = ops.rnn_tc_tiles(max(self.R, 1), H)
         self.dYext = torch.zeros((self.nloc, H), **f32)
+        # K1's row work counter (two int32, left zeroed by every launch)
+        self.spmm_work = torch.zeros(2, dtype=torch.int32, device=dev)
         self.colsum_scratch = torch.zeros(2 * 148 * max(GH, cfg.C, H), **f32)
         # fused bias-gradient partial sums (produced inside the kernels that write
         # the gradient tensors, reduced in fixed order by dgc_reduce_rows)
@@ -486,7 +488,7 @@ class Shard:
             Y = self.Yext[l]
             if l == 0 and self.agg_first:
                 ops.spmm_csr(self.row_ptr, self.col, self.dinv, self.X, None, self.AX, act=rnd2,
-                             nnz=self.nnz, n_cols=self.nloc)
+                             nnz=self.nnz, n_cols=self.nloc, work=self.spmm_work)
                 oact = 1 | rnd2  # ReLU (+ TF32 rounding of the next GEMM's operand)
                 if self.evolve:
                     ops.gemm_segmented(self.AX, self.evo[0]["Wstack"][kin:], self.Hl[0], n, H, kin,
@@ -514,17 +516,17 @@ class Shard:
                 # interior rows need no halo row: they aggregate while the exchange flies
                 ops.spmm_csr_rows(self.row_ptr, self.col, self.dinv, Y, self.p(b), self.Hl[l],
                                   act=1 | rnd2, rows=self.rows_int, nnz=self.nnz_int,
-                                  n_cols=self.rows_int.numel(), out16=self._x16_out(l))
+                                  n_cols=self.rows_int.numel(), out16=self._x16_out(l), work=self.spmm_work)
                 ev = yield from self._land(xp, tok, H, Y)
                 info["rows"] += sum(xp.sent_host)
                 info["xbytes"] += sum(xp.sent_host) * (H + 4) * 4
                 self._wait(ev)
                 ops.spmm_csr_rows(self.row_ptr, self.col, self.dinv, Y, self.p(b), self.Hl[l],
                                   act=1 | rnd2, rows=self.rows_bnd, nnz=self.nnz_bnd,
-                                  n_cols=self.nh + self.rows_bnd.numel(), out16=self._x16_out(l))
+                                  n_cols=self.nh + self.rows_bnd.numel(), out16=self._x16_out(l), work=self.spmm_work)
             else:
                 ops.spmm_csr(self.row_ptr, self.col, self.dinv, Y, self.p(b), self.Hl[l],
-                             act=1 | rnd2, nnz=self.nnz, n_cols=self.nloc, out16=self._x16_out(l))
+                             act=1 | rnd2, nnz=self.nnz, n_cols=self.nloc, out16=self._x16_out(l), work=self.spmm_work)
             hin, ldin, kin = self.Hl[l], H, H
         # ---------------- forward: time encoder ----------------
         xr, ldx = self.Hl[1], H
@@ -653,14 +655,14 @@ class Shard:
                 # the own block aggregates (Appendix B.4: only fresh rows return)
                 xp = self.xs[l]
                 ops.spmm_csr_rows(self.t_row_ptr, self.t_col, self.dinv, dZ, None, self.dYext,
-                                  act=rnd2, n_rows=self.nh, row_begin=n, name="spmm_csr_t")
+                                  act=rnd2, n_rows=self.nh, row_begin=n, name="spmm_csr_t", work=self.spmm_work)
                 ops.exchange_pack_back(xp.recvbuf, H, xp.rcounts, D, xp.rlist, xp.rlist_ptr,
                                        sum(xp.recv_host), self.dYext, xp.backsend)
                 tok = yield ("a2a_start", xp.backsend, list(xp.recv_host), None, xp.backrecv, H,
                              list(xp.sent_host), None)
                 ops.spmm_csr_rows(self.t_row_ptr, self.t_col, self.dinv, dZ, None, self.dYext,
                                   act=rnd2, n_rows=n, row_begin=0, nnz=self.nnz, n_cols=n,
-                                  name="spmm_csr_t")
+                                  name="spmm_csr_t", work=self.spmm_work)
                 res = yield ("a2a_finish", tok)
                 info["xbytes"] += sum(xp.recv_host) * H * 4
                 if res.get("stream") is not None:
@@ -671,7 +673,7 @@ class Shard:
                                       xp.ent_slot if self.stale_on else None, self.dYext)
             else:
                 ops.spmm_csr(self.t_row_ptr, self.t_col, self.dinv, dZ, None, self.dYext,
-                             act=rnd2, nnz=self.nnz, n_cols=n)
+                             act=rnd2, nnz=self.nnz, n_cols=n, work=self.spmm_work)
             hin_l, ldin_l, kin_l = (self.X, cfg.F, cfg.F) if l == 0 else (self.Hl[0], H, H)
             if self.evolve:
                 e = self.evo[l]

@@ -423,6 +423,32 @@ def test_spmm_row_subsets_equal_full():
     ops.spmm_csr_rows(t(row_ptr, torch.int32), t(col, torch.int32), t(dinv), Y, b, part, act=1,
                       n_rows=n - 1234, row_begin=0)
     assert torch.equal(part, full)
+    # dynamic row scheduling (work counter; 2.5M rows of width 128 so that every
+    # resident warp has >= 256 rows and the dynamic path runs): bitwise the
+    # static result, and the counter pair is left zeroed for the next launch
+    work = torch.zeros(2, dtype=torch.int32, device=dev)
+    nb = 148 * 64 * 256 + 3333
+    deg2 = rng.integers(1, 6, nb)
+    rp2 = np.concatenate([[0], np.cumsum(deg2)]).astype(np.int32)
+    c2 = np.sort(rng.integers(0, nb, (nb, 5)), 1)[np.arange(5)[None, :] < deg2[:, None]].astype(np.int32)
+    d2 = t(rng.random(nb).astype(np.float32))
+    Y2 = torch.randn((nb, W), device=dev)
+    st, dy = torch.zeros((nb, W), device=dev), torch.zeros((nb, W), device=dev)
+    ops.spmm_csr(t(rp2, torch.int32), t(c2, torch.int32), d2, Y2, None, st, act=0)
+    for _ in range(2):
+        ops.spmm_csr(t(rp2, torch.int32), t(c2, torch.int32), d2, Y2, None, dy, act=0, work=work)
+        assert torch.equal(st, dy) and work.cpu().tolist() == [0, 0]
+    for _ in range(3):
+        dyn = torch.zeros((n, W), device=dev)
+        ops.spmm_csr(t(row_ptr, torch.int32), t(col, torch.int32), t(dinv), Y, b, dyn, act=1,
+                     work=work)
+        assert torch.equal(dyn, full)
+        assert work.cpu().tolist() == [0, 0]
+    part.zero_()
+    for rows in (np.flatnonzero(~bnd), np.flatnonzero(bnd)):
+        ops.spmm_csr_rows(t(row_ptr, torch.int32), t(col, torch.int32), t(dinv), Y, b, part, act=1,
+                          rows=t(rows, torch.int32), work=work)
+    assert torch.equal(part, full) and work.cpu().tolist() == [0, 0]
 
 
 def test_softmax_xent_colsum_optimizers():

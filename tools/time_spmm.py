@@ -39,3 +39,19 @@ t = float(np.median(ts))
 alg = 8 * W * n + 4 * (n + 1) + 4 * nnz + 4 * n
 print(f"{cfg} W={W} rows {n} nnz {nnz}: {t:7.1f} us  alg {alg / t / 1e3:7.0f} GB/s  "
       f"gathered rows {nnz * W * 4 / t / 1e3:7.0f} GB/s")
+work = torch.zeros(2, dtype=torch.int32, device=dev)
+out3 = torch.empty_like(out)
+rund = lambda: _native.check(lib.dgc_spmm_csr_x(rp.data_ptr(), col.data_ptr(), dinv.data_ptr(),
+                                                Y.data_ptr(), None, out3.data_ptr(), None, None, n,
+                                                0, W, 0, work.data_ptr(), None), "spmm_x")
+rund(); torch.cuda.synchronize()
+assert torch.equal(out3, out)
+ts = []
+for _ in range(5):
+    flush.zero_()
+    s = torch.cuda.Event(enable_timing=True); e = torch.cuda.Event(enable_timing=True)
+    s.record(); rund(); e.record(); torch.cuda.synchronize()
+    ts.append(s.elapsed_time(e) * 1e3)
+t = float(np.median(ts))
+print(f"{cfg} W={W} dynamic rows: {t:7.1f} us  alg {alg / t / 1e3:7.0f} GB/s  "
+      f"gathered rows {nnz * W * 4 / t / 1e3:7.0f} GB/s")
