@@ -81,14 +81,22 @@ __device__ __forceinline__ float rna_tf32(float x) {
 // Compiled in only with -DDGC_LSTM_TIMESTAMPS (make DGC_TS=1): the production
 // kernels carry no probe.
 __device__ unsigned long long g_lstm_ts[256][8];
+__device__ unsigned long long g_lstm_ts2[256][8];  // forward chunk-0 internals
 #ifdef DGC_LSTM_TIMESTAMPS
 #define DGC_TS(cond, p, k) \
   do {                     \
     if (cond) g_lstm_ts[p][k] = globaltimer(); \
   } while (0)
+#define DGC_TS2(cond, p, k) \
+  do {                      \
+    if (cond) g_lstm_ts2[p][k] = globaltimer(); \
+  } while (0)
 #else
 #define DGC_TS(cond, p, k) \
   do {                     \
+  } while (0)
+#define DGC_TS2(cond, p, k) \
+  do {                      \
   } while (0)
 #endif
 
@@ -674,6 +682,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
         const int j = u0 + c0 + uq * 4;
         float4 pre[4];
         const uint32_t ta = tl + ab * kAccCols + c0;
+        DGC_TS2(ch == 0 && blockIdx.x == 0 && threadIdx.x == 64 && p < 256, p, 0);
         // staging row k (64 B) holds its 16-B quads XOR-swizzled by (k >> 1) & 3:
         // the 8 writing lanes and the 8 lanes of every read phase hit 8
         // distinct bank quads (conflict-free both ways)
@@ -695,6 +704,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
         if (kStgGates == 4) {
           float a[64];
           tmem_ld16x4(ta, ta + HU, ta + 2 * HU, ta + 3 * HU, a);
+          DGC_TS2(ch == 0 && blockIdx.x == 0 && threadIdx.x == 64 && p < 256, p, 1);
           stage(a, 4);
 #pragma unroll
           for (int gi = 0; gi < 4; ++gi)
@@ -712,6 +722,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
             __syncwarp();
           }
         }
+        DGC_TS2(ch == 0 && blockIdx.x == 0 && threadIdx.x == 64 && p < 256, p, 2);
         // next chunk's gx in flight while this chunk computes
         float4 xn[4];
 #pragma unroll
@@ -736,6 +747,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   hn.c = FX ? f16r(og.c * tc.c) : rna_tf32(og.c * tc.c);
           DGC_LSTM_CELL(x) DGC_LSTM_CELL(y) DGC_LSTM_CELL(z) DGC_LSTM_CELL(w)
 #undef DGC_LSTM_CELL
+          DGC_TS2(ch == 0 && blockIdx.x == 0 && threadIdx.x == 64 && p < 256, p, 3);
           constexpr int kSF = tc_save_floats<H>();
           float* sv = save + (int64_t)inst * kSF + j;
           if (H == 128) {  // compact fp16 row: h_in, c_in, i, f, g, o (the BPTT recomputes tanh(c))
@@ -758,6 +770,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           // read); inside a run it lives in creg and in the successor's c_in save
           if (!(has_next && n_mk)) st4(c_out + (int64_t)inst * ld + j, cn);
         }
+        DGC_TS2(ch == 0 && blockIdx.x == 0 && threadIdx.x == 64 && p < 256, p, 4);
         sts4(creg + ch * 512, cn);
         if (has_next) {
           float4 v;
@@ -769,6 +782,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           }
           put_h(j, v);
         }
+        DGC_TS2(ch == 0 && blockIdx.x == 0 && threadIdx.x == 64 && p < 256, p, 5);
         // first half of this CTA's units done: the MMA of p+1 may start on it
         if (kHalves == 2 && has_next && ch == NCH / 2 - 1) publish(0);
 #pragma unroll
@@ -1589,8 +1603,10 @@ extern "C" int dgc_rnn_fwd_tc_fused_available(int32_t F, int32_t H) {
 }
 
 extern "C" int dgc_debug_lstm_timestamps(unsigned long long* out, int n) {
-  if (n > 256 * 8) n = 256 * 8;
-  cudaError_t e = cudaMemcpyFromSymbol(out, g_lstm_ts, n * sizeof(unsigned long long));
+  if (n > 256 * 16) n = 256 * 16;
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_lstm_ts, (n < 256 * 8 ? n : 256 * 8) * sizeof(unsigned long long));
+  if (e == cudaSuccess && n > 256 * 8)
+    e = cudaMemcpyFromSymbol(out + 256 * 8, g_lstm_ts2, (n - 256 * 8) * sizeof(unsigned long long));
   return e == cudaSuccess ? DGC_OK : dgc::cuda_fail(e, "debug timestamps");
 }
 

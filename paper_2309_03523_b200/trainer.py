@@ -1213,17 +1213,21 @@ class DGNNTrainer:
         if self.pa.n_devices > 1 and len(self.shards) == 1:  # NCCL: this rank's share
             full = np.asarray([2 * int(self.layouts[0].key_ncut.sum()),
                                cfg.n_rnn * len(self.layouts[0].tkey_rows)], np.int64)
-        if stale_on:
-            billed = torch.stack([sh.billed_dev for sh in self.shards]).sum(0)
-        else:
-            billed = torch.as_tensor(full, device=self.device)
-        rows = torch.tensor([sum(i["rows"] for i in infos), sum(i["xbytes"] for i in infos)],
-                            dtype=torch.int64, device=self.device)
-        acc = torch.cat([billed.to(torch.int64), torch.as_tensor(full, device=self.device), rows])
-        if self.pa.n_devices > 1 and len(self.shards) == 1:
-            import torch.distributed as dist
-            dist.all_reduce(acc)
-        acc = [int(x) for x in acc.tolist()]
+        rows = [sum(i["rows"] for i in infos), sum(i["xbytes"] for i in infos)]
+        nccl = self.pa.n_devices > 1 and len(self.shards) == 1
+        if stale_on or nccl:  # device-side counters / a cross-rank sum
+            if stale_on:
+                billed = torch.stack([sh.billed_dev for sh in self.shards]).sum(0)
+            else:
+                billed = torch.as_tensor(full, device=self.device)
+            acc = torch.cat([billed.to(torch.int64), torch.as_tensor(full, device=self.device),
+                             torch.tensor(rows, dtype=torch.int64, device=self.device)])
+            if nccl:
+                import torch.distributed as dist
+                dist.all_reduce(acc)
+            acc = [int(x) for x in acc.tolist()]
+        else:  # host values only: no stream work behind an epoch that may already be queued
+            acc = [int(full[0]), int(full[1]), int(full[0]), int(full[1]), rows[0], rows[1]]
         billed_sp, billed_tm = acc[0] * per_msg, acc[1] * per_msg
         full_b = (acc[2] + acc[3]) * per_msg
         n_rows, xbytes = acc[4], acc[5]

@@ -27,3 +27,54 @@ for _ in range(3): tr.run_epoch(next_inputs=(xs, ys))
 print("epoch + next H2D staging (e2e loop): event ms, host ms, graph ms", timed(lambda: tr.run_epoch(next_inputs=(xs, ys))))
 print("epoch alone:                         ", timed(lambda: tr.run_epoch()))
 print("staging alone:                       ", timed(lambda: tr.stage_inputs(xs, ys)))
+def pipelined(k, stage=True):
+    prev = None
+    for _ in range(k):
+        p = tr.submit_epoch(next_inputs=(xs, ys) if stage else None)
+        if prev is not None:
+            float(prev.result().loss)
+        prev = p
+    float(prev.result().loss)
+    torch.cuda.synchronize()
+for stage in (True, False):
+    pipelined(3, stage)
+    torch.cuda.synchronize()
+    s = torch.cuda.Event(enable_timing=True); e = torch.cuda.Event(enable_timing=True)
+    s.record(); c0 = time.perf_counter(); pipelined(10, stage); c1 = time.perf_counter(); e.record(); torch.cuda.synchronize()
+    print(f"pipelined x10 stage={stage}: {s.elapsed_time(e) / 10:.3f} ms/step (host {(c1 - c0) * 100:.3f} ms/step)")
+# graph epochs back to back without any host read
+g, _ = next(iter(tr._graphs.values()))
+torch.cuda.synchronize()
+s = torch.cuda.Event(enable_timing=True); e = torch.cuda.Event(enable_timing=True)
+s.record()
+for _ in range(10): g.replay()
+e.record(); torch.cuda.synchronize()
+print(f"raw graph replay x10: {s.elapsed_time(e) / 10:.3f} ms/step")
+slot = torch.empty(1, dtype=torch.float64, pin_memory=True)
+src = torch.zeros(1, dtype=torch.float64, device="cuda")
+torch.cuda.synchronize()
+s.record()
+for _ in range(10):
+    g.replay(); slot.copy_(src, non_blocking=True)
+e.record(); torch.cuda.synchronize()
+print(f"graph replay + 8-B D2H copy x10: {s.elapsed_time(e) / 10:.3f} ms/step")
+torch.cuda.synchronize()
+s.record()
+for _ in range(10):
+    g.replay(); ev = torch.cuda.Event(); ev.record()
+e.record(); torch.cuda.synchronize()
+print(f"graph replay + event x10: {s.elapsed_time(e) / 10:.3f} ms/step")
+torch.cuda.synchronize()
+s.record(); c0 = time.perf_counter()
+pend = []
+for _ in range(10):
+    pend.append(tr.submit_epoch())
+    if len(pend) > 1: pend[-2].result()
+pend[-1].result()
+e.record(); torch.cuda.synchronize()
+print(f"submit_epoch x10 (no staging): {s.elapsed_time(e) / 10:.3f} ms/step; host {(time.perf_counter() - c0) * 100:.3f}")
+import cProfile, pstats
+pr = cProfile.Profile(); pr.enable()
+for _ in range(10):
+    tr.submit_epoch().result()
+pr.disable(); pstats.Stats(pr).sort_stats("tottime").print_stats(8)

@@ -28,8 +28,8 @@ for _ in range(3): fn()
 e.record(); torch.cuda.synchronize()
 print(f"fused fwd H {H}: {s.elapsed_time(e) / 3:.3f} ms")
 fn(); torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * (256 * 8))()
-_native.lib().dgc_debug_lstm_timestamps(buf, 256 * 8)
+buf = (ctypes.c_ulonglong * (256 * 16))()
+_native.lib().dgc_debug_lstm_timestamps(buf, 256 * 16)
 ts = np.array(buf[:L * 8], dtype=np.float64).reshape(L, 8)
 print("per-step us: h-ready->acc", np.mean(ts[:, 1] - ts[:, 0]) / 1e3, "epi", np.mean(ts[:, 2] - ts[:, 1]) / 1e3,
       "epi_end->next h-ready", np.mean(ts[1:, 0] - ts[:-1, 2]) / 1e3, "step", np.mean(np.diff(ts[:, 0])) / 1e3)
@@ -39,3 +39,7 @@ print("MMA warp (us rel. to h-ready[p]): x-part issued for p (before h-ready)", 
       "U kb2 ready", np.mean(ts[:, 7] - ts[:, 0]) / 1e3, "acc ready", np.mean(ts[:, 1] - ts[:, 0]) / 1e3)
 for p in range(1, 6):
     print(p, " ".join(f"{(ts[p, k] - ts[p, 0]) / 1e3:6.2f}" for k in (6, 0, 7, 1, 3, 4, 5, 2)))
+t2 = np.array(buf[256 * 8:256 * 8 + L * 8], dtype=np.float64).reshape(L, 8)
+d = np.diff(t2[1:, :6], axis=1) / 1e3
+print("chunk 0 (us): tmem ld", d[:, 0].mean(), "stage+lds", d[:, 1].mean(), "math", d[:, 2].mean(),
+      "stores", d[:, 3].mean(), "put_h", d[:, 4].mean())
