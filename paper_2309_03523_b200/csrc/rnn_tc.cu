@@ -1294,7 +1294,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           load_fields(0, it, dho[0][it], cvv[0][it], gv0[0][it], gv1[0][it]);
           if (inst[it] >= 0) {
             const int j = u0 + 32 + 4 * u8;
-            const __half* sv = reinterpret_cast<const __half*>(save + (int64_t)inst[it] * kSF + H);
+            const __half* sv = reinterpret_cast<const __half*>(save + (int64_t)inst[it] * kSF) + H;
             asm volatile("prefetch.global.L2 [%0];" ::"l"(sv + H + 4 * j));
             if (u8 == 0) {
               asm volatile("prefetch.global.L2 [%0];" ::"l"(sv + j));
