@@ -82,6 +82,7 @@ __device__ __forceinline__ float rna_tf32(float x) {
 // kernels carry no probe.
 __device__ unsigned long long g_lstm_ts[256][8];
 __device__ unsigned long long g_lstm_ts2[256][8];  // forward chunk-0 internals
+__device__ unsigned long long g_lstm_ts3[256][16];  // BPTT: each epilogue warp's lc1 done
 #ifdef DGC_LSTM_TIMESTAMPS
 #define DGC_TS(cond, p, k) \
   do {                     \
@@ -91,7 +92,14 @@ __device__ unsigned long long g_lstm_ts2[256][8];  // forward chunk-0 internals
   do {                      \
     if (cond) g_lstm_ts2[p][k] = globaltimer(); \
   } while (0)
+#define DGC_TS3(cond, p, k) \
+  do {                      \
+    if (cond) g_lstm_ts3[p][k] = globaltimer(); \
+  } while (0)
 #else
+#define DGC_TS3(cond, p, k) \
+  do {                      \
+  } while (0)
 #define DGC_TS(cond, p, k) \
   do {                     \
   } while (0)
@@ -403,11 +411,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
     }
     // local epilogue threads arrive (CTA scope); the peer's half of the h tile
     // lands by st.async (complete_tx), expected by one local arrive.expect_tx
-    mbar_init(&a_full[0], kEpiT);
-    mbar_init(&a_full[1], kEpiT);
+    // one arrival per epilogue warp (lane 0 after the warp's proxy fences and a
+    // __syncwarp): 384 per-thread arrivals on one mbarrier serialise for ~0.4 us
+    mbar_init(&a_full[0], kVEW);
+    mbar_init(&a_full[1], kVEW);
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 2);  // both CTAs' MMAs (multicast commit)
-      mbar_init(&acc_empty[a], kEpiT);
+      mbar_init(&acc_empty[a], kVEW);
     }
     for (int st = 0; st < kStages; ++st) {
       mbar_init(&x_full[st], 1);
@@ -625,8 +635,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
     }
     auto publish = [&](int half) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      if (ew == 0 && lane == 0) mbar_arrive_expect_tx(&a_full[half], kPeerBytes / kHalves);
-      else mbar_arrive(&a_full[half]);
+      __syncwarp();
+      if (lane == 0) {
+        if (ew == 0) mbar_arrive_expect_tx(&a_full[half], kPeerBytes / kHalves);
+        else mbar_arrive(&a_full[half]);
+      }
+    };
+    auto drained = [&](int ab) {  // this warp has read accumulator ab
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[ab]);
     };
     auto publish_all = [&]() {
       for (int h = 0; h < kHalves; ++h) publish(h);
@@ -664,7 +682,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       const uint32_t acc_par = FX ? ((p >> 1) & 1) : (p & 1);
       if (!active) {  // keep the a_full / acc_empty phase order: step p's MMA done first
         mbar_wait(&acc_full[ab], acc_par);
-        if (FX) mbar_arrive(&acc_empty[ab]);
+        if (FX) drained(ab);
         if (has_next) publish_all();
         continue;
       }
@@ -791,8 +809,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
         DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && p < 256 && ch < 3, p, 3 + ch);
       }
       DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && p < 256, p, 2);
-      fence_before();
-      if (FX) mbar_arrive(&acc_empty[ab]);  // this accumulator is drained
+      if (FX) drained(ab);  // this accumulator is drained
       if (has_next) publish(kHalves - 1);
     }
   }
@@ -1169,13 +1186,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   const int64_t row0 = tile * 4 * rq;
   const int u0 = (int)crank * HU, pu0 = (int)peer * HU;
   if (warp == 0 && lane == 0) {
+    // one arrival per epilogue warp (lane 0 after the warp's fences and a
+    // __syncwarp): 384 per-thread arrivals on one mbarrier serialise for ~0.4 us
     for (int s = 0; s < kKsAStages; ++s) {
-      mbar_init(&a_full[s], kEpiT);
+      mbar_init(&a_full[s], EW);
       mbar_init(&a_empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
-      mbar_init(&acc_empty[a], kEpiT);
+      mbar_init(&acc_empty[a], EW);
       mbar_init(&recv_full[a], 1);  // local arrive.expect_tx + the peer's st.async bytes
     }
     mbar_init(u_ready, 32);
@@ -1222,6 +1241,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
         const int sa = seq % kKsAStages;
         mbar_wait(&a_full[sa], (seq / kKsAStages) & 1);
         fence_after();
+        DGC_TS(i == KBO - 1 && blockIdx.x == 0 && lane == 0 && t < 256, t, 7);
         if (lane == 0) {
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
@@ -1348,7 +1368,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           }
         }
         fence_before();
-        mbar_arrive(&acc_empty[(p + 1) & 1]);  // this accumulator is fully read
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[(p + 1) & 1]);  // this accumulator is fully read
         DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 3);
         mbar_wait(&recv_full[t & 1], ((t - 1) >> 1) & 1);
         DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 4);
@@ -1439,10 +1460,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
         }
         fence_async_smem();
         DGC_TS(lc == 1 && blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 2);
+        DGC_TS3(lc == 1 && blockIdx.x == 0 && lane == 0 && t < 256, t, ew);
         DGC_TS(lc == 0 && blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 5);
-#pragma unroll
-        for (int g = 0; g < 2; ++g) mbar_arrive(&a_full[(seq0 + g) % kKsAStages]);
         __syncwarp();
+        if (lane == 0) {
+#pragma unroll
+          for (int g = 0; g < 2; ++g) mbar_arrive(&a_full[(seq0 + g) % kKsAStages]);
+        }
       }
 #pragma unroll
       for (int it = 0; it < 2; ++it) {
@@ -1607,6 +1631,12 @@ extern "C" int dgc_debug_lstm_timestamps(unsigned long long* out, int n) {
   cudaError_t e = cudaMemcpyFromSymbol(out, g_lstm_ts, (n < 256 * 8 ? n : 256 * 8) * sizeof(unsigned long long));
   if (e == cudaSuccess && n > 256 * 8)
     e = cudaMemcpyFromSymbol(out + 256 * 8, g_lstm_ts2, (n - 256 * 8) * sizeof(unsigned long long));
+  return e == cudaSuccess ? DGC_OK : dgc::cuda_fail(e, "debug timestamps");
+}
+
+extern "C" int dgc_debug_lstm_timestamps_warps(unsigned long long* out, int n) {
+  if (n > 256 * 16) n = 256 * 16;
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_lstm_ts3, n * sizeof(unsigned long long));
   return e == cudaSuccess ? DGC_OK : dgc::cuda_fail(e, "debug timestamps");
 }
 
