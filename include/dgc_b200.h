@@ -184,6 +184,14 @@ int dgc_spmm_csr_x(const int32_t* row_ptr, const int32_t* col, const float* dinv
                    const int32_t* rows, int64_t n_rows, int64_t row_begin, int32_t width,
                    int32_t act, int32_t* work, void* stream);
 
+/* K1 over all rows with an fp16 gathered operand Y16 [rows, width] (width 32..256):
+ * TF32 mode's resident fp16 features feed the layer-1 aggregation directly (no
+ * fp32 copy, no expansion kernel in the input pipeline). fp32 accumulation in CSR
+ * order and fp32 out; act and work as dgc_spmm_csr_x. */
+int dgc_spmm_csr_h(const int32_t* row_ptr, const int32_t* col, const float* dinv,
+                   const void* Y16, const float* bias, float* out, int64_t n_rows,
+                   int32_t width, int32_t act, int32_t* work, void* stream);
+
 /* K2: tcgen05 TF32 GEMM (TMA -> SMEM -> TMEM), fp32 storage, fp32 accumulate.
  *   C[M,N] = (accumulate ? C : 0) + op(A) op(B)  (+ bias[N]) (* (relu_src > 0))
  *   a_mn = 0: A is [M,K] (row stride lda); a_mn = 1: A stored as [K,M] (A^T)

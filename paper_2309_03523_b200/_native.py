@@ -75,6 +75,7 @@ _SIGS = {
     "dgc_stale_select": (_i32, [_p, _p, _p, _f32, _p, _p, _p, _i64, _i32, _p]),
     "dgc_compact_sent": (_i32, [_p, _i64, _p, _p, _p, _p]),
     "dgc_spmm_csr_rows": (_i32, [_p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i32, _i32, _p]),
+    "dgc_spmm_csr_h": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i32, _i32, _p, _p]),
     "dgc_spmm_csr_x": (_i32, [_p, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i32, _i32, _p, _p]),
     "dgc_stale_select2": (_i32, [_p, _p, _p, C.c_double, _p, C.c_double, _p, _p, _p, _i64, _i32,
                                  _p, _p, _p]),

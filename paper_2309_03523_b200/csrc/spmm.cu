@@ -147,6 +147,109 @@ __global__ void __launch_bounds__(256, NV == 1 ? 8 : 4) spmm_csr_kernel(
   }
 }
 
+// fp16 gathered operand (TF32 mode's resident fp16 features: no fp32 copy and
+// no expansion kernel in the input pipeline); lane = 8 halves (16 B), fp32
+// accumulation in the same CSR order, rows scheduled as spmm_csr_kernel.
+template <int LPR>
+__global__ void __launch_bounds__(256, 8) spmm_csr_h_kernel(
+    const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+    const float* __restrict__ dinv, const uint4* __restrict__ Y,
+    const float* __restrict__ bias, float* __restrict__ out, int64_t n_rows, int act,
+    int32_t* __restrict__ work) {
+  constexpr int W = LPR * 8;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = (int)(tid % LPR);
+  auto fma8 = [](float w, const uint4& u, float* a) {
+    const uint32_t q[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&q[k]));
+      a[2 * k] = fmaf(w, f.x, a[2 * k]);
+      a[2 * k + 1] = fmaf(w, f.y, a[2 * k + 1]);
+    }
+  };
+  auto process = [&](int64_t row) {
+    const int beg = __ldg(row_ptr + row), end = __ldg(row_ptr + row + 1);
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    int e = beg;
+    for (; e + kUnr <= end; e += kUnr) {
+      int c[kUnr];
+      float w[kUnr];
+      uint4 y[kUnr];
+#pragma unroll
+      for (int u = 0; u < kUnr; ++u) c[u] = __ldg(col + e + u);
+#pragma unroll
+      for (int u = 0; u < kUnr; ++u) w[u] = __ldg(dinv + c[u]);
+#pragma unroll
+      for (int u = 0; u < kUnr; ++u) y[u] = __ldg(Y + (int64_t)c[u] * LPR + lane);
+#pragma unroll
+      for (int u = 0; u < kUnr; ++u) fma8(w[u], y[u], acc);
+    }
+    for (; e < end; ++e) {
+      const int c = __ldg(col + e);
+      fma8(__ldg(dinv + c), __ldg(Y + (int64_t)c * LPR + lane), acc);
+    }
+    const float di = __ldg(dinv + row);
+    float o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float v = fmaf(di, acc[k], bias ? __ldg(bias + lane * 8 + k) : 0.f);
+      if (act & 1) v = fmaxf(v, 0.f);
+      if (act & 2) v = dgc::rna_tf32_f(v);
+      o[k] = v;
+    }
+    float4* op = reinterpret_cast<float4*>(out + row * W + lane * 8);
+    op[0] = make_float4(o[0], o[1], o[2], o[3]);
+    op[1] = make_float4(o[4], o[5], o[6], o[7]);
+  };
+  if (!work) {
+    const int64_t stride = ((int64_t)gridDim.x * blockDim.x) / LPR;
+    for (int64_t i = tid / LPR; i < n_rows; i += stride) process(i);
+    return;
+  }
+  constexpr int RPI = 32 / LPR, kIt = 16, kGrab = kIt * RPI;
+  const int wl = threadIdx.x & 31, sub = wl / LPR;
+  while (true) {
+    int base = 0;
+    if (wl == 0) base = atomicAdd(work, kGrab);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if ((int64_t)base >= n_rows) break;
+#pragma unroll 1
+    for (int k = 0; k < kIt; ++k) {
+      const int64_t i = (int64_t)base + k * RPI + sub;
+      if (i < n_rows) process(i);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(work + 1, 1) == (int)gridDim.x - 1) {
+      work[0] = 0;
+      work[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+template <int LPR>
+int launch_h(const int32_t* rp, const int32_t* col, const float* dinv, const void* Y,
+             const float* bias, float* out, int64_t n, int act, int32_t* work, cudaStream_t s) {
+  static const int resident = [] {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, spmm_csr_h_kernel<LPR>, 256, 0) !=
+            cudaSuccess || b < 1)
+      b = 1;
+    return b;
+  }();
+  const int grid = dgc::grid_for(n * LPR, 256, resident);
+  const int64_t warps = (int64_t)grid * 8;
+  if (n * LPR / 32 < 256 * warps) work = nullptr;  // as spmm_csr_kernel
+  spmm_csr_h_kernel<LPR><<<grid, 256, 0, s>>>(rp, col, dinv, static_cast<const uint4*>(Y), bias,
+                                               out, n, act, work);
+  DGC_CHECK_LAUNCH("spmm_csr_h_kernel");
+  return DGC_OK;
+}
+
 template <int LPR, int NV, bool F16>
 int launch(const int32_t* rp, const int32_t* col, const float* dinv, const float* Y,
            const float* bias, float* out, __half* out16, const int32_t* rows, int64_t n,
@@ -221,4 +324,19 @@ extern "C" int dgc_spmm_csr(const int32_t* row_ptr, const int32_t* col, const fl
                             int32_t width, int32_t act, void* stream) {
   return dgc_spmm_csr_x(row_ptr, col, dinv, Y, bias, out, nullptr, nullptr, n_rows, 0, width, act,
                         nullptr, stream);
+}
+
+extern "C" int dgc_spmm_csr_h(const int32_t* row_ptr, const int32_t* col, const float* dinv,
+                              const void* Y16, const float* bias, float* out, int64_t n_rows,
+                              int32_t width, int32_t act, int32_t* work, void* stream) {
+  DGC_REQUIRE(n_rows < (int64_t)INT32_MAX - 4096, "spmm_h: too many rows for the work counter");
+  if (n_rows == 0) return DGC_OK;
+  cudaStream_t s = dgc::as_stream(stream);
+  switch (width) {
+    case 32: return launch_h<4>(row_ptr, col, dinv, Y16, bias, out, n_rows, act, work, s);
+    case 64: return launch_h<8>(row_ptr, col, dinv, Y16, bias, out, n_rows, act, work, s);
+    case 128: return launch_h<16>(row_ptr, col, dinv, Y16, bias, out, n_rows, act, work, s);
+    case 256: return launch_h<32>(row_ptr, col, dinv, Y16, bias, out, n_rows, act, work, s);
+    default: return dgc::fail(DGC_ERR_ARG, "spmm_h: width must be 32, 64, 128 or 256");
+  }
 }

@@ -92,6 +92,19 @@ def spmm_csr(row_ptr, col, dinv, Y, bias, out, act: int, nnz=0, n_cols=0, out16=
     return out
 
 
+def spmm_csr_h(row_ptr, col, dinv, Y16, bias, out, act: int, nnz=0, n_cols=0, work=None):
+    """K1 with an fp16 gathered operand (dgc_spmm_csr_h), all rows."""
+    _req(row_ptr, torch.int32, "row_ptr"); _req(col, torch.int32, "col"); _req16(Y16, "Y16")
+    _req(out, torch.float32, "out")
+    n = row_ptr.numel() - 1
+    W = out.shape[-1]
+    nb = 2 * W * n_cols + 4 * W * n + 4 * (n + 1) + 4 * nnz + 4 * n_cols
+    _run("spmm_csr", lambda: _native.check(_native.lib().dgc_spmm_csr_h(
+        _p(row_ptr), _p(col), _p(dinv), _p(Y16), _p(bias), _p(out), n, W, act, _p(work),
+        _stream()), "dgc_spmm_csr_h"), nb, 2 * nnz * W)
+    return out
+
+
 def spmm_csr_rows(row_ptr, col, dinv, Y, bias, out, act: int, rows=None, n_rows=0, row_begin=0,
                   nnz=0, n_cols=0, name="spmm_csr", out16=None, work=None):
     """K1 over a row subset (dgc_spmm_csr_rows): the rows of the int32 list

@@ -246,6 +246,10 @@ class Shard:
                           and (cfg.precision == "tf32" or os.environ.get("DGC_AGG_FIRST") == "1")
                           and not os.environ.get("DGC_TRANSFORM_FIRST"))
         self.AX = torch.zeros((n, cfg.F), **f32) if self.agg_first else None
+        if self.agg_first and self.x_f16:
+            # the features feed only the layer-1 aggregation: keep them resident as
+            # fp16 (exact after round_f16), gathered by dgc_spmm_csr_h
+            self.X = self.X.half()
         self.hw = cfg.carry_width
         self.gx = torch.zeros((n, GH), **f32)
         self.hbuf = [torch.zeros((n, self.hw), **f32) for _ in range(cfg.n_rnn)]
@@ -487,8 +491,12 @@ class Shard:
         for l, (W, b) in enumerate((("W1", "b1"), ("W2", "b2"))):
             Y = self.Yext[l]
             if l == 0 and self.agg_first:
-                ops.spmm_csr(self.row_ptr, self.col, self.dinv, self.X, None, self.AX, act=rnd2,
-                             nnz=self.nnz, n_cols=self.nloc, work=self.spmm_work)
+                if self.X.dtype == torch.float16:
+                    ops.spmm_csr_h(self.row_ptr, self.col, self.dinv, self.X, None, self.AX,
+                                   act=rnd2, nnz=self.nnz, n_cols=self.nloc, work=self.spmm_work)
+                else:
+                    ops.spmm_csr(self.row_ptr, self.col, self.dinv, self.X, None, self.AX,
+                                 act=rnd2, nnz=self.nnz, n_cols=self.nloc, work=self.spmm_work)
                 oact = 1 | rnd2  # ReLU (+ TF32 rounding of the next GEMM's operand)
                 if self.evolve:
                     ops.gemm_segmented(self.AX, self.evo[0]["Wstack"][kin:], self.Hl[0], n, H, kin,
@@ -1045,7 +1053,8 @@ class DGNNTrainer:
         if self._copy_stream is None:
             self._copy_stream = torch.cuda.Stream(self.device)
             for sh, x in zip(self.shards, xs):
-                sh.X_stage = torch.empty(x.shape, dtype=x.dtype, device=self.device)
+                sh.X_stage = (None if sh.X.dtype == torch.float16 else
+                              torch.empty(x.shape, dtype=x.dtype, device=self.device))
                 sh.X_alt = torch.empty_like(sh.X)
                 sh.y_alt = torch.empty_like(sh.y)
         with torch.cuda.stream(self._copy_stream):
@@ -1053,6 +1062,10 @@ class DGNNTrainer:
             if self._alt_free_ev is not None:
                 self._copy_stream.wait_event(self._alt_free_ev)
             for sh, x, y in zip(self.shards, xs, ys):
+                if sh.X.dtype == torch.float16:  # resident fp16 features: straight in
+                    sh.X_alt.copy_(x, non_blocking=True)
+                    sh.y_alt.copy_(y, non_blocking=True)
+                    continue
                 sh.X_stage.copy_(x, non_blocking=True)
                 if sh.X_stage.dtype == torch.float16:  # fp16 features
                     ops.unpack_f16(sh.X_stage, sh.X_alt)
