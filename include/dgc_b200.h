@@ -173,7 +173,9 @@ int dgc_spmm_csr_rows(const int32_t* row_ptr, const int32_t* col, const float* d
 
 /* K1 (as dgc_spmm_csr_rows) that also writes an fp16 copy of `out` to out16
  * (same [rows, width] layout; may be NULL): the gathered x operand of the
- * fp16 tensor-core recurrence (dgc_lstm_fwd_tc_f16x). work (may be NULL): two
+ * fp16 tensor-core recurrence (dgc_lstm_fwd_tc_f16x) or of the fp16 GEMMs, as
+ * fp16(scale16 * out) (a power of two lifting a gradient into fp16's normal
+ * range; 1 for activations); out may then be NULL. work (may be NULL): two
  * int32 zeros in device memory; on large graphs (>= 256 rows per resident
  * warp) the warps then take rows in order from this counter (the rows in
  * flight stay one compact window, so their neighbour rows stay L2-resident)
@@ -182,15 +184,16 @@ int dgc_spmm_csr_rows(const int32_t* row_ptr, const int32_t* col, const float* d
 int dgc_spmm_csr_x(const int32_t* row_ptr, const int32_t* col, const float* dinv,
                    const float* Y, const float* bias, float* out, void* out16,
                    const int32_t* rows, int64_t n_rows, int64_t row_begin, int32_t width,
-                   int32_t act, int32_t* work, void* stream);
+                   int32_t act, int32_t* work, float scale16, void* stream);
 
 /* K1 over all rows with an fp16 gathered operand Y16 [rows, width] (width 32..256):
  * TF32 mode's resident fp16 features feed the layer-1 aggregation directly (no
  * fp32 copy, no expansion kernel in the input pipeline). fp32 accumulation in CSR
- * order and fp32 out; act and work as dgc_spmm_csr_x. */
+ * order; fp32 out and / or fp16(scale16 * out) in out16; act and work as
+ * dgc_spmm_csr_x. */
 int dgc_spmm_csr_h(const int32_t* row_ptr, const int32_t* col, const float* dinv,
-                   const void* Y16, const float* bias, float* out, int64_t n_rows,
-                   int32_t width, int32_t act, int32_t* work, void* stream);
+                   const void* Y16, const float* bias, float* out, void* out16, float scale16,
+                   int64_t n_rows, int32_t width, int32_t act, int32_t* work, void* stream);
 
 /* K2: tcgen05 TF32 GEMM (TMA -> SMEM -> TMEM), fp32 storage, fp32 accumulate.
  *   C[M,N] = (accumulate ? C : 0) + op(A) op(B)  (+ bias[N]) (* (relu_src > 0))
@@ -250,11 +253,16 @@ int dgc_gemm_tf32_stacked_a(const float* A0, int64_t lda0, const float* A1, int6
  * alpha undoing a power-of-two operand scale exactly (the BPTT's fp16 dgx is
  * S * dgx). Majorness, split-K, accumulate and colsum as dgc_gemm_tf32; A and
  * B are fp16 with row strides lda / ldb in elements (multiples of 8); an
- * MN-major B needs N % 64 == 0. The stacked form = dgc_gemm_tf32_stacked_a. */
+ * MN-major B needs N % 64 == 0. Unsplit K only: C16 (may be NULL) receives fp16(c16_scale * C)
+ * of the final C (after bias / activation / mask; row stride ldc16) -- the next fp16 operand,
+ * c16_scale a power of two for gradients -- and with C == NULL it is the only output; relu16
+ * (may be NULL) is an fp16 ReLU-mask source (row stride ldr16) in place of relu_src. The stacked
+ * form = dgc_gemm_tf32_stacked_a. */
 int dgc_gemm_f16(const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
                  int64_t M, int64_t N, int64_t K, int32_t a_mn, int32_t b_mn, float alpha,
                  const float* bias, const float* relu_src, int32_t accumulate, int32_t k_splits,
-                 float* partial, float* colsum_partial, void* stream);
+                 float* partial, float* colsum_partial, void* C16, int64_t ldc16, float c16_scale,
+                 const void* relu16, int64_t ldr16, void* stream);
 int dgc_gemm_f16_stacked_a(const void* A0, int64_t lda0, const void* A1, int64_t lda1, int64_t M0,
                            const void* B, int64_t ldb, float* C, int64_t ldc, int64_t M, int64_t N,
                            int64_t K, int32_t a_mn, int32_t b_mn, float alpha, int32_t k_splits,

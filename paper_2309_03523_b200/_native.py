@@ -36,7 +36,7 @@ _SIGS = {
     "dgc_round_f16": (_i32, [_p, _p, _i64, _p]),
     "dgc_unpack_f16": (_i32, [_p, _p, _i64, _p]),
     "dgc_gemm_f16": (_i32, [_p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _i32, _i32, _f32, _p, _p,
-                            _i32, _i32, _p, _p, _p]),
+                            _i32, _i32, _p, _p, _p, _i64, _f32, _p, _i64, _p]),
     "dgc_gemm_f16_stacked_a": (_i32, [_p, _i64, _p, _i64, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64,
                                       _i32, _i32, _f32, _i32, _p, _p]),
     "dgc_generate_graph": (_i32, [_p, _p, _p, _p, _i32]),
@@ -75,8 +75,8 @@ _SIGS = {
     "dgc_stale_select": (_i32, [_p, _p, _p, _f32, _p, _p, _p, _i64, _i32, _p]),
     "dgc_compact_sent": (_i32, [_p, _i64, _p, _p, _p, _p]),
     "dgc_spmm_csr_rows": (_i32, [_p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i32, _i32, _p]),
-    "dgc_spmm_csr_h": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i32, _i32, _p, _p]),
-    "dgc_spmm_csr_x": (_i32, [_p, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i32, _i32, _p, _p]),
+    "dgc_spmm_csr_h": (_i32, [_p, _p, _p, _p, _p, _p, _p, _f32, _i64, _i32, _i32, _p, _p]),
+    "dgc_spmm_csr_x": (_i32, [_p, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i32, _i32, _p, _f32, _p]),
     "dgc_stale_select2": (_i32, [_p, _p, _p, C.c_double, _p, C.c_double, _p, _p, _p, _i64, _i32,
                                  _p, _p, _p]),
     "dgc_exchange_rank": (_i32, [_p, _i64, _p, _i32, _p, _p, _p, _p]),

@@ -16,6 +16,8 @@
 // wait carries a watchdog (trap after ~4 s) so a bad descriptor can never
 // hang the GPU.
 
+#include <cuda_fp16.h>
+
 #include "tc_common.cuh"
 
 namespace {
@@ -38,7 +40,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                      int accumulate, float* __restrict__ partial,
                      float* __restrict__ colsum_partial, int b_res,
                      const int32_t* __restrict__ seg_of_mtile, int b_seg_rows,
-                     const int32_t* __restrict__ kitems, float alpha) {
+                     const int32_t* __restrict__ kitems, float alpha, __half* __restrict__ C16,
+                     int64_t ldc16, float c16_scale, const __half* __restrict__ relu16,
+                     int64_t ldr16) {
+  // C16: fp16(c16_scale * C) of the final tile (the next fp16 GEMM's / SpMM's
+  // operand); with C == nullptr it is the only output. relu16: an fp16 ReLU-mask
+  // source (the fp16 activation the forward consumed).
   // F16: fp16 operands (kind::f16, 64 elements per 128-B k-block row; MN-major
   // boxes of 64 MN elements x 64 k-rows), C = alpha * A B (alpha undoes an
   // operand's power-of-two scale exactly); else fp32 storage, TF32 math
@@ -315,6 +322,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           const int64_t row = m0 + q * 32 + lane;
+          if (relu16 && row < M) {  // fp16 mask source: 64-B row segment
+            const uint4* rs = reinterpret_cast<const uint4*>(relu16 + row * ldr16 + nb);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint4 m = (nb + 8 * j < N) ? __ldg(rs + j) : make_uint4(0u, 0u, 0u, 0u);
+              const uint32_t q[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&q[k]));
+                if (!(f.x > 0.f)) v[8 * j + 2 * k] = 0.f;
+                if (!(f.y > 0.f)) v[8 * j + 2 * k + 1] = 0.f;
+              }
+            }
+          }
           if (relu_src || colsum_partial) {
             // ReLU mask from the forward activation (thread = row, 128-B row segment)
             const bool rok = row < M;
@@ -348,6 +369,22 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (nb + lane < N) colsum_partial[((m0 / BM) * 4 + q) * N + nb + lane] = x[0];
             }
           }
+          if (C16 && row < M) {  // fp16 copy of the final tile row (thread = row)
+            __half* o = C16 + row * ldc16 + nb;
+            if (nb + 32 <= N) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                __half2 h[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  h[k] = __floats2half2_rn(v[8 * j + 2 * k] * c16_scale, v[8 * j + 2 * k + 1] * c16_scale);
+                *reinterpret_cast<uint4*>(o + 8 * j) = *reinterpret_cast<const uint4*>(h);
+              }
+            } else {
+              for (int u = 0; u < 32 && nb + u < N; ++u) o[u] = __float2half_rn(v[u] * c16_scale);
+            }
+          }
+          if (!C) continue;  // fp16-only output: no fp32 box to store
           if (lane == 0) {  // the store that last used this box has read it
             if (tma_store == 2) bulk_wait_read<1>();
             else bulk_wait_read<0>();
@@ -405,6 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (out_act & 1) y = fmaxf(y, 0.f);
               if (out_act & 2) y = dgc::rna_tf32_f(y);
               C[row * ldc + n] = y;
+              if (C16) C16[row * ldc16 + n] = __float2half_rn(y * c16_scale);
               csum += y;
             }
           }
@@ -519,7 +557,9 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
                 float* C, int64_t ldc, int64_t M,
                 int64_t N, int bn, int ntiles, int kb_total, int splits, int kb_per,
                 const float* bias, const float* relu_src, int accumulate, float* partial,
-                float* colsum_partial, const SegOpts& so, cudaStream_t s, float alpha = 1.f) {
+                float* colsum_partial, const SegOpts& so, cudaStream_t s, float alpha = 1.f,
+                __half* C16 = nullptr, int64_t ldc16 = 0, float c16_scale = 1.f,
+                const __half* relu16 = nullptr, int64_t ldr16 = 0) {
   const int ab = kABytes + bn * BK * 4;
   const int stage_bytes = ab * (SPLIT3 ? 2 : 1);
   // shared memory: pipeline stages (+ resident B panel) + the epilogue staging
@@ -556,7 +596,7 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   kern<<<grid, kThreads, smem, s>>>(ma, mb, mc, tma_store, c_rows_per_z, ma2, a2_row0, C, ldc, M, N, bn, stages, kb_total, kb_per, m_tiles,
                                     ntiles, splits, bias, relu_src, accumulate, partial,
                                     colsum_partial, b_res, so.seg_of_mtile, so.b_seg_rows,
-                                    so.kitems, alpha);
+                                    so.kitems, alpha, C16, ldc16, c16_scale, relu16, ldr16);
   DGC_CHECK_LAUNCH("gemm_tf32_kernel");
   return DGC_OK;
 }
@@ -593,7 +633,9 @@ static int gemm_impl(const float* A, int64_t lda, const float* B, int64_t ldb, f
                      int64_t ldc, int64_t M, int64_t N, int64_t K, int32_t a_mn, int32_t b_mn,
                      int32_t precision, const float* bias, const float* relu_src,
                      int32_t accumulate, int32_t k_splits, float* partial, float* colsum_partial,
-                     const SegOpts& so, void* stream, float alpha = 1.f) {
+                     const SegOpts& so, void* stream, float alpha = 1.f, void* C16 = nullptr,
+                     int64_t ldc16 = 0, float c16_scale = 1.f, const void* relu16 = nullptr,
+                     int64_t ldr16 = 0) {
   DGC_REQUIRE(M >= 0 && N >= 0 && K >= 0, "gemm: bad shape");
   const int out_act = (accumulate >> 1) & 3;  // bit 1 ReLU, bit 2 TF32-round the output
   accumulate &= 1;
@@ -666,12 +708,25 @@ static int gemm_impl(const float* A, int64_t lda, const float* B, int64_t ldb, f
   if (rc) return rc;
   float* part = (splits > 1 || so.kitems) ? partial : nullptr;
   DGC_REQUIRE(!(part && out_act), "gemm: an output activation needs an unsplit K");
+  DGC_REQUIRE(!(part && (C16 || relu16)), "gemm: fp16 outputs / masks need an unsplit K");
+  DGC_REQUIRE(C || C16 || M == 0 || N == 0, "gemm: no output");
+  DGC_REQUIRE(!C16 || (ldc16 % 8 == 0 && (reinterpret_cast<uintptr_t>(C16) & 15) == 0),
+              "gemm: the fp16 output needs 16-byte aligned rows");
+  DGC_REQUIRE(!relu16 || (ldr16 % 8 == 0 && (reinterpret_cast<uintptr_t>(relu16) & 15) == 0 &&
+                          !relu_src && !accumulate),
+              "gemm: the fp16 ReLU mask needs 16-byte aligned rows (and no fp32 mask / accumulate)");
   const bool s3 = precision == 3;
   // plain / bias-only outputs leave through TMA stores (box 32 cols x 32 rows)
   CUtensorMap mc;
   int tma_store = 0;
   int64_t c_rows_per_z = 0;
-  if (!getenv("DGC_GEMM_NO_TMA_STORE")) {
+  if (!part && !C) {
+    tma_store = 1;  // fp16-only output: the row path (thread = row), no fp32 box store
+  } else if (relu16) {
+    DGC_REQUIRE(!part, "gemm: the fp16 ReLU mask needs an unsplit K");
+    tma_store = make_map(&mc, C, M, N, ldc, 32, 32, false) == DGC_OK ? 1 : 0;
+    DGC_REQUIRE(tma_store, "gemm: the fp16 ReLU mask needs a TMA-storable C");
+  } else if (!getenv("DGC_GEMM_NO_TMA_STORE")) {
     if (!part) {
       tma_store = (!accumulate && ((ldc * 4) % 16 == 0) && (!relu_src || N % 4 == 0)) ? 1 : 0;
       if (tma_store && make_map(&mc, C, M, N, ldc, 32, 32, false) != DGC_OK) tma_store = 0;
@@ -693,7 +748,8 @@ static int gemm_impl(const float* A, int64_t lda, const float* B, int64_t ldb, f
                                      splits, kb_per,                                             \
                                      part ? nullptr : bias, part ? nullptr : relu_src,           \
                                      part ? 0 : (accumulate | (out_act << 1)), part,             \
-                                     colsum_partial, so, s, alpha);
+                                     colsum_partial, so, s, alpha, static_cast<__half*>(C16), ldc16,  \
+                                     c16_scale, static_cast<const __half*>(relu16), ldr16);
 #define DGC_GEMM_CASE(AM, BMN, S3) DGC_GEMM_CASE4(AM, BMN, S3, false)
     DGC_GEMM_CASE4(false, false, false, true)
     DGC_GEMM_CASE4(false, true, false, true)
@@ -778,10 +834,12 @@ extern "C" int dgc_gemm_tf32_stacked_a(const float* A0, int64_t lda0, const floa
 extern "C" int dgc_gemm_f16(const void* A, int64_t lda, const void* B, int64_t ldb, float* C,
                             int64_t ldc, int64_t M, int64_t N, int64_t K, int32_t a_mn, int32_t b_mn,
                             float alpha, const float* bias, const float* relu_src, int32_t accumulate,
-                            int32_t k_splits, float* partial, float* colsum_partial, void* stream) {
+                            int32_t k_splits, float* partial, float* colsum_partial, void* C16,
+                            int64_t ldc16, float c16_scale, const void* relu16, int64_t ldr16,
+                            void* stream) {
   return gemm_impl(static_cast<const float*>(A), lda, static_cast<const float*>(B), ldb, C, ldc, M,
                    N, K, a_mn, b_mn, 2, bias, relu_src, accumulate, k_splits, partial,
-                   colsum_partial, SegOpts{}, stream, alpha);
+                   colsum_partial, SegOpts{}, stream, alpha, C16, ldc16, c16_scale, relu16, ldr16);
 }
 
 extern "C" int dgc_gemm_f16_stacked_a(const void* A0, int64_t lda0, const void* A1, int64_t lda1,

@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(256, NV == 1 ? 8 : 4) spmm_csr_kernel(
     const float* __restrict__ dinv, const float4* __restrict__ Y,
     const float* __restrict__ bias, float4* __restrict__ out, __half* __restrict__ out16,
     const int32_t* __restrict__ rows, int64_t n_rows, int64_t row_begin, int act,
-    int32_t* __restrict__ work) {
+    int32_t* __restrict__ work, float scale16) {
   constexpr int W4 = LPR * NV;  // float4 per row
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = (int)(tid % LPR);
@@ -104,9 +104,10 @@ __global__ void __launch_bounds__(256, NV == 1 ? 8 : 4) spmm_csr_kernel(
         o.z = dgc::rna_tf32_f(o.z);
         o.w = dgc::rna_tf32_f(o.w);
       }
-      out[row * W4 + j4] = o;
+      if (out) out[row * W4 + j4] = o;
       if (F16) {
-        const __half2 a = __floats2half2_rn(o.x, o.y), h = __floats2half2_rn(o.z, o.w);
+        const __half2 a = __floats2half2_rn(o.x * scale16, o.y * scale16),
+                      h = __floats2half2_rn(o.z * scale16, o.w * scale16);
         reinterpret_cast<uint2*>(out16)[row * W4 + j4] =
             make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&h));
       }
@@ -154,8 +155,8 @@ template <int LPR>
 __global__ void __launch_bounds__(256, 8) spmm_csr_h_kernel(
     const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
     const float* __restrict__ dinv, const uint4* __restrict__ Y,
-    const float* __restrict__ bias, float* __restrict__ out, int64_t n_rows, int act,
-    int32_t* __restrict__ work) {
+    const float* __restrict__ bias, float* __restrict__ out, __half* __restrict__ out16,
+    float scale16, int64_t n_rows, int act, int32_t* __restrict__ work) {
   constexpr int W = LPR * 8;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = (int)(tid % LPR);
@@ -198,9 +199,17 @@ __global__ void __launch_bounds__(256, 8) spmm_csr_h_kernel(
       if (act & 2) v = dgc::rna_tf32_f(v);
       o[k] = v;
     }
-    float4* op = reinterpret_cast<float4*>(out + row * W + lane * 8);
-    op[0] = make_float4(o[0], o[1], o[2], o[3]);
-    op[1] = make_float4(o[4], o[5], o[6], o[7]);
+    if (out) {
+      float4* op = reinterpret_cast<float4*>(out + row * W + lane * 8);
+      op[0] = make_float4(o[0], o[1], o[2], o[3]);
+      op[1] = make_float4(o[4], o[5], o[6], o[7]);
+    }
+    if (out16) {
+      __half2 h[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) h[k] = __floats2half2_rn(o[2 * k] * scale16, o[2 * k + 1] * scale16);
+      reinterpret_cast<uint4*>(out16)[row * LPR + lane] = *reinterpret_cast<const uint4*>(h);
+    }
   };
   if (!work) {
     const int64_t stride = ((int64_t)gridDim.x * blockDim.x) / LPR;
@@ -233,7 +242,8 @@ __global__ void __launch_bounds__(256, 8) spmm_csr_h_kernel(
 
 template <int LPR>
 int launch_h(const int32_t* rp, const int32_t* col, const float* dinv, const void* Y,
-             const float* bias, float* out, int64_t n, int act, int32_t* work, cudaStream_t s) {
+             const float* bias, float* out, __half* out16, float scale16, int64_t n, int act,
+             int32_t* work, cudaStream_t s) {
   static const int resident = [] {
     int b = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, spmm_csr_h_kernel<LPR>, 256, 0) !=
@@ -245,7 +255,7 @@ int launch_h(const int32_t* rp, const int32_t* col, const float* dinv, const voi
   const int64_t warps = (int64_t)grid * 8;
   if (n * LPR / 32 < 256 * warps) work = nullptr;  // as spmm_csr_kernel
   spmm_csr_h_kernel<LPR><<<grid, 256, 0, s>>>(rp, col, dinv, static_cast<const uint4*>(Y), bias,
-                                               out, n, act, work);
+                                               out, out16, scale16, n, act, work);
   DGC_CHECK_LAUNCH("spmm_csr_h_kernel");
   return DGC_OK;
 }
@@ -253,7 +263,7 @@ int launch_h(const int32_t* rp, const int32_t* col, const float* dinv, const voi
 template <int LPR, int NV, bool F16>
 int launch(const int32_t* rp, const int32_t* col, const float* dinv, const float* Y,
            const float* bias, float* out, __half* out16, const int32_t* rows, int64_t n,
-           int64_t row_begin, int act, int32_t* work, cudaStream_t s) {
+           int64_t row_begin, int act, int32_t* work, float scale16, cudaStream_t s) {
   const int block = 256;
   static const int resident = [] {  // CTAs per SM at this instantiation's register count
     int b = 0;
@@ -271,7 +281,7 @@ int launch(const int32_t* rp, const int32_t* col, const float* dinv, const float
   if (n * LPR / 32 < 256 * warps) work = nullptr;
   spmm_csr_kernel<LPR, NV, F16><<<grid, block, 0, s>>>(
       rp, col, dinv, reinterpret_cast<const float4*>(Y), bias, reinterpret_cast<float4*>(out),
-      out16, rows, n, row_begin, act, work);
+      out16, rows, n, row_begin, act, work, scale16);
   DGC_CHECK_LAUNCH("spmm_csr_kernel");
   return DGC_OK;
 }
@@ -279,9 +289,11 @@ int launch(const int32_t* rp, const int32_t* col, const float* dinv, const float
 template <int LPR, int NV>
 int launch_f(const int32_t* rp, const int32_t* col, const float* dinv, const float* Y,
              const float* bias, float* out, __half* out16, const int32_t* rows, int64_t n,
-             int64_t row_begin, int act, int32_t* work, cudaStream_t s) {
-  return out16 ? launch<LPR, NV, true>(rp, col, dinv, Y, bias, out, out16, rows, n, row_begin, act, work, s)
-               : launch<LPR, NV, false>(rp, col, dinv, Y, bias, out, nullptr, rows, n, row_begin, act, work, s);
+             int64_t row_begin, int act, int32_t* work, float scale16, cudaStream_t s) {
+  return out16 ? launch<LPR, NV, true>(rp, col, dinv, Y, bias, out, out16, rows, n, row_begin, act, work,
+                                       scale16, s)
+               : launch<LPR, NV, false>(rp, col, dinv, Y, bias, out, nullptr, rows, n, row_begin, act, work,
+                                        1.f, s);
 }
 
 }  // namespace
@@ -289,14 +301,17 @@ int launch_f(const int32_t* rp, const int32_t* col, const float* dinv, const flo
 extern "C" int dgc_spmm_csr_x(const int32_t* row_ptr, const int32_t* col, const float* dinv,
                               const float* Y, const float* bias, float* out, void* out16,
                               const int32_t* rows, int64_t n_rows, int64_t row_begin,
-                              int32_t width, int32_t act, int32_t* work, void* stream) {
+                              int32_t width, int32_t act, int32_t* work, float scale16,
+                              void* stream) {
   DGC_REQUIRE(n_rows < (int64_t)INT32_MAX - 4096, "spmm: too many rows for the work counter");
+  if (n_rows == 0) return DGC_OK;  // (an empty output tensor has a null data pointer)
+  DGC_REQUIRE(out || out16, "spmm: no output");
   DGC_REQUIRE(width > 0 && width % 4 == 0, "spmm: width must be a positive multiple of 4");
   if (n_rows == 0) return DGC_OK;
   cudaStream_t s = dgc::as_stream(stream);
   __half* o16 = static_cast<__half*>(out16);
 #define DGC_SPMM_L(LPR, NV) \
-  launch_f<LPR, NV>(row_ptr, col, dinv, Y, bias, out, o16, rows, n_rows, row_begin, act, work, s)
+  launch_f<LPR, NV>(row_ptr, col, dinv, Y, bias, out, o16, rows, n_rows, row_begin, act, work, scale16, s)
   switch (width) {
     case 4: return DGC_SPMM_L(1, 1);
     case 8: return DGC_SPMM_L(2, 1);
@@ -316,27 +331,31 @@ extern "C" int dgc_spmm_csr_rows(const int32_t* row_ptr, const int32_t* col, con
                                  const int32_t* rows, int64_t n_rows, int64_t row_begin,
                                  int32_t width, int32_t act, void* stream) {
   return dgc_spmm_csr_x(row_ptr, col, dinv, Y, bias, out, nullptr, rows, n_rows, row_begin, width,
-                        act, nullptr, stream);
+                        act, nullptr, 1.f, stream);
 }
 
 extern "C" int dgc_spmm_csr(const int32_t* row_ptr, const int32_t* col, const float* dinv,
                             const float* Y, const float* bias, float* out, int64_t n_rows,
                             int32_t width, int32_t act, void* stream) {
   return dgc_spmm_csr_x(row_ptr, col, dinv, Y, bias, out, nullptr, nullptr, n_rows, 0, width, act,
-                        nullptr, stream);
+                        nullptr, 1.f, stream);
 }
 
 extern "C" int dgc_spmm_csr_h(const int32_t* row_ptr, const int32_t* col, const float* dinv,
-                              const void* Y16, const float* bias, float* out, int64_t n_rows,
-                              int32_t width, int32_t act, int32_t* work, void* stream) {
+                              const void* Y16, const float* bias, float* out, void* out16,
+                              float scale16, int64_t n_rows, int32_t width, int32_t act,
+                              int32_t* work, void* stream) {
   DGC_REQUIRE(n_rows < (int64_t)INT32_MAX - 4096, "spmm_h: too many rows for the work counter");
+  if (n_rows == 0) return DGC_OK;  // (an empty output tensor has a null data pointer)
+  DGC_REQUIRE(out || out16, "spmm_h: no output");
+  __half* o16 = static_cast<__half*>(out16);
   if (n_rows == 0) return DGC_OK;
   cudaStream_t s = dgc::as_stream(stream);
   switch (width) {
-    case 32: return launch_h<4>(row_ptr, col, dinv, Y16, bias, out, n_rows, act, work, s);
-    case 64: return launch_h<8>(row_ptr, col, dinv, Y16, bias, out, n_rows, act, work, s);
-    case 128: return launch_h<16>(row_ptr, col, dinv, Y16, bias, out, n_rows, act, work, s);
-    case 256: return launch_h<32>(row_ptr, col, dinv, Y16, bias, out, n_rows, act, work, s);
+    case 32: return launch_h<4>(row_ptr, col, dinv, Y16, bias, out, o16, scale16, n_rows, act, work, s);
+    case 64: return launch_h<8>(row_ptr, col, dinv, Y16, bias, out, o16, scale16, n_rows, act, work, s);
+    case 128: return launch_h<16>(row_ptr, col, dinv, Y16, bias, out, o16, scale16, n_rows, act, work, s);
+    case 256: return launch_h<32>(row_ptr, col, dinv, Y16, bias, out, o16, scale16, n_rows, act, work, s);
     default: return dgc::fail(DGC_ERR_ARG, "spmm_h: width must be 32, 64, 128 or 256");
   }
 }

@@ -77,47 +77,55 @@ def _req(t, dtype, name):
         raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
 
 
-def spmm_csr(row_ptr, col, dinv, Y, bias, out, act: int, nnz=0, n_cols=0, out16=None, work=None):
+def spmm_csr(row_ptr, col, dinv, Y, bias, out, act: int, nnz=0, n_cols=0, out16=None, work=None,
+             scale16=1.0):
     """K1 dgc_spmm_csr: out = act(dinv_i * sum_c dinv_c Y_c + bias).
     Algorithmic bytes: 4W(n_cols + n_rows) + 4(n_rows+1)
     + 4 nnz (+ 4 n_cols for dinv)."""
     _req(row_ptr, torch.int32, "row_ptr"); _req(col, torch.int32, "col")
     _req(Y, torch.float32, "Y"); _req(out, torch.float32, "out")
     n = row_ptr.numel() - 1
-    W = out.shape[-1] if out.dim() > 1 else 1
-    nb = 4 * W * (n_cols + n) + 4 * (n + 1) + 4 * nnz + 4 * n_cols + (2 * W * n if out16 is not None else 0)
+    ref = out if out is not None else out16
+    W = ref.shape[-1] if ref.dim() > 1 else 1
+    nb = (4 * W * n_cols + (4 * W * n if out is not None else 0) + 4 * (n + 1) + 4 * nnz
+          + 4 * n_cols + (2 * W * n if out16 is not None else 0))
     _run("spmm_csr", lambda: _native.check(_native.lib().dgc_spmm_csr_x(
         _p(row_ptr), _p(col), _p(dinv), _p(Y), _p(bias), _p(out), _p(out16), None, n, 0, W, act,
-        _p(work), _stream()), "dgc_spmm_csr_x"), nb, 2 * nnz * W)
+        _p(work), float(scale16), _stream()), "dgc_spmm_csr_x"), nb, 2 * nnz * W)
     return out
 
 
-def spmm_csr_h(row_ptr, col, dinv, Y16, bias, out, act: int, nnz=0, n_cols=0, work=None):
-    """K1 with an fp16 gathered operand (dgc_spmm_csr_h), all rows."""
+def spmm_csr_h(row_ptr, col, dinv, Y16, bias, out, act: int, nnz=0, n_cols=0, work=None,
+               out16=None, scale16=1.0, name="spmm_csr"):
+    """K1 with an fp16 gathered operand (dgc_spmm_csr_h), all rows; fp32 out
+    and / or fp16(scale16 * out) in out16."""
     _req(row_ptr, torch.int32, "row_ptr"); _req(col, torch.int32, "col"); _req16(Y16, "Y16")
-    _req(out, torch.float32, "out")
+    _req(out, torch.float32, "out"); _req16(out16, "out16")
     n = row_ptr.numel() - 1
-    W = out.shape[-1]
-    nb = 2 * W * n_cols + 4 * W * n + 4 * (n + 1) + 4 * nnz + 4 * n_cols
-    _run("spmm_csr", lambda: _native.check(_native.lib().dgc_spmm_csr_h(
-        _p(row_ptr), _p(col), _p(dinv), _p(Y16), _p(bias), _p(out), n, W, act, _p(work),
-        _stream()), "dgc_spmm_csr_h"), nb, 2 * nnz * W)
+    W = (out if out is not None else out16).shape[-1]
+    nb = (2 * W * n_cols + (4 * W * n if out is not None else 0) + (2 * W * n if out16 is not None else 0)
+          + 4 * (n + 1) + 4 * nnz + 4 * n_cols)
+    _run(name, lambda: _native.check(_native.lib().dgc_spmm_csr_h(
+        _p(row_ptr), _p(col), _p(dinv), _p(Y16), _p(bias), _p(out), _p(out16), float(scale16), n, W,
+        act, _p(work), _stream()), "dgc_spmm_csr_h"), nb, 2 * nnz * W)
     return out
 
 
 def spmm_csr_rows(row_ptr, col, dinv, Y, bias, out, act: int, rows=None, n_rows=0, row_begin=0,
-                  nnz=0, n_cols=0, name="spmm_csr", out16=None, work=None):
+                  nnz=0, n_cols=0, name="spmm_csr", out16=None, work=None, scale16=1.0):
     """K1 over a row subset (dgc_spmm_csr_rows): the rows of the int32 list
     ``rows``, or the range [row_begin, row_begin + n_rows). nnz / n_cols: the
     subset's nonzeros and distinct gathered columns (algorithmic bytes)."""
     _req(row_ptr, torch.int32, "row_ptr"); _req(col, torch.int32, "col")
     _req(Y, torch.float32, "Y"); _req(out, torch.float32, "out"); _req(rows, torch.int32, "rows")
     n = rows.numel() if rows is not None else int(n_rows)
-    W = out.shape[-1] if out.dim() > 1 else 1
+    ref = out if out is not None else out16
+    W = ref.shape[-1] if ref.dim() > 1 else 1
     nb = 4 * W * (n_cols + n) + 8 * n + 4 * nnz + 4 * n_cols + (2 * W * n if out16 is not None else 0)
     _run(name, lambda: _native.check(_native.lib().dgc_spmm_csr_x(
         _p(row_ptr), _p(col), _p(dinv), _p(Y), _p(bias), _p(out), _p(out16), _p(rows), n,
-        int(row_begin), W, act, _p(work), _stream()), "dgc_spmm_csr_x"), nb, 2 * nnz * W)
+        int(row_begin), W, act, _p(work), float(scale16), _stream()), "dgc_spmm_csr_x"), nb,
+        2 * nnz * W)
     return out
 
 
@@ -226,22 +234,29 @@ def _req16(t, name):
 
 def gemm_f16(A, B, C, M, N, K, *, a_mn=False, b_mn=True, lda=None, ldb=None, ldc=None, alpha=1.0,
              bias=None, relu_src=None, accumulate=False, k_splits=1, partial=None,
-             colsum_partial=None, act=0):
+             colsum_partial=None, act=0, C16=None, c16_scale=1.0, relu16=None):
     """K2 with fp16 operands (dgc_gemm_f16): C = alpha * op(A) op(B) [+ epilogue
-    as gemm()]; alpha undoes a power-of-two operand scale."""
-    _req16(A, "A"); _req16(B, "B"); _req(C, torch.float32, "C")
+    as gemm()]; alpha undoes a power-of-two operand scale. C16: fp16(c16_scale *
+    C) (C may be None: fp16-only output); relu16: fp16 ReLU-mask source."""
+    _req16(A, "A"); _req16(B, "B"); _req(C, torch.float32, "C"); _req16(C16, "C16")
+    _req16(relu16, "relu16")
     if partial is None and gemm_splits(K, 2, k_splits) > 1:
         raise ValueError(f"gemm_f16: K={K} needs a split-K partial buffer")
     lda = lda if lda is not None else (M if a_mn else K)
     ldb = ldb if ldb is not None else (N if b_mn else K)
     ldc = ldc if ldc is not None else N
     splits = gemm_splits(K, 2, k_splits)
-    nb = 2 * (M * K + K * N) + 4 * M * N * (1 + int(accumulate) + int(relu_src is not None))
+    nb = (2 * (M * K + K * N) + (4 * M * N if C is not None else 0) * (1 + int(accumulate))
+          + 4 * M * N * int(relu_src is not None) + 2 * M * N * (int(C16 is not None)
+                                                                 + int(relu16 is not None)))
     gname = "gemm_f16" + (f"[{M}x{N}x{K} a{int(a_mn)}b{int(b_mn)} s{splits}]" if _prof_detail else "")
+    ldc16 = C16.stride(0) if C16 is not None else 0
+    ldr16 = relu16.stride(0) if relu16 is not None else 0
     _run(gname, lambda: _native.check(_native.lib().dgc_gemm_f16(
         _p(A), lda, _p(B), ldb, _p(C), ldc, M, N, K, int(a_mn), int(b_mn), float(alpha), _p(bias),
         _p(relu_src), int(accumulate) | ((int(act) & 3) << 1), k_splits, _p(partial),
-        _p(colsum_partial), _stream()), "dgc_gemm_f16"), nb, 2.0 * M * N * K, 1 + int(splits > 1))
+        _p(colsum_partial), _p(C16), ldc16, float(c16_scale), _p(relu16), ldr16, _stream()),
+        "dgc_gemm_f16"), nb, 2.0 * M * N * K, 1 + int(splits > 1))
     return C
 
 

@@ -283,8 +283,9 @@ class Shard:
         self.f16_bwd = bool(self.fused_xproj)
         if self.f16_bwd:
             self.dgx = torch.zeros((n, GH), dtype=torch.float16, device=dev)
-            self.Wx16 = [torch.zeros((H, GH), dtype=torch.float16, device=dev)
-                         for _ in range(cfg.n_rnn)]
+            # fp16 mirror of the (TF32-rounded) parameters: the fp16 GEMMs' weights
+            self.params16 = torch.zeros(self.params.numel(), dtype=torch.float16, device=dev)
+            ops.to_f16(self.params_r, self.params16)
         if self.tc_rnn:
             self.rnn_dc_scratch = torch.zeros(((max(self.R, 1) + 127) // 128 * 128, H), **f32)
             self.rnn_tc_prows = ops.rnn_tc_tiles(max(self.R, 1), H)
@@ -315,6 +316,19 @@ class Shard:
         self.evolve = cfg.model == "evolve"
         if self.evolve:
             self._init_evolve(lay, cfg, dev)
+        # fp16 GCN (single device, aggregate-first, fused LSTM model): every
+        # structure-encoder tensor exists once, as fp16 -- A X, H1, Y2, H2 (the
+        # LSTM's x16[0]) forward; dZ2, dY2, dZ1 backward as S-scaled fp16 -- and
+        # the GEMMs / SpMMs read and write them directly (fp32 accumulation)
+        self.f16_gcn = bool(self.f16_bwd and self.agg_first and not self.evolve
+                            and self.X.dtype == torch.float16)
+        if self.f16_gcn:
+            h16 = dict(dtype=torch.float16, device=dev)
+            self.AX = None
+            self.AX16 = torch.zeros((n, cfg.F), **h16)
+            self.H1_16, self.Y16 = torch.zeros((n, H), **h16), torch.zeros((n, H), **h16)
+            self.dZ2_16, self.dY16 = torch.zeros((n, H), **h16), torch.zeros((n, H), **h16)
+            self.dZ1_16 = torch.zeros((n, H), **h16)
         # exchange data plane (D > 1): one record buffer per exchange, all peers
         # per launch; interior rows (no halo column) aggregate while it is in
         # flight, boundary rows after it lands
@@ -387,6 +401,12 @@ class Shard:
     def _x16_out(self, l):
         """fp16 copy target of GCN layer l's output: the first LSTM layer's x16."""
         return self.x16[0] if (self.x16 is not None and l == 1 and not self.evolve) else None
+
+    def p16(self, name):
+        """fp16 view of a parameter (the fp16-operand GEMMs' weights)."""
+        o, shape = self.offs[name]
+        n = int(np.prod(shape))
+        return self.params16[o:o + n].view(*shape)
 
     def pr(self, name):
         """GEMM operand view of a parameter (TF32-rounded copy in TF32 mode)."""
@@ -490,6 +510,19 @@ class Shard:
         hin, ldin, kin = self.X, cfg.F, cfg.F
         for l, (W, b) in enumerate((("W1", "b1"), ("W2", "b2"))):
             Y = self.Yext[l]
+            if l == 0 and self.f16_gcn:  # A X and H1 = relu((A X) W1 + b1), fp16 only
+                ops.spmm_csr_h(self.row_ptr, self.col, self.dinv, self.X, None, None, act=0,
+                               nnz=self.nnz, n_cols=self.nloc, work=self.spmm_work,
+                               out16=self.AX16)
+                ops.gemm_f16(self.AX16, self.p16(W), None, n, H, kin, lda=kin, bias=self.p(b),
+                             act=1, C16=self.H1_16)
+                continue
+            if l == 1 and self.f16_gcn:  # Y2 = H1 W2 and H2 = relu(A Y2 + b2), fp16 only
+                ops.gemm_f16(self.H1_16, self.p16(W), None, n, H, H, lda=H, C16=self.Y16)
+                ops.spmm_csr_h(self.row_ptr, self.col, self.dinv, self.Y16, self.p(b), None, act=1,
+                               nnz=self.nnz, n_cols=self.nloc, work=self.spmm_work,
+                               out16=self.x16[0])
+                continue
             if l == 0 and self.agg_first:
                 if self.X.dtype == torch.float16:
                     ops.spmm_csr_h(self.row_ptr, self.col, self.dinv, self.X, None, self.AX,
@@ -633,9 +666,13 @@ class Shard:
                     ops.gemm(self.save[k], self.dgx, gU, H, GH, n, a_mn=True, lda=self.sf,
                              ldb=GH, ldc=GH, precision=prec, k_splits=ks, partial=part)
             relu_src = self.Hl[1] if k == 0 else None
-            if self.f16_bwd:
-                ops.to_f16(self.pr(f"Wx{k}"), self.Wx16[k])
-                ops.gemm_f16(self.dgx, self.Wx16[k], self.dh2, n, H, GH, b_mn=False, ldb=GH,
+            if self.f16_gcn and k == 0:  # dZ2 = (dgx Wx^T) * (H2 > 0) as S-scaled fp16
+                ops.gemm_f16(self.dgx, self.p16(f"Wx{k}"), None, n, H, GH, b_mn=False, ldb=GH,
+                             alpha=self.inv_da_scale, relu16=self.x16[0],
+                             colsum_partial=self.bp_b[1], C16=self.dZ2_16,
+                             c16_scale=2.0 ** self.da_exp)
+            elif self.f16_bwd:
+                ops.gemm_f16(self.dgx, self.p16(f"Wx{k}"), self.dh2, n, H, GH, b_mn=False, ldb=GH,
                              alpha=self.inv_da_scale, relu_src=relu_src,
                              colsum_partial=self.bp_b[1] if k == 0 else None)
             else:
@@ -648,6 +685,22 @@ class Shard:
         dZ = self.dh  # = dH2 * (H2 > 0), fused into the last GEMM epilogue
         for l in (1, 0):
             W, b = ("W1", "b1") if l == 0 else ("W2", "b2")
+            if self.f16_gcn:  # S-scaled fp16 gradients, alpha = 1/S in every contraction
+                inv, S = self.inv_da_scale, 2.0 ** self.da_exp
+                if l == 1:
+                    ops.spmm_csr_h(self.t_row_ptr, self.t_col, self.dinv, self.dZ2_16, None, None,
+                                   act=0, nnz=self.nnz, n_cols=n, work=self.spmm_work,
+                                   out16=self.dY16, name="spmm_csr_t")
+                    ops.gemm_f16(self.H1_16, self.dY16, self.g(W), H, H, n, a_mn=True, lda=H,
+                                 ldb=H, alpha=inv, k_splits=ks, partial=part)
+                    ops.gemm_f16(self.dY16, self.p16(W), None, n, H, H, b_mn=False, ldb=H,
+                                 alpha=inv, relu16=self.H1_16, colsum_partial=self.bp_b[0],
+                                 C16=self.dZ1_16, c16_scale=S)
+                    rjobs.append((self.bp_b[0], 4 * self.m_tiles, H, self.g("b1")))
+                else:
+                    ops.gemm_f16(self.AX16, self.dZ1_16, self.g(W), cfg.F, H, n, a_mn=True,
+                                 lda=cfg.F, ldb=H, alpha=inv, k_splits=ks, partial=part)
+                continue
             if l == 0 and self.agg_first:  # dW1 = (A X)^T dZ1: no transposed SpMM
                 if self.evolve:
                     ops.gemm_segmented(self.AX, dZ, self.evo[0]["dW_direct"], cfg.F, H, n,
@@ -746,6 +799,8 @@ class Shard:
             ops.sgd(self.params, self.grads, self.m, cfg.lr, cfg.momentum)
         if self.tf32:
             ops.round_tf32(self.params, self.params_r)
+        if self.f16_bwd:
+            ops.to_f16(self.params_r, self.params16)
         return info
 
 
@@ -1287,8 +1342,11 @@ class DGNNTrainer:
                 int(sh.step_dev.item()) if self.cfg.optimizer == "adam" else sh.step_count)
 
     def relu_masks(self, shard: int = 0):
-        """{GCN layer: bool (n_own, H)} -- this epoch's ReLU decisions (H_l > 0)."""
+        """{GCN layer: bool (n_own, H)} -- this epoch's ReLU decisions (H_l > 0;
+        the fp16 activations the next layer consumed on the fp16 GCN path)."""
         sh = self.shards[shard]
+        if sh.f16_gcn:
+            return {0: (sh.H1_16 > 0).cpu().numpy(), 1: (sh.x16[0] > 0).cpu().numpy()}
         return {l: (sh.Hl[l] > 0).cpu().numpy() for l in range(2)}
 
 

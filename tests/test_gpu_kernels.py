@@ -71,6 +71,61 @@ def test_gemm_f16(a_mn, b_mn, M, N, K):
     close(C.cpu().numpy(), ref, 1e-5, f"gemm_f16 a_mn={a_mn} b_mn={b_mn}")
 
 
+def test_gemm_f16_fp16_outputs_and_mask():
+    """fp16-only output (C16 = fp16(S * C), no fp32 C) with an fp16 ReLU-mask
+    source and column sums, against fp64; and the same with an fp32 C beside."""
+    from paper_2309_03523_b200 import ops
+    rng = np.random.default_rng(23)
+    M, N, K, S = 1000, 128, 128, 4096.0
+    A = (rng.standard_normal((M, K)) * S * 1e-4).astype(np.float16)   # an S-scaled gradient
+    B = rng.standard_normal((N, K)).astype(np.float16)                # [N, K]: K-major B
+    mask16 = rng.standard_normal((M, N)).astype(np.float16)
+    ref = (A.astype(np.float64) @ B.astype(np.float64).T) / S * (mask16 > 0)
+    C16 = torch.zeros((M, N), dtype=torch.float16, device=dev)
+    cs = torch.zeros(((M + 127) // 128 * 4) * N, device=dev)
+    ops.gemm_f16(t(A, torch.float16), t(B, torch.float16), None, M, N, K, b_mn=False, ldb=K,
+                 alpha=1 / S, relu16=t(mask16, torch.float16), colsum_partial=cs, C16=C16,
+                 c16_scale=S)
+    torch.cuda.synchronize()
+    close(C16.float().cpu().numpy() / S, ref, 2e-3, "fp16-only output")
+    close(cs.view(-1, N).sum(0).cpu().numpy(), ref.sum(0), 1e-5, "column sums")
+    C = torch.zeros((M, N), device=dev)
+    ops.gemm_f16(t(A, torch.float16), t(B, torch.float16), C, M, N, K, b_mn=False, ldb=K,
+                 alpha=1 / S, relu16=t(mask16, torch.float16))
+    torch.cuda.synchronize()
+    close(C.cpu().numpy(), ref, 1e-5, "fp32 output, fp16 mask")
+
+
+def test_spmm_fp16_operand_and_outputs():
+    """dgc_spmm_csr_h (fp16 gathered rows) equals the fp32 kernel on the same
+    fp16 values bitwise; fp16 outputs = fp16(scale16 * out), with or without out."""
+    from paper_2309_03523_b200 import ops
+    rng = np.random.default_rng(31)
+    n, nc, W = 5000, 6000, 128
+    deg = rng.integers(1, 20, n)
+    rp = np.concatenate([[0], np.cumsum(deg)]).astype(np.int32)
+    col = np.concatenate([np.sort(rng.choice(nc, d, replace=False)) for d in deg]).astype(np.int32)
+    dinv = t(rng.random(nc).astype(np.float32) + 0.1)
+    Y16 = t(rng.standard_normal((nc, W)).astype(np.float16), torch.float16)
+    b = t(rng.standard_normal(W).astype(np.float32))
+    ref = torch.zeros((n, W), device=dev)
+    ops.spmm_csr(t(rp, torch.int32), t(col, torch.int32), dinv, Y16.float(), b, ref, act=1)
+    out = torch.zeros((n, W), device=dev)
+    o16 = torch.zeros((n, W), dtype=torch.float16, device=dev)
+    ops.spmm_csr_h(t(rp, torch.int32), t(col, torch.int32), dinv, Y16, b, out, act=1, out16=o16,
+                   scale16=8.0)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref) and torch.equal(o16, (ref * 8.0).half())
+    o16b = torch.zeros_like(o16)
+    ops.spmm_csr_h(t(rp, torch.int32), t(col, torch.int32), dinv, Y16, b, None, act=1, out16=o16b,
+                   scale16=8.0)
+    o16c = torch.zeros_like(o16)
+    ops.spmm_csr(t(rp, torch.int32), t(col, torch.int32), dinv, Y16.float(), b, None, act=1,
+                 out16=o16c, scale16=8.0)
+    torch.cuda.synchronize()
+    assert torch.equal(o16b, o16) and torch.equal(o16c, o16)
+
+
 def test_gemm_f16_stacked_split_k():
     """[dWx; dU] = [x; h_in]^T (S dgx) with fp16 operands, split-K, alpha = 1/S:
     the BPTT weight-gradient form (MN-major A halves with their own strides)."""
