@@ -25,6 +25,7 @@ namespace {
 using namespace dgc::tc;
 using dgc::make_map;
 using dgc::make_map_f16;
+using dgc::make_map_f16_sw64;
 constexpr int kEpiWarps = 8;  // 2 per TMEM lane quadrant, round-robin 32-column chunks
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kABytes = BM * BK * 4;  // 16 KiB
@@ -283,14 +284,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int a = i & 1;
       const uint32_t aph = (i >> 1) & 1;
-      if (relu_src && tma_store) {
+      if ((relu_src || relu16) && tma_store) {
         // this thread's row of the ReLU mask streams into L1 while the tile's
         // MMAs finish (thread = row; its chunks of the tile's columns)
         const int64_t row = m0 + q * 32 + lane;
         if (row < M)
           for (int c = 32 * chalf; c < bn; c += 32 * (kEpiWarps / 4))
-            if (n0 + c < N)
-              asm volatile("prefetch.global.L1 [%0];" ::"l"(relu_src + row * ldc + n0 + c));
+            if (n0 + c < N) {
+              if (relu_src) asm volatile("prefetch.global.L1 [%0];" ::"l"(relu_src + row * ldc + n0 + c));
+              else asm volatile("prefetch.global.L1 [%0];" ::"l"(relu16 + row * ldr16 + n0 + c));
+            }
       }
       mbar_wait(&tfull[a], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -369,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (nb + lane < N) colsum_partial[((m0 / BM) * 4 + q) * N + nb + lane] = x[0];
             }
           }
-          if (C16 && row < M) {  // fp16 copy of the final tile row (thread = row)
+          if (C16 && C && row < M) {  // fp16 copy beside C (thread = row, direct stores)
             __half* o = C16 + row * ldc16 + nb;
             if (nb + 32 <= N) {
 #pragma unroll
@@ -384,12 +387,29 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int u = 0; u < 32 && nb + u < N; ++u) o[u] = __float2half_rn(v[u] * c16_scale);
             }
           }
-          if (!C) continue;  // fp16-only output: no fp32 box to store
           if (lane == 0) {  // the store that last used this box has read it
             if (tma_store == 2) bulk_wait_read<1>();
             else bulk_wait_read<0>();
           }
           __syncwarp();
+          if (!C) {  // fp16-only output: a [32 rows x 64 B] SWIZZLE_64B box, one TMA store
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              __half2 h[4];
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                h[k] = __floats2half2_rn(v[8 * j + 2 * k] * c16_scale, v[8 * j + 2 * k + 1] * c16_scale);
+              *reinterpret_cast<uint4*>(box + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
+                  *reinterpret_cast<const uint4*>(h);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmC, box, (int)(n0 + c), (int)(m0 + q * 32));
+              bulk_commit();
+            }
+            continue;
+          }
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             *reinterpret_cast<float4*>(box + sw128_offset(lane, 4 * j)) =
@@ -721,7 +741,11 @@ static int gemm_impl(const float* A, int64_t lda, const float* B, int64_t ldb, f
   int tma_store = 0;
   int64_t c_rows_per_z = 0;
   if (!part && !C) {
-    tma_store = 1;  // fp16-only output: the row path (thread = row), no fp32 box store
+    // fp16-only output: the row path (thread = row) and TMA stores of
+    // [32 x 32] fp16 boxes (SWIZZLE_64B) from the per-warp staging box
+    rc = make_map_f16_sw64(&mc, C16, M, N, ldc16, 32, 32);
+    if (rc) return rc;
+    tma_store = 1;
   } else if (relu16) {
     DGC_REQUIRE(!part, "gemm: the fp16 ReLU mask needs an unsplit K");
     tma_store = make_map(&mc, C, M, N, ldc, 32, 32, false) == DGC_OK ? 1 : 0;

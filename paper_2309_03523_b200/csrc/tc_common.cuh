@@ -387,6 +387,25 @@ inline int make_map_f16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t
   return DGC_OK;
 }
 
+// Row-major [rows, cols] fp16 tensor, SWIZZLE_64B boxes (64-B box rows: the
+// epilogue's [32 rows x 32 cols] fp16 output tiles)
+inline int make_map_f16_sw64(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols,
+                             int64_t ld, uint32_t box_cols, uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return dgc::fail(DGC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || ((ld * 2) & 15))
+    return dgc::fail(DGC_ERR_ARG, "gemm: fp16 output needs 16-byte aligned base and row stride");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return dgc::fail(DGC_ERR_CUDA, "cuTensorMapEncodeTiled (fp16 out) failed");
+  return DGC_OK;
+}
+
 // Row gathers (tile::gather4) of a row-major [rows, cols] fp16 tensor: boxes of
 // 64 columns (128 B) x 1 row, SWIZZLE_128B (the K-major UMMA operand layout).
 inline int make_gather_map_f16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols,
