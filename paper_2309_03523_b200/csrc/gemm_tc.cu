@@ -384,7 +384,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 *reinterpret_cast<uint4*>(o + 8 * j) = *reinterpret_cast<const uint4*>(h);
               }
             } else {
-              for (int u = 0; u < 32 && nb + u < N; ++u) o[u] = __float2half_rn(v[u] * c16_scale);
+#pragma unroll
+              for (int u = 0; u < 32; ++u)  // (unrolled: v stays in registers)
+                if (nb + u < N) o[u] = __float2half_rn(v[u] * c16_scale);
             }
           }
           if (lane == 0) {  // the store that last used this box has read it
