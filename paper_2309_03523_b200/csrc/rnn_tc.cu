@@ -82,7 +82,7 @@ __device__ __forceinline__ float rna_tf32(float x) {
 // kernels carry no probe.
 __device__ unsigned long long g_lstm_ts[256][8];
 __device__ unsigned long long g_lstm_ts2[256][8];  // forward chunk-0 internals
-__device__ unsigned long long g_lstm_ts3[256][16];  // BPTT: each epilogue warp's lc1 done
+__device__ unsigned long long g_lstm_ts3[256][32];  // BPTT: each epilogue warp's last chunk done
 #ifdef DGC_LSTM_TIMESTAMPS
 #define DGC_TS(cond, p, k) \
   do {                     \
@@ -1197,8 +1197,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       mbar_init(&acc_empty[a], EW);
       mbar_init(&recv_full[a], 1);  // local arrive.expect_tx + the peer's st.async bytes
     }
-    mbar_init(u_ready, 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  {
+    // the MMA's B operand, resident for the launch: U's 256 own gate columns for
+    // all H units as fp16, K-major SWIZZLE_128B ([4 k-blocks][H rows][128 B]),
+    // written by every thread (one warp took ~20 us, the first MMA's wait)
+#pragma unroll 4
+    for (int c = threadIdx.x; c < H * (4 * HU / 8); c += 64 + 32 * EW) {
+      const int n = c % H, k0 = (c / H) * 8;
+      const int i = k0 >> 5, gcol = (i & 3) * H + 32 * (2 * (int)crank + (i >> 2)) + (k0 & 31);
+      const float* src = U + (int64_t)n * G4 + gcol;
+      const float4 a = ldg4(src), b = ldg4(src + 4);
+      const uint32_t dst = smem_u32(sU) + (uint32_t)((k0 >> 6) * H * 128 + n * 128 +
+                                                     ((((k0 & 63) >> 3) ^ (n & 7)) << 4));
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(h2u(a.x, a.y)),
+                   "r"(h2u(a.z, a.w)), "r"(h2u(b.x, b.y)), "r"(h2u(b.z, b.w))
+                   : "memory");
+    }
+    fence_async_smem();
   }
   if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
   fence_before();
@@ -1210,27 +1227,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   // 4 lc + g (chunk lc: global chunk 2*crank + lc, gate g); fp16 k-block k >> 6
 
   if (warp == 0) {
-    // the MMA's B operand, resident for the launch: U's 256 own gate columns for
-    // all H units as fp16, K-major SWIZZLE_128B ([4 k-blocks][H rows][128 B])
-    for (int c = lane; c < H * (4 * HU / 8); c += 32) {
-      const int n = c % H, k0 = (c / H) * 8;
-      const int i = k0 >> 5, gcol = (i & 3) * H + 32 * (2 * (int)crank + (i >> 2)) + (k0 & 31);
-      const float* src = U + (int64_t)n * G4 + gcol;
-      const float4 a = ldg4(src), b = ldg4(src + 4);
-      const uint32_t dst = smem_u32(sU) + (uint32_t)((k0 >> 6) * H * 128 + n * 128 +
-                                                     ((((k0 & 63) >> 3) ^ (n & 7)) << 4));
-      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(h2u(a.x, a.y)),
-                   "r"(h2u(a.z, a.w)), "r"(h2u(b.x, b.y)), "r"(h2u(b.z, b.w))
-                   : "memory");
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_arrive(u_ready);
+    // idle after the prologue
   } else if (warp == 1) {
     // dh partial = (S da)[128, own 256] x U_own^T -> TMEM (kind::f16, fp32 accumulate)
     const uint32_t idesc16 = idesc_f16(H);
     const uint32_t a_base = smem_u32(sA), u_base = smem_u32(sU);
-    mbar_wait(u_ready, 0);
-    fence_after();
     for (int t = 0; t < L; ++t) {
       const int p = L - 1 - t;
       const int a = p & 1;
@@ -1542,6 +1543,392 @@ int launch_lstm_bwd_tc2k(const float* U, const int32_t* slot_row, const uint8_t*
                                         bias_partial, rq, da_scale, dgx16, s);
 }
 
+// BPTT on the 2-SM tensor core (cta_group::2). Each CTA of the pair owns
+// 4 x rq rows (rq per TMEM lane quadrant) and ALL H units of them, so the
+// position's dh = (S da) U^T needs no exchange of partials: A is the CTA's own
+// [128 rows x 4H gates] fp16 da tile (8 k-blocks of 64 gate columns), B = U's
+// rows split along N (CTA c holds units 64c .. 64c + 63, all 4H gate columns,
+// resident for the launch), and the even CTA issues one M = 256 MMA per k-block
+// once both CTAs' epilogue warps have written it; the commits are multicast to
+// both CTAs' barriers and each CTA reads its own rows x 128 units from its TMEM.
+// Epilogue lane = 4 rows x 8 unit quads (one row, 4 units per 32-unit chunk,
+// 4 chunks per position); the TMEM rows pass through a per-warp staging tile to
+// reach that mapping. Own gate column k (0..4H-1) of a position: 32-column
+// block i = k >> 5 = 4 lc + g (chunk lc, gate g); fp16 k-block k >> 6.
+#define TS2M(t, k)                                                     \
+  do {                                                                 \
+    DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && (t) < 256, t, k);   \
+    DGC_TS2(blockIdx.x == 1 && threadIdx.x == 64 && (t) < 256, t, k);  \
+  } while (0)
+template <int kEW> __host__ __device__ constexpr int km_a_stages() { return 8; }
+constexpr int kKmStgStride = 128 + 4;  // staging row stride (floats, 16-B aligned)
+// rows per quadrant of the 2-SM kernel: R over all 148 SMs, at most 16
+inline int pair_rows_per_quadrant(int64_t R) {
+  const int64_t per = (R + 4 * dgc::kNumSMs - 1) / (4 * dgc::kNumSMs);
+  return (int)(per < 1 ? 1 : per > 16 ? 16 : per);
+}
+inline int64_t pair_cta_tiles(int64_t R) {
+  const int64_t rows = 4 * (int64_t)pair_rows_per_quadrant(R);
+  const int64_t t = (R + rows - 1) / rows;
+  return t + (t & 1);
+}
+template <int H, int kEW>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEW, 1)
+    lstm_bwd_tc2m_kernel(const float* __restrict__ U, const int32_t* __restrict__ slot_row,
+                         const uint8_t* __restrict__ slot_mask, int64_t R, int L,
+                         const float* __restrict__ save, const float* __restrict__ dh_out,
+                         float* __restrict__ dgx, int rnd, float* __restrict__ bias_partial,
+                         int rq, float da_scale, int dgx16) {
+  static_assert(H == 128, "2-SM BPTT is specialised for H = 128");
+  constexpr int EW = kEW;
+  constexpr int kEpiT = 32 * EW;
+  constexpr int RPW = 4;                     // rows per warp (one per lane row group)
+  constexpr int G4 = 4 * H;
+  constexpr int HN = H / 2;                  // B rows (units) held by each CTA
+  constexpr int KB = G4 / 64;                // fp16 k-blocks per position
+  constexpr int NC = H / 32;                 // 32-unit chunks per position
+  constexpr int kAStage = BM * 128;          // 128 rows x 64 fp16 gate columns
+  constexpr int kUBytes = KB * HN * 128;
+  constexpr int kS = kKmStgStride;
+  constexpr int kStgW = RPW * kS;
+  static_assert(kStgW >= 4 * NC * 32, "staging must hold the warp's bias partials");
+  constexpr int kAS = km_a_stages<kEW>();
+  constexpr uint32_t kTmemCols = 2 * H;      // two N = H accumulators
+  constexpr int kSF = tc_save_floats<H>();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = smem;
+  uint8_t* sU = sA + kAS * kAStage;
+  float* stg_all = reinterpret_cast<float*>(sU + kUBytes);
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(stg_all + EW * kStgW);  // used in CTA 0
+  uint64_t* a_empty = a_full + kAS;
+  uint64_t* acc_full = a_empty + kAS;    // [2]
+  uint64_t* acc_empty = acc_full + 2;    // [2], used in CTA 0
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_rank();
+  const int64_t tile = blockIdx.x;
+  const int64_t row0 = tile * 4 * rq;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kAS; ++s) {
+      mbar_init(&a_full[s], 2 * EW);  // one arrival per epilogue warp of both CTAs
+      mbar_init(&a_empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 2 * EW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  {
+    // this CTA's half of B: U rows 64 crank + n (n < 64) over all 4H gate
+    // columns in k order, fp16, K-major SWIZZLE_128B ([KB][HN rows][128 B]);
+    // every thread takes a share before the barriers below
+#pragma unroll 4
+    for (int c = threadIdx.x; c < HN * (G4 / 8); c += 64 + 32 * EW) {
+      const int n = c % HN, k0 = (c / HN) * 8;
+      const int i = k0 >> 5, gcol = (i & 3) * H + 32 * (i >> 2) + (k0 & 31);
+      const float* src = U + (int64_t)(HN * (int)crank + n) * G4 + gcol;
+      const float4 a = ldg4(src), b = ldg4(src + 4);
+      const uint32_t dst = smem_u32(sU) + (uint32_t)((k0 >> 6) * HN * 128 + n * 128 +
+                                                     ((((k0 & 63) >> 3) ^ (n & 7)) << 4));
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(h2u(a.x, a.y)),
+                   "r"(h2u(a.z, a.w)), "r"(h2u(b.x, b.y)), "r"(h2u(b.z, b.w))
+                   : "memory");
+    }
+    fence_async_smem();
+  }
+  if (warp == 1) tmem_alloc2(tmem_slot, kTmemCols);
+  fence_before();
+  __syncthreads();
+  cluster_sync_all();  // both CTAs' barriers initialised before any remote arrival
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  DGC_TS3(blockIdx.x == 0 && threadIdx.x == 0, 0, 30);
+
+  if (warp == 0) {
+    // idle after the prologue
+  } else if (warp == 1) {
+    if (crank == 0) {
+      const uint32_t idesc = idesc_f16_m256(H);
+      const uint32_t a_base = smem_u32(sA), u_base = smem_u32(sU);
+      DGC_TS3(blockIdx.x == 0 && lane == 0, 0, 31);
+      for (int t = 0; t < L; ++t) {
+        const int a = (L - 1 - t) & 1;
+        mbar_wait_cluster(&acc_empty[a], ((t >> 1) & 1) ^ 1);
+        fence_after();
+        for (int i = 0; i < KB; ++i) {
+          const int seq = t * KB + i;
+          const int sa = seq % kAS;
+          mbar_wait_cluster(&a_full[sa], (seq / kAS) & 1);
+          fence_after();
+          DGC_TS(i == KB - 1 && blockIdx.x == 0 && lane == 0 && t < 256, t, 7);
+          DGC_TS2(i == 0 && blockIdx.x == 0 && lane == 0 && t < 256, t, 7);
+          if (lane == 0) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma2_f16(tmem_base + a * H, kdesc(a_base + sa * kAStage + kk * 32),
+                       kdesc(u_base + i * HN * 128 + kk * 32), idesc, (i > 0 || kk > 0) ? 1u : 0u);
+            mma2_commit_mc(&a_empty[sa], 3);
+            if (i == KB - 1) mma2_commit_mc(&acc_full[a], 3);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else {
+    const int ew = warp - 2;
+    const int q = warp & 3;                   // TMEM lane quadrant (warp id % 4)
+    const int rb = (ew >> 2) * RPW;           // first quadrant row of this warp
+    const int r4 = lane >> 3, u8 = lane & 7;  // row rb + r4, units 32 lc + 4 u8 .. +3
+    const int rl = rb + r4;
+    const int r = q * 32 + rl;                // A-tile / TMEM row
+    const uint32_t stg_s = smem_u32(stg_all + ew * kStgW);
+    const uint32_t sA_s = smem_u32(sA);
+    const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
+    const uint32_t a_full_l = map_peer(a_full, 0), acc_empty_l = map_peer(acc_empty, 0);
+    const bool active = rb < rq;
+    const float inv_scale = 1.f / da_scale;
+    const int64_t vrow = row0 + q * rq + rl;
+    const int sbase = (rl < rq && vrow < R) ? (int)(vrow * L) : -1;
+    int inst = sbase >= 0 ? slot_row[sbase + L - 1] : -1;
+    int mk = sbase >= 0 ? slot_mask[sbase + L - 1] : 0;
+    float mnext = 0.f;
+    float4 bsum[NC][4], dcr[NC];
+#pragma unroll
+    for (int lc = 0; lc < NC; ++lc) {
+#pragma unroll
+      for (int g = 0; g < 4; ++g) bsum[lc][g] = zero4();
+      dcr[lc] = zero4();
+    }
+    auto load_fields = [&](int lc, float4& dho, uint2& cv, uint4& g0, uint4& g1) {
+      const int j = 32 * lc + 4 * u8;
+      if (inst >= 0) {
+        dho = ldg4(dh_out + (int64_t)inst * H + j);
+        const __half* sv = reinterpret_cast<const __half*>(save + (int64_t)inst * kSF) + H;
+        cv = __ldg(reinterpret_cast<const uint2*>(sv + j));
+        g0 = __ldg(reinterpret_cast<const uint4*>(sv + H + 4 * j));
+        g1 = __ldg(reinterpret_cast<const uint4*>(sv + H + 4 * j + 8));
+      } else {
+        dho = zero4();
+        cv = make_uint2(0u, 0u);
+        g0 = g1 = make_uint4(0u, 0u, 0u, 0u);
+      }
+    };
+    for (int t = 0; t < L; ++t) {
+      const int p = L - 1 - t;
+      const bool has_next = p + 1 < L;
+      TS2M(t, 0);
+      float4 dho[NC];
+      uint2 cvv[NC];
+      uint4 gv0[NC], gv1[NC];
+      // chunks 0-1 now, the rest of the row's lines into L2
+#pragma unroll
+      for (int lc = 0; lc < 2; ++lc) load_fields(lc, dho[lc], cvv[lc], gv0[lc], gv1[lc]);
+      if (inst >= 0) {
+        const __half* sv = reinterpret_cast<const __half*>(save + (int64_t)inst * kSF) + H;
+#pragma unroll
+        for (int lc = 2; lc < NC; ++lc) {
+          const int j = 32 * lc + 4 * u8;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(sv + H + 4 * j));
+        }
+        if (u8 == 0) {
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(sv + 64));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(dh_out + (int64_t)inst * H + 64));
+        }
+      }
+      const bool nok = sbase >= 0 && p > 0;
+      const int n_inst = nok ? slot_row[sbase + p - 1] : -1;
+      const int n_mk = nok ? slot_mask[sbase + p - 1] : 0;
+      if (has_next) {
+        mbar_wait(&acc_full[(p + 1) & 1], ((t - 1) >> 1) & 1);
+        fence_after();
+        TS2M(t, 1);
+        if (active) {
+          const uint32_t ta = tl + ((p + 1) & 1) * H;
+          const bool mine = lane >= rb && lane < rb + RPW;
+#pragma unroll
+          for (int h4 = 0; h4 < H / 16; ++h4) {
+            float v[16];
+            tmem_ld16(ta + 16 * h4, v);
+            if (mine) {
+              const uint32_t d = stg_s + (uint32_t)(((lane - rb) * kS + 16 * h4) * 4);
+#pragma unroll
+              for (int u = 0; u < 16; u += 4)
+                sts4(d + u * 4, make_float4(v[u], v[u + 1], v[u + 2], v[u + 3]));
+            }
+          }
+        }
+        fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (crank) mbar_arrive_remote(acc_empty_l + (uint32_t)(((p + 1) & 1) * 8));
+          else mbar_arrive(&acc_empty[(p + 1) & 1]);
+        }
+        TS2M(t, 3);
+      }
+#pragma unroll
+      for (int lc = 0; lc < NC; ++lc) {
+        const int seq0 = t * KB + lc * 2;   // this chunk's 2 fp16 k-blocks (gates 0-1, 2-3)
+        const int jo = 32 * lc + 4 * u8;
+        if (lc >= 2) load_fields(lc, dho[lc], cvv[lc], gv0[lc], gv1[lc]);
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          const int seq = seq0 + g;
+          mbar_wait(&a_empty[seq % kAS], ((seq / kAS) & 1) ^ 1);
+        }
+        float4 dh = zero4();
+        if (has_next) {
+          const float4 a = lds4(stg_s + (uint32_t)((r4 * kS + jo) * 4));
+          const float mn = mnext * inv_scale;  // the accumulator is S-scaled (exact)
+          dh = make_float4(mn * a.x, mn * a.y, mn * a.z, mn * a.w);
+        }
+        float4 da[4] = {zero4(), zero4(), zero4(), zero4()};
+        float4 dcp = zero4();
+        if (inst >= 0) {
+          const float4 ho = dho[lc];
+          dh = make_float4(dh.x + ho.x, dh.y + ho.y, dh.z + ho.z, dh.w + ho.w);
+          const float2 c01 = u2h(cvv[lc].x), c23 = u2h(cvv[lc].y);
+          const float cin[4] = {c01.x, c01.y, c23.x, c23.y};
+          const uint32_t gw[8] = {gv0[lc].x, gv0[lc].y, gv0[lc].z, gv0[lc].w,
+                                  gv1[lc].x, gv1[lc].y, gv1[lc].z, gv1[lc].w};
+          const float dhk[4] = {dh.x, dh.y, dh.z, dh.w};
+          const float dck[4] = {dcr[lc].x, dcr[lc].y, dcr[lc].z, dcr[lc].w};
+          const float mp = (float)mk;
+          float dak[4][4], dcpk[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float2 if_ = u2h(gw[2 * k]), go = u2h(gw[2 * k + 1]);
+            const float ig = if_.x, fg = if_.y, gg = go.x, og = go.y;
+            const float tc = tanh_fast(fg * cin[k] + ig * gg);  // the forward's tanh(c)
+            const float g_ = dhk[k];
+            const float d_o = g_ * tc;
+            const float dcn = dck[k] + g_ * og * (1.f - tc * tc);
+            dak[0][k] = dcn * gg * ig * (1.f - ig);
+            dak[1][k] = dcn * cin[k] * fg * (1.f - fg);
+            dak[2][k] = dcn * ig * (1.f - gg * gg);
+            dak[3][k] = d_o * og * (1.f - og);
+            dcpk[k] = dcn * fg * mp;
+          }
+          dcp = make_float4(dcpk[0], dcpk[1], dcpk[2], dcpk[3]);
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            float4 v = make_float4(dak[g][0], dak[g][1], dak[g][2], dak[g][3]);
+            if (!dgx16 && rnd) v = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
+            da[g] = v;
+          }
+        }
+        dcr[lc] = dcp;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int k16 = (g & 1) * 32 + 4 * u8;
+          const uint32_t addr = sA_s + (uint32_t)(((seq0 + (g >> 1)) % kAS) * kAStage) +
+                                (uint32_t)(r * 128 + ((((k16 >> 3) ^ (r & 7))) << 4) + (k16 & 7) * 2);
+          asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr),
+                       "r"(h2u(da[g].x * da_scale, da[g].y * da_scale)),
+                       "r"(h2u(da[g].z * da_scale, da[g].w * da_scale))
+                       : "memory");
+        }
+        fence_async_smem();
+        __syncwarp();
+        // the even CTA's MMA reads both CTAs' k-blocks: the odd CTA arrives on
+        // the even CTA's barrier (CTA-scope release after the proxy fence)
+        if (lane == 0) {
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            if (crank) mbar_arrive_remote(a_full_l + (uint32_t)(((seq0 + g) % kAS) * 8));
+            else mbar_arrive(&a_full[(seq0 + g) % kAS]);
+          }
+        }
+        if (inst >= 0) {
+          const int64_t oi = (int64_t)inst * G4 + jo;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const float4 v = da[g];
+            if (dgx16)
+              sth4(reinterpret_cast<__half*>(dgx) + oi + g * H,
+                   make_float4(v.x * da_scale, v.y * da_scale, v.z * da_scale, v.w * da_scale));
+            else
+              st4(dgx + oi + g * H, v);
+            bsum[lc][g] = make_float4(bsum[lc][g].x + v.x, bsum[lc][g].y + v.y,
+                                      bsum[lc][g].z + v.z, bsum[lc][g].w + v.w);
+          }
+        }
+        TS2M(t, lc == NC - 1 ? 2 : 4 + lc);
+        DGC_TS3(lc == NC - 1 && blockIdx.x < 2 && lane == 0 && t < 256, t, ew + 16 * (int)blockIdx.x);
+              }
+      mnext = (float)mk;
+      inst = n_inst;
+      mk = n_mk;
+    }
+    if (bias_partial) {
+#pragma unroll
+      for (int lc = 0; lc < NC; ++lc)
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          float4 v = bsum[lc][g];
+#pragma unroll
+          for (int m = 8; m <= 16; m <<= 1) {
+            v.x += __shfl_xor_sync(0xffffffffu, v.x, m);
+            v.y += __shfl_xor_sync(0xffffffffu, v.y, m);
+            v.z += __shfl_xor_sync(0xffffffffu, v.z, m);
+            v.w += __shfl_xor_sync(0xffffffffu, v.w, m);
+          }
+          if (r4 == 0) sts4(stg_s + (uint32_t)(((lc * 4 + g) * 32 + 4 * u8) * 4), v);
+        }
+      asm volatile("bar.sync 1, %0;" ::"r"(kEpiT));
+      if (ew == 0) {
+        for (int lc = 0; lc < NC; ++lc)
+          for (int g = 0; g < 4; ++g) {
+            float acc = 0.f;
+            for (int w = 0; w < EW; ++w) acc += stg_all[w * kStgW + (lc * 4 + g) * 32 + lane];
+            bias_partial[tile * G4 + g * H + 32 * lc + lane] = acc;
+          }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  DGC_TS3(blockIdx.x == 0 && threadIdx.x == 0, 1, 30);
+  cluster_sync_all();  // the pair's MMAs and remote arrivals are done before TMEM is freed
+  if (warp == 1) tmem_dealloc2(tmem_base, kTmemCols);
+}
+
+template <int H, int EW>
+int launch_lstm_bwd_tc2m_ew(const float* U, const int32_t* slot_row, const uint8_t* slot_mask,
+                            int64_t R, int L, const float* save, const float* dh_out, float* dgx,
+                            int rnd, float* bias_partial, int rq, float da_scale, int dgx16,
+                            cudaStream_t s) {
+  const size_t smem = (size_t)km_a_stages<EW>() * BM * 128 + (size_t)(4 * H / 64) * (H / 2) * 128 +
+                      (size_t)EW * 4 * kKmStgStride * 4 + 1024 + 512;
+  auto kern = lstm_bwd_tc2m_kernel<H, EW>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_bwd_tc2m: set smem");
+  const int grid = (int)pair_cta_tiles(R);
+  kern<<<grid, 64 + 32 * EW, smem, s>>>(U, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
+                                        bias_partial, rq, da_scale, dgx16);
+  DGC_CHECK_LAUNCH("lstm_bwd_tc2m_kernel");
+  return DGC_OK;
+}
+
+template <int H>
+int launch_lstm_bwd_tc2m(const float* U, const int32_t* slot_row, const uint8_t* slot_mask,
+                         int64_t R, int L, const float* save, const float* dh_out, float* dgx,
+                         int rnd, float* bias_partial, float da_scale, int dgx16, cudaStream_t s) {
+  DGC_REQUIRE(R * (int64_t)L < (int64_t)INT32_MAX, "lstm_bwd_tc2m: R * L must fit int32");
+  const int rq = pair_rows_per_quadrant(R);
+  DGC_REQUIRE(rq <= 12, "lstm_bwd_tc2m: at most 12 rows per quadrant");
+  return launch_lstm_bwd_tc2m_ew<H, 12>(U, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
+                                        bias_partial, rq, da_scale, dgx16, s);
+}
+// The 2-SM BPTT is opt-in (DGC_BPTT_2SM; up to 48 rows per SM in one wave,
+// R <= 7104): at C2 its positions take 7.7 us against the K-split kernel's 7.2
+// (the exchange it removes is cheaper than the four-chunk epilogue it costs).
+static bool bptt_2sm(int64_t R) {
+  return getenv("DGC_BPTT_2SM") != nullptr && (R + 4 * dgc::kNumSMs - 1) / (4 * dgc::kNumSMs) <= 12;
+}
+
 template <int H>
 int launch_lstm_bwd_tc(const float* U, const int32_t* slot_row, const uint8_t* slot_mask,
                        int64_t R, int L, const float* save, const float* dh_out, float* dgx,
@@ -1635,7 +2022,7 @@ extern "C" int dgc_debug_lstm_timestamps(unsigned long long* out, int n) {
 }
 
 extern "C" int dgc_debug_lstm_timestamps_warps(unsigned long long* out, int n) {
-  if (n > 256 * 16) n = 256 * 16;
+  if (n > 256 * 32) n = 256 * 32;
   cudaError_t e = cudaMemcpyFromSymbol(out, g_lstm_ts3, n * sizeof(unsigned long long));
   return e == cudaSuccess ? DGC_OK : dgc::cuda_fail(e, "debug timestamps");
 }
@@ -1653,9 +2040,12 @@ extern "C" int dgc_rnn_bwd_tc(int32_t cell_flags, const float* U, const int32_t*
     case 64: return launch_lstm_bwd_tc<64>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
     case 128:
       return cluster_rnn_enabled()
-                 ? launch_lstm_bwd_tc2k<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, rnd, bias_partial,
-                                             ldexpf(1.f, (cell_flags >> 16) & 0x7f),
-                                             (cell_flags >> 24) & 1, s)
+                 ? (bptt_2sm(n_rows) ? launch_lstm_bwd_tc2m<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, rnd,
+                                                           bias_partial, ldexpf(1.f, (cell_flags >> 16) & 0x7f),
+                                                           (cell_flags >> 24) & 1, s)
+                               : launch_lstm_bwd_tc2k<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, rnd,
+                                                           bias_partial, ldexpf(1.f, (cell_flags >> 16) & 0x7f),
+                                                           (cell_flags >> 24) & 1, s))
                  : launch_lstm_bwd_tc<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
     default: return dgc::fail(DGC_ERR_ARG, "rnn_bwd_tc: H must be 32, 64 or 128");
   }
@@ -1666,5 +2056,6 @@ extern "C" int32_t dgc_rnn_tc_save_floats(int32_t H) {
 }
 
 extern "C" int64_t dgc_rnn_tc_tiles(int64_t n_rows, int32_t H) {
-  return (H == 128 && cluster_rnn_enabled()) ? cluster_tiles(n_rows) : (n_rows + 127) / 128;
+  if (H == 128 && cluster_rnn_enabled()) return bptt_2sm(n_rows) ? pair_cta_tiles(n_rows) : cluster_tiles(n_rows);
+  return (n_rows + 127) / 128;
 }

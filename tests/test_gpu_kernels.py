@@ -676,16 +676,22 @@ def test_lstm_fwd_fused_projection_matches_two_step(n_seq, carry_frac):
     close(tc_save_decode(outs[1][1], H), tc_save_decode(outs[0][1], H), 2e-3, "fused save")
 
 
-@pytest.mark.parametrize("H,ew16", [(32, False), (64, False), (128, False), (128, True)])
-def test_lstm_bwd_tensor_core_matches_simt(H, ew16, monkeypatch):
-    """K4 BPTT on tcgen05 (TF32) vs the fp32 SIMT BPTT on the same packed runs:
-    dgx and the fused bias partial sums (ew16: the 16-warp cluster variant)."""
-    if ew16:
+@pytest.mark.parametrize("H,variant,n_seq", [(32, "", 700), (64, "", 700), (128, "", 700),
+                                             (128, "", 6900), (128, "ew16", 700),
+                                             (128, "2sm", 700), (128, "2sm", 6900)])
+def test_lstm_bwd_tensor_core_matches_simt(H, variant, n_seq, monkeypatch):
+    """K4 BPTT on tcgen05 vs the fp32 SIMT BPTT on the same packed runs: dgx and
+    the fused bias partial sums. H = 128: the K-split cluster kernel with 12 / 16
+    (ew16) epilogue warps, or the opt-in 2-SM (cta_group::2) kernel (6900 runs:
+    12 rows per lane quadrant, every epilogue warp busy)."""
+    if variant == "2sm":
+        monkeypatch.setenv("DGC_BPTT_2SM", "1")
+    if variant == "ew16":
         monkeypatch.setenv("DGC_RNN_EW16", "1")
     from paper_2309_03523_b200 import ops
     from paper_2309_03523_b200.layout import pack_sequences_native
     rng = np.random.default_rng(H + 1)
-    lengths = rng.integers(1, 20, size=700)
+    lengths = rng.integers(1, 20, size=n_seq)
     seq, pos, mask, _ = pack_sequences_native(lengths)
     R, L = seq.shape
     offs = np.concatenate([[0], np.cumsum(lengths)])

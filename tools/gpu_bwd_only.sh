@@ -8,5 +8,5 @@ for k, v in sorted(d["kernels"].items(), key=lambda kv: -kv[1]["ms_per_step"])[:
     print(f"  {k:55s} {v['ms_per_step']*1e3:8.1f} us")
 PY
 make clean > /dev/null && make -j8 DGC_TS=1 > /dev/null 2>&1
-timeout 200 python tools/time_lstm_c2.py 2>&1 | tail -1
+timeout 200 python tools/time_lstm_2sm.py 2>&1 | tail -4
 make clean > /dev/null
