@@ -336,6 +336,14 @@ __device__ __forceinline__ float4 zero4() { return make_float4(0.f, 0.f, 0.f, 0.
 // accumulators (2 x 256 columns), so the x part of position p+1 runs while the
 // epilogue drains position p. The gx GEMM and every per-position global load of
 // the epilogue disappear; the bias is added from L1.
+// FX accumulator column order: inside each 16-unit chunk, TMEM column k holds
+// unit 4 (k/2 % 4) + 2 (k >= 8) + (k & 1), so the 16x256b TMEM load hands lane
+// (row r, unit quad uq) exactly units 4 uq .. 4 uq + 3 of its row (columns
+// 2 uq, 2 uq + 1, 8 + 2 uq, 9 + 2 uq): the epilogue reads its gates straight
+// from TMEM, with no shared-memory staging. Applied to both B operands (U^T, Wx^T).
+__host__ __device__ constexpr int fx_unit(int col) {
+  return (col & ~15) + 4 * ((col & 7) >> 1) + ((col & 8) ? 2 : 0) + (col & 1);
+}
 template <int H, int kVEW, bool FX>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
     lstm_fwd_tc2v_kernel(const __grid_constant__ CUtensorMap tmUt,
@@ -436,6 +444,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   cluster_sync_all();
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  DGC_TS3(blockIdx.x == 0 && threadIdx.x == 64, 2, 30);
 
   if (warp == 0) {
     if (!FX) {
@@ -618,11 +627,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       // straight from U and Wx [H, 4H] (the transpose happens here: consecutive
       // threads take consecutive gate columns, so the fp32 reads coalesce);
       // resident for the whole launch, ordered before the first MMA by the
-      // prologue's a_full arrival
+      // prologue's a_full arrival (unrolled: the L2 round trips of 4 items overlap)
+#pragma unroll 4
       for (int c = threadIdx.x - 64; c < 2 * NP * (H / 8); c += kEpiT) {
         const int mat = c / (NP * (H / 8)), cc = c % (NP * (H / 8));
         const int n = cc % NP, k0 = (cc / NP) * 8;
-        const float* src = (mat ? Wxw : Uw) + (int64_t)k0 * G4 + (n / HU) * H + u0 + (n % HU);
+        const float* src = (mat ? Wxw : Uw) + (int64_t)k0 * G4 + (n / HU) * H + u0 + fx_unit(n % HU);
         float v[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = __ldg(src + (int64_t)i * G4);
@@ -665,6 +675,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       }
     }
     publish_all();
+    DGC_TS3(blockIdx.x == 0 && threadIdx.x == 64, 2, 31);
     int n_inst = ok ? slot_row[grow * L] : -1, n_mk = 0, n_ci = ok ? slot_carry[grow * L] : -1;
     for (int p = 0; p < L; ++p) {
       const bool has_next = p + 1 < L;
@@ -719,7 +730,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           }
           __syncwarp();
         };
-        if (kStgGates == 4) {
+        if (FX) {
+          // lanes q*32 + (rb & 16) .. +15 of the quadrant; this warp's 8 rows are
+          // the lane-L or lane-L+8 half
+          float a[16];
+          const uint32_t t16 = ta + ((uint32_t)(rb & 16) << 16);
+          tmem_ld16x256x4(t16, t16 + HU, t16 + 2 * HU, t16 + 3 * HU, (rb & 8) != 0, a);
+#pragma unroll
+          for (int gi = 0; gi < 4; ++gi)
+            pre[gi] = make_float4(a[4 * gi], a[4 * gi + 1], a[4 * gi + 2], a[4 * gi + 3]);
+        } else if (kStgGates == 4) {
           float a[64];
           tmem_ld16x4(ta, ta + HU, ta + 2 * HU, ta + 3 * HU, a);
           DGC_TS2(ch == 0 && blockIdx.x == 0 && threadIdx.x == 64 && p < 256, p, 1);
@@ -813,9 +833,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       if (has_next) publish(kHalves - 1);
     }
   }
+  DGC_TS3(blockIdx.x == 0 && threadIdx.x == 64, 3, 30);
   fence_before();
   __syncthreads();
   cluster_sync_all();
+  DGC_TS3(blockIdx.x == 0 && threadIdx.x == 64, 3, 31);
   if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
 }
 

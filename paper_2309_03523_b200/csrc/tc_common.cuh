@@ -226,6 +226,33 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
+// Four tcgen05.ld.16x256b.x2 (16 TMEM lanes from `t*`'s lane, 16 columns each)
+// with one wait. Thread t receives, per load, lanes L = t/4 and L + 8 at
+// columns 2(t%4), 2(t%4)+1 and 8 + the same: registers {0,1} / {4,5} lane L,
+// {2,3} / {6,7} lane L + 8 (tools/probes/tmem_shapes.cu). `hi` selects the
+// lane-L+8 half: v[4 i + 0..3] = lane L (+8) columns 2(t%4), +1, +8, +9.
+__device__ __forceinline__ void tmem_ld16x256x4(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3,
+                                                bool hi, float* v) {
+  uint32_t r[32];
+#define DGC_LD256(T, o)                                                                        \
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"       \
+               : "=r"(r[o]), "=r"(r[o + 1]), "=r"(r[o + 2]), "=r"(r[o + 3]), "=r"(r[o + 4]),   \
+                 "=r"(r[o + 5]), "=r"(r[o + 6]), "=r"(r[o + 7])                                \
+               : "r"(T));
+  DGC_LD256(t0, 0) DGC_LD256(t1, 8) DGC_LD256(t2, 16) DGC_LD256(t3, 24)
+#undef DGC_LD256
+#define DGC_R8(o) "+r"(r[o]), "+r"(r[o + 1]), "+r"(r[o + 2]), "+r"(r[o + 3]), "+r"(r[o + 4]), \
+                  "+r"(r[o + 5]), "+r"(r[o + 6]), "+r"(r[o + 7])
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : DGC_R8(0), DGC_R8(8), DGC_R8(16), DGC_R8(24) : : "memory");
+#undef DGC_R8
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {  // selects, not a runtime register index (no local memory)
+    v[4 * i + 0] = __uint_as_float(hi ? r[8 * i + 2] : r[8 * i + 0]);
+    v[4 * i + 1] = __uint_as_float(hi ? r[8 * i + 3] : r[8 * i + 1]);
+    v[4 * i + 2] = __uint_as_float(hi ? r[8 * i + 6] : r[8 * i + 4]);
+    v[4 * i + 3] = __uint_as_float(hi ? r[8 * i + 7] : r[8 * i + 5]);
+  }
+}
 // --- clusters / DSMEM ---
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;

@@ -43,3 +43,10 @@ t2 = np.array(buf[256 * 8:256 * 8 + L * 8], dtype=np.float64).reshape(L, 8)
 d = np.diff(t2[1:, :6], axis=1) / 1e3
 print("chunk 0 (us): tmem ld", d[:, 0].mean(), "stage+lds", d[:, 1].mean(), "math", d[:, 2].mean(),
       "stores", d[:, 3].mean(), "put_h", d[:, 4].mean())
+wb = (ctypes.c_ulonglong * (256 * 32))()
+_native.lib().dgc_debug_lstm_timestamps_warps(wb, 256 * 32)
+w = np.array(wb, dtype=np.float64).reshape(256, 32)
+k0 = w[2, 30]
+print(f"kernel (CTA0, us after setup): prologue done {(w[2,31]-k0)/1e3:.2f}, first h-ready {(ts[0,0]-k0)/1e3:.2f}, "
+      f"first acc {(ts[0,1]-k0)/1e3:.2f}, last epilogue done {(ts[L-1,2]-k0)/1e3:.2f}, "
+      f"before exit sync {(w[3,30]-k0)/1e3:.2f}, after {(w[3,31]-k0)/1e3:.2f}")
