@@ -1160,7 +1160,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 // drain the first chunk's stages.
 template <int kVEW> __host__ __device__ constexpr int ks_a_stages() { return kVEW <= 12 ? 5 : 3; }
 template <int kVEW> __host__ __device__ constexpr int ks_recv_rq() { return kVEW <= 12 ? 24 : 32; }
-constexpr int kKsStgStride = 64 + 4;  // own-half staging row stride (floats, 16-B aligned)
+constexpr int kKsStgStride = 64 + 16;  // own-half staging row stride (floats): conflict-free
+                                        // for the (row, unit quad) writes and the (r4, u8) reads
 template <int H, int kVEW>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
     lstm_bwd_tc2k_kernel(const float* __restrict__ U, const int32_t* __restrict__ slot_row,
@@ -1229,7 +1230,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
     for (int c = threadIdx.x; c < H * (4 * HU / 8); c += 64 + 32 * EW) {
       const int n = c % H, k0 = (c / H) * 8;
       const int i = k0 >> 5, gcol = (i & 3) * H + 32 * (2 * (int)crank + (i >> 2)) + (k0 & 31);
-      const float* src = U + (int64_t)n * G4 + gcol;
+      const float* src = U + (int64_t)fx_unit(n) * G4 + gcol;  // N order: see fx_unit
       const float4 a = ldg4(src), b = ldg4(src + 4);
       const uint32_t dst = smem_u32(sU) + (uint32_t)((k0 >> 6) * H * 128 + n * 128 +
                                                      ((((k0 & 63) >> 3) ^ (n & 7)) << 4));
@@ -1361,34 +1362,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
         fence_after();
         DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 1);
         if (active) {
-          // partial dh of this warp's 8 rows (thread = row = TMEM lane): own
-          // units -> staging, the peer's units -> the peer's receive tile
-          const uint32_t ta = tl + ((p + 1) & 1) * H;
-          const bool mine = lane >= rb && lane < rb + RPW;
+          // partial dh of this warp's 8 rows: 16x256b TMEM loads of lanes
+          // q*32 + (rb & 16) .. +15 hand lane (r8, uq) units 16 i + 4 uq .. +3 of
+          // row rb + r8 (U's rows are in fx_unit order): own units -> staging,
+          // the peer's units -> the peer's receive tile, all lanes storing
+          const uint32_t ta = tl + ((p + 1) & 1) * H + ((uint32_t)(rb & 16) << 16);
+          const bool hi = (rb & 8) != 0;
+          const int r8 = lane >> 2, uq = lane & 3;
+          float v[16];
+          tmem_ld16x256x4(ta + u0, ta + u0 + 16, ta + u0 + 32, ta + u0 + 48, hi, v);
 #pragma unroll
-          for (int h4 = 0; h4 < 4; ++h4) {
-            float v[16];
-            tmem_ld16(ta + u0 + 16 * h4, v);
-            if (mine) {
-              const uint32_t d = stg_s + (uint32_t)(((lane - rb) * kS + 16 * h4) * 4);
+          for (int i = 0; i < 4; ++i)
+            sts4(stg_s + (uint32_t)((r8 * kS + 16 * i + 4 * uq) * 4),
+                 make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
+          tmem_ld16x256x4(ta + pu0, ta + pu0 + 16, ta + pu0 + 32, ta + pu0 + 48, hi, v);
+          const uint32_t dst = recv_peer + (uint32_t)(((t & 1) * kRecv + (q * kRQ + rb + r8) * HU + 4 * uq) * 4);
 #pragma unroll
-              for (int u = 0; u < 16; u += 4)
-                sts4(d + u * 4, make_float4(v[u], v[u + 1], v[u + 2], v[u + 3]));
-            }
-          }
-#pragma unroll
-          for (int h4 = 0; h4 < 4; ++h4) {
-            float v[16];
-            tmem_ld16(ta + pu0 + 16 * h4, v);
-            if (mine) {
-              const uint32_t dst =
-                  recv_peer + (uint32_t)(((t & 1) * kRecv + (q * kRQ + lane) * HU + 16 * h4) * 4);
-#pragma unroll
-              for (int u = 0; u < 16; u += 4)
-                st_async_v4(dst + u * 4, make_float4(v[u], v[u + 1], v[u + 2], v[u + 3]),
-                            rfull_peer + (uint32_t)((t & 1) * 8));
-            }
-          }
+          for (int i = 0; i < 4; ++i)
+            st_async_v4(dst + 64 * i, make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]),
+                        rfull_peer + (uint32_t)((t & 1) * 8));
         }
         fence_before();
         __syncwarp();
