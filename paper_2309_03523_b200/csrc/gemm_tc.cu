@@ -591,7 +591,10 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   const int budget = 232448 - 1024 - 256 - 1024 - stg_bytes;
   // B panel resident in shared memory when one CTA keeps one n-tile and it fits
   const int bres_bytes = kb_total * bn * BK * 4;
-  const int b_res = (!SPLIT3 && splits == 1 && bres_bytes <= 96 * 1024 && !so.seg_of_mtile &&
+  int bres_max = 96 * 1024;
+  if (const char* env = getenv("DGC_GEMM_BRES_KB")) bres_max = atoi(env) * 1024;
+  const int b_res = (!SPLIT3 && splits == 1 && bres_bytes <= bres_max && bres_bytes + 2 * kABytes <= budget &&
+                     !so.seg_of_mtile &&
                      !so.kitems && !getenv("DGC_GEMM_NO_BRES")) ? 1 : 0;
   int stages = b_res ? (budget - bres_bytes) / kABytes : budget / stage_bytes;
   int max_stages = 4;

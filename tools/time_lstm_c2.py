@@ -31,7 +31,7 @@ print(f"mean per position (us): wait-acc {ph(0,1):.2f} tmem+send {ph(1,3):.2f} r
       f"position {np.mean(np.diff(ts[:, 0])) / 1e3:.2f}")
 wb = (ctypes.c_ulonglong * (256 * 32))()
 _native.lib().dgc_debug_lstm_timestamps_warps(wb, 256 * 32)
-w = np.array(wb[:L * 16], dtype=np.float64).reshape(L, 32)[:, :12]
+w = np.array(wb[:L * 32], dtype=np.float64).reshape(L, 32)[:, :12]
 rel = (w[1:] - ts[1:, 0:1]) / 1e3  # per epilogue warp: chunk-1 done, us after the position start
 print("per-warp chunk-1 done (us after position start, mean over positions):", np.round(rel.mean(0), 2))
 print("slowest warp minus warp 0, mean:", round(float((rel.max(1) - rel[:, 0]).mean()), 2))
