@@ -437,6 +437,13 @@ int dgc_softmax_xent(const float* logits, const int32_t* labels, int64_t n, int3
                      float scale, int32_t flags, float* dlogits, double* loss_partial,
                      float* dl_partial, void* stream);
 /* dl_partial (may be NULL): per-block column sums of dlogits [ceil(n/256), C]. */
+/* As dgc_softmax_xent (no TF32 rounding) with an fp16 copy dlogits16 =
+ * fp16(scale16 * dlogits) [n, C] (the fp16 readout GEMMs' operand; scale16 a
+ * power of two lifting ~1/n gradients into fp16's normal range); dlogits
+ * (fp32) may be NULL. C in {8, 16, 24, 32}. */
+int dgc_softmax_xent_f16(const float* logits, const int32_t* labels, int64_t n, int32_t C,
+                         float scale, float* dlogits, double* loss_partial, float* dl_partial,
+                         void* dlogits16, float scale16, void* stream);
 /* out[j] (+)= sum_r partial[r, j] in fixed row order (deterministic). */
 int dgc_reduce_rows(const float* partial, int64_t rows, int32_t width, float* out,
                     int32_t accumulate, void* stream);

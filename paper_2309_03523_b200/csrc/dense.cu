@@ -128,7 +128,7 @@ template <int CM>
 __global__ void __launch_bounds__(256) softmax_xent_small_kernel(
     const float* __restrict__ logits, const int32_t* __restrict__ labels, int64_t n, int C,
     float scale, int round_out, float* __restrict__ dlogits, double* __restrict__ loss_partial,
-    float* __restrict__ dl_partial) {
+    float* __restrict__ dl_partial, __half* __restrict__ dl16, float scale16) {
   __shared__ double lred[8];
   __shared__ float cred[8][CM];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -170,15 +170,33 @@ __global__ void __launch_bounds__(256) softmax_xent_small_kernel(
       p *= scale;
       x[c] = round_out ? dgc::rna_tf32_f(p) : p;
     }
-    float* drow = dlogits + i * C;
+    if (dlogits) {
+      float* drow = dlogits + i * C;
 #pragma unroll
-    for (int c = 0; c < CM; c += 4) {
-      if (c < C) {
-        if (vec) {
-          *reinterpret_cast<float4*>(drow + c) = make_float4(x[c], x[c + 1], x[c + 2], x[c + 3]);
-        } else {
+      for (int c = 0; c < CM; c += 4) {
+        if (c < C) {
+          if (vec) {
+            *reinterpret_cast<float4*>(drow + c) = make_float4(x[c], x[c + 1], x[c + 2], x[c + 3]);
+          } else {
 #pragma unroll
-          for (int e = 0; e < 4; ++e) if (c + e < C) drow[c + e] = x[c + e];
+            for (int e = 0; e < 4; ++e) if (c + e < C) drow[c + e] = x[c + e];
+          }
+        }
+      }
+    }
+    if (dl16) {  // fp16(scale16 * dlogits): the fp16 readout GEMMs' operand (C % 8 == 0)
+      __half* hrow = dl16 + i * C;
+#pragma unroll
+      for (int c = 0; c < CM; c += 8) {
+        if (c < C) {
+          uint4 v;
+          __half2 h0 = __floats2half2_rn(x[c] * scale16, x[c + 1] * scale16);
+          __half2 h1 = __floats2half2_rn(x[c + 2] * scale16, x[c + 3] * scale16);
+          __half2 h2 = __floats2half2_rn(x[c + 4] * scale16, x[c + 5] * scale16);
+          __half2 h3 = __floats2half2_rn(x[c + 6] * scale16, x[c + 7] * scale16);
+          v.x = *reinterpret_cast<uint32_t*>(&h0); v.y = *reinterpret_cast<uint32_t*>(&h1);
+          v.z = *reinterpret_cast<uint32_t*>(&h2); v.w = *reinterpret_cast<uint32_t*>(&h3);
+          *reinterpret_cast<uint4*>(hrow + c) = v;
         }
       }
     }
@@ -288,12 +306,30 @@ extern "C" int dgc_softmax_xent(const float* logits, const int32_t* labels, int6
                        (reinterpret_cast<uintptr_t>(dlogits) & 15) == 0;
   if (C <= 32 && (aligned || (C & 3) != 0)) {
     softmax_xent_small_kernel<32><<<blocks, 256, 0, dgc::as_stream(stream)>>>(
-        logits, labels, n, C, scale, flags & 1, dlogits, loss_partial, dl_partial);
+        logits, labels, n, C, scale, flags & 1, dlogits, loss_partial, dl_partial, nullptr, 1.f);
   } else {
     softmax_xent_kernel<<<blocks, 256, 0, dgc::as_stream(stream)>>>(logits, labels, n, C, scale,
                                                                    flags & 1, dlogits, loss_partial,
                                                                    dl_partial);
   }
+  DGC_CHECK_LAUNCH("softmax_xent_kernel");
+  return DGC_OK;
+}
+
+extern "C" int dgc_softmax_xent_f16(const float* logits, const int32_t* labels, int64_t n, int32_t C,
+                                    float scale, float* dlogits, double* loss_partial,
+                                    float* dl_partial, void* dlogits16, float scale16, void* stream) {
+  DGC_REQUIRE(C >= 1 && C <= 32 && C % 8 == 0, "softmax_xent_f16: C must be 8, 16, 24 or 32");
+  DGC_REQUIRE(dlogits16 != nullptr && (reinterpret_cast<uintptr_t>(dlogits16) & 15) == 0,
+              "softmax_xent_f16: dlogits16 must be 16-byte aligned");
+  DGC_REQUIRE((reinterpret_cast<uintptr_t>(logits) & 15) == 0 &&
+                  (reinterpret_cast<uintptr_t>(dlogits) & 15) == 0,
+              "softmax_xent_f16: logits / dlogits must be 16-byte aligned");
+  if (n == 0) return DGC_OK;
+  const int blocks = (int)((n + 255) / 256);
+  softmax_xent_small_kernel<32><<<blocks, 256, 0, dgc::as_stream(stream)>>>(
+      logits, labels, n, C, scale, 0, dlogits, loss_partial, dl_partial,
+      static_cast<__half*>(dlogits16), scale16);
   DGC_CHECK_LAUNCH("softmax_xent_kernel");
   return DGC_OK;
 }

@@ -510,9 +510,17 @@ def scatter_rows(src, rows, idx, n, width, dst, add=False):
 
 
 def softmax_xent(logits, labels, C, scale, dlogits, loss_partial, round_tf32=False,
-                 dl_partial=None):
-    """K8 dgc_softmax_xent."""
+                 dl_partial=None, dlogits16=None, scale16=1.0):
+    """K8 dgc_softmax_xent; with dlogits16 (fp16 [n, C]) dgc_softmax_xent_f16,
+    which also writes fp16(scale16 * dlogits) (dlogits may then be None)."""
     n = labels.numel()
+    if dlogits16 is not None:
+        _req16(dlogits16, "dlogits16")
+        _run("softmax_xent", lambda: _native.check(_native.lib().dgc_softmax_xent_f16(
+            _p(logits), _p(labels), n, C, float(scale), _p(dlogits), _p(loss_partial),
+            _p(dl_partial), _p(dlogits16), float(scale16), _stream()), "dgc_softmax_xent_f16"),
+            n * (6 * C + 4))
+        return
     _run("softmax_xent", lambda: _native.check(_native.lib().dgc_softmax_xent(
         _p(logits), _p(labels), n, C, float(scale), int(round_tf32), _p(dlogits),
         _p(loss_partial), _p(dl_partial), _stream()), "dgc_softmax_xent"), n * (8 * C + 4))

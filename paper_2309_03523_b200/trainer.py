@@ -281,6 +281,13 @@ class Shard:
         # fp16 and [dWx; dU] = [x16; h_in16]^T dgx16, dx = dgx16 Wx16^T run as
         # fp16-operand GEMMs with alpha = 1/S (half the bytes of the 4H-wide dgx)
         self.f16_bwd = bool(self.fused_xproj)
+        # fp16 readout (C % 8 == 0, C <= 32): the last LSTM layer also writes its h
+        # as fp16 (x16[n_rnn]); logits = h16 Wo16 + bo, and the softmax emits
+        # S-scaled fp16 dlogits for dWo = h16^T dlogits16 / S, dh = dlogits16 Wo16^T / S
+        self.f16_readout = bool(self.f16_bwd and cfg.C <= 32 and cfg.C % 8 == 0)
+        if self.f16_readout:
+            self.x16.append(torch.zeros((n, H), dtype=torch.float16, device=dev))
+            self.dlogits16 = torch.zeros((n, cfg.C), dtype=torch.float16, device=dev)
         if self.f16_bwd:
             self.dgx = torch.zeros((n, GH), dtype=torch.float16, device=dev)
             # fp16 mirror of the (TF32-rounded) parameters: the fp16 GEMMs' weights
@@ -581,7 +588,7 @@ class Shard:
                                      self.p(f"br{k}"), self.slot_row, self.slot_mask,
                                      self.slot_carry, self.carry[k], self.R, self.L, H, self.hw,
                                      hb, c_out, self.save[k],
-                                     h_out16=self.x16[k + 1] if k + 1 < cfg.n_rnn else None,
+                                     h_out16=self.x16[k + 1] if k + 1 < len(self.x16) else None,
                                      c_rows=self.n_run_ends)
             elif self.tc_rnn:
                 ops.gemm(xr, self.pr(f"Wx{k}"), self.gx, n, GH, H, lda=ldx, precision=prec,
@@ -608,17 +615,32 @@ class Shard:
                 pending_t.append((k, tok))
             xr, ldx = hb, self.hw
         # ---------------- readout + loss ----------------
-        ops.gemm(xr, self.pr("Wo"), self.logits, n, cfg.C, H, lda=ldx, precision=prec,
-                 bias=self.p("bo"))
-        ops.softmax_xent(self.logits, self.y, cfg.C, 1.0 / self.n_total, self.dlogits,
-                         self.loss_partial, round_tf32=self.tf32, dl_partial=self.dl_partial)
+        f16r = self.f16_readout and cfg.n_rnn > 0 and not self.evolve
+        if f16r:
+            xr16 = self.x16[cfg.n_rnn]
+            ops.gemm_f16(xr16, self.p16("Wo"), self.logits, n, cfg.C, H, lda=H, bias=self.p("bo"))
+            ops.softmax_xent(self.logits, self.y, cfg.C, 1.0 / self.n_total, None,
+                             self.loss_partial, dl_partial=self.dl_partial,
+                             dlogits16=self.dlogits16, scale16=2.0 ** self.da_exp)
+        else:
+            ops.gemm(xr, self.pr("Wo"), self.logits, n, cfg.C, H, lda=ldx, precision=prec,
+                     bias=self.p("bo"))
+            ops.softmax_xent(self.logits, self.y, cfg.C, 1.0 / self.n_total, self.dlogits,
+                             self.loss_partial, round_tf32=self.tf32, dl_partial=self.dl_partial)
         # ---------------- backward ----------------
         self.grads.zero_()
         ks, part = self.ksplit, self.partial
-        ops.gemm(xr, self.dlogits, self.g("Wo"), H, cfg.C, n, a_mn=True, lda=ldx, precision=prec,
-                 k_splits=ks, partial=part)
+        if f16r:
+            ops.gemm_f16(xr16, self.dlogits16, self.g("Wo"), H, cfg.C, n, a_mn=True, lda=H,
+                         alpha=self.inv_da_scale, k_splits=ks, partial=part)
+        else:
+            ops.gemm(xr, self.dlogits, self.g("Wo"), H, cfg.C, n, a_mn=True, lda=ldx,
+                     precision=prec, k_splits=ks, partial=part)
         rjobs = [(self.dl_partial, max(1, (n + 255) // 256), cfg.C, self.g("bo"))]
-        if self.evolve:  # no time encoder: dZ2 = (dlogits Wo^T) * (H2 > 0), b2 fused
+        if f16r:
+            ops.gemm_f16(self.dlogits16, self.p16("Wo"), self.dh, n, H, cfg.C, b_mn=False,
+                         ldb=cfg.C, alpha=self.inv_da_scale)
+        elif self.evolve:  # no time encoder: dZ2 = (dlogits Wo^T) * (H2 > 0), b2 fused
             ops.gemm(self.dlogits, self.pr("Wo"), self.dh, n, H, cfg.C, b_mn=False, ldb=cfg.C,
                      precision=prec, relu_src=self.Hl[1], colsum_partial=self.bp_b[1])
             rjobs.append((self.bp_b[1], 4 * self.m_tiles, H, self.g("b2")))
