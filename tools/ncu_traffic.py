@@ -42,12 +42,17 @@ def record(path):
 
 
 def main(out, tag, specs):
-    kernels = {}
+    # merge: records of other kernels / configs already in OUT are kept
+    try:
+        kernels = json.load(open(out)).get("kernels", {})
+    except (OSError, ValueError):
+        kernels = {}
     for spec in specs:
         parts = spec.split(":")
         config, name, path = parts[:3]
         rec = record(path)
         rec["config"] = config
+        rec["round"] = tag
         if len(parts) > 3:
             rec["shape"] = parts[3]
         kernels[f"{config}/{name}"] = rec
