@@ -623,24 +623,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
     const uint32_t kPeerBytes = 4u * (uint32_t)((rq + 7) / 8) * 8u * HU * (FX ? 2u : 4u);
     if (FX) {
       // this CTA's halves of U^T and Wx^T (B row n = gate column (n / HU) * H +
-      // u0 + n % HU, K = the H input units) as fp16, K-major SWIZZLE_128B, read
-      // straight from U and Wx [H, 4H] (the transpose happens here: consecutive
-      // threads take consecutive gate columns, so the fp32 reads coalesce);
+      // u0 + fx_unit(n % HU), K = the H input units) as fp16, K-major
+      // SWIZZLE_128B, read straight from U and Wx [H, 4H]: an item is 8 input
+      // units x 4 consecutive gate columns (eight 16-B loads, coalesced across
+      // the warp), transposed in registers into four 16-B B-row segments;
       // resident for the whole launch, ordered before the first MMA by the
-      // prologue's a_full arrival (unrolled: the L2 round trips of 4 items overlap)
-#pragma unroll 4
-      for (int c = threadIdx.x - 64; c < 2 * NP * (H / 8); c += kEpiT) {
-        const int mat = c / (NP * (H / 8)), cc = c % (NP * (H / 8));
-        const int n = cc % NP, k0 = (cc / NP) * 8;
-        const float* src = (mat ? Wxw : Uw) + (int64_t)k0 * G4 + (n / HU) * H + u0 + fx_unit(n % HU);
-        float v[8];
+      // prologue's a_full arrival
+      constexpr int kQuads = NP / 4;  // gate-column quads of this CTA
+#pragma unroll 2
+      for (int c = threadIdx.x - 64; c < 2 * (H / 8) * kQuads; c += kEpiT) {
+        const int qd = c % kQuads, kg = (c / kQuads) % (H / 8), mat = c / (kQuads * (H / 8));
+        const int g = qd / (HU / 4), j0 = 4 * (qd % (HU / 4));  // gate, first own unit
+        const int k0 = kg * 8;
+        const float* src = (mat ? Wxw : Uw) + (int64_t)k0 * G4 + g * H + u0 + j0;
+        float4 v[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = __ldg(src + (int64_t)i * G4);
-        const uint32_t dst = smem_u32(mat ? sW : sU) +
-                             (uint32_t)((k0 >> 6) * NP * 128 + n * 128 + ((((k0 & 63) >> 3) ^ (n & 7)) << 4));
-        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(h2u(v[0], v[1])),
-                     "r"(h2u(v[2], v[3])), "r"(h2u(v[4], v[5])), "r"(h2u(v[6], v[7]))
-                     : "memory");
+        for (int i = 0; i < 8; ++i) v[i] = ldg4(src + (int64_t)i * G4);
+        // units j0 + e sit in B rows g HU + (j0 & ~15) + {2p, 2p+1, 8+2p, 9+2p} (fx_unit)
+        const int p4 = (j0 & 15) >> 2, nb = g * HU + (j0 & ~15);
+        const int rows[4] = {nb + 2 * p4, nb + 2 * p4 + 1, nb + 8 + 2 * p4, nb + 9 + 2 * p4};
+        const uint32_t base = smem_u32(mat ? sW : sU) + (uint32_t)((k0 >> 6) * NP * 128);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          auto el = [&](const float4& f) { return e == 0 ? f.x : e == 1 ? f.y : e == 2 ? f.z : f.w; };
+          const int n = rows[e];
+          const uint32_t dst = base + (uint32_t)(n * 128 + ((((k0 & 63) >> 3) ^ (n & 7)) << 4));
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst),
+                       "r"(h2u(el(v[0]), el(v[1]))), "r"(h2u(el(v[2]), el(v[3]))),
+                       "r"(h2u(el(v[4]), el(v[5]))), "r"(h2u(el(v[6]), el(v[7])))
+                       : "memory");
+        }
       }
     }
     auto publish = [&](int half) {
