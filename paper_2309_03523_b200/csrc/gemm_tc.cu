@@ -486,22 +486,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// Split-K reduction, fixed order. Block = 64 float4 column groups x 4 split
-// slices: thread (g, s) sums splits s, s+4, ... of 4 consecutive elements (16-B
-// loads, 4x the loads in flight of a thread-per-element loop), the 4 slices are
-// then combined in order through shared memory. Needs N % 4 == 0.
-__global__ void __launch_bounds__(256) splitk_reduce4_kernel(
+// Split-K reduction, fixed order. Block = 64 float4 column groups x 16 split
+// slices: thread (g, s) sums splits s, s+16, ... of 4 consecutive elements
+// (16-B loads, unrolled by 4), the 16 slices are then combined in order through
+// shared memory. The small weight gradients (128 x 16, 128 x 128 over ~143
+// splits) were latency-bound at 4 slices (13-14 us per launch). Needs N % 4 == 0.
+constexpr int kRedSlices = 16;  // split slices per element quad (one 64 x 16 block)
+__global__ void __launch_bounds__(64 * kRedSlices) splitk_reduce4_kernel(
     const float* __restrict__ partial, int splits, int64_t M, int64_t N, float* __restrict__ C,
     int64_t ldc, const float* __restrict__ bias, const float* __restrict__ relu_src,
     int accumulate) {
-  __shared__ float4 red[4][64];
+  __shared__ float4 red[kRedSlices][64];
   const int64_t total4 = M * N / 4;
   const int64_t e4 = (int64_t)blockIdx.x * 64 + threadIdx.x;
   const int sl = threadIdx.y;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   if (e4 < total4) {
     const float4* p4 = reinterpret_cast<const float4*>(partial);
-    for (int z = sl; z < splits; z += 4) {
+    // unrolled: the loads of 4 splits are in flight together (the sums keep
+    // their sequential order)
+#pragma unroll 4
+    for (int z = sl; z < splits; z += kRedSlices) {
       const float4 v = __ldg(p4 + (int64_t)z * total4 + e4);
       acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
     }
@@ -510,7 +515,7 @@ __global__ void __launch_bounds__(256) splitk_reduce4_kernel(
   __syncthreads();
   if (sl != 0 || e4 >= total4) return;
   float4 t = red[0][threadIdx.x];
-  for (int k = 1; k < 4; ++k) {
+  for (int k = 1; k < kRedSlices; ++k) {
     const float4 v = red[k][threadIdx.x];
     t.x += v.x; t.y += v.y; t.z += v.z; t.w += v.w;
   }
@@ -803,7 +808,7 @@ static int gemm_impl(const float* A, int64_t lda, const float* B, int64_t ldb, f
   } else if (part) {
     if (N % 4 == 0 && (reinterpret_cast<uintptr_t>(part) & 15) == 0) {
       const int64_t total4 = M * N / 4;
-      splitk_reduce4_kernel<<<(unsigned)((total4 + 63) / 64), dim3(64, 4), 0, s>>>(
+      splitk_reduce4_kernel<<<(unsigned)((total4 + 63) / 64), dim3(64, kRedSlices), 0, s>>>(
           part, splits, M, N, C, ldc, bias, relu_src, accumulate);
     } else {
       splitk_reduce_kernel<<<dgc::grid_for(M * N, 256), 256, 0, s>>>(part, splits, M, N, C, ldc,
