@@ -487,6 +487,17 @@ int dgc_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, 
  * an epoch can be captured once in a CUDA graph and replayed. */
 int dgc_adam_dev(float* p, const float* g, float* m, float* v, int64_t n, float lr, float beta1,
                  float beta2, float eps, const int32_t* step_dev, void* stream);
+/* dgc_adam_dev that also refreshes the step's parameter mirrors in the same
+ * pass: p_r = TF32 round-to-nearest-away of the updated p, p16 = fp16(p_r)
+ * (each may be NULL) -- one launch instead of adam + round_tf32 + to_f16. */
+int dgc_adam_dev_mirror(float* p, const float* g, float* m, float* v, int64_t n, float lr,
+                        float beta1, float beta2, float eps, const int32_t* step_dev, float* p_r,
+                        void* p16, void* stream);
+/* End of a training step: loss_out[0] = sum of loss_partial[0..n) (fp64, fixed
+ * order, one block) and, when step_dev is non-NULL, ++*step_dev (the device
+ * step count a CUDA-graph-replayed Adam reads). */
+int dgc_epoch_finish(const double* loss_partial, int64_t n, double* loss_out, int32_t* step_dev,
+                     void* stream);
 
 #ifdef __cplusplus
 }

@@ -97,6 +97,8 @@ _SIGS = {
     "dgc_sgd": (_i32, [_p, _p, _p, _i64, _f32, _f32, _p]),
     "dgc_adam": (_i32, [_p, _p, _p, _p, _i64, _f32, _f32, _f32, _f32, _i32, _p]),
     "dgc_adam_dev": (_i32, [_p, _p, _p, _p, _i64, _f32, _f32, _f32, _f32, _p, _p]),
+    "dgc_adam_dev_mirror": (_i32, [_p, _p, _p, _p, _i64, _f32, _f32, _f32, _f32, _p, _p, _p, _p]),
+    "dgc_epoch_finish": (_i32, [_p, _i64, _p, _p, _p]),
 }
 
 _lib = None

@@ -104,19 +104,21 @@ __global__ void __launch_bounds__(256) colsum_stage1(const float* __restrict__ X
 
 // stage 2: out[j] (+)= sum of the nblk partial rows; block = 32 columns x 8
 // slab groups (each thread sums every 8th slab), combined in fixed order.
-__global__ void __launch_bounds__(256) colsum_stage2(const float* __restrict__ scratch, int nblk,
-                                                     int width, float* __restrict__ out,
-                                                     int accumulate) {
-  __shared__ float red[8][33];
+// 32 columns x 32 block groups (the order reduce_rows_batched_stage2 uses)
+__global__ void __launch_bounds__(1024) colsum_stage2(const float* __restrict__ scratch, int nblk,
+                                                      int width, float* __restrict__ out,
+                                                      int accumulate) {
+  __shared__ float red[32][33];
   const int j = blockIdx.x * 32 + threadIdx.x;
   float acc = 0.f;
   if (j < width)
-    for (int b = threadIdx.y; b < nblk; b += 8) acc += scratch[(int64_t)b * width + j];
+#pragma unroll 4
+    for (int b = threadIdx.y; b < nblk; b += 32) acc += scratch[(int64_t)b * width + j];
   red[threadIdx.y][threadIdx.x] = acc;
   __syncthreads();
   if (threadIdx.y == 0 && j < width) {
     float s = 0.f;
-    for (int g = 0; g < 8; ++g) s += red[g][threadIdx.x];
+    for (int g = 0; g < 32; ++g) s += red[g][threadIdx.x];
     out[j] = accumulate ? out[j] + s : s;
   }
 }
@@ -294,7 +296,72 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g,
   }
 }
 
+// Adam with the device step count and the step's parameter mirrors in one
+// pass: p_r = rna_tf32(p) (the TF32-rounded operand copy) and p16 = fp16(p_r)
+// (the fp16 GEMMs' weights), each when non-NULL.
+__global__ void adam_mirror_kernel(float* __restrict__ p, const float* __restrict__ g,
+                                   float* __restrict__ m, float* __restrict__ v, int64_t n,
+                                   float lr, float b1, float b2, float eps,
+                                   const int32_t* __restrict__ step_dev, float* __restrict__ p_r,
+                                   __half* __restrict__ p16) {
+  const float st = (float)*step_dev;
+  const float c1 = 1.f - powf(b1, st), c2 = 1.f - powf(b2, st);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    const float mi = b1 * m[i] + (1.f - b1) * gi;
+    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    const float pn = p[i] - lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+    p[i] = pn;
+    const float pr = p_r ? dgc::rna_tf32_f(pn) : pn;
+    if (p_r) p_r[i] = pr;
+    if (p16) p16[i] = __float2half_rn(pr);
+  }
+}
+
+// End of a step: loss = sum of the per-block loss partials in a fixed order
+// (one block), and the device step count advanced for the optimizer.
+__global__ void __launch_bounds__(256) epoch_finish_kernel(const double* __restrict__ part, int64_t n,
+                                                           double* __restrict__ out,
+                                                           int32_t* __restrict__ step_dev) {
+  __shared__ double red[256];
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 256) acc += part[i];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int off = 128; off > 0; off >>= 1) {
+    if ((int)threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = red[0];
+    if (step_dev) *step_dev += 1;
+  }
+}
+
 }  // namespace
+
+extern "C" int dgc_adam_dev_mirror(float* p, const float* g, float* m, float* v, int64_t n,
+                                   float lr, float beta1, float beta2, float eps,
+                                   const int32_t* step_dev, float* p_r, void* p16, void* stream) {
+  DGC_REQUIRE(step_dev != nullptr, "adam_dev_mirror: step_dev is NULL");
+  if (n == 0) return DGC_OK;
+  adam_mirror_kernel<<<dgc::grid_for(n, 256), 256, 0, dgc::as_stream(stream)>>>(
+      p, g, m, v, n, lr, beta1, beta2, eps, step_dev, p_r, static_cast<__half*>(p16));
+  DGC_CHECK_LAUNCH("adam_mirror_kernel");
+  return DGC_OK;
+}
+
+extern "C" int dgc_epoch_finish(const double* loss_partial, int64_t n, double* loss_out,
+                                int32_t* step_dev, void* stream) {
+  DGC_REQUIRE(loss_out != nullptr && (n == 0 || loss_partial != nullptr),
+              "epoch_finish: NULL buffer");
+  epoch_finish_kernel<<<1, 256, 0, dgc::as_stream(stream)>>>(loss_partial, n, loss_out, step_dev);
+  DGC_CHECK_LAUNCH("epoch_finish_kernel");
+  return DGC_OK;
+}
 
 extern "C" int dgc_softmax_xent(const float* logits, const int32_t* labels, int64_t n, int32_t C,
                                 float scale, int32_t flags, float* dlogits, double* loss_partial,
@@ -346,7 +413,7 @@ extern "C" int dgc_colsum(const float* X, int64_t n, int32_t width, int64_t ld, 
     colsum_stage1<<<nblk, 256, 256 * sizeof(float4), s>>>(X, n, width, ld, rows_per, scratch);
     DGC_CHECK_LAUNCH("colsum_stage1");
   }
-  colsum_stage2<<<(width + 31) / 32, dim3(32, 8), 0, s>>>(scratch, nblk, width, out, accumulate);
+  colsum_stage2<<<(width + 31) / 32, dim3(32, 32), 0, s>>>(scratch, nblk, width, out, accumulate);
   DGC_CHECK_LAUNCH("colsum_stage2");
   return DGC_OK;
 }
@@ -411,20 +478,23 @@ __global__ void __launch_bounds__(256) reduce_rows_batched_stage1(RRJobs J, floa
   }
 }
 
-__global__ void __launch_bounds__(256) reduce_rows_batched_stage2(RRJobs J, const float* __restrict__ scratch) {
-  __shared__ float red[8][33];
+// 32 slab groups per column (<= 8 slabs per thread: the 256-slab sums were a
+// latency chain of 32 loads at 8 groups)
+__global__ void __launch_bounds__(1024) reduce_rows_batched_stage2(RRJobs J, const float* __restrict__ scratch) {
+  __shared__ float red[32][33];
   int j = 0;
   while (j + 1 < J.n && (int)blockIdx.x >= J.blk2[j + 1]) ++j;
   const int width = J.width[j];
   const int c = (blockIdx.x - J.blk2[j]) * 32 + threadIdx.x;
   float acc = 0.f;
   if (c < width)
-    for (int b = threadIdx.y; b < J.nslab[j]; b += 8) acc += scratch[J.scr[j] + (int64_t)b * width + c];
+#pragma unroll 4
+    for (int b = threadIdx.y; b < J.nslab[j]; b += 32) acc += scratch[J.scr[j] + (int64_t)b * width + c];
   red[threadIdx.y][threadIdx.x] = acc;
   __syncthreads();
   if (threadIdx.y == 0 && c < width) {
     float s = 0.f;
-    for (int g = 0; g < 8; ++g) s += red[g][threadIdx.x];
+    for (int g = 0; g < 32; ++g) s += red[g][threadIdx.x];
     J.out[j][c] = s;
   }
 }
@@ -466,7 +536,7 @@ extern "C" int dgc_reduce_rows_batched(int32_t n_jobs, const float* const* parti
   cudaStream_t s = dgc::as_stream(stream);
   reduce_rows_batched_stage1<<<J.blk1[n_jobs], dim3(32, 8), 0, s>>>(J, scratch);
   DGC_CHECK_LAUNCH("reduce_rows_batched_stage1");
-  reduce_rows_batched_stage2<<<J.blk2[n_jobs], dim3(32, 8), 0, s>>>(J, scratch);
+  reduce_rows_batched_stage2<<<J.blk2[n_jobs], dim3(32, 32), 0, s>>>(J, scratch);
   DGC_CHECK_LAUNCH("reduce_rows_batched_stage2");
   return DGC_OK;
 }
@@ -492,7 +562,7 @@ extern "C" int dgc_reduce_rows(const float* partial, int64_t rows, int32_t width
     reduce_rows_stage1<<<grid, dim3(32, 8), 0, s>>>(partial, rows, width, slab, scratch);
     DGC_CHECK_LAUNCH("reduce_rows_stage1");
   }
-  colsum_stage2<<<(width + 31) / 32, dim3(32, 8), 0, s>>>(scratch, (int)slabs, width, out,
+  colsum_stage2<<<(width + 31) / 32, dim3(32, 32), 0, s>>>(scratch, (int)slabs, width, out,
                                                          accumulate);
   DGC_CHECK_LAUNCH("reduce_rows_stage2");
   return DGC_OK;

@@ -595,6 +595,26 @@ def sgd(p, g, mom, lr, momentum):
         20 * p.numel())
 
 
+def adam_mirror(p, g, m, v, lr, b1, b2, eps, step, p_r=None, p16=None):
+    """dgc_adam_dev_mirror: Adam (device step count) + the TF32 / fp16 parameter
+    mirrors (p_r = rna_tf32(p), p16 = fp16(p_r)) in one launch."""
+    _req(step, torch.int32, "step"); _req(p_r, torch.float32, "p_r"); _req16(p16, "p16")
+    _run("adam", lambda: _native.check(_native.lib().dgc_adam_dev_mirror(
+        _p(p), _p(g), _p(m), _p(v), p.numel(), float(lr), float(b1), float(b2), float(eps),
+        _p(step), _p(p_r), _p(p16), _stream()), "dgc_adam_dev_mirror"),
+        (28 + 4 * int(p_r is not None) + 2 * int(p16 is not None)) * p.numel())
+
+
+def epoch_finish(loss_partial, loss_out, step=None):
+    """dgc_epoch_finish: loss_out[0] = fixed-order sum of loss_partial (fp64);
+    step (int32 CUDA tensor) += 1 when given."""
+    _req(loss_partial, torch.float64, "loss_partial"); _req(loss_out, torch.float64, "loss_out")
+    _req(step, torch.int32, "step")
+    _run("epoch_finish", lambda: _native.check(_native.lib().dgc_epoch_finish(
+        _p(loss_partial), loss_partial.numel(), _p(loss_out), _p(step), _stream()),
+        "dgc_epoch_finish"), 8 * loss_partial.numel())
+
+
 def adam(p, g, m, v, lr, b1, b2, eps, step):
     """dgc_adam (host step count) or dgc_adam_dev (step: int32 CUDA tensor)."""
     if isinstance(step, torch.Tensor):

@@ -361,6 +361,7 @@ class Shard:
             self.billed_dev = torch.zeros(2, dtype=torch.int64, device=dev)
         self.step_count = 0
         self.step_dev = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.loss_sum = torch.zeros(1, dtype=torch.float64, device=dev)
         self.events = None
         self.timing = None  # list of (start, end) events of compute-stream stalls
 
@@ -808,17 +809,20 @@ class Shard:
             info["rows"] += sum(xp.sent_host)
             info["xbytes"] += sum(xp.sent_host) * (self.hw + 4) * 4
             self._wait(ev)
-        loss_local = self.loss_partial.sum().reshape(1)
+        # loss sum + the device step count (the epoch is replayable as a graph)
+        adam = cfg.optimizer == "adam"
+        ops.epoch_finish(self.loss_partial, self.loss_sum, self.step_dev if adam else None)
+        loss_local = self.loss_sum
         info["loss_sum"] = (yield ("sum", loss_local)) if D > 1 else loss_local
         if D > 1:
             yield ("sum", self.grads)
         self.step_count += 1
-        if cfg.optimizer == "adam":
-            self.step_dev.add_(1)  # device step count: the epoch is replayable as a graph
-            ops.adam(self.params, self.grads, self.m, self.v, cfg.lr, cfg.beta1, cfg.beta2,
-                     cfg.eps, self.step_dev)
-        else:
-            ops.sgd(self.params, self.grads, self.m, cfg.lr, cfg.momentum)
+        if adam:
+            ops.adam_mirror(self.params, self.grads, self.m, self.v, cfg.lr, cfg.beta1, cfg.beta2,
+                            cfg.eps, self.step_dev, p_r=self.params_r if self.tf32 else None,
+                            p16=self.params16 if self.f16_bwd else None)
+            return info
+        ops.sgd(self.params, self.grads, self.m, cfg.lr, cfg.momentum)
         if self.tf32:
             ops.round_tf32(self.params, self.params_r)
         if self.f16_bwd:
