@@ -420,7 +420,7 @@ def run_ours(args):
         "e2e": {"value": edges_total / (e2e_step / 1e3), "unit": UNIT,
                 "h2d_bytes_per_step": int(sum(x.numel() * x.element_size() + t.numel() * t.element_size()
                                               for x, t in zip(xs, ys))),
-                "pipeline": ("inputs double-buffered: step i+1's H2D overlaps step i on a copy stream; "
+                "pipeline": ("inputs double-buffered: step i+1's H2D overlaps step i (4 concurrent copy streams: one pinned stream moved 26-55 GB/s on these boxes, four 45+); "
                              + ("TF32 mode consumes in-range features at fp16 precision and ships "
                                 "them as fp16 (bit-identical to on-device rounding); the host-side "
                                 "fp32->fp16 conversion happens once, outside the timed region"

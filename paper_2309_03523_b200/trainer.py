@@ -1133,21 +1133,36 @@ class DGNNTrainer:
         pipeline, two input buffers per shard."""
         if self._copy_stream is None:
             self._copy_stream = torch.cuda.Stream(self.device)
+            # one pinned H2D copy stream moved 26-35 GB/s on the B200 boxes, four
+            # concurrent ones 45 GB/s (tools/h2d_bw.py): big inputs go in 4 slices
+            self._copy_lanes = [torch.cuda.Stream(self.device) for _ in range(4)]
             for sh, x in zip(self.shards, xs):
                 sh.X_stage = (None if sh.X.dtype == torch.float16 else
                               torch.empty(x.shape, dtype=x.dtype, device=self.device))
                 sh.X_alt = torch.empty_like(sh.X)
                 sh.y_alt = torch.empty_like(sh.y)
+        def h2d(dst, src):  # dst <- src (pinned host), in row slices on the copy lanes
+            rows = src.shape[0]
+            k = len(self._copy_lanes) if src.numel() * src.element_size() >= (8 << 20) else 1
+            step = (rows + k - 1) // k
+            for i in range(k):
+                lane = self._copy_lanes[i]
+                lane.wait_stream(self._copy_stream)
+                with torch.cuda.stream(lane):
+                    dst[i * step:(i + 1) * step].copy_(src[i * step:(i + 1) * step], non_blocking=True)
+            for i in range(k):
+                self._copy_stream.wait_stream(self._copy_lanes[i])
+
         with torch.cuda.stream(self._copy_stream):
             # the second buffers were last read by the epoch before the running one
             if self._alt_free_ev is not None:
                 self._copy_stream.wait_event(self._alt_free_ev)
             for sh, x, y in zip(self.shards, xs, ys):
                 if sh.X.dtype == torch.float16:  # resident fp16 features: straight in
-                    sh.X_alt.copy_(x, non_blocking=True)
+                    h2d(sh.X_alt, x)
                     sh.y_alt.copy_(y, non_blocking=True)
                     continue
-                sh.X_stage.copy_(x, non_blocking=True)
+                h2d(sh.X_stage, x)
                 if sh.X_stage.dtype == torch.float16:  # fp16 features
                     ops.unpack_f16(sh.X_stage, sh.X_alt)
                 elif sh.X_stage.dtype == torch.uint8:  # TF32 values shipped in 3 bytes
