@@ -324,13 +324,15 @@ int dgc_rnn_fwd_tc(int32_t cell, const float* gx, const float* Ut, const int32_t
  * fp16 (the layer input); Wx, U [128, 512] fp32 as the model stores them; bias
  * [512]. h_out is rounded to fp16 precision (exact in TF32), so the next
  * position's fp16 h tile equals it; h_out16 (may be NULL) receives its fp16
- * copy [n, 128] for the next layer's x16. Replaces the gx GEMM +
+ * copy [n, 128] for the next layer's x16. flags bit 0 (needs h_out16): h_out
+ * (fp32) is written only at run ends, like c (the fp16 copy is then the
+ * layer's output; the run-end rows are the carries). Replaces the gx GEMM +
  * dgc_rnn_fwd_tc pair; save/h/c outputs as dgc_rnn_fwd_tc. */
 int dgc_lstm_fwd_tc_f16x(const void* x16, int64_t n_x, const float* Wx, const float* U,
                          const float* bias, const int32_t* slot_row, const uint8_t* slot_mask,
                          const int32_t* slot_carry, const float* carry, int64_t n_rows,
                          int32_t row_len, int64_t ld_out, float* h_out, float* c_out, float* save,
-                         void* h_out16, void* stream);
+                         void* h_out16, int32_t flags, void* stream);
 /* 1 if dgc_lstm_fwd_tc_f16x serves this (F, H) in this process, else 0. */
 int dgc_rnn_fwd_tc_fused_available(int32_t F, int32_t H);
 /* Tensor-core BPTT (LSTM, H in {32,64,128}): takes U itself [H, 4H] (the

@@ -48,7 +48,7 @@ _SIGS = {
                                        _i64, _i64, _i64, _p, _p, _p, _p]),
     "dgc_propagate_labels": (_i32, [_i64, _i64, _p, _i64, _p, _i64, _p, _i64, _i32, _p, _p, _p]),
     "dgc_lstm_fwd_tc_f16x": (_i32, [_p, _i64, _p, _p, _p, _p, _p, _p, _p, _i64, _i32, _i64, _p, _p,
-                                    _p, _p, _p]),
+                                    _p, _p, _i32, _p]),
     "dgc_rnn_fwd_tc_fused_available": (_i32, [_i32, _i32]),
     "dgc_pack_sequences": (_i32, [_p, _i64, _i32, _i64, _p, _p, _p, _p, _p]),
     "dgc_spmm_csr": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i32, _i32, _p]),

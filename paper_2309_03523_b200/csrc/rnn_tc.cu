@@ -355,7 +355,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
                          int64_t R, int L, int64_t ld, float* __restrict__ h_out,
                          float* __restrict__ c_out, float* __restrict__ save, int rq,
                          const float* __restrict__ Uw, const float* __restrict__ Wxw,
-                         __half* __restrict__ h16) {
+                         __half* __restrict__ h16, int hends) {
   constexpr int kEpiT = 32 * kVEW;
   constexpr int G4 = 4 * H;
   constexpr int HU = H / 2;
@@ -814,7 +814,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
             st4(sv + 5 * H, og);
             st4(sv + 6 * H, tc);
           }
-          st4(h_out + (int64_t)inst * ld + j, hn);
+          // hends: the fp16 copy is the layer's output; fp32 h only where a run
+          // ends (the carries other devices read), like c
+          if (!hends || !(has_next && n_mk)) st4(h_out + (int64_t)inst * ld + j, hn);
           if (FX && h16) sth4(h16 + (int64_t)inst * H + j, hn);  // the next layer's fp16 x
           // c leaves the kernel only where a run ends (the carries other devices
           // read); inside a run it lives in creg and in the successor's c_in save
@@ -859,7 +861,7 @@ int launch_lstm_tc2v_ew(const CUtensorMap& m, const CUtensorMap& mwx, const CUte
                         const uint8_t* slot_mask, const int32_t* slot_carry, const float* carry,
                         int64_t R, int L, int64_t ld, float* h_out, float* c_out, float* save,
                         int rq, cudaStream_t s, const float* Uw = nullptr,
-                        const float* Wxw = nullptr, __half* h16 = nullptr) {
+                        const float* Wxw = nullptr, __half* h16 = nullptr, int hends = 0) {
   // FX: fp16 h tile + resident fp16 U^T / Wx^T halves + one x stage
   const size_t smem = (FX ? (size_t)2 * BM * 128 + (size_t)2 * 2 * 2 * H * 128 + (size_t)BM * 128
                          : (size_t)(H / BK) * BM * 128 + (size_t)kStages * 2 * H * 128) +
@@ -870,7 +872,7 @@ int launch_lstm_tc2v_ew(const CUtensorMap& m, const CUtensorMap& mwx, const CUte
   if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_fwd_tc2v: set smem");
   const int grid = 2 * (int)cluster_tiles(R);
   kern<<<grid, 64 + 32 * EW, smem, s>>>(m, mwx, mx, bias, gx, slot_row, slot_mask, slot_carry,
-                                        carry, R, L, ld, h_out, c_out, save, rq, Uw, Wxw, h16);
+                                        carry, R, L, ld, h_out, c_out, save, rq, Uw, Wxw, h16, hends);
   DGC_CHECK_LAUNCH("lstm_fwd_tc2v_kernel");
   return DGC_OK;
 }
@@ -898,7 +900,7 @@ int launch_lstm_tc2v(const float* gx, const float* Ut, const int32_t* slot_row,
 int launch_lstm_tc2x(const void* x16, int64_t n_x, const float* Wx, const float* U,
                      const float* bias, const int32_t* slot_row, const uint8_t* slot_mask,
                      const int32_t* slot_carry, const float* carry, int64_t R, int L, int64_t ld,
-                     float* h_out, float* c_out, float* save, __half* h16, cudaStream_t s) {
+                     float* h_out, float* c_out, float* save, __half* h16, int hends, cudaStream_t s) {
   constexpr int H = 128;
   CUtensorMap mx;  // (the fp32 weight maps of the other instantiations are unused here)
   int rc = make_gather_map_f16(&mx, x16, n_x, H, H);
@@ -907,10 +909,10 @@ int launch_lstm_tc2x(const void* x16, int64_t n_x, const float* Wx, const float*
   if (rq <= 24 && !getenv("DGC_RNN_EW16"))
     return launch_lstm_tc2v_ew<H, 12, true>(mx, mx, mx, bias, nullptr, slot_row, slot_mask,
                                             slot_carry, carry, R, L, ld, h_out, c_out, save, rq, s,
-                                            U, Wx, h16);
+                                            U, Wx, h16, hends);
   return launch_lstm_tc2v_ew<H, 16, true>(mx, mx, mx, bias, nullptr, slot_row, slot_mask,
                                           slot_carry, carry, R, L, ld, h_out, c_out, save, rq, s, U,
-                                          Wx, h16);
+                                          Wx, h16, hends);
 }
 
 // ---------------------------------------------------------------------------
@@ -2026,13 +2028,14 @@ extern "C" int dgc_lstm_fwd_tc_f16x(const void* x16, int64_t n_x, const float* W
                                     const uint8_t* slot_mask, const int32_t* slot_carry,
                                     const float* carry, int64_t n_rows, int32_t row_len,
                                     int64_t ld_out, float* h_out, float* c_out, float* save,
-                                    void* h_out16, void* stream) {
+                                    void* h_out16, int32_t flags, void* stream) {
   DGC_REQUIRE(cluster_rnn_enabled(), "lstm_fwd_tc_f16x: needs the cluster kernels (DGC_NO_CLUSTER_RNN set)");
+  DGC_REQUIRE(!(flags & 1) || h_out16 != nullptr, "lstm_fwd_tc_f16x: h at run ends only needs h_out16");
   DGC_REQUIRE(c_out != nullptr && bias != nullptr, "lstm_fwd_tc_f16x: c_out and bias required");
   if (n_rows == 0 || row_len == 0) return DGC_OK;
   return launch_lstm_tc2x(x16, n_x, Wx, U, bias, slot_row, slot_mask, slot_carry, carry, n_rows,
                           row_len, ld_out, h_out, c_out, save, static_cast<__half*>(h_out16),
-                          dgc::as_stream(stream));
+                          flags & 1, dgc::as_stream(stream));
 }
 
 extern "C" int dgc_rnn_fwd_tc_fused_available(int32_t F, int32_t H) {

@@ -366,11 +366,13 @@ def rnn_fwd_tc_fused_available(F, H):
 
 
 def lstm_fwd_tc_f16x(x16, Wx, U, bias, slot_row, slot_mask, slot_carry, carry, n_rows, row_len,
-                     H, ld_out, h_out, c_out, save, h_out16=None, c_rows=None):
+                     H, ld_out, h_out, c_out, save, h_out16=None, c_rows=None,
+                     h32_run_ends_only=False):
     """K4 on tcgen05 with the input projection fused (dgc_lstm_fwd_tc_f16x): the
     fp16 x rows of each position are TMA-gathered and multiplied by Wx^T in TMEM
     next to h U^T, both weight halves resident in shared memory as fp16; no gx
-    round trip through HBM and no weight traffic per position."""
+    round trip through HBM and no weight traffic per position. With
+    h32_run_ends_only (needs h_out16) the fp32 h is written only at run ends."""
     if x16.dtype != torch.float16 or not x16.is_cuda:
         raise ValueError("x16 must be a CUDA fp16 tensor")
     _req(Wx, torch.float32, "Wx"); _req(U, torch.float32, "U")
@@ -381,13 +383,17 @@ def lstm_fwd_tc_f16x(x16, Wx, U, bias, slot_row, slot_mask, slot_carry, carry, n
     # the run ends
     sf = rnn_tc_save_floats(H)
     c_rows = n_inst if c_rows is None else c_rows
-    nb = (n_inst * (2 * F + 4 * sf + 4 * H + (2 * H if h_out16 is not None else 0))
-          + 4 * c_rows * H + 9 * n_rows * row_len + 4 * G * H * (H + F))
+    if h32_run_ends_only and h_out16 is None:
+        raise ValueError("h32_run_ends_only needs h_out16")
+    h32_rows = c_rows if h32_run_ends_only else n_inst
+    nb = (n_inst * (2 * F + 4 * sf + (2 * H if h_out16 is not None else 0))
+          + 4 * h32_rows * H + 4 * c_rows * H + 9 * n_rows * row_len + 4 * G * H * (H + F))
     _run("lstm_fwd_tc", lambda: _native.check(
         _native.lib().dgc_lstm_fwd_tc_f16x(_p(x16), x16.shape[0], _p(Wx), _p(U), _p(bias),
                                            _p(slot_row), _p(slot_mask), _p(slot_carry), _p(carry),
                                            n_rows, row_len, ld_out, _p(h_out), _p(c_out), _p(save),
-                                           _p(h_out16), _stream()), "dgc_lstm_fwd_tc_f16x"),
+                                           _p(h_out16), int(bool(h32_run_ends_only)), _stream()),
+        "dgc_lstm_fwd_tc_f16x"),
         nb, 2.0 * n_rows * row_len * H * G * (H + F))
 
 

@@ -585,12 +585,15 @@ class Shard:
             if self.fused_xproj:
                 # x Wx + h U + b in one tensor-core recurrence (fp16 operands,
                 # resident weights; no gx round trip)
+                # the fp16 copy feeds the next layer (or the fp16 readout): the
+                # fp32 h is then needed only at run ends (the carries)
+                h16 = self.x16[k + 1] if k + 1 < len(self.x16) else None
                 ops.lstm_fwd_tc_f16x(self.x16[k], self.p(f"Wx{k}"), self.p(f"U{k}"),
                                      self.p(f"br{k}"), self.slot_row, self.slot_mask,
                                      self.slot_carry, self.carry[k], self.R, self.L, H, self.hw,
                                      hb, c_out, self.save[k],
-                                     h_out16=self.x16[k + 1] if k + 1 < len(self.x16) else None,
-                                     c_rows=self.n_run_ends)
+                                     h_out16=h16, c_rows=self.n_run_ends,
+                                     h32_run_ends_only=h16 is not None)
             elif self.tc_rnn:
                 ops.gemm(xr, self.pr(f"Wx{k}"), self.gx, n, GH, H, lda=ldx, precision=prec,
                          bias=self.p(f"br{k}"))

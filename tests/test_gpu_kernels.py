@@ -664,6 +664,18 @@ def test_lstm_fwd_fused_projection_matches_two_step(n_seq, carry_frac):
                                  hc[:, H:], save, h_out16=h16)
             torch.cuda.synchronize()
             assert torch.equal(h16.float(), hc[:, :H])
+            # fp32 h at run ends only: same fp16 output, same run-end rows, nothing else
+            hc2 = torch.zeros_like(hc)
+            h16b = torch.zeros_like(h16)
+            ops.lstm_fwd_tc_f16x(x[:, :H].half(), Wx, U, b, sr, sm, sc, carry, R, L, H, 2 * H,
+                                 hc2, hc2[:, H:], torch.zeros_like(save), h_out16=h16b,
+                                 h32_run_ends_only=True)
+            torch.cuda.synchronize()
+            assert torch.equal(h16b, h16)
+            ends_t = torch.as_tensor(run_end_rows(slot_row, mask), device=dev)
+            inner = torch.ones(n, dtype=torch.bool, device=dev)
+            inner[ends_t] = False
+            assert torch.equal(hc2[ends_t], hc[ends_t]) and not hc2[inner, :H].any()
         else:
             gx = torch.zeros((n, 4 * H), device=dev)
             ops.gemm(x, Wx, gx, n, 4 * H, H, lda=2 * H, precision=1, bias=b)
