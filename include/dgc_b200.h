@@ -195,6 +195,11 @@ int dgc_spmm_csr_h(const int32_t* row_ptr, const int32_t* col, const float* dinv
                    const void* Y16, const float* bias, float* out, void* out16, float scale16,
                    int64_t n_rows, int32_t width, int32_t act, int32_t* work, void* stream);
 
+/* Cap on the CTAs of the following GEMM launches (0: one per SM); returns the
+ * previous cap. For two GEMMs issued on concurrent streams that stream the
+ * same operand (each takes part of the machine, and the second reader of a
+ * tile finds it in L2). Host-side state of the calling process. */
+int32_t dgc_gemm_max_ctas(int32_t n);
 /* K2: tcgen05 TF32 GEMM (TMA -> SMEM -> TMEM), fp32 storage, fp32 accumulate.
  *   C[M,N] = (accumulate ? C : 0) + op(A) op(B)  (+ bias[N]) (* (relu_src > 0))
  *   a_mn = 0: A is [M,K] (row stride lda); a_mn = 1: A stored as [K,M] (A^T)

@@ -54,6 +54,7 @@ _SIGS = {
     "dgc_spmm_csr": (_i32, [_p, _p, _p, _p, _p, _p, _i64, _i32, _i32, _p]),
     "dgc_gemm_tf32": (_i32, [_p, _i64, _p, _i64, _p, _i64, _i64, _i64, _i64, _i32, _i32, _i32,
                               _p, _p, _i32, _i32, _p, _p, _p]),
+    "dgc_gemm_max_ctas": (_i32, [_i32]),
     "dgc_gemm_splits": (_i32, [_i64, _i32, _i32]),
     "dgc_gemm_tf32_stacked_a": (_i32, [_p, _i64, _p, _i64, _i64, _p, _i64, _p, _i64, _i64, _i64,
                                        _i64, _i32, _i32, _i32, _i32, _p, _p]),

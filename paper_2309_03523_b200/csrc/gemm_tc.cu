@@ -578,6 +578,8 @@ struct SegOpts {
   int64_t a2_row0 = 0;
 };
 
+int g_max_ctas = 0;  // 0: every SM (dgc_gemm_max_ctas)
+
 template <bool A_MN, bool B_MN, bool SPLIT3, bool F16 = false>
 int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, int tma_store,
                 int64_t c_rows_per_z, const CUtensorMap& ma2, int64_t a2_row0,
@@ -621,7 +623,11 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   if (e != cudaSuccess) return dgc::cuda_fail(e, "gemm: set smem");
   const int m_tiles = (int)((M + BM - 1) / BM);
   const int total = m_tiles * ntiles * splits;
-  int grid = (dgc::kNumSMs / ntiles) * ntiles;  // multiple of n_tiles: fixed n per CTA
+  // multiple of n_tiles: fixed n per CTA; g_max_ctas caps it for GEMMs that
+  // run concurrently with another one (dgc_gemm_max_ctas)
+  const int sms = g_max_ctas > 0 && g_max_ctas < dgc::kNumSMs ? g_max_ctas : dgc::kNumSMs;
+  int grid = (sms / ntiles) * ntiles;
+  if (grid < ntiles) grid = ntiles;
   if (grid > total) grid = total;
   kern<<<grid, kThreads, smem, s>>>(ma, mb, mc, tma_store, c_rows_per_z, ma2, a2_row0, C, ldc, M, N, bn, stages, kb_total, kb_per, m_tiles,
                                     ntiles, splits, bias, relu_src, accumulate, partial,
@@ -632,6 +638,12 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
 }
 
 }  // namespace
+
+extern "C" int32_t dgc_gemm_max_ctas(int32_t n) {
+  const int32_t prev = g_max_ctas;
+  g_max_ctas = n > 0 ? n : 0;
+  return prev;
+}
 
 extern "C" int dgc_gemm_splits(int64_t K, int32_t precision, int32_t k_splits) {
   const int KE = precision == 2 ? 64 : BK;

@@ -232,6 +232,12 @@ def _req16(t, name):
         raise ValueError(f"{name} must be a CUDA fp16 tensor")
 
 
+def gemm_max_ctas(n):
+    """dgc_gemm_max_ctas: cap the CTAs of the following GEMM launches (0: all
+    SMs); returns the previous cap."""
+    return int(_native.lib().dgc_gemm_max_ctas(int(n)))
+
+
 def gemm_f16(A, B, C, M, N, K, *, a_mn=False, b_mn=True, lda=None, ldb=None, ldc=None, alpha=1.0,
              bias=None, relu_src=None, accumulate=False, k_splits=1, partial=None,
              colsum_partial=None, act=0, C16=None, c16_scale=1.0, relu16=None):

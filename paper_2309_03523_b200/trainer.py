@@ -362,6 +362,12 @@ class Shard:
         self.step_count = 0
         self.step_dev = torch.zeros(1, dtype=torch.int32, device=dev)
         self.loss_sum = torch.zeros(1, dtype=torch.float64, device=dev)
+        # concurrent LSTM weight-/input-gradient GEMMs (CTA split, e.g. "74,74";
+        # DGC_CONC_BWD=0 runs them one after the other)
+        conc = os.environ.get("DGC_CONC_BWD", "74,74")
+        self.conc_split = None if conc in ("0", "") else tuple(int(v) for v in conc.split(","))
+        self._side = torch.cuda.Stream(dev) if self.conc_split else None
+        self._ev_fork, self._ev_join = torch.cuda.Event(), torch.cuda.Event()
         self.events = None
         self.timing = None  # list of (start, end) events of compute-stream stalls
 
@@ -667,12 +673,25 @@ class Shard:
                 rjobs.append((self.bp_r[k], self.rnn_prows, GH, self.g(f"br{k}")))
             xin, ldxin = (self.Hl[1], H) if k == 0 else (self.hbuf[k - 1], self.hw)
             gU = self.g(f"U{k}")
+            conc = self.f16_bwd and self.conc_split is not None
+            if conc:
+                # the weight-gradient GEMM and the input-gradient GEMM below both
+                # stream dgx (4H fp16 per instance): run them side by side on
+                # parts of the machine so the second reader of a dgx tile finds
+                # it in L2 (one HBM pass instead of two)
+                main = torch.cuda.current_stream()
+                self._ev_fork.record(main)
+                self._side.wait_event(self._ev_fork)
+                prev_cap = ops.gemm_max_ctas(self.conc_split[0])
             if self.f16_bwd:
                 # [dWx; dU] = [x16; h_in16]^T (S dgx16) / S, fp16 operands, one launch
-                ops.gemm_f16_stacked_a(self.x16[k], self.save[k].view(torch.float16), self.dgx,
-                                       self.g(f"Wx{k}"), H, 2 * H, GH, n, a_mn=True, lda0=H,
-                                       lda1=2 * self.sf, ldb=GH, ldc=GH, alpha=self.inv_da_scale,
-                                       k_splits=ks, partial=part)
+                with torch.cuda.stream(self._side if conc else torch.cuda.current_stream()):
+                    ops.gemm_f16_stacked_a(self.x16[k], self.save[k].view(torch.float16), self.dgx,
+                                           self.g(f"Wx{k}"), H, 2 * H, GH, n, a_mn=True, lda0=H,
+                                           lda1=2 * self.sf, ldb=GH, ldc=GH,
+                                           alpha=self.inv_da_scale, k_splits=ks, partial=part)
+                if conc:
+                    ops.gemm_max_ctas(self.conc_split[1])
             elif cell == 1 and H % 128 == 0:
                 # [dWx; dU] = [x; h_in]^T dgx in ONE launch: dgx is streamed once
                 # (Wx{k} and U{k} are adjacent in the flat gradient buffer)
@@ -705,6 +724,10 @@ class Shard:
                 ops.gemm(self.dgx, self.pr(f"Wx{k}"), self.dh2, n, H, GH, b_mn=False, ldb=GH,
                          precision=prec, relu_src=relu_src,
                          colsum_partial=self.bp_b[1] if k == 0 else None)
+            if conc:  # join before the next BPTT rewrites dgx
+                ops.gemm_max_ctas(prev_cap)
+                self._ev_join.record(self._side)
+                main.wait_event(self._ev_join)
             if k == 0:  # dZ2 = dH2 * (H2 > 0): its column sums are the b2 gradient
                 rjobs.append((self.bp_b[1], 4 * self.m_tiles, H, self.g("b2")))
             self.dh, self.dh2 = self.dh2, self.dh
