@@ -1182,7 +1182,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
                          const uint8_t* __restrict__ slot_mask, int64_t R, int L,
                          const float* __restrict__ save, const float* __restrict__ dh_out,
                          float* __restrict__ dgx, int rnd, float* __restrict__ bias_partial,
-                         int rq, float da_scale, int dgx16) {
+                         int rq, float da_scale, int dgx16, uint32_t recv_bytes) {
   static_assert(H == 128, "K-split cluster BPTT is specialised for H = 128");
   constexpr int EW = kVEW;
   constexpr int kEpiT = 32 * EW;
@@ -1303,9 +1303,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
     const uint32_t rfull_peer = map_peer(recv_full, peer);
     const bool active = rb < rq;
     const float inv_scale = 1.f / da_scale;  // da_scale: a power of two
-    // bytes the peer sends into our receive tile per position: 8 rows x HU per
-    // active peer warp (4 quadrants x ceil(rq / 8) warps)
-    const uint32_t kRecvBytes = 4u * (uint32_t)((rq + RPW - 1) / RPW) * RPW * HU * 4u;
     int sbase[2];  // first slot of each of this lane's rows (R * L < 2^31), -1: no row
     int inst[2], mk[2];
 #pragma unroll
@@ -1371,7 +1368,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       }
       DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 6);
       if (has_next) {
-        if (ew == 0 && lane == 0) mbar_arrive_expect_tx(&recv_full[t & 1], kRecvBytes);
+        // recv_bytes: what the peer sends into our receive tile per position
+        // (8 rows x HU per active peer warp); a kernel parameter, so it is not
+        // held in (spilled) registers across the loop
+        if (ew == 0 && lane == 0) mbar_arrive_expect_tx(&recv_full[t & 1], recv_bytes);
         mbar_wait(&acc_full[(p + 1) & 1], ((t - 1) >> 1) & 1);
         fence_after();
         DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 1);
@@ -1549,8 +1549,11 @@ int launch_lstm_bwd_tc2k_ew(const float* U, const int32_t* slot_row, const uint8
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_bwd_tc2k: set smem");
   const int grid = 2 * (int)cluster_tiles(R);
+  // bytes the peer sends into a receive tile per position: 8 rows x H/2 fp32
+  // per active peer warp (4 quadrants x ceil(rq / 8) warps)
+  const uint32_t recv_bytes = 4u * (uint32_t)((rq + 7) / 8) * 8u * (H / 2) * 4u;
   kern<<<grid, 64 + 32 * EW, smem, s>>>(U, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
-                                        bias_partial, rq, da_scale, dgx16);
+                                        bias_partial, rq, da_scale, dgx16, recv_bytes);
   DGC_CHECK_LAUNCH("lstm_bwd_tc2k_kernel");
   return DGC_OK;
 }

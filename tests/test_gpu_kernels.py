@@ -793,3 +793,75 @@ def test_reduce_rows_batched_equals_separate_calls():
     torch.cuda.synchronize()
     for a, b in zip(sep, bat):
         assert np.array_equal(a.cpu().numpy(), b.cpu().numpy())
+
+
+def test_softmax_xent_f16_output_and_step_tail():
+    """dgc_softmax_xent_f16: the same loss partials and fp32 dlogits as
+    dgc_softmax_xent, plus fp16(scale16 * dlogits) (round to nearest even) and
+    the same dlogits column sums; dgc_epoch_finish: fixed-order fp64 loss sum and
+    the device step count; dgc_adam_dev_mirror: bitwise the adam + round_tf32 +
+    to_f16 sequence it replaces."""
+    from paper_2309_03523_b200 import ops
+    rng = np.random.default_rng(11)
+    n, C = 5003, 16
+    logits = t(rng.standard_normal((n, C)).astype(np.float32) * 3)
+    y = rng.integers(0, C, n).astype(np.int32)
+    y[::97] = -1  # padding rows
+    yt = t(y, torch.int32)
+    nb = (n + 255) // 256
+    dl, lp, dp = torch.zeros((n, C), device=dev), torch.zeros(nb, dtype=torch.float64, device=dev), \
+        torch.zeros(nb * C, device=dev)
+    ops.softmax_xent(logits, yt, C, 1.0 / n, dl, lp, dl_partial=dp)
+    dl2, lp2, dp2 = torch.zeros_like(dl), torch.zeros_like(lp), torch.zeros_like(dp)
+    d16 = torch.zeros((n, C), dtype=torch.float16, device=dev)
+    S = 2.0 ** 12
+    ops.softmax_xent(logits, yt, C, 1.0 / n, dl2, lp2, dl_partial=dp2, dlogits16=d16, scale16=S)
+    d16b = torch.zeros_like(d16)
+    ops.softmax_xent(logits, yt, C, 1.0 / n, None, lp2, dl_partial=dp2, dlogits16=d16b, scale16=S)
+    torch.cuda.synchronize()
+    assert torch.equal(dl2, dl) and torch.equal(lp2, lp) and torch.equal(dp2, dp)
+    assert torch.equal(d16, (dl * S).half()) and torch.equal(d16b, d16)
+    loss = torch.zeros(1, dtype=torch.float64, device=dev)
+    step = torch.full((1,), 6, dtype=torch.int32, device=dev)
+    ops.epoch_finish(lp, loss, step)
+    ops.epoch_finish(lp, loss, None)
+    torch.cuda.synchronize()
+    assert float(loss) == pytest.approx(float(lp.sum()), rel=1e-15) and int(step) == 7
+    m = 70001
+    p = t(rng.standard_normal(m).astype(np.float32))
+    g = t(rng.standard_normal(m).astype(np.float32) * 1e-3)
+    mv = [torch.zeros(m, device=dev) for _ in range(4)]
+    p2 = p.clone()
+    ops.adam(p, g, mv[0], mv[1], 1e-3, 0.9, 0.999, 1e-8, step)
+    pr, p16 = torch.zeros_like(p), torch.zeros(m, dtype=torch.float16, device=dev)
+    ops.round_tf32(p, pr)
+    ops.to_f16(pr, p16)
+    pr2, p162 = torch.zeros_like(p), torch.zeros_like(p16)
+    ops.adam_mirror(p2, g, mv[2], mv[3], 1e-3, 0.9, 0.999, 1e-8, step, p_r=pr2, p16=p162)
+    torch.cuda.synchronize()
+    for a, b in ((p2, p), (mv[2], mv[0]), (mv[3], mv[1]), (pr2, pr), (p162, p16)):
+        assert torch.equal(a, b)
+
+
+def test_gemm_cta_cap_same_result():
+    """dgc_gemm_max_ctas: a capped grid (the concurrent-GEMM mode) gives bitwise
+    the same output and split-K partial reduction as the full grid."""
+    from paper_2309_03523_b200 import ops
+    rng = np.random.default_rng(12)
+    M, N, K = 3000, 128, 512
+    A = t(rng.standard_normal((M, K)).astype(np.float32)).half()
+    B = t(rng.standard_normal((N, K)).astype(np.float32)).half()
+    outs = []
+    for cap in (0, 37):
+        prev = ops.gemm_max_ctas(cap)
+        C = torch.zeros((M, N), device=dev)
+        ops.gemm_f16(A, B, C, M, N, K, b_mn=False, ldb=K)
+        G = torch.zeros((K, N), device=dev)
+        part = torch.zeros(ops.gemm_splits(M, 2, 64) * K * N, device=dev)
+        ops.gemm_f16(A, C.half(), G, K, N, M, a_mn=True, lda=K, k_splits=64, partial=part)
+        ops.gemm_max_ctas(prev)
+        torch.cuda.synchronize()
+        outs.append((C.clone(), G.clone()))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    ref = A.float() @ B.float().t()
+    close(outs[0][0].cpu().numpy(), ref.cpu().numpy(), 2e-3, "capped gemm")
