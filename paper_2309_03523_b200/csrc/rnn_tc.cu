@@ -1298,22 +1298,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
     const int r4 = lane >> 3, u8 = lane & 7;  // vector lane: rows rb + 4 it + r4, units 4 u8 .. +3
     const uint32_t stg_s = smem_u32(stg_all + ew * kStgW);
     const uint32_t sA_s = smem_u32(sA), recv_s = smem_u32(recv);
-    const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
-    const uint32_t recv_peer = map_peer(recv, peer);
-    const uint32_t rfull_peer = map_peer(recv_full, peer);
+    // the TMEM base and the peer's receive-tile addresses are re-derived where
+    // they are used (a shared-memory load / one mapa): held in registers across
+    // the position loop they were spilled to local memory and reloaded on the
+    // critical path
+    const uint32_t tslot_s = smem_u32(tmem_slot);
     const bool active = rb < rq;
     const float inv_scale = 1.f / da_scale;  // da_scale: a power of two
     int sbase[2];  // first slot of each of this lane's rows (R * L < 2^31), -1: no row
-    int inst[2], mk[2];
+    int inst[2];
+    // slot masks as bits: bit it = this position's mask of row it, bit 2 + it =
+    // the mask of its successor slot (mnext)
+    uint32_t mbits = 0;
 #pragma unroll
     for (int it = 0; it < 2; ++it) {
       const int rl = rb + 4 * it + r4;
       const int64_t vrow = row0 + q * rq + rl;
       sbase[it] = (rl < rq && vrow < R) ? (int)(vrow * L) : -1;
       inst[it] = sbase[it] >= 0 ? slot_row[sbase[it] + L - 1] : -1;
-      mk[it] = sbase[it] >= 0 ? slot_mask[sbase[it] + L - 1] : 0;
+      mbits |= (sbase[it] >= 0 && slot_mask[sbase[it] + L - 1]) ? (1u << it) : 0u;
     }
-    float mnext[2] = {0.f, 0.f};
     float4 bsum[2][4], dcr[2][2];
 #pragma unroll
     for (int lc = 0; lc < 2; ++lc) {
@@ -1359,12 +1363,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
         }
       }
       // the next position's slots (consumed one position later)
-      int n_inst[2], n_mk[2];
+      int n_inst[2];
+      uint32_t n_mbits = 0;
 #pragma unroll
       for (int it = 0; it < 2; ++it) {
         const bool ok = sbase[it] >= 0 && p > 0;
         n_inst[it] = ok ? slot_row[sbase[it] + p - 1] : -1;
-        n_mk[it] = ok ? slot_mask[sbase[it] + p - 1] : 0;
+        n_mbits |= (ok && slot_mask[sbase[it] + p - 1]) ? (1u << it) : 0u;
       }
       DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 6);
       if (has_next) {
@@ -1380,7 +1385,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           // q*32 + (rb & 16) .. +15 hand lane (r8, uq) units 16 i + 4 uq .. +3 of
           // row rb + r8 (U's rows are in fx_unit order): own units -> staging,
           // the peer's units -> the peer's receive tile, all lanes storing
-          const uint32_t ta = tl + ((p + 1) & 1) * H + ((uint32_t)(rb & 16) << 16);
+          uint32_t tbase;
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tbase) : "r"(tslot_s));
+          const uint32_t ta = tbase + ((uint32_t)(q * 32 + (rb & 16)) << 16) + ((p + 1) & 1) * H;
           const bool hi = (rb & 8) != 0;
           const int r8 = lane >> 2, uq = lane & 3;
           float v[16];
@@ -1390,11 +1397,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
             sts4(stg_s + (uint32_t)((r8 * kS + 16 * i + 4 * uq) * 4),
                  make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
           tmem_ld16x256x4(ta + pu0, ta + pu0 + 16, ta + pu0 + 32, ta + pu0 + 48, hi, v);
-          const uint32_t dst = recv_peer + (uint32_t)(((t & 1) * kRecv + (q * kRQ + rb + r8) * HU + 4 * uq) * 4);
+          const uint32_t dst = map_peer(recv, peer) +
+                               (uint32_t)(((t & 1) * kRecv + (q * kRQ + rb + r8) * HU + 4 * uq) * 4);
+          const uint32_t rfull = map_peer(recv_full, peer) + (uint32_t)((t & 1) * 8);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
             st_async_v4(dst + 64 * i, make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]),
-                        rfull_peer + (uint32_t)((t & 1) * 8));
+                        rfull);
         }
         fence_before();
         __syncwarp();
@@ -1426,7 +1435,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           if (has_next) {
             const float4 a = lds4(stg_s + (uint32_t)(((4 * it + r4) * kS + jo) * 4));
             const float4 b = lds4(recv_s + (uint32_t)((((t & 1) * kRecv) + (q * kRQ + rl) * HU + jo) * 4));
-            const float mn = mnext[it] * inv_scale;  // the partials are S-scaled (exact)
+            const float mn = ((mbits >> (2 + it)) & 1u) ? inv_scale : 0.f;  // S-scaled partials (exact)
             dh = make_float4(mn * (a.x + b.x), mn * (a.y + b.y), mn * (a.z + b.z), mn * (a.w + b.w));
           }
           float4 da[4] = {zero4(), zero4(), zero4(), zero4()};
@@ -1440,7 +1449,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
                                     gv1[lc][it].x, gv1[lc][it].y, gv1[lc][it].z, gv1[lc][it].w};
             const float dhk[4] = {dh.x, dh.y, dh.z, dh.w};
             const float dck[4] = {dcr[lc][it].x, dcr[lc][it].y, dcr[lc][it].z, dcr[lc][it].w};
-            const float mp = (float)mk[it];
+            const float mp = ((mbits >> it) & 1u) ? 1.f : 0.f;
             float dak[4][4], dcpk[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -1497,12 +1506,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           for (int g = 0; g < 2; ++g) mbar_arrive(&a_full[(seq0 + g) % kKsAStages]);
         }
       }
+      mbits = ((mbits & 3u) << 2) | n_mbits;  // this position's masks become mnext
 #pragma unroll
-      for (int it = 0; it < 2; ++it) {
-        mnext[it] = (float)mk[it];
-        inst[it] = n_inst[it];
-        mk[it] = n_mk[it];
-      }
+      for (int it = 0; it < 2; ++it) inst[it] = n_inst[it];
     }
     if (bias_partial) {
       // the 4 row lanes of each unit quad (xor 8, 16), then the EW warps in fixed order
