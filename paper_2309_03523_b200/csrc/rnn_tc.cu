@@ -1199,7 +1199,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   constexpr int kKsAStages = ks_a_stages<kVEW>();
   constexpr int kRQ = ks_recv_rq<kVEW>();    // receive-tile rows per lane quadrant
   constexpr int kRecv = 4 * kRQ * HU;        // floats per receive tile
-  constexpr uint32_t kTmemCols = 2 * H;      // two N = H accumulators
+  // two N = H accumulators + the epilogue's carried dc (thread-private words
+  // at columns 2H + 16 * (warp's row group): 16 floats per lane)
+  constexpr uint32_t kTmemCols = 4 * H;
   constexpr int kSF = tc_save_floats<H>();   // compact save row (floats)
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned base, derived from the __shared__ array (keeps shared-space
@@ -1318,12 +1320,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       inst[it] = sbase[it] >= 0 ? slot_row[sbase[it] + L - 1] : -1;
       mbits |= (sbase[it] >= 0 && slot_mask[sbase[it] + L - 1]) ? (1u << it) : 0u;
     }
-    float4 bsum[2][4], dcr[2][2];
+    float4 bsum[2][4];
 #pragma unroll
-    for (int lc = 0; lc < 2; ++lc) {
+    for (int lc = 0; lc < 2; ++lc)
 #pragma unroll
       for (int g = 0; g < 4; ++g) bsum[lc][g] = zero4();
-      dcr[lc][0] = dcr[lc][1] = zero4();
+    // carried dc of (chunk lc, row it) at TMEM columns tdc + 8 lc + 4 it (kept
+    // out of the register file: held there it was spilled to local memory)
+    const uint32_t tdc = tmem_base + ((uint32_t)(q * 32) << 16) + 2 * H + 16 * (uint32_t)(ew >> 2);
+    {
+      const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      tmem_st8(tdc, z);
+      tmem_st8(tdc + 8, z);
     }
     // this lane's saved fields of (chunk lc, row it): dh_out (4 units), c_in, i/f/g/o
     auto load_fields = [&](int lc, int it, float4& dho, uint2& cv, uint4& g0, uint4& g1) {
@@ -1427,6 +1435,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           const int seq = seq0 + g;
           mbar_wait(&a_empty[seq % kKsAStages], ((seq / kKsAStages) & 1) ^ 1);
         }
+        float dcv[8];  // carried dc of this chunk: row it at dcv[4 it .. 4 it + 3]
+        tmem_ld8_after_st(tdc + 8 * lc, dcv);
 #pragma unroll
         for (int it = 0; it < 2; ++it) {
           const int rl = rb + 4 * it + r4;
@@ -1448,7 +1458,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
             const uint32_t gw[8] = {gv0[lc][it].x, gv0[lc][it].y, gv0[lc][it].z, gv0[lc][it].w,
                                     gv1[lc][it].x, gv1[lc][it].y, gv1[lc][it].z, gv1[lc][it].w};
             const float dhk[4] = {dh.x, dh.y, dh.z, dh.w};
-            const float dck[4] = {dcr[lc][it].x, dcr[lc][it].y, dcr[lc][it].z, dcr[lc][it].w};
+            const float dck[4] = {dcv[4 * it], dcv[4 * it + 1], dcv[4 * it + 2], dcv[4 * it + 3]};
             const float mp = ((mbits >> it) & 1u) ? 1.f : 0.f;
             float dak[4][4], dcpk[4];
 #pragma unroll
@@ -1482,7 +1492,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
                                         bsum[lc][g].z + v.z, bsum[lc][g].w + v.w);
             }
           }
-          dcr[lc][it] = dcp;
+          dcv[4 * it] = dcp.x; dcv[4 * it + 1] = dcp.y; dcv[4 * it + 2] = dcp.z; dcv[4 * it + 3] = dcp.w;
           // S da as fp16 into the A tiles: gate g -> k-block seq0 + g/2, columns
           // 32 (g & 1) + 4 u8 .. +3 of its 64 (8 B of a 16-B swizzle chunk)
 #pragma unroll
@@ -1496,6 +1506,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
                          : "memory");
           }
         }
+        tmem_st8(tdc + 8 * lc, dcv);
         fence_async_smem();
         DGC_TS(lc == 1 && blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 2);
         DGC_TS3(lc == 1 && blockIdx.x == 0 && lane == 0 && t < 256, t, ew);

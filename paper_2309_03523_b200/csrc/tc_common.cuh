@@ -226,6 +226,18 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
+// Thread-private TMEM words (32x32b: thread t = lane t of the warp's quadrant)
+// used as spill space next to the accumulators: store 8 values; the load
+// waits for this thread's earlier stores first (tcgen05.st is asynchronous).
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld8_after_st(uint32_t taddr, float* v) {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  tmem_ld8(taddr, v);
+}
 // Four tcgen05.ld.16x256b.x2 (16 TMEM lanes from `t*`'s lane, 16 columns each)
 // with one wait. Thread t receives, per load, lanes L = t/4 and L + 8 at
 // columns 2(t%4), 2(t%4)+1 and 8 + the same: registers {0,1} / {4,5} lane L,
