@@ -1320,18 +1320,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       inst[it] = sbase[it] >= 0 ? slot_row[sbase[it] + L - 1] : -1;
       mbits |= (sbase[it] >= 0 && slot_mask[sbase[it] + L - 1]) ? (1u << it) : 0u;
     }
-    float4 bsum[2][4];
-#pragma unroll
-    for (int lc = 0; lc < 2; ++lc)
-#pragma unroll
-      for (int g = 0; g < 4; ++g) bsum[lc][g] = zero4();
-    // carried dc of (chunk lc, row it) at TMEM columns tdc + 8 lc + 4 it (kept
-    // out of the register file: held there it was spilled to local memory)
-    const uint32_t tdc = tmem_base + ((uint32_t)(q * 32) << 16) + 2 * H + 16 * (uint32_t)(ew >> 2);
+    // thread-private TMEM words next to the accumulators (kept out of the
+    // register file, where they were spilled to local memory): the carried dc
+    // of (chunk lc, row it) at tdc + 8 lc + 4 it, and the bias partial sums of
+    // (chunk lc, gate g) at tbs + 16 lc + 4 g
+    const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16);
+    const uint32_t tdc = tq + 2 * H + 16 * (uint32_t)(ew >> 2);
+    const uint32_t tbs = tq + 2 * H + 64 + 32 * (uint32_t)(ew >> 2);
     {
-      const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      tmem_st8(tdc, z);
-      tmem_st8(tdc + 8, z);
+      const float z[16] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      tmem_st16(tdc, z);
+      tmem_st16(tbs, z);
+      tmem_st16(tbs + 16, z);
     }
     // this lane's saved fields of (chunk lc, row it): dh_out (4 units), c_in, i/f/g/o
     auto load_fields = [&](int lc, int it, float4& dho, uint2& cv, uint4& g0, uint4& g1) {
@@ -1437,6 +1437,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
         }
         float dcv[8];  // carried dc of this chunk: row it at dcv[4 it .. 4 it + 3]
         tmem_ld8_after_st(tdc + 8 * lc, dcv);
+        float bs[16];  // running bias sums of this chunk: gate g at bs[4 g .. 4 g + 3]
+        tmem_ld16(tbs + 16 * lc, bs);
 #pragma unroll
         for (int it = 0; it < 2; ++it) {
           const int rl = rb + 4 * it + r4;
@@ -1488,8 +1490,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
                 st4(dgx + oi + g * H, v);
               }
               da[g] = v;
-              bsum[lc][g] = make_float4(bsum[lc][g].x + v.x, bsum[lc][g].y + v.y,
-                                        bsum[lc][g].z + v.z, bsum[lc][g].w + v.w);
+              bs[4 * g] += v.x; bs[4 * g + 1] += v.y; bs[4 * g + 2] += v.z; bs[4 * g + 3] += v.w;
             }
           }
           dcv[4 * it] = dcp.x; dcv[4 * it + 1] = dcp.y; dcv[4 * it + 2] = dcp.z; dcv[4 * it + 3] = dcp.w;
@@ -1507,6 +1508,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           }
         }
         tmem_st8(tdc + 8 * lc, dcv);
+        tmem_st16(tbs + 16 * lc, bs);
         fence_async_smem();
         DGC_TS(lc == 1 && blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 2);
         DGC_TS3(lc == 1 && blockIdx.x == 0 && lane == 0 && t < 256, t, ew);
@@ -1524,10 +1526,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
     if (bias_partial) {
       // the 4 row lanes of each unit quad (xor 8, 16), then the EW warps in fixed order
 #pragma unroll
-      for (int lc = 0; lc < 2; ++lc)
+      for (int lc = 0; lc < 2; ++lc) {
+        float bs[16];
+        tmem_ld8_after_st(tbs + 16 * lc, bs);
+        tmem_ld8(tbs + 16 * lc + 8, bs + 8);
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
-          float4 v = bsum[lc][g];
+          float4 v = make_float4(bs[4 * g], bs[4 * g + 1], bs[4 * g + 2], bs[4 * g + 3]);
 #pragma unroll
           for (int m = 8; m <= 16; m <<= 1) {
             v.x += __shfl_xor_sync(0xffffffffu, v.x, m);
@@ -1537,6 +1542,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           }
           if (r4 == 0) sts4(stg_s + (uint32_t)(((lc * 4 + g) * 32 + 4 * u8) * 4), v);
         }
+      }
       asm volatile("bar.sync 1, %0;" ::"r"(kEpiT));
       if (ew == 0) {
         for (int lc = 0; lc < 2; ++lc)
