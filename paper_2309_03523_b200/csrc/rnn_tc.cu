@@ -717,7 +717,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       mbar_wait(&acc_full[ab], acc_par);
       fence_after();
       DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && p < 256, p, 1);
-#pragma unroll 1
+#pragma unroll (FX ? 2 : 1)
       for (int ch = 0; ch < NCH; ++ch) {
         const int c0 = ch * 16;
         const int j = u0 + c0 + uq * 4;
