@@ -314,15 +314,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           const int64_t nb = n0 + c;
           if (bias) {
+            if (nb + 32 <= N && (reinterpret_cast<uintptr_t>(bias + nb) & 15) == 0) {
+              // 8 broadcast 16-B loads (every lane reads the same 32 values)
 #pragma unroll
-            for (int u = 0; u < 32; ++u) v[u] += (nb + u < N) ? __ldg(bias + nb + u) : 0.f;
-          }
-          if (out_act) {
+              for (int j = 0; j < 8; ++j) {
+                const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + nb) + j);
+                v[4 * j] += b4.x; v[4 * j + 1] += b4.y; v[4 * j + 2] += b4.z; v[4 * j + 3] += b4.w;
+              }
+            } else {
 #pragma unroll
-            for (int u = 0; u < 32; ++u) {
-              if (out_act & 1) v[u] = fmaxf(v[u], 0.f);
-              if (out_act & 2) v[u] = dgc::rna_tf32_f(v[u]);
+              for (int u = 0; u < 32; ++u) v[u] += (nb + u < N) ? __ldg(bias + nb + u) : 0.f;
             }
+          }
+          if (out_act & 1) {
+#pragma unroll
+            for (int u = 0; u < 32; ++u) v[u] = fmaxf(v[u], 0.f);
+          }
+          if (out_act & 2) {
+#pragma unroll
+            for (int u = 0; u < 32; ++u) v[u] = dgc::rna_tf32_f(v[u]);
           }
           const int64_t row = m0 + q * 32 + lane;
           if (relu16 && row < M) {  // fp16 mask source: 64-B row segment
