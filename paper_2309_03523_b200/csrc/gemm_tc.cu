@@ -34,6 +34,7 @@ template <bool A_MN, bool B_MN, bool SPLIT3, bool F16>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC, int tma_store, int64_t c_rows_per_z,
+                     const __grid_constant__ CUtensorMap tmR, int mask_boxes,
                      const __grid_constant__ CUtensorMap tmA2, int64_t a2_row0,
                      float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, int bn, int stages,
                      int kb_total, int kb_per_split, int m_tiles, int n_tiles, int splits,
@@ -74,7 +75,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = conv + stages;   // [2]
   uint64_t* tempty = tfull + 2;      // [2]
   uint64_t* bres_full = tempty + 2;  // [1]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_full + 1);
+  uint64_t* mfull = bres_full + 1;   // [kEpiWarps] fp16 ReLU-mask boxes landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mfull + kEpiWarps);
   // epilogue staging (transpose buffers, or 4 KB SWIZZLE_128B boxes), 1024-B aligned
   uint8_t* stg_raw = reinterpret_cast<uint8_t*>(tmem_slot + 4);
   float* stg_base = reinterpret_cast<float*>(stg_raw + ((1024u - (smem_u32(stg_raw) & 1023u)) & 1023u));
@@ -95,6 +97,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tempty[a], 32 * kEpiWarps);
     }
     mbar_init(bres_full, 1);
+    for (int w = 0; w < kEpiWarps; ++w) mbar_init(&mfull[w], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
@@ -284,7 +287,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int a = i & 1;
       const uint32_t aph = (i >> 1) & 1;
-      if ((relu_src || relu16) && tma_store) {
+      // mask_boxes: the fp16 ReLU mask of this warp's chunks arrives by TMA
+      // ([32 rows x 32 cols] SWIZZLE_64B boxes, the output boxes' layout) under
+      // the accumulator wait; thread-per-row loads of it cost ~18 us per
+      // 200000 x 128 launch (32 row segments per warp load)
+      uint8_t* mbox = reinterpret_cast<uint8_t*>(stg_base) + (size_t)kEpiWarps * tma_store * 4096 +
+                      (size_t)(warp - 2) * mask_boxes * 2048;
+      if (relu16 && mask_boxes) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();  // the previous tile's mask reads are done
+        if (lane == 0) {
+          int nbx = 0;
+          for (int c = 32 * chalf; c < bn; c += 32 * (kEpiWarps / 4)) ++nbx;
+          mbar_arrive_expect_tx(&mfull[warp - 2], (uint32_t)nbx * 2048u);
+          int ci = 0;
+          for (int c = 32 * chalf; c < bn; c += 32 * (kEpiWarps / 4), ++ci)
+            tma_load_2d(mbox + ci * 2048, &tmR, (int)(n0 + c), (int)(m0 + q * 32), &mfull[warp - 2]);
+        }
+      }
+      if ((relu_src || (relu16 && !mask_boxes)) && tma_store) {
         // this thread's row of the ReLU mask streams into L1 while the tile's
         // MMAs finish (thread = row; its chunks of the tile's columns)
         const int64_t row = m0 + q * 32 + lane;
@@ -335,7 +356,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int u = 0; u < 32; ++u) v[u] = dgc::rna_tf32_f(v[u]);
           }
           const int64_t row = m0 + q * 32 + lane;
-          if (relu16 && row < M) {  // fp16 mask source: 64-B row segment
+          if (relu16 && mask_boxes) {  // this chunk's box (zero-filled outside the matrix)
+            if (c == 32 * chalf) mbar_wait(&mfull[warp - 2], (uint32_t)(i & 1));
+            const uint8_t* mb = mbox + ((c - 32 * chalf) / (32 * (kEpiWarps / 4))) * 2048;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint4 m = *reinterpret_cast<const uint4*>(mb + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4));
+              const uint32_t q4[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&q4[k]));
+                if (!(f.x > 0.f)) v[8 * j + 2 * k] = 0.f;
+                if (!(f.y > 0.f)) v[8 * j + 2 * k + 1] = 0.f;
+              }
+            }
+          } else if (relu16 && row < M) {  // fp16 mask source: 64-B row segment
             const uint4* rs = reinterpret_cast<const uint4*>(relu16 + row * ldr16 + nb);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -605,7 +640,15 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   // (8 x 4 KB TMA-store boxes, or 8 padded 32x33 transpose tiles) + alignment
   // and barriers, within the 227 KB per-CTA limit
   int stg_bytes = tma_store ? kEpiWarps * 4096 : kEpiWarps * 32 * 33 * 4;
-  const int budget = 232448 - 1024 - 256 - 1024 - stg_bytes;
+  // fp16 ReLU mask by TMA: one 2 KB box per 32-column chunk of each epilogue warp
+  const int mask_boxes = (relu16 && tma_store && !getenv("DGC_GEMM_NO_MASK_TMA")) ? (bn + 63) / 64 : 0;
+  const int mask_bytes = kEpiWarps * mask_boxes * 2048;
+  CUtensorMap mr = mc;
+  if (mask_boxes) {
+    const int rc = make_map_f16_sw64(&mr, relu16, M, N, ldr16, 32, 32);
+    if (rc) return rc;
+  }
+  const int budget = 232448 - 1024 - 512 - 1024 - stg_bytes - mask_bytes;
   // B panel resident in shared memory when one CTA keeps one n-tile and it fits
   const int bres_bytes = kb_total * bn * BK * 4;
   int bres_max = 96 * 1024;
@@ -623,11 +666,12 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   if (stages < 1) return dgc::fail(DGC_ERR_ARG, "gemm: tile does not fit shared memory");
   const size_t pipe = (size_t)stages * (b_res ? kABytes : stage_bytes) + (b_res ? (size_t)bres_bytes : 0);
   // a second TMA-store box per warp when it fits beside the pipeline
-  if (tma_store && pipe + 1024 + 256 + 1024 + 2 * stg_bytes <= 232448 && !getenv("DGC_GEMM_ONE_BOX")) {
+  if (tma_store && pipe + 1024 + 512 + 1024 + 2 * stg_bytes + mask_bytes <= 232448 &&
+      !getenv("DGC_GEMM_ONE_BOX")) {
     tma_store = 2;
     stg_bytes *= 2;
   }
-  const size_t smem = pipe + 1024 + 256 + 1024 + stg_bytes;
+  const size_t smem = pipe + 1024 + 512 + 1024 + stg_bytes + mask_bytes;
   auto kern = gemm_tf32_kernel<A_MN, B_MN, SPLIT3, F16>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return dgc::cuda_fail(e, "gemm: set smem");
@@ -639,7 +683,7 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   int grid = (sms / ntiles) * ntiles;
   if (grid < ntiles) grid = ntiles;
   if (grid > total) grid = total;
-  kern<<<grid, kThreads, smem, s>>>(ma, mb, mc, tma_store, c_rows_per_z, ma2, a2_row0, C, ldc, M, N, bn, stages, kb_total, kb_per, m_tiles,
+  kern<<<grid, kThreads, smem, s>>>(ma, mb, mc, tma_store, c_rows_per_z, mr, mask_boxes, ma2, a2_row0, C, ldc, M, N, bn, stages, kb_total, kb_per, m_tiles,
                                     ntiles, splits, bias, relu_src, accumulate, partial,
                                     colsum_partial, b_res, so.seg_of_mtile, so.b_seg_rows,
                                     so.kitems, alpha, C16, ldc16, c16_scale, relu16, ldr16);
