@@ -1425,7 +1425,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       for (int lc = 0; lc < 2; ++lc) {
         const int seq0 = t * KBO + lc * 2;   // this chunk's 2 fp16 k-blocks (gates 0-1, 2-3)
         const int jo = 32 * lc + 4 * u8;     // own unit index of this lane's 4 units
-        if (!kHoist || lc == 1) {
+        if (!kHoist) {
 #pragma unroll
           for (int it = 0; it < 2; ++it)
             load_fields(lc, it, dho[lc][it], cvv[lc][it], gv0[lc][it], gv1[lc][it]);
@@ -1494,6 +1494,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
             }
           }
           dcv[4 * it] = dcp.x; dcv[4 * it + 1] = dcp.y; dcv[4 * it + 2] = dcp.z; dcv[4 * it + 3] = dcp.w;
+          // chunk 1's fields of this row: issued as soon as chunk 0's fields of the
+          // row are consumed (their registers), so they are in flight under the
+          // rest of chunk 0
+          if (kHoist && lc == 0)
+            load_fields(1, it, dho[1][it], cvv[1][it], gv0[1][it], gv1[1][it]);
           // S da as fp16 into the A tiles: gate g -> k-block seq0 + g/2, columns
           // 32 (g & 1) + 4 u8 .. +3 of its 64 (8 B of a 16-B swizzle chunk)
 #pragma unroll
