@@ -284,12 +284,23 @@ class Shard:
         # fp16 readout (C % 8 == 0, C <= 32): the last LSTM layer also writes its h
         # as fp16 (x16[n_rnn]); logits = h16 Wo16 + bo, and the softmax emits
         # S-scaled fp16 dlogits for dWo = h16^T dlogits16 / S, dh = dlogits16 Wo16^T / S
-        self.f16_readout = bool(self.f16_bwd and cfg.C <= 32 and cfg.C % 8 == 0)
+        # EvolveGCN (TF32): the readout input is H2, whose fp16 copy the layer-2
+        # SpMM writes (h2_16); dZ2 = (dlogits16 Wo16^T / S) * (H2 > 0) takes the
+        # fp16 ReLU mask from it
+        evolve = cfg.model == "evolve"
+        self.f16_readout = bool(cfg.C <= 32 and cfg.C % 8 == 0 and
+                                (self.f16_bwd or (evolve and self.tf32 and H % 8 == 0)))
+        self.h2_16 = None
         if self.f16_readout:
-            self.x16.append(torch.zeros((n, H), dtype=torch.float16, device=dev))
+            if evolve:
+                self.h2_16 = torch.zeros((n, H), dtype=torch.float16, device=dev)
+            else:
+                self.x16.append(torch.zeros((n, H), dtype=torch.float16, device=dev))
             self.dlogits16 = torch.zeros((n, cfg.C), dtype=torch.float16, device=dev)
         if self.f16_bwd:
             self.dgx = torch.zeros((n, GH), dtype=torch.float16, device=dev)
+        self.params16 = None
+        if self.f16_bwd or self.f16_readout:
             # fp16 mirror of the (TF32-rounded) parameters: the fp16 GEMMs' weights
             self.params16 = torch.zeros(self.params.numel(), dtype=torch.float16, device=dev)
             ops.to_f16(self.params_r, self.params16)
@@ -413,7 +424,10 @@ class Shard:
         return self.params[o:o + n].view(*shape)
 
     def _x16_out(self, l):
-        """fp16 copy target of GCN layer l's output: the first LSTM layer's x16."""
+        """fp16 copy target of GCN layer l's output: the first LSTM layer's x16, or
+        (EvolveGCN, fp16 readout) the readout's input h2_16."""
+        if l == 1 and self.evolve:
+            return self.h2_16
         return self.x16[0] if (self.x16 is not None and l == 1 and not self.evolve) else None
 
     def p16(self, name):
@@ -625,9 +639,9 @@ class Shard:
                 pending_t.append((k, tok))
             xr, ldx = hb, self.hw
         # ---------------- readout + loss ----------------
-        f16r = self.f16_readout and cfg.n_rnn > 0 and not self.evolve
+        f16r = self.f16_readout and (cfg.n_rnn > 0 or self.evolve)
         if f16r:
-            xr16 = self.x16[cfg.n_rnn]
+            xr16 = self.h2_16 if self.evolve else self.x16[cfg.n_rnn]
             ops.gemm_f16(xr16, self.p16("Wo"), self.logits, n, cfg.C, H, lda=H, bias=self.p("bo"))
             ops.softmax_xent(self.logits, self.y, cfg.C, 1.0 / self.n_total, None,
                              self.loss_partial, dl_partial=self.dl_partial,
@@ -647,7 +661,12 @@ class Shard:
             ops.gemm(xr, self.dlogits, self.g("Wo"), H, cfg.C, n, a_mn=True, lda=ldx,
                      precision=prec, k_splits=ks, partial=part)
         rjobs = [(self.dl_partial, max(1, (n + 255) // 256), cfg.C, self.g("bo"))]
-        if f16r:
+        if f16r and self.evolve:  # dZ2 = (dlogits Wo^T) * (H2 > 0), b2 fused
+            ops.gemm_f16(self.dlogits16, self.p16("Wo"), self.dh, n, H, cfg.C, b_mn=False,
+                         ldb=cfg.C, alpha=self.inv_da_scale, relu16=self.h2_16,
+                         colsum_partial=self.bp_b[1])
+            rjobs.append((self.bp_b[1], 4 * self.m_tiles, H, self.g("b2")))
+        elif f16r:
             ops.gemm_f16(self.dlogits16, self.p16("Wo"), self.dh, n, H, cfg.C, b_mn=False,
                          ldb=cfg.C, alpha=self.inv_da_scale)
         elif self.evolve:  # no time encoder: dZ2 = (dlogits Wo^T) * (H2 > 0), b2 fused
@@ -846,12 +865,12 @@ class Shard:
         if adam:
             ops.adam_mirror(self.params, self.grads, self.m, self.v, cfg.lr, cfg.beta1, cfg.beta2,
                             cfg.eps, self.step_dev, p_r=self.params_r if self.tf32 else None,
-                            p16=self.params16 if self.f16_bwd else None)
+                            p16=self.params16)
             return info
         ops.sgd(self.params, self.grads, self.m, cfg.lr, cfg.momentum)
         if self.tf32:
             ops.round_tf32(self.params, self.params_r)
-        if self.f16_bwd:
+        if self.params16 is not None:
             ops.to_f16(self.params_r, self.params16)
         return info
 
