@@ -371,7 +371,10 @@ extern "C" int dgc_softmax_xent(const float* logits, const int32_t* labels, int6
   const int blocks = (int)((n + 255) / 256);
   const bool aligned = (reinterpret_cast<uintptr_t>(logits) & 15) == 0 &&
                        (reinterpret_cast<uintptr_t>(dlogits) & 15) == 0;
-  if (C <= 32 && (aligned || (C & 3) != 0)) {
+  if (C <= 16 && (aligned || (C & 3) != 0)) {  // (16 logits in registers: no idle guarded lanes)
+    softmax_xent_small_kernel<16><<<blocks, 256, 0, dgc::as_stream(stream)>>>(
+        logits, labels, n, C, scale, flags & 1, dlogits, loss_partial, dl_partial, nullptr, 1.f);
+  } else if (C <= 32 && (aligned || (C & 3) != 0)) {
     softmax_xent_small_kernel<32><<<blocks, 256, 0, dgc::as_stream(stream)>>>(
         logits, labels, n, C, scale, flags & 1, dlogits, loss_partial, dl_partial, nullptr, 1.f);
   } else {
@@ -394,9 +397,14 @@ extern "C" int dgc_softmax_xent_f16(const float* logits, const int32_t* labels, 
               "softmax_xent_f16: logits / dlogits must be 16-byte aligned");
   if (n == 0) return DGC_OK;
   const int blocks = (int)((n + 255) / 256);
-  softmax_xent_small_kernel<32><<<blocks, 256, 0, dgc::as_stream(stream)>>>(
-      logits, labels, n, C, scale, 0, dlogits, loss_partial, dl_partial,
-      static_cast<__half*>(dlogits16), scale16);
+  if (C <= 16)
+    softmax_xent_small_kernel<16><<<blocks, 256, 0, dgc::as_stream(stream)>>>(
+        logits, labels, n, C, scale, 0, dlogits, loss_partial, dl_partial,
+        static_cast<__half*>(dlogits16), scale16);
+  else
+    softmax_xent_small_kernel<32><<<blocks, 256, 0, dgc::as_stream(stream)>>>(
+        logits, labels, n, C, scale, 0, dlogits, loss_partial, dl_partial,
+        static_cast<__half*>(dlogits16), scale16);
   DGC_CHECK_LAUNCH("softmax_xent_kernel");
   return DGC_OK;
 }
