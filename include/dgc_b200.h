@@ -347,7 +347,9 @@ int dgc_rnn_fwd_tc_fused_available(int32_t F, int32_t H);
  * U resident in shared memory as fp16 and da as fp16 scaled by 2^e, e = bits
  * 16..22 of cell (0: unscaled); the scale is removed exactly from dh. Size e to
  * the loss normalisation (a mean over n instances: e = round(log2 n)) so that
- * S da sits in fp16's normal range. */
+ * S da sits in fp16's normal range. Bit 24: dgx is written as fp16 S * dgx.
+ * Bit 25 (K-split cluster kernel only): dh_out holds S * dh as fp16 (the fp16
+ * readout / input-gradient GEMMs' C16 output), unscaled exactly at use. */
 int dgc_rnn_bwd_tc(int32_t cell, const float* U, const int32_t* slot_row,
                    const uint8_t* slot_mask, int64_t n_rows, int32_t row_len, int32_t H,
                    const float* save, const float* dh_out, float* dgx, float* dc_scratch,

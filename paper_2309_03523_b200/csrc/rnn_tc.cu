@@ -15,6 +15,8 @@
 // The input projection x Wx + b of all slots is one K2 GEMM ahead of this kernel.
 #include <cuda_fp16.h>
 
+#include <type_traits>
+
 #include "tc_common.cuh"
 
 namespace {
@@ -1176,7 +1178,7 @@ template <int kVEW> __host__ __device__ constexpr int ks_a_stages() { return kVE
 template <int kVEW> __host__ __device__ constexpr int ks_recv_rq() { return kVEW <= 12 ? 24 : 32; }
 constexpr int kKsStgStride = 64 + 16;  // own-half staging row stride (floats): conflict-free
                                         // for the (row, unit quad) writes and the (r4, u8) reads
-template <int H, int kVEW>
+template <int H, int kVEW, bool DH16>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
     lstm_bwd_tc2k_kernel(const float* __restrict__ U, const int32_t* __restrict__ slot_row,
                          const uint8_t* __restrict__ slot_mask, int64_t R, int L,
@@ -1203,6 +1205,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   // at columns 2H + 16 * (warp's row group): 16 floats per lane)
   constexpr uint32_t kTmemCols = 4 * H;
   constexpr int kSF = tc_save_floats<H>();   // compact save row (floats)
+  using DhoT = typename std::conditional<DH16, uint2, float4>::type;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned base, derived from the __shared__ array (keeps shared-space
   // addressing: STS/LDS instead of generic ST/LD)
@@ -1333,17 +1336,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       tmem_st16(tbs, z);
       tmem_st16(tbs + 16, z);
     }
-    // this lane's saved fields of (chunk lc, row it): dh_out (4 units), c_in, i/f/g/o
-    auto load_fields = [&](int lc, int it, float4& dho, uint2& cv, uint4& g0, uint4& g1) {
+    // this lane's saved fields of (chunk lc, row it): dh_out (4 units), c_in, i/f/g/o.
+    // DH16: dh_out is S-scaled fp16 (8 B per lane, kept raw until its use)
+    auto load_fields = [&](int lc, int it, DhoT& dho, uint2& cv, uint4& g0, uint4& g1) {
       const int j = u0 + 32 * lc + 4 * u8;
       if (inst[it] >= 0) {
-        dho = ldg4(dh_out + (int64_t)inst[it] * H + j);
+        if constexpr (DH16)
+          dho = __ldg(reinterpret_cast<const uint2*>(dh_out) + (((int64_t)inst[it] * H + j) >> 2));
+        else
+          dho = ldg4(dh_out + (int64_t)inst[it] * H + j);
         const __half* sv = reinterpret_cast<const __half*>(save + (int64_t)inst[it] * kSF) + H;
         cv = __ldg(reinterpret_cast<const uint2*>(sv + j));
         g0 = __ldg(reinterpret_cast<const uint4*>(sv + H + 4 * j));
         g1 = __ldg(reinterpret_cast<const uint4*>(sv + H + 4 * j + 8));
       } else {
-        dho = zero4();
+        if constexpr (DH16)
+          dho = make_uint2(0u, 0u);
+        else
+          dho = zero4();
         cv = make_uint2(0u, 0u);
         g0 = g1 = make_uint4(0u, 0u, 0u, 0u);
       }
@@ -1352,7 +1362,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
       const int p = L - 1 - t;
       const bool has_next = p + 1 < L;
       DGC_TS(blockIdx.x == 0 && threadIdx.x == 64 && t < 256, t, 0);
-      float4 dho[2][2];
+      DhoT dho[2][2];
       uint2 cvv[2][2];
       uint4 gv0[2][2], gv1[2][2];
       if (kHoist) {  // chunk 0 now; chunk 1's lines into L2 (loaded before chunk 1's math)
@@ -1453,7 +1463,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
           float4 da[4] = {zero4(), zero4(), zero4(), zero4()};
           float4 dcp = zero4();
           if (inst[it] >= 0) {
-            const float4 ho = dho[lc][it];
+            float4 ho;
+            if constexpr (DH16) {
+              const float2 a = u2h(dho[lc][it].x), b = u2h(dho[lc][it].y);
+              ho = make_float4(a.x * inv_scale, a.y * inv_scale, b.x * inv_scale, b.y * inv_scale);
+            } else {
+              ho = dho[lc][it];
+            }
             dh = make_float4(dh.x + ho.x, dh.y + ho.y, dh.z + ho.z, dh.w + ho.w);
             const float2 c01 = u2h(cvv[lc][it].x), c23 = u2h(cvv[lc][it].y);
             const float cin[4] = {c01.x, c01.y, c23.x, c23.y};
@@ -1565,7 +1581,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kVEW, 1)
   if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
 }
 
-template <int H, int EW>
+template <int H, int EW, bool DH16>
 int launch_lstm_bwd_tc2k_ew(const float* U, const int32_t* slot_row, const uint8_t* slot_mask,
                             int64_t R, int L, const float* save, const float* dh_out, float* dgx,
                             int rnd, float* bias_partial, int rq, float da_scale, int dgx16,
@@ -1573,7 +1589,7 @@ int launch_lstm_bwd_tc2k_ew(const float* U, const int32_t* slot_row, const uint8
   const size_t smem = (size_t)ks_a_stages<EW>() * BM * 128 + (size_t)4 * H * 128 +
                       (size_t)2 * 4 * ks_recv_rq<EW>() * (H / 2) * 4 + (size_t)EW * 8 * kKsStgStride * 4 +
                       1024 + 512;
-  auto kern = lstm_bwd_tc2k_kernel<H, EW>;
+  auto kern = lstm_bwd_tc2k_kernel<H, EW, DH16>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return dgc::cuda_fail(e, "lstm_bwd_tc2k: set smem");
   const int grid = 2 * (int)cluster_tiles(R);
@@ -1589,17 +1605,22 @@ int launch_lstm_bwd_tc2k_ew(const float* U, const int32_t* slot_row, const uint8
 // da_scale: power of two applied to da before its fp16 conversion (the MMA
 // operand) and removed exactly from the dh partials; sized by the caller to
 // the loss normalisation (mean over n instances: da ~ 1/n).
+// dh16: dh_out holds S * dh as fp16 (the fp16 readout / input-gradient GEMMs'
+// output), unscaled exactly at use
 template <int H>
 int launch_lstm_bwd_tc2k(const float* U, const int32_t* slot_row, const uint8_t* slot_mask,
                          int64_t R, int L, const float* save, const float* dh_out, float* dgx,
-                         int rnd, float* bias_partial, float da_scale, int dgx16, cudaStream_t s) {
+                         int rnd, float* bias_partial, float da_scale, int dgx16, int dh16,
+                         cudaStream_t s) {
   DGC_REQUIRE(R * (int64_t)L < (int64_t)INT32_MAX, "lstm_bwd_tc2k: R * L must fit int32");
   const int rq = cluster_rows_per_quadrant(R);
-  if (rq <= 24 && !getenv("DGC_RNN_EW16"))
-    return launch_lstm_bwd_tc2k_ew<H, 12>(U, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
-                                          bias_partial, rq, da_scale, dgx16, s);
-  return launch_lstm_bwd_tc2k_ew<H, 16>(U, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,
-                                        bias_partial, rq, da_scale, dgx16, s);
+  const bool ew12 = rq <= 24 && !getenv("DGC_RNN_EW16");
+#define DGC_BWD2K(EW, D16)                                                                       \
+  launch_lstm_bwd_tc2k_ew<H, EW, D16>(U, slot_row, slot_mask, R, L, save, dh_out, dgx, rnd,     \
+                                      bias_partial, rq, da_scale, dgx16, s)
+  if (dh16) return ew12 ? DGC_BWD2K(12, true) : DGC_BWD2K(16, true);
+  return ew12 ? DGC_BWD2K(12, false) : DGC_BWD2K(16, false);
+#undef DGC_BWD2K
 }
 
 // BPTT on the 2-SM tensor core (cta_group::2). Each CTA of the pair owns
@@ -2099,13 +2120,15 @@ extern "C" int dgc_rnn_bwd_tc(int32_t cell_flags, const float* U, const int32_t*
     case 32: return launch_lstm_bwd_tc<32>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
     case 64: return launch_lstm_bwd_tc<64>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
     case 128:
+      DGC_REQUIRE(!((cell_flags >> 25) & 1) || (cluster_rnn_enabled() && !bptt_2sm(n_rows)),
+                  "rnn_bwd_tc: an fp16 dh_out needs the K-split cluster BPTT");
       return cluster_rnn_enabled()
                  ? (bptt_2sm(n_rows) ? launch_lstm_bwd_tc2m<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, rnd,
                                                            bias_partial, ldexpf(1.f, (cell_flags >> 16) & 0x7f),
                                                            (cell_flags >> 24) & 1, s)
                                : launch_lstm_bwd_tc2k<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, rnd,
                                                            bias_partial, ldexpf(1.f, (cell_flags >> 16) & 0x7f),
-                                                           (cell_flags >> 24) & 1, s))
+                                                           (cell_flags >> 24) & 1, (cell_flags >> 25) & 1, s))
                  : launch_lstm_bwd_tc<128>(U, slot_row, slot_mask, n_rows, row_len, save, dh_out, dgx, dc_scratch, rnd, bias_partial, s);
     default: return dgc::fail(DGC_ERR_ARG, "rnn_bwd_tc: H must be 32, 64 or 128");
   }

@@ -408,7 +408,12 @@ def rnn_bwd_tc(cell, U, slot_row, slot_mask, n_rows, row_len, H, save, dh_out, d
     """K4 BPTT on tcgen05 (dgc_rnn_bwd_tc): dh = da U^T on tensor cores. An fp16
     dgx (H = 128 cluster kernel, cell bit 24) receives S * dgx, S = 2^(cell bits
     16..22): the operand of the fp16 weight-gradient GEMMs."""
-    _req(dh_out, torch.float32, "dh_out")
+    dh16 = dh_out.dtype == torch.float16
+    if dh16:  # S * dh as fp16 (S = the dgx scale): the K-split cluster BPTT only
+        _req16(dh_out, "dh_out")
+        cell |= 1 << 25
+    else:
+        _req(dh_out, torch.float32, "dh_out")
     f16 = dgx.dtype == torch.float16
     if f16:
         _req16(dgx, "dgx")
@@ -421,7 +426,8 @@ def rnn_bwd_tc(cell, U, slot_row, slot_mask, n_rows, row_len, H, save, dh_out, d
     # reads the saved c_in, i, f, g, o (fp16 in the H = 128 cluster kernel, which
     # recomputes tanh(c); fp32 + tanh(c) otherwise) and dh; writes dgx
     saved_bytes = 2 * 5 * H if rnn_tc_save_floats(H) < 7 * H else 4 * 6 * H
-    nb = (n_inst * ((2 if f16 else 4) * G * H + saved_bytes + 4 * H) + 5 * n_rows * row_len
+    nb = (n_inst * ((2 if f16 else 4) * G * H + saved_bytes + (2 if dh16 else 4) * H)
+          + 5 * n_rows * row_len
           + 4 * G * H * H)
     _run("lstm_bwd_tc", lambda: _native.check(
         _native.lib().dgc_rnn_bwd_tc(cell, _p(U), _p(slot_row), _p(slot_mask), n_rows, row_len, H,

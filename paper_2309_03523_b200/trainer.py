@@ -299,6 +299,14 @@ class Shard:
             self.dlogits16 = torch.zeros((n, cfg.C), dtype=torch.float16, device=dev)
         if self.f16_bwd:
             self.dgx = torch.zeros((n, GH), dtype=torch.float16, device=dev)
+        # fp16 LSTM output gradients: with the fp16 readout the dh the BPTT reads
+        # (readout dh = dlogits16 Wo16^T, layer k's dx = dgx16 Wx16^T for layer k-1)
+        # leaves its GEMM as S-scaled fp16 (S dh, the same scale as dgx16) instead
+        # of fp32: half the bytes written and read back per LSTM layer
+        self.dh16 = None
+        if (self.f16_bwd and self.f16_readout and not evolve
+                and not os.environ.get("DGC_BPTT_2SM") and os.environ.get("DGC_DH16", "1") != "0"):
+            self.dh16 = [torch.zeros((n, H), dtype=torch.float16, device=dev) for _ in range(2)]
         self.params16 = None
         if self.f16_bwd or self.f16_readout:
             # fp16 mirror of the (TF32-rounded) parameters: the fp16 GEMMs' weights
@@ -666,6 +674,10 @@ class Shard:
                          ldb=cfg.C, alpha=self.inv_da_scale, relu16=self.h2_16,
                          colsum_partial=self.bp_b[1])
             rjobs.append((self.bp_b[1], 4 * self.m_tiles, H, self.g("b2")))
+        elif f16r and self.dh16 is not None:  # S dh as fp16 (the BPTT unscales it)
+            ops.gemm_f16(self.dlogits16, self.p16("Wo"), None, n, H, cfg.C, b_mn=False,
+                         ldb=cfg.C, alpha=self.inv_da_scale, C16=self.dh16[0],
+                         c16_scale=2.0 ** self.da_exp)
         elif f16r:
             ops.gemm_f16(self.dlogits16, self.p16("Wo"), self.dh, n, H, cfg.C, b_mn=False,
                          ldb=cfg.C, alpha=self.inv_da_scale)
@@ -681,8 +693,8 @@ class Shard:
                 # the H = 128 cluster BPTT multiplies fp16 S*da by resident fp16 U:
                 # S = 2^round(log2 n_total) lifts da ~ 1/n_total into fp16's normal range
                 ops.rnn_bwd_tc(cell | rflag | (self.da_exp << 16), self.pr(f"U{k}"), self.slot_row,
-                               self.slot_mask,
-                               self.R, self.L, H, self.save[k], self.dh, self.dgx,
+                               self.slot_mask, self.R, self.L, H, self.save[k],
+                               self.dh16[0] if self.dh16 is not None else self.dh, self.dgx,
                                self.rnn_dc_scratch, bias_partial=self.bp_r[k])
                 rjobs.append((self.bp_r[k], self.rnn_tc_prows, GH, self.g(f"br{k}")))
             else:
@@ -735,6 +747,10 @@ class Shard:
                              alpha=self.inv_da_scale, relu16=self.x16[0],
                              colsum_partial=self.bp_b[1], C16=self.dZ2_16,
                              c16_scale=2.0 ** self.da_exp)
+            elif self.f16_bwd and self.dh16 is not None and k > 0:  # S dx as fp16
+                ops.gemm_f16(self.dgx, self.p16(f"Wx{k}"), None, n, H, GH, b_mn=False, ldb=GH,
+                             alpha=self.inv_da_scale, C16=self.dh16[1],
+                             c16_scale=2.0 ** self.da_exp)
             elif self.f16_bwd:
                 ops.gemm_f16(self.dgx, self.p16(f"Wx{k}"), self.dh2, n, H, GH, b_mn=False, ldb=GH,
                              alpha=self.inv_da_scale, relu_src=relu_src,
@@ -750,6 +766,8 @@ class Shard:
             if k == 0:  # dZ2 = dH2 * (H2 > 0): its column sums are the b2 gradient
                 rjobs.append((self.bp_b[1], 4 * self.m_tiles, H, self.g("b2")))
             self.dh, self.dh2 = self.dh2, self.dh
+            if self.dh16 is not None:
+                self.dh16.reverse()
         dZ = self.dh  # = dH2 * (H2 > 0), fused into the last GEMM epilogue
         for l in (1, 0):
             W, b = ("W1", "b1") if l == 0 else ("W2", "b2")

@@ -738,6 +738,43 @@ def test_lstm_bwd_tensor_core_matches_simt(H, variant, n_seq, monkeypatch):
     close(outs[1][1], outs[0][1], 3e-3, "lstm bwd tc bias")
 
 
+@pytest.mark.parametrize("variant,dgx16", [("", False), ("", True), ("ew16", True)])
+def test_lstm_bwd_tc_f16_dh_out_equals_fp32(variant, dgx16, monkeypatch):
+    """K-split cluster BPTT with an S-scaled fp16 dh_out (cell bit 25, the fp16
+    readout / input-gradient GEMMs' output) is bitwise the fp32-dh_out kernel
+    fed the same values (fp16(S dh) / S is exact in fp32)."""
+    if variant == "ew16":
+        monkeypatch.setenv("DGC_RNN_EW16", "1")
+    from paper_2309_03523_b200 import ops
+    from paper_2309_03523_b200.layout import pack_sequences_native
+    H, e = 128, 12
+    rng = np.random.default_rng(5)
+    lengths = rng.integers(1, 20, size=900)
+    seq, pos, mask, _ = pack_sequences_native(lengths)
+    R, L = seq.shape
+    offs = np.concatenate([[0], np.cumsum(lengths)])
+    n = int(offs[-1])
+    slot_row = np.where(seq >= 0, offs[np.maximum(seq, 0)] + pos, -1).astype(np.int32).reshape(-1)
+    U = (rng.standard_normal((H, 4 * H)) / np.sqrt(H)).astype(np.float32)
+    save = np.concatenate([rng.standard_normal((n, 2 * H)), rng.random((n, 4 * H)),
+                           np.zeros((n, H))], 1).astype(np.float32)
+    dh16 = (rng.standard_normal((n, H)) / 64).astype(np.float16)  # S dh
+    dh32 = dh16.astype(np.float32) / np.float32(2.0 ** e)
+    sr, sm = t(slot_row, torch.int32), t(mask.reshape(-1), torch.uint8)
+    sv = t(tc_save_encode(save, H))
+    outs = []
+    for d in (t(dh32), torch.as_tensor(dh16).to(dev)):
+        dgx = torch.zeros((n, 4 * H), device=dev, dtype=torch.float16 if dgx16 else torch.float32)
+        bp = torch.zeros((ops.rnn_tc_tiles(R, H), 4 * H), device=dev)
+        scr = torch.zeros(((R + 127) // 128 * 128, H), device=dev)
+        ops.rnn_bwd_tc(1 | (e << 16), t(U), sr, sm, R, L, H, sv, d, dgx, scr, bias_partial=bp)
+        torch.cuda.synchronize()
+        outs.append((dgx.float().cpu().numpy(), bp.cpu().numpy()))
+    assert np.abs(outs[0][0]).max() > 0
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
+
+
 def test_tf32x24_input_pipeline_is_bit_exact():
     """Host pack (round-to-nearest-away to TF32, keep 3 bytes) + device unpack
     equals the device's cvt.rna.tf32 rounding of the fp32 values, bit for bit,

@@ -1,4 +1,4 @@
-"""K1 SpMM variants (DGC_SPMM_MODE, read once per process) on a plan's CSR:
+"""K1 SpMM variants (DGC_SPMM_STREAM / DGC_SPMM_MODE, read once per process) on a plan's CSR:
 fp16-row (dgc_spmm_csr_h) and fp32-row (dgc_spmm_csr) launches, CUDA events,
 L2 flushed per launch; prints us per launch and a hash of the output (the
 variants must agree bitwise). usage: python tools/time_spmm_modes.py c2|c3 [W]"""
@@ -53,17 +53,17 @@ def h(*ts):
     return m.hexdigest()[:12]
 
 
-mode = os.environ.get("DGC_SPMM_MODE", "2")
+mode = os.environ.get("DGC_SPMM_STREAM", os.environ.get("DGC_SPMM_MODE", "-"))
 runh = lambda: _native.check(lib.dgc_spmm_csr_h(rp.data_ptr(), col.data_ptr(), dinv.data_ptr(),
                                                 Y16.data_ptr(), bias.data_ptr(), None, o16.data_ptr(),
                                                 1.0, n, W, 1, work.data_ptr(), None), "spmm_h")
 t = t_of(runh)
-print(f"{cfg} mode {mode:>2} fp16 rows W={W} n={n} nnz={nnz}: {t:7.1f} us  "
+print(f"{cfg} mode {mode:>3} fp16 rows W={W} n={n} nnz={nnz}: {t:7.1f} us  "
       f"{nnz / t / 1e3:6.2f} G nbr rows/s  hash {h(o16)}")
 runf = lambda: _native.check(lib.dgc_spmm_csr_x(rp.data_ptr(), col.data_ptr(), dinv.data_ptr(),
                                                 Y.data_ptr(), bias.data_ptr(), out.data_ptr(), None,
                                                 None, n, 0, W, 1, work.data_ptr(), 1.0, None), "spmm_x")
 t = t_of(runf)
 alg = 8 * W * n + 4 * (n + 1) + 4 * nnz + 4 * n
-print(f"{cfg} mode {mode:>2} fp32 rows W={W}: {t:7.1f} us  alg {alg / t / 1e3:6.0f} GB/s  "
+print(f"{cfg} mode {mode:>3} fp32 rows W={W}: {t:7.1f} us  alg {alg / t / 1e3:6.0f} GB/s  "
       f"{nnz / t / 1e3:6.2f} G nbr rows/s  hash {h(out)}")
