@@ -8,7 +8,7 @@ NVFLAGS += -DDGC_LSTM_TIMESTAMPS
 endif
 SRC := paper_2309_03523_b200/csrc
 OUT := paper_2309_03523_b200/lib
-CU := common spmm stale exchange dense rnn gemm_tc rnn_tc evolve
+CU := common spmm stale exchange dense rnn gemm_tc rnn_tc evolve readout_tc
 OBJS := $(addprefix build/,$(addsuffix .o,$(CU))) build/layout.o build/fusion_plan.o build/propagate.o build/generate.o
 
 all: $(OUT)/libdgc_b200.so

@@ -453,6 +453,20 @@ int dgc_softmax_xent(const float* logits, const int32_t* labels, int64_t n, int3
 int dgc_softmax_xent_f16(const float* logits, const int32_t* labels, int64_t n, int32_t C,
                          float scale, float* dlogits, double* loss_partial, float* dl_partial,
                          void* dlogits16, float scale16, void* stream);
+/* Fused fp16 readout (LSTM model, H = 128, C in {16, 32}), one persistent
+ * tcgen05 launch over 128-row tiles of h16 [n, H] (fp16, 16-B aligned rows):
+ * logits = h16 Wo16 + bo (Wo16 [H, C] fp16, bo fp32), softmax cross-entropy
+ * with labels (y < 0: padding), dlogits = scale (softmax - onehot); writes
+ * dh16 [n, H] = fp16(scale16 * dlogits Wo^T) (the S-scaled input of
+ * dgc_rnn_bwd_tc bit 25), loss_partial [ceil(n/128)] (fp64 per tile),
+ * dl_partial [ceil(n/128), C] (dlogits column sums per tile: the bo gradient)
+ * and dwo_partial [dgc_readout_f16_grid(n), H, C] (per-CTA dWo sums; reduce the
+ * rows with dgc_reduce_rows). Replaces logits GEMM + dgc_softmax_xent_f16 +
+ * dWo GEMM + dh GEMM (sim.py:323-324's loss, restated in oracle/dgnn.py). */
+int dgc_readout_f16(const void* h16, const void* Wo16, const float* bo, const int32_t* labels,
+                    int64_t n, int32_t H, int32_t C, float scale, float scale16, void* dh16,
+                    double* loss_partial, float* dl_partial, float* dwo_partial, void* stream);
+int32_t dgc_readout_f16_grid(int64_t n);
 /* out[j] (+)= sum_r partial[r, j] in fixed row order (deterministic). */
 int dgc_reduce_rows(const float* partial, int64_t rows, int32_t width, float* out,
                     int32_t accumulate, void* stream);

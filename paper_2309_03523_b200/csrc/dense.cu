@@ -450,6 +450,9 @@ __global__ void __launch_bounds__(256) reduce_rows_stage1(const float* __restric
 // stage 1 = reduce_rows_stage1 over every job's (32-column block, slab) pairs,
 // stage 2 = colsum_stage2 over every job's column blocks; same fixed order as
 // dgc_reduce_rows, so the results are bitwise those of separate calls.
+// slabs of a row reduction: 8 rows per slab up to 2048 rows (one-row slabs made
+// stage 1 a copy: 148 x 2048 dWo partials took ~11 us), 256 slabs beyond
+inline int64_t rr_slabs(int64_t rows) { return rows <= 2048 ? (rows + 7) / 8 : 256; }
 constexpr int kRRMaxJobs = 8;
 struct RRJobs {
   const float* in[kRRMaxJobs];
@@ -521,7 +524,7 @@ extern "C" int dgc_reduce_rows_batched(int32_t n_jobs, const float* const* parti
     J.out[j] = outs[j];
     J.rows[j] = rows[j];
     J.width[j] = widths[j];
-    int64_t slabs = rows[j] < 256 ? rows[j] : 256;  // as dgc_reduce_rows
+    int64_t slabs = rr_slabs(rows[j]);  // as dgc_reduce_rows
     const int64_t slab = (rows[j] + slabs - 1) / slabs;
     slabs = (rows[j] + slab - 1) / slab;
     J.slab[j] = slab;
@@ -556,7 +559,7 @@ extern "C" int dgc_reduce_rows(const float* partial, int64_t rows, int32_t width
   // slab partials live in a small static scratch (<= 256 slabs x 4096 columns)
   static float* scratch = nullptr;
   static size_t scratch_n = 0;
-  int64_t slabs = rows < 256 ? (rows > 0 ? rows : 1) : 256;
+  int64_t slabs = rr_slabs(rows > 0 ? rows : 1);
   if (slabs * width > 256 * 4096) return dgc::fail(DGC_ERR_ARG, "reduce_rows: width too large");
   if (!scratch) {
     scratch_n = 256 * 4096;

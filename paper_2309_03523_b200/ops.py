@@ -544,6 +544,32 @@ def softmax_xent(logits, labels, C, scale, dlogits, loss_partial, round_tf32=Fal
         _p(loss_partial), _p(dl_partial), _stream()), "dgc_softmax_xent"), n * (8 * C + 4))
 
 
+def readout_f16_grid(n):
+    """CTAs (= rows of the dWo partial) of dgc_readout_f16 for n instances."""
+    return int(_native.lib().dgc_readout_f16_grid(int(n)))
+
+
+def readout_f16(h16, Wo16, bo, labels, C, scale, scale16, dh16, loss_partial, dl_partial,
+                dwo_partial):
+    """Fused fp16 readout (dgc_readout_f16): logits = h16 Wo16 + bo, softmax
+    cross-entropy, S dh = (S dlogits16) Wo16^T as fp16, per-tile loss and bo
+    partials, per-CTA dWo partials -- one tcgen05 launch."""
+    n, H = h16.shape
+    _req16(h16, "h16"); _req16(Wo16, "Wo16"); _req16(dh16, "dh16")
+    _req(bo, torch.float32, "bo"); _req(labels, torch.int32, "labels")
+    _req(loss_partial, torch.float64, "loss_partial"); _req(dl_partial, torch.float32, "dl_partial")
+    _req(dwo_partial, torch.float32, "dwo_partial")
+    tiles, grid = (n + 127) // 128, readout_f16_grid(n)
+    if loss_partial.numel() < tiles or dl_partial.numel() < tiles * C or dwo_partial.numel() < grid * H * C:
+        raise ValueError("readout_f16: partial buffers too small")
+    # h16 read once, dh16 written, labels; the weights once per CTA
+    nb = n * (2 * H + 2 * H + 4) + grid * (2 * H * C + 4 * H * C) + tiles * (8 + 4 * C)
+    _run("readout_f16", lambda: _native.check(_native.lib().dgc_readout_f16(
+        _p(h16), _p(Wo16), _p(bo), _p(labels), n, H, C, float(scale), float(scale16), _p(dh16),
+        _p(loss_partial), _p(dl_partial), _p(dwo_partial), _stream()), "dgc_readout_f16"),
+        nb, 2.0 * n * H * C * 3)
+
+
 def pack_tf32x24(x: np.ndarray) -> np.ndarray:
     """Host side of the TF32 input pipeline: round fp32 values to TF32 (round to
     nearest, ties away: cvt.rna.tf32) and keep the top three bytes of each

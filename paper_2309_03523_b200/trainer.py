@@ -307,6 +307,16 @@ class Shard:
         if (self.f16_bwd and self.f16_readout and not evolve
                 and not os.environ.get("DGC_BPTT_2SM") and os.environ.get("DGC_DH16", "1") != "0"):
             self.dh16 = [torch.zeros((n, H), dtype=torch.float16, device=dev) for _ in range(2)]
+        # fused fp16 readout (dgc_readout_f16): logits, softmax-xent, S dh and dWo in
+        # one tcgen05 launch that reads h16 once (replaces 4 launches)
+        self.fused_readout = bool(self.dh16 is not None and H == 128 and cfg.C in (16, 32)
+                                  and cfg.n_rnn > 0 and os.environ.get("DGC_FUSED_READOUT", "1") != "0")
+        if self.fused_readout:
+            ro_tiles = max(1, (n + 127) // 128)
+            self.loss_partial = torch.zeros(ro_tiles, dtype=torch.float64, device=dev)
+            self.dl_partial = torch.zeros(ro_tiles * cfg.C, **f32)
+            self.ro_grid = ops.readout_f16_grid(max(n, 1))
+            self.dwo_partial = torch.zeros(self.ro_grid * H * cfg.C, **f32)
         self.params16 = None
         if self.f16_bwd or self.f16_readout:
             # fp16 mirror of the (TF32-rounded) parameters: the fp16 GEMMs' weights
@@ -323,7 +333,8 @@ class Shard:
         # the gradient tensors, reduced in fixed order by dgc_reduce_rows)
         self.m_tiles = max(1, (n + 127) // 128)
         self.rnn_prows = ops.rnn_bwd_partial_rows(self.R, H) if self.R else 1
-        self.dl_partial = torch.zeros(max(1, (n + 255) // 256) * cfg.C, **f32)
+        if not getattr(self, "fused_readout", False):
+            self.dl_partial = torch.zeros(max(1, (n + 255) // 256) * cfg.C, **f32)
         prows = max(self.rnn_prows, ops.rnn_tc_tiles(max(self.R, 1), H))
         # one partial buffer per bias gradient: their fixed-order reductions run
         # together at the end of the backward (dgc_reduce_rows_batched, 2 launches)
@@ -648,7 +659,11 @@ class Shard:
             xr, ldx = hb, self.hw
         # ---------------- readout + loss ----------------
         f16r = self.f16_readout and (cfg.n_rnn > 0 or self.evolve)
-        if f16r:
+        if self.fused_readout:  # logits, loss, S dh (into dh16[0]) and dWo partials
+            ops.readout_f16(self.x16[cfg.n_rnn], self.p16("Wo"), self.p("bo"), self.y, cfg.C,
+                            1.0 / self.n_total, 2.0 ** self.da_exp, self.dh16[0], self.loss_partial,
+                            self.dl_partial, self.dwo_partial)
+        elif f16r:
             xr16 = self.h2_16 if self.evolve else self.x16[cfg.n_rnn]
             ops.gemm_f16(xr16, self.p16("Wo"), self.logits, n, cfg.C, H, lda=H, bias=self.p("bo"))
             ops.softmax_xent(self.logits, self.y, cfg.C, 1.0 / self.n_total, None,
@@ -662,18 +677,26 @@ class Shard:
         # ---------------- backward ----------------
         self.grads.zero_()
         ks, part = self.ksplit, self.partial
-        if f16r:
+        if self.fused_readout:
+            pass  # dWo partials came with the forward readout (reduced below)
+        elif f16r:
             ops.gemm_f16(xr16, self.dlogits16, self.g("Wo"), H, cfg.C, n, a_mn=True, lda=H,
                          alpha=self.inv_da_scale, k_splits=ks, partial=part)
         else:
             ops.gemm(xr, self.dlogits, self.g("Wo"), H, cfg.C, n, a_mn=True, lda=ldx,
                      precision=prec, k_splits=ks, partial=part)
-        rjobs = [(self.dl_partial, max(1, (n + 255) // 256), cfg.C, self.g("bo"))]
+        if self.fused_readout:
+            rjobs = [(self.dl_partial, max(1, (n + 127) // 128), cfg.C, self.g("bo")),
+                     (self.dwo_partial, self.ro_grid, H * cfg.C, self.g("Wo"))]
+        else:
+            rjobs = [(self.dl_partial, max(1, (n + 255) // 256), cfg.C, self.g("bo"))]
         if f16r and self.evolve:  # dZ2 = (dlogits Wo^T) * (H2 > 0), b2 fused
             ops.gemm_f16(self.dlogits16, self.p16("Wo"), self.dh, n, H, cfg.C, b_mn=False,
                          ldb=cfg.C, alpha=self.inv_da_scale, relu16=self.h2_16,
                          colsum_partial=self.bp_b[1])
             rjobs.append((self.bp_b[1], 4 * self.m_tiles, H, self.g("b2")))
+        elif self.fused_readout:
+            pass  # S dh16 came with the forward readout
         elif f16r and self.dh16 is not None:  # S dh as fp16 (the BPTT unscales it)
             ops.gemm_f16(self.dlogits16, self.p16("Wo"), None, n, H, cfg.C, b_mn=False,
                          ldb=cfg.C, alpha=self.inv_da_scale, C16=self.dh16[0],

@@ -775,6 +775,52 @@ def test_lstm_bwd_tc_f16_dh_out_equals_fp32(variant, dgx16, monkeypatch):
     assert np.array_equal(outs[0][1], outs[1][1])
 
 
+@pytest.mark.parametrize("n,C", [(300, 16), (5000, 16), (2049, 32), (40000, 16)])
+def test_fused_readout_f16_matches_fp64(n, C):
+    """dgc_readout_f16 (logits GEMM + softmax-xent + S dh + dWo in one tcgen05
+    launch) vs an fp64 restatement on the same fp16 operands: loss, bo / Wo
+    gradients and the S-scaled fp16 dh; ragged last tile and padding labels."""
+    from paper_2309_03523_b200 import ops
+    H, e = 128, 13
+    S = 2.0 ** e
+    rng = np.random.default_rng(n + C)
+    h16 = rng.standard_normal((n, H)).astype(np.float16)
+    Wo16 = (rng.standard_normal((H, C)) / np.sqrt(H)).astype(np.float16)
+    bo = (0.1 * rng.standard_normal(C)).astype(np.float32)
+    y = rng.integers(0, C, size=n).astype(np.int32)
+    y[rng.random(n) < 0.1] = -1  # padding rows
+    scale = 1.0 / n
+    tiles, grid = (n + 127) // 128, ops.readout_f16_grid(n)
+    dh16 = torch.zeros((n, H), device=dev, dtype=torch.float16)
+    lp = torch.zeros(tiles, device=dev, dtype=torch.float64)
+    dp = torch.zeros(tiles * C, device=dev)
+    wp = torch.zeros(grid * H * C, device=dev)
+    ops.readout_f16(torch.as_tensor(h16).to(dev), torch.as_tensor(Wo16).to(dev), t(bo),
+                    t(y, torch.int32), C, scale, S, dh16, lp, dp, wp)
+    gWo = torch.zeros(H * C, device=dev)
+    gbo = torch.zeros(C, device=dev)
+    ops.reduce_rows_batched([(dp, tiles, C, gbo), (wp, grid, H * C, gWo)])
+    torch.cuda.synchronize()
+    # fp64 reference on the same fp16 operands
+    hd, Wd = h16.astype(np.float64), Wo16.astype(np.float64)
+    z = hd @ Wd + bo.astype(np.float64)
+    z -= z.max(1, keepdims=True)
+    p = np.exp(z) / np.exp(z).sum(1, keepdims=True)
+    real = y >= 0
+    loss = -np.log(p[np.arange(n)[real], y[real]]).sum()
+    dl = p.copy()
+    dl[np.arange(n)[real], y[real]] -= 1.0
+    dl[~real] = 0.0
+    dl *= scale
+    dl16 = (dl * S).astype(np.float16).astype(np.float64)
+    dh_ref = dl16 @ Wd.T
+    dWo_ref = hd.T @ dl16 / S
+    assert abs(lp.sum().item() - loss) <= 1e-5 * abs(loss)
+    close(gbo.cpu().numpy(), dl.sum(0), 1e-4, "bo grad")
+    close(gWo.cpu().numpy().reshape(H, C), dWo_ref, 5e-3, "Wo grad")
+    close(dh16.float().cpu().numpy(), dh_ref, 5e-3, "S dh16")
+
+
 def test_tf32x24_input_pipeline_is_bit_exact():
     """Host pack (round-to-nearest-away to TF32, keep 3 bytes) + device unpack
     equals the device's cvt.rna.tf32 rounding of the fp32 values, bit for bit,
