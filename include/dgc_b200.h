@@ -458,8 +458,9 @@ int dgc_softmax_xent_f16(const float* logits, const int32_t* labels, int64_t n, 
  * logits = h16 Wo16 + bo (Wo16 [H, C] fp16, bo fp32), softmax cross-entropy
  * with labels (y < 0: padding), dlogits = scale (softmax - onehot); writes
  * dh16 [n, H] = fp16(scale16 * dlogits Wo^T) (the S-scaled input of
- * dgc_rnn_bwd_tc bit 25), loss_partial [ceil(n/128)] (fp64 per tile),
- * dl_partial [ceil(n/128), C] (dlogits column sums per tile: the bo gradient)
+ * dgc_rnn_bwd_tc bit 25), loss_partial [4 ceil(n/128)] (fp64 per tile and TMEM
+ * lane quadrant), dl_partial [4 ceil(n/128), C] (dlogits column sums per tile
+ * and quadrant: the bo gradient)
  * and dwo_partial [dgc_readout_f16_grid(n), H, C] (per-CTA dWo sums; reduce the
  * rows with dgc_reduce_rows). Replaces logits GEMM + dgc_softmax_xent_f16 +
  * dWo GEMM + dh GEMM (sim.py:323-324's loss, restated in oracle/dgnn.py). */

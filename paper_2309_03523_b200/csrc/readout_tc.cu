@@ -12,9 +12,9 @@
 // MMA 2) and transposed (K-major B of MMA 3). It replaces four launches of the
 // unfused path (logits GEMM, dgc_softmax_xent_f16, the dWo split-K GEMM and the
 // dh GEMM) and their round trips of logits / dlogits through HBM. The loss and
-// the dlogits column sums (the bo gradient) leave as per-tile partials and the
-// dWo accumulator as one per-CTA partial; dgc_epoch_finish / dgc_reduce_rows
-// reduce them in fixed order (deterministic).
+// the dlogits column sums (the bo gradient) leave as partials per (tile, TMEM
+// lane quadrant) and the dWo accumulator as one partial per CTA;
+// dgc_epoch_finish / dgc_reduce_rows reduce them in fixed order (deterministic).
 //
 // Replaces: the synthetic readout + loss of the reference's simulated epoch
 // (sim.py:323-324, restated in oracle/dgnn.py); S = 2^e is the trainer's
@@ -49,6 +49,29 @@ __device__ __forceinline__ void sts_b16(uint32_t addr, __half v) {
   asm volatile("st.shared.b16 [%0], %1;" ::"r"(addr), "h"(__half_as_ushort(v)) : "memory");
 }
 
+// one level of a butterfly column-sum over the warp: keep W/2 of the lane's W
+// column partials, exchange the other half with lane ^ OFF; once a lane holds
+// one column, the remaining levels sum it plainly
+template <int W, int OFF>
+__device__ __forceinline__ void butterfly_colsum(float* v, int lane, int& col) {
+  if constexpr (OFF >= 1) {
+    if constexpr (W > 1) {
+      const bool up = (lane & OFF) != 0;
+#pragma unroll
+      for (int j = 0; j < W / 2; ++j) {
+        const float send = up ? v[j] : v[j + W / 2];
+        const float keep = up ? v[j + W / 2] : v[j];
+        v[j] = keep + __shfl_xor_sync(0xffffffffu, send, OFF);
+      }
+      col += up ? W / 2 : 0;
+      butterfly_colsum<W / 2, OFF / 2>(v, lane, col);
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], OFF);
+      butterfly_colsum<1, OFF / 2>(v, lane, col);
+    }
+  }
+}
+
 template <int C>
 __global__ void __launch_bounds__(kThreads, 1)
     readout_f16_kernel(const __grid_constant__ CUtensorMap tmH, const __half* __restrict__ Wo16,
@@ -65,10 +88,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sDlA = sWo + kH * 128;                       // MMA 2 A: [128 rows][128 B] (k < C used)
   uint8_t* sDlT = sDlA + BM * 128;                      // MMA 3 B: [2 k-blocks][C rows][128 B]
   uint8_t* sStg = sDlT + 2 * C * 128;                   // dh staging [8 warps][32 rows][144 B]
-  // per-warp partials, double-buffered by tile parity
-  float* sRedC = reinterpret_cast<float*>(sStg + 8 * 32 * kStgStride);  // [2][4][C]
-  double* sRedL = reinterpret_cast<double*>(sRedC + 8 * C);             // [2][4]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sRedL + 8);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + 8 * 32 * kStgStride);
   uint64_t* empty = full + kStages;
   uint64_t* acc1_full = empty + kStages;
   uint64_t* acc1_empty = acc1_full + 1;
@@ -182,7 +202,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else if (warp < 6) {
     const int q = warp & 3;  // TMEM lane quadrant
-    const int ew = warp - 2;
     const int rl = 32 * q + lane;  // this thread's instance row in the tile
     const uint32_t tq = tmem_base + ((uint32_t)(32 * q) << 16);
     const uint32_t dlA = smem_u32(sDlA), dlT = smem_u32(sDlT);
@@ -190,9 +209,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int c = 0; c < C; ++c) bov[c] = __ldg(bo + c);
     int i = 0;
+    // labels one tile ahead (their load latency was exposed before every softmax)
+    int y_next = (int64_t)blockIdx.x * BM + rl < n ? __ldg(labels + (int64_t)blockIdx.x * BM + rl) : -1;
     for (int t = blockIdx.x; t < m_tiles; t += gridDim.x, ++i) {
       const int64_t row = (int64_t)t * BM + rl;
-      const int y = row < n ? __ldg(labels + row) : -1;  // y < 0: padding (no loss, no gradient)
+      const int y = y_next;  // y < 0: padding (no loss, no gradient)
+      {
+        const int64_t nrow = row + (int64_t)gridDim.x * BM;
+        y_next = (t + (int)gridDim.x < m_tiles && nrow < n) ? __ldg(labels + nrow) : -1;
+      }
       mbar_wait(acc1_full, i & 1);
       fence_after();
       float x[C];
@@ -251,24 +276,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(dl_ready);
-      // per-tile loss and dlogits column sums (the bo gradient), fixed order
+      // loss and dlogits column sums (the bo gradient) per (tile, lane quadrant):
+      // no barrier among the softmax warps; the partial rows are reduced in fixed order
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-      float* rc = sRedC + (i & 1) * 4 * C;
-      double* rl2 = sRedL + (i & 1) * 4;
+      if (lane == 0) loss_partial[4 * (int64_t)t + q] = l;
+      {
+        // butterfly: each level halves the columns a lane keeps (C - 1 shuffles
+        // for C <= 32 instead of 5 C); the lane ends with column col
+        float v[C];
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        float v = x[c];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) rc[q * C + c] = v;
-      }
-      if (lane == 0) rl2[q] = l;
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (ew == 0) {  // quadrants in fixed order 0..3
-        if (lane == 0) loss_partial[t] = rl2[0] + rl2[1] + rl2[2] + rl2[3];
-        if (lane < C)
-          dl_partial[(int64_t)t * C + lane] = rc[lane] + rc[C + lane] + rc[2 * C + lane] + rc[3 * C + lane];
+        for (int c = 0; c < C; ++c) v[c] = x[c];
+        int col = 0;
+        butterfly_colsum<C, 16>(v, lane, col);
+        if (C == 32 || (lane & 1) == 0) dl_partial[(4 * (int64_t)t + q) * C + col] = v[0];
       }
     }
     // the launch's S dWo accumulator: lane = hidden unit, C columns -> partial / S
@@ -344,7 +365,7 @@ int launch_readout(const void* h16, const void* Wo16, const float* bo, const int
   if (rc != DGC_OK) return rc;
   const int m_tiles = (int)((n + BM - 1) / BM);
   const size_t smem = 1024 + (size_t)kStages * kTileBytes + 2 * C * 128 + kH * 128 + BM * 128 +
-                      2 * C * 128 + 8 * 32 * kStgStride + 8 * C * 4 + 8 * 8 + 16 * 8 + 16;
+                      2 * C * 128 + 8 * 32 * kStgStride + 16 * 8 + 16;
   auto kern = readout_f16_kernel<C>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return dgc::cuda_fail(e, "readout_f16: set smem");

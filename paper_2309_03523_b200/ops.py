@@ -552,14 +552,15 @@ def readout_f16_grid(n):
 def readout_f16(h16, Wo16, bo, labels, C, scale, scale16, dh16, loss_partial, dl_partial,
                 dwo_partial):
     """Fused fp16 readout (dgc_readout_f16): logits = h16 Wo16 + bo, softmax
-    cross-entropy, S dh = (S dlogits16) Wo16^T as fp16, per-tile loss and bo
-    partials, per-CTA dWo partials -- one tcgen05 launch."""
+    cross-entropy, S dh = (S dlogits16) Wo16^T as fp16, loss and bo partials per
+    (128-row tile, TMEM lane quadrant) [4 ceil(n/128)], per-CTA dWo partials --
+    one tcgen05 launch."""
     n, H = h16.shape
     _req16(h16, "h16"); _req16(Wo16, "Wo16"); _req16(dh16, "dh16")
     _req(bo, torch.float32, "bo"); _req(labels, torch.int32, "labels")
     _req(loss_partial, torch.float64, "loss_partial"); _req(dl_partial, torch.float32, "dl_partial")
     _req(dwo_partial, torch.float32, "dwo_partial")
-    tiles, grid = (n + 127) // 128, readout_f16_grid(n)
+    tiles, grid = 4 * ((n + 127) // 128), readout_f16_grid(n)  # partial rows per (tile, quadrant)
     if loss_partial.numel() < tiles or dl_partial.numel() < tiles * C or dwo_partial.numel() < grid * H * C:
         raise ValueError("readout_f16: partial buffers too small")
     # h16 read once, dh16 written, labels; the weights once per CTA

@@ -312,7 +312,7 @@ class Shard:
         self.fused_readout = bool(self.dh16 is not None and H == 128 and cfg.C in (16, 32)
                                   and cfg.n_rnn > 0 and os.environ.get("DGC_FUSED_READOUT", "1") != "0")
         if self.fused_readout:
-            ro_tiles = max(1, (n + 127) // 128)
+            ro_tiles = 4 * max(1, (n + 127) // 128)  # partial rows per (tile, lane quadrant)
             self.loss_partial = torch.zeros(ro_tiles, dtype=torch.float64, device=dev)
             self.dl_partial = torch.zeros(ro_tiles * cfg.C, **f32)
             self.ro_grid = ops.readout_f16_grid(max(n, 1))
@@ -686,7 +686,7 @@ class Shard:
             ops.gemm(xr, self.dlogits, self.g("Wo"), H, cfg.C, n, a_mn=True, lda=ldx,
                      precision=prec, k_splits=ks, partial=part)
         if self.fused_readout:
-            rjobs = [(self.dl_partial, max(1, (n + 127) // 128), cfg.C, self.g("bo")),
+            rjobs = [(self.dl_partial, 4 * max(1, (n + 127) // 128), cfg.C, self.g("bo")),
                      (self.dwo_partial, self.ro_grid, H * cfg.C, self.g("Wo"))]
         else:
             rjobs = [(self.dl_partial, max(1, (n + 255) // 256), cfg.C, self.g("bo"))]

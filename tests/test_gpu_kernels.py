@@ -790,7 +790,7 @@ def test_fused_readout_f16_matches_fp64(n, C):
     y = rng.integers(0, C, size=n).astype(np.int32)
     y[rng.random(n) < 0.1] = -1  # padding rows
     scale = 1.0 / n
-    tiles, grid = (n + 127) // 128, ops.readout_f16_grid(n)
+    tiles, grid = 4 * ((n + 127) // 128), ops.readout_f16_grid(n)  # (tile, quadrant) rows
     dh16 = torch.zeros((n, H), device=dev, dtype=torch.float16)
     lp = torch.zeros(tiles, device=dev, dtype=torch.float64)
     dp = torch.zeros(tiles * C, device=dev)
