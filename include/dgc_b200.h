@@ -468,6 +468,15 @@ int dgc_readout_f16(const void* h16, const void* Wo16, const float* bo, const in
                     int64_t n, int32_t H, int32_t C, float scale, float scale16, void* dh16,
                     double* loss_partial, float* dl_partial, float* dwo_partial, void* stream);
 int32_t dgc_readout_f16_grid(int64_t n);
+/* dgc_readout_f16 for EvolveGCN-O (readout input H2 = relu(.), fp16 copy h2_16):
+ * instead of S dh it writes dz2 [n, H] fp32 = dh * (H2 > 0) (the mask is the
+ * input tile itself) and b2_partial [4 ceil(n/128), H] = dz2 column sums per
+ * (tile, lane quadrant), the b2 gradient. Replaces the logits GEMM, the
+ * softmax, the dWo GEMM and the masked dZ2 GEMM of the EvolveGCN readout. */
+int dgc_readout_f16_evolve(const void* h2_16, const void* Wo16, const float* bo,
+                           const int32_t* labels, int64_t n, int32_t H, int32_t C, float scale,
+                           float scale16, float* dz2, float* b2_partial, double* loss_partial,
+                           float* dl_partial, float* dwo_partial, void* stream);
 /* out[j] (+)= sum_r partial[r, j] in fixed row order (deterministic). */
 int dgc_reduce_rows(const float* partial, int64_t rows, int32_t width, float* out,
                     int32_t accumulate, void* stream);

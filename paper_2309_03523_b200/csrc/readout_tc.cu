@@ -39,6 +39,7 @@ constexpr int kStages = 3;            // h16 tiles in flight
 constexpr int kTileBytes = BM * kH * 2;  // 32 KB: two [128 x 64] SWIZZLE_128B boxes
 constexpr int kStgStride = 144;       // dh staging row stride (bytes): conflict-free 16-B accesses
 constexpr int kThreads = 64 + 128 + 256;
+constexpr int kStgStrideEvo = 272;    // fp32 dZ2 staging: 32 rows x 64 floats + 16 B
 
 // byte offset of fp16 element (row, k) (k < 64) in a K-major SWIZZLE_128B tile
 __device__ __forceinline__ uint32_t sw128_h(int row, int k) {
@@ -72,13 +73,19 @@ __device__ __forceinline__ void butterfly_colsum(float* v, int lane, int& col) {
   }
 }
 
-template <int C>
+// EVO (EvolveGCN-O, whose readout input is H2 = relu(.)): the dh group writes
+// dZ2 = dh * (H2 > 0) as fp32 (the mask is the h tile itself, held in shared
+// memory until the group has read it) and the dZ2 column sums (the b2 gradient)
+// per (tile, quadrant); else S dh as fp16.
+template <int C, bool EVO>
 __global__ void __launch_bounds__(kThreads, 1)
     readout_f16_kernel(const __grid_constant__ CUtensorMap tmH, const __half* __restrict__ Wo16,
                        const float* __restrict__ bo, const int32_t* __restrict__ labels, int64_t n,
                        int m_tiles, float scale, float scale16, __half* __restrict__ dh16,
                        double* __restrict__ loss_partial, float* __restrict__ dl_partial,
-                       float* __restrict__ dwo_partial) {
+                       float* __restrict__ dwo_partial, float* __restrict__ dz2,
+                       float* __restrict__ b2_partial) {
+  constexpr int kStg = EVO ? kStgStrideEvo : kStgStride;
   static_assert(C == 16 || C == 32, "readout_f16: C must be 16 or 32");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -88,7 +95,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sDlA = sWo + kH * 128;                       // MMA 2 A: [128 rows][128 B] (k < C used)
   uint8_t* sDlT = sDlA + BM * 128;                      // MMA 3 B: [2 k-blocks][C rows][128 B]
   uint8_t* sStg = sDlT + 2 * C * 128;                   // dh staging [8 warps][32 rows][144 B]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + 8 * 32 * kStgStride);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + 8 * 32 * kStg);
   uint64_t* empty = full + kStages;
   uint64_t* acc1_full = empty + kStages;
   uint64_t* acc1_empty = acc1_full + 1;
@@ -105,7 +112,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], EVO ? 9 : 1);  // EVO: + the 8 dh warps (the mask)
     }
     mbar_init(acc1_full, 1);
     mbar_init(acc1_empty, 4);
@@ -310,43 +317,93 @@ __global__ void __launch_bounds__(kThreads, 1)
     // dh group: S dh of 32 rows x 64 columns per warp: TMEM -> fp16 -> staging ->
     // coalesced 128-B row segments
     const int q = warp & 3, half = (warp - 6) >> 2;
+    const float inv16 = 1.f / scale16;
     const uint32_t tq = tmem_base + ((uint32_t)(32 * q) << 16) + kAcc2 + 64 * half;
-    const uint32_t stg = smem_u32(sStg) + (uint32_t)((warp - 6) * 32 * kStgStride);
+    const uint32_t stg = smem_u32(sStg) + (uint32_t)((warp - 6) * 32 * kStg);
+    const int rl = 32 * q + lane;
     int i = 0;
     for (int t = blockIdx.x; t < m_tiles; t += gridDim.x, ++i) {
       const int a2 = i & 1;
       mbar_wait(&acc2_full[a2], (i >> 1) & 1);
       fence_after();
+      if constexpr (EVO) {
+        // dZ2 = (S dh / S) * (H2 > 0), H2 = this tile's h (stage i % kStages, box = half)
+        const uint32_t hb = smem_u32(sH + (i % kStages) * kTileBytes) + (uint32_t)(half * BM * 128 + rl * 128);
 #pragma unroll
-      for (int ch = 0; ch < 2; ++ch) {
-        float v[32];
-        tmem_ld32(tq + a2 * 128 + 32 * ch, v);
+        for (int ch = 0; ch < 2; ++ch) {
+          float v[32];
+          tmem_ld32(tq + a2 * 128 + 32 * ch, v);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          uint32_t p[4];
+          for (int jj = 0; jj < 4; ++jj) {
+            uint4 m;
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(m.x), "=r"(m.y), "=r"(m.z), "=r"(m.w)
+                         : "r"(hb + ((((uint32_t)(4 * ch + jj)) ^ ((uint32_t)rl & 7u)) << 4)));
+            const uint32_t mq[4] = {m.x, m.y, m.z, m.w};
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const __half2 h2 = __floats2half2_rn(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
-            p[e] = *reinterpret_cast<const uint32_t*>(&h2);
+            for (int k = 0; k < 4; ++k) {
+              const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&mq[k]));
+              v[8 * jj + 2 * k] = f.x > 0.f ? v[8 * jj + 2 * k] * inv16 : 0.f;
+              v[8 * jj + 2 * k + 1] = f.y > 0.f ? v[8 * jj + 2 * k + 1] * inv16 : 0.f;
+            }
           }
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
-                           stg + (uint32_t)(lane * kStgStride + (ch * 4 + j) * 16)),
-                       "r"(p[0]), "r"(p[1]), "r"(p[2]), "r"(p[3])
-                       : "memory");
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                             stg + (uint32_t)(lane * kStg + (ch * 8 + j) * 16)),
+                         "f"(v[4 * j]), "f"(v[4 * j + 1]), "f"(v[4 * j + 2]), "f"(v[4 * j + 3])
+                         : "memory");
+          // column sums of the warp's 32 rows (lane ends with column lane)
+          int col = 0;
+          butterfly_colsum<32, 16>(v, lane, col);
+          b2_partial[(4 * (int64_t)t + q) * kH + 64 * half + 32 * ch + col] = v[0];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[i % kStages]);  // the mask tile is read
+      } else {
+  #pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+          float v[32];
+          tmem_ld32(tq + a2 * 128 + 32 * ch, v);
+  #pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint32_t p[4];
+  #pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const __half2 h2 = __floats2half2_rn(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
+              p[e] = *reinterpret_cast<const uint32_t*>(&h2);
+            }
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                             stg + (uint32_t)(lane * kStgStride + (ch * 4 + j) * 16)),
+                         "r"(p[0]), "r"(p[1]), "r"(p[2]), "r"(p[3])
+                         : "memory");
+          }
         }
       }
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc2_empty[a2]);
       const int64_t wrow0 = (int64_t)t * BM + 32 * q;
-#pragma unroll
-      for (int it = 0; it < 8; ++it) {
-        const int r = 4 * it + (lane >> 3), ch = lane & 7;
-        uint4 v;
-        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                     : "r"(stg + (uint32_t)(r * kStgStride + ch * 16)));
-        if (wrow0 + r < n) reinterpret_cast<uint4*>(dh16 + (wrow0 + r) * kH + 64 * half)[ch] = v;
+      if constexpr (EVO) {
+#pragma unroll 4
+        for (int it = 0; it < 16; ++it) {
+          const int r = 2 * it + (lane >> 4), c16 = lane & 15;
+          uint4 v;
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                       : "r"(stg + (uint32_t)(r * kStg + c16 * 16)));
+          if (wrow0 + r < n) reinterpret_cast<uint4*>(dz2 + (wrow0 + r) * kH + 64 * half)[c16] = v;
+        }
+      } else {
+  #pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int r = 4 * it + (lane >> 3), ch = lane & 7;
+          uint4 v;
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                       : "r"(stg + (uint32_t)(r * kStgStride + ch * 16)));
+          if (wrow0 + r < n) reinterpret_cast<uint4*>(dh16 + (wrow0 + r) * kH + 64 * half)[ch] = v;
+        }
       }
       __syncwarp();
     }
@@ -356,22 +413,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
 }
 
-template <int C>
+template <int C, bool EVO>
 int launch_readout(const void* h16, const void* Wo16, const float* bo, const int32_t* labels,
                    int64_t n, float scale, float scale16, void* dh16, double* loss_partial,
-                   float* dl_partial, float* dwo_partial, int grid, cudaStream_t s) {
+                   float* dl_partial, float* dwo_partial, float* dz2, float* b2_partial, int grid,
+                   cudaStream_t s) {
   CUtensorMap tmH;
   int rc = dgc::make_map_f16(&tmH, h16, n, kH, kH, 64, BM);
   if (rc != DGC_OK) return rc;
   const int m_tiles = (int)((n + BM - 1) / BM);
   const size_t smem = 1024 + (size_t)kStages * kTileBytes + 2 * C * 128 + kH * 128 + BM * 128 +
-                      2 * C * 128 + 8 * 32 * kStgStride + 16 * 8 + 16;
-  auto kern = readout_f16_kernel<C>;
+                      2 * C * 128 + 8 * 32 * (EVO ? kStgStrideEvo : kStgStride) + 16 * 8 + 16;
+  auto kern = readout_f16_kernel<C, EVO>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return dgc::cuda_fail(e, "readout_f16: set smem");
   kern<<<grid, kThreads, smem, s>>>(tmH, static_cast<const __half*>(Wo16), bo, labels, n, m_tiles, scale,
-                               scale16, static_cast<__half*>(dh16), loss_partial, dl_partial,
-                               dwo_partial);
+                                    scale16, static_cast<__half*>(dh16), loss_partial, dl_partial,
+                                    dwo_partial, dz2, b2_partial);
   DGC_CHECK_LAUNCH("readout_f16_kernel");
   return DGC_OK;
 }
@@ -395,8 +453,27 @@ extern "C" int dgc_readout_f16(const void* h16, const void* Wo16, const float* b
               "readout_f16: dh16 / dwo_partial must be 16-byte aligned");
   cudaStream_t s = dgc::as_stream(stream);
   const int grid = dgc_readout_f16_grid(n);
-  return C == 16 ? launch_readout<16>(h16, Wo16, bo, labels, n, scale, scale16, dh16, loss_partial,
-                                      dl_partial, dwo_partial, grid, s)
-                 : launch_readout<32>(h16, Wo16, bo, labels, n, scale, scale16, dh16, loss_partial,
-                                      dl_partial, dwo_partial, grid, s);
+  return C == 16 ? launch_readout<16, false>(h16, Wo16, bo, labels, n, scale, scale16, dh16, loss_partial,
+                                             dl_partial, dwo_partial, nullptr, nullptr, grid, s)
+                 : launch_readout<32, false>(h16, Wo16, bo, labels, n, scale, scale16, dh16, loss_partial,
+                                             dl_partial, dwo_partial, nullptr, nullptr, grid, s);
+}
+
+extern "C" int dgc_readout_f16_evolve(const void* h2_16, const void* Wo16, const float* bo,
+                                      const int32_t* labels, int64_t n, int32_t H, int32_t C,
+                                      float scale, float scale16, float* dz2, float* b2_partial,
+                                      double* loss_partial, float* dl_partial, float* dwo_partial,
+                                      void* stream) {
+  DGC_REQUIRE(H == kH, "readout_f16_evolve: H must be 128");
+  DGC_REQUIRE(C == 16 || C == 32, "readout_f16_evolve: C must be 16 or 32");
+  DGC_REQUIRE(n > 0 && n < (int64_t)INT32_MAX / 2, "readout_f16_evolve: bad row count");
+  DGC_REQUIRE((reinterpret_cast<uintptr_t>(dz2) & 15) == 0 &&
+                  (reinterpret_cast<uintptr_t>(dwo_partial) & 15) == 0,
+              "readout_f16_evolve: dz2 / dwo_partial must be 16-byte aligned");
+  cudaStream_t s = dgc::as_stream(stream);
+  const int grid = dgc_readout_f16_grid(n);
+  return C == 16 ? launch_readout<16, true>(h2_16, Wo16, bo, labels, n, scale, scale16, nullptr,
+                                            loss_partial, dl_partial, dwo_partial, dz2, b2_partial, grid, s)
+                 : launch_readout<32, true>(h2_16, Wo16, bo, labels, n, scale, scale16, nullptr,
+                                            loss_partial, dl_partial, dwo_partial, dz2, b2_partial, grid, s);
 }

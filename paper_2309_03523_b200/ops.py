@@ -571,6 +571,28 @@ def readout_f16(h16, Wo16, bo, labels, C, scale, scale16, dh16, loss_partial, dl
         nb, 2.0 * n * H * C * 3)
 
 
+def readout_f16_evolve(h2_16, Wo16, bo, labels, C, scale, scale16, dz2, b2_partial, loss_partial,
+                       dl_partial, dwo_partial):
+    """dgc_readout_f16_evolve: the fused readout of EvolveGCN-O (input H2 =
+    relu(.)): dz2 = dh * (H2 > 0) as fp32 and its column-sum partials (the b2
+    gradient) instead of S dh16."""
+    n, H = h2_16.shape
+    _req16(h2_16, "h2_16"); _req16(Wo16, "Wo16"); _req(dz2, torch.float32, "dz2")
+    _req(b2_partial, torch.float32, "b2_partial")
+    _req(bo, torch.float32, "bo"); _req(labels, torch.int32, "labels")
+    _req(loss_partial, torch.float64, "loss_partial"); _req(dl_partial, torch.float32, "dl_partial")
+    _req(dwo_partial, torch.float32, "dwo_partial")
+    tiles, grid = 4 * ((n + 127) // 128), readout_f16_grid(n)
+    if (loss_partial.numel() < tiles or dl_partial.numel() < tiles * C or b2_partial.numel() < tiles * H
+            or dwo_partial.numel() < grid * H * C):
+        raise ValueError("readout_f16_evolve: partial buffers too small")
+    nb = n * (2 * H + 4 * H + 4) + grid * (2 * H * C + 4 * H * C) + tiles * (8 + 4 * C + 4 * H)
+    _run("readout_f16", lambda: _native.check(_native.lib().dgc_readout_f16_evolve(
+        _p(h2_16), _p(Wo16), _p(bo), _p(labels), n, H, C, float(scale), float(scale16), _p(dz2),
+        _p(b2_partial), _p(loss_partial), _p(dl_partial), _p(dwo_partial), _stream()),
+        "dgc_readout_f16_evolve"), nb, 2.0 * n * H * C * 3)
+
+
 def pack_tf32x24(x: np.ndarray) -> np.ndarray:
     """Host side of the TF32 input pipeline: round fp32 values to TF32 (round to
     nearest, ties away: cvt.rna.tf32) and keep the top three bytes of each

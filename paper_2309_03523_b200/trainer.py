@@ -311,7 +311,10 @@ class Shard:
         # one tcgen05 launch that reads h16 once (replaces 4 launches)
         self.fused_readout = bool(self.dh16 is not None and H == 128 and cfg.C in (16, 32)
                                   and cfg.n_rnn > 0 and os.environ.get("DGC_FUSED_READOUT", "1") != "0")
-        if self.fused_readout:
+        # EvolveGCN-O: the same kernel writes dZ2 = dh * (H2 > 0) (fp32) and the b2 partials
+        self.fused_readout_evo = bool(evolve and self.f16_readout and H == 128 and cfg.C in (16, 32)
+                                      and os.environ.get("DGC_FUSED_READOUT", "1") != "0")
+        if self.fused_readout or self.fused_readout_evo:
             ro_tiles = 4 * max(1, (n + 127) // 128)  # partial rows per (tile, lane quadrant)
             self.loss_partial = torch.zeros(ro_tiles, dtype=torch.float64, device=dev)
             self.dl_partial = torch.zeros(ro_tiles * cfg.C, **f32)
@@ -333,7 +336,7 @@ class Shard:
         # the gradient tensors, reduced in fixed order by dgc_reduce_rows)
         self.m_tiles = max(1, (n + 127) // 128)
         self.rnn_prows = ops.rnn_bwd_partial_rows(self.R, H) if self.R else 1
-        if not getattr(self, "fused_readout", False):
+        if not (self.fused_readout or self.fused_readout_evo):
             self.dl_partial = torch.zeros(max(1, (n + 255) // 256) * cfg.C, **f32)
         prows = max(self.rnn_prows, ops.rnn_tc_tiles(max(self.R, 1), H))
         # one partial buffer per bias gradient: their fixed-order reductions run
@@ -663,6 +666,10 @@ class Shard:
             ops.readout_f16(self.x16[cfg.n_rnn], self.p16("Wo"), self.p("bo"), self.y, cfg.C,
                             1.0 / self.n_total, 2.0 ** self.da_exp, self.dh16[0], self.loss_partial,
                             self.dl_partial, self.dwo_partial)
+        elif self.fused_readout_evo:  # + dZ2 = dh * (H2 > 0) into self.dh, b2 partials
+            ops.readout_f16_evolve(self.h2_16, self.p16("Wo"), self.p("bo"), self.y, cfg.C,
+                                   1.0 / self.n_total, 2.0 ** self.da_exp, self.dh, self.bp_b[1],
+                                   self.loss_partial, self.dl_partial, self.dwo_partial)
         elif f16r:
             xr16 = self.h2_16 if self.evolve else self.x16[cfg.n_rnn]
             ops.gemm_f16(xr16, self.p16("Wo"), self.logits, n, cfg.C, H, lda=H, bias=self.p("bo"))
@@ -677,7 +684,7 @@ class Shard:
         # ---------------- backward ----------------
         self.grads.zero_()
         ks, part = self.ksplit, self.partial
-        if self.fused_readout:
+        if self.fused_readout or self.fused_readout_evo:
             pass  # dWo partials came with the forward readout (reduced below)
         elif f16r:
             ops.gemm_f16(xr16, self.dlogits16, self.g("Wo"), H, cfg.C, n, a_mn=True, lda=H,
@@ -685,12 +692,14 @@ class Shard:
         else:
             ops.gemm(xr, self.dlogits, self.g("Wo"), H, cfg.C, n, a_mn=True, lda=ldx,
                      precision=prec, k_splits=ks, partial=part)
-        if self.fused_readout:
+        if self.fused_readout or self.fused_readout_evo:
             rjobs = [(self.dl_partial, 4 * max(1, (n + 127) // 128), cfg.C, self.g("bo")),
                      (self.dwo_partial, self.ro_grid, H * cfg.C, self.g("Wo"))]
         else:
             rjobs = [(self.dl_partial, max(1, (n + 255) // 256), cfg.C, self.g("bo"))]
-        if f16r and self.evolve:  # dZ2 = (dlogits Wo^T) * (H2 > 0), b2 fused
+        if self.fused_readout_evo:  # dZ2 and its b2 partials came with the forward readout
+            rjobs.append((self.bp_b[1], 4 * self.m_tiles, H, self.g("b2")))
+        elif f16r and self.evolve:  # dZ2 = (dlogits Wo^T) * (H2 > 0), b2 fused
             ops.gemm_f16(self.dlogits16, self.p16("Wo"), self.dh, n, H, cfg.C, b_mn=False,
                          ldb=cfg.C, alpha=self.inv_da_scale, relu16=self.h2_16,
                          colsum_partial=self.bp_b[1])

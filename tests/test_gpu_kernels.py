@@ -821,6 +821,51 @@ def test_fused_readout_f16_matches_fp64(n, C):
     close(dh16.float().cpu().numpy(), dh_ref, 5e-3, "S dh16")
 
 
+@pytest.mark.parametrize("n,C", [(300, 16), (9000, 16), (2049, 32)])
+def test_fused_readout_f16_evolve_matches_fp64(n, C):
+    """dgc_readout_f16_evolve (EvolveGCN-O readout on H2 = relu(.)): dZ2 = dh *
+    (H2 > 0) as fp32 and its column sums (the b2 gradient) vs fp64 on the same
+    fp16 operands; loss, bo and Wo gradients as the LSTM variant."""
+    from paper_2309_03523_b200 import ops
+    H, e = 128, 13
+    S = 2.0 ** e
+    rng = np.random.default_rng(2 * n + C)
+    h16 = np.maximum(rng.standard_normal((n, H)), 0).astype(np.float16)  # relu output
+    Wo16 = (rng.standard_normal((H, C)) / np.sqrt(H)).astype(np.float16)
+    bo = (0.1 * rng.standard_normal(C)).astype(np.float32)
+    y = rng.integers(0, C, size=n).astype(np.int32)
+    y[rng.random(n) < 0.1] = -1
+    scale = 1.0 / n
+    tiles, grid = 4 * ((n + 127) // 128), ops.readout_f16_grid(n)
+    dz2 = torch.zeros((n, H), device=dev)
+    b2p = torch.zeros(tiles * H, device=dev)
+    lp = torch.zeros(tiles, device=dev, dtype=torch.float64)
+    dp = torch.zeros(tiles * C, device=dev)
+    wp = torch.zeros(grid * H * C, device=dev)
+    ops.readout_f16_evolve(torch.as_tensor(h16).to(dev), torch.as_tensor(Wo16).to(dev), t(bo),
+                           t(y, torch.int32), C, scale, S, dz2, b2p, lp, dp, wp)
+    gWo, gbo, gb2 = torch.zeros(H * C, device=dev), torch.zeros(C, device=dev), torch.zeros(H, device=dev)
+    ops.reduce_rows_batched([(dp, tiles, C, gbo), (wp, grid, H * C, gWo), (b2p, tiles, H, gb2)])
+    torch.cuda.synchronize()
+    hd, Wd = h16.astype(np.float64), Wo16.astype(np.float64)
+    z = hd @ Wd + bo.astype(np.float64)
+    z -= z.max(1, keepdims=True)
+    p = np.exp(z) / np.exp(z).sum(1, keepdims=True)
+    real = y >= 0
+    loss = -np.log(p[np.arange(n)[real], y[real]]).sum()
+    dl = p.copy()
+    dl[np.arange(n)[real], y[real]] -= 1.0
+    dl[~real] = 0.0
+    dl *= scale
+    dl16 = (dl * S).astype(np.float16).astype(np.float64)
+    dz_ref = (dl16 @ Wd.T / S) * (hd > 0)
+    assert abs(lp.sum().item() - loss) <= 1e-5 * abs(loss)
+    close(gbo.cpu().numpy(), dl.sum(0), 1e-4, "bo grad")
+    close(gWo.cpu().numpy().reshape(H, C), hd.T @ dl16 / S, 5e-3, "Wo grad")
+    close(dz2.cpu().numpy(), dz_ref, 5e-3, "dZ2")
+    close(gb2.cpu().numpy(), dz_ref.sum(0), 5e-3, "b2 grad")
+
+
 def test_tf32x24_input_pipeline_is_bit_exact():
     """Host pack (round-to-nearest-away to TF32, keep 3 bytes) + device unpack
     equals the device's cvt.rna.tf32 rounding of the fp32 values, bit for bit,
