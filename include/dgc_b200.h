@@ -529,6 +529,9 @@ int dgc_adam_dev_mirror(float* p, const float* g, float* m, float* v, int64_t n,
 /* End of a training step: loss_out[0] = sum of loss_partial[0..n) (fp64, fixed
  * order, one block) and, when step_dev is non-NULL, ++*step_dev (the device
  * step count a CUDA-graph-replayed Adam reads). */
+/* bytes of ptr set to zero on the stream (cudaMemsetAsync: a memset node, not a
+ * kernel, inside a captured step) */
+int dgc_zero_async(void* ptr, int64_t bytes, void* stream);
 int dgc_epoch_finish(const double* loss_partial, int64_t n, double* loss_out, int32_t* step_dev,
                      void* stream);
 

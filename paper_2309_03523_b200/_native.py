@@ -91,6 +91,7 @@ _SIGS = {
     "dgc_softmax_xent_f16": (_i32, [_p, _p, _i64, _i32, _f32, _p, _p, _p, _p, _f32, _p]),
     "dgc_readout_f16": (_i32, [_p, _p, _p, _p, _i64, _i32, _i32, _f32, _f32, _p, _p, _p, _p, _p]),
     "dgc_readout_f16_grid": (_i32, [_i64]),
+    "dgc_zero_async": (_i32, [_p, _i64, _p]),
     "dgc_readout_f16_evolve": (_i32, [_p, _p, _p, _p, _i64, _i32, _i32, _f32, _f32, _p, _p, _p, _p, _p, _p]),
     "dgc_reduce_rows_batched": (_i32, [_i32, _p, _p, _p, _p, _p]),
     "dgc_reduce_rows": (_i32, [_p, _i64, _i32, _p, _i32, _p]),

@@ -689,3 +689,10 @@ extern "C" int dgc_adam_dev(float* p, const float* g, float* m, float* v, int64_
   DGC_CHECK_LAUNCH("adam_kernel");
   return DGC_OK;
 }
+
+extern "C" int dgc_zero_async(void* ptr, int64_t bytes, void* stream) {
+  DGC_REQUIRE(bytes >= 0, "zero_async: negative size");
+  if (bytes == 0) return DGC_OK;
+  cudaError_t e = cudaMemsetAsync(ptr, 0, (size_t)bytes, dgc::as_stream(stream));
+  return e == cudaSuccess ? DGC_OK : dgc::cuda_fail(e, "zero_async");
+}

@@ -544,6 +544,13 @@ def softmax_xent(logits, labels, C, scale, dlogits, loss_partial, round_tf32=Fal
         _p(loss_partial), _p(dl_partial), _stream()), "dgc_softmax_xent"), n * (8 * C + 4))
 
 
+def zero_(t):
+    """dgc_zero_async: t = 0 by cudaMemsetAsync on the current stream (a memset
+    node in a captured step instead of a torch fill kernel)."""
+    _native.check(_native.lib().dgc_zero_async(_p(t), t.numel() * t.element_size(), _stream()),
+                  "dgc_zero_async")
+
+
 def readout_f16_grid(n):
     """CTAs (= rows of the dWo partial) of dgc_readout_f16 for n instances."""
     return int(_native.lib().dgc_readout_f16_grid(int(n)))

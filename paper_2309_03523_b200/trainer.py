@@ -682,7 +682,7 @@ class Shard:
             ops.softmax_xent(self.logits, self.y, cfg.C, 1.0 / self.n_total, self.dlogits,
                              self.loss_partial, round_tf32=self.tf32, dl_partial=self.dl_partial)
         # ---------------- backward ----------------
-        self.grads.zero_()
+        ops.zero_(self.grads)
         ks, part = self.ksplit, self.partial
         if self.fused_readout or self.fused_readout_evo:
             pass  # dWo partials came with the forward readout (reduced below)
