@@ -53,7 +53,7 @@ def h(*ts):
     return m.hexdigest()[:12]
 
 
-mode = os.environ.get("DGC_SPMM_STREAM", os.environ.get("DGC_SPMM_MODE", "-"))
+mode = os.environ.get("DGC_SPMM_STREAM", os.environ.get("DGC_SPMM_MODE", os.environ.get("DGC_SPMM_LD", "-")))
 runh = lambda: _native.check(lib.dgc_spmm_csr_h(rp.data_ptr(), col.data_ptr(), dinv.data_ptr(),
                                                 Y16.data_ptr(), bias.data_ptr(), None, o16.data_ptr(),
                                                 1.0, n, W, 1, work.data_ptr(), None), "spmm_h")
